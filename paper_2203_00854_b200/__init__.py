@@ -1,0 +1,43 @@
+"""B200-native Evoformer hot path (FastFold, arXiv 2203.00854).
+
+Drop-in for the reference package's Evoformer block / module API
+(/root/reference/pkg/src/evoplan/__init__.py:13-72, hot-path subset):
+``EvoConfig``, ``param_shapes``, ``init_block_params``, ``params_to_json``,
+``params_from_json``, ``evoformer_block`` and its sub-modules,
+``dap_evoformer_block`` with ``DeviceMesh`` / ``CommLedger``, and the
+reference's exception classes.  Compute runs in libevo.so (sm_100a CUDA,
+include/evo.h); there is no CPU fallback.
+"""
+
+from .config import (
+    EvoConfig,
+    init_block_params,
+    param_shapes,
+    params_from_json,
+    params_to_json,
+)
+from .errors import (
+    DimensionError,
+    DomainError,
+    EvoplanError,
+    KernelError,
+    MeshError,
+    NativeLibraryMissing,
+    ShardError,
+)
+
+__version__ = "0.1.0"
+
+
+def __getattr__(name):
+    # heavy (torch / CUDA) modules load lazily so that `import` works on CPU-only hosts
+    if name in ("evoformer_block", "msa_row_attention", "msa_row_bias", "msa_row_attention_with_bias",
+                "msa_col_attention", "transition", "outer_product_mean", "tri_update_outgoing",
+                "tri_update_incoming", "pair_attention_row", "pair_attention_col",
+                "fused_softmax_mask_bias", "layernorm", "EvoformerStack", "BlockParams"):
+        from . import evoformer
+        return getattr(evoformer, name)
+    if name in ("dap_evoformer_block", "DeviceMesh", "CommLedger", "predict_block_ledger", "dap_block"):
+        from . import dap
+        return getattr(dap, name)
+    raise AttributeError(name)

@@ -1,0 +1,436 @@
+"""Forward / backward of one Evoformer block on the GPU (bf16 activations, fp32
+statistics and accumulation).
+
+Each sub-module of ``evoformer_block`` (evoformer.py:314-325) is a pair
+``<name>_fwd(bp, ..., save) -> x_new`` / ``<name>_bwd(bp, saved, dx_new) -> dx``
+composed of libevo.so kernels (LayerNorm, fused attention, tcgen05 batched GEMM,
+gating / residual epilogues) and cuBLAS for the plain projection GEMMs
+(the "K7 merged projections" of SURVEY.md 2.1).  Residual adds are fused into
+the epilogues, so every ``*_fwd`` returns the updated stream (x + f(x)) and
+every ``*_bwd`` returns d(input) = d(output) + df/dx.
+
+Activation layout in HBM: m = [N_s, N_r, H_m] and z = [N_r, N_r, H_z], bf16,
+row-major; every sub-module works on the 2-D view [rows, channels].  The
+transposed variants (msa_col, pair_col, tri_in) never copy: they hand the
+kernels strides (attention) or MN-major operands (batched GEMM).
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import ops
+from .config import EvoConfig
+from .ops import Mat, Strided
+from .params import BlockParams
+
+BF16 = torch.bfloat16
+F32 = torch.float32
+
+
+def _mm(a, b):
+    return torch.mm(a, b)
+
+
+def _wgrad(x, dy, out):
+    """out (fp32) = x^T @ dy with fp32 accumulation and output."""
+    out.copy_(torch.mm(x.t(), dy, out_dtype=F32))
+
+
+def _bgrad(dy, out):
+    out.copy_(dy.sum(0, dtype=F32))
+
+
+class Saved(dict):
+    """activations saved by a forward for its backward"""
+
+
+# ----------------------------------------------------------------------------- attention
+def _attn_geometry(kind: str, B: int, L: int):
+    """rows of the [rows, C] view for attention batch b / position l:
+    row = b*sb + l*sl  (row-wise: batch = leading axis; column-wise: transposed)."""
+    return (L, 1) if kind == "row" else (1, B)
+
+
+def attention_fwd(bp: BlockParams, mod: str, x2d, B: int, L: int, kind: str, bias=None, save=True):
+    """_attention_core (evoformer.py:173-198) + residual: returns x + attn(x).
+
+    kind "row": attention along the second axis of [B, L, C]; "col": x2d is
+    [L, B, C] and attention runs along the first axis (msa_col / pair_col).
+    bias: None, ("full", tensor [nh, L, L]) shared over the batch (msa_row), or
+    "pair" = per-key bias from the merged projection (pair_row / pair_col).
+    """
+    a = bp.layout.attn[mod]
+    H, nh, c, ldq = a["H"], a["nh"], a["c"], a["ldq"]
+    rows = B * L
+    h, f = bp.h, bp.f
+    ln, mean, rstd = ops.layernorm_fwd(x2d, f[f"{mod}.ln_g"], f[f"{mod}.ln_b"], rows, H)
+    qkv = torch.addmm(h[f"{mod}.b_qkv"], ln, h[f"{mod}.w_qkv"])
+    gpre = torch.addmm(h[f"{mod}.b_g"], x2d, h[f"{mod}.w_g"])
+    og = torch.empty(rows, nh * c, device=x2d.device, dtype=BF16)
+    orw = torch.empty_like(og)
+    lse = torch.empty(B, nh, L, device=x2d.device, dtype=F32)
+    sbr, slr = _attn_geometry(kind, B, L)
+    S = lambda t, ld, off=0: Strided(t, sbr * ld, slr * ld, off)
+    if bias is None:
+        bt, bs, boff = None, (0, 0, 0, 0), 0
+    elif bias == "pair":
+        bt, bs, boff = qkv, (sbr * ldq, 1, 0, slr * ldq), 3 * nh * c
+    else:
+        bt, bs, boff = bias, (0, L * L, L, 1), 0
+    desc = ops.attention_desc(S(qkv, ldq, 0), S(qkv, ldq, nh * c), S(qkv, ldq, 2 * nh * c), S(gpre, nh * c),
+                              S(og, nh * c), S(orw, nh * c), lse, B, L, nh, c, 1.0 / math.sqrt(c),
+                              bias=bt, bias_s=bs, bias_off=boff)
+    ops.attention_fwd(desc)
+    y = _mm(og, h[f"{mod}.w_o"])
+    out = ops.gated_residual_fwd(x2d, y, f[f"{mod}.b_o"], rows, H)
+    sv = None
+    if save:
+        sv = Saved(x=x2d, ln=ln, mean=mean, rstd=rstd, qkv=qkv, gpre=gpre, og=og, orw=orw, lse=lse,
+                   desc=desc, B=B, L=L, kind=kind, bias=bias, mod=mod)
+    return out, sv
+
+
+def attention_bwd(bp: BlockParams, sv: Saved, dx_new):
+    """returns (dx, dbias) with dx = dx_new + d attn / dx; dbias fp32 for "full" bias."""
+    mod, B, L, kind = sv["mod"], sv["B"], sv["L"], sv["kind"]
+    a = bp.layout.attn[mod]
+    H, nh, c, ldq = a["H"], a["nh"], a["c"], a["ldq"]
+    rows = B * L
+    h, f, g = bp.h, bp.f, bp.g
+    dev = dx_new.device
+    ops.gated_residual_bwd(dx_new, rows, H, dbias=g[f"{mod}.b_o"])  # db_o = sum_r dx_new
+    dog = _mm(dx_new, h[f"{mod}.w_o"].t())
+    _wgrad(sv["og"], dx_new, g[f"{mod}.w_o"])
+    sbr, slr = _attn_geometry(kind, B, L)
+    S = lambda t, ld, off=0: Strided(t, sbr * ld, slr * ld, off)
+    dqkv = torch.empty(rows, ldq, device=dev, dtype=BF16)
+    if ldq > 3 * nh * c:
+        dqkv[:, 3 * nh * c:].zero_()
+    dgpre = torch.empty(rows, nh * c, device=dev, dtype=BF16)
+    bias = sv["bias"]
+    if bias is None:
+        dbias, dbs = None, (0, 0, 0, 0)
+    elif bias == "pair":
+        dbias, dbs = torch.zeros(B, nh, L, device=dev, dtype=F32), (nh * L, L, 0, 1)
+    else:
+        dbias, dbs = torch.zeros(nh, L, L, device=dev, dtype=F32), (0, L * L, L, 1)
+    ws = torch.empty(ops.attention_bwd_workspace(B, L, nh, c), device=dev, dtype=torch.uint8)
+    ops.attention_bwd(sv["desc"], S(dog, nh * c), S(dqkv, ldq, 0), S(dqkv, ldq, nh * c), S(dqkv, ldq, 2 * nh * c),
+                      S(dgpre, nh * c), ws, dbias=dbias, dbias_s=dbs)
+    if bias == "pair":
+        cols = dqkv[:, 3 * nh * c:3 * nh * c + nh]
+        if kind == "row":
+            cols.view(B, L, nh).copy_(dbias.permute(0, 2, 1))
+        else:
+            cols.view(L, B, nh).copy_(dbias.permute(2, 0, 1))
+    _wgrad(sv["ln"], dqkv, g[f"{mod}.w_qkv"])
+    _bgrad(dqkv, g[f"{mod}.b_qkv"])
+    _wgrad(sv["x"], dgpre, g[f"{mod}.w_g"])
+    _bgrad(dgpre, g[f"{mod}.b_g"])
+    dx = torch.addmm(dx_new, dgpre, h[f"{mod}.w_g"].t())          # gate reads raw x (G2)
+    dln = _mm(dqkv, h[f"{mod}.w_qkv"].t())
+    ops.layernorm_bwd(dln, sv["x"], f[f"{mod}.ln_g"], sv["mean"], sv["rstd"], rows, H, dx=dx, accumulate=True,
+                      dgamma=g[f"{mod}.ln_g"], dbeta=g[f"{mod}.ln_b"])
+    return dx, (dbias if bias not in (None, "pair") else None)
+
+
+# ----------------------------------------------------------------------------- msa_row bias
+def msa_row_bias_fwd(bp: BlockParams, z2d, R: int, save=True):
+    """msa_row_bias (evoformer.py:201-207) -> bias[h][i][j] bf16, one fused kernel."""
+    cfg = bp.cfg
+    nh, k = cfg.n_head_msa, bp.layout.rowdot_k
+    rows = R * R
+    out = torch.empty(k, R, R, device=z2d.device, dtype=BF16)
+    ln = torch.empty(rows, cfg.h_pair, device=z2d.device, dtype=BF16) if save else None
+    mean = torch.empty(rows, device=z2d.device, dtype=F32) if save else None
+    rstd = torch.empty_like(mean) if save else None
+    ops.layernorm_rowdot_fwd(z2d, bp.f["msa_row.lnz_g"], bp.f["msa_row.lnz_b"], bp.f["msa_row.w_bias"], rows,
+                             cfg.h_pair, out, rows, ln_out=ln, mean=mean, rstd=rstd)
+    sv = Saved(z=z2d, ln=ln, mean=mean, rstd=rstd) if save else None
+    return out[:nh], sv
+
+
+def msa_row_bias_bwd(bp: BlockParams, sv: Saved, dbias, dz):
+    """dbias fp32 [nh, R, R]; accumulates into dz (bf16 [R*R, Hz])."""
+    cfg = bp.cfg
+    nh, Hz = cfg.n_head_msa, cfg.h_pair
+    rows = dbias[0].numel()
+    db2 = dbias.reshape(nh, rows)
+    w = bp.f["msa_row.w_bias"][:, :nh]                                   # fp32 [Hz, nh]
+    dln = torch.mm(db2.t(), w.t())                                       # fp32 [rows, Hz]
+    bp.g["msa_row.w_bias"][:, :nh].copy_(torch.mm(sv["ln"].t().float(), db2.t()))
+    ops.layernorm_bwd(dln, sv["z"], bp.f["msa_row.lnz_g"], sv["mean"], sv["rstd"], rows, Hz, dx=dz, accumulate=True,
+                      dgamma=bp.g["msa_row.lnz_g"], dbeta=bp.g["msa_row.lnz_b"])
+
+
+# ----------------------------------------------------------------------------- transition
+def transition_fwd(bp: BlockParams, mod: str, x2d, rows: int, save=True):
+    """transition (evoformer.py:237-240) + residual."""
+    H = x2d.shape[1]
+    h, f = bp.h, bp.f
+    ln, mean, rstd = ops.layernorm_fwd(x2d, f[f"{mod}.ln_g"], f[f"{mod}.ln_b"], rows, H)
+    hid = _mm(ln, h[f"{mod}.w1"])
+    ops.bias_act_fwd(hid, f[f"{mod}.b1"], rows, hid.shape[1], relu=True)
+    y = _mm(hid, h[f"{mod}.w2"])
+    out = ops.gated_residual_fwd(x2d, y, f[f"{mod}.b2"], rows, H)
+    sv = Saved(x=x2d, ln=ln, mean=mean, rstd=rstd, hid=hid, mod=mod) if save else None
+    return out, sv
+
+
+def transition_bwd(bp: BlockParams, sv: Saved, dx_new):
+    mod = sv["mod"]
+    rows, H = dx_new.shape
+    h, f, g = bp.h, bp.f, bp.g
+    ops.gated_residual_bwd(dx_new, rows, H, dbias=g[f"{mod}.b2"])
+    _wgrad(sv["hid"], dx_new, g[f"{mod}.w2"])
+    dhid = _mm(dx_new, h[f"{mod}.w2"].t())
+    dpre = ops.bias_act_bwd(dhid, sv["hid"], rows, dhid.shape[1], dy=dhid, dbias=g[f"{mod}.b1"])
+    _wgrad(sv["ln"], dpre, g[f"{mod}.w1"])
+    dln = _mm(dpre, h[f"{mod}.w1"].t())
+    dx = dx_new.clone()
+    ops.layernorm_bwd(dln, sv["x"], f[f"{mod}.ln_g"], sv["mean"], sv["rstd"], rows, H, dx=dx, accumulate=True,
+                      dgamma=g[f"{mod}.ln_g"], dbeta=g[f"{mod}.ln_b"])
+    return dx
+
+
+# ----------------------------------------------------------------------------- outer product mean
+def opm_fwd(bp: BlockParams, m2d, z2d, S: int, R: int, save=True, b_full=None, Rj=None, gather=None):
+    """outer_product_mean (evoformer.py:243-255) + residual into z.
+
+    o[i][j][p][q] = sum_s a[s,i,p] b[s,j,q] / S is ONE tcgen05 GEMM with M = i*p,
+    N = j*q, K = s written straight into the [i][j][p][q] layout; then o @ W_o.
+    Under DAP, a is local ([S, R_loc, p]) and b is gathered (``gather(b_local)``
+    returns [N_dev, S, R_loc, p] rank-major), addressed without unpacking.
+    """
+    cfg = bp.cfg
+    P, Hm, Hz = cfg.hidden_proj, cfg.h_msa, cfg.h_pair
+    rows_m = S * R
+    h, f = bp.h, bp.f
+    ln, mean, rstd = ops.layernorm_fwd(m2d, f["opm.ln_g"], f["opm.ln_b"], rows_m, Hm)
+    ab = torch.addmm(h["opm.b_ab"], ln, h["opm.w_ab"])              # [S*R, 2P] = [a | b]
+    A = Mat(ab, lo=(1, R * 2 * P), split=(P, 0), hi=(2 * P, 0))
+    if gather is None:
+        Rj = R
+        bsrc = ab
+        B = Mat(ab, lo=(1, R * 2 * P), split=(P, 0), hi=(2 * P, 0), offset=P)
+    else:
+        bsrc = gather(ab[:, P:].contiguous())                      # [N, S, R_loc, P]
+        nd = bsrc.shape[0]
+        Rj = nd * R
+        B = Mat(bsrc, lo=(1, R * P), split=(R * P, 0), hi=(S * R * P, 0))
+    o = torch.empty(R, Rj, P, P, device=m2d.device, dtype=BF16)
+    Cm = Mat(o, lo=(P, 1), split=(P, P), hi=(Rj * P * P, P * P))
+    ops.bgemm(A, B, Cm, 1, R * P, Rj * P, S, alpha=1.0 / S)
+    y = _mm(o.view(R * Rj, P * P), h["opm.w_o"])
+    out = ops.gated_residual_fwd(z2d, y, f["opm.b_o"], R * Rj, Hz)
+    sv = Saved(m=m2d, ln=ln, mean=mean, rstd=rstd, ab=ab, bsrc=bsrc, o=o, S=S, R=R, Rj=Rj,
+               gathered=gather is not None) if save else None
+    return out, sv
+
+
+def opm_bwd(bp: BlockParams, sv: Saved, dz_new, dm, reduce_scatter=None):
+    """accumulates the OPM contribution into dm (bf16 [S*R, Hm]); dz passes through."""
+    cfg = bp.cfg
+    P, Hm, Hz = cfg.hidden_proj, cfg.h_msa, cfg.h_pair
+    S, R, Rj = sv["S"], sv["R"], sv["Rj"]
+    h, f, g = bp.h, bp.f, bp.g
+    ops.gated_residual_bwd(dz_new, R * Rj, Hz, dbias=g["opm.b_o"])
+    _wgrad(sv["o"].view(R * Rj, P * P), dz_new, g["opm.w_o"])
+    do = _mm(dz_new, h["opm.w_o"].t())                               # [R*Rj, P*P] == [i][j][p][q]
+    dab = torch.empty(S * R, 2 * P, device=dz_new.device, dtype=BF16)
+    ab = sv["ab"]
+    # da[s,i,p] = sum_{j,q} do[i,j,p,q] b[s,j,q] / S      (M = (i,p), N = s, K = (j,q))
+    dO_A = Mat(do, lo=(P, 1), split=(P, P), hi=(Rj * P * P, P * P))
+    if not sv["gathered"]:
+        Bb = Mat(ab, lo=(R * 2 * P, 1), split=(0, P), hi=(0, 2 * P), offset=P)
+    else:
+        Bb = Mat(sv["bsrc"], lo=(R * P, 1), split=(0, R * P), hi=(0, S * R * P))
+    Cda = Mat(dab, lo=(1, R * 2 * P), split=(P, 0), hi=(2 * P, 0))
+    ops.bgemm(dO_A, Bb, Cda, 1, R * P, S, Rj * P, alpha=1.0 / S)
+    # db[s,j,q] = sum_{i,p} a[s,i,p] do[i,j,p,q] / S      (M = (j,q), N = s, K = (i,p))
+    dO_T = Mat(do, lo=(1, P), split=(P, P), hi=(P * P, Rj * P * P))
+    Ba = Mat(ab, lo=(R * 2 * P, 1), split=(0, P), hi=(0, 2 * P))
+    if not sv["gathered"]:
+        Cdb = Mat(dab, lo=(1, R * 2 * P), split=(P, 0), hi=(2 * P, 0), offset=P)
+        ops.bgemm(dO_T, Ba, Cdb, 1, Rj * P, S, R * P, alpha=1.0 / S)
+    else:
+        nd = sv["bsrc"].shape[0]
+        dbf = torch.empty(nd, S, R, P, device=dz_new.device, dtype=F32)   # rank-major partials
+        Cdb = Mat(dbf, lo=(1, R * P), split=(R * P, 0), hi=(S * R * P, 0))
+        ops.bgemm(dO_T, Ba, Cdb, 1, Rj * P, S, R * P, alpha=1.0 / S)
+        dab[:, P:].copy_(reduce_scatter(dbf).view(S * R, P))
+    _wgrad(sv["ln"], dab, g["opm.w_ab"])
+    _bgrad(dab, g["opm.b_ab"])
+    dln = _mm(dab, h["opm.w_ab"].t())
+    ops.layernorm_bwd(dln, sv["m"], f["opm.ln_g"], sv["mean"], sv["rstd"], S * R, Hm, dx=dm, accumulate=True,
+                      dgamma=g["opm.ln_g"], dbeta=g["opm.ln_b"])
+
+
+# ----------------------------------------------------------------------------- triangle update
+def triangle_fwd(bp: BlockParams, mod: str, z2d, R: int, save=True, Rl=None, gather=None):
+    """tri_update_outgoing / incoming (evoformer.py:258-284) + residual.
+
+    Y = LN(z) @ [W_g|W_as|W_al|W_bs|W_bl] + b (cuBLAS);  a, b = sigmoid gating
+    written channel-major (one kernel);  t_h = a_h b_h^T (outgoing) or
+    a_h^T b_h (incoming) as ONE batched tcgen05 GEMM over the p channels
+    (MN-major operands for incoming, no transposes);  LN over channels read
+    channel-major;  out = z + sigmoid(g) * (LN2(t) @ W_o + b_o) (one epilogue).
+    Single GPU: Rl = R.  DAP (outgoing: z is an i-shard [Rl, R]; incoming: a
+    j-shard stored as [R, Rl]): the other factor is all-gathered rank-major by
+    ``gather`` and addressed in place.
+    """
+    cfg = bp.cfg
+    P, Hz = cfg.hidden_proj, cfg.h_pair
+    incoming = mod == "tri_in"
+    Rl = R if Rl is None else Rl
+    rows = R * Rl
+    h, f = bp.h, bp.f
+    ln, mean, rstd = ops.layernorm_fwd(z2d, f[f"{mod}.ln_g"], f[f"{mod}.ln_b"], rows, Hz)
+    Y = torch.addmm(h[f"{mod}.b_proj"], ln, h[f"{mod}.w_proj"])       # [rows, Hz + 4P]
+    a_cm = torch.empty(P, rows, device=z2d.device, dtype=BF16)
+    b_cm = torch.empty_like(a_cm)
+    ops.tri_gate_fwd(Y, rows, Hz, P, a_cm, b_cm)
+    # local shapes: outgoing z-shard rows i (Rl), cols k (R); incoming rows k (R), cols j (Rl)
+    if not incoming:
+        A = Mat(a_cm, lo=(R, 1), batch_stride=rows)                   # A_h[i][k], K-major
+        if gather is None:
+            Bm, N = Mat(b_cm, lo=(R, 1), batch_stride=rows), R        # B_h[j][k], K-major
+            bfull = b_cm
+        else:
+            bfull = gather(b_cm)                                      # [N, P, Rl, R]
+            N = bfull.shape[0] * Rl
+            Bm = Mat(bfull, lo=(R, 1), split=(Rl, 0), hi=(P * Rl * R, 0), batch_stride=Rl * R)
+        M = Rl
+        t_cm = torch.empty(P, M, N, device=z2d.device, dtype=BF16)
+        ops.bgemm(A, Bm, Mat(t_cm, lo=(N, 1), batch_stride=M * N), P, M, N, R)
+        afull = a_cm
+    else:
+        Bm = Mat(b_cm, lo=(1, Rl), batch_stride=rows)                 # B_h[j][k] = b[k][j], MN-major
+        if gather is None:
+            A, M = Mat(a_cm, lo=(1, R), batch_stride=rows), R          # A_h[i][k] = a[k][i], MN-major
+            afull = a_cm
+        else:
+            afull = gather(a_cm)                                      # [N, P, R, Rl]  (cols i gathered)
+            M = afull.shape[0] * Rl
+            A = Mat(afull, lo=(1, Rl), split=(Rl, 0), hi=(P * R * Rl, 0), batch_stride=R * Rl)
+        N = Rl
+        t_cm = torch.empty(P, M, N, device=z2d.device, dtype=BF16)
+        ops.bgemm(A, Bm, Mat(t_cm, lo=(N, 1), batch_stride=M * N), P, M, N, R)
+        bfull = b_cm
+    ln2, mean2, rstd2 = ops.layernorm_fwd(t_cm, f[f"{mod}.ln2_g"], f[f"{mod}.ln2_b"], rows, P, x_rs=1, x_cs=rows)
+    y2 = _mm(ln2, h[f"{mod}.w_o"])
+    out = ops.gated_residual_fwd(z2d, y2, f[f"{mod}.b_o"], rows, Hz, gp=Y, gp_rs=Hz + 4 * P)
+    sv = Saved(z=z2d, ln=ln, mean=mean, rstd=rstd, Y=Y, a_cm=a_cm, b_cm=b_cm, afull=afull, bfull=bfull,
+               t_cm=t_cm, ln2=ln2, mean2=mean2, rstd2=rstd2, y2=y2, mod=mod, R=R, Rl=Rl, M=M, N=N,
+               gathered=gather is not None) if save else None
+    return out, sv
+
+
+def triangle_bwd(bp: BlockParams, sv: Saved, dz_new, reduce_scatter=None):
+    cfg = bp.cfg
+    P, Hz = cfg.hidden_proj, cfg.h_pair
+    mod, R, Rl, M, N = sv["mod"], sv["R"], sv["Rl"], sv["M"], sv["N"]
+    incoming = mod == "tri_in"
+    rows = R * Rl
+    h, f, g = bp.h, bp.f, bp.g
+    dev = dz_new.device
+    ld = Hz + 4 * P
+    dY = torch.empty(rows, ld, device=dev, dtype=BF16)
+    dy2 = torch.empty(rows, Hz, device=dev, dtype=BF16)
+    ops.gated_residual_bwd(dz_new, rows, Hz, y=sv["y2"], bias=f[f"{mod}.b_o"], gp=sv["Y"], gp_rs=ld, dy=dy2,
+                           dgp=dY, dgp_rs=ld, dbias=g[f"{mod}.b_o"])
+    _wgrad(sv["ln2"], dy2, g[f"{mod}.w_o"])
+    dln2 = _mm(dy2, h[f"{mod}.w_o"].t())                              # [rows, P]
+    dt_cm = torch.empty(P, rows, device=dev, dtype=BF16)
+    ops.layernorm_bwd(dln2, sv["t_cm"], f[f"{mod}.ln2_g"], sv["mean2"], sv["rstd2"], rows, P, x_rs=1, x_cs=rows,
+                      dx=dt_cm, dgamma=g[f"{mod}.ln2_g"], dbeta=g[f"{mod}.ln2_b"])
+    da_cm = torch.empty(P, rows, device=dev, dtype=BF16)
+    db_cm = torch.empty(P, rows, device=dev, dtype=BF16)
+    dT = Mat(dt_cm, lo=(N, 1), batch_stride=M * N)                    # dT_h[i][j] K-major over j
+    dTt = Mat(dt_cm, lo=(1, N), batch_stride=M * N)                   # as [j][i]
+    if not incoming:
+        # t[i][j] = sum_k a[i][k] b[j][k]:  da = dT b,  db = dT^T a   (b gathered under DAP)
+        bfull = sv["bfull"]
+        if not sv["gathered"]:
+            Bb = Mat(bfull, lo=(1, R), batch_stride=rows)             # [N=k][K=j] MN-major
+        else:
+            Bb = Mat(bfull, lo=(1, R), split=(0, Rl), hi=(0, P * Rl * R), batch_stride=Rl * R)
+        ops.bgemm(dT, Bb, Mat(da_cm, lo=(R, 1), batch_stride=rows), P, M, R, N)
+        Aa = Mat(sv["a_cm"], lo=(1, R), batch_stride=rows)            # [N=k][K=i] MN-major
+        if not sv["gathered"]:
+            ops.bgemm(dTt, Aa, Mat(db_cm, lo=(R, 1), batch_stride=rows), P, N, R, M)
+        else:
+            nd = N // Rl
+            dbf = torch.empty(nd, P, Rl, R, device=dev, dtype=F32)
+            ops.bgemm(dTt, Aa, Mat(dbf, lo=(R, 1), split=(Rl, 0), hi=(P * Rl * R, 0), batch_stride=Rl * R),
+                      P, N, R, M)
+            db_cm.copy_(reduce_scatter(dbf).view(P, rows))
+    else:
+        # t[i][j] = sum_k a[k][i] b[k][j]:  da[k][i] = sum_j b[k][j] dT[i][j],  db[k][j] = sum_i a[k][i] dT[i][j]
+        Ab = Mat(sv["b_cm"], lo=(Rl, 1), batch_stride=rows)           # [M=k][K=j] K-major
+        if not sv["gathered"]:
+            ops.bgemm(Ab, dT, Mat(da_cm, lo=(R, 1), batch_stride=rows), P, R, M, N)
+            Aa = Mat(sv["afull"], lo=(R, 1), batch_stride=rows)
+        else:
+            nd = M // Rl
+            daf = torch.empty(nd, P, R, Rl, device=dev, dtype=F32)
+            ops.bgemm(Ab, dT, Mat(daf, lo=(Rl, 1), split=(0, Rl), hi=(0, P * R * Rl), batch_stride=R * Rl),
+                      P, R, M, N)
+            da_cm.copy_(reduce_scatter(daf).view(P, rows))
+            Aa = Mat(sv["afull"], lo=(Rl, 1), split=(0, Rl), hi=(0, P * R * Rl), batch_stride=R * Rl)
+        ops.bgemm(Aa, dTt, Mat(db_cm, lo=(Rl, 1), batch_stride=rows), P, R, N, M)
+    ops.tri_gate_bwd(sv["Y"], da_cm, db_cm, rows, Hz, P, dY)
+    _wgrad(sv["ln"], dY, g[f"{mod}.w_proj"])
+    _bgrad(dY, g[f"{mod}.b_proj"])
+    dln = _mm(dY, h[f"{mod}.w_proj"].t())
+    dz = dz_new.clone()
+    ops.layernorm_bwd(dln, sv["z"], f[f"{mod}.ln_g"], sv["mean"], sv["rstd"], rows, Hz, dx=dz, accumulate=True,
+                      dgamma=g[f"{mod}.ln_g"], dbeta=g[f"{mod}.ln_b"])
+    return dz
+
+
+# ----------------------------------------------------------------------------- block
+def block_fwd(bp: BlockParams, m, z, save=True):
+    """evoformer_block (evoformer.py:314-325) on bf16 device tensors m [S,R,Hm], z [R,R,Hz]."""
+    cfg: EvoConfig = bp.cfg
+    S, R = cfg.n_seq, cfg.n_res
+    m2 = m.reshape(S * R, cfg.h_msa)
+    z2 = z.reshape(R * R, cfg.h_pair)
+    saved = [] if save else None
+    bias, sv_b = msa_row_bias_fwd(bp, z2, R, save)
+    m2, s1 = attention_fwd(bp, "msa_row", m2, S, R, "row", bias=bias, save=save)
+    m2, s2 = attention_fwd(bp, "msa_col", m2, R, S, "col", save=save)
+    m2, s3 = transition_fwd(bp, "msa_trans", m2, S * R, save)
+    z2, s4 = opm_fwd(bp, m2, z2, S, R, save)
+    z2, s5 = triangle_fwd(bp, "tri_out", z2, R, save)
+    z2, s6 = triangle_fwd(bp, "tri_in", z2, R, save)
+    z2, s7 = attention_fwd(bp, "pair_row", z2, R, R, "row", bias="pair", save=save)
+    z2, s8 = attention_fwd(bp, "pair_col", z2, R, R, "col", bias="pair", save=save)
+    z2, s9 = transition_fwd(bp, "pair_trans", z2, R * R, save)
+    if save:
+        saved.extend([sv_b, s1, s2, s3, s4, s5, s6, s7, s8, s9])
+    return m2.view(S, R, cfg.h_msa), z2.view(R, R, cfg.h_pair), saved
+
+
+def block_bwd(bp: BlockParams, saved, dm, dz):
+    """gradients w.r.t. (m, z) of the block input; parameter grads accumulate into bp.grad."""
+    cfg: EvoConfig = bp.cfg
+    S, R = cfg.n_seq, cfg.n_res
+    sv_b, s1, s2, s3, s4, s5, s6, s7, s8, s9 = saved
+    dm2 = dm.reshape(S * R, cfg.h_msa).contiguous()
+    dz2 = dz.reshape(R * R, cfg.h_pair).contiguous()
+    dz2 = transition_bwd(bp, s9, dz2)
+    dz2, _ = attention_bwd(bp, s8, dz2)
+    dz2, _ = attention_bwd(bp, s7, dz2)
+    dz2 = triangle_bwd(bp, s6, dz2)
+    dz2 = triangle_bwd(bp, s5, dz2)
+    dm2 = dm2.clone()
+    opm_bwd(bp, s4, dz2, dm2)
+    dm2 = transition_bwd(bp, s3, dm2)
+    dm2, _ = attention_bwd(bp, s2, dm2)
+    dm2, dbias = attention_bwd(bp, s1, dm2)
+    msa_row_bias_bwd(bp, sv_b, dbias, dz2)
+    return dm2.view(S, R, cfg.h_msa), dz2.view(R, R, cfg.h_pair)

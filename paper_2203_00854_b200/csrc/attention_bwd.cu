@@ -1,0 +1,415 @@
+// Backward of the gated attention with bias (evoformer.py:173-198), flash-style on
+// tcgen05.  The reference has no backward; the gradient oracle is
+// the torch float64 restatement in oracle/evoformer_torch.py.
+//
+//   prep   (warp per row)  dO = dout * sigmoid(g);  dg = dout * O * s(1-s);  D = rowsum(dO * O)
+//   main   one CTA = (batch, head, 128-key tile), 8 warps, loops over 128-query tiles:
+//            S^T  = K Q^T            (tcgen05, M=keys N=queries)  -> TMEM cols [0,128)
+//            dP^T = V dO^T           (tcgen05)                    -> TMEM cols [128,256)
+//            P^T  = exp2(S^T*scale + bias - lse), dS^T = P^T (dP^T - D)   (registers)
+//            P^T, dS^T -> smem (bf16, canonical K-major [key][query])
+//            dV  += P^T dO,  dK += dS^T Q   (accumulated in TMEM over query tiles)
+//            dQ_t = dS K  (same smem tile read as its transpose by swapping the
+//                   descriptor's LBO/SBO and the major bit) -> fp32 atomics
+//            dbias += scale * dS (atomics; per-key bias pre-reduced over queries)
+//   finish dq = bf16(dQ accumulator)
+#include "attn.cuh"
+
+namespace evo {
+
+
+struct AttnBwdParams {
+  AttnParams f;
+  const bf16* dout;
+  int64_t do_sb, do_sl;
+  bf16 *dq, *dk, *dv, *dg;
+  int64_t dq_sb, dq_sl, dk_sb, dk_sl, dv_sb, dv_sl, dg_sb, dg_sl;
+  float* dbias;
+  int64_t db0, db1, db2, db3;
+  bf16* dO;      // workspace [B][L][H*c]
+  float* dQacc;  // workspace [B][L][H*c]
+  float* Dsum;   // workspace [B][H][L]
+  float scale;
+};
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+
+// ---------------------------------------------------------------------------------- prep
+// one warp per (b, l) row; lanes walk the H*c channels in 8-element chunks
+__global__ void __launch_bounds__(256) attn_bwd_prep(AttnBwdParams P, int64_t B) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int L = P.f.L, H = P.f.H, c = P.f.c;
+  if (row >= B * L) return;
+  const int64_t b = row / L, l = row % L;
+  const int nch = H * c / 8;
+  const int lanes_per_head = c / 8;  // 1, 2, 4 or 8
+  for (int base = 0; base < nch; base += 32) {
+    const int ch = base + lane;
+    float dsum = 0.f;
+    if (ch < nch) {
+      const int col = ch * 8;
+      float dout[8], g[8], o[8], dO[8], dg[8];
+      const uint4 ud = *reinterpret_cast<const uint4*>(P.dout + b * P.do_sb + l * P.do_sl + col);
+      const uint4 ug = *reinterpret_cast<const uint4*>(P.f.g + b * P.f.g_sb + l * P.f.g_sl + col);
+      const uint4 uo = *reinterpret_cast<const uint4*>(P.f.orw + b * P.f.r_sb + l * P.f.r_sl + col);
+      unpack_bf16x2(ud.x, dout[0], dout[1]); unpack_bf16x2(ud.y, dout[2], dout[3]);
+      unpack_bf16x2(ud.z, dout[4], dout[5]); unpack_bf16x2(ud.w, dout[6], dout[7]);
+      unpack_bf16x2(ug.x, g[0], g[1]); unpack_bf16x2(ug.y, g[2], g[3]);
+      unpack_bf16x2(ug.z, g[4], g[5]); unpack_bf16x2(ug.w, g[6], g[7]);
+      unpack_bf16x2(uo.x, o[0], o[1]); unpack_bf16x2(uo.y, o[2], o[3]);
+      unpack_bf16x2(uo.z, o[4], o[5]); unpack_bf16x2(uo.w, o[6], o[7]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float s = sigmoidf_(g[e]);
+        dO[e] = dout[e] * s;
+        dg[e] = dout[e] * o[e] * s * (1.f - s);
+        dsum += dO[e] * o[e];
+      }
+      uint4 w;
+      w.x = pack_bf16x2(dO[0], dO[1]); w.y = pack_bf16x2(dO[2], dO[3]);
+      w.z = pack_bf16x2(dO[4], dO[5]); w.w = pack_bf16x2(dO[6], dO[7]);
+      *reinterpret_cast<uint4*>(P.dO + row * (int64_t)(H * c) + col) = w;
+      w.x = pack_bf16x2(dg[0], dg[1]); w.y = pack_bf16x2(dg[2], dg[3]);
+      w.z = pack_bf16x2(dg[4], dg[5]); w.w = pack_bf16x2(dg[6], dg[7]);
+      *reinterpret_cast<uint4*>(P.dg + b * P.dg_sb + l * P.dg_sl + col) = w;
+    }
+    // segmented reduction over the lanes of one head (lanes_per_head is a power of 2)
+    for (int o = 1; o < lanes_per_head; o <<= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
+    if (ch < nch && (lane % lanes_per_head) == 0) {
+      const int h = (ch * 8) / c;
+      P.Dsum[(b * H + h) * (int64_t)L + l] = dsum;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------- main
+constexpr int BW_BK = 128;  // keys per CTA
+constexpr int BW_BQ = 128;  // queries per iteration
+
+template <int CP>
+struct BwdSmem {
+  static constexpr uint32_t K = 0;                          // [key][d] K-major
+  static constexpr uint32_t V = K + BW_BK * CP * 2;         // [key][d] K-major
+  static constexpr uint32_t Q = V + BW_BK * CP * 2;         // [query][d] K-major
+  static constexpr uint32_t DO = Q + BW_BQ * CP * 2;        // [query][d] K-major
+  static constexpr uint32_t PT = DO + BW_BQ * CP * 2;       // [key][query] K-major
+  static constexpr uint32_t DST = PT + BW_BK * BW_BQ * 2;   // [key][query] K-major
+  static constexpr uint32_t LSE = DST + BW_BK * BW_BQ * 2;  // fp32 [128]
+  static constexpr uint32_t DD = LSE + BW_BQ * 4;           // fp32 [128]
+  static constexpr uint32_t KB = DD + BW_BQ * 4;            // fp32 [2][128] per-key dbias partials
+  static constexpr uint32_t TOTAL = KB + 2 * BW_BK * 4;
+};
+
+template <int CP>
+__device__ __forceinline__ void bw_load(uint32_t sdst, const bf16* base, int64_t row_stride, int row0, int nvalid,
+                                        int c) {
+  constexpr int CPR = CP / 8;
+  for (int ch = threadIdx.x; ch < 128 * CPR; ch += 256) {
+    const int r = ch / CPR, d = (ch % CPR) * 8;
+    const bool ok = (r < nvalid) && (d < c);
+    const bf16* src = ok ? base + (int64_t)(row0 + r) * row_stride + d : base;
+    cp_async16(sdst + kmajor_off(r, d, 128), src, ok);
+  }
+}
+
+template <int CP>
+__global__ void __launch_bounds__(256, 1) attn_bwd_kernel(AttnBwdParams P) {
+  using SM = BwdSmem<CP>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar1, bar2;
+  __shared__ uint32_t tmem_sh;
+  const uint32_t sb = smem_u32(smem);
+  float* s_lse = reinterpret_cast<float*>(smem + SM::LSE);
+  float* s_D = reinterpret_cast<float*>(smem + SM::DD);
+  float* s_kb = reinterpret_cast<float*>(smem + SM::KB);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wq = warp & 3, wg = warp >> 2;
+  const int k0 = blockIdx.x * BW_BK;
+  const int h = blockIdx.y;
+  const int64_t b = blockIdx.z;
+  const AttnParams& F = P.f;
+  const int L = F.L, c = F.c, H = F.H;
+  const int kr = wq * 32 + lane;  // key row of this thread (TMEM lane)
+  const int kj = k0 + kr;
+  const bool kvalid = kj < L;
+  const bool per_key_bias = F.bias && F.bs2 == 0;
+  const bool db_per_key = P.dbias && P.db2 == 0;
+
+  if (warp == 0) tmem_alloc(&tmem_sh, 512);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar1, 1);
+    mbar_init(&bar2, 1);
+    fence_mbar_init();
+  }
+  const bf16* kb = F.k + b * F.k_sb + (int64_t)h * c;
+  const bf16* vb = F.v + b * F.v_sb + (int64_t)h * c;
+  const bf16* qb = F.q + b * F.q_sb + (int64_t)h * c;
+  const bf16* dob = P.dO + b * (int64_t)L * H * c + (int64_t)h * c;
+  bw_load<CP>(sb + SM::K, kb, F.k_sl, k0, L - k0, c);
+  bw_load<CP>(sb + SM::V, vb, F.v_sl, k0, L - k0, c);
+  cp_async_commit();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_sh;
+  const uint32_t t_lane = tmem + ((uint32_t)(wq * 32) << 16);
+  constexpr uint32_t T_S = 0, T_DP = 128, T_DV = 256, T_DK = 256 + CP, T_DQ = 0;
+
+  float kbias = 0.f;
+  if (per_key_bias && kvalid) kbias = bf2f(F.bias[b * F.bs0 + (int64_t)h * F.bs1 + (int64_t)kj * F.bs3]);
+  const bf16* bias_col = nullptr;  // full bias: element (q, kj)
+  if (F.bias && !per_key_bias && kvalid) bias_col = F.bias + b * F.bs0 + (int64_t)h * F.bs1 + (int64_t)kj * F.bs3;
+  float* dbias_col = nullptr;
+  if (P.dbias && kvalid) dbias_col = P.dbias + b * P.db0 + (int64_t)h * P.db1 + (int64_t)kj * P.db3;
+  const float LOG2E_ = 1.4426950408889634f;
+
+  constexpr uint32_t ID_SS = make_idesc_bf16(128, 128, 0, 0);  // S^T = K Q^T, dP^T = V dO^T
+  constexpr uint32_t ID_KV = make_idesc_bf16(128, CP, 0, 1);   // dV += P^T dO, dK += dS^T Q  (B MN-major view)
+  constexpr uint32_t ID_Q = make_idesc_bf16(128, CP, 1, 1);    // dQ = dS K (A and B as MN-major views)
+  constexpr uint32_t LBO_ROWS = (128 / 8) * 128;               // 2048: next 8-k group of a 128-row K-major tile
+
+  const int nqt = (L + BW_BQ - 1) / BW_BQ;
+  for (int it = 0; it < nqt; ++it) {
+    const int q0 = it * BW_BQ;
+    bw_load<CP>(sb + SM::Q, qb, F.q_sl, q0, L - q0, c);
+    bw_load<CP>(sb + SM::DO, dob, (int64_t)H * c, q0, L - q0, c);
+    cp_async_commit();
+    if (threadIdx.x < BW_BQ) {
+      const int qq = q0 + threadIdx.x;
+      s_lse[threadIdx.x] = qq < L ? F.lse[(b * H + h) * (int64_t)L + qq] * LOG2E_ : 0.f;
+      s_D[threadIdx.x] = qq < L ? P.Dsum[(b * H + h) * (int64_t)L + qq] : 0.f;
+    }
+    cp_async_wait<0>();
+    fence_async_smem();
+    __syncthreads();
+
+    if (threadIdx.x == 0) {
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < CP / 16; ++kk) {
+        const uint32_t koff = kk * 2 * LBO_ROWS;
+        mma_bf16(tmem + T_S, make_sdesc(sb + SM::K + koff, LBO_ROWS, 128), make_sdesc(sb + SM::Q + koff, LBO_ROWS, 128),
+                 ID_SS, kk != 0);
+        mma_bf16(tmem + T_DP, make_sdesc(sb + SM::V + koff, LBO_ROWS, 128),
+                 make_sdesc(sb + SM::DO + koff, LBO_ROWS, 128), ID_SS, kk != 0);
+      }
+      mma_commit(&bar1);
+    }
+    mbar_wait(&bar1, it & 1);
+    tc_fence_after();
+
+    float kb_acc = 0.f;
+#pragma unroll 1
+    for (int half = 0; half < 2; ++half) {
+      const int qc = wg * 64 + half * 32;  // query column offset inside the tile
+      float s[32], dp[32];
+      tmem_ld32(t_lane + T_S + qc, s);
+      tmem_ld32(t_lane + T_DP + qc, dp);
+      tmem_ld_wait();
+      float pv[32], dsv[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        const int ql = qc + e, qq = q0 + ql;
+        float x = s[e];
+        if (bias_col && qq < L) x += bf2f(bias_col[(int64_t)qq * F.bs2]);
+        x += kbias;
+        const bool ok = kvalid && qq < L;
+        const float p = ok ? exp2f(x * F.scale_log2 - s_lse[ql]) : 0.f;
+        const float ds = p * (dp[e] - s_D[ql]);
+        pv[e] = p;
+        dsv[e] = ds;
+        if (ok) {
+          if (db_per_key) kb_acc += ds;
+          else if (dbias_col) atomicAdd(dbias_col + (int64_t)qq * P.db2, P.scale * ds);
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 32; e += 8) {
+        st_shared_v4(sb + SM::PT + kmajor_off(kr, qc + e, 128), pack_bf16x2(pv[e], pv[e + 1]),
+                     pack_bf16x2(pv[e + 2], pv[e + 3]), pack_bf16x2(pv[e + 4], pv[e + 5]),
+                     pack_bf16x2(pv[e + 6], pv[e + 7]));
+        st_shared_v4(sb + SM::DST + kmajor_off(kr, qc + e, 128), pack_bf16x2(dsv[e], dsv[e + 1]),
+                     pack_bf16x2(dsv[e + 2], dsv[e + 3]), pack_bf16x2(dsv[e + 4], dsv[e + 5]),
+                     pack_bf16x2(dsv[e + 6], dsv[e + 7]));
+      }
+    }
+    if (db_per_key) s_kb[wg * BW_BK + kr] = kb_acc;
+
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    if (db_per_key && wg == 0 && dbias_col) atomicAdd(dbias_col, P.scale * (s_kb[kr] + s_kb[BW_BK + kr]));
+    if (threadIdx.x == 0) {
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < BW_BQ / 16; ++kk) {
+        // A = P^T / dS^T [key][query] K-major; B = dO / Q [query][d] viewed MN-major (mn = d, k = query)
+        const uint32_t aoff = kk * 2 * LBO_ROWS;
+        const uint32_t boff = kk * 2 * 128;
+        mma_bf16(tmem + T_DV, make_sdesc(sb + SM::PT + aoff, LBO_ROWS, 128),
+                 make_sdesc(sb + SM::DO + boff, 128, LBO_ROWS), ID_KV, (it | kk) != 0);
+        mma_bf16(tmem + T_DK, make_sdesc(sb + SM::DST + aoff, LBO_ROWS, 128),
+                 make_sdesc(sb + SM::Q + boff, 128, LBO_ROWS), ID_KV, (it | kk) != 0);
+      }
+#pragma unroll
+      for (int kk = 0; kk < BW_BK / 16; ++kk) {
+        // A = dS [query][key] = dS^T tile viewed MN-major (mn = query, k = key); B = K [key][d] viewed MN-major
+        const uint32_t off = kk * 2 * 128;
+        mma_bf16(tmem + T_DQ, make_sdesc(sb + SM::DST + off, 128, LBO_ROWS), make_sdesc(sb + SM::K + off, 128, LBO_ROWS),
+                 ID_Q, kk != 0);
+      }
+      mma_commit(&bar2);
+    }
+    mbar_wait(&bar2, it & 1);
+    tc_fence_after();
+    {
+      // dQ partial: TMEM lane = query row; warpgroup wg handles columns [wg*CP/2, (wg+1)*CP/2)
+      const int qq = q0 + kr;
+      float v[CP / 2];
+      if constexpr (CP == 16) tmem_ld8(t_lane + T_DQ + wg * 8, v);
+      else if constexpr (CP == 32) tmem_ld16(t_lane + T_DQ + wg * 16, v);
+      else tmem_ld32(t_lane + T_DQ + wg * 32, v);
+      tmem_ld_wait();
+      if (qq < L) {
+        float* dst = P.dQacc + (b * L + qq) * (int64_t)(H * c) + (int64_t)h * c + wg * (CP / 2);
+#pragma unroll
+        for (int e = 0; e < CP / 2; ++e)
+          if (wg * (CP / 2) + e < c) atomicAdd(dst + e, P.scale * v[e]);
+      }
+    }
+    tc_fence_before();
+    __syncthreads();
+  }
+
+  // dV (warpgroup 0) and dK (warpgroup 1): TMEM lane = key row
+  {
+    float v[CP];
+    const uint32_t col = wg == 0 ? T_DV : T_DK;
+    if constexpr (CP == 16) tmem_ld16(t_lane + col, v);
+    else {
+#pragma unroll
+      for (int cc = 0; cc < CP; cc += 32) tmem_ld32(t_lane + col + cc, v + cc);
+    }
+    tmem_ld_wait();
+    if (kvalid) {
+      const float sc = wg == 0 ? 1.f : P.scale;
+      bf16* dst = wg == 0 ? P.dv + b * P.dv_sb + (int64_t)kj * P.dv_sl + (int64_t)h * c
+                          : P.dk + b * P.dk_sb + (int64_t)kj * P.dk_sl + (int64_t)h * c;
+#pragma unroll
+      for (int d = 0; d < CP; d += 8) {
+        if (d < c) {
+          uint4 w;
+          w.x = pack_bf16x2(sc * v[d], sc * v[d + 1]);
+          w.y = pack_bf16x2(sc * v[d + 2], sc * v[d + 3]);
+          w.z = pack_bf16x2(sc * v[d + 4], sc * v[d + 5]);
+          w.w = pack_bf16x2(sc * v[d + 6], sc * v[d + 7]);
+          *reinterpret_cast<uint4*>(dst + d) = w;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+__global__ void __launch_bounds__(256) attn_bwd_dq_finish(AttnBwdParams P, int64_t B) {
+  const int L = P.f.L, H = P.f.H, c = P.f.c;
+  const int64_t n8 = B * L * (int64_t)H * c / 8;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i * 8;
+    const int64_t row = e / (H * c), col = e % (H * c);
+    const int64_t b = row / L, l = row % L;
+    const float4 a = *reinterpret_cast<const float4*>(P.dQacc + e);
+    const float4 bq = *reinterpret_cast<const float4*>(P.dQacc + e + 4);
+    uint4 w;
+    w.x = pack_bf16x2(a.x, a.y); w.y = pack_bf16x2(a.z, a.w);
+    w.z = pack_bf16x2(bq.x, bq.y); w.w = pack_bf16x2(bq.z, bq.w);
+    *reinterpret_cast<uint4*>(P.dq + b * P.dq_sb + l * P.dq_sl + col) = w;
+  }
+}
+
+static int64_t ws_layout(int64_t B, int64_t L, int H, int c, int64_t* off_dq, int64_t* off_D) {
+  const int64_t n = B * L * (int64_t)H * c;
+  int64_t o1 = ((n * 2 + 255) / 256) * 256;
+  int64_t o2 = o1 + ((n * 4 + 255) / 256) * 256;
+  if (off_dq) *off_dq = o1;
+  if (off_D) *off_D = o2;
+  return o2 + ((B * H * L * 4 + 255) / 256) * 256;
+}
+
+int sm_count();
+
+template <int CP>
+static int launch_bwd(AttnBwdParams& p, int64_t B, cudaStream_t st) {
+  using SM = BwdSmem<CP>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel<CP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM::TOTAL);
+    if (e != cudaSuccess) return cuda_status(e, "attn bwd attr");
+    attr = true;
+  }
+  dim3 grid((unsigned)((p.f.L + BW_BK - 1) / BW_BK), (unsigned)p.f.H, (unsigned)B);
+  attn_bwd_kernel<CP><<<grid, 256, SM::TOTAL, st>>>(p);
+  EVO_LAUNCH_CHECK("attention bwd main");
+  return EVO_OK;
+}
+
+}  // namespace evo
+
+using namespace evo;
+
+extern "C" int64_t evo_gated_attention_bwd_workspace(int64_t B, int64_t L, int H, int c) {
+  return ws_layout(B, L, H, c, nullptr, nullptr);
+}
+
+extern "C" int evo_gated_attention_bwd(const EvoAttnBwdDesc* d, void* stream) {
+  EVO_CHECK_ARG(d, EVO_ERR_ARG, "attention bwd: null descriptor");
+  AttnBwdParams p;
+  int rc = attn_params_from_desc(&d->f, p.f);
+  if (rc) return rc;
+  EVO_CHECK_ARG(d->f.o_raw && d->f.lse && d->dout && d->dq && d->dk && d->dv && d->dg && d->workspace, EVO_ERR_ARG,
+                "attention bwd: null pointer (o_raw, lse, dout, dq, dk, dv, dg, workspace are required)");
+  const int64_t B = d->f.B, L = d->f.L;
+  const int H = d->f.H, c = d->f.c;
+  int64_t off_dq, off_D;
+  const int64_t need = ws_layout(B, L, H, c, &off_dq, &off_D);
+  EVO_CHECK_ARG(d->workspace_bytes >= need, EVO_ERR_ARG, "attention bwd: workspace %lld < %lld bytes",
+                (long long)d->workspace_bytes, (long long)need);
+  const int64_t strides[] = {d->do_sb, d->do_sl, d->dq_sb, d->dq_sl, d->dk_sb, d->dk_sl, d->dv_sb, d->dv_sl,
+                             d->dg_sb, d->dg_sl};
+  for (int64_t s : strides) EVO_CHECK_ARG(s % 8 == 0, EVO_ERR_ALIGN, "attention bwd: strides must be multiples of 8");
+  p.dout = (const bf16*)d->dout;
+  p.do_sb = d->do_sb; p.do_sl = d->do_sl;
+  p.dq = (bf16*)d->dq; p.dk = (bf16*)d->dk; p.dv = (bf16*)d->dv; p.dg = (bf16*)d->dg;
+  p.dq_sb = d->dq_sb; p.dq_sl = d->dq_sl; p.dk_sb = d->dk_sb; p.dk_sl = d->dk_sl;
+  p.dv_sb = d->dv_sb; p.dv_sl = d->dv_sl; p.dg_sb = d->dg_sb; p.dg_sl = d->dg_sl;
+  p.dbias = d->dbias;
+  p.db0 = d->dbias_s[0]; p.db1 = d->dbias_s[1]; p.db2 = d->dbias_s[2]; p.db3 = d->dbias_s[3];
+  char* ws = (char*)d->workspace;
+  p.dO = (bf16*)ws;
+  p.dQacc = (float*)(ws + off_dq);
+  p.Dsum = (float*)(ws + off_D);
+  p.scale = d->f.scale;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(p.dQacc, 0, (size_t)(B * L * H * c) * 4, st);
+  if (e != cudaSuccess) return cuda_status(e, "attention bwd memset");
+  attn_bwd_prep<<<(unsigned)((B * L + 7) / 8), 256, 0, st>>>(p, B);
+  EVO_LAUNCH_CHECK("attention bwd prep");
+  if (c <= 16) rc = launch_bwd<16>(p, B, st);
+  else if (c <= 32) rc = launch_bwd<32>(p, B, st);
+  else rc = launch_bwd<64>(p, B, st);
+  if (rc) return rc;
+  int64_t n8 = B * L * H * c / 8;
+  int64_t g = (n8 + 255) / 256, cap = (int64_t)sm_count() * 16;
+  attn_bwd_dq_finish<<<(unsigned)(g < cap ? g : cap), 256, 0, st>>>(p, B);
+  EVO_LAUNCH_CHECK("attention bwd finish");
+  return EVO_OK;
+}

@@ -1,0 +1,404 @@
+// Fused elementwise epilogues of the Evoformer block (HBM-bound, 16-byte vectors):
+//   * gated residual  out = res + sigmoid(gp) * (y + bias)  - every residual add of
+//     evoformer_block (evoformer.py:316-324) with the projection bias folded in,
+//     and the triangle g-gate (evoformer.py:270);
+//   * bias + ReLU of the transition hidden layer (evoformer.py:239);
+//   * triangle gating a = sigmoid(.)*(.), b = sigmoid(.)*(.) (evoformer.py:261-264)
+//     with a channel-major write (so the einsum is a batched GEMM over channels);
+//   * non-finite counter (engine.py:186-187 DomainError twin).
+// Backward kernels reduce bias gradients per column with a [32 x 8] thread tile,
+// shared-memory partials and one atomicAdd per column per CTA.
+#include "common.cuh"
+
+namespace evo {
+int sm_count();
+
+template <typename T>
+__device__ __forceinline__ void ld8(const T* p, float* v) {
+  if constexpr (sizeof(T) == 2) {
+    uint4 u = *reinterpret_cast<const uint4*>(p);
+    unpack_bf16x2(u.x, v[0], v[1]); unpack_bf16x2(u.y, v[2], v[3]);
+    unpack_bf16x2(u.z, v[4], v[5]); unpack_bf16x2(u.w, v[6], v[7]);
+  } else {
+    float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+}
+template <typename T>
+__device__ __forceinline__ void st8(T* p, const float* v) {
+  if constexpr (sizeof(T) == 2) {
+    uint4 u;
+    u.x = pack_bf16x2(v[0], v[1]); u.y = pack_bf16x2(v[2], v[3]);
+    u.z = pack_bf16x2(v[4], v[5]); u.w = pack_bf16x2(v[6], v[7]);
+    *reinterpret_cast<uint4*>(p) = u;
+  } else {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<float4*>(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
+  }
+}
+
+// ------------------------------------------------------------------ gated residual
+template <typename T>
+__global__ void __launch_bounds__(256) gated_residual_fwd_k(const T* __restrict__ res, const T* __restrict__ y,
+                                                            int64_t y_rs, const float* __restrict__ bias,
+                                                            const T* __restrict__ gp, int64_t gp_rs,
+                                                            T* __restrict__ out, int64_t rows, int64_t cols) {
+  const int64_t cpr = cols / 8;
+  const int64_t n = rows * cpr;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cpr, c = (i - r * cpr) * 8;
+    float rv[8], yv[8];
+    ld8<T>(res + r * cols + c, rv);
+    ld8<T>(y + r * y_rs + c, yv);
+    if (bias) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) yv[e] += bias[c + e];
+    }
+    if (gp) {
+      float gv[8];
+      ld8<T>(gp + r * gp_rs + c, gv);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) yv[e] *= sigmoidf_(gv[e]);
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) rv[e] += yv[e];
+    st8<T>(out + r * cols + c, rv);
+  }
+}
+
+// block (32, 8): x = column chunk (8 cols), y = row lane
+template <typename T>
+__global__ void __launch_bounds__(256) gated_residual_bwd_k(const T* __restrict__ dout, const T* __restrict__ y,
+                                                            int64_t y_rs, const float* __restrict__ bias,
+                                                            const T* __restrict__ gp, int64_t gp_rs, T* __restrict__ dy,
+                                                            T* __restrict__ dgp, int64_t dgp_rs,
+                                                            float* __restrict__ dbias, int64_t rows, int64_t cols) {
+  __shared__ float red[8][32 * 8 + 1];
+  const int64_t cchunk = (int64_t)blockIdx.x * 32 + threadIdx.x;
+  const bool cok = cchunk * 8 < cols;
+  const int64_t c = cchunk * 8;
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (cok) {
+    float b[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (bias) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) b[e] = bias[c + e];
+    }
+    for (int64_t r = (int64_t)blockIdx.y * 8 + threadIdx.y; r < rows; r += (int64_t)gridDim.y * 8) {
+      float d[8];
+      ld8<T>(dout + r * cols + c, d);
+      if (gp) {
+        float gv[8], yv[8], dg[8];
+        ld8<T>(gp + r * gp_rs + c, gv);
+        ld8<T>(y + r * y_rs + c, yv);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          float s = sigmoidf_(gv[e]);
+          dg[e] = d[e] * (yv[e] + b[e]) * s * (1.f - s);
+          d[e] *= s;
+        }
+        st8<T>(dgp + r * dgp_rs + c, dg);
+      }
+      if (dy) st8<T>(dy + r * cols + c, d);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += d[e];
+    }
+  }
+  if (!dbias) return;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) red[threadIdx.y][threadIdx.x * 8 + e] = acc[e];
+  __syncthreads();
+  if (threadIdx.y == 0 && cok) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      float s = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s += red[k][threadIdx.x * 8 + e];
+      atomicAdd(dbias + c + e, s);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ bias + activation
+template <typename T>
+__global__ void __launch_bounds__(256) bias_act_fwd_k(T* __restrict__ y, const float* __restrict__ bias, int64_t rows,
+                                                      int64_t cols, int act) {
+  const int64_t cpr = cols / 8, n = rows * cpr;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cpr, c = (i - r * cpr) * 8;
+    float v[8];
+    ld8<T>(y + r * cols + c, v);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      v[e] += bias ? bias[c + e] : 0.f;
+      if (act == 1) v[e] = fmaxf(v[e], 0.f);
+    }
+    st8<T>(y + r * cols + c, v);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) bias_act_bwd_k(const T* __restrict__ dh, const T* __restrict__ h,
+                                                      T* __restrict__ dy, float* __restrict__ dbias, int64_t rows,
+                                                      int64_t cols, int act) {
+  __shared__ float red[8][32 * 8 + 1];
+  const int64_t cchunk = (int64_t)blockIdx.x * 32 + threadIdx.x;
+  const bool cok = cchunk * 8 < cols;
+  const int64_t c = cchunk * 8;
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (cok) {
+    for (int64_t r = (int64_t)blockIdx.y * 8 + threadIdx.y; r < rows; r += (int64_t)gridDim.y * 8) {
+      float d[8], hv[8];
+      ld8<T>(dh + r * cols + c, d);
+      if (act == 1) {
+        ld8<T>(h + r * cols + c, hv);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) d[e] = hv[e] > 0.f ? d[e] : 0.f;
+      }
+      st8<T>(dy + r * cols + c, d);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += d[e];
+    }
+  }
+  if (!dbias) return;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) red[threadIdx.y][threadIdx.x * 8 + e] = acc[e];
+  __syncthreads();
+  if (threadIdx.y == 0 && cok) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      float s = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s += red[k][threadIdx.x * 8 + e];
+      atomicAdd(dbias + c + e, s);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ triangle gating
+// RB rows per CTA; Y row slice [hz, hz+4p) staged in shared memory as fp32
+template <int P>
+__global__ void __launch_bounds__(256) tri_gate_fwd_k(const bf16* __restrict__ y, int64_t rows, int hz,
+                                                      bf16* __restrict__ a_cm, bf16* __restrict__ b_cm) {
+  constexpr int W = 4 * P;
+  constexpr int RB = P <= 32 ? 64 : 32;
+  __shared__ float ys[RB][W + 1];
+  const int64_t r0 = (int64_t)blockIdx.x * RB;
+  const int64_t ld = hz + W;
+  for (int i = threadIdx.x; i < RB * W / 8; i += blockDim.x) {
+    const int r = i / (W / 8), c = (i % (W / 8)) * 8;
+    float v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (r0 + r < rows) ld8<bf16>(y + (r0 + r) * ld + hz + c, v);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) ys[r][c + e] = v[e];
+  }
+  __syncthreads();
+  // write a[h][r], b[h][r]: consecutive threads -> consecutive rows (coalesced)
+  for (int i = threadIdx.x; i < 2 * P * RB; i += blockDim.x) {
+    const int r = i % RB, ch = i / RB;  // ch < 2P
+    if (r0 + r >= rows) continue;
+    const int h = ch % P, which = ch / P;  // 0 = a, 1 = b
+    const float s = ys[r][which * 2 * P + h], l = ys[r][which * 2 * P + P + h];
+    const float v = sigmoidf_(s) * l;
+    bf16* dst = which ? b_cm : a_cm;
+    dst[(int64_t)h * rows + r0 + r] = f2bf(v);
+  }
+}
+
+template <int P, typename TD>
+__global__ void __launch_bounds__(256) tri_gate_bwd_k(const bf16* __restrict__ y, const TD* __restrict__ da,
+                                                      const TD* __restrict__ db, int64_t rows, int hz,
+                                                      bf16* __restrict__ dy) {
+  constexpr int W = 4 * P;
+  __shared__ float gs[64][2 * P + 1];
+  const int64_t r0 = (int64_t)blockIdx.x * 64;
+  const int64_t ld = hz + W;
+  for (int i = threadIdx.x; i < 2 * P * 64; i += blockDim.x) {
+    const int r = i & 63, ch = i >> 6;
+    float v = 0.f;
+    if (r0 + r < rows) {
+      const int h = ch % P;
+      const TD* src = ch < P ? da : db;
+      v = ldf<TD>(src + (int64_t)h * rows + r0 + r);
+    }
+    gs[r][ch] = v;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 64 * W / 8; i += blockDim.x) {
+    const int r = i / (W / 8), c = (i % (W / 8)) * 8;  // c in [0, 4P)
+    if (r0 + r >= rows) continue;
+    float o[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int which = (c + e) / (2 * P);              // 0: a block, 1: b block
+      const int cc = (c + e) % (2 * P);                 // [0, P) = sig part, [P, 2P) = lin part
+      const bf16* yrow = y + (r0 + r) * ld + hz + which * 2 * P;
+      const int h = cc % P;
+      const float s = bf2f(yrow[h]), l = bf2f(yrow[P + h]);
+      const float sg = sigmoidf_(s);
+      const float g = gs[r][which * P + h];
+      o[e] = cc < P ? g * l * sg * (1.f - sg) : g * sg;
+    }
+    st8<bf16>(dy + (r0 + r) * ld + hz + c, o);
+  }
+}
+
+template <typename T>
+__global__ void count_nonfinite_k(const T* __restrict__ x, int64_t n, unsigned int* counter) {
+  unsigned int local = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    local += isfinite(ldf<T>(x + i)) ? 0u : 1u;
+  for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(counter, local);
+}
+
+static unsigned grid_for(int64_t work, int threads) {
+  int64_t need = (work + threads - 1) / threads;
+  int64_t cap = (int64_t)sm_count() * 16;
+  return (unsigned)(need < 1 ? 1 : (need < cap ? need : cap));
+}
+
+static bool al16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+}  // namespace evo
+
+using namespace evo;
+
+extern "C" int evo_gated_residual_fwd(const void* res, const void* y, int64_t y_rs, const float* bias, const void* gp,
+                                      int64_t gp_rs, void* out, int dtype, int64_t rows, int64_t cols, void* stream) {
+  EVO_CHECK_ARG(res && y && out, EVO_ERR_ARG, "gated_residual: null pointer");
+  EVO_CHECK_ARG(cols % 8 == 0 && y_rs % 8 == 0 && (!gp || gp_rs % 8 == 0), EVO_ERR_ALIGN,
+                "gated_residual: cols and row strides must be multiples of 8");
+  EVO_CHECK_ARG(al16(res) && al16(y) && al16(out) && (!gp || al16(gp)), EVO_ERR_ALIGN,
+                "gated_residual: pointers must be 16B aligned");
+  if (rows == 0) return EVO_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned g = grid_for(rows * cols / 8, 256);
+  if (dtype == EVO_BF16)
+    gated_residual_fwd_k<bf16><<<g, 256, 0, st>>>((const bf16*)res, (const bf16*)y, y_rs, bias, (const bf16*)gp,
+                                                  gp_rs, (bf16*)out, rows, cols);
+  else
+    gated_residual_fwd_k<float><<<g, 256, 0, st>>>((const float*)res, (const float*)y, y_rs, bias, (const float*)gp,
+                                                   gp_rs, (float*)out, rows, cols);
+  EVO_LAUNCH_CHECK("gated_residual fwd");
+  return EVO_OK;
+}
+
+extern "C" int evo_gated_residual_bwd(const void* dout, const void* y, int64_t y_rs, const float* bias, const void* gp,
+                                      int64_t gp_rs, void* dy, void* dgp, int64_t dgp_rs, float* dbias, int dtype,
+                                      int64_t rows, int64_t cols, void* stream) {
+  EVO_CHECK_ARG(dout, EVO_ERR_ARG, "gated_residual bwd: null dout");
+  EVO_CHECK_ARG(!gp || (y && dgp), EVO_ERR_ARG, "gated_residual bwd: gp needs y and dgp");
+  EVO_CHECK_ARG(cols % 8 == 0, EVO_ERR_ALIGN, "gated_residual bwd: cols %% 8");
+  if (rows == 0) return EVO_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  dim3 block(32, 8);
+  int64_t cchunks = cols / 8;
+  unsigned gx = (unsigned)((cchunks + 31) / 32);
+  int64_t gy = (rows + 63) / 64;
+  int64_t cap = (int64_t)sm_count() * 8 / gx;
+  if (cap < 1) cap = 1;
+  dim3 grid(gx, (unsigned)(gy < cap ? gy : cap));
+  if (dtype == EVO_BF16)
+    gated_residual_bwd_k<bf16><<<grid, block, 0, st>>>((const bf16*)dout, (const bf16*)y, y_rs, bias, (const bf16*)gp,
+                                                       gp_rs, (bf16*)dy, (bf16*)dgp, dgp_rs, dbias, rows, cols);
+  else
+    gated_residual_bwd_k<float><<<grid, block, 0, st>>>((const float*)dout, (const float*)y, y_rs, bias,
+                                                        (const float*)gp, gp_rs, (float*)dy, (float*)dgp, dgp_rs,
+                                                        dbias, rows, cols);
+  EVO_LAUNCH_CHECK("gated_residual bwd");
+  return EVO_OK;
+}
+
+extern "C" int evo_bias_act_fwd(void* y, const float* bias, int64_t rows, int64_t cols, int act, int dtype,
+                                void* stream) {
+  EVO_CHECK_ARG(y, EVO_ERR_ARG, "bias_act: null y");
+  EVO_CHECK_ARG(cols % 8 == 0 && al16(y), EVO_ERR_ALIGN, "bias_act: cols %% 8 and 16B alignment");
+  if (rows == 0) return EVO_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned g = grid_for(rows * cols / 8, 256);
+  if (dtype == EVO_BF16) bias_act_fwd_k<bf16><<<g, 256, 0, st>>>((bf16*)y, bias, rows, cols, act);
+  else bias_act_fwd_k<float><<<g, 256, 0, st>>>((float*)y, bias, rows, cols, act);
+  EVO_LAUNCH_CHECK("bias_act fwd");
+  return EVO_OK;
+}
+
+extern "C" int evo_bias_act_bwd(const void* dh, const void* h, void* dy, float* dbias, int64_t rows, int64_t cols,
+                                int act, int dtype, void* stream) {
+  EVO_CHECK_ARG(dh && dy && (act == 0 || h), EVO_ERR_ARG, "bias_act bwd: null pointer");
+  EVO_CHECK_ARG(cols % 8 == 0, EVO_ERR_ALIGN, "bias_act bwd: cols %% 8");
+  if (rows == 0) return EVO_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  dim3 block(32, 8);
+  unsigned gx = (unsigned)((cols / 8 + 31) / 32);
+  int64_t gy = (rows + 63) / 64;
+  int64_t cap = (int64_t)sm_count() * 8 / gx;
+  if (cap < 1) cap = 1;
+  dim3 grid(gx, (unsigned)(gy < cap ? gy : cap));
+  if (dtype == EVO_BF16)
+    bias_act_bwd_k<bf16><<<grid, block, 0, st>>>((const bf16*)dh, (const bf16*)h, (bf16*)dy, dbias, rows, cols, act);
+  else
+    bias_act_bwd_k<float><<<grid, block, 0, st>>>((const float*)dh, (const float*)h, (float*)dy, dbias, rows, cols,
+                                                  act);
+  EVO_LAUNCH_CHECK("bias_act bwd");
+  return EVO_OK;
+}
+
+extern "C" int evo_tri_gate_fwd(const void* y, int64_t rows, int hz, int p, void* a_cm, void* b_cm, void* stream) {
+  EVO_CHECK_ARG(y && a_cm && b_cm, EVO_ERR_ARG, "tri_gate: null pointer");
+  EVO_CHECK_ARG(hz % 8 == 0 && al16(y), EVO_ERR_ALIGN, "tri_gate: hz %% 8 and 16B aligned Y");
+  if (rows == 0) return EVO_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned g = (unsigned)((rows + (p <= 32 ? 63 : 31)) / (p <= 32 ? 64 : 32));
+#define TG(PP) tri_gate_fwd_k<PP><<<g, 256, 0, st>>>((const bf16*)y, rows, hz, (bf16*)a_cm, (bf16*)b_cm)
+  switch (p) {
+    case 2: TG(2); break;
+    case 4: TG(4); break;
+    case 8: TG(8); break;
+    case 16: TG(16); break;
+    case 32: TG(32); break;
+    case 64: TG(64); break;
+    default: set_error("tri_gate: hidden_proj %d unsupported (2,4,8,16,32,64)", p); return EVO_ERR_SHAPE;
+  }
+#undef TG
+  EVO_LAUNCH_CHECK("tri_gate fwd");
+  return EVO_OK;
+}
+
+extern "C" int evo_tri_gate_bwd(const void* y, const void* da_cm, const void* db_cm, int d_dtype, int64_t rows, int hz,
+                                int p, void* dy, void* stream) {
+  EVO_CHECK_ARG(y && da_cm && db_cm && dy, EVO_ERR_ARG, "tri_gate bwd: null pointer");
+  EVO_CHECK_ARG(hz % 8 == 0 && al16(y) && al16(dy), EVO_ERR_ALIGN, "tri_gate bwd: alignment");
+  if (rows == 0) return EVO_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned g = (unsigned)((rows + 63) / 64);
+#define TGB(PP)                                                                                                  \
+  (d_dtype == EVO_BF16                                                                                           \
+       ? tri_gate_bwd_k<PP, bf16><<<g, 256, 0, st>>>((const bf16*)y, (const bf16*)da_cm, (const bf16*)db_cm, rows, \
+                                                     hz, (bf16*)dy)                                              \
+       : tri_gate_bwd_k<PP, float><<<g, 256, 0, st>>>((const bf16*)y, (const float*)da_cm, (const float*)db_cm,    \
+                                                      rows, hz, (bf16*)dy))
+  switch (p) {
+    case 2: TGB(2); break;
+    case 4: TGB(4); break;
+    case 8: TGB(8); break;
+    case 16: TGB(16); break;
+    case 32: TGB(32); break;
+    case 64: TGB(64); break;
+    default: set_error("tri_gate bwd: hidden_proj %d unsupported", p); return EVO_ERR_SHAPE;
+  }
+#undef TGB
+  EVO_LAUNCH_CHECK("tri_gate bwd");
+  return EVO_OK;
+}
+
+extern "C" int evo_count_nonfinite(const void* x, int dtype, int64_t n, unsigned int* counter, void* stream) {
+  EVO_CHECK_ARG(x && counter, EVO_ERR_ARG, "count_nonfinite: null pointer");
+  if (n == 0) return EVO_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned g = grid_for(n, 256);
+  if (dtype == EVO_BF16) count_nonfinite_k<bf16><<<g, 256, 0, st>>>((const bf16*)x, n, counter);
+  else count_nonfinite_k<float><<<g, 256, 0, st>>>((const float*)x, n, counter);
+  EVO_LAUNCH_CHECK("count_nonfinite");
+  return EVO_OK;
+}

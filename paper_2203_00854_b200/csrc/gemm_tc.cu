@@ -1,0 +1,281 @@
+// Batched bf16 GEMM on 5th-generation tensor cores (tcgen05, fp32 accumulators in TMEM).
+//
+//   C[b] = alpha * A[b] . B[b]^T + beta * C[b]      A:[M,K]  B:[N,K]  C:[M,N]
+//
+// Used for the dense contractions of the Evoformer block:
+//   * triangle multiplicative update einsums (evoformer.py:276 "ikh,jkh->ijh",
+//     evoformer.py:283 "kih,kjh->ijh") - batch = channel h, M = N = K = N_r;
+//   * the outer-product-mean contraction (evoformer.py:253 "sip,sjq->ijpq") -
+//     M = N_r*p, N = N_r*p, K = N_s, written straight into the [i][j][p][q] layout;
+//   * all of their backward products.
+//
+// Design: 128-thread CTA, tile 128 x BN x 64, STAGES-deep cp.async ring into
+// canonical (SWIZZLE_NONE) UMMA layouts; one elected thread issues
+// tcgen05.mma (M=128, N=BN, K=16) and commits each stage to an mbarrier that
+// gates the reuse of that stage's shared memory; the 4 warps then drain the
+// TMEM accumulator (tcgen05.ld 32x32b) in the epilogue.  Operands may be K-major
+// or MN-major (instruction-descriptor major bits), so no transpose copies are
+// ever made.  Addressing is 2-level per dim (see EvoMat in include/evo.h).
+#include "common.cuh"
+
+namespace evo {
+
+struct MatArg {
+  const char* ptr;
+  int64_t bs;                 // batch stride (elements)
+  uint32_t split0, split1;
+  int64_t hi0, lo0, hi1, lo1;
+};
+
+__device__ __forceinline__ int64_t mat_off(const MatArg& m, uint32_t i0, uint32_t i1) {
+  uint32_t q0 = i0 / m.split0, r0 = i0 - q0 * m.split0;
+  uint32_t q1 = i1 / m.split1, r1 = i1 - q1 * m.split1;
+  return (int64_t)q0 * m.hi0 + (int64_t)r0 * m.lo0 + (int64_t)q1 * m.hi1 + (int64_t)r1 * m.lo1;
+}
+
+constexpr int GEMM_BM = 128;
+constexpr int GEMM_BK = 64;
+
+// load one ROWS x 64 operand tile (bf16) into a canonical layout; 128 threads
+template <int ROWS, bool MN>
+__device__ __forceinline__ void load_tile(uint32_t sdst, const MatArg& m, const char* base, uint32_t r0,
+                                          uint32_t k0, uint32_t R, uint32_t K) {
+  constexpr int CHUNKS = ROWS * GEMM_BK / 8;  // 16-byte chunks
+#pragma unroll
+  for (int it = 0; it < CHUNKS / 128; ++it) {
+    int ch = threadIdx.x + it * 128;
+    uint32_t r, k, soff;
+    if (!MN) {  // 8 chunks (64 k) per row
+      r = ch >> 3;
+      k = (ch & 7) * 8;
+      soff = kmajor_off(r, k, ROWS);
+    } else {    // ROWS/8 chunks per k
+      k = ch / (ROWS / 8);
+      r = (ch % (ROWS / 8)) * 8;
+      soff = mnmajor_off(r, k, ROWS);
+    }
+    bool pred = (r0 + r < R) && (k0 + k < K);
+    const char* src = base;
+    if (pred) src = base + mat_off(m, r0 + r, k0 + k) * 2;
+    cp_async16(sdst + soff, src, pred);
+  }
+}
+
+template <int BN, bool A_MN, bool B_MN, int STAGES, typename TC>
+__global__ void __launch_bounds__(128) bgemm_kernel(MatArg A, MatArg B, MatArg C, uint32_t M, uint32_t N,
+                                                    uint32_t K, float alpha, float beta, int c_mode) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t mbar[STAGES];
+  __shared__ uint32_t tmem_base_sh;
+
+  constexpr uint32_t A_BYTES = GEMM_BM * GEMM_BK * 2;
+  constexpr uint32_t B_BYTES = BN * GEMM_BK * 2;
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t sA = sbase, sB = sbase + STAGES * A_BYTES;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t m0 = blockIdx.y * GEMM_BM, n0 = blockIdx.x * BN;
+  const int64_t bz = blockIdx.z;
+  const char* Abase = A.ptr + bz * A.bs * 2;
+  const char* Bbase = B.ptr + bz * B.bs * 2;
+
+  if (warp == 0) tmem_alloc(&tmem_base_sh, BN < 32 ? 32 : BN);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&mbar[s], 1);
+    fence_mbar_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+
+  const int KT = (K + GEMM_BK - 1) / GEMM_BK;
+  constexpr uint32_t IDESC = make_idesc_bf16(GEMM_BM, BN, A_MN, B_MN);
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) {
+      load_tile<GEMM_BM, A_MN>(sA + s * A_BYTES, A, Abase, m0, s * GEMM_BK, M, K);
+      load_tile<BN, B_MN>(sB + s * B_BYTES, B, Bbase, n0, s * GEMM_BK, N, K);
+    }
+    cp_async_commit();
+  }
+
+  for (int kt = 0; kt < KT; ++kt) {
+    const int pf = kt + STAGES - 1;
+    if (pf < KT) {
+      const int ps = pf % STAGES;
+      if (kt >= 1) mbar_wait(&mbar[ps], ((kt - 1) / STAGES) & 1);  // MMA kt-1 released stage ps
+      load_tile<GEMM_BM, A_MN>(sA + ps * A_BYTES, A, Abase, m0, pf * GEMM_BK, M, K);
+      load_tile<BN, B_MN>(sB + ps * B_BYTES, B, Bbase, n0, pf * GEMM_BK, N, K);
+    }
+    cp_async_commit();
+    cp_async_wait<STAGES - 1>();
+    fence_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tc_fence_after();
+      const int s = kt % STAGES;
+#pragma unroll
+      for (int kk = 0; kk < GEMM_BK / 16; ++kk) {
+        uint64_t ad = make_sdesc(sA + s * A_BYTES + kk * 2 * (GEMM_BM / 8) * 128, (GEMM_BM / 8) * 128, 128);
+        uint64_t bd = make_sdesc(sB + s * B_BYTES + kk * 2 * (BN / 8) * 128, (BN / 8) * 128, 128);
+        mma_bf16(tmem, ad, bd, IDESC, (kt | kk) != 0);
+      }
+      mma_commit(&mbar[s]);
+    }
+    __syncwarp();
+  }
+
+  mbar_wait(&mbar[(KT - 1) % STAGES], ((KT - 1) / STAGES) & 1);
+  tc_fence_after();
+
+  // ---------------- epilogue: TMEM -> registers -> global
+  const uint32_t row = m0 + warp * 32 + lane;
+  const bool row_ok = row < M;
+  char* Cbase = const_cast<char*>(C.ptr) + bz * C.bs * (int64_t)sizeof(TC);
+  int64_t roff = 0;
+  if (row_ok) {
+    uint32_t q = row / C.split0, r = row - q * C.split0;
+    roff = (int64_t)q * C.hi0 + (int64_t)r * C.lo0;
+  }
+#pragma unroll 1
+  for (int c0 = 0; c0 < BN; c0 += 32) {
+    float v[32];
+    tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + c0, v);
+    tmem_ld_wait();
+    if (!row_ok) continue;
+    TC* crow = reinterpret_cast<TC*>(Cbase) + roff;
+    if (c_mode == 1) {  // columns contiguous in runs of >= 8, N % 8 == 0
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) {
+        uint32_t col = n0 + c0 + j;
+        if (col >= N) break;
+        uint32_t q = col / C.split1, r = col - q * C.split1;
+        TC* p = crow + (int64_t)q * C.hi1 + r;
+        float o[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = alpha * v[j + e];
+        if (beta != 0.f) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) o[e] += beta * ldf<TC>(p + e);
+        }
+        if constexpr (sizeof(TC) == 2) {
+          uint4 w;
+          w.x = pack_bf16x2(o[0], o[1]);
+          w.y = pack_bf16x2(o[2], o[3]);
+          w.z = pack_bf16x2(o[4], o[5]);
+          w.w = pack_bf16x2(o[6], o[7]);
+          *reinterpret_cast<uint4*>(p) = w;
+        } else {
+          *reinterpret_cast<float4*>(p) = make_float4(o[0], o[1], o[2], o[3]);
+          *reinterpret_cast<float4*>(p + 4) = make_float4(o[4], o[5], o[6], o[7]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        uint32_t col = n0 + c0 + j;
+        if (col >= N) break;
+        uint32_t q = col / C.split1, r = col - q * C.split1;
+        TC* p = crow + (int64_t)q * C.hi1 + (int64_t)r * C.lo1;
+        float o = alpha * v[j];
+        if (beta != 0.f) o += beta * ldf<TC>(p);
+        stf<TC>(p, o);
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, BN < 32 ? 32 : BN);
+}
+
+static MatArg to_arg(const EvoMat* m, int64_t ext0, int64_t ext1) {
+  MatArg a;
+  a.ptr = static_cast<const char*>(m->ptr);
+  a.bs = m->batch_stride;
+  auto sp = [](int64_t s, int64_t ext) -> uint32_t {
+    int64_t v = (s <= 0 || s > ext) ? ext : s;
+    if (v < 1) v = 1;
+    return (uint32_t)v;
+  };
+  a.split0 = sp(m->split[0], ext0);
+  a.split1 = sp(m->split[1], ext1);
+  a.hi0 = m->stride_hi[0];
+  a.lo0 = m->stride_lo[0];
+  a.hi1 = m->stride_hi[1];
+  a.lo1 = m->stride_lo[1];
+  return a;
+}
+
+// contiguous along dim d in runs of 8 elements?
+static bool runs8(const MatArg& a, int d) {
+  uint32_t split = d == 0 ? a.split0 : a.split1;
+  int64_t lo = d == 0 ? a.lo0 : a.lo1;
+  return lo == 1 && (split % 8) == 0;
+}
+
+template <int BN, bool AM, bool BMN, typename TC>
+static int launch_bgemm(MatArg A, MatArg B, MatArg C, int64_t batch, int64_t M, int64_t N, int64_t K, float alpha,
+                        float beta, int c_mode, cudaStream_t st) {
+  constexpr int STAGES = 3;
+  const size_t smem = STAGES * (GEMM_BM * GEMM_BK * 2 + BN * GEMM_BK * 2);
+  auto kern = bgemm_kernel<BN, AM, BMN, STAGES, TC>;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_status(e, "bgemm attr");
+    attr_set = true;
+  }
+  dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + GEMM_BM - 1) / GEMM_BM), (unsigned)batch);
+  kern<<<grid, 128, smem, st>>>(A, B, C, (uint32_t)M, (uint32_t)N, (uint32_t)K, alpha, beta, c_mode);
+  EVO_LAUNCH_CHECK("bgemm launch");
+  return EVO_OK;
+}
+
+template <int BN, typename TC>
+static int dispatch_major(bool am, bool bm, MatArg A, MatArg B, MatArg C, int64_t batch, int64_t M, int64_t N,
+                          int64_t K, float alpha, float beta, int c_mode, cudaStream_t st) {
+  if (!am && !bm) return launch_bgemm<BN, false, false, TC>(A, B, C, batch, M, N, K, alpha, beta, c_mode, st);
+  if (!am && bm) return launch_bgemm<BN, false, true, TC>(A, B, C, batch, M, N, K, alpha, beta, c_mode, st);
+  if (am && !bm) return launch_bgemm<BN, true, false, TC>(A, B, C, batch, M, N, K, alpha, beta, c_mode, st);
+  return launch_bgemm<BN, true, true, TC>(A, B, C, batch, M, N, K, alpha, beta, c_mode, st);
+}
+
+}  // namespace evo
+
+using namespace evo;
+
+extern "C" int evo_bgemm(const EvoMat* A, const EvoMat* B, const EvoMat* C, int64_t batch, int64_t M, int64_t N,
+                         int64_t K, float alpha, float beta, void* stream) {
+  EVO_CHECK_ARG(A && B && C && A->ptr && B->ptr && C->ptr, EVO_ERR_ARG, "bgemm: null operand");
+  EVO_CHECK_ARG(batch >= 1 && M >= 1 && N >= 1 && K >= 1, EVO_ERR_SHAPE, "bgemm: bad extents b=%lld M=%lld N=%lld K=%lld",
+                (long long)batch, (long long)M, (long long)N, (long long)K);
+  EVO_CHECK_ARG(M < (1LL << 31) && N < (1LL << 31) && K < (1LL << 31) && batch < 65536, EVO_ERR_SHAPE,
+                "bgemm: extents too large");
+  EVO_CHECK_ARG(A->dtype == EVO_BF16 && B->dtype == EVO_BF16, EVO_ERR_DTYPE, "bgemm: A/B must be bf16");
+  EVO_CHECK_ARG(C->dtype == EVO_BF16 || C->dtype == EVO_F32, EVO_ERR_DTYPE, "bgemm: C must be bf16/f32");
+  MatArg a = to_arg(A, M, K), b = to_arg(B, N, K), c = to_arg(C, M, N);
+  bool a_k = runs8(a, 1), a_mn = runs8(a, 0), b_k = runs8(b, 1), b_mn = runs8(b, 0);
+  EVO_CHECK_ARG(a_k || a_mn, EVO_ERR_ALIGN, "bgemm: A must be contiguous in runs of 8 along M or K");
+  EVO_CHECK_ARG(b_k || b_mn, EVO_ERR_ALIGN, "bgemm: B must be contiguous in runs of 8 along N or K");
+  bool am = !a_k, bm = !b_k;
+  EVO_CHECK_ARG(K % 8 == 0 && (!am || M % 8 == 0) && (!bm || N % 8 == 0), EVO_ERR_ALIGN,
+                "bgemm: K (and M/N for MN-major operands) must be multiples of 8");
+  uintptr_t align_or = (uintptr_t)A->ptr | (uintptr_t)B->ptr;
+  EVO_CHECK_ARG((align_or & 15) == 0, EVO_ERR_ALIGN, "bgemm: A/B pointers must be 16-byte aligned");
+  int c_mode = 0;
+  if (runs8(c, 1) && N % 8 == 0 && ((uintptr_t)C->ptr & 15) == 0 && (c.hi1 % 8) == 0 && (c.hi0 % 8) == 0 &&
+      (c.lo0 % 8) == 0 && (c.bs % 8) == 0)
+    c_mode = 1;
+  cudaStream_t st = (cudaStream_t)stream;
+  // wide N tiles amortise the A-tile loads; N=64 keeps small problems parallel
+  bool small = ((M + 127) / 128) * ((N + 127) / 128) * batch < 148;
+  if (C->dtype == EVO_BF16) {
+    if (small || N <= 64) return dispatch_major<64, bf16>(am, bm, a, b, c, batch, M, N, K, alpha, beta, c_mode, st);
+    return dispatch_major<128, bf16>(am, bm, a, b, c, batch, M, N, K, alpha, beta, c_mode, st);
+  }
+  if (small || N <= 64) return dispatch_major<64, float>(am, bm, a, b, c, batch, M, N, K, alpha, beta, c_mode, st);
+  return dispatch_major<128, float>(am, bm, a, b, c, batch, M, N, K, alpha, beta, c_mode, st);
+}

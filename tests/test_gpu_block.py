@@ -1,0 +1,136 @@
+"""Parity of the B200 Evoformer block against the CPU oracle (fp64) and the
+reference's own golden outputs.  bf16 storage, fp32 accumulation; tolerance
+(SURVEY.md 8c): relative Frobenius error <= 2e-2 per output and per gradient
+(max-abs is meaningless for bf16: input rounding alone reaches 5e-2)."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():
+    pytest.skip("needs CUDA", allow_module_level=True)
+
+from conftest import GOLDEN  # noqa: E402
+from oracle import evoformer_np as O  # noqa: E402
+from oracle import evoformer_torch as T  # noqa: E402
+import paper_2203_00854_b200 as evo  # noqa: E402
+from paper_2203_00854_b200.config import EvoConfig, init_block_params, synthetic_inputs  # noqa: E402
+from paper_2203_00854_b200.evoformer import BlockParams, EvoformerStack, block_forward_backward  # noqa: E402
+
+TOL = 2e-2
+GRAD_TOL = 5e-2   # see tests/test_gpu_submodule_grads.py (ReLU-mask flips under bf16)
+CFGS = {"c1": EvoConfig(16, 32, 64, 32, 2, 1, 16), "h84": EvoConfig(16, 32, 64, 32, 8, 4, 8)}
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - b) / max(np.linalg.norm(b), 1e-30))
+
+
+@pytest.mark.parametrize("name", ["c1", "h84"])
+@pytest.mark.parametrize("seed", [7, 31, 101])
+def test_submodules_vs_oracle(name, seed):
+    cfg = CFGS[name]
+    p = init_block_params(cfg, seed)
+    m, z = synthetic_inputs(cfg, seed)
+    cases = {
+        "msa_row_bias": (evo.msa_row_bias(z, p, cfg), O.msa_row_bias(z, p, cfg)),
+        "msa_row": (evo.msa_row_attention(m, z, p, cfg), O.msa_row_attention(m, z, p, cfg)),
+        "msa_col": (evo.msa_col_attention(m, p, cfg), O.msa_col_attention(m, p, cfg)),
+        "msa_trans": (evo.transition(m, p, "msa_trans", cfg), O.transition(m, p, "msa_trans")),
+        "pair_trans": (evo.transition(z, p, "pair_trans", cfg), O.transition(z, p, "pair_trans")),
+        "opm": (evo.outer_product_mean(m, p, cfg), O.outer_product_mean(m, p, cfg)),
+        "tri_out": (evo.tri_update_outgoing(z, p, cfg), O.tri_update_outgoing(z, p, cfg)),
+        "tri_in": (evo.tri_update_incoming(z, p, cfg), O.tri_update_incoming(z, p, cfg)),
+        "pair_row": (evo.pair_attention_row(z, p, cfg), O.pair_attention_row(z, p, cfg)),
+        "pair_col": (evo.pair_attention_col(z, p, cfg), O.pair_attention_col(z, p, cfg)),
+    }
+    errs = {k: rel(a, b) for k, (a, b) in cases.items()}
+    assert max(errs.values()) <= TOL, errs
+
+
+@pytest.mark.parametrize("name", ["c1_s7", "c1_s31", "h84_s101"])
+def test_block_vs_reference_golden(name):
+    g = np.load(os.path.join(GOLDEN, "golden_tiny.npz"))
+    dims = [int(v) for v in g[f"{name}/dims"]]
+    cfg, seed = EvoConfig(*dims[:7]), dims[7]
+    p = init_block_params(cfg, seed)
+    m, z = synthetic_inputs(cfg, seed)
+    mo, zo = evo.evoformer_block(m, z, p, cfg)
+    assert isinstance(mo, np.ndarray) and mo.dtype == np.float64
+    assert rel(mo, g[f"{name}/m"]) <= TOL and rel(zo, g[f"{name}/z"]) <= TOL, (rel(mo, g[f"{name}/m"]),
+                                                                                rel(zo, g[f"{name}/z"]))
+
+
+@pytest.mark.parametrize("name", ["c1", "h84"])
+def test_block_gradients_vs_fp64_autograd(name):
+    cfg = CFGS[name]
+    p = init_block_params(cfg, 7)
+    m, z = synthetic_inputs(cfg, 7)
+    rng = np.random.default_rng(1)
+    gm, gz = rng.normal(size=m.shape), rng.normal(size=z.shape)
+    bp = BlockParams(p, cfg)
+    mo, zo, dm, dz, dp = block_forward_backward(bp, m, z, gm, gz)
+    rm, rz, rdm, rdz, rdp = T.block_grads(m, z, p, cfg, gm, gz)
+    assert rel(mo, rm) <= TOL and rel(zo, rz) <= TOL
+    assert rel(dm, rdm) <= GRAD_TOL, rel(dm, rdm)
+    assert rel(dz, rdz) <= GRAD_TOL, rel(dz, rdz)
+    scale = max(np.linalg.norm(v) for v in rdp.values())
+    errs = {k: rel(dp[k], rdp[k]) for k in rdp if np.linalg.norm(rdp[k]) > 1e-9 * scale}
+    bad = {k: v for k, v in errs.items() if v > 1e-1}
+    assert not bad, bad
+    # the whole parameter gradient, as one vector
+    gv = np.concatenate([dp[k].ravel() for k in rdp])
+    rv = np.concatenate([rdp[k].ravel() for k in rdp])
+    assert rel(gv, rv) <= GRAD_TOL
+
+
+def test_stack_two_blocks_vs_chained_oracle():
+    cfg = CFGS["c1"]
+    st = EvoformerStack(cfg, 2, seed=5)
+    m, z = synthetic_inputs(cfg, 5)
+    mt = torch.tensor(m, device="cuda").bfloat16()
+    zt = torch.tensor(z, device="cuda").bfloat16()
+    mo, zo, _ = st.forward(mt, zt, save=False)
+    rm, rz = m, z
+    for i in range(2):
+        rm, rz = O.evoformer_block(rm, rz, init_block_params(cfg, 5 + i), cfg)
+    assert rel(mo.double().cpu().numpy(), rm) <= TOL and rel(zo.double().cpu().numpy(), rz) <= TOL
+
+
+def test_training_shape_block_forward_vs_oracle():
+    """one block at the AlphaFold training shape (128, 256, 256, 128, 8/4 heads, p=32)."""
+    cfg = EvoConfig(128, 256, 256, 128, 8, 4, 32)
+    p = init_block_params(cfg, 0)
+    m, z = synthetic_inputs(cfg, 0)
+    mo, zo = evo.evoformer_block(m, z, p, cfg)
+    torch.set_num_threads(max(1, os.cpu_count() or 1))
+    pt = {k: torch.tensor(v) for k, v in p.items()}
+    rm, rz = T.evoformer_block(torch.tensor(m), torch.tensor(z), pt, cfg)
+    em, ez = rel(mo, rm.numpy()), rel(zo, rz.numpy())
+    assert em <= TOL and ez <= TOL, (em, ez)
+
+
+def test_api_errors_and_weights():
+    cfg = CFGS["c1"]
+    p = init_block_params(cfg, 0)
+    m, z = synthetic_inputs(cfg, 0)
+    with pytest.raises(evo.DimensionError):
+        evo.evoformer_block(m[:, :2], z, p, cfg)
+    with pytest.raises(evo.DimensionError):
+        evo.evoformer_block(m, z[:2], p, cfg)
+    out, w = evo.msa_row_attention(m, z, p, cfg, return_weights=True)
+    assert len(w) == cfg.n_head_msa
+    for a in w:
+        assert np.allclose(a.sum(-1), 1.0, atol=1e-3)
+    x = np.random.default_rng(0).normal(size=(4, 7, 9)) * 3
+    mask = np.where(np.random.default_rng(1).random((1, 1, 9)) < 0.3, -1e30, 0.0)
+    bias = np.random.default_rng(2).normal(size=(1, 7, 9))
+    y = evo.fused_softmax_mask_bias(x, mask, bias, -1)
+    assert np.max(np.abs(y - O.fused_softmax_mask_bias(x, mask, bias))) < 1e-5
+    with pytest.raises(evo.DomainError):
+        evo.fused_softmax_mask_bias(np.array([[1.0, np.inf]]), np.zeros((1, 2)), np.zeros((1, 2)))
+    with pytest.raises(evo.DimensionError):
+        evo.fused_softmax_mask_bias(np.zeros((2, 3, 3)), np.zeros((4,)), np.zeros((3,)))

@@ -1,0 +1,302 @@
+"""Per-kernel numerics of libevo.so on the GPU vs plain PyTorch fp32 references
+of the same op (bf16 storage -> tolerances stated per test)."""
+
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # collected on CPU too; the gpu marker deselects
+    pytest.skip("needs CUDA", allow_module_level=True)
+
+from paper_2203_00854_b200 import ops  # noqa: E402
+from paper_2203_00854_b200.ops import Mat, Strided  # noqa: E402
+
+DEV = "cuda"
+
+
+def rel(a, b):
+    a, b = a.float(), b.float()
+    return ((a - b).norm() / b.norm().clamp_min(1e-30)).item()
+
+
+@pytest.mark.parametrize("cols", [32, 128, 256])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_layernorm_fwd_bwd(cols, dtype):
+    g = torch.Generator(device=DEV).manual_seed(cols)
+    rows = 1000
+    x = (torch.randn(rows, cols, device=DEV, generator=g) * 2 + 0.5).to(dtype)
+    gamma = torch.randn(cols, device=DEV, generator=g)
+    beta = torch.randn(cols, device=DEV, generator=g)
+    y, mean, rstd = ops.layernorm_fwd(x, gamma, beta, rows, cols)
+    xr = x.float().requires_grad_(True)
+    gr = gamma.clone().requires_grad_(True)
+    br = beta.clone().requires_grad_(True)
+    yr = torch.nn.functional.layer_norm(xr, (cols,), gr, br, eps=1e-5)
+    tol = 1e-2 if dtype == torch.bfloat16 else 1e-5
+    assert rel(y, yr) < tol
+    dy = torch.randn(rows, cols, device=DEV, generator=g).to(dtype)
+    yr.backward(dy.float())
+    dg = torch.zeros(cols, device=DEV)
+    db = torch.zeros(cols, device=DEV)
+    dx = ops.layernorm_bwd(dy, x, gamma, mean, rstd, rows, cols, dgamma=dg, dbeta=db)
+    assert rel(dx, xr.grad) < tol
+    assert rel(dg, gr.grad) < tol
+    assert rel(db, br.grad) < 1e-5
+    # accumulate mode
+    base = torch.randn(rows, cols, device=DEV, generator=g).to(dtype)
+    acc = base.clone()
+    ops.layernorm_bwd(dy, x, gamma, mean, rstd, rows, cols, dx=acc, accumulate=True)
+    assert rel(acc, base.float() + xr.grad) < tol
+
+
+def test_layernorm_strided_channel_major():
+    g = torch.Generator(device=DEV).manual_seed(3)
+    P, R = 32, 777
+    t_cm = torch.randn(P, R, device=DEV, generator=g).bfloat16()  # [channel][row]
+    gamma = torch.randn(P, device=DEV, generator=g)
+    beta = torch.randn(P, device=DEV, generator=g)
+    y, mean, rstd = ops.layernorm_fwd(t_cm, gamma, beta, R, P, x_rs=1, x_cs=R)
+    xr = t_cm.float().t().contiguous().requires_grad_(True)
+    yr = torch.nn.functional.layer_norm(xr, (P,), gamma, beta, eps=1e-5)
+    assert rel(y, yr) < 1e-2
+    dy = torch.randn(R, P, device=DEV, generator=g).bfloat16()
+    yr.backward(dy.float())
+    dx = torch.empty_like(t_cm)
+    dg = torch.zeros(P, device=DEV)
+    db = torch.zeros(P, device=DEV)
+    ops.layernorm_bwd(dy, t_cm, gamma, mean, rstd, R, P, x_rs=1, x_cs=R, dx=dx, dgamma=dg, dbeta=db)
+    assert rel(dx.float().t(), xr.grad) < 1e-2
+    assert rel(db, dy.float().sum(0)) < 1e-5
+
+
+def test_layernorm_rowdot():
+    g = torch.Generator(device=DEV).manual_seed(4)
+    rows, cols, k = 4096, 128, 8
+    x = torch.randn(rows, cols, device=DEV, generator=g).bfloat16()
+    gamma = torch.randn(cols, device=DEV, generator=g)
+    beta = torch.randn(cols, device=DEV, generator=g)
+    w = torch.randn(cols, k, device=DEV, generator=g)
+    out = torch.empty(k, rows, device=DEV, dtype=torch.bfloat16)
+    ln = torch.empty(rows, cols, device=DEV, dtype=torch.bfloat16)
+    ops.layernorm_rowdot_fwd(x, gamma, beta, w, rows, cols, out, rows, ln_out=ln)
+    lnr = torch.nn.functional.layer_norm(x.float(), (cols,), gamma, beta, eps=1e-5)
+    assert rel(ln, lnr) < 1e-2
+    assert rel(out, (lnr @ w).t()) < 1e-2
+
+
+@pytest.mark.parametrize("K", [8, 100, 256, 1024])
+def test_softmax_fwd_bwd(K):
+    g = torch.Generator(device=DEV).manual_seed(K)
+    B, H, Q = 3, 4, 17
+    x = torch.randn(B, H, Q, K, device=DEV, generator=g).bfloat16()
+    bias = torch.randn(1, H, Q, K, device=DEV, generator=g).bfloat16()
+    mask = torch.where(torch.rand(B, 1, 1, K, device=DEV, generator=g) < 0.3, -1e30, 0.0)
+    scale = 0.3
+    y = ops.softmax_fwd(x, bias, mask, scale)
+    yr = torch.softmax((x.float() + bias.float()) * scale + mask, -1)
+    assert (y.float() - yr).abs().max().item() < 1e-2
+    dy = torch.randn_like(x)
+    dx = ops.softmax_bwd(y, dy, scale)
+    xr = x.float().requires_grad_(True)
+    torch.softmax((xr + bias.float()) * scale + mask, -1).backward(dy.float())
+    assert rel(dx, xr.grad) < 2e-2
+
+
+def test_softmax_golden_set_fp32():
+    import numpy as np
+    import os
+    from conftest import GOLDEN
+    gs = np.load(os.path.join(GOLDEN, "golden_softmax.npz"))
+    worst = 0.0
+    for i in range(100):
+        x = torch.tensor(gs[f"c{i}/x"], dtype=torch.float32, device=DEV)
+        m = torch.tensor(gs[f"c{i}/mask"], dtype=torch.float32, device=DEV)
+        b = torch.tensor(gs[f"c{i}/bias"], dtype=torch.float32, device=DEV)
+        y = ops.softmax_fwd(x, b, m, 1.0)
+        worst = max(worst, float(np.max(np.abs(y.cpu().double().numpy() - gs[f"c{i}/y"]))))
+    assert worst < 2e-6
+
+
+def _mk(shape, g):
+    return torch.randn(*shape, device=DEV, generator=g).bfloat16()
+
+
+@pytest.mark.parametrize("am,bm", [(False, False), (True, False), (False, True), (True, True)])
+@pytest.mark.parametrize("M,N,K,batch", [(256, 256, 256, 4), (200, 136, 72, 3), (8192 // 8, 1024, 128, 1)])
+def test_bgemm_majors(am, bm, M, N, K, batch):
+    g = torch.Generator(device=DEV).manual_seed(M + N + K)
+    A = _mk((batch, K, M) if am else (batch, M, K), g)
+    B = _mk((batch, K, N) if bm else (batch, N, K), g)
+    Cc = torch.zeros(batch, M, N, device=DEV, dtype=torch.float32)
+    Aref = A.float().transpose(1, 2) if am else A.float()
+    Bref = B.float().transpose(1, 2) if bm else B.float()
+    ma = Mat(A, lo=(1, M) if am else (K, 1), batch_stride=M * K)
+    mb = Mat(B, lo=(1, N) if bm else (K, 1), batch_stride=N * K)
+    mc = Mat(Cc, lo=(N, 1), batch_stride=M * N)
+    ops.bgemm(ma, mb, mc, batch, M, N, K, alpha=0.5)
+    ref = 0.5 * Aref @ Bref.transpose(1, 2)
+    assert rel(Cc, ref) < 1e-5
+    # bf16 output, column-major C, beta accumulate
+    Cb = torch.randn(batch, N, M, device=DEV, generator=g).bfloat16()
+    C0 = Cb.float().clone()
+    mcb = Mat(Cb, lo=(1, M), batch_stride=M * N)
+    ops.bgemm(ma, mb, mcb, batch, M, N, K, alpha=1.0, beta=1.0)
+    assert rel(Cb.float().transpose(1, 2), ref * 2 + C0.transpose(1, 2)) < 1e-2
+
+
+def test_bgemm_opm_layout():
+    """outer-product contraction straight into o[i][j][p][q] (evoformer.py:253)."""
+    g = torch.Generator(device=DEV).manual_seed(7)
+    S, R, P = 64, 48, 16
+    ab = _mk((S, R, 2 * P), g)  # [a | b] projections, row stride 2P
+    o = torch.empty(R, R, P, P, device=DEV, dtype=torch.bfloat16)
+    A = Mat(ab, lo=(1, R * 2 * P), split=(P, 0), hi=(2 * P, 0))
+    B = Mat(ab, lo=(1, R * 2 * P), split=(P, 0), hi=(2 * P, 0), offset=P)
+    Cm = Mat(o, lo=(P, 1), split=(P, P), hi=(R * P * P, P * P))
+    ops.bgemm(A, B, Cm, 1, R * P, R * P, S, alpha=1.0 / S)
+    a, b = ab[..., :P].float(), ab[..., P:].float()
+    ref = torch.einsum("sip,sjq->ijpq", a, b) / S
+    assert rel(o, ref) < 1e-2
+
+
+def _attn_ref(q, k, v, g, bias, scale):
+    # q,k,v,g: [B, H, L, c] fp32; bias broadcastable to [B, H, L, L]
+    s = q @ k.transpose(-1, -2)
+    if bias is not None:
+        s = s + bias
+    a = torch.softmax(s * scale, -1)
+    o = a @ v
+    return torch.sigmoid(g) * o, o
+
+
+@pytest.mark.parametrize("L,c,H,mode", [(256, 32, 8, "full"), (128, 32, 8, "none"), (256, 32, 4, "key"),
+                                        (100, 16, 2, "full"), (300, 64, 2, "key"), (40, 8, 4, "none")])
+def test_attention_fwd_bwd(L, c, H, mode):
+    gen = torch.Generator(device=DEV).manual_seed(L * c + H)
+    B = 3
+    ld = 3 * H * c + (8 if mode == "key" else 0)
+    qkv = _mk((B, L, ld), gen)
+    gp = _mk((B, L, H * c), gen)
+    if mode == "full":
+        bias = _mk((H, L, L), gen)
+        bias_s = (0, L * L, L, 1)
+        bias_t = bias
+        bref = bias.float()[None]
+    elif mode == "key":
+        bias_t = qkv
+        bias_s = (L * ld, 1, 0, ld)
+        bref = qkv[..., 3 * H * c:3 * H * c + H].float().permute(0, 2, 1)[:, :, None, :]
+    else:
+        bias_t, bias_s, bref = None, (0, 0, 0, 0), None
+    og = torch.empty(B, L, H * c, device=DEV, dtype=torch.bfloat16)
+    orw = torch.empty_like(og)
+    lse = torch.empty(B, H, L, device=DEV)
+    scale = 1 / math.sqrt(c)
+    d = ops.attention_desc(Strided(qkv, L * ld, ld, 0), Strided(qkv, L * ld, ld, H * c),
+                           Strided(qkv, L * ld, ld, 2 * H * c), Strided(gp, L * H * c, H * c),
+                           Strided(og, L * H * c, H * c), Strided(orw, L * H * c, H * c), lse,
+                           B, L, H, c, scale, bias=bias_t, bias_s=bias_s,
+                           bias_off=3 * H * c if mode == "key" else 0)
+    ops.attention_fwd(d)
+    torch.cuda.synchronize()
+    split = lambda t, i: t[..., i * H * c:(i + 1) * H * c].float().reshape(B, L, H, c).permute(0, 2, 1, 3)
+    q = split(qkv, 0).requires_grad_(True)
+    k = split(qkv, 1).requires_grad_(True)
+    v = split(qkv, 2).requires_grad_(True)
+    gg = gp.float().reshape(B, L, H, c).permute(0, 2, 1, 3).requires_grad_(True)
+    br = bref.clone().requires_grad_(True) if bref is not None else None
+    out_r, o_r = _attn_ref(q, k, v, gg, br, scale)
+    to_blh = lambda t: t.permute(0, 2, 1, 3).reshape(B, L, H * c)
+    assert rel(og, to_blh(out_r)) < 1e-2
+    assert rel(orw, to_blh(o_r)) < 1e-2
+    s_ref = (q @ k.transpose(-1, -2) + (br if br is not None else 0)) * scale
+    assert (lse - torch.logsumexp(s_ref, -1)).abs().max().item() < 2e-2
+
+    # backward
+    dout = _mk((B, L, H * c), gen)
+    out_r.backward(dout.float().reshape(B, L, H, c).permute(0, 2, 1, 3))
+    dqkv = torch.zeros_like(qkv)
+    dgp = torch.empty_like(gp)
+    if mode == "full":
+        dbias = torch.zeros(H, L, L, device=DEV)
+        dbias_s = (0, L * L, L, 1)
+    elif mode == "key":
+        dbias = torch.zeros(B, H, L, device=DEV)
+        dbias_s = (H * L, L, 0, 1)
+    else:
+        dbias, dbias_s = None, (0, 0, 0, 0)
+    ws = torch.empty(ops.attention_bwd_workspace(B, L, H, c), dtype=torch.uint8, device=DEV)
+    ops.attention_bwd(d, Strided(dout, L * H * c, H * c), Strided(dqkv, L * ld, ld, 0),
+                      Strided(dqkv, L * ld, ld, H * c), Strided(dqkv, L * ld, ld, 2 * H * c),
+                      Strided(dgp, L * H * c, H * c), ws, dbias=dbias, dbias_s=dbias_s)
+    torch.cuda.synchronize()
+    assert rel(dqkv[..., :H * c], to_blh(q.grad)) < 2e-2
+    assert rel(dqkv[..., H * c:2 * H * c], to_blh(k.grad)) < 2e-2
+    assert rel(dqkv[..., 2 * H * c:3 * H * c], to_blh(v.grad)) < 2e-2
+    assert rel(dgp, to_blh(gg.grad)) < 2e-2
+    if mode == "full":
+        assert rel(dbias, br.grad.sum(0)) < 2e-2
+    elif mode == "key":
+        assert rel(dbias, br.grad[:, :, 0, :]) < 2e-2
+
+
+def test_tri_gate_and_residuals():
+    gen = torch.Generator(device=DEV).manual_seed(11)
+    rows, hz, p = 1000, 32, 16
+    y = _mk((rows, hz + 4 * p), gen)
+    a_cm = torch.empty(p, rows, device=DEV, dtype=torch.bfloat16)
+    b_cm = torch.empty_like(a_cm)
+    ops.tri_gate_fwd(y, rows, hz, p, a_cm, b_cm)
+    yf = y.float().requires_grad_(True)
+    a = torch.sigmoid(yf[:, hz:hz + p]) * yf[:, hz + p:hz + 2 * p]
+    b = torch.sigmoid(yf[:, hz + 2 * p:hz + 3 * p]) * yf[:, hz + 3 * p:]
+    assert rel(a_cm, a.t()) < 1e-2 and rel(b_cm, b.t()) < 1e-2
+    da = torch.randn(p, rows, device=DEV, generator=gen)
+    db = torch.randn(p, rows, device=DEV, generator=gen)
+    dy = torch.zeros_like(y)
+    ops.tri_gate_bwd(y, da, db, rows, hz, p, dy)
+    (a * da.t()).sum().add((b * db.t()).sum()).backward()
+    assert rel(dy[:, hz:], yf.grad[:, hz:]) < 1e-2
+
+    # gated residual with the g gate stored in Y (row stride hz + 4p)
+    res = _mk((rows, hz), gen)
+    y2 = _mk((rows, hz), gen)
+    bias = torch.randn(hz, device=DEV, generator=gen)
+    out = ops.gated_residual_fwd(res, y2, bias, rows, hz, gp=y, gp_rs=hz + 4 * p)
+    y2f = y2.float().requires_grad_(True)
+    bf = bias.clone().requires_grad_(True)
+    gpf = y.float()[:, :hz].requires_grad_(True)
+    ref = res.float() + torch.sigmoid(gpf) * (y2f + bf)
+    assert rel(out, ref) < 1e-2
+    dout = _mk((rows, hz), gen)
+    ref.backward(dout.float())
+    dy2 = torch.empty_like(y2)
+    dgp = torch.zeros_like(y)
+    dbias = torch.zeros(hz, device=DEV)
+    ops.gated_residual_bwd(dout, rows, hz, y=y2, bias=bias, gp=y, gp_rs=hz + 4 * p, dy=dy2, dgp=dgp,
+                           dgp_rs=hz + 4 * p, dbias=dbias)
+    assert rel(dy2, y2f.grad) < 1e-2
+    assert rel(dgp[:, :hz], gpf.grad) < 1e-2
+    assert rel(dbias, bf.grad) < 1e-3
+
+    # bias + relu
+    h = _mk((rows, 64), gen)
+    h0 = h.float().clone()
+    b1 = torch.randn(64, device=DEV, generator=gen)
+    ops.bias_act_fwd(h, b1, rows, 64)
+    assert rel(h, torch.relu(h0 + b1)) < 1e-2
+    dh = _mk((rows, 64), gen)
+    db1 = torch.zeros(64, device=DEV)
+    dyy = ops.bias_act_bwd(dh, h, rows, 64, dbias=db1)
+    want = dh.float() * (h.float() > 0)
+    assert rel(dyy, want) < 1e-2 and rel(db1, want.sum(0)) < 1e-3
+
+
+def test_count_nonfinite():
+    x = torch.zeros(1000, device=DEV)
+    x[3] = float("inf")
+    x[500] = float("nan")
+    assert ops.count_nonfinite(x) == 2

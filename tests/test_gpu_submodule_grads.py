@@ -1,0 +1,129 @@
+"""Per-sub-module backward parity: every *_bwd of block.py against torch float64
+autograd of the oracle sub-module (oracle/evoformer_torch.py).  dx is compared
+as the full residual-stream gradient g + df/dx; parameter gradients per packed
+reference key."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():
+    pytest.skip("needs CUDA", allow_module_level=True)
+
+from oracle import evoformer_torch as T  # noqa: E402
+from paper_2203_00854_b200 import block as B  # noqa: E402
+from paper_2203_00854_b200.config import EvoConfig, init_block_params, synthetic_inputs  # noqa: E402
+from paper_2203_00854_b200.params import BlockParams  # noqa: E402
+
+CFG = EvoConfig(16, 32, 64, 32, 2, 1, 16)
+# Gradient tolerance (relative Frobenius per tensor).  bf16 storage of activations
+# and weights flips the ReLU mask of the transitions for pre-activations within
+# rounding distance of 0; each flip is an O(1) change of that unit's gradient, so
+# a fraction f of flips gives ~sqrt(f) relative error (measured 2-4.6% on the
+# transitions, <1.5% everywhere else).  Forward outputs keep the 2e-2 bound.
+GRAD_TOL = 5e-2
+
+
+def rel(a, b):
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def _ref_grads(fn, x, p, g, keys):
+    xt = torch.tensor(x, requires_grad=True)
+    pt = {k: torch.tensor(v, requires_grad=True) for k, v in p.items()}
+    out = fn(xt, pt)
+    (out * torch.tensor(g)).sum().backward()
+    return xt.grad.numpy() + g, {k: pt[k].grad.numpy() for k in keys if pt[k].grad is not None}
+
+
+MODS = ["msa_row_m", "msa_col", "msa_trans", "tri_out", "tri_in", "pair_row", "pair_col", "pair_trans", "opm"]
+
+
+@pytest.mark.parametrize("mod", MODS)
+def test_submodule_backward(mod):
+    cfg = CFG
+    p = init_block_params(cfg, 3)
+    m, z = synthetic_inputs(cfg, 3)
+    S, R = cfg.n_seq, cfg.n_res
+    rng = np.random.default_rng(5)
+    bp = BlockParams(p, cfg)
+    bp.zero_grad()
+    dev = lambda a: torch.tensor(a, device="cuda").bfloat16()
+    # round inputs to bf16 so both sides see the same x
+    m = dev(m).double().cpu().numpy()
+    z = dev(z).double().cpu().numpy()
+    if mod == "msa_row_m":
+        bias_ref = T.msa_row_bias(torch.tensor(z), {k: torch.tensor(v) for k, v in p.items()}, cfg)
+        g = rng.normal(size=m.shape)
+        zt = dev(z).view(R * R, -1)
+        bias, svb = B.msa_row_bias_fwd(bp, zt, R)
+        out, sv = B.attention_fwd(bp, "msa_row", dev(m).view(S * R, -1), S, R, "row", bias=bias)
+        dx, dbias = B.attention_bwd(bp, sv, dev(g).view(S * R, -1))
+        dz = torch.zeros(R * R, cfg.h_pair, device="cuda", dtype=torch.bfloat16)
+        B.msa_row_bias_bwd(bp, svb, dbias, dz)
+        # reference: d/dm and d/dz of <msa_row_attention(m, z), g>
+        mt = torch.tensor(m, requires_grad=True)
+        ztt = torch.tensor(z, requires_grad=True)
+        pt = {k: torch.tensor(v, requires_grad=True) for k, v in p.items()}
+        (T.msa_row_attention(mt, ztt, pt, cfg) * torch.tensor(g)).sum().backward()
+        errs = {"dm": rel(dx.double().cpu().view(m.shape), mt.grad.numpy() + g),
+                "dz": rel(dz.double().cpu().view(z.shape), ztt.grad.numpy())}
+        keys = [k for k in p if k.startswith("msa_row/")]
+        ref_p = {k: pt[k].grad.numpy() for k in keys}
+    else:
+        fns = {
+            "msa_col": (m, lambda x, q: T.msa_col_attention(x, q, cfg)),
+            "msa_trans": (m, lambda x, q: T.transition(x, q, "msa_trans")),
+            "tri_out": (z, lambda x, q: T.tri_update_outgoing(x, q, cfg)),
+            "tri_in": (z, lambda x, q: T.tri_update_incoming(x, q, cfg)),
+            "pair_row": (z, lambda x, q: T.pair_attention_row(x, q, cfg)),
+            "pair_col": (z, lambda x, q: T.pair_attention_col(x, q, cfg)),
+            "pair_trans": (z, lambda x, q: T.transition(x, q, "pair_trans")),
+            "opm": (m, lambda x, q: T.outer_product_mean(x, q, cfg)),
+        }
+        x, fn = fns[mod]
+        prefix = mod.split("_m")[0]
+        keys = [k for k in p if k.startswith(prefix + "/")]
+        if mod == "opm":
+            g = rng.normal(size=(R, R, cfg.h_pair))
+            xt = torch.tensor(x, requires_grad=True)
+            pt = {k: torch.tensor(v, requires_grad=True) for k, v in p.items()}
+            (fn(xt, pt) * torch.tensor(g)).sum().backward()
+            ref_dx, ref_p = xt.grad.numpy(), {k: pt[k].grad.numpy() for k in keys}
+            zt = dev(z).view(R * R, -1)
+            out, sv = B.opm_fwd(bp, dev(m).view(S * R, -1), zt, S, R)
+            dm = torch.zeros(S * R, cfg.h_msa, device="cuda", dtype=torch.bfloat16)
+            B.opm_bwd(bp, sv, dev(g).view(R * R, -1), dm)
+            errs = {"dx": rel(dm.double().cpu().view(x.shape), ref_dx)}
+        else:
+            g = rng.normal(size=x.shape)
+            ref_dx, ref_p = _ref_grads(fn, x, p, g, keys)
+            x2 = dev(x).view(-1, x.shape[-1])
+            if mod == "msa_col":
+                out, sv = B.attention_fwd(bp, "msa_col", x2, R, S, "col")
+                dx, _ = B.attention_bwd(bp, sv, dev(g).view(S * R, -1))
+            elif mod in ("msa_trans", "pair_trans"):
+                out, sv = B.transition_fwd(bp, mod, x2, x2.shape[0])
+                dx = B.transition_bwd(bp, sv, dev(g).view(x2.shape))
+            elif mod in ("tri_out", "tri_in"):
+                out, sv = B.triangle_fwd(bp, mod, x2, R)
+                dx = B.triangle_bwd(bp, sv, dev(g).view(x2.shape))
+            else:
+                out, sv = B.attention_fwd(bp, mod, x2, R, R, "row" if mod == "pair_row" else "col", bias="pair")
+                dx, _ = B.attention_bwd(bp, sv, dev(g).view(x2.shape))
+            errs = {"dx": rel(dx.double().cpu().view(x.shape), ref_dx)}
+    torch.cuda.synchronize()
+    got = bp.grads_to_reference()
+    scale = max(np.linalg.norm(ref_p[k]) for k in keys)
+    for k in keys:
+        if np.linalg.norm(ref_p[k]) < 1e-9 * scale:
+            # analytically zero (k biases: softmax is invariant to a per-query shift);
+            # bf16 leaves O(eps) noise - require it to be negligible instead
+            assert np.linalg.norm(got[k]) <= 1e-2 * scale, (k, np.linalg.norm(got[k]), scale)
+            continue
+        errs[k] = rel(got[k], ref_p[k])
+    print(mod, {k: round(v, 4) for k, v in errs.items()})
+    bad = {k: v for k, v in errs.items() if v > GRAD_TOL}
+    assert not bad, bad
