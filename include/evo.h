@@ -176,6 +176,9 @@ int evo_gated_residual_bwd(const void* dout, const void* y, int64_t y_rs, const 
                            const void* gp, int64_t gp_rs, void* dy, void* dgp, int64_t dgp_rs,
                            float* dbias, int dtype, int64_t rows, int64_t cols, void* stream);
 
+/* out[c] += sum_r x[r*ld + c]  (fp32 out; bias gradients of the projection GEMMs) */
+int evo_colsum(const void* x, int dtype, int64_t ld, int64_t rows, int64_t cols, float* out, void* stream);
+
 /* h = act(y + bias) in place (act 0 = identity, 1 = ReLU: transition, evoformer.py:239) */
 int evo_bias_act_fwd(void* y, const float* bias, int64_t rows, int64_t cols, int act, int dtype, void* stream);
 /* dy = dh * (h > 0) (act 1) and dbias += sum_r dy; h is the activated output */

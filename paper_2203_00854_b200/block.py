@@ -43,7 +43,11 @@ def _wgrad(x, dy, out):
 
 
 def _bgrad(dy, out):
-    out.copy_(dy.sum(0, dtype=F32))
+    """bias gradient (accumulated into the zeroed fp32 grad view)"""
+    if dy.is_cuda:
+        ops.colsum(dy, out)
+    else:  # CPU only in the host-logic tests (fake kernel backend)
+        out += dy.float().sum(0)
 
 
 class Saved(dict):

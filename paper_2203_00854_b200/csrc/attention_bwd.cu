@@ -30,6 +30,7 @@ struct AttnBwdParams {
   float* dQacc;  // workspace [B][L][H*c]
   float* Dsum;   // workspace [B][H][L]
   float scale;
+  int64_t B;
 };
 
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
@@ -92,7 +93,7 @@ __global__ void __launch_bounds__(256) attn_bwd_prep(AttnBwdParams P, int64_t B)
 constexpr int BW_BK = 128;  // keys per CTA
 constexpr int BW_BQ = 128;  // queries per iteration
 
-template <int CP>
+template <int CP, bool RED>
 struct BwdSmem {
   static constexpr uint32_t K = 0;                          // [key][d] K-major
   static constexpr uint32_t V = K + BW_BK * CP * 2;         // [key][d] K-major
@@ -103,7 +104,8 @@ struct BwdSmem {
   static constexpr uint32_t LSE = DST + BW_BK * BW_BQ * 2;  // fp32 [128]
   static constexpr uint32_t DD = LSE + BW_BQ * 4;           // fp32 [128]
   static constexpr uint32_t KB = DD + BW_BQ * 4;            // fp32 [2][128] per-key dbias partials
-  static constexpr uint32_t TOTAL = KB + 2 * BW_BK * 4;
+  static constexpr uint32_t RB = KB + 2 * BW_BK * 4;        // fp32 [2 qtiles][128 keys][128 q] (RED only)
+  static constexpr uint32_t TOTAL = RB + (RED ? 2 * BW_BK * BW_BQ * 4 : 0);
 };
 
 template <int CP>
@@ -118,9 +120,11 @@ __device__ __forceinline__ void bw_load(uint32_t sdst, const bf16* base, int64_t
   }
 }
 
-template <int CP>
-__global__ void __launch_bounds__(256, 1) attn_bwd_kernel(AttnBwdParams P) {
-  using SM = BwdSmem<CP>;
+// RED: the bias is shared over the batch (msa_row, dbias stride 0 on b) and L <= 256:
+//      dbias is reduced over the CTA's batch group in shared memory, flushed once.
+template <int CP, bool RED>
+__global__ void __launch_bounds__(256, 1) attn_bwd_kernel(AttnBwdParams P, int G, int dq_partial) {
+  using SM = BwdSmem<CP, RED>;
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar1, bar2;
   __shared__ uint32_t tmem_sh;
@@ -128,176 +132,212 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_kernel(AttnBwdParams P) {
   float* s_lse = reinterpret_cast<float*>(smem + SM::LSE);
   float* s_D = reinterpret_cast<float*>(smem + SM::DD);
   float* s_kb = reinterpret_cast<float*>(smem + SM::KB);
+  float* s_red = reinterpret_cast<float*>(smem + SM::RB);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wq = warp & 3, wg = warp >> 2;
   const int k0 = blockIdx.x * BW_BK;
   const int h = blockIdx.y;
-  const int64_t b = blockIdx.z;
   const AttnParams& F = P.f;
   const int L = F.L, c = F.c, H = F.H;
+  const int64_t Btot = P.B;
+  const int64_t b_begin = (int64_t)blockIdx.z * G;
+  const int64_t b_end = b_begin + G < Btot ? b_begin + G : Btot;
   const int kr = wq * 32 + lane;  // key row of this thread (TMEM lane)
   const int kj = k0 + kr;
   const bool kvalid = kj < L;
   const bool per_key_bias = F.bias && F.bs2 == 0;
   const bool db_per_key = P.dbias && P.db2 == 0;
+  const int nqt = (L + BW_BQ - 1) / BW_BQ;
+  const int nkt = gridDim.x;
+  const float LOG2E_ = 1.4426950408889634f;
 
-  if (warp == 0) tmem_alloc(&tmem_sh, 512);
+  if (warp == 0) tmem_alloc(&tmem_sh, 256);
   if (threadIdx.x == 0) {
     mbar_init(&bar1, 1);
     mbar_init(&bar2, 1);
     fence_mbar_init();
   }
-  const bf16* kb = F.k + b * F.k_sb + (int64_t)h * c;
-  const bf16* vb = F.v + b * F.v_sb + (int64_t)h * c;
-  const bf16* qb = F.q + b * F.q_sb + (int64_t)h * c;
-  const bf16* dob = P.dO + b * (int64_t)L * H * c + (int64_t)h * c;
-  bw_load<CP>(sb + SM::K, kb, F.k_sl, k0, L - k0, c);
-  bw_load<CP>(sb + SM::V, vb, F.v_sl, k0, L - k0, c);
-  cp_async_commit();
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = tmem_sh;
-  const uint32_t t_lane = tmem + ((uint32_t)(wq * 32) << 16);
-  constexpr uint32_t T_S = 0, T_DP = 128, T_DV = 256, T_DK = 256 + CP, T_DQ = 0;
-
-  float kbias = 0.f;
-  if (per_key_bias && kvalid) kbias = bf2f(F.bias[b * F.bs0 + (int64_t)h * F.bs1 + (int64_t)kj * F.bs3]);
-  const bf16* bias_col = nullptr;  // full bias: element (q, kj)
-  if (F.bias && !per_key_bias && kvalid) bias_col = F.bias + b * F.bs0 + (int64_t)h * F.bs1 + (int64_t)kj * F.bs3;
-  float* dbias_col = nullptr;
-  if (P.dbias && kvalid) dbias_col = P.dbias + b * P.db0 + (int64_t)h * P.db1 + (int64_t)kj * P.db3;
-  const float LOG2E_ = 1.4426950408889634f;
-
-  constexpr uint32_t ID_SS = make_idesc_bf16(128, 128, 0, 0);  // S^T = K Q^T, dP^T = V dO^T
-  constexpr uint32_t ID_KV = make_idesc_bf16(128, CP, 0, 1);   // dV += P^T dO, dK += dS^T Q  (B MN-major view)
-  constexpr uint32_t ID_Q = make_idesc_bf16(128, CP, 1, 1);    // dQ = dS K (A and B as MN-major views)
-  constexpr uint32_t LBO_ROWS = (128 / 8) * 128;               // 2048: next 8-k group of a 128-row K-major tile
-
-  const int nqt = (L + BW_BQ - 1) / BW_BQ;
-  for (int it = 0; it < nqt; ++it) {
-    const int q0 = it * BW_BQ;
-    bw_load<CP>(sb + SM::Q, qb, F.q_sl, q0, L - q0, c);
-    bw_load<CP>(sb + SM::DO, dob, (int64_t)H * c, q0, L - q0, c);
+  if (RED) {
+    for (int i = threadIdx.x; i < 2 * BW_BK * BW_BQ; i += 256) s_red[i] = 0.f;
+  }
+  const int64_t HC = (int64_t)H * c;
+  auto issue_loads = [&](int64_t b, int qt, bool with_kv) {
+    const int q0 = qt * BW_BQ;
+    if (with_kv) {
+      bw_load<CP>(sb + SM::K, F.k + b * F.k_sb + (int64_t)h * c, F.k_sl, k0, L - k0, c);
+      bw_load<CP>(sb + SM::V, F.v + b * F.v_sb + (int64_t)h * c, F.v_sl, k0, L - k0, c);
+    }
+    bw_load<CP>(sb + SM::Q, F.q + b * F.q_sb + (int64_t)h * c, F.q_sl, q0, L - q0, c);
+    bw_load<CP>(sb + SM::DO, P.dO + b * (int64_t)L * HC + (int64_t)h * c, HC, q0, L - q0, c);
     cp_async_commit();
     if (threadIdx.x < BW_BQ) {
       const int qq = q0 + threadIdx.x;
       s_lse[threadIdx.x] = qq < L ? F.lse[(b * H + h) * (int64_t)L + qq] * LOG2E_ : 0.f;
       s_D[threadIdx.x] = qq < L ? P.Dsum[(b * H + h) * (int64_t)L + qq] : 0.f;
     }
-    cp_async_wait<0>();
-    fence_async_smem();
-    __syncthreads();
+  };
+  issue_loads(b_begin, 0, true);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_sh;
+  const uint32_t t_lane = tmem + ((uint32_t)(wq * 32) << 16);
+  constexpr uint32_t T_S = 0, T_DP = 128, T_DV = 0, T_DK = CP, T_DQ = 2 * CP;
 
-    if (threadIdx.x == 0) {
-      tc_fence_after();
+  constexpr uint32_t ID_SS = make_idesc_bf16(128, 128, 0, 0);  // S^T = K Q^T, dP^T = V dO^T
+  constexpr uint32_t ID_KV = make_idesc_bf16(128, CP, 0, 1);   // dV = P^T dO, dK = dS^T Q  (B: MN-major view)
+  constexpr uint32_t ID_Q = make_idesc_bf16(128, CP, 1, 1);    // dQ = dS K  (A and B: MN-major views)
+  constexpr uint32_t LBO_ROWS = (128 / 8) * 128;               // 2048: next 8-k group of a 128-row K-major tile
+
+  int it = 0;
+  for (int64_t b = b_begin; b < b_end; ++b) {
+    float acc[CP];  // dV (warpgroup 0) or dK (warpgroup 1) of this key row, summed over query tiles
 #pragma unroll
-      for (int kk = 0; kk < CP / 16; ++kk) {
-        const uint32_t koff = kk * 2 * LBO_ROWS;
-        mma_bf16(tmem + T_S, make_sdesc(sb + SM::K + koff, LBO_ROWS, 128), make_sdesc(sb + SM::Q + koff, LBO_ROWS, 128),
-                 ID_SS, kk != 0);
-        mma_bf16(tmem + T_DP, make_sdesc(sb + SM::V + koff, LBO_ROWS, 128),
-                 make_sdesc(sb + SM::DO + koff, LBO_ROWS, 128), ID_SS, kk != 0);
+    for (int d = 0; d < CP; ++d) acc[d] = 0.f;
+    float kbias = 0.f;
+    if (per_key_bias && kvalid) kbias = bf2f(F.bias[b * F.bs0 + (int64_t)h * F.bs1 + (int64_t)kj * F.bs3]);
+    const bf16* bias_col = nullptr;
+    if (F.bias && !per_key_bias && kvalid) bias_col = F.bias + b * F.bs0 + (int64_t)h * F.bs1 + (int64_t)kj * F.bs3;
+    float* dbias_col = nullptr;
+    if (P.dbias && kvalid) dbias_col = P.dbias + b * P.db0 + (int64_t)h * P.db1 + (int64_t)kj * P.db3;
+
+    for (int qt = 0; qt < nqt; ++qt, ++it) {
+      const int q0 = qt * BW_BQ;
+      cp_async_wait<0>();
+      fence_async_smem();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < CP / 16; ++kk) {
+          const uint32_t koff = kk * 2 * LBO_ROWS;
+          mma_bf16(tmem + T_S, make_sdesc(sb + SM::K + koff, LBO_ROWS, 128),
+                   make_sdesc(sb + SM::Q + koff, LBO_ROWS, 128), ID_SS, kk != 0);
+          mma_bf16(tmem + T_DP, make_sdesc(sb + SM::V + koff, LBO_ROWS, 128),
+                   make_sdesc(sb + SM::DO + koff, LBO_ROWS, 128), ID_SS, kk != 0);
+        }
+        mma_commit(&bar1);
       }
-      mma_commit(&bar1);
-    }
-    mbar_wait(&bar1, it & 1);
-    tc_fence_after();
+      mbar_wait(&bar1, it & 1);
+      tc_fence_after();
 
-    float kb_acc = 0.f;
+      float kb_acc = 0.f;
 #pragma unroll 1
-    for (int half = 0; half < 2; ++half) {
-      const int qc = wg * 64 + half * 32;  // query column offset inside the tile
-      float s[32], dp[32];
-      tmem_ld32(t_lane + T_S + qc, s);
-      tmem_ld32(t_lane + T_DP + qc, dp);
-      tmem_ld_wait();
-      float pv[32], dsv[32];
+      for (int half = 0; half < 2; ++half) {
+        const int qc = wg * 64 + half * 32;  // query column offset inside the tile
+        float s[32], dp[32];
+        tmem_ld32(t_lane + T_S + qc, s);
+        tmem_ld32(t_lane + T_DP + qc, dp);
+        tmem_ld_wait();
+        float pv[32], dsv[32];
 #pragma unroll
-      for (int e = 0; e < 32; ++e) {
-        const int ql = qc + e, qq = q0 + ql;
-        float x = s[e];
-        if (bias_col && qq < L) x += bf2f(bias_col[(int64_t)qq * F.bs2]);
-        x += kbias;
-        const bool ok = kvalid && qq < L;
-        const float p = ok ? exp2f(x * F.scale_log2 - s_lse[ql]) : 0.f;
-        const float ds = p * (dp[e] - s_D[ql]);
-        pv[e] = p;
-        dsv[e] = ds;
-        if (ok) {
-          if (db_per_key) kb_acc += ds;
-          else if (dbias_col) atomicAdd(dbias_col + (int64_t)qq * P.db2, P.scale * ds);
+        for (int e = 0; e < 32; ++e) {
+          const int ql = qc + e, qq = q0 + ql;
+          float x = s[e] + kbias;
+          if (bias_col && qq < L) x += bf2f(bias_col[(int64_t)qq * F.bs2]);
+          const bool ok = kvalid && qq < L;
+          const float p = ok ? exp2f(x * F.scale_log2 - s_lse[ql]) : 0.f;
+          const float ds = p * (dp[e] - s_D[ql]);
+          pv[e] = p;
+          dsv[e] = ds;
+        }
+        if (RED) {
+          float* r = s_red + (qt * BW_BK + kr) * BW_BQ + qc;
+#pragma unroll
+          for (int e = 0; e < 32; e += 4) {
+            float4 o = *reinterpret_cast<float4*>(r + e);
+            o.x += dsv[e]; o.y += dsv[e + 1]; o.z += dsv[e + 2]; o.w += dsv[e + 3];
+            *reinterpret_cast<float4*>(r + e) = o;
+          }
+        } else if (db_per_key) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) kb_acc += dsv[e];
+        } else if (dbias_col) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (q0 + qc + e < L) atomicAdd(dbias_col + (int64_t)(q0 + qc + e) * P.db2, P.scale * dsv[e]);
+        }
+#pragma unroll
+        for (int e = 0; e < 32; e += 8) {
+          st_shared_v4(sb + SM::PT + kmajor_off(kr, qc + e, 128), pack_bf16x2(pv[e], pv[e + 1]),
+                       pack_bf16x2(pv[e + 2], pv[e + 3]), pack_bf16x2(pv[e + 4], pv[e + 5]),
+                       pack_bf16x2(pv[e + 6], pv[e + 7]));
+          st_shared_v4(sb + SM::DST + kmajor_off(kr, qc + e, 128), pack_bf16x2(dsv[e], dsv[e + 1]),
+                       pack_bf16x2(dsv[e + 2], dsv[e + 3]), pack_bf16x2(dsv[e + 4], dsv[e + 5]),
+                       pack_bf16x2(dsv[e + 6], dsv[e + 7]));
         }
       }
-#pragma unroll
-      for (int e = 0; e < 32; e += 8) {
-        st_shared_v4(sb + SM::PT + kmajor_off(kr, qc + e, 128), pack_bf16x2(pv[e], pv[e + 1]),
-                     pack_bf16x2(pv[e + 2], pv[e + 3]), pack_bf16x2(pv[e + 4], pv[e + 5]),
-                     pack_bf16x2(pv[e + 6], pv[e + 7]));
-        st_shared_v4(sb + SM::DST + kmajor_off(kr, qc + e, 128), pack_bf16x2(dsv[e], dsv[e + 1]),
-                     pack_bf16x2(dsv[e + 2], dsv[e + 3]), pack_bf16x2(dsv[e + 4], dsv[e + 5]),
-                     pack_bf16x2(dsv[e + 6], dsv[e + 7]));
-      }
-    }
-    if (db_per_key) s_kb[wg * BW_BK + kr] = kb_acc;
+      if (db_per_key) s_kb[wg * BW_BK + kr] = kb_acc;
 
-    fence_async_smem();
-    tc_fence_before();
-    __syncthreads();
-    if (db_per_key && wg == 0 && dbias_col) atomicAdd(dbias_col, P.scale * (s_kb[kr] + s_kb[BW_BK + kr]));
-    if (threadIdx.x == 0) {
+      fence_async_smem();
+      tc_fence_before();
+      __syncthreads();
+      if (db_per_key && wg == 0 && dbias_col) atomicAdd(dbias_col, P.scale * (s_kb[kr] + s_kb[BW_BK + kr]));
+      if (threadIdx.x == 0) {
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < BW_BQ / 16; ++kk) {
+          const uint32_t aoff = kk * 2 * LBO_ROWS;
+          const uint32_t boff = kk * 2 * 128;
+          mma_bf16(tmem + T_DV, make_sdesc(sb + SM::PT + aoff, LBO_ROWS, 128),
+                   make_sdesc(sb + SM::DO + boff, 128, LBO_ROWS), ID_KV, kk != 0);
+          mma_bf16(tmem + T_DK, make_sdesc(sb + SM::DST + aoff, LBO_ROWS, 128),
+                   make_sdesc(sb + SM::Q + boff, 128, LBO_ROWS), ID_KV, kk != 0);
+        }
+#pragma unroll
+        for (int kk = 0; kk < BW_BK / 16; ++kk) {
+          const uint32_t off = kk * 2 * 128;
+          mma_bf16(tmem + T_DQ, make_sdesc(sb + SM::DST + off, 128, LBO_ROWS),
+                   make_sdesc(sb + SM::K + off, 128, LBO_ROWS), ID_Q, kk != 0);
+        }
+        mma_commit(&bar2);
+      }
+      mbar_wait(&bar2, it & 1);
       tc_fence_after();
+      // the tiles are free: prefetch the next (batch, query tile) while draining TMEM
+      const bool last_q = qt + 1 == nqt;
+      if (!(last_q && b + 1 == b_end)) issue_loads(last_q ? b + 1 : b, last_q ? 0 : qt + 1, last_q);
+      {
+        float v[CP];
+        if constexpr (CP == 16) tmem_ld16(t_lane + (wg == 0 ? T_DV : T_DK), v);
+        else {
 #pragma unroll
-      for (int kk = 0; kk < BW_BQ / 16; ++kk) {
-        // A = P^T / dS^T [key][query] K-major; B = dO / Q [query][d] viewed MN-major (mn = d, k = query)
-        const uint32_t aoff = kk * 2 * LBO_ROWS;
-        const uint32_t boff = kk * 2 * 128;
-        mma_bf16(tmem + T_DV, make_sdesc(sb + SM::PT + aoff, LBO_ROWS, 128),
-                 make_sdesc(sb + SM::DO + boff, 128, LBO_ROWS), ID_KV, (it | kk) != 0);
-        mma_bf16(tmem + T_DK, make_sdesc(sb + SM::DST + aoff, LBO_ROWS, 128),
-                 make_sdesc(sb + SM::Q + boff, 128, LBO_ROWS), ID_KV, (it | kk) != 0);
+          for (int cc = 0; cc < CP; cc += 32) tmem_ld32(t_lane + (wg == 0 ? T_DV : T_DK) + cc, v + cc);
+        }
+        float w[CP / 2];
+        if constexpr (CP == 16) tmem_ld8(t_lane + T_DQ + wg * 8, w);
+        else if constexpr (CP == 32) tmem_ld16(t_lane + T_DQ + wg * 16, w);
+        else tmem_ld32(t_lane + T_DQ + wg * 32, w);
+        tmem_ld_wait();
+#pragma unroll
+        for (int d = 0; d < CP; ++d) acc[d] += v[d];
+        const int qq = q0 + kr;  // dQ: TMEM lane = query row
+        if (qq < L) {
+          if (dq_partial) {
+            float* dst = P.dQacc + (((int64_t)blockIdx.x * Btot + b) * L + qq) * HC + (int64_t)h * c + wg * (CP / 2);
+            if (wg * (CP / 2) + CP / 2 <= c) {
+#pragma unroll
+              for (int e = 0; e < CP / 2; e += 4)
+                *reinterpret_cast<float4*>(dst + e) =
+                    make_float4(P.scale * w[e], P.scale * w[e + 1], P.scale * w[e + 2], P.scale * w[e + 3]);
+            } else {
+#pragma unroll
+              for (int e = 0; e < CP / 2; ++e)
+                if (wg * (CP / 2) + e < c) dst[e] = P.scale * w[e];
+            }
+          } else {
+            float* dst = P.dQacc + (b * L + qq) * HC + (int64_t)h * c + wg * (CP / 2);
+#pragma unroll
+            for (int e = 0; e < CP / 2; ++e)
+              if (wg * (CP / 2) + e < c) atomicAdd(dst + e, P.scale * w[e]);
+          }
+        }
       }
-#pragma unroll
-      for (int kk = 0; kk < BW_BK / 16; ++kk) {
-        // A = dS [query][key] = dS^T tile viewed MN-major (mn = query, k = key); B = K [key][d] viewed MN-major
-        const uint32_t off = kk * 2 * 128;
-        mma_bf16(tmem + T_DQ, make_sdesc(sb + SM::DST + off, 128, LBO_ROWS), make_sdesc(sb + SM::K + off, 128, LBO_ROWS),
-                 ID_Q, kk != 0);
-      }
-      mma_commit(&bar2);
+      tc_fence_before();
+      __syncthreads();
     }
-    mbar_wait(&bar2, it & 1);
-    tc_fence_after();
-    {
-      // dQ partial: TMEM lane = query row; warpgroup wg handles columns [wg*CP/2, (wg+1)*CP/2)
-      const int qq = q0 + kr;
-      float v[CP / 2];
-      if constexpr (CP == 16) tmem_ld8(t_lane + T_DQ + wg * 8, v);
-      else if constexpr (CP == 32) tmem_ld16(t_lane + T_DQ + wg * 16, v);
-      else tmem_ld32(t_lane + T_DQ + wg * 32, v);
-      tmem_ld_wait();
-      if (qq < L) {
-        float* dst = P.dQacc + (b * L + qq) * (int64_t)(H * c) + (int64_t)h * c + wg * (CP / 2);
-#pragma unroll
-        for (int e = 0; e < CP / 2; ++e)
-          if (wg * (CP / 2) + e < c) atomicAdd(dst + e, P.scale * v[e]);
-      }
-    }
-    tc_fence_before();
-    __syncthreads();
-  }
-
-  // dV (warpgroup 0) and dK (warpgroup 1): TMEM lane = key row
-  {
-    float v[CP];
-    const uint32_t col = wg == 0 ? T_DV : T_DK;
-    if constexpr (CP == 16) tmem_ld16(t_lane + col, v);
-    else {
-#pragma unroll
-      for (int cc = 0; cc < CP; cc += 32) tmem_ld32(t_lane + col + cc, v + cc);
-    }
-    tmem_ld_wait();
+    // dV (warpgroup 0) and dK (warpgroup 1) of batch b
     if (kvalid) {
       const float sc = wg == 0 ? 1.f : P.scale;
       bf16* dst = wg == 0 ? P.dv + b * P.dv_sb + (int64_t)kj * P.dv_sl + (int64_t)h * c
@@ -305,30 +345,49 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_kernel(AttnBwdParams P) {
 #pragma unroll
       for (int d = 0; d < CP; d += 8) {
         if (d < c) {
-          uint4 w;
-          w.x = pack_bf16x2(sc * v[d], sc * v[d + 1]);
-          w.y = pack_bf16x2(sc * v[d + 2], sc * v[d + 3]);
-          w.z = pack_bf16x2(sc * v[d + 4], sc * v[d + 5]);
-          w.w = pack_bf16x2(sc * v[d + 6], sc * v[d + 7]);
-          *reinterpret_cast<uint4*>(dst + d) = w;
+          uint4 wv;
+          wv.x = pack_bf16x2(sc * acc[d], sc * acc[d + 1]);
+          wv.y = pack_bf16x2(sc * acc[d + 2], sc * acc[d + 3]);
+          wv.z = pack_bf16x2(sc * acc[d + 4], sc * acc[d + 5]);
+          wv.w = pack_bf16x2(sc * acc[d + 6], sc * acc[d + 7]);
+          *reinterpret_cast<uint4*>(dst + d) = wv;
         }
       }
     }
   }
+  if (RED && P.dbias) {
+    // flush the batch-group sums: thread (kr, wg) owns keys kr, queries [wg*64, wg*64+64) of each tile
+    if (kvalid) {
+      float* col = P.dbias + (int64_t)h * P.db1 + (int64_t)kj * P.db3;
+      for (int qt = 0; qt < nqt; ++qt)
+        for (int e = 0; e < 64; ++e) {
+          const int ql = wg * 64 + e, qq = qt * BW_BQ + ql;
+          if (qq < L) atomicAdd(col + (int64_t)qq * P.db2, P.scale * s_red[(qt * BW_BK + kr) * BW_BQ + ql]);
+        }
+    }
+  }
+  (void)nkt;
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, 512);
+  if (warp == 0) tmem_dealloc(tmem, 256);
 }
 
-__global__ void __launch_bounds__(256) attn_bwd_dq_finish(AttnBwdParams P, int64_t B) {
+__global__ void __launch_bounds__(256) attn_bwd_dq_finish(AttnBwdParams P, int64_t B, int nparts) {
   const int L = P.f.L, H = P.f.H, c = P.f.c;
-  const int64_t n8 = B * L * (int64_t)H * c / 8;
+  const int64_t n = B * L * (int64_t)H * c;
+  const int64_t n8 = n / 8;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = i * 8;
     const int64_t row = e / (H * c), col = e % (H * c);
     const int64_t b = row / L, l = row % L;
-    const float4 a = *reinterpret_cast<const float4*>(P.dQacc + e);
-    const float4 bq = *reinterpret_cast<const float4*>(P.dQacc + e + 4);
+    float4 a = *reinterpret_cast<const float4*>(P.dQacc + e);
+    float4 bq = *reinterpret_cast<const float4*>(P.dQacc + e + 4);
+    for (int p = 1; p < nparts; ++p) {
+      const float4 a2 = *reinterpret_cast<const float4*>(P.dQacc + p * n + e);
+      const float4 b2 = *reinterpret_cast<const float4*>(P.dQacc + p * n + e + 4);
+      a.x += a2.x; a.y += a2.y; a.z += a2.z; a.w += a2.w;
+      bq.x += b2.x; bq.y += b2.y; bq.z += b2.z; bq.w += b2.w;
+    }
     uint4 w;
     w.x = pack_bf16x2(a.x, a.y); w.y = pack_bf16x2(a.z, a.w);
     w.z = pack_bf16x2(bq.x, bq.y); w.w = pack_bf16x2(bq.z, bq.w);
@@ -336,10 +395,14 @@ __global__ void __launch_bounds__(256) attn_bwd_dq_finish(AttnBwdParams P, int64
   }
 }
 
+constexpr int DQ_MAX_PARTS = 4;  // <= 4 key tiles (L <= 512): per-tile dQ partials, plain stores
+
 static int64_t ws_layout(int64_t B, int64_t L, int H, int c, int64_t* off_dq, int64_t* off_D) {
   const int64_t n = B * L * (int64_t)H * c;
+  const int64_t nkt = (L + BW_BK - 1) / BW_BK;
+  const int64_t parts = nkt <= DQ_MAX_PARTS ? nkt : 1;
   int64_t o1 = ((n * 2 + 255) / 256) * 256;
-  int64_t o2 = o1 + ((n * 4 + 255) / 256) * 256;
+  int64_t o2 = o1 + ((parts * n * 4 + 255) / 256) * 256;
   if (off_dq) *off_dq = o1;
   if (off_D) *off_D = o2;
   return o2 + ((B * H * L * 4 + 255) / 256) * 256;
@@ -347,19 +410,34 @@ static int64_t ws_layout(int64_t B, int64_t L, int H, int c, int64_t* off_dq, in
 
 int sm_count();
 
-template <int CP>
-static int launch_bwd(AttnBwdParams& p, int64_t B, cudaStream_t st) {
-  using SM = BwdSmem<CP>;
+template <int CP, bool RED>
+static int launch_bwd(AttnBwdParams& p, int64_t B, int G, int dq_partial, cudaStream_t st) {
+  using SM = BwdSmem<CP, RED>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel<CP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM::TOTAL);
+    cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel<CP, RED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)SM::TOTAL);
     if (e != cudaSuccess) return cuda_status(e, "attn bwd attr");
     attr = true;
   }
-  dim3 grid((unsigned)((p.f.L + BW_BK - 1) / BW_BK), (unsigned)p.f.H, (unsigned)B);
-  attn_bwd_kernel<CP><<<grid, 256, SM::TOTAL, st>>>(p);
+  dim3 grid((unsigned)((p.f.L + BW_BK - 1) / BW_BK), (unsigned)p.f.H, (unsigned)((B + G - 1) / G));
+  attn_bwd_kernel<CP, RED><<<grid, 256, SM::TOTAL, st>>>(p, G, dq_partial);
   EVO_LAUNCH_CHECK("attention bwd main");
   return EVO_OK;
+}
+
+template <int CP>
+static int launch_bwd_cp(AttnBwdParams& p, int64_t B, int dq_partial, cudaStream_t st) {
+  const int64_t nkt = (p.f.L + BW_BK - 1) / BW_BK;
+  const int64_t units = B * p.f.H * nkt;
+  // batch-shared bias (msa_row) with L <= 256: reduce dbias over a batch group in smem
+  const bool red = p.dbias && p.db0 == 0 && p.db2 != 0 && p.f.L <= 2 * BW_BQ;
+  const int64_t ctas_per_sm = red ? 1 : 2;
+  int64_t G = units / ((int64_t)sm_count() * ctas_per_sm * 2);  // ~2 waves
+  if (G < 1) G = 1;
+  if (G > 16) G = 16;
+  if (red) return launch_bwd<CP, true>(p, B, (int)G, dq_partial, st);
+  return launch_bwd<CP, false>(p, B, (int)G, dq_partial, st);
 }
 
 }  // namespace evo
@@ -399,17 +477,22 @@ extern "C" int evo_gated_attention_bwd(const EvoAttnBwdDesc* d, void* stream) {
   p.Dsum = (float*)(ws + off_D);
   p.scale = d->f.scale;
   cudaStream_t st = (cudaStream_t)stream;
-  cudaError_t e = cudaMemsetAsync(p.dQacc, 0, (size_t)(B * L * H * c) * 4, st);
-  if (e != cudaSuccess) return cuda_status(e, "attention bwd memset");
+  const int64_t nkt = (L + BW_BK - 1) / BW_BK;
+  const int dq_partial = nkt <= DQ_MAX_PARTS ? 1 : 0;
+  p.B = B;
+  if (!dq_partial) {
+    cudaError_t e = cudaMemsetAsync(p.dQacc, 0, (size_t)(B * L * H * c) * 4, st);
+    if (e != cudaSuccess) return cuda_status(e, "attention bwd memset");
+  }
   attn_bwd_prep<<<(unsigned)((B * L + 7) / 8), 256, 0, st>>>(p, B);
   EVO_LAUNCH_CHECK("attention bwd prep");
-  if (c <= 16) rc = launch_bwd<16>(p, B, st);
-  else if (c <= 32) rc = launch_bwd<32>(p, B, st);
-  else rc = launch_bwd<64>(p, B, st);
+  if (c <= 16) rc = launch_bwd_cp<16>(p, B, dq_partial, st);
+  else if (c <= 32) rc = launch_bwd_cp<32>(p, B, dq_partial, st);
+  else rc = launch_bwd_cp<64>(p, B, dq_partial, st);
   if (rc) return rc;
   int64_t n8 = B * L * H * c / 8;
   int64_t g = (n8 + 255) / 256, cap = (int64_t)sm_count() * 16;
-  attn_bwd_dq_finish<<<(unsigned)(g < cap ? g : cap), 256, 0, st>>>(p, B);
+  attn_bwd_dq_finish<<<(unsigned)(g < cap ? g : cap), 256, 0, st>>>(p, B, dq_partial ? (int)nkt : 1);
   EVO_LAUNCH_CHECK("attention bwd finish");
   return EVO_OK;
 }

@@ -66,25 +66,58 @@ __global__ void __launch_bounds__(256) gated_residual_fwd_k(const T* __restrict_
   }
 }
 
-// block (32, 8): x = column chunk (8 cols), y = row lane
+// Column-reduction layout shared by the backward epilogues and colsum:
+// 256 threads, tpr = cols/8 threads per row (8 columns = 16 bytes each), rpi =
+// 256/tpr rows per iteration; CTA b owns the contiguous row slab
+// [b*slab, (b+1)*slab) and keeps its column partials in registers; one
+// shared-memory pass and one atomicAdd per column per CTA at the end
+// (grid ~ 2 x SMs, so each dbias address sees ~300 atomics, not ~rows/8).
+struct ColTile {
+  int tpr, rpi, tr, tc;
+  int64_t r0, r1;
+  __device__ ColTile(int64_t rows, int64_t cols) {
+    tpr = (int)(cols / 8);
+    rpi = blockDim.x / tpr;
+    tr = threadIdx.x / tpr;
+    tc = threadIdx.x % tpr;
+    const int64_t slab = (rows + gridDim.x - 1) / gridDim.x;
+    r0 = blockIdx.x * slab;
+    r1 = r0 + slab < rows ? r0 + slab : rows;
+  }
+  __device__ bool active() const { return tr < rpi; }
+};
+
+// red: shared [rpi][cols]; adds the CTA's column sums into out (fp32)
+__device__ __forceinline__ void col_flush(float* red, const ColTile& t, const float* acc, int64_t cols, float* out) {
+  if (t.active()) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) red[t.tr * cols + t.tc * 8 + e] = acc[e];
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+    float s = 0.f;
+    for (int r = 0; r < t.rpi; ++r) s += red[r * cols + c];
+    atomicAdd(out + c, s);
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) gated_residual_bwd_k(const T* __restrict__ dout, const T* __restrict__ y,
                                                             int64_t y_rs, const float* __restrict__ bias,
                                                             const T* __restrict__ gp, int64_t gp_rs, T* __restrict__ dy,
                                                             T* __restrict__ dgp, int64_t dgp_rs,
                                                             float* __restrict__ dbias, int64_t rows, int64_t cols) {
-  __shared__ float red[8][32 * 8 + 1];
-  const int64_t cchunk = (int64_t)blockIdx.x * 32 + threadIdx.x;
-  const bool cok = cchunk * 8 < cols;
-  const int64_t c = cchunk * 8;
+  extern __shared__ float red[];
+  const ColTile t(rows, cols);
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  if (cok) {
+  if (t.active()) {
+    const int64_t c = t.tc * 8;
     float b[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    if (bias) {
+    if (bias && gp) {
 #pragma unroll
       for (int e = 0; e < 8; ++e) b[e] = bias[c + e];
     }
-    for (int64_t r = (int64_t)blockIdx.y * 8 + threadIdx.y; r < rows; r += (int64_t)gridDim.y * 8) {
+    for (int64_t r = t.r0 + t.tr; r < t.r1; r += t.rpi) {
       float d[8];
       ld8<T>(dout + r * cols + c, d);
       if (gp) {
@@ -104,19 +137,33 @@ __global__ void __launch_bounds__(256) gated_residual_bwd_k(const T* __restrict_
       for (int e = 0; e < 8; ++e) acc[e] += d[e];
     }
   }
-  if (!dbias) return;
+  if (dbias) col_flush(red, t, acc, cols, dbias);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) colsum_k(const T* __restrict__ x, int64_t ld, int64_t rows, int64_t cols,
+                                                float* __restrict__ out) {
+  extern __shared__ float red[];
+  const ColTile t(rows, cols);
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (t.active()) {
+    const int64_t c = t.tc * 8;
+    int64_t r = t.r0 + t.tr;
+    for (; r + t.rpi < t.r1; r += 2 * t.rpi) {  // two rows in flight
+      float u[8], v[8];
+      ld8<T>(x + r * ld + c, u);
+      ld8<T>(x + (r + t.rpi) * ld + c, v);
 #pragma unroll
-  for (int e = 0; e < 8; ++e) red[threadIdx.y][threadIdx.x * 8 + e] = acc[e];
-  __syncthreads();
-  if (threadIdx.y == 0 && cok) {
+      for (int e = 0; e < 8; ++e) acc[e] += u[e] + v[e];
+    }
+    if (r < t.r1) {
+      float u[8];
+      ld8<T>(x + r * ld + c, u);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      float s = 0.f;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) s += red[k][threadIdx.x * 8 + e];
-      atomicAdd(dbias + c + e, s);
+      for (int e = 0; e < 8; ++e) acc[e] += u[e];
     }
   }
+  col_flush(red, t, acc, cols, out);
 }
 
 // ------------------------------------------------------------------ bias + activation
@@ -141,13 +188,12 @@ template <typename T>
 __global__ void __launch_bounds__(256) bias_act_bwd_k(const T* __restrict__ dh, const T* __restrict__ h,
                                                       T* __restrict__ dy, float* __restrict__ dbias, int64_t rows,
                                                       int64_t cols, int act) {
-  __shared__ float red[8][32 * 8 + 1];
-  const int64_t cchunk = (int64_t)blockIdx.x * 32 + threadIdx.x;
-  const bool cok = cchunk * 8 < cols;
-  const int64_t c = cchunk * 8;
+  extern __shared__ float red[];
+  const ColTile t(rows, cols);
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  if (cok) {
-    for (int64_t r = (int64_t)blockIdx.y * 8 + threadIdx.y; r < rows; r += (int64_t)gridDim.y * 8) {
+  if (t.active()) {
+    const int64_t c = t.tc * 8;
+    for (int64_t r = t.r0 + t.tr; r < t.r1; r += t.rpi) {
       float d[8], hv[8];
       ld8<T>(dh + r * cols + c, d);
       if (act == 1) {
@@ -160,19 +206,7 @@ __global__ void __launch_bounds__(256) bias_act_bwd_k(const T* __restrict__ dh, 
       for (int e = 0; e < 8; ++e) acc[e] += d[e];
     }
   }
-  if (!dbias) return;
-#pragma unroll
-  for (int e = 0; e < 8; ++e) red[threadIdx.y][threadIdx.x * 8 + e] = acc[e];
-  __syncthreads();
-  if (threadIdx.y == 0 && cok) {
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      float s = 0.f;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) s += red[k][threadIdx.x * 8 + e];
-      atomicAdd(dbias + c + e, s);
-    }
-  }
+  if (dbias) col_flush(red, t, acc, cols, dbias);
 }
 
 // ------------------------------------------------------------------ triangle gating
@@ -284,29 +318,54 @@ extern "C" int evo_gated_residual_fwd(const void* res, const void* y, int64_t y_
   return EVO_OK;
 }
 
+static int col_grid(int64_t rows, int64_t cols, dim3& grid, size_t& smem) {
+  if (cols % 8 || cols / 8 > 256) {
+    set_error("column reduction: cols must be a multiple of 8 and <= 2048 (got %lld)", (long long)cols);
+    return EVO_ERR_SHAPE;
+  }
+  const int tpr = (int)(cols / 8), rpi = 256 / tpr;
+  int64_t want = (rows + 8 * rpi - 1) / (8 * rpi);  // >= 8 row-iterations per CTA
+  int64_t cap = (int64_t)sm_count() * 2;
+  grid = dim3((unsigned)(want < 1 ? 1 : (want < cap ? want : cap)));
+  smem = (size_t)rpi * cols * sizeof(float);
+  return EVO_OK;
+}
+
 extern "C" int evo_gated_residual_bwd(const void* dout, const void* y, int64_t y_rs, const float* bias, const void* gp,
                                       int64_t gp_rs, void* dy, void* dgp, int64_t dgp_rs, float* dbias, int dtype,
                                       int64_t rows, int64_t cols, void* stream) {
   EVO_CHECK_ARG(dout, EVO_ERR_ARG, "gated_residual bwd: null dout");
   EVO_CHECK_ARG(!gp || (y && dgp), EVO_ERR_ARG, "gated_residual bwd: gp needs y and dgp");
-  EVO_CHECK_ARG(cols % 8 == 0, EVO_ERR_ALIGN, "gated_residual bwd: cols %% 8");
   if (rows == 0) return EVO_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  dim3 block(32, 8);
-  int64_t cchunks = cols / 8;
-  unsigned gx = (unsigned)((cchunks + 31) / 32);
-  int64_t gy = (rows + 63) / 64;
-  int64_t cap = (int64_t)sm_count() * 8 / gx;
-  if (cap < 1) cap = 1;
-  dim3 grid(gx, (unsigned)(gy < cap ? gy : cap));
+  dim3 grid;
+  size_t smem;
+  int rc = col_grid(rows, cols, grid, smem);
+  if (rc) return rc;
   if (dtype == EVO_BF16)
-    gated_residual_bwd_k<bf16><<<grid, block, 0, st>>>((const bf16*)dout, (const bf16*)y, y_rs, bias, (const bf16*)gp,
-                                                       gp_rs, (bf16*)dy, (bf16*)dgp, dgp_rs, dbias, rows, cols);
+    gated_residual_bwd_k<bf16><<<grid, 256, smem, st>>>((const bf16*)dout, (const bf16*)y, y_rs, bias,
+                                                        (const bf16*)gp, gp_rs, (bf16*)dy, (bf16*)dgp, dgp_rs, dbias,
+                                                        rows, cols);
   else
-    gated_residual_bwd_k<float><<<grid, block, 0, st>>>((const float*)dout, (const float*)y, y_rs, bias,
-                                                        (const float*)gp, gp_rs, (float*)dy, (float*)dgp, dgp_rs,
-                                                        dbias, rows, cols);
+    gated_residual_bwd_k<float><<<grid, 256, smem, st>>>((const float*)dout, (const float*)y, y_rs, bias,
+                                                         (const float*)gp, gp_rs, (float*)dy, (float*)dgp, dgp_rs,
+                                                         dbias, rows, cols);
   EVO_LAUNCH_CHECK("gated_residual bwd");
+  return EVO_OK;
+}
+
+extern "C" int evo_colsum(const void* x, int dtype, int64_t ld, int64_t rows, int64_t cols, float* out, void* stream) {
+  EVO_CHECK_ARG(x && out, EVO_ERR_ARG, "colsum: null pointer");
+  EVO_CHECK_ARG(ld % 8 == 0 && al16(x), EVO_ERR_ALIGN, "colsum: 16B-aligned rows required");
+  if (rows == 0) return EVO_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  dim3 grid;
+  size_t smem;
+  int rc = col_grid(rows, cols, grid, smem);
+  if (rc) return rc;
+  if (dtype == EVO_BF16) colsum_k<bf16><<<grid, 256, smem, st>>>((const bf16*)x, ld, rows, cols, out);
+  else colsum_k<float><<<grid, 256, smem, st>>>((const float*)x, ld, rows, cols, out);
+  EVO_LAUNCH_CHECK("colsum");
   return EVO_OK;
 }
 
@@ -326,20 +385,17 @@ extern "C" int evo_bias_act_fwd(void* y, const float* bias, int64_t rows, int64_
 extern "C" int evo_bias_act_bwd(const void* dh, const void* h, void* dy, float* dbias, int64_t rows, int64_t cols,
                                 int act, int dtype, void* stream) {
   EVO_CHECK_ARG(dh && dy && (act == 0 || h), EVO_ERR_ARG, "bias_act bwd: null pointer");
-  EVO_CHECK_ARG(cols % 8 == 0, EVO_ERR_ALIGN, "bias_act bwd: cols %% 8");
   if (rows == 0) return EVO_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  dim3 block(32, 8);
-  unsigned gx = (unsigned)((cols / 8 + 31) / 32);
-  int64_t gy = (rows + 63) / 64;
-  int64_t cap = (int64_t)sm_count() * 8 / gx;
-  if (cap < 1) cap = 1;
-  dim3 grid(gx, (unsigned)(gy < cap ? gy : cap));
+  dim3 grid;
+  size_t smem;
+  int rc = col_grid(rows, cols, grid, smem);
+  if (rc) return rc;
   if (dtype == EVO_BF16)
-    bias_act_bwd_k<bf16><<<grid, block, 0, st>>>((const bf16*)dh, (const bf16*)h, (bf16*)dy, dbias, rows, cols, act);
+    bias_act_bwd_k<bf16><<<grid, 256, smem, st>>>((const bf16*)dh, (const bf16*)h, (bf16*)dy, dbias, rows, cols, act);
   else
-    bias_act_bwd_k<float><<<grid, block, 0, st>>>((const float*)dh, (const float*)h, (float*)dy, dbias, rows, cols,
-                                                  act);
+    bias_act_bwd_k<float><<<grid, 256, smem, st>>>((const float*)dh, (const float*)h, (float*)dy, dbias, rows, cols,
+                                                   act);
   EVO_LAUNCH_CHECK("bias_act bwd");
   return EVO_OK;
 }

@@ -281,3 +281,12 @@ def bias_act_bwd(dh, h, rows, cols, dy=None, dbias=None, relu=True):
     call("evo_bias_act_bwd", _p(dh), _p(h), _p(dy), _p(dbias), rows, cols, 1 if relu else 0, _dt(dh),
          stream_handle())
     return dy
+
+
+def colsum(x, out, rows=None, cols=None, ld=None):
+    """out (fp32) += column sums of the 2-D view x [rows, cols] (row stride ld)."""
+    rows = x.shape[0] if rows is None else rows
+    cols = x.shape[-1] if cols is None else cols
+    ld = x.stride(0) if ld is None else ld
+    call("evo_colsum", _p(x), _dt(x), ld, rows, cols, _p(out), stream_handle())
+    return out

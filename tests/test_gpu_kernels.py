@@ -300,3 +300,12 @@ def test_count_nonfinite():
     x[3] = float("inf")
     x[500] = float("nan")
     assert ops.count_nonfinite(x) == 2
+
+
+@pytest.mark.parametrize("rows,cols", [(32768, 256), (65536, 128), (1000, 1024), (7, 392)])
+def test_colsum(rows, cols):
+    gen = torch.Generator(device=DEV).manual_seed(rows)
+    x = torch.randn(rows, cols, device=DEV, generator=gen).bfloat16()
+    out = torch.ones(cols, device=DEV)
+    ops.colsum(x, out)
+    assert rel(out - 1, x.float().sum(0)) < 1e-5
