@@ -118,7 +118,8 @@ int evo_gated_attention_fwd(const EvoAttnDesc* d, void* stream);
  * dg (gradient of the gate PRE-activation).  dbias is fp32 and ACCUMULATED at
  * dbias[b*s[0] + h*s[1] + i*s[2] + j*s[3]]; a zero stride reduces over that axis
  * (msa_row sums over sequences: s[0] = 0; per-key pair bias: s[2] = 0).
- * workspace: device scratch of evo_gated_attention_bwd_workspace(B, L, H, c) bytes. */
+ * workspace: device scratch of evo_gated_attention_bwd_workspace(B, L, H, c, batch_reduced)
+ * bytes, batch_reduced = (bias given and dbias_s[0] == 0 and dbias_s[2] != 0). */
 typedef struct EvoAttnBwdDesc {
   EvoAttnDesc f;
   const void* dout; int64_t do_sb, do_sl;
@@ -127,7 +128,7 @@ typedef struct EvoAttnBwdDesc {
   float* dbias; int64_t dbias_s[4];
   void* workspace; int64_t workspace_bytes;
 } EvoAttnBwdDesc;
-int64_t evo_gated_attention_bwd_workspace(int64_t B, int64_t L, int H, int c);
+int64_t evo_gated_attention_bwd_workspace(int64_t B, int64_t L, int H, int c, int bias_batch_reduced);
 int evo_gated_attention_bwd(const EvoAttnBwdDesc* d, void* stream);
 
 /* ------------------------------------------------------------------ batched GEMM (tcgen05)

@@ -63,7 +63,7 @@ _SIGS = {
     "evo_softmax_bwd": [vp, C.c_int, vp, C.c_int, vp, C.c_int, i64, i64, C.c_float, vp],
     "evo_gated_attention_fwd": [C.POINTER(EvoAttnDesc), vp],
     "evo_gated_attention_bwd": [C.POINTER(EvoAttnBwdDesc), vp],
-    "evo_gated_attention_bwd_workspace": [i64, i64, C.c_int, C.c_int],
+    "evo_gated_attention_bwd_workspace": [i64, i64, C.c_int, C.c_int, C.c_int],
     "evo_bgemm": [C.POINTER(EvoMat), C.POINTER(EvoMat), C.POINTER(EvoMat), i64, i64, i64, i64,
                   C.c_float, C.c_float, vp],
     "evo_tri_gate_fwd": [vp, i64, C.c_int, C.c_int, vp, vp, vp],
@@ -122,7 +122,7 @@ def check(rc: int) -> None:
 
 
 # kernels launched per C-ABI call (evo_gated_attention_bwd = memset + prep + main + finish)
-LAUNCHES = {"evo_gated_attention_bwd": 4}
+LAUNCHES = {"evo_gated_attention_bwd": 4}  # (+1 dbias reduce for msa_row; +0 memset when dQ partials)
 
 
 class Instrument:

@@ -124,7 +124,8 @@ def attention_bwd(bp: BlockParams, sv: Saved, dx_new):
         dbias, dbs = torch.zeros(B, nh, L, device=dev, dtype=F32), (nh * L, L, 0, 1)
     else:
         dbias, dbs = torch.zeros(nh, L, L, device=dev, dtype=F32), (0, L * L, L, 1)
-    ws = torch.empty(ops.attention_bwd_workspace(B, L, nh, c), device=dev, dtype=torch.uint8)
+    ws = torch.empty(ops.attention_bwd_workspace(B, L, nh, c, batch_reduced_bias=bias not in (None, "pair")),
+                     device=dev, dtype=torch.uint8)
     ops.attention_bwd(sv["desc"], S(dog, nh * c), S(dqkv, ldq, 0), S(dqkv, ldq, nh * c), S(dqkv, ldq, 2 * nh * c),
                       S(dgpre, nh * c), ws, dbias=dbias, dbias_s=dbs)
     if bias == "pair":

@@ -2,13 +2,14 @@
 // _attention_core, evoformer.py:173-198, for msa_row / msa_col / pair_row / pair_col).
 //
 // One CTA (4 warps, 128 threads) owns 128 queries of one (batch, head) and streams
-// the keys in tiles of 128 (flash-style online softmax, so N_r = 4096 never
-// materialises a logit matrix):
-//   S   = Q K^T                 tcgen05.mma M=128 N=128 K=16..64  -> TMEM (fp32)
+// the keys in tiles of 64 (flash-style online softmax, so N_r = 4096 never
+// materialises a logit matrix).  <= 128 registers, 64 TMEM columns and ~41 KB of
+// shared memory per CTA -> 4 CTAs (16 warps) per SM hide each other's latency:
+//   S   = Q K^T                 tcgen05.mma M=128 N=64 K=16..64   -> TMEM (fp32)
 //   s   = (S + bias) * scale    thread r owns query row r (tcgen05.ld 32x32b),
 //   p   = exp2(s - m)           running max / sum in registers (no shuffles)
 //   P  -> smem (bf16, canonical K-major, conflict-free 16-byte stores)
-//   O  += P V                   tcgen05.mma M=128 N=c K=128 -> TMEM -> registers
+//   O  += P V                   tcgen05.mma M=128 N=c K=64 -> TMEM -> registers
 // Epilogue: o = O / l, out = sigmoid(g) * o (gate on raw x, G2), log-sum-exp saved.
 // K/V tiles are double-buffered with cp.async; several CTAs per SM overlap the
 // MMA of one CTA with the softmax of another.
@@ -17,7 +18,7 @@
 namespace evo {
 
 constexpr int ATT_BQ = 128;
-constexpr int ATT_BK = 128;
+constexpr int ATT_BK = 64;   // keys per tile: S = 64 TMEM columns, P = 16 KB
 constexpr float LOG2E = 1.4426950408889634f;
 
 
@@ -31,18 +32,18 @@ struct AttnSmem {
   static constexpr uint32_t TOTAL = BIAS + 2 * ATT_BK * 4;
 };
 
-// rows x CP K-major tile from a strided [row][col] source (cols contiguous)
-template <int CP>
+// ROWS x CP K-major tile from a strided [row][col] source (cols contiguous)
+template <int CP, int ROWS>
 __device__ __forceinline__ void att_load_kmajor(uint32_t sdst, const bf16* base, int64_t row_stride, int row0,
                                                 int nrows_valid, int c) {
   constexpr int CPR = CP / 8;
 #pragma unroll
-  for (int it = 0; it < 128 * CPR / 128; ++it) {
+  for (int it = 0; it < ROWS * CPR / 128; ++it) {
     const int ch = threadIdx.x + it * 128;
     const int r = ch / CPR, d = (ch % CPR) * 8;
     const bool ok = (r < nrows_valid) && (d < c);
     const bf16* src = ok ? base + (int64_t)(row0 + r) * row_stride + d : base;
-    cp_async16(sdst + kmajor_off(r, d, 128), src, ok);
+    cp_async16(sdst + kmajor_off(r, d, ROWS), src, ok);
   }
 }
 // keys x CP tile stored MN-major over d (the PV B operand: N = d, K = key)
@@ -51,7 +52,7 @@ __device__ __forceinline__ void att_load_v(uint32_t sdst, const bf16* base, int6
                                            int nrows_valid, int c) {
   constexpr int CPR = CP / 8;
 #pragma unroll
-  for (int it = 0; it < 128 * CPR / 128; ++it) {
+  for (int it = 0; it < ATT_BK * CPR / 128; ++it) {
     const int ch = threadIdx.x + it * 128;
     const int r = ch / CPR, d = (ch % CPR) * 8;
     const bool ok = (r < nrows_valid) && (d < c);
@@ -61,7 +62,7 @@ __device__ __forceinline__ void att_load_v(uint32_t sdst, const bf16* base, int6
 }
 
 template <int CP>
-__global__ void __launch_bounds__(128) attn_fwd_kernel(AttnParams P) {
+__global__ void __launch_bounds__(128, CP == 32 ? 4 : 3) attn_fwd_kernel(AttnParams P) {
   using SM = AttnSmem<CP>;
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar_s, bar_o;
@@ -78,7 +79,7 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(AttnParams P) {
   const int qi = q0 + r;
   const bool per_key_bias = P.bias && P.bs2 == 0;
 
-  if (warp == 0) tmem_alloc(&tmem_sh, 128);
+  if (warp == 0) tmem_alloc(&tmem_sh, ATT_BK);
   if (threadIdx.x == 0) {
     mbar_init(&bar_s, 1);
     mbar_init(&bar_o, 1);
@@ -88,8 +89,8 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(AttnParams P) {
   const bf16* qb = P.q + b * P.q_sb + (int64_t)h * c;
   const bf16* kb = P.k + b * P.k_sb + (int64_t)h * c;
   const bf16* vb = P.v + b * P.v_sb + (int64_t)h * c;
-  att_load_kmajor<CP>(sb + SM::Q, qb, P.q_sl, q0, L - q0, c);
-  att_load_kmajor<CP>(sb + SM::KT, kb, P.k_sl, 0, L, c);
+  att_load_kmajor<CP, ATT_BQ>(sb + SM::Q, qb, P.q_sl, q0, L - q0, c);
+  att_load_kmajor<CP, ATT_BK>(sb + SM::KT, kb, P.k_sl, 0, L, c);
   att_load_v<CP>(sb + SM::VT, vb, P.v_sl, 0, L, c);
   cp_async_commit();
 
@@ -117,14 +118,15 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(AttnParams P) {
     if (per_key_bias) {
       const bf16* bp = P.bias + b * P.bs0 + (int64_t)h * P.bs1;
       const int kk = threadIdx.x;
-      sbias[st * ATT_BK + kk] = (k0 + kk < L) ? bf2f(bp[(int64_t)(k0 + kk) * P.bs3]) : 0.f;
+      if (kk < ATT_BK) sbias[st * ATT_BK + kk] = (k0 + kk < L) ? bf2f(bp[(int64_t)(k0 + kk) * P.bs3]) : 0.f;
     }
     cp_async_wait<0>();
     fence_async_smem();
     __syncthreads();
     // prefetch the next K/V tile into the other stage (its MMAs finished last iteration)
     if (j + 1 < nkt) {
-      att_load_kmajor<CP>(sb + SM::KT + (st ^ 1) * ATT_BK * CP * 2, kb, P.k_sl, k0 + ATT_BK, L - k0 - ATT_BK, c);
+      att_load_kmajor<CP, ATT_BK>(sb + SM::KT + (st ^ 1) * ATT_BK * CP * 2, kb, P.k_sl, k0 + ATT_BK,
+                                  L - k0 - ATT_BK, c);
       att_load_v<CP>(sb + SM::VT + (st ^ 1) * ATT_BK * CP * 2, vb, P.v_sl, k0 + ATT_BK, L - k0 - ATT_BK, c);
     }
     cp_async_commit();
@@ -192,7 +194,7 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(AttnParams P) {
         pv[e] = exp2f(s[kk + e] - mx);
         lsum += pv[e];
       }
-      st_shared_v4(prow + kmajor_off(r, kk, 128), pack_bf16x2(pv[0], pv[1]), pack_bf16x2(pv[2], pv[3]),
+      st_shared_v4(prow + kmajor_off(r, kk, ATT_BQ), pack_bf16x2(pv[0], pv[1]), pack_bf16x2(pv[2], pv[3]),
                    pack_bf16x2(pv[4], pv[5]), pack_bf16x2(pv[6], pv[7]));
     }
     l_run = l_run * corr + lsum;
@@ -262,7 +264,7 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(AttnParams P) {
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, 128);
+  if (warp == 0) tmem_dealloc(tmem, ATT_BK);
 }
 
 static bool a16(const void* p) { return ((uintptr_t)p & 15) == 0; }

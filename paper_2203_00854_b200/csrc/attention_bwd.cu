@@ -29,9 +29,39 @@ struct AttnBwdParams {
   bf16* dO;      // workspace [B][L][H*c]
   float* dQacc;  // workspace [B][L][H*c]
   float* Dsum;   // workspace [B][H][L]
+  bf16* dS;      // workspace [B][H][L][L] (batch-shared bias only) or null
   float scale;
   int64_t B;
 };
+
+// dbias[h][q][k] += sum_b dS[b][h][q][k]   (batch-shared bias: msa_row, evoformer.py:214)
+template <int VEC>
+__global__ void __launch_bounds__(256) attn_dbias_reduce(const bf16* __restrict__ dS, float* __restrict__ dbias,
+                                                         int64_t B, int H, int L, int64_t d1, int64_t d2, int64_t d3) {
+  const int64_t per = (int64_t)H * L * L;
+  const int64_t nv = per / VEC;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i * VEC;
+    float acc[VEC];
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) acc[k] = 0.f;
+    for (int64_t b = 0; b < B; ++b) {
+      if constexpr (VEC == 8) {
+        const uint4 u = *reinterpret_cast<const uint4*>(dS + b * per + e);
+        float t[8];
+        unpack_bf16x2(u.x, t[0], t[1]); unpack_bf16x2(u.y, t[2], t[3]);
+        unpack_bf16x2(u.z, t[4], t[5]); unpack_bf16x2(u.w, t[6], t[7]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] += t[k];
+      } else {
+        acc[0] += bf2f(dS[b * per + e]);
+      }
+    }
+    const int64_t h = e / ((int64_t)L * L), q = (e / L) % L, k = e % L;
+#pragma unroll
+    for (int t = 0; t < VEC; ++t) dbias[h * d1 + q * d2 + (k + t) * d3] += acc[t];
+  }
+}
 
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
   uint32_t* r = reinterpret_cast<uint32_t*>(v);
@@ -93,7 +123,7 @@ __global__ void __launch_bounds__(256) attn_bwd_prep(AttnBwdParams P, int64_t B)
 constexpr int BW_BK = 128;  // keys per CTA
 constexpr int BW_BQ = 128;  // queries per iteration
 
-template <int CP, bool RED>
+template <int CP>
 struct BwdSmem {
   static constexpr uint32_t K = 0;                          // [key][d] K-major
   static constexpr uint32_t V = K + BW_BK * CP * 2;         // [key][d] K-major
@@ -104,8 +134,7 @@ struct BwdSmem {
   static constexpr uint32_t LSE = DST + BW_BK * BW_BQ * 2;  // fp32 [128]
   static constexpr uint32_t DD = LSE + BW_BQ * 4;           // fp32 [128]
   static constexpr uint32_t KB = DD + BW_BQ * 4;            // fp32 [2][128] per-key dbias partials
-  static constexpr uint32_t RB = KB + 2 * BW_BK * 4;        // fp32 [2 qtiles][128 keys][128 q] (RED only)
-  static constexpr uint32_t TOTAL = RB + (RED ? 2 * BW_BK * BW_BQ * 4 : 0);
+  static constexpr uint32_t TOTAL = KB + 2 * BW_BK * 4;
 };
 
 template <int CP>
@@ -120,11 +149,13 @@ __device__ __forceinline__ void bw_load(uint32_t sdst, const bf16* base, int64_t
   }
 }
 
-// RED: the bias is shared over the batch (msa_row, dbias stride 0 on b) and L <= 256:
-//      dbias is reduced over the CTA's batch group in shared memory, flushed once.
-template <int CP, bool RED>
-__global__ void __launch_bounds__(256, 1) attn_bwd_kernel(AttnBwdParams P, int G, int dq_partial) {
-  using SM = BwdSmem<CP, RED>;
+// <= 128 registers, 256 TMEM columns, ~98 KB smem -> 2 CTAs (16 warps) per SM.
+// A batch-shared bias (msa_row: dbias stride 0 over b) is handled by writing the
+// scaled dS (bf16) per batch and reducing over batches in attn_dbias_reduce
+// (deterministic, no atomics).
+template <int CP>
+__global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int G, int dq_partial) {
+  using SM = BwdSmem<CP>;
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar1, bar2;
   __shared__ uint32_t tmem_sh;
@@ -132,7 +163,6 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_kernel(AttnBwdParams P, int G
   float* s_lse = reinterpret_cast<float*>(smem + SM::LSE);
   float* s_D = reinterpret_cast<float*>(smem + SM::DD);
   float* s_kb = reinterpret_cast<float*>(smem + SM::KB);
-  float* s_red = reinterpret_cast<float*>(smem + SM::RB);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wq = warp & 3, wg = warp >> 2;
@@ -148,6 +178,7 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_kernel(AttnBwdParams P, int G
   const bool kvalid = kj < L;
   const bool per_key_bias = F.bias && F.bs2 == 0;
   const bool db_per_key = P.dbias && P.db2 == 0;
+  const bool db_store = P.dbias && P.dS != nullptr;  // batch-shared full bias -> dS workspace
   const int nqt = (L + BW_BQ - 1) / BW_BQ;
   const int nkt = gridDim.x;
   const float LOG2E_ = 1.4426950408889634f;
@@ -157,9 +188,6 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_kernel(AttnBwdParams P, int G
     mbar_init(&bar1, 1);
     mbar_init(&bar2, 1);
     fence_mbar_init();
-  }
-  if (RED) {
-    for (int i = threadIdx.x; i < 2 * BW_BK * BW_BQ; i += 256) s_red[i] = 0.f;
   }
   const int64_t HC = (int64_t)H * c;
   auto issue_loads = [&](int64_t b, int qt, bool with_kv) {
@@ -201,6 +229,7 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_kernel(AttnBwdParams P, int G
     if (F.bias && !per_key_bias && kvalid) bias_col = F.bias + b * F.bs0 + (int64_t)h * F.bs1 + (int64_t)kj * F.bs3;
     float* dbias_col = nullptr;
     if (P.dbias && kvalid) dbias_col = P.dbias + b * P.db0 + (int64_t)h * P.db1 + (int64_t)kj * P.db3;
+    bf16* ds_col = db_store && kvalid ? P.dS + ((b * H + h) * (int64_t)L) * L + kj : nullptr;
 
     for (int qt = 0; qt < nqt; ++qt, ++it) {
       const int q0 = qt * BW_BQ;
@@ -224,15 +253,15 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_kernel(AttnBwdParams P, int G
 
       float kb_acc = 0.f;
 #pragma unroll 1
-      for (int half = 0; half < 2; ++half) {
-        const int qc = wg * 64 + half * 32;  // query column offset inside the tile
-        float s[32], dp[32];
-        tmem_ld32(t_lane + T_S + qc, s);
-        tmem_ld32(t_lane + T_DP + qc, dp);
+      for (int part = 0; part < 4; ++part) {
+        const int qc = wg * 64 + part * 16;  // query column offset inside the tile
+        float s[16], dp[16];
+        tmem_ld16(t_lane + T_S + qc, s);
+        tmem_ld16(t_lane + T_DP + qc, dp);
         tmem_ld_wait();
-        float pv[32], dsv[32];
+        float pv[16], dsv[16];
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
+        for (int e = 0; e < 16; ++e) {
           const int ql = qc + e, qq = q0 + ql;
           float x = s[e] + kbias;
           if (bias_col && qq < L) x += bf2f(bias_col[(int64_t)qq * F.bs2]);
@@ -242,24 +271,20 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_kernel(AttnBwdParams P, int G
           pv[e] = p;
           dsv[e] = ds;
         }
-        if (RED) {
-          float* r = s_red + (qt * BW_BK + kr) * BW_BQ + qc;
+        if (ds_col) {
 #pragma unroll
-          for (int e = 0; e < 32; e += 4) {
-            float4 o = *reinterpret_cast<float4*>(r + e);
-            o.x += dsv[e]; o.y += dsv[e + 1]; o.z += dsv[e + 2]; o.w += dsv[e + 3];
-            *reinterpret_cast<float4*>(r + e) = o;
-          }
+          for (int e = 0; e < 16; ++e)
+            if (q0 + qc + e < L) ds_col[(int64_t)(q0 + qc + e) * L] = f2bf(P.scale * dsv[e]);
         } else if (db_per_key) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) kb_acc += dsv[e];
+          for (int e = 0; e < 16; ++e) kb_acc += dsv[e];
         } else if (dbias_col) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e)
+          for (int e = 0; e < 16; ++e)
             if (q0 + qc + e < L) atomicAdd(dbias_col + (int64_t)(q0 + qc + e) * P.db2, P.scale * dsv[e]);
         }
 #pragma unroll
-        for (int e = 0; e < 32; e += 8) {
+        for (int e = 0; e < 16; e += 8) {
           st_shared_v4(sb + SM::PT + kmajor_off(kr, qc + e, 128), pack_bf16x2(pv[e], pv[e + 1]),
                        pack_bf16x2(pv[e + 2], pv[e + 3]), pack_bf16x2(pv[e + 4], pv[e + 5]),
                        pack_bf16x2(pv[e + 6], pv[e + 7]));
@@ -299,19 +324,19 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_kernel(AttnBwdParams P, int G
       const bool last_q = qt + 1 == nqt;
       if (!(last_q && b + 1 == b_end)) issue_loads(last_q ? b + 1 : b, last_q ? 0 : qt + 1, last_q);
       {
-        float v[CP];
-        if constexpr (CP == 16) tmem_ld16(t_lane + (wg == 0 ? T_DV : T_DK), v);
-        else {
 #pragma unroll
-          for (int cc = 0; cc < CP; cc += 32) tmem_ld32(t_lane + (wg == 0 ? T_DV : T_DK) + cc, v + cc);
+        for (int cc = 0; cc < CP; cc += 16) {
+          float v[16];
+          tmem_ld16(t_lane + (wg == 0 ? T_DV : T_DK) + cc, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) acc[cc + e] += v[e];
         }
         float w[CP / 2];
         if constexpr (CP == 16) tmem_ld8(t_lane + T_DQ + wg * 8, w);
         else if constexpr (CP == 32) tmem_ld16(t_lane + T_DQ + wg * 16, w);
         else tmem_ld32(t_lane + T_DQ + wg * 32, w);
         tmem_ld_wait();
-#pragma unroll
-        for (int d = 0; d < CP; ++d) acc[d] += v[d];
         const int qq = q0 + kr;  // dQ: TMEM lane = query row
         if (qq < L) {
           if (dq_partial) {
@@ -355,17 +380,6 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_kernel(AttnBwdParams P, int G
       }
     }
   }
-  if (RED && P.dbias) {
-    // flush the batch-group sums: thread (kr, wg) owns keys kr, queries [wg*64, wg*64+64) of each tile
-    if (kvalid) {
-      float* col = P.dbias + (int64_t)h * P.db1 + (int64_t)kj * P.db3;
-      for (int qt = 0; qt < nqt; ++qt)
-        for (int e = 0; e < 64; ++e) {
-          const int ql = wg * 64 + e, qq = qt * BW_BQ + ql;
-          if (qq < L) atomicAdd(col + (int64_t)qq * P.db2, P.scale * s_red[(qt * BW_BK + kr) * BW_BQ + ql]);
-        }
-    }
-  }
   (void)nkt;
   tc_fence_before();
   __syncthreads();
@@ -397,55 +411,49 @@ __global__ void __launch_bounds__(256) attn_bwd_dq_finish(AttnBwdParams P, int64
 
 constexpr int DQ_MAX_PARTS = 4;  // <= 4 key tiles (L <= 512): per-tile dQ partials, plain stores
 
-static int64_t ws_layout(int64_t B, int64_t L, int H, int c, int64_t* off_dq, int64_t* off_D) {
+static int64_t ws_layout(int64_t B, int64_t L, int H, int c, int bias_batch_reduced, int64_t* off_dq, int64_t* off_D,
+                         int64_t* off_dS) {
   const int64_t n = B * L * (int64_t)H * c;
   const int64_t nkt = (L + BW_BK - 1) / BW_BK;
   const int64_t parts = nkt <= DQ_MAX_PARTS ? nkt : 1;
   int64_t o1 = ((n * 2 + 255) / 256) * 256;
   int64_t o2 = o1 + ((parts * n * 4 + 255) / 256) * 256;
+  int64_t o3 = o2 + ((B * H * L * 4 + 255) / 256) * 256;
   if (off_dq) *off_dq = o1;
   if (off_D) *off_D = o2;
-  return o2 + ((B * H * L * 4 + 255) / 256) * 256;
+  if (off_dS) *off_dS = o3;
+  return o3 + (bias_batch_reduced ? ((B * H * L * L * 2 + 255) / 256) * 256 : 0);
 }
 
 int sm_count();
 
-template <int CP, bool RED>
-static int launch_bwd(AttnBwdParams& p, int64_t B, int G, int dq_partial, cudaStream_t st) {
-  using SM = BwdSmem<CP, RED>;
+template <int CP>
+static int launch_bwd(AttnBwdParams& p, int64_t B, int dq_partial, cudaStream_t st) {
+  using SM = BwdSmem<CP>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel<CP, RED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel<CP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)SM::TOTAL);
     if (e != cudaSuccess) return cuda_status(e, "attn bwd attr");
     attr = true;
   }
-  dim3 grid((unsigned)((p.f.L + BW_BK - 1) / BW_BK), (unsigned)p.f.H, (unsigned)((B + G - 1) / G));
-  attn_bwd_kernel<CP, RED><<<grid, 256, SM::TOTAL, st>>>(p, G, dq_partial);
-  EVO_LAUNCH_CHECK("attention bwd main");
-  return EVO_OK;
-}
-
-template <int CP>
-static int launch_bwd_cp(AttnBwdParams& p, int64_t B, int dq_partial, cudaStream_t st) {
   const int64_t nkt = (p.f.L + BW_BK - 1) / BW_BK;
   const int64_t units = B * p.f.H * nkt;
-  // batch-shared bias (msa_row) with L <= 256: reduce dbias over a batch group in smem
-  const bool red = p.dbias && p.db0 == 0 && p.db2 != 0 && p.f.L <= 2 * BW_BQ;
-  const int64_t ctas_per_sm = red ? 1 : 2;
-  int64_t G = units / ((int64_t)sm_count() * ctas_per_sm * 2);  // ~2 waves
+  int64_t G = units / ((int64_t)sm_count() * 2 * 2);  // ~2 waves at 2 CTAs/SM
   if (G < 1) G = 1;
   if (G > 16) G = 16;
-  if (red) return launch_bwd<CP, true>(p, B, (int)G, dq_partial, st);
-  return launch_bwd<CP, false>(p, B, (int)G, dq_partial, st);
+  dim3 grid((unsigned)nkt, (unsigned)p.f.H, (unsigned)((B + G - 1) / G));
+  attn_bwd_kernel<CP><<<grid, 256, SM::TOTAL, st>>>(p, (int)G, dq_partial);
+  EVO_LAUNCH_CHECK("attention bwd main");
+  return EVO_OK;
 }
 
 }  // namespace evo
 
 using namespace evo;
 
-extern "C" int64_t evo_gated_attention_bwd_workspace(int64_t B, int64_t L, int H, int c) {
-  return ws_layout(B, L, H, c, nullptr, nullptr);
+extern "C" int64_t evo_gated_attention_bwd_workspace(int64_t B, int64_t L, int H, int c, int bias_batch_reduced) {
+  return ws_layout(B, L, H, c, bias_batch_reduced, nullptr, nullptr, nullptr);
 }
 
 extern "C" int evo_gated_attention_bwd(const EvoAttnBwdDesc* d, void* stream) {
@@ -457,8 +465,9 @@ extern "C" int evo_gated_attention_bwd(const EvoAttnBwdDesc* d, void* stream) {
                 "attention bwd: null pointer (o_raw, lse, dout, dq, dk, dv, dg, workspace are required)");
   const int64_t B = d->f.B, L = d->f.L;
   const int H = d->f.H, c = d->f.c;
-  int64_t off_dq, off_D;
-  const int64_t need = ws_layout(B, L, H, c, &off_dq, &off_D);
+  int64_t off_dq, off_D, off_dS;
+  const int batch_reduced = d->dbias && d->f.bias && d->dbias_s[0] == 0 && d->dbias_s[2] != 0;
+  const int64_t need = ws_layout(B, L, H, c, batch_reduced, &off_dq, &off_D, &off_dS);
   EVO_CHECK_ARG(d->workspace_bytes >= need, EVO_ERR_ARG, "attention bwd: workspace %lld < %lld bytes",
                 (long long)d->workspace_bytes, (long long)need);
   const int64_t strides[] = {d->do_sb, d->do_sl, d->dq_sb, d->dq_sl, d->dk_sb, d->dk_sl, d->dv_sb, d->dv_sl,
@@ -475,6 +484,7 @@ extern "C" int evo_gated_attention_bwd(const EvoAttnBwdDesc* d, void* stream) {
   p.dO = (bf16*)ws;
   p.dQacc = (float*)(ws + off_dq);
   p.Dsum = (float*)(ws + off_D);
+  p.dS = batch_reduced ? (bf16*)(ws + off_dS) : nullptr;
   p.scale = d->f.scale;
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t nkt = (L + BW_BK - 1) / BW_BK;
@@ -486,10 +496,19 @@ extern "C" int evo_gated_attention_bwd(const EvoAttnBwdDesc* d, void* stream) {
   }
   attn_bwd_prep<<<(unsigned)((B * L + 7) / 8), 256, 0, st>>>(p, B);
   EVO_LAUNCH_CHECK("attention bwd prep");
-  if (c <= 16) rc = launch_bwd_cp<16>(p, B, dq_partial, st);
-  else if (c <= 32) rc = launch_bwd_cp<32>(p, B, dq_partial, st);
-  else rc = launch_bwd_cp<64>(p, B, dq_partial, st);
+  if (c <= 16) rc = launch_bwd<16>(p, B, dq_partial, st);
+  else if (c <= 32) rc = launch_bwd<32>(p, B, dq_partial, st);
+  else rc = launch_bwd<64>(p, B, dq_partial, st);
   if (rc) return rc;
+  if (batch_reduced) {
+    const int vec = L % 8 == 0 ? 8 : 1;
+    int64_t nv = (int64_t)H * L * L / vec;
+    int64_t g2 = (nv + 255) / 256, cap2 = (int64_t)sm_count() * 8;
+    unsigned g2u = (unsigned)(g2 < cap2 ? g2 : cap2);
+    if (vec == 8) attn_dbias_reduce<8><<<g2u, 256, 0, st>>>(p.dS, p.dbias, B, H, L, p.db1, p.db2, p.db3);
+    else attn_dbias_reduce<1><<<g2u, 256, 0, st>>>(p.dS, p.dbias, B, H, L, p.db1, p.db2, p.db3);
+    EVO_LAUNCH_CHECK("attention bwd dbias reduce");
+  }
   int64_t n8 = B * L * H * c / 8;
   int64_t g = (n8 + 255) / 256, cap = (int64_t)sm_count() * 16;
   attn_bwd_dq_finish<<<(unsigned)(g < cap ? g : cap), 256, 0, st>>>(p, B, dq_partial ? (int)nkt : 1);

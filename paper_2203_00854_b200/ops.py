@@ -188,8 +188,8 @@ def attention_fwd(desc: EvoAttnDesc):
     call("evo_gated_attention_fwd", C.byref(desc), stream_handle(), work=_attn_work(desc))
 
 
-def attention_bwd_workspace(B, L, H, c) -> int:
-    return int(_lib.load().evo_gated_attention_bwd_workspace(B, L, H, c))
+def attention_bwd_workspace(B, L, H, c, batch_reduced_bias=False) -> int:
+    return int(_lib.load().evo_gated_attention_bwd_workspace(B, L, H, c, int(batch_reduced_bias)))
 
 
 def attention_bwd(fdesc: EvoAttnDesc, dout: Strided, dq: Strided, dk: Strided, dv: Strided, dg: Strided,

@@ -228,7 +228,7 @@ def test_attention_fwd_bwd(L, c, H, mode):
         dbias_s = (H * L, L, 0, 1)
     else:
         dbias, dbias_s = None, (0, 0, 0, 0)
-    ws = torch.empty(ops.attention_bwd_workspace(B, L, H, c), dtype=torch.uint8, device=DEV)
+    ws = torch.empty(ops.attention_bwd_workspace(B, L, H, c, mode == "full"), dtype=torch.uint8, device=DEV)
     ops.attention_bwd(d, Strided(dout, L * H * c, H * c), Strided(dqkv, L * ld, ld, 0),
                       Strided(dqkv, L * ld, ld, H * c), Strided(dqkv, L * ld, ld, 2 * H * c),
                       Strided(dgp, L * H * c, H * c), ws, dbias=dbias, dbias_s=dbias_s)
