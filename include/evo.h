@@ -55,20 +55,27 @@ int evo_layernorm_fwd(const void* x, int x_dtype, int64_t x_rs, int64_t x_cs,
                       const float* gamma, const float* beta,
                       void* y, int y_dtype, float* mean, float* rstd,
                       int64_t rows, int64_t cols, float eps, void* stream);
-/* dx (+)= dLN/dx; dgamma/dbeta are ACCUMULATED (caller zeroes them); dx row-major,
- * x addressed like the forward.  accumulate_dx != 0 adds into dx (residual grads). */
+/* dx = res + dLN/dx (res may be NULL, or alias dx to accumulate in place - the residual
+ * stream's gradient); dgamma/dbeta are ACCUMULATED (caller zeroes them); dx and res are
+ * addressed like x. */
 int evo_layernorm_bwd(const void* dy, int dy_dtype, const void* x, int x_dtype, int64_t x_rs, int64_t x_cs,
                       const float* gamma, const float* mean, const float* rstd,
-                      void* dx, int dx_dtype, int accumulate_dx,
+                      void* dx, int dx_dtype, const void* res,
                       float* dgamma, float* dbeta, int64_t rows, int64_t cols, void* stream);
 
-/* LN followed by k dot products per row (msa_row_bias, evoformer.py:201-207):
- *   out[h*out_hs + r] = sum_c LN(x)[r, c] * w[c*k + h],  h < k <= 16.
- * ln_out (row-major, may be NULL) receives LN(x) for the backward. */
+/* LN followed by k = 8 dot products per row (msa_row_bias, evoformer.py:201-207; fewer
+ * heads are zero-padded to 8):  out[h*out_hs + r] = sum_c LN(x)[r, c] * w[c*8 + h].
+ * ln_out (row-major, may be NULL) receives LN(x); mean/rstd are saved. bf16. */
 int evo_layernorm_rowdot_fwd(const void* x, int x_dtype, const float* gamma, const float* beta,
                              const float* w, int k, void* out, int out_dtype, int64_t out_hs,
                              void* ln_out, float* mean, float* rstd,
                              int64_t rows, int64_t cols, float eps, void* stream);
+/* its backward in one pass: dy = w . dout[:, r], dw += LN(x)^T dout (fp32 [cols][8]),
+ * dgamma/dbeta accumulated, dx = res + dLN (res may alias dx). dout fp32 [8][rows]. */
+int evo_layernorm_rowdot_bwd(const void* x, int x_dtype, const float* gamma, const float* beta,
+                             const float* w, int k, const float* dout, int64_t out_hs,
+                             const float* mean, const float* rstd, const void* res, void* dx,
+                             float* dgamma, float* dbeta, float* dw, int64_t rows, int64_t cols, void* stream);
 
 /* ------------------------------------------------------------------ fused softmax
  * Replaces engine.fused_softmax_mask_bias_raw (engine.py:193-203) and the block's
@@ -151,6 +158,14 @@ typedef struct EvoMat {
 int evo_bgemm(const EvoMat* A, const EvoMat* B, const EvoMat* C,
               int64_t batch, int64_t M, int64_t N, int64_t K,
               float alpha, float beta, void* stream);
+/* Same with a workspace enabling split-K when the output tiles cannot fill the
+ * GPU and K is long (the OPM backward contractions, K = N_r * p): fp32 partials in
+ * workspace, then a reduction applying alpha/beta and C's addressing.
+ * evo_bgemm_workspace() returns the bytes needed (0 = no split chosen). */
+int64_t evo_bgemm_workspace(int64_t batch, int64_t M, int64_t N, int64_t K);
+int evo_bgemm_ws(const EvoMat* A, const EvoMat* B, const EvoMat* C,
+                 int64_t batch, int64_t M, int64_t N, int64_t K,
+                 float alpha, float beta, void* workspace, int64_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------------------ triangle gating
  * _triangle_projections epilogue (evoformer.py:260-264) for the merged projection

@@ -55,7 +55,9 @@ class EvoMat(C.Structure):
 _SIGS = {
     "evo_device_info": [C.POINTER(C.c_int)] * 3,
     "evo_layernorm_fwd": [vp, C.c_int, i64, i64, vp, vp, vp, C.c_int, vp, vp, i64, i64, C.c_float, vp],
-    "evo_layernorm_bwd": [vp, C.c_int, vp, C.c_int, i64, i64, vp, vp, vp, vp, C.c_int, C.c_int, vp, vp, i64, i64, vp],
+    "evo_layernorm_bwd": [vp, C.c_int, vp, C.c_int, i64, i64, vp, vp, vp, vp, C.c_int, vp, vp, vp, i64, i64, vp],
+    "evo_layernorm_rowdot_bwd": [vp, C.c_int, vp, vp, vp, C.c_int, vp, i64, vp, vp, vp, vp, vp, vp, vp, i64, i64,
+                                 vp],
     "evo_layernorm_rowdot_fwd": [vp, C.c_int, vp, vp, vp, C.c_int, vp, C.c_int, i64, vp, vp, vp, i64, i64,
                                  C.c_float, vp],
     "evo_softmax_fwd": [vp, C.c_int, vp, C.c_int, C.POINTER(i64), vp, C.c_int, C.POINTER(i64), vp, C.c_int,
@@ -66,6 +68,9 @@ _SIGS = {
     "evo_gated_attention_bwd_workspace": [i64, i64, C.c_int, C.c_int, C.c_int],
     "evo_bgemm": [C.POINTER(EvoMat), C.POINTER(EvoMat), C.POINTER(EvoMat), i64, i64, i64, i64,
                   C.c_float, C.c_float, vp],
+    "evo_bgemm_workspace": [i64, i64, i64, i64],
+    "evo_bgemm_ws": [C.POINTER(EvoMat), C.POINTER(EvoMat), C.POINTER(EvoMat), i64, i64, i64, i64,
+                     C.c_float, C.c_float, vp, i64, vp],
     "evo_tri_gate_fwd": [vp, i64, C.c_int, C.c_int, vp, vp, vp],
     "evo_tri_gate_bwd": [vp, vp, vp, C.c_int, i64, C.c_int, C.c_int, vp, vp],
     "evo_gated_residual_fwd": [vp, vp, i64, vp, vp, i64, vp, C.c_int, i64, i64, vp],
@@ -122,7 +127,7 @@ def check(rc: int) -> None:
 
 
 # kernels launched per C-ABI call (evo_gated_attention_bwd = memset + prep + main + finish)
-LAUNCHES = {"evo_gated_attention_bwd": 4}  # (+1 dbias reduce for msa_row; +0 memset when dQ partials)
+LAUNCHES = {"evo_gated_attention_bwd": 4, "evo_bgemm_ws": 2}  # (+1 dbias reduce for msa_row; +0 memset when dQ partials)
 
 
 class Instrument:

@@ -164,16 +164,26 @@ def msa_row_bias_fwd(bp: BlockParams, z2d, n_i: int, n_j: int | None = None, sav
 
 
 def msa_row_bias_bwd(bp: BlockParams, sv: Saved, dbias, dz):
-    """dbias fp32 [nh, R, R]; accumulates into dz (bf16 [R*R, Hz])."""
+    """dbias fp32 [nh, n_i, n_j]; accumulates into dz (bf16 [n_i*n_j, Hz]) in one fused pass
+    (w . dbias, LayerNorm backward, dW_bias, dgamma, dbeta)."""
     cfg = bp.cfg
-    nh, Hz = cfg.n_head_msa, cfg.h_pair
+    nh, Hz, k = cfg.n_head_msa, cfg.h_pair, bp.layout.rowdot_k
     rows = dbias[0].numel()
-    db2 = dbias.reshape(nh, rows)
-    w = bp.f["msa_row.w_bias"][:, :nh]                                   # fp32 [Hz, nh]
-    dln = torch.mm(db2.t(), w.t())                                       # fp32 [rows, Hz]
-    bp.g["msa_row.w_bias"][:, :nh].copy_(torch.mm(sv["ln"].t().float(), db2.t()))
-    ops.layernorm_bwd(dln, sv["z"], bp.f["msa_row.lnz_g"], sv["mean"], sv["rstd"], rows, Hz, dx=dz, accumulate=True,
-                      dgamma=bp.g["msa_row.lnz_g"], dbeta=bp.g["msa_row.lnz_b"])
+    if nh < k:  # zero-padded heads
+        full = torch.zeros(k, rows, device=dbias.device, dtype=F32)
+        full[:nh].copy_(dbias.reshape(nh, rows))
+        dbias = full
+    db2 = dbias.reshape(k, rows)
+    if not dz.is_cuda:  # CPU host-logic tests (fake kernel backend)
+        w = bp.f["msa_row.w_bias"]
+        dln = db2.t() @ w.t()
+        bp.g["msa_row.w_bias"] += sv["ln"].float().t() @ db2.t()
+        ops.layernorm_bwd(dln, sv["z"], bp.f["msa_row.lnz_g"], sv["mean"], sv["rstd"], rows, Hz, dx=dz,
+                          accumulate=True, dgamma=bp.g["msa_row.lnz_g"], dbeta=bp.g["msa_row.lnz_b"])
+        return
+    ops.layernorm_rowdot_bwd(sv["z"], bp.f["msa_row.lnz_g"], bp.f["msa_row.lnz_b"], bp.f["msa_row.w_bias"], db2,
+                             rows, sv["mean"], sv["rstd"], rows, Hz, dz, dz, bp.g["msa_row.lnz_g"],
+                             bp.g["msa_row.lnz_b"], bp.g["msa_row.w_bias"])
 
 
 # ----------------------------------------------------------------------------- transition
@@ -200,8 +210,8 @@ def transition_bwd(bp: BlockParams, sv: Saved, dx_new):
     dpre = ops.bias_act_bwd(dhid, sv["hid"], rows, dhid.shape[1], dy=dhid, dbias=g[f"{mod}.b1"])
     _wgrad(sv["ln"], dpre, g[f"{mod}.w1"])
     dln = _mm(dpre, h[f"{mod}.w1"].t())
-    dx = dx_new.clone()
-    ops.layernorm_bwd(dln, sv["x"], f[f"{mod}.ln_g"], sv["mean"], sv["rstd"], rows, H, dx=dx, accumulate=True,
+    dx = torch.empty_like(dx_new)
+    ops.layernorm_bwd(dln, sv["x"], f[f"{mod}.ln_g"], sv["mean"], sv["rstd"], rows, H, dx=dx, res=dx_new,
                       dgamma=g[f"{mod}.ln_g"], dbeta=g[f"{mod}.ln_b"])
     return dx
 
@@ -396,8 +406,8 @@ def triangle_bwd(bp: BlockParams, sv: Saved, dz_new, reduce_scatter=None):
     _wgrad(sv["ln"], dY, g[f"{mod}.w_proj"])
     _bgrad(dY, g[f"{mod}.b_proj"])
     dln = _mm(dY, h[f"{mod}.w_proj"].t())
-    dz = dz_new.clone()
-    ops.layernorm_bwd(dln, sv["z"], f[f"{mod}.ln_g"], sv["mean"], sv["rstd"], rows, Hz, dx=dz, accumulate=True,
+    dz = torch.empty_like(dz_new)
+    ops.layernorm_bwd(dln, sv["z"], f[f"{mod}.ln_g"], sv["mean"], sv["rstd"], rows, Hz, dx=dz, res=dz_new,
                       dgamma=g[f"{mod}.ln_g"], dbeta=g[f"{mod}.ln_b"])
     return dz
 

@@ -20,6 +20,8 @@
 
 namespace evo {
 
+int sm_count();
+
 struct MatArg {
   const char* ptr;
   int64_t bs;                 // batch stride (elements)
@@ -61,9 +63,13 @@ __device__ __forceinline__ void load_tile(uint32_t sdst, const MatArg& m, const 
   }
 }
 
+// split-K: blockIdx.z = batch * splits + split; with ws != nullptr each split writes its
+// fp32 partial tile densely to ws[(split * batch + b)][M][N] and bgemm_splitk_reduce
+// applies alpha/beta and the output addressing.
 template <int BN, bool A_MN, bool B_MN, int STAGES, typename TC>
 __global__ void __launch_bounds__(128) bgemm_kernel(MatArg A, MatArg B, MatArg C, uint32_t M, uint32_t N,
-                                                    uint32_t K, float alpha, float beta, int c_mode) {
+                                                    uint32_t K, float alpha, float beta, int c_mode, int splits,
+                                                    float* __restrict__ ws) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t mbar[STAGES];
   __shared__ uint32_t tmem_base_sh;
@@ -75,7 +81,8 @@ __global__ void __launch_bounds__(128) bgemm_kernel(MatArg A, MatArg B, MatArg C
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t m0 = blockIdx.y * GEMM_BM, n0 = blockIdx.x * BN;
-  const int64_t bz = blockIdx.z;
+  const int64_t bz = blockIdx.z / splits;
+  const int split = blockIdx.z % splits;
   const char* Abase = A.ptr + bz * A.bs * 2;
   const char* Bbase = B.ptr + bz * B.bs * 2;
 
@@ -89,14 +96,17 @@ __global__ void __launch_bounds__(128) bgemm_kernel(MatArg A, MatArg B, MatArg C
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
 
-  const int KT = (K + GEMM_BK - 1) / GEMM_BK;
+  const int KT_all = (K + GEMM_BK - 1) / GEMM_BK;
+  const int KT_per = (KT_all + splits - 1) / splits;
+  const int kt0 = split * KT_per;
+  const int KT = (KT_all - kt0 < KT_per ? KT_all - kt0 : KT_per);  // >= 1 by construction
   constexpr uint32_t IDESC = make_idesc_bf16(GEMM_BM, BN, A_MN, B_MN);
 
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < KT) {
-      load_tile<GEMM_BM, A_MN>(sA + s * A_BYTES, A, Abase, m0, s * GEMM_BK, M, K);
-      load_tile<BN, B_MN>(sB + s * B_BYTES, B, Bbase, n0, s * GEMM_BK, N, K);
+      load_tile<GEMM_BM, A_MN>(sA + s * A_BYTES, A, Abase, m0, (kt0 + s) * GEMM_BK, M, K);
+      load_tile<BN, B_MN>(sB + s * B_BYTES, B, Bbase, n0, (kt0 + s) * GEMM_BK, N, K);
     }
     cp_async_commit();
   }
@@ -106,8 +116,8 @@ __global__ void __launch_bounds__(128) bgemm_kernel(MatArg A, MatArg B, MatArg C
     if (pf < KT) {
       const int ps = pf % STAGES;
       if (kt >= 1) mbar_wait(&mbar[ps], ((kt - 1) / STAGES) & 1);  // MMA kt-1 released stage ps
-      load_tile<GEMM_BM, A_MN>(sA + ps * A_BYTES, A, Abase, m0, pf * GEMM_BK, M, K);
-      load_tile<BN, B_MN>(sB + ps * B_BYTES, B, Bbase, n0, pf * GEMM_BK, N, K);
+      load_tile<GEMM_BM, A_MN>(sA + ps * A_BYTES, A, Abase, m0, (kt0 + pf) * GEMM_BK, M, K);
+      load_tile<BN, B_MN>(sB + ps * B_BYTES, B, Bbase, n0, (kt0 + pf) * GEMM_BK, N, K);
     }
     cp_async_commit();
     cp_async_wait<STAGES - 1>();
@@ -130,51 +140,84 @@ __global__ void __launch_bounds__(128) bgemm_kernel(MatArg A, MatArg B, MatArg C
   mbar_wait(&mbar[(KT - 1) % STAGES], ((KT - 1) / STAGES) & 1);
   tc_fence_after();
 
-  // ---------------- epilogue: TMEM -> registers -> global
+  // ---------------- epilogue: TMEM -> registers -> (smem staging) -> global
   const uint32_t row = m0 + warp * 32 + lane;
   const bool row_ok = row < M;
   char* Cbase = const_cast<char*>(C.ptr) + bz * C.bs * (int64_t)sizeof(TC);
-  int64_t roff = 0;
-  if (row_ok) {
-    uint32_t q = row / C.split0, r = row - q * C.split0;
-    roff = (int64_t)q * C.hi0 + (int64_t)r * C.lo0;
-  }
+  if (c_mode == 1 && ws == nullptr) {
+    // stage the alpha-scaled tile in the (now idle) pipeline buffers, row pitch padded by
+    // 16 bytes (conflict-free 16-byte stores), then write 16-byte chunks with consecutive
+    // threads on consecutive chunks of a row: full-sector, coalesced row segments.
+    constexpr int PITCH = BN * (int)sizeof(TC) + 16;
+    uint8_t* stile = smem;
 #pragma unroll 1
-  for (int c0 = 0; c0 < BN; c0 += 32) {
-    float v[32];
-    tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + c0, v);
-    tmem_ld_wait();
-    if (!row_ok) continue;
-    TC* crow = reinterpret_cast<TC*>(Cbase) + roff;
-    if (c_mode == 1) {  // columns contiguous in runs of >= 8, N % 8 == 0
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      float v[32];
+      tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + c0, v);
+      tmem_ld_wait();
+      uint8_t* dst = stile + (warp * 32 + lane) * PITCH + c0 * (int)sizeof(TC);
 #pragma unroll
       for (int j = 0; j < 32; j += 8) {
-        uint32_t col = n0 + c0 + j;
-        if (col >= N) break;
-        uint32_t q = col / C.split1, r = col - q * C.split1;
-        TC* p = crow + (int64_t)q * C.hi1 + r;
-        float o[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = alpha * v[j + e];
-        if (beta != 0.f) {
-#pragma unroll
-          for (int e = 0; e < 8; ++e) o[e] += beta * ldf<TC>(p + e);
-        }
         if constexpr (sizeof(TC) == 2) {
-          uint4 w;
-          w.x = pack_bf16x2(o[0], o[1]);
-          w.y = pack_bf16x2(o[2], o[3]);
-          w.z = pack_bf16x2(o[4], o[5]);
-          w.w = pack_bf16x2(o[6], o[7]);
-          *reinterpret_cast<uint4*>(p) = w;
+          *reinterpret_cast<uint4*>(dst + j * 2) =
+              make_uint4(pack_bf16x2(alpha * v[j], alpha * v[j + 1]), pack_bf16x2(alpha * v[j + 2], alpha * v[j + 3]),
+                         pack_bf16x2(alpha * v[j + 4], alpha * v[j + 5]), pack_bf16x2(alpha * v[j + 6], alpha * v[j + 7]));
         } else {
-          *reinterpret_cast<float4*>(p) = make_float4(o[0], o[1], o[2], o[3]);
-          *reinterpret_cast<float4*>(p + 4) = make_float4(o[4], o[5], o[6], o[7]);
+          *reinterpret_cast<float4*>(dst + j * 4) =
+              make_float4(alpha * v[j], alpha * v[j + 1], alpha * v[j + 2], alpha * v[j + 3]);
+          *reinterpret_cast<float4*>(dst + j * 4 + 16) =
+              make_float4(alpha * v[j + 4], alpha * v[j + 5], alpha * v[j + 6], alpha * v[j + 7]);
         }
       }
-    } else {
+    }
+    __syncthreads();
+    constexpr int CPR = BN * (int)sizeof(TC) / 16;  // 16-byte chunks per tile row
+    constexpr int EPC = 16 / (int)sizeof(TC);        // elements per chunk
+    for (int ch = threadIdx.x; ch < GEMM_BM * CPR; ch += 128) {
+      const int r = ch / CPR, cc = ch % CPR;
+      const uint32_t grow = m0 + r, gcol = n0 + cc * EPC;
+      if (grow >= M || gcol >= N) continue;
+      const uint32_t qr = grow / C.split0, rr = grow - qr * C.split0;
+      const uint32_t qc = gcol / C.split1, rc = gcol - qc * C.split1;
+      TC* p = reinterpret_cast<TC*>(Cbase) + (int64_t)qr * C.hi0 + (int64_t)rr * C.lo0 + (int64_t)qc * C.hi1 + rc;
+      uint4 val = *reinterpret_cast<const uint4*>(stile + r * PITCH + cc * 16);
+      if (beta != 0.f) {
+        const TC* sv = reinterpret_cast<const TC*>(&val);
+        uint4 outv;
+        TC* ov = reinterpret_cast<TC*>(&outv);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
+        for (int e = 0; e < EPC; ++e) stf<TC>(ov + e, ldf<TC>(sv + e) + beta * ldf<TC>(p + e));
+        val = outv;
+      }
+      *reinterpret_cast<uint4*>(p) = val;
+    }
+  } else {
+    int64_t roff = 0;
+    if (row_ok) {
+      uint32_t q = row / C.split0, r = row - q * C.split0;
+      roff = (int64_t)q * C.hi0 + (int64_t)r * C.lo0;
+    }
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      float v[32];
+      tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + c0, v);
+      tmem_ld_wait();
+      if (!row_ok) continue;
+      if (ws != nullptr) {  // split-K partial, dense fp32 [M][N]
+        float* wrow = ws + ((int64_t)(split * (gridDim.z / splits) + bz) * M + row) * N;
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          const uint32_t col = n0 + c0 + j;
+          if (col + 4 <= N) *reinterpret_cast<float4*>(wrow + col) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+          else
+            for (int e = 0; e < 4; ++e)
+              if (col + e < N) wrow[col + e] = v[j + e];
+        }
+        continue;
+      }
+      TC* crow = reinterpret_cast<TC*>(Cbase) + roff;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {  // generic addressing (e.g. rows contiguous: coalesced per column)
         uint32_t col = n0 + c0 + j;
         if (col >= N) break;
         uint32_t q = col / C.split1, r = col - q * C.split1;
@@ -189,6 +232,49 @@ __global__ void __launch_bounds__(128) bgemm_kernel(MatArg A, MatArg B, MatArg C
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc(tmem, BN < 32 ? 32 : BN);
+}
+
+// C = alpha * sum_split ws[split] + beta * C   (output addressing of C; 8 elements per thread
+// along whichever C dimension is contiguous)
+template <typename TC>
+__global__ void __launch_bounds__(256) bgemm_splitk_reduce(const float* __restrict__ ws, MatArg C, uint32_t M,
+                                                           uint32_t N, int64_t batch, int splits, float alpha,
+                                                           float beta, int rows_contig) {
+  const int64_t MN = (int64_t)M * N;
+  const int64_t n8 = batch * MN / 8;
+  char* Cbase = const_cast<char*>(C.ptr);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t b, r0, c0;
+    if (rows_contig) {  // 8 consecutive rows of one column
+      const int64_t per_b = MN / 8;
+      b = i / per_b;
+      const int64_t t = i % per_b;
+      c0 = t / (M / 8);
+      r0 = (t % (M / 8)) * 8;
+    } else {            // 8 consecutive columns of one row
+      const int64_t per_b = MN / 8;
+      b = i / per_b;
+      const int64_t t = i % per_b;
+      r0 = t / (N / 8);
+      c0 = (t % (N / 8)) * 8;
+    }
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int s = 0; s < splits; ++s) {
+      const float* w = ws + ((int64_t)s * batch + b) * MN;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += rows_contig ? w[(r0 + e) * N + c0] : w[r0 * N + c0 + e];
+    }
+    TC* cb = reinterpret_cast<TC*>(Cbase) + b * C.bs;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const uint32_t r = (uint32_t)(rows_contig ? r0 + e : r0), c = (uint32_t)(rows_contig ? c0 : c0 + e);
+      const uint32_t qr = r / C.split0, rr = r - qr * C.split0, qc = c / C.split1, rc = c - qc * C.split1;
+      TC* p = cb + (int64_t)qr * C.hi0 + (int64_t)rr * C.lo0 + (int64_t)qc * C.hi1 + (int64_t)rc * C.lo1;
+      float o = alpha * acc[e];
+      if (beta != 0.f) o += beta * ldf<TC>(p);
+      stf<TC>(p, o);
+    }
+  }
 }
 
 static MatArg to_arg(const EvoMat* m, int64_t ext0, int64_t ext1) {
@@ -218,7 +304,7 @@ static bool runs8(const MatArg& a, int d) {
 
 template <int BN, bool AM, bool BMN, typename TC>
 static int launch_bgemm(MatArg A, MatArg B, MatArg C, int64_t batch, int64_t M, int64_t N, int64_t K, float alpha,
-                        float beta, int c_mode, cudaStream_t st) {
+                        float beta, int c_mode, int splits, float* ws, cudaStream_t st) {
   constexpr int STAGES = 3;
   const size_t smem = STAGES * (GEMM_BM * GEMM_BK * 2 + BN * GEMM_BK * 2);
   auto kern = bgemm_kernel<BN, AM, BMN, STAGES, TC>;
@@ -228,27 +314,51 @@ static int launch_bgemm(MatArg A, MatArg B, MatArg C, int64_t batch, int64_t M, 
     if (e != cudaSuccess) return cuda_status(e, "bgemm attr");
     attr_set = true;
   }
-  dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + GEMM_BM - 1) / GEMM_BM), (unsigned)batch);
-  kern<<<grid, 128, smem, st>>>(A, B, C, (uint32_t)M, (uint32_t)N, (uint32_t)K, alpha, beta, c_mode);
+  dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + GEMM_BM - 1) / GEMM_BM), (unsigned)(batch * splits));
+  kern<<<grid, 128, smem, st>>>(A, B, C, (uint32_t)M, (uint32_t)N, (uint32_t)K, alpha, beta, c_mode, splits,
+                                splits > 1 ? ws : nullptr);
   EVO_LAUNCH_CHECK("bgemm launch");
+  if (splits > 1) {
+    const bool rows_contig = C.lo0 == 1 && C.split0 % 8 == 0 && M % 8 == 0;
+    EVO_CHECK_ARG(rows_contig || N % 8 == 0, EVO_ERR_ALIGN, "bgemm split-K: M or N must be a multiple of 8");
+    int64_t n8 = batch * M * N / 8;
+    int64_t g = (n8 + 255) / 256, cap = (int64_t)sm_count() * 16;
+    bgemm_splitk_reduce<TC><<<(unsigned)(g < cap ? g : cap), 256, 0, st>>>(ws, C, (uint32_t)M, (uint32_t)N, batch,
+                                                                           splits, alpha, beta, rows_contig ? 1 : 0);
+    EVO_LAUNCH_CHECK("bgemm split-K reduce");
+  }
   return EVO_OK;
 }
 
 template <int BN, typename TC>
 static int dispatch_major(bool am, bool bm, MatArg A, MatArg B, MatArg C, int64_t batch, int64_t M, int64_t N,
-                          int64_t K, float alpha, float beta, int c_mode, cudaStream_t st) {
-  if (!am && !bm) return launch_bgemm<BN, false, false, TC>(A, B, C, batch, M, N, K, alpha, beta, c_mode, st);
-  if (!am && bm) return launch_bgemm<BN, false, true, TC>(A, B, C, batch, M, N, K, alpha, beta, c_mode, st);
-  if (am && !bm) return launch_bgemm<BN, true, false, TC>(A, B, C, batch, M, N, K, alpha, beta, c_mode, st);
-  return launch_bgemm<BN, true, true, TC>(A, B, C, batch, M, N, K, alpha, beta, c_mode, st);
+                          int64_t K, float alpha, float beta, int c_mode, int splits, float* ws, cudaStream_t st) {
+  if (!am && !bm)
+    return launch_bgemm<BN, false, false, TC>(A, B, C, batch, M, N, K, alpha, beta, c_mode, splits, ws, st);
+  if (!am && bm)
+    return launch_bgemm<BN, false, true, TC>(A, B, C, batch, M, N, K, alpha, beta, c_mode, splits, ws, st);
+  if (am && !bm)
+    return launch_bgemm<BN, true, false, TC>(A, B, C, batch, M, N, K, alpha, beta, c_mode, splits, ws, st);
+  return launch_bgemm<BN, true, true, TC>(A, B, C, batch, M, N, K, alpha, beta, c_mode, splits, ws, st);
 }
 
-}  // namespace evo
+// split-K factor: only when the output tiles cannot fill the machine and K is long
+static int pick_splits(int64_t batch, int64_t M, int64_t N, int64_t K, int bn) {
+  const int64_t tiles = ((M + 127) / 128) * ((N + bn - 1) / bn) * batch;
+  const int64_t kt = (K + GEMM_BK - 1) / GEMM_BK;
+  const int64_t target = 2 * (int64_t)sm_count();
+  if (tiles >= target || kt < 16) return 1;
+  int64_t s = (target + tiles - 1) / tiles;
+  if (s > kt / 8) s = kt / 8;  // >= 8 k-tiles per split
+  if (s > 16) s = 16;
+  if (s < 1) s = 1;
+  const int64_t per = (kt + s - 1) / s;
+  return (int)((kt + per - 1) / per);  // every split owns >= 1 k-tile
+}
 
-using namespace evo;
 
-extern "C" int evo_bgemm(const EvoMat* A, const EvoMat* B, const EvoMat* C, int64_t batch, int64_t M, int64_t N,
-                         int64_t K, float alpha, float beta, void* stream) {
+static int bgemm_entry(const EvoMat* A, const EvoMat* B, const EvoMat* C, int64_t batch, int64_t M, int64_t N,
+                       int64_t K, float alpha, float beta, void* workspace, int64_t ws_bytes, void* stream) {
   EVO_CHECK_ARG(A && B && C && A->ptr && B->ptr && C->ptr, EVO_ERR_ARG, "bgemm: null operand");
   EVO_CHECK_ARG(batch >= 1 && M >= 1 && N >= 1 && K >= 1, EVO_ERR_SHAPE, "bgemm: bad extents b=%lld M=%lld N=%lld K=%lld",
                 (long long)batch, (long long)M, (long long)N, (long long)K);
@@ -272,10 +382,33 @@ extern "C" int evo_bgemm(const EvoMat* A, const EvoMat* B, const EvoMat* C, int6
   cudaStream_t st = (cudaStream_t)stream;
   // wide N tiles amortise the A-tile loads; N=64 keeps small problems parallel
   bool small = ((M + 127) / 128) * ((N + 127) / 128) * batch < 148;
+  const int bn = (small || N <= 64) ? 64 : 128;
+  int splits = pick_splits(batch, M, N, K, bn);
+  if (splits > 1 && (!workspace || ws_bytes < splits * batch * M * N * 4)) splits = 1;
+  float* ws = (float*)workspace;
   if (C->dtype == EVO_BF16) {
-    if (small || N <= 64) return dispatch_major<64, bf16>(am, bm, a, b, c, batch, M, N, K, alpha, beta, c_mode, st);
-    return dispatch_major<128, bf16>(am, bm, a, b, c, batch, M, N, K, alpha, beta, c_mode, st);
+    if (bn == 64) return dispatch_major<64, bf16>(am, bm, a, b, c, batch, M, N, K, alpha, beta, c_mode, splits, ws, st);
+    return dispatch_major<128, bf16>(am, bm, a, b, c, batch, M, N, K, alpha, beta, c_mode, splits, ws, st);
   }
-  if (small || N <= 64) return dispatch_major<64, float>(am, bm, a, b, c, batch, M, N, K, alpha, beta, c_mode, st);
-  return dispatch_major<128, float>(am, bm, a, b, c, batch, M, N, K, alpha, beta, c_mode, st);
+  if (bn == 64) return dispatch_major<64, float>(am, bm, a, b, c, batch, M, N, K, alpha, beta, c_mode, splits, ws, st);
+  return dispatch_major<128, float>(am, bm, a, b, c, batch, M, N, K, alpha, beta, c_mode, splits, ws, st);
+}
+
+}  // namespace evo
+
+extern "C" int evo_bgemm(const EvoMat* A, const EvoMat* B, const EvoMat* C, int64_t batch, int64_t M, int64_t N,
+                         int64_t K, float alpha, float beta, void* stream) {
+  return evo::bgemm_entry(A, B, C, batch, M, N, K, alpha, beta, nullptr, 0, stream);
+}
+
+extern "C" int64_t evo_bgemm_workspace(int64_t batch, int64_t M, int64_t N, int64_t K) {
+  bool small = ((M + 127) / 128) * ((N + 127) / 128) * batch < 148;
+  const int bn = (small || N <= 64) ? 64 : 128;
+  const int splits = evo::pick_splits(batch, M, N, K, bn);
+  return splits > 1 ? (int64_t)splits * batch * M * N * 4 : 0;
+}
+
+extern "C" int evo_bgemm_ws(const EvoMat* A, const EvoMat* B, const EvoMat* C, int64_t batch, int64_t M, int64_t N,
+                            int64_t K, float alpha, float beta, void* workspace, int64_t ws_bytes, void* stream) {
+  return evo::bgemm_entry(A, B, C, batch, M, N, K, alpha, beta, workspace, ws_bytes, stream);
 }

@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(256) ln_fwd_warp(const TX* __restrict__ x, int
                                                    float* __restrict__ rstd_out, int64_t rows, float eps,
                                                    const float* __restrict__ w, TY* __restrict__ dot_out,
                                                    int64_t dot_hs) {
+  static_assert(K == 0, "fused row dots live in ln_rowdot_fwd");
   constexpr int COLS = VPT * 32;
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -106,16 +107,187 @@ __global__ void __launch_bounds__(256) ln_fwd_warp(const TX* __restrict__ x, int
     if (mean_out) mean_out[row] = mu;
     if (rstd_out) rstd_out[row] = rstd;
   }
-  if constexpr (K > 0) {
-    // fused per-row dot products with w[COLS, k] (msa_row_bias, evoformer.py:204-206)
+}
+
+// ------------------------------------------------------------- LN + k row dots (msa_row_bias)
+// Sum of K per-lane partials across the 32 lanes with a transposing butterfly:
+// after the xor-16/8/4 steps each lane holds 1 of the K=8 sums (K/8 per lane for
+// larger K), 9 shuffles instead of 5*K.  Returns the sum for head  (lane >> 2) & 7.
+template <int K>
+__device__ __forceinline__ float butterfly_sum8(float* v, int lane) {
+  static_assert(K == 8, "butterfly for 8 heads");
+  // step 16: keep heads [0,4) on lanes < 16, [4,8) on lanes >= 16
+  const bool up16 = lane & 16;
+  float a[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float send = up16 ? v[i] : v[4 + i];
+    const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
+    a[i] = (up16 ? v[4 + i] : v[i]) + recv;
+  }
+  const bool up8 = lane & 8;
+  float b2[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float send = up8 ? a[i] : a[2 + i];
+    const float recv = __shfl_xor_sync(0xffffffffu, send, 8);
+    b2[i] = (up8 ? a[2 + i] : a[i]) + recv;
+  }
+  const bool up4 = lane & 4;
+  const float send = up4 ? b2[0] : b2[1];
+  float c = (up4 ? b2[1] : b2[0]) + __shfl_xor_sync(0xffffffffu, send, 4);
+  c += __shfl_xor_sync(0xffffffffu, c, 2);
+  c += __shfl_xor_sync(0xffffffffu, c, 1);
+  return c;  // head = ((lane>>4)&1)*4 + ((lane>>3)&1)*2 + ((lane>>2)&1)
+}
+
+// one warp per row, persistent over rows (w cached in registers); K <= 8 heads
+// (padded), output out[h * out_hs + row]
+template <typename TX, int VPT>
+__global__ void __launch_bounds__(256) ln_rowdot_fwd(const TX* __restrict__ x, const float* __restrict__ gamma,
+                                                     const float* __restrict__ beta, const float* __restrict__ w,
+                                                     TX* __restrict__ out, int64_t out_hs, TX* __restrict__ ln_out,
+                                                     float* __restrict__ mean_out, float* __restrict__ rstd_out,
+                                                     int64_t rows, float eps) {
+  constexpr int COLS = VPT * 32, K = 8;
+  const int lane = threadIdx.x & 31;
+  float g[VPT], bt[VPT], wr[VPT][K];
+  load_row<float, VPT>(gamma + lane * VPT, g);
+  load_row<float, VPT>(beta + lane * VPT, bt);
+#pragma unroll
+  for (int i = 0; i < VPT; ++i)
+#pragma unroll
+    for (int h = 0; h < K; ++h) wr[i][h] = w[(lane * VPT + i) * K + h];
+  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows; row += wstride) {
+    float v[VPT];
+    load_row<TX, VPT>(x + row * COLS + lane * VPT, v);
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) s += v[i];
+    const float mu = warp_sum(s) * (1.0f / COLS);
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      v[i] -= mu;
+      q += v[i] * v[i];
+    }
+    const float rs = rsqrtf(warp_sum(q) * (1.0f / COLS) + eps);
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) v[i] = v[i] * rs * g[i] + bt[i];
+    if (ln_out) store_row<TX, VPT>(ln_out + row * COLS + lane * VPT, v);
+    if (lane == 0 && mean_out) {
+      mean_out[row] = mu;
+      rstd_out[row] = rs;
+    }
+    float d[K];
 #pragma unroll
     for (int h = 0; h < K; ++h) {
-      float d = 0.f;
+      d[h] = 0.f;
 #pragma unroll
-      for (int i = 0; i < VPT; ++i) d += v[i] * w[(lane * VPT + i) * K + h];
-      d = warp_sum(d);
-      if (lane == h) stf<TY>(dot_out + h * dot_hs + row, d);
+      for (int i = 0; i < VPT; ++i) d[h] += v[i] * wr[i][h];
     }
+    const float r = butterfly_sum8<K>(d, lane);
+    if ((lane & 3) == 0) {
+      const int h = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+      stf<TX>(out + h * out_hs + row, r);
+    }
+  }
+}
+
+// backward of LN + row dots, fused: dy = w . dout_row; dW += LN(x) dout^T; LN backward
+// into dx (dx = res + dLN, res may alias dx); dgamma/dbeta/dW: CTA partials + one
+// atomic per element per CTA.
+template <typename TX, int VPT>
+__global__ void __launch_bounds__(256) ln_rowdot_bwd(const TX* __restrict__ x, const float* __restrict__ gamma,
+                                                     const float* __restrict__ beta, const float* __restrict__ w,
+                                                     const float* __restrict__ dout, int64_t out_hs,
+                                                     const float* __restrict__ mean, const float* __restrict__ rstd,
+                                                     const TX* res, TX* dx, float* __restrict__ dgamma,
+                                                     float* __restrict__ dbeta, float* __restrict__ dw,
+                                                     int64_t rows) {
+  constexpr int COLS = VPT * 32, K = 8;
+  __shared__ float red[8][COLS * (2 + K) / 8 + 1];  // per-warp partials, flushed in column slices
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  float g[VPT], bt[VPT], wr[VPT][K];
+  load_row<float, VPT>(gamma + lane * VPT, g);
+  load_row<float, VPT>(beta + lane * VPT, bt);
+#pragma unroll
+  for (int i = 0; i < VPT; ++i)
+#pragma unroll
+    for (int h = 0; h < K; ++h) wr[i][h] = w[(lane * VPT + i) * K + h];
+  float dg[VPT], db[VPT], dwa[VPT][K];
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    dg[i] = db[i] = 0.f;
+#pragma unroll
+    for (int h = 0; h < K; ++h) dwa[i][h] = 0.f;
+  }
+  const int64_t slab = (rows + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = blockIdx.x * slab, r1 = r0 + slab < rows ? r0 + slab : rows;
+  for (int64_t row = r0 + wid; row < r1; row += 8) {
+    float xv[VPT];
+    load_row<TX, VPT>(x + row * COLS + lane * VPT, xv);
+    const float mu = mean[row], rs = rstd[row];
+    float dh[K];
+#pragma unroll
+    for (int h = 0; h < K; ++h) dh[h] = dout[h * out_hs + row];
+    float d[VPT], s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      xv[i] = (xv[i] - mu) * rs;  // xhat
+      const float lnv = xv[i] * g[i] + bt[i];
+      d[i] = 0.f;
+#pragma unroll
+      for (int h = 0; h < K; ++h) {
+        d[i] += dh[h] * wr[i][h];
+        dwa[i][h] += lnv * dh[h];
+      }
+      const float gd = g[i] * d[i];
+      s1 += gd;
+      s2 += gd * xv[i];
+      dg[i] += d[i] * xv[i];
+      db[i] += d[i];
+    }
+    s1 = warp_sum(s1) * (1.0f / COLS);
+    s2 = warp_sum(s2) * (1.0f / COLS);
+    float o[VPT];
+    if (res) load_row<TX, VPT>(res + row * COLS + lane * VPT, o);
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) o[i] = (res ? o[i] : 0.f) + rs * (g[i] * d[i] - s1 - xv[i] * s2);
+    store_row<TX, VPT>(dx + row * COLS + lane * VPT, o);
+  }
+  // CTA reduction: dgamma, dbeta, dW (COLS * (2 + K) values), 8 warps
+  constexpr int NV = COLS * (2 + K);
+  float* flat = &red[0][0];
+  constexpr int PITCH = COLS * (2 + K) / 8 + 1;
+  for (int base = 0; base < NV; base += NV / 8) {
+    // each warp deposits its values of slice [base, base + NV/8)
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      const int c = lane * VPT + i;
+      const int idx[2] = {c, COLS + c};
+      const float val[2] = {dg[i], db[i]};
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+        if (idx[t] >= base && idx[t] < base + NV / 8) flat[wid * PITCH + idx[t] - base] = val[t];
+#pragma unroll
+      for (int h = 0; h < K; ++h) {
+        const int id = 2 * COLS + c * K + h;
+        if (id >= base && id < base + NV / 8) flat[wid * PITCH + id - base] = dwa[i][h];
+      }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < NV / 8; t += blockDim.x) {
+      float acc = 0.f;
+#pragma unroll
+      for (int ww = 0; ww < 8; ++ww) acc += flat[ww * PITCH + t];
+      const int id = base + t;
+      if (id < COLS) atomicAdd(dgamma + id, acc);
+      else if (id < 2 * COLS) atomicAdd(dbeta + id - COLS, acc);
+      else atomicAdd(dw + (id - 2 * COLS), acc);
+    }
+    __syncthreads();
   }
 }
 
@@ -157,21 +329,20 @@ __global__ void __launch_bounds__(256) ln_fwd_thread(const TX* __restrict__ x, i
 template <typename TD, typename TX, typename TO, int VPT>
 __global__ void __launch_bounds__(256) ln_bwd_warp(const TD* __restrict__ dy, const TX* __restrict__ x, int64_t x_rs,
                                                    const float* __restrict__ gamma, const float* __restrict__ mean,
-                                                   const float* __restrict__ rstd, TO* __restrict__ dx, int acc,
+                                                   const float* __restrict__ rstd, TO* dx, const TO* res,
                                                    float* __restrict__ dgamma, float* __restrict__ dbeta,
                                                    int64_t rows) {
   constexpr int COLS = VPT * 32;
-  extern __shared__ float red[];  // [2][COLS]
-  for (int i = threadIdx.x; i < 2 * COLS; i += blockDim.x) red[i] = 0.f;
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int wpb = blockDim.x >> 5;
+  extern __shared__ float red[];  // [8 warps][2][COLS]
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   float g[VPT];
   load_row<float, VPT>(gamma + lane * VPT, g);
   float dg[VPT], db[VPT];
 #pragma unroll
   for (int i = 0; i < VPT; ++i) dg[i] = db[i] = 0.f;
-  for (int64_t row = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); row < rows; row += (int64_t)gridDim.x * wpb) {
+  const int64_t slab = (rows + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = blockIdx.x * slab, r1 = r0 + slab < rows ? r0 + slab : rows;
+  for (int64_t row = r0 + wid; row < r1; row += 8) {
     float xv[VPT], d[VPT];
     load_row<TX, VPT>(x + row * x_rs + lane * VPT, xv);
     load_row<TD, VPT>(dy + row * COLS + lane * VPT, d);
@@ -189,84 +360,85 @@ __global__ void __launch_bounds__(256) ln_bwd_warp(const TD* __restrict__ dy, co
     s1 = warp_sum(s1) * (1.0f / COLS);
     s2 = warp_sum(s2) * (1.0f / COLS);
     float o[VPT];
+    if (res) load_row<TO, VPT>(res + row * x_rs + lane * VPT, o);
 #pragma unroll
-    for (int i = 0; i < VPT; ++i) o[i] = rs * (g[i] * d[i] - s1 - xv[i] * s2);
-    TO* dp = dx + row * x_rs + lane * VPT;
-    if (acc) {
-      float prev[VPT];
-      load_row<TO, VPT>(dp, prev);
-#pragma unroll
-      for (int i = 0; i < VPT; ++i) o[i] += prev[i];
-    }
-    store_row<TO, VPT>(dp, o);
+    for (int i = 0; i < VPT; ++i) o[i] = (res ? o[i] : 0.f) + rs * (g[i] * d[i] - s1 - xv[i] * s2);
+    store_row<TO, VPT>(dx + row * x_rs + lane * VPT, o);
   }
   if (dgamma || dbeta) {
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
-      atomicAdd(&red[lane * VPT + i], dg[i]);
-      atomicAdd(&red[COLS + lane * VPT + i], db[i]);
+      red[(wid * 2) * COLS + lane * VPT + i] = dg[i];
+      red[(wid * 2 + 1) * COLS + lane * VPT + i] = db[i];
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < COLS; i += blockDim.x) {
-      if (dgamma) atomicAdd(dgamma + i, red[i]);
-      if (dbeta) atomicAdd(dbeta + i, red[COLS + i]);
+    for (int c = threadIdx.x; c < COLS; c += blockDim.x) {
+      float a = 0.f, b = 0.f;
+#pragma unroll
+      for (int ww = 0; ww < 8; ++ww) {
+        a += red[(ww * 2) * COLS + c];
+        b += red[(ww * 2 + 1) * COLS + c];
+      }
+      if (dgamma) atomicAdd(dgamma + c, a);
+      if (dbeta) atomicAdd(dbeta + c, b);
     }
   }
 }
 
-template <typename TD, typename TX, typename TO, int MAXC>
+// strided (channel-major) rows, one thread per row, exact width C
+template <typename TD, typename TX, typename TO, int C>
 __global__ void __launch_bounds__(256) ln_bwd_thread(const TD* __restrict__ dy, const TX* __restrict__ x, int64_t x_rs,
                                                      int64_t x_cs, const float* __restrict__ gamma,
                                                      const float* __restrict__ mean, const float* __restrict__ rstd,
-                                                     TO* __restrict__ dx, int acc, float* __restrict__ dgamma,
-                                                     float* __restrict__ dbeta, int64_t rows, int cols) {
-  __shared__ float red[2 * MAXC];
-  for (int i = threadIdx.x; i < 2 * MAXC; i += blockDim.x) red[i] = 0.f;
-  __syncthreads();
-  float dg[MAXC], db[MAXC];
+                                                     TO* dx, const TO* res, float* __restrict__ dgamma,
+                                                     float* __restrict__ dbeta, int64_t rows) {
+  __shared__ float red[2][8][C];
+  float dg[C], db[C];
 #pragma unroll
-  for (int c = 0; c < MAXC; ++c) dg[c] = db[c] = 0.f;
+  for (int c = 0; c < C; ++c) dg[c] = db[c] = 0.f;
   for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < rows;
        row += (int64_t)gridDim.x * blockDim.x) {
-    float xh[MAXC], d[MAXC];
+    float xh[C], d[C];
     const float mu = mean[row], rs = rstd[row];
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
-    for (int c = 0; c < MAXC; ++c)
-      if (c < cols) {
-        xh[c] = (ldf<TX>(x + row * x_rs + c * x_cs) - mu) * rs;
-        d[c] = ldf<TD>(dy + row * cols + c);
-        float gd = gamma[c] * d[c];
-        s1 += gd;
-        s2 += gd * xh[c];
-        dg[c] += d[c] * xh[c];
-        db[c] += d[c];
-      }
-    s1 /= cols;
-    s2 /= cols;
+    for (int c = 0; c < C; ++c) {
+      xh[c] = (ldf<TX>(x + row * x_rs + c * x_cs) - mu) * rs;
+      d[c] = ldf<TD>(dy + row * C + c);
+      const float gd = gamma[c] * d[c];
+      s1 += gd;
+      s2 += gd * xh[c];
+      dg[c] += d[c] * xh[c];
+      db[c] += d[c];
+    }
+    s1 *= 1.0f / C;
+    s2 *= 1.0f / C;
 #pragma unroll
-    for (int c = 0; c < MAXC; ++c)
-      if (c < cols) {
-        TO* p = dx + row * x_rs + c * x_cs;
-        float o = rs * (gamma[c] * d[c] - s1 - xh[c] * s2);
-        if (acc) o += ldf<TO>(p);
-        stf<TO>(p, o);
-      }
+    for (int c = 0; c < C; ++c) {
+      float o = rs * (gamma[c] * d[c] - s1 - xh[c] * s2);
+      if (res) o += ldf<TO>(res + row * x_rs + c * x_cs);
+      stf<TO>(dx + row * x_rs + c * x_cs, o);
+    }
   }
   if (dgamma || dbeta) {
+    const int wid = threadIdx.x >> 5;
 #pragma unroll
-    for (int c = 0; c < MAXC; ++c)
-      if (c < cols) {
-        float a = warp_sum(dg[c]), b = warp_sum(db[c]);
-        if ((threadIdx.x & 31) == 0) {
-          atomicAdd(&red[c], a);
-          atomicAdd(&red[MAXC + c], b);
-        }
+    for (int c = 0; c < C; ++c) {
+      const float a = warp_sum(dg[c]), b = warp_sum(db[c]);
+      if ((threadIdx.x & 31) == 0) {
+        red[0][wid][c] = a;
+        red[1][wid][c] = b;
       }
+    }
     __syncthreads();
-    for (int c = threadIdx.x; c < cols; c += blockDim.x) {
-      if (dgamma) atomicAdd(dgamma + c, red[c]);
-      if (dbeta) atomicAdd(dbeta + c, red[MAXC + c]);
+    for (int c = threadIdx.x; c < C; c += blockDim.x) {
+      float a = 0.f, b = 0.f;
+      for (int ww = 0; ww < 8; ++ww) {
+        a += red[0][ww][c];
+        b += red[1][ww][c];
+      }
+      if (dgamma) atomicAdd(dgamma + c, a);
+      if (dbeta) atomicAdd(dbeta + c, b);
     }
   }
 }
@@ -346,43 +518,64 @@ extern "C" int evo_layernorm_rowdot_fwd(const void* x, int x_dtype, const float*
                                         void* ln_out, float* mean, float* rstd, int64_t rows, int64_t cols, float eps,
                                         void* stream) {
   EVO_CHECK_ARG(x && gamma && beta && w && out, EVO_ERR_ARG, "layernorm_rowdot: null pointer");
-  EVO_CHECK_ARG(k >= 1 && k <= 16 && cols % 32 == 0 && cols <= 1024, EVO_ERR_SHAPE,
-                "layernorm_rowdot: need 1<=k<=16 and cols %% 32 == 0, <= 1024");
-  EVO_CHECK_ARG(x_dtype == out_dtype, EVO_ERR_DTYPE, "layernorm_rowdot: x and out dtype must match");
+  EVO_CHECK_ARG(k == 8, EVO_ERR_SHAPE, "layernorm_rowdot: w must be padded to 8 heads (got %d)", k);
+  EVO_CHECK_ARG(x_dtype == out_dtype && x_dtype == EVO_BF16, EVO_ERR_DTYPE, "layernorm_rowdot: bf16 only");
   EVO_CHECK_ARG(((uintptr_t)x & 15) == 0, EVO_ERR_ALIGN, "layernorm_rowdot: x must be 16B aligned");
-  cudaStream_t st = (cudaStream_t)stream;
   if (rows == 0) return EVO_OK;
-#define RD(KK)                                                                                                   \
-  (x_dtype == EVO_BF16 ? ln_fwd_dispatch_warp<bf16, bf16, KK>(x, cols, gamma, beta, ln_out, mean, rstd, rows,   \
-                                                               cols, eps, w, out, out_hs, st)                   \
-                       : ln_fwd_dispatch_warp<float, float, KK>(x, cols, gamma, beta, ln_out, mean, rstd, rows, \
-                                                                cols, eps, w, out, out_hs, st))
-  switch (k) {
-    case 1: return RD(1);
-    case 2: return RD(2);
-    case 4: return RD(4);
-    case 8: return RD(8);
-    case 16: return RD(16);
-    default: break;
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t need = (rows + 7) / 8, cap = (int64_t)sm_count() * 8;
+  dim3 grid((unsigned)(need < cap ? need : cap));
+#define RDF(VPT)                                                                                               \
+  ln_rowdot_fwd<bf16, VPT><<<grid, 256, 0, st>>>((const bf16*)x, gamma, beta, w, (bf16*)out, out_hs, (bf16*)ln_out, \
+                                                 mean, rstd, rows, eps)
+  switch (cols) {
+    case 32: RDF(1); break;
+    case 64: RDF(2); break;
+    case 128: RDF(4); break;
+    case 256: RDF(8); break;
+    default: set_error("layernorm_rowdot: unsupported width %lld", (long long)cols); return EVO_ERR_SHAPE;
   }
-#undef RD
-  set_error("layernorm_rowdot: k must be 1, 2, 4, 8 or 16 (got %d)", k);
-  return EVO_ERR_SHAPE;
+#undef RDF
+  EVO_LAUNCH_CHECK("layernorm_rowdot fwd");
+  return EVO_OK;
+}
+
+extern "C" int evo_layernorm_rowdot_bwd(const void* x, int x_dtype, const float* gamma, const float* beta,
+                                        const float* w, int k, const float* dout, int64_t out_hs, const float* mean,
+                                        const float* rstd, const void* res, void* dx, float* dgamma, float* dbeta,
+                                        float* dw, int64_t rows, int64_t cols, void* stream) {
+  EVO_CHECK_ARG(x && gamma && beta && w && dout && mean && rstd && dx && dgamma && dbeta && dw, EVO_ERR_ARG,
+                "layernorm_rowdot bwd: null pointer");
+  EVO_CHECK_ARG(k == 8 && x_dtype == EVO_BF16, EVO_ERR_SHAPE, "layernorm_rowdot bwd: k == 8, bf16");
+  if (rows == 0) return EVO_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t need = (rows + 63) / 64, cap = (int64_t)sm_count() * 2;
+  dim3 grid((unsigned)(need < cap ? need : cap));
+#define RDB(VPT)                                                                                                 \
+  ln_rowdot_bwd<bf16, VPT><<<grid, 256, 0, st>>>((const bf16*)x, gamma, beta, w, dout, out_hs, mean, rstd,        \
+                                                 (const bf16*)res, (bf16*)dx, dgamma, dbeta, dw, rows)
+  switch (cols) {
+    case 32: RDB(1); break;
+    case 64: RDB(2); break;
+    case 128: RDB(4); break;
+    default: set_error("layernorm_rowdot bwd: unsupported width %lld", (long long)cols); return EVO_ERR_SHAPE;
+  }
+#undef RDB
+  EVO_LAUNCH_CHECK("layernorm_rowdot bwd");
+  return EVO_OK;
 }
 
 template <typename TD, typename TX, typename TO>
 static int ln_bwd_impl(const void* dy, const void* x, int64_t x_rs, int64_t x_cs, const float* g, const float* mean,
-                       const float* rstd, void* dx, int acc, float* dg, float* db, int64_t rows, int64_t cols,
+                       const float* rstd, void* dx, const void* res, float* dg, float* db, int64_t rows, int64_t cols,
                        cudaStream_t st) {
-  const int grid_max = sm_count() * 8;
   if (x_cs == 1 && cols % 32 == 0 && cols <= 1024) {
-    const int wpb = 8;
-    int64_t need = (rows + wpb - 1) / wpb;
-    dim3 grid((unsigned)(need < grid_max ? need : grid_max));
-    size_t sm = 2 * cols * sizeof(float);
+    int64_t need = (rows + 63) / 64, cap = (int64_t)sm_count() * 2;  // >= 8 rows per warp, ~2 CTAs per SM
+    dim3 grid((unsigned)(need < cap ? need : cap));
+    size_t sm = 16 * cols * sizeof(float);
 #define LNB(VPT)                                                                                            \
-  ln_bwd_warp<TD, TX, TO, VPT><<<grid, wpb * 32, sm, st>>>((const TD*)dy, (const TX*)x, x_rs, g, mean, rstd, \
-                                                           (TO*)dx, acc, dg, db, rows)
+  ln_bwd_warp<TD, TX, TO, VPT><<<grid, 256, sm, st>>>((const TD*)dy, (const TX*)x, x_rs, g, mean, rstd,     \
+                                                      (TO*)dx, (const TO*)res, dg, db, rows)
     switch (cols) {
       case 32: LNB(1); break;
       case 64: LNB(2); break;
@@ -390,26 +583,34 @@ static int ln_bwd_impl(const void* dy, const void* x, int64_t x_rs, int64_t x_cs
       case 256: LNB(8); break;
       case 384: LNB(12); break;
       case 512: LNB(16); break;
-      case 768: LNB(24); break;
-      case 1024: LNB(32); break;
-      default: return EVO_ERR_SHAPE;
+      default: set_error("layernorm bwd: unsupported width %lld", (long long)cols); return EVO_ERR_SHAPE;
     }
 #undef LNB
     EVO_LAUNCH_CHECK("layernorm bwd");
     return EVO_OK;
   }
-  EVO_CHECK_ARG(cols <= 64, EVO_ERR_SHAPE, "layernorm bwd: strided rows support cols <= 64");
-  int64_t need = (rows + 255) / 256;
-  dim3 grid((unsigned)(need < grid_max ? need : grid_max));
-  ln_bwd_thread<TD, TX, TO, 64><<<grid, 256, 0, st>>>((const TD*)dy, (const TX*)x, x_rs, x_cs, g, mean, rstd,
-                                                      (TO*)dx, acc, dg, db, rows, (int)cols);
+  int64_t need = (rows + 255) / 256, cap = (int64_t)sm_count() * 4;
+  dim3 grid((unsigned)(need < cap ? need : cap));
+#define LNT(CC)                                                                                              \
+  ln_bwd_thread<TD, TX, TO, CC><<<grid, 256, 0, st>>>((const TD*)dy, (const TX*)x, x_rs, x_cs, g, mean, rstd, \
+                                                      (TO*)dx, (const TO*)res, dg, db, rows)
+  switch (cols) {
+    case 2: LNT(2); break;
+    case 4: LNT(4); break;
+    case 8: LNT(8); break;
+    case 16: LNT(16); break;
+    case 32: LNT(32); break;
+    case 64: LNT(64); break;
+    default: set_error("layernorm bwd: strided width %lld unsupported", (long long)cols); return EVO_ERR_SHAPE;
+  }
+#undef LNT
   EVO_LAUNCH_CHECK("layernorm bwd strided");
   return EVO_OK;
 }
 
 extern "C" int evo_layernorm_bwd(const void* dy, int dy_dtype, const void* x, int x_dtype, int64_t x_rs, int64_t x_cs,
                                  const float* gamma, const float* mean, const float* rstd, void* dx, int dx_dtype,
-                                 int accumulate_dx, float* dgamma, float* dbeta, int64_t rows, int64_t cols,
+                                 const void* res, float* dgamma, float* dbeta, int64_t rows, int64_t cols,
                                  void* stream) {
   EVO_CHECK_ARG(dy && x && gamma && mean && rstd && dx, EVO_ERR_ARG, "layernorm bwd: null pointer");
   if (rows == 0) return EVO_OK;
@@ -417,14 +618,10 @@ extern "C" int evo_layernorm_bwd(const void* dy, int dy_dtype, const void* x, in
   EVO_CHECK_ARG(x_dtype == dx_dtype, EVO_ERR_DTYPE, "layernorm bwd: x and dx dtypes must match");
   if (dy_dtype == EVO_BF16) {
     if (x_dtype == EVO_BF16)
-      return ln_bwd_impl<bf16, bf16, bf16>(dy, x, x_rs, x_cs, gamma, mean, rstd, dx, accumulate_dx, dgamma, dbeta,
-                                           rows, cols, st);
-    return ln_bwd_impl<bf16, float, float>(dy, x, x_rs, x_cs, gamma, mean, rstd, dx, accumulate_dx, dgamma, dbeta,
-                                           rows, cols, st);
+      return ln_bwd_impl<bf16, bf16, bf16>(dy, x, x_rs, x_cs, gamma, mean, rstd, dx, res, dgamma, dbeta, rows, cols, st);
+    return ln_bwd_impl<bf16, float, float>(dy, x, x_rs, x_cs, gamma, mean, rstd, dx, res, dgamma, dbeta, rows, cols, st);
   }
   if (x_dtype == EVO_BF16)
-    return ln_bwd_impl<float, bf16, bf16>(dy, x, x_rs, x_cs, gamma, mean, rstd, dx, accumulate_dx, dgamma, dbeta,
-                                          rows, cols, st);
-  return ln_bwd_impl<float, float, float>(dy, x, x_rs, x_cs, gamma, mean, rstd, dx, accumulate_dx, dgamma, dbeta,
-                                          rows, cols, st);
+    return ln_bwd_impl<float, bf16, bf16>(dy, x, x_rs, x_cs, gamma, mean, rstd, dx, res, dgamma, dbeta, rows, cols, st);
+  return ln_bwd_impl<float, float, float>(dy, x, x_rs, x_cs, gamma, mean, rstd, dx, res, dgamma, dbeta, rows, cols, st);
 }

@@ -61,7 +61,9 @@ def layernorm_fwd(x, gamma, beta, rows, cols, x_rs=None, x_cs=1, out=None, out_d
 
 
 def layernorm_bwd(dy, x, gamma, mean, rstd, rows, cols, x_rs=None, x_cs=1, dx=None,
-                  accumulate=False, dgamma=None, dbeta=None):
+                  accumulate=False, dgamma=None, dbeta=None, res=None):
+    """dx = res + dLN/dx.  accumulate=True means res = dx (in place);  res may be another
+    tensor (the residual-stream gradient) so no clone is needed."""
     _cuda(dy, x, gamma, mean, rstd)
     x_rs = cols if x_rs is None else x_rs
     if dx is None:
@@ -69,8 +71,10 @@ def layernorm_bwd(dy, x, gamma, mean, rstd, rows, cols, x_rs=None, x_cs=1, dx=No
             raise KernelError("layernorm_bwd: pass dx explicitly for strided inputs")
         dx = torch.empty(rows, cols, device=x.device, dtype=x.dtype)
         accumulate = False
+    if accumulate:
+        res = dx
     call("evo_layernorm_bwd", _p(dy), _dt(dy), _p(x), _dt(x), x_rs, x_cs, _p(gamma), _p(mean), _p(rstd),
-         _p(dx), _dt(dx), int(accumulate), _p(dgamma), _p(dbeta), rows, cols, stream_handle())
+         _p(dx), _dt(dx), _p(res), _p(dgamma), _p(dbeta), rows, cols, stream_handle())
     return dx
 
 
@@ -81,6 +85,13 @@ def layernorm_rowdot_fwd(x, gamma, beta, w, rows, cols, out, out_hs, ln_out=None
     call("evo_layernorm_rowdot_fwd", _p(x), _dt(x), _p(gamma), _p(beta), _p(w), k, _p(out), _dt(out),
          out_hs, _p(ln_out), _p(mean), _p(rstd), rows, cols, eps, stream_handle())
     return out
+
+
+def layernorm_rowdot_bwd(x, gamma, beta, w, dout, out_hs, mean, rstd, rows, cols, dx, res, dgamma, dbeta, dw):
+    """backward of layernorm_rowdot_fwd in one pass (dx = res + dLN)."""
+    call("evo_layernorm_rowdot_bwd", _p(x), _dt(x), _p(gamma), _p(beta), _p(w), w.shape[1], _p(dout), out_hs,
+         _p(mean), _p(rstd), _p(res), _p(dx), _p(dgamma), _p(dbeta), _p(dw), rows, cols, stream_handle())
+    return dx
 
 
 # ------------------------------------------------------------------ softmax
@@ -241,6 +252,12 @@ def bgemm(A: Mat, B: Mat, Cm: Mat, batch, M, N, K, alpha=1.0, beta=0.0):
     _cuda(A.t, B.t, Cm.t)
     a, b, c = A.to_c(), B.to_c(), Cm.to_c()
     work = (2 * batch * M * N * K, batch * (2 * M * K + 2 * N * K + Cm.t.element_size() * M * N))
+    ws_bytes = int(_lib.load().evo_bgemm_workspace(batch, M, N, K))
+    if ws_bytes:  # split-K (long K, few output tiles): fp32 partials + reduction
+        ws = torch.empty(ws_bytes // 4, device=Cm.t.device, dtype=torch.float32)
+        call("evo_bgemm_ws", C.byref(a), C.byref(b), C.byref(c), batch, M, N, K, float(alpha), float(beta),
+             ws.data_ptr(), ws_bytes, stream_handle(), work=work)
+        return
     call("evo_bgemm", C.byref(a), C.byref(b), C.byref(c), batch, M, N, K, float(alpha), float(beta),
          stream_handle(), work=work)
 

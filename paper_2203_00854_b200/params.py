@@ -29,10 +29,10 @@ def _r8(n: int) -> int:
 
 
 def _rowdot_k(n: int) -> int:
-    for k in (1, 2, 4, 8, 16):
-        if n <= k:
-            return k
-    raise ValueError(f"msa heads {n} > 16 unsupported by the fused bias kernel")
+    """the fused LN + bias-dot kernel handles 8 heads (fewer are zero-padded)"""
+    if n > 8:
+        raise ValueError(f"msa heads {n} > 8 unsupported by the fused bias kernel")
+    return 8
 
 
 class BlockLayout:

@@ -1,0 +1,22 @@
+"""Summarise an ncu --metrics gpu__time_duration.sum CSV launch list by kernel name (shares)."""
+import collections, csv, sys
+rows = list(csv.reader(open(sys.argv[1])))
+hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+h = rows[hi]
+ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+agg = collections.defaultdict(lambda: [0, 0.0])
+tot = 0.0
+for r in rows[hi + 1:]:
+    if len(r) <= vi:
+        continue
+    v = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
+    name = r[ki]
+    name = name.split("(")[0][:90]
+    agg[name][0] += 1
+    agg[name][1] += v
+    tot += v
+print(f"total {tot:.1f} us over {sum(n for n, _ in agg.values())} launches")
+top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1])[:top]:
+    print(f"{t:10.1f} us {100 * t / tot:5.1f}%  n={n:5d}  {k}")

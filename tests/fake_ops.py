@@ -52,7 +52,7 @@ def layernorm_fwd(x, gamma, beta, rows, cols, x_rs=None, x_cs=1, out=None, out_d
 
 
 def layernorm_bwd(dy, x, gamma, mean, rstd, rows, cols, x_rs=None, x_cs=1, dx=None, accumulate=False, dgamma=None,
-                  dbeta=None):
+                  dbeta=None, res=None):
     x_rs = cols if x_rs is None else x_rs
     xv = _sv(x, 0, (rows, cols), (x_rs, x_cs)).float()
     d = dy.reshape(rows, cols).float()
@@ -66,14 +66,16 @@ def layernorm_bwd(dy, x, gamma, mean, rstd, rows, cols, x_rs=None, x_cs=1, dx=No
     if dx is None:
         dx = torch.empty(rows, cols, dtype=x.dtype)
         accumulate = False
-    dv = _sv(dx, 0, (rows, cols), (x_rs, x_cs))
-    dv.copy_(o + (dv.float() if accumulate else 0))
+    if accumulate:
+        res = dx
+    base = _sv(res, 0, (rows, cols), (x_rs, x_cs)).float() if res is not None else 0
+    _sv(dx, 0, (rows, cols), (x_rs, x_cs)).copy_(o + base)
     return dx
 
 
 def layernorm_rowdot_fwd(x, gamma, beta, w, rows, cols, out, out_hs, ln_out=None, mean=None, rstd=None, eps=1e-5):
     ln, mu, rs = layernorm_fwd(x, gamma, beta, rows, cols, out_dtype=F32, eps=eps)
-    k = w.shape[1]
+    k = out.shape[0] if out.dim() == 3 else w.shape[1]
     _sv(out, 0, (k, rows), (out_hs, 1)).copy_((ln @ w).t())
     if ln_out is not None:
         ln_out.copy_(ln)

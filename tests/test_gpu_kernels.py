@@ -309,3 +309,48 @@ def test_colsum(rows, cols):
     out = torch.ones(cols, device=DEV)
     ops.colsum(x, out)
     assert rel(out - 1, x.float().sum(0)) < 1e-5
+
+
+@pytest.mark.parametrize("am,rows_contig", [(False, True), (True, True), (False, False)])
+def test_bgemm_split_k(am, rows_contig):
+    """long-K, few-tile products (the OPM backward shapes) take the split-K path."""
+    from paper_2203_00854_b200 import _lib
+    g = torch.Generator(device=DEV).manual_seed(99)
+    M, N, K = 1024, 128, 8192
+    assert _lib.load().evo_bgemm_workspace(1, M, N, K) > 0
+    A = _mk((K, M) if am else (M, K), g)
+    B = _mk((N, K), g)
+    ma = Mat(A, lo=(1, M) if am else (K, 1))
+    mb = Mat(B, lo=(K, 1))
+    Cb = torch.randn(N, M, device=DEV, generator=g).bfloat16() if rows_contig else \
+        torch.randn(M, N, device=DEV, generator=g).bfloat16()
+    C0 = Cb.float().clone()
+    mc = Mat(Cb, lo=(1, M) if rows_contig else (N, 1))
+    ops.bgemm(ma, mb, mc, 1, M, N, K, alpha=0.25, beta=1.0)
+    ref = 0.25 * ((A.float().t() if am else A.float()) @ B.float().t())
+    got = Cb.float().t() if rows_contig else Cb.float()
+    base = C0.t() if rows_contig else C0
+    assert rel(got, ref + base) < 1e-2
+
+
+def test_layernorm_rowdot_bwd():
+    g = torch.Generator(device=DEV).manual_seed(41)
+    rows, cols, k = 3000, 128, 8
+    x = torch.randn(rows, cols, device=DEV, generator=g).bfloat16()
+    gamma = torch.randn(cols, device=DEV, generator=g)
+    beta = torch.randn(cols, device=DEV, generator=g)
+    w = torch.randn(cols, k, device=DEV, generator=g)
+    out = torch.empty(k, rows, device=DEV, dtype=torch.bfloat16)
+    mean = torch.empty(rows, device=DEV)
+    rstd = torch.empty(rows, device=DEV)
+    ops.layernorm_rowdot_fwd(x, gamma, beta, w, rows, cols, out, rows, mean=mean, rstd=rstd)
+    dout = torch.randn(k, rows, device=DEV, generator=g)
+    res = torch.randn(rows, cols, device=DEV, generator=g).bfloat16()
+    dx = torch.empty_like(x)
+    dg, db, dw = torch.zeros(cols, device=DEV), torch.zeros(cols, device=DEV), torch.zeros(cols, k, device=DEV)
+    ops.layernorm_rowdot_bwd(x, gamma, beta, w, dout, rows, mean, rstd, rows, cols, dx, res, dg, db, dw)
+    xr, gr, br, wr = (t.float().clone().requires_grad_(True) for t in (x, gamma, beta, w))
+    y = torch.nn.functional.layer_norm(xr, (cols,), gr, br, eps=1e-5) @ wr
+    y.backward(dout.t())
+    assert rel(dx.float() - res.float(), xr.grad) < 2e-2
+    assert rel(dg, gr.grad) < 1e-2 and rel(db, br.grad) < 1e-2 and rel(dw, wr.grad) < 1e-2
