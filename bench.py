@@ -47,6 +47,12 @@ def _args():
     ap.add_argument("--blocks", type=int, default=N_BLOCKS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--workload", default="train", choices=["train", "longseq"],
+                    help="train: 48-block fwd+bwd at the training shape (BASELINE configs[1], default); "
+                         "longseq: 48-block forward (inference) at --n-res (configs[3])")
+    ap.add_argument("--n-res", type=int, default=1024)
+    ap.add_argument("--graph", type=int, default=1,
+                    help="1 GPU: replay the whole step as one captured CUDA graph in the timed region")
     return ap.parse_args()
 
 
@@ -178,36 +184,41 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     _lib.load()
-    cfg = EvoConfig(*TRAIN_DIMS)
+    longseq = args.workload == "longseq"
+    cfg = EvoConfig(*TRAIN_DIMS) if not longseq else EvoConfig(128, args.n_res, 256, 128, 8, 4, 32)
     nb = args.blocks
 
     # ------------------------------------------------------------------ workload
     m64, z64 = synthetic_inputs(cfg, 0)
     rng = np.random.default_rng(1)
-    gm64, gz64 = rng.normal(size=m64.shape), rng.normal(size=z64.shape)
+    gm64, gz64 = (rng.normal(size=m64.shape), rng.normal(size=z64.shape)) if not longseq else (None, None)
     if world == 1:
         stack = EvoformerStack(cfg, nb, seed=0, device=dev)
         m = torch.tensor(m64, device=dev).bfloat16()
         z = torch.tensor(z64, device=dev).bfloat16()
-        gm = torch.tensor(gm64, device=dev).bfloat16()
-        gz = torch.tensor(gz64, device=dev).bfloat16()
-
-        def step():
-            stack.zero_grad()
-            loss, dm, dz = stack.forward_backward(m, z, gm, gz)
-            return loss
+        if not longseq:
+            gm = torch.tensor(gm64, device=dev).bfloat16()
+            gz = torch.tensor(gz64, device=dev).bfloat16()
         parallelism = "single"
     else:
         from paper_2203_00854_b200.dap import DapStack
         stack = DapStack(cfg, nb, seed=0, device=dev)
         m, z = stack.shard_inputs(m64, z64, dev)
-        gm, gz = stack.shard_inputs(gm64, gz64, dev)
+        if not longseq:
+            gm, gz = stack.shard_inputs(gm64, gz64, dev)
+        parallelism = f"dap{world}"
+    del m64, z64
 
+    if longseq:
+        def step():
+            with torch.no_grad():
+                mo, zo, _ = stack.forward(m, z, save=False)
+            return zo
+    else:
         def step():
             stack.zero_grad()
             loss, dm, dz = stack.forward_backward(m, z, gm, gz)
             return loss
-        parallelism = f"dap{world}"
 
     def barrier():
         if world > 1:
@@ -225,8 +236,18 @@ def main():
     census = inst.summary()
     dominant = max(census, key=lambda k: census[k]["total_ms"]) if census else None
 
+    # ------------------------------------------------------------------ CUDA graph of the step
+    use_graph = bool(args.graph) and world == 1 and not longseq
+    if use_graph:
+        from paper_2203_00854_b200.evoformer import GraphedStep
+        gstep = GraphedStep(stack, m, z, gm, gz)
+        launches_eager = inst.launches()
+        run_step = gstep.replay
+    else:
+        run_step = step
+
     # ------------------------------------------------------------------ timed region
-    timed = _lib.Instrument(timed=(dominant,) if dominant else ())
+    timed = _lib.Instrument(timed=(dominant,) if dominant and not use_graph else ())
     clocks = ClockSampler(local)
     barrier()
     torch.cuda.synchronize()
@@ -237,7 +258,7 @@ def main():
     _lib.INSTRUMENT = timed
     e0.record(st)
     for _ in range(args.steps):
-        loss = step()
+        loss = run_step()
     e1.record(st)
     _lib.INSTRUMENT = None
     torch.cuda.synchronize()
@@ -249,12 +270,25 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_step = total_ms / args.steps
-    launches_per_step = timed.launches() / args.steps
-    dom = timed.summary().get(dominant, None)
+    if use_graph:
+        # the graph holds exactly the kernels of one eager step; per-launch durations of the
+        # dominant entry point are taken with CUDA events on one eager step right after
+        launches_per_step = launches_eager
+        post = _lib.Instrument(timed=(dominant,) if dominant else ())
+        _lib.INSTRUMENT = post
+        step()
+        _lib.INSTRUMENT = None
+        torch.cuda.synchronize()
+        dom = post.summary().get(dominant, None)
+        if dom:
+            dom = dict(dom, launches=dom["launches"] * args.steps, total_ms=dom["total_ms"] * args.steps)
+    else:
+        launches_per_step = timed.launches() / args.steps
+        dom = timed.summary().get(dominant, None)
 
     # ------------------------------------------------------------------ e2e via the public API
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not longseq:
         hm = torch.tensor(m64, dtype=torch.float32).pin_memory() if world == 1 else None
         if world == 1:
             hz = torch.tensor(z64, dtype=torch.float32).pin_memory()
@@ -270,8 +304,12 @@ def main():
                 dz_ = hz.to(dev, non_blocking=True).bfloat16()
                 dgm = hgm.to(dev, non_blocking=True).bfloat16()
                 dgz = hgz.to(dev, non_blocking=True).bfloat16()
-                stack.zero_grad()
-                loss, _, _ = stack.forward_backward(dm_, dz_, dgm, dgz)
+                if use_graph:   # GraphedStep: static inputs refreshed from this step's host data
+                    gstep.set_inputs(dm_, dz_, dgm, dgz)
+                    loss = gstep.replay()
+                else:
+                    stack.zero_grad()
+                    loss, _, _ = stack.forward_backward(dm_, dz_, dgm, dgz)
                 hloss.copy_(loss.view(1), non_blocking=True)
                 torch.cuda.current_stream().synchronize()
             b.record(st)
@@ -279,7 +317,8 @@ def main():
             e2e_step = a.elapsed_time(b) / args.steps
             e2e = {"value": round(e2e_step / nb, 4), "unit": UNIT, "h2d_bytes_per_step": bi,
                    "d2h_bytes_per_step": 4, "ms_per_step": round(e2e_step, 3),
-                   "path": "EvoformerStack.forward_backward with pinned fp32 host inputs, loss read back"}
+                   "path": ("GraphedStep(EvoformerStack) replay" if use_graph else "EvoformerStack.forward_backward")
+                   + ": pinned fp32 host inputs copied in every step, loss read back"}
         else:
             e2e = stack.e2e(m64, z64, gm64, gz64, args.steps, nb)
 
@@ -309,25 +348,34 @@ def main():
                      "launches_per_step": dom["launches"] / args.steps, "avg_launch_ms": round(dom["avg_ms"], 4),
                      "share_of_step": round(dom["total_ms"] / total_ms, 4),
                      "algorithmic_flops_per_launch": flops, "algorithmic_bytes_per_launch": byts,
-                     "arithmetic_intensity": round(ai, 1)})
+                     "arithmetic_intensity": round(ai, 1),
+                     "timed_on": "eager step after the graph-replayed timed region" if use_graph
+                     else "inside the timed region"})
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not longseq:
         v, cores, sample = cpu_fwd_bwd_sample(1)
         cpu = {"value": round(v, 1), "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
 
     if rank == 0:
+        if longseq:
+            metric = f"long-seq inference ms (Nres{cfg.n_res}/Nseq{cfg.n_seq}, {nb}-block forward)"
+            value, unit = round(ms_step, 3), "ms/stack-forward"
+            workload = f"evoformer_stack_forward_longseq_nres{cfg.n_res}"
+            step_desc = f"{nb}-block forward, no grad (inference)"
+        else:
+            metric, value, unit = METRIC, round(ms_step / nb, 4), UNIT
+            workload = "evoformer_stack_fwd_bwd_training_shape"
+            step_desc = "48-block forward + backward incl. all weight gradients; no optimizer"
         line = {
-            "metric": METRIC, "value": round(ms_step / nb, 4), "unit": UNIT, "n_gpus": world,
+            "metric": metric, "value": value, "unit": unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (reference draw order: default_rng(0) m then z; init_block_params(cfg, i))",
-            "config": {"workload": "evoformer_stack_fwd_bwd_training_shape", "blocks": nb, "n_seq": 128,
-                       "n_res": 256, "c_m": 256, "c_z": 128, "heads_msa": 8, "heads_pair": 4,
-                       "hidden_proj": 32, "parallelism": parallelism,
-                       "l2": "per-step working set ~45 GB >> 126 MB L2 (no flush needed)",
-                       "step": "48-block forward + backward incl. all weight gradients; no optimizer"},
+            "config": {"workload": workload, "blocks": nb, "n_seq": cfg.n_seq, "n_res": cfg.n_res, "c_m": 256,
+                       "c_z": 128, "heads_msa": 8, "heads_pair": 4, "hidden_proj": 32, "parallelism": parallelism,
+                       "l2": "per-step working set >> 126 MB L2 (no flush needed)", "step": step_desc},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches_per_step * args.steps),
-            "gpu_launches_per_step": launches_per_step, "clocks": clk,
+            "gpu_launches_per_step": launches_per_step, "clocks": clk, "cuda_graph": use_graph,
             "kernel_census_ms_per_step": {k: round(v["total_ms"], 3) for k, v in census.items()},
         }
         print(json.dumps(line), flush=True)

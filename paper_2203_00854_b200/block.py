@@ -192,8 +192,11 @@ def transition_fwd(bp: BlockParams, mod: str, x2d, rows: int, save=True):
     H = x2d.shape[1]
     h, f = bp.h, bp.f
     ln, mean, rstd = ops.layernorm_fwd(x2d, f[f"{mod}.ln_g"], f[f"{mod}.ln_b"], rows, H)
-    hid = _mm(ln, h[f"{mod}.w1"])
-    ops.bias_act_fwd(hid, f[f"{mod}.b1"], rows, hid.shape[1], relu=True)
+    if ln.is_cuda:  # bias + ReLU in the cuBLASLt epilogue (RELU_BIAS): hid is written once
+        hid = torch._addmm_activation(h[f"{mod}.b1"], ln, h[f"{mod}.w1"])
+    else:
+        hid = _mm(ln, h[f"{mod}.w1"])
+        ops.bias_act_fwd(hid, f[f"{mod}.b1"], rows, hid.shape[1], relu=True)
     y = _mm(hid, h[f"{mod}.w2"])
     out = ops.gated_residual_fwd(x2d, y, f[f"{mod}.b2"], rows, H)
     sv = Saved(x=x2d, ln=ln, mean=mean, rstd=rstd, hid=hid, mod=mod) if save else None

@@ -33,7 +33,7 @@ __all__ = ["evoformer_block", "msa_row_attention", "msa_row_bias", "msa_row_atte
            "msa_col_attention", "transition", "outer_product_mean", "tri_update_outgoing",
            "tri_update_incoming", "pair_attention_row", "pair_attention_col", "layernorm",
            "fused_softmax_mask_bias", "BlockParams", "block_forward_backward", "EvoformerStack",
-           "EvoformerBlockFunction"]
+           "EvoformerBlockFunction", "GraphedStep"]
 
 _DEV = "cuda"
 
@@ -413,6 +413,42 @@ class EvoformerStack:
         loss = (mo.float() * gm.float()).sum() + (zo.float() * gz.float()).sum()
         dm, dz = self.backward(saved, gm.to(torch.bfloat16), gz.to(torch.bfloat16))
         return loss, dm, dz
+
+
+class GraphedStep:
+    """One fwd+bwd step of a stack captured as a single CUDA graph (no host work per
+    kernel at replay).  ``inputs`` are copied into static buffers; ``replay()`` returns
+    the static loss tensor; gradients land in the stack's BlockParams.grad buffers and
+    ``dm`` / ``dz``.  Works for EvoformerStack and dap.DapStack (NCCL collectives are
+    capturable)."""
+
+    def __init__(self, stack, m, z, gm, gz, warmup: int = 2):
+        self.stack = stack
+        self.m, self.z, self.gm, self.gz = (t.detach().clone() for t in (m, z, gm, gz))
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(warmup):
+                self._body()
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.loss, self.dm, self.dz = self._body()
+
+    def _body(self):
+        self.stack.zero_grad()
+        return self.stack.forward_backward(self.m, self.z, self.gm, self.gz)
+
+    def set_inputs(self, m=None, z=None, gm=None, gz=None):
+        for dst, src in ((self.m, m), (self.z, z), (self.gm, gm), (self.gz, gz)):
+            if src is not None:
+                dst.copy_(src, non_blocking=True)
+
+    def replay(self):
+        self.graph.replay()
+        return self.loss
 
 
 class EvoformerBlockFunction(torch.autograd.Function):
