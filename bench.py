@@ -207,7 +207,7 @@ def main():
         if not longseq:
             gm, gz = stack.shard_inputs(gm64, gz64, dev)
         parallelism = f"dap{world}"
-    del m64, z64
+
 
     if longseq:
         def step():

@@ -81,9 +81,11 @@ def attention_fwd(bp: BlockParams, mod: str, x2d, B: int, L: int, kind: str, bia
     lse = torch.empty(B, nh, L, device=x2d.device, dtype=F32)
     sbr, slr = _attn_geometry(kind, B, L)
     S = lambda t, ld, off=0: Strided(t, sbr * ld, slr * ld, off)
+    if callable(bias):  # deferred (e.g. a DAP all-gather completing while the GEMMs above ran)
+        bias = bias()
     if bias is None:
         bt, bs, boff = None, (0, 0, 0, 0), 0
-    elif bias == "pair":
+    elif isinstance(bias, str) and bias == "pair":
         bt, bs, boff = qkv, (sbr * ldq, 1, 0, slr * ldq), 3 * nh * c
     else:
         bt, bs, boff = bias, (0, L * L, L, 1), 0
@@ -96,7 +98,7 @@ def attention_fwd(bp: BlockParams, mod: str, x2d, B: int, L: int, kind: str, bia
     sv = None
     if save:
         sv = Saved(x=x2d, ln=ln, mean=mean, rstd=rstd, qkv=qkv, gpre=gpre, og=og, orw=orw, lse=lse,
-                   desc=desc, B=B, L=L, kind=kind, bias=bias, mod=mod)
+                   desc=desc, B=B, L=L, kind=kind, bias=bias, mod=mod)  # bias: resolved tensor / "pair" / None
     return out, sv
 
 
@@ -120,15 +122,16 @@ def attention_bwd(bp: BlockParams, sv: Saved, dx_new):
     bias = sv["bias"]
     if bias is None:
         dbias, dbs = None, (0, 0, 0, 0)
-    elif bias == "pair":
+    elif isinstance(bias, str) and bias == "pair":
         dbias, dbs = torch.zeros(B, nh, L, device=dev, dtype=F32), (nh * L, L, 0, 1)
     else:
         dbias, dbs = torch.zeros(nh, L, L, device=dev, dtype=F32), (0, L * L, L, 1)
-    ws = torch.empty(ops.attention_bwd_workspace(B, L, nh, c, batch_reduced_bias=bias not in (None, "pair")),
+    full_bias = bias is not None and not isinstance(bias, str)
+    ws = torch.empty(ops.attention_bwd_workspace(B, L, nh, c, batch_reduced_bias=full_bias),
                      device=dev, dtype=torch.uint8)
     ops.attention_bwd(sv["desc"], S(dog, nh * c), S(dqkv, ldq, 0), S(dqkv, ldq, nh * c), S(dqkv, ldq, 2 * nh * c),
                       S(dgpre, nh * c), ws, dbias=dbias, dbias_s=dbs)
-    if bias == "pair":
+    if isinstance(bias, str) and bias == "pair":
         cols = dqkv[:, 3 * nh * c:3 * nh * c + nh]
         if kind == "row":
             cols.view(B, L, nh).copy_(dbias.permute(0, 2, 1))
@@ -142,7 +145,7 @@ def attention_bwd(bp: BlockParams, sv: Saved, dx_new):
     dln = _mm(dqkv, h[f"{mod}.w_qkv"].t())
     ops.layernorm_bwd(dln, sv["x"], f[f"{mod}.ln_g"], sv["mean"], sv["rstd"], rows, H, dx=dx, accumulate=True,
                       dgamma=g[f"{mod}.ln_g"], dbeta=g[f"{mod}.ln_b"])
-    return dx, (dbias if bias not in (None, "pair") else None)
+    return dx, (dbias if full_bias else None)
 
 
 # ----------------------------------------------------------------------------- msa_row bias

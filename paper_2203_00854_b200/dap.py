@@ -131,17 +131,18 @@ class DapComm:
         if self.ledger is not None:
             self.ledger.record(category, [elems] * self.N)
 
-    def all_gather(self, t, category="all_gather"):
+    def all_gather(self, t, category="all_gather", async_op=False):
+        """-> out [N, *t.shape]  (or (out, handle) with async_op: call handle.wait() before use)"""
         t = t.contiguous()
         out = torch.empty((self.N,) + tuple(t.shape), dtype=t.dtype, device=t.device)
         if self.N == 1:
             out[0].copy_(t)
-            return out
+            return (out, _Done()) if async_op else out
         # concatenated-along-dim-0 form (accepted by NCCL and gloo); same memory as [N, ...]
-        self.dist.all_gather_into_tensor(out.view((self.N * t.shape[0],) + tuple(t.shape[1:])), t,
-                                         group=self.group)
+        work = self.dist.all_gather_into_tensor(out.view((self.N * t.shape[0],) + tuple(t.shape[1:])), t,
+                                                group=self.group, async_op=async_op)
         self._rec(category, t.numel() * (self.N - 1))
-        return out
+        return (out, work) if async_op else out
 
     def reduce_scatter(self, t, category="reduce_scatter"):
         t = t.contiguous()
@@ -152,14 +153,14 @@ class DapComm:
         self._rec(category, t[0].numel() * (self.N - 1))
         return out
 
-    def all_to_all(self, t, category="all_to_all"):
+    def all_to_all(self, t, category="all_to_all", async_op=False):
         t = t.contiguous()
         if self.N == 1:
-            return t
+            return (t, _Done()) if async_op else t
         out = torch.empty_like(t)
-        self.dist.all_to_all_single(out, t, group=self.group)
+        work = self.dist.all_to_all_single(out, t, group=self.group, async_op=async_op)
         self._rec(category, t.numel() - t.numel() // self.N)
-        return out
+        return (out, work) if async_op else out
 
     def all_reduce_(self, t, category="grad_all_reduce"):
         if self.N == 1:
@@ -174,6 +175,13 @@ class DapComm:
         t = torch.tensor([x], device="cuda" if torch.cuda.is_available() else "cpu")
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
         return float(t.item())
+
+
+class _Done:
+    """handle of an already-completed collective"""
+
+    def wait(self):
+        return None
 
 
 class ThreadMesh:
@@ -209,11 +217,12 @@ class ThreadComm(DapComm):
         if self.ledger is not None and self.rank == 0:
             self.ledger.record(category, [elems] * self.N)
 
-    def all_gather(self, t, category="all_gather"):
+    def all_gather(self, t, category="all_gather", async_op=False):
         parts = self.mesh.exchange(self.rank, t.contiguous())
         if self.N > 1:
             self._rec(category, t.numel() * (self.N - 1))
-        return torch.stack(parts, 0)
+        out = torch.stack(parts, 0)
+        return (out, _Done()) if async_op else out
 
     def reduce_scatter(self, t, category="reduce_scatter"):
         parts = self.mesh.exchange(self.rank, t.contiguous())
@@ -224,11 +233,12 @@ class ThreadComm(DapComm):
             out += p[self.rank]
         return out
 
-    def all_to_all(self, t, category="all_to_all"):
+    def all_to_all(self, t, category="all_to_all", async_op=False):
         parts = self.mesh.exchange(self.rank, t.contiguous())
         if self.N > 1:
             self._rec(category, t.numel() - t.numel() // self.N)
-        return torch.stack([p[self.rank] for p in parts], 0)
+        out = torch.stack([p[self.rank] for p in parts], 0)
+        return (out, _Done()) if async_op else out
 
     def all_reduce_(self, t, category="grad_all_reduce"):
         parts = self.mesh.exchange(self.rank, t.clone())
@@ -242,29 +252,44 @@ class ThreadComm(DapComm):
 
 
 # ----------------------------------------------------------------------------- axis switches
-def switch_rows_to_cols(comm: DapComm, x):
+def switch_rows_to_cols(comm: DapComm, x, async_op=False):
     """[A/N, Bf, C] sharded on axis 0 -> [A, Bf/N, C] sharded on axis 1
     (all_to_all_switch_axis(t, 1), sharding.py:130-159).  The send side packs the
     destination-major buffer; the received rank-major buffer IS the result."""
     N = comm.N
     if N == 1:
-        return x
+        return (lambda: x) if async_op else x
     Al, Bf, C = x.shape
     if Bf % N:
         raise ShardError(f"extent {Bf} on axis 1 not divisible by {N} devices")
     send = x.view(Al, N, Bf // N, C).permute(1, 0, 2, 3)
+    if async_op:
+        recv, work = comm.all_to_all(send, async_op=True)
+
+        def finish():
+            work.wait()
+            return recv.view(N * Al, Bf // N, C)
+        return finish
     return comm.all_to_all(send).view(N * Al, Bf // N, C)
 
 
-def switch_cols_to_rows(comm: DapComm, x):
+def switch_cols_to_rows(comm: DapComm, x, async_op=False):
     """[A, Bl, C] sharded on axis 1 -> [A/N, Bl*N, C] sharded on axis 0.  The send
-    buffer is x itself (chunks along axis 0 are contiguous); the receive side unpacks."""
+    buffer is x itself (chunks along axis 0 are contiguous); the receive side unpacks.
+    async_op: returns a zero-argument callable that waits and unpacks (DAO overlap)."""
     N = comm.N
     if N == 1:
-        return x
+        return (lambda: x) if async_op else x
     A, Bl, C = x.shape
     if A % N:
         raise ShardError(f"extent {A} on axis 0 not divisible by {N} devices")
+    if async_op:
+        recv, work = comm.all_to_all(x.view(N, A // N, Bl, C), async_op=True)
+
+        def finish():
+            work.wait()
+            return recv.permute(1, 0, 2, 3).reshape(A // N, N * Bl, C)
+        return finish
     recv = comm.all_to_all(x.view(N, A // N, Bl, C))
     return recv.permute(1, 0, 2, 3).reshape(A // N, N * Bl, C)
 
@@ -285,17 +310,24 @@ def dap_block_fwd(bp, comm: DapComm, m_loc, z_loc, save=True):
     sv = {}
     # 1) pair-derived row-attention bias from local pair rows, gathered (dap_block.py:63-64)
     bias_loc, sv["bias"] = B.msa_row_bias_fwd(bp, z_loc.reshape(Rl * R, Hz), Rl, R, save)
-    g = comm.all_gather(bias_loc, "bias_gather")                     # [N, nh, Rl, R]
-    bias = g.permute(1, 0, 2, 3).reshape(nh, R, R) if N > 1 else g[0]
-    m2, sv["msa_row"] = B.attention_fwd(bp, "msa_row", m_loc.reshape(Sl * R, Hm), Sl, R, "row", bias=bias,
+    # DAO: the gather runs on NCCL's stream while msa_row's LN + q/k/v/g GEMMs run here
+    g, work = comm.all_gather(bias_loc, "bias_gather", async_op=True)    # [N, nh, Rl, R]
+
+    def bias_ready():
+        work.wait()
+        return g.permute(1, 0, 2, 3).reshape(nh, R, R) if N > 1 else g[0]
+    m2, sv["msa_row"] = B.attention_fwd(bp, "msa_row", m_loc.reshape(Sl * R, Hm), Sl, R, "row", bias=bias_ready,
                                         save=save)
     # 2) sequence shard -> residue shard (dap_block.py:69)
     m_r = switch_rows_to_cols(comm, m2.view(Sl, R, Hm))               # [S, Rl, Hm]
     m2, sv["msa_col"] = B.attention_fwd(bp, "msa_col", m_r.reshape(S * Rl, Hm), Rl, S, "col", save=save)
     m2, sv["msa_trans"] = B.transition_fwd(bp, "msa_trans", m2, S * Rl, save)
+    # DAO: m is final here; its switch back to the sequence shard overlaps the pair stack
+    m_out_ready = None  # issued after the OPM (which still reads m2)
     # 3) outer product mean: right projection gathered (dap_block.py:81-94)
     gat = (lambda t: comm.all_gather(t)) if N > 1 else None
     z2, sv["opm"] = B.opm_fwd(bp, m2, z_loc.reshape(Rl * R, Hz), S, Rl, save, gather=gat)
+    m_out_ready = switch_cols_to_rows(comm, m2.view(S, Rl, Hm), async_op=True)
     # 4) outgoing triangle: b gathered across the row shard (dap_block.py:98-111)
     z2, sv["tri_out"] = B.triangle_fwd(bp, "tri_out", z2, R, save, Rl=Rl, gather=gat)
     # 5) row shard -> column shard, incoming triangle gathers a (dap_block.py:114-128)
@@ -311,8 +343,8 @@ def dap_block_fwd(bp, comm: DapComm, m_loc, z_loc, save=True):
                                          save=save)
     z2, sv["pair_trans"] = B.transition_fwd(bp, "pair_trans", z2, R * Rl, save)
     # 8) restore canonical shards (dap_block.py:150-151)
-    m_out = switch_cols_to_rows(comm, m2.view(S, Rl, Hm))             # [Sl, R, Hm]
     z_out = switch_cols_to_rows(comm, z2.view(R, Rl, Hz))             # [Rl, R, Hz]
+    m_out = m_out_ready()                                             # [Sl, R, Hm]
     return m_out.contiguous(), z_out.contiguous(), (sv if save else None)
 
 
@@ -327,8 +359,8 @@ def dap_block_bwd(bp, comm: DapComm, sv, dm_loc, dz_loc):
     Sl, Rl = S // N, R // N
     nh = cfg.n_head_msa
     rs = (lambda t: comm.reduce_scatter(t)) if N > 1 else None
+    dm_r_ready = switch_rows_to_cols(comm, dm_loc.view(Sl, R, Hm), async_op=True)  # overlaps the pair stack
     dz_c = switch_rows_to_cols(comm, dz_loc.view(Rl, R, Hz))          # inverse of step 8
-    dm_r = switch_rows_to_cols(comm, dm_loc.view(Sl, R, Hm))
     dz2 = B.transition_bwd(bp, sv["pair_trans"], dz_c.reshape(R * Rl, Hz).contiguous())
     dz2, _ = B.attention_bwd(bp, sv["pair_col"], dz2)
     dz_r = switch_cols_to_rows(comm, dz2.view(R, Rl, Hz))             # inverse of step 7
@@ -337,7 +369,7 @@ def dap_block_bwd(bp, comm: DapComm, sv, dm_loc, dz_loc):
     dz2 = B.triangle_bwd(bp, sv["tri_in"], dz_c.reshape(R * Rl, Hz).contiguous(), reduce_scatter=rs)
     dz_r = switch_cols_to_rows(comm, dz2.view(R, Rl, Hz))             # inverse of step 5
     dz2 = B.triangle_bwd(bp, sv["tri_out"], dz_r.reshape(Rl * R, Hz).contiguous(), reduce_scatter=rs)
-    dm2 = dm_r.reshape(S * Rl, Hm).contiguous().clone()
+    dm2 = dm_r_ready().reshape(S * Rl, Hm).contiguous().clone()
     B.opm_bwd(bp, sv["opm"], dz2, dm2, reduce_scatter=rs)
     dm2 = B.transition_bwd(bp, sv["msa_trans"], dm2)
     dm2, _ = B.attention_bwd(bp, sv["msa_col"], dm2)
