@@ -280,8 +280,8 @@ def main():
         _lib.INSTRUMENT = None
         torch.cuda.synchronize()
         dom = post.summary().get(dominant, None)
-        if dom:
-            dom = dict(dom, launches=dom["launches"] * args.steps, total_ms=dom["total_ms"] * args.steps)
+        if dom:  # one step's launches -> per-step share as if over the K timed steps
+            dom = dict(dom, step_ms=dom["total_ms"])
     else:
         launches_per_step = timed.launches() / args.steps
         dom = timed.summary().get(dominant, None)
@@ -345,8 +345,9 @@ def main():
             roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                     "frac": round(ach / hbm, 4)}
         roof.update({"traffic": None, "kernel": dominant, "peak_source": peak_src,
-                     "launches_per_step": dom["launches"] / args.steps, "avg_launch_ms": round(dom["avg_ms"], 4),
-                     "share_of_step": round(dom["total_ms"] / total_ms, 4),
+                     "launches_per_step": dom["launches"] if use_graph else dom["launches"] / args.steps,
+                     "avg_launch_ms": round(dom["avg_ms"], 4),
+                     "share_of_step": round((dom["step_ms"] / ms_step) if use_graph else (dom["total_ms"] / total_ms), 4),
                      "algorithmic_flops_per_launch": flops, "algorithmic_bytes_per_launch": byts,
                      "arithmetic_intensity": round(ai, 1),
                      "timed_on": "eager step after the graph-replayed timed region" if use_graph
