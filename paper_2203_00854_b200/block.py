@@ -36,8 +36,8 @@ def _mm(a, b):
 
 def _wgrad(x, dy, out):
     """out (fp32) = x^T @ dy with fp32 accumulation and output."""
-    if x.is_cuda:
-        out.copy_(torch.mm(x.t(), dy, out_dtype=F32))
+    if x.is_cuda:  # cuBLAS writes the fp32 result straight into the grad buffer view
+        torch.mm(x.t(), dy, out_dtype=F32, out=out)
     else:  # CPU only in the host-logic tests (fake kernel backend)
         out.copy_(x.t().float() @ dy.float())
 

@@ -2,8 +2,9 @@
 // tcgen05.  The reference has no backward; the gradient oracle is
 // the torch float64 restatement in oracle/evoformer_torch.py.
 //
-//   prep   (warp per row)  dO = dout * sigmoid(g);  dg = dout * O * s(1-s);  D = rowsum(dO * O)
-//   main   one CTA = (batch, head, 128-key tile), 8 warps, loops over 128-query tiles:
+//   main   one CTA = (batch, head, 128-key tile), 8 warps, loops over 128-query tiles; the
+//          gate backward is fused into the query-tile load (dO = dout*sigmoid(g) staged in
+//          smem, D = rowsum(dO*O), dg = dout*O*s(1-s) written by the key-tile-0 CTAs):
 //            S^T  = K Q^T            (tcgen05, M=keys N=queries)  -> TMEM cols [0,128)
 //            dP^T = V dO^T           (tcgen05)                    -> TMEM cols [128,256)
 //            P^T  = exp2(S^T*scale + bias - lse), dS^T = P^T (dP^T - D)   (registers)
@@ -190,6 +191,9 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int G
     fence_mbar_init();
   }
   const int64_t HC = (int64_t)H * c;
+  // gate backward fused into the tile load: dO = dout * sigmoid(g) (staged in smem),
+  // D = rowsum(dO * O) (4 lanes per row for c = 32), and - by the key-tile-0 CTAs only -
+  // dg = dout * O * s(1-s) written once per query row.
   auto issue_loads = [&](int64_t b, int qt, bool with_kv) {
     const int q0 = qt * BW_BQ;
     if (with_kv) {
@@ -197,12 +201,52 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int G
       bw_load<CP>(sb + SM::V, F.v + b * F.v_sb + (int64_t)h * c, F.v_sl, k0, L - k0, c);
     }
     bw_load<CP>(sb + SM::Q, F.q + b * F.q_sb + (int64_t)h * c, F.q_sl, q0, L - q0, c);
-    bw_load<CP>(sb + SM::DO, P.dO + b * (int64_t)L * HC + (int64_t)h * c, HC, q0, L - q0, c);
     cp_async_commit();
     if (threadIdx.x < BW_BQ) {
       const int qq = q0 + threadIdx.x;
       s_lse[threadIdx.x] = qq < L ? F.lse[(b * H + h) * (int64_t)L + qq] * LOG2E_ : 0.f;
-      s_D[threadIdx.x] = qq < L ? P.Dsum[(b * H + h) * (int64_t)L + qq] : 0.f;
+    }
+    constexpr int CPR = CP / 8;
+    for (int ch = threadIdx.x; ch < BW_BQ * CPR; ch += 256) {
+      const int r = ch / CPR, d0 = (ch % CPR) * 8, qq = q0 + r;
+      float dO[8], part = 0.f;
+      if (qq < L && d0 < c) {
+        float dout[8], g[8], o[8];
+        const uint4 ud = *reinterpret_cast<const uint4*>(P.dout + b * P.do_sb + (int64_t)qq * P.do_sl + h * c + d0);
+        const uint4 ug = *reinterpret_cast<const uint4*>(F.g + b * F.g_sb + (int64_t)qq * F.g_sl + h * c + d0);
+        const uint4 uo = *reinterpret_cast<const uint4*>(F.orw + b * F.r_sb + (int64_t)qq * F.r_sl + h * c + d0);
+        unpack_bf16x2(ud.x, dout[0], dout[1]); unpack_bf16x2(ud.y, dout[2], dout[3]);
+        unpack_bf16x2(ud.z, dout[4], dout[5]); unpack_bf16x2(ud.w, dout[6], dout[7]);
+        unpack_bf16x2(ug.x, g[0], g[1]); unpack_bf16x2(ug.y, g[2], g[3]);
+        unpack_bf16x2(ug.z, g[4], g[5]); unpack_bf16x2(ug.w, g[6], g[7]);
+        unpack_bf16x2(uo.x, o[0], o[1]); unpack_bf16x2(uo.y, o[2], o[3]);
+        unpack_bf16x2(uo.z, o[4], o[5]); unpack_bf16x2(uo.w, o[6], o[7]);
+        float dg[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float sg = sigmoidf_(g[e]);
+          dO[e] = dout[e] * sg;
+          dg[e] = dout[e] * o[e] * sg * (1.f - sg);
+        }
+        // D uses the bf16-rounded dO that the MMAs see
+#pragma unroll
+        for (int e = 0; e < 8; ++e) part += bf2f(f2bf(dO[e])) * o[e];
+        if (blockIdx.x == 0) {
+          uint4 w;
+          w.x = pack_bf16x2(dg[0], dg[1]); w.y = pack_bf16x2(dg[2], dg[3]);
+          w.z = pack_bf16x2(dg[4], dg[5]); w.w = pack_bf16x2(dg[6], dg[7]);
+          *reinterpret_cast<uint4*>(P.dg + b * P.dg_sb + (int64_t)qq * P.dg_sl + h * c + d0) = w;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) dO[e] = 0.f;
+      }
+      st_shared_v4(sb + SM::DO + kmajor_off(r, d0, 128), pack_bf16x2(dO[0], dO[1]), pack_bf16x2(dO[2], dO[3]),
+                   pack_bf16x2(dO[4], dO[5]), pack_bf16x2(dO[6], dO[7]));
+      // the CPR chunks of a row sit on consecutive lanes
+#pragma unroll
+      for (int o = 1; o < CPR; o <<= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      if (ch % CPR == 0) s_D[r] = part;
     }
   };
   issue_loads(b_begin, 0, true);
@@ -494,8 +538,6 @@ extern "C" int evo_gated_attention_bwd(const EvoAttnBwdDesc* d, void* stream) {
     cudaError_t e = cudaMemsetAsync(p.dQacc, 0, (size_t)(B * L * H * c) * 4, st);
     if (e != cudaSuccess) return cuda_status(e, "attention bwd memset");
   }
-  attn_bwd_prep<<<(unsigned)((B * L + 7) / 8), 256, 0, st>>>(p, B);
-  EVO_LAUNCH_CHECK("attention bwd prep");
   if (c <= 16) rc = launch_bwd<16>(p, B, dq_partial, st);
   else if (c <= 32) rc = launch_bwd<32>(p, B, dq_partial, st);
   else rc = launch_bwd<64>(p, B, dq_partial, st);

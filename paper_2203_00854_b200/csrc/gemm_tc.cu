@@ -302,11 +302,12 @@ static bool runs8(const MatArg& a, int d) {
   return lo == 1 && (split % 8) == 0;
 }
 
-template <int BN, bool AM, bool BMN, typename TC>
-static int launch_bgemm(MatArg A, MatArg B, MatArg C, int64_t batch, int64_t M, int64_t N, int64_t K, float alpha,
-                        float beta, int c_mode, int splits, float* ws, cudaStream_t st) {
-  constexpr int STAGES = 3;
-  const size_t smem = STAGES * (GEMM_BM * GEMM_BK * 2 + BN * GEMM_BK * 2);
+template <int BN, bool AM, bool BMN, typename TC, int STAGES>
+static int launch_bgemm_s(MatArg A, MatArg B, MatArg C, int64_t batch, int64_t M, int64_t N, int64_t K, float alpha,
+                          float beta, int c_mode, int splits, float* ws, cudaStream_t st) {
+  const size_t pipe = STAGES * (GEMM_BM * GEMM_BK * 2 + BN * GEMM_BK * 2);
+  const size_t stage_tile = (size_t)GEMM_BM * (BN * sizeof(TC) + 16);  // epilogue staging (reuses the ring)
+  const size_t smem = pipe > stage_tile ? pipe : stage_tile;
   auto kern = bgemm_kernel<BN, AM, BMN, STAGES, TC>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
@@ -328,6 +329,16 @@ static int launch_bgemm(MatArg A, MatArg B, MatArg C, int64_t batch, int64_t M, 
     EVO_LAUNCH_CHECK("bgemm split-K reduce");
   }
   return EVO_OK;
+}
+
+// short K (<= 2 k-tiles, e.g. the OPM contraction over N_s = 128): 2 stages -> 64 KB smem,
+// 3 CTAs per SM so one CTA's epilogue overlaps another's main loop
+template <int BN, bool AM, bool BMN, typename TC>
+static int launch_bgemm(MatArg A, MatArg B, MatArg C, int64_t batch, int64_t M, int64_t N, int64_t K, float alpha,
+                        float beta, int c_mode, int splits, float* ws, cudaStream_t st) {
+  const int64_t kt = (K + GEMM_BK - 1) / GEMM_BK / splits;
+  if (kt <= 2) return launch_bgemm_s<BN, AM, BMN, TC, 2>(A, B, C, batch, M, N, K, alpha, beta, c_mode, splits, ws, st);
+  return launch_bgemm_s<BN, AM, BMN, TC, 3>(A, B, C, batch, M, N, K, alpha, beta, c_mode, splits, ws, st);
 }
 
 template <int BN, typename TC>

@@ -81,31 +81,40 @@ __global__ void __launch_bounds__(256) ln_fwd_warp(const TX* __restrict__ x, int
                                                    int64_t dot_hs) {
   static_assert(K == 0, "fused row dots live in ln_rowdot_fwd");
   constexpr int COLS = VPT * 32;
+  constexpr int U = VPT <= 8 ? 2 : 1;  // rows in flight per warp
   const int lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (row >= rows) return;
-  float v[VPT];
-  load_row<TX, VPT>(x + row * x_rs + lane * VPT, v);
-  float s = 0.f;
-#pragma unroll
-  for (int i = 0; i < VPT; ++i) s += v[i];
-  const float mu = warp_sum(s) * (1.0f / COLS);
-  float q = 0.f;
-#pragma unroll
-  for (int i = 0; i < VPT; ++i) {
-    v[i] -= mu;
-    q += v[i] * v[i];
-  }
-  const float rstd = rsqrtf(warp_sum(q) * (1.0f / COLS) + eps);
   float g[VPT], b[VPT];
   load_row<float, VPT>(gamma + lane * VPT, g);
   load_row<float, VPT>(beta + lane * VPT, b);
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t rb = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * U; rb < rows; rb += nw * U) {
+    float v[U][VPT];
 #pragma unroll
-  for (int i = 0; i < VPT; ++i) v[i] = v[i] * rstd * g[i] + b[i];
-  if (y) store_row<TY, VPT>(y + row * COLS + lane * VPT, v);
-  if (lane == 0) {
-    if (mean_out) mean_out[row] = mu;
-    if (rstd_out) rstd_out[row] = rstd;
+    for (int u = 0; u < U; ++u)
+      if (rb + u < rows) load_row<TX, VPT>(x + (rb + u) * x_rs + lane * VPT, v[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t row = rb + u;
+      if (row >= rows) break;
+      float s = 0.f;
+#pragma unroll
+      for (int i = 0; i < VPT; ++i) s += v[u][i];
+      const float mu = warp_sum(s) * (1.0f / COLS);
+      float q = 0.f;
+#pragma unroll
+      for (int i = 0; i < VPT; ++i) {
+        v[u][i] -= mu;
+        q += v[u][i] * v[u][i];
+      }
+      const float rstd = rsqrtf(warp_sum(q) * (1.0f / COLS) + eps);
+#pragma unroll
+      for (int i = 0; i < VPT; ++i) v[u][i] = v[u][i] * rstd * g[i] + b[i];
+      if (y) store_row<TY, VPT>(y + row * COLS + lane * VPT, v[u]);
+      if (lane == 0) {
+        if (mean_out) mean_out[row] = mu;
+        if (rstd_out) rstd_out[row] = rstd;
+      }
+    }
   }
 }
 
@@ -342,28 +351,39 @@ __global__ void __launch_bounds__(256) ln_bwd_warp(const TD* __restrict__ dy, co
   for (int i = 0; i < VPT; ++i) dg[i] = db[i] = 0.f;
   const int64_t slab = (rows + gridDim.x - 1) / gridDim.x;
   const int64_t r0 = blockIdx.x * slab, r1 = r0 + slab < rows ? r0 + slab : rows;
-  for (int64_t row = r0 + wid; row < r1; row += 8) {
-    float xv[VPT], d[VPT];
-    load_row<TX, VPT>(x + row * x_rs + lane * VPT, xv);
-    load_row<TD, VPT>(dy + row * COLS + lane * VPT, d);
-    const float mu = mean[row], rs = rstd[row];
-    float s1 = 0.f, s2 = 0.f;
+  constexpr int U = VPT <= 4 ? 4 : (VPT <= 8 ? 2 : 1);  // rows in flight per warp (memory-level parallelism)
+  for (int64_t rb = r0 + wid * U; rb < r1; rb += 8 * U) {
+    float xv[U][VPT], d[U][VPT], o[U][VPT];
 #pragma unroll
-    for (int i = 0; i < VPT; ++i) {
-      xv[i] = (xv[i] - mu) * rs;  // xhat
-      float gd = g[i] * d[i];
-      s1 += gd;
-      s2 += gd * xv[i];
-      dg[i] += d[i] * xv[i];
-      db[i] += d[i];
+    for (int u = 0; u < U; ++u) {
+      if (rb + u < r1) {
+        load_row<TX, VPT>(x + (rb + u) * x_rs + lane * VPT, xv[u]);
+        load_row<TD, VPT>(dy + (rb + u) * COLS + lane * VPT, d[u]);
+        if (res) load_row<TO, VPT>(res + (rb + u) * x_rs + lane * VPT, o[u]);
+      }
     }
-    s1 = warp_sum(s1) * (1.0f / COLS);
-    s2 = warp_sum(s2) * (1.0f / COLS);
-    float o[VPT];
-    if (res) load_row<TO, VPT>(res + row * x_rs + lane * VPT, o);
 #pragma unroll
-    for (int i = 0; i < VPT; ++i) o[i] = (res ? o[i] : 0.f) + rs * (g[i] * d[i] - s1 - xv[i] * s2);
-    store_row<TO, VPT>(dx + row * x_rs + lane * VPT, o);
+    for (int u = 0; u < U; ++u) {
+      const int64_t row = rb + u;
+      if (row >= r1) break;
+      const float mu = mean[row], rs = rstd[row];
+      float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+      for (int i = 0; i < VPT; ++i) {
+        xv[u][i] = (xv[u][i] - mu) * rs;  // xhat
+        float gd = g[i] * d[u][i];
+        s1 += gd;
+        s2 += gd * xv[u][i];
+        dg[i] += d[u][i] * xv[u][i];
+        db[i] += d[u][i];
+      }
+      s1 = warp_sum(s1) * (1.0f / COLS);
+      s2 = warp_sum(s2) * (1.0f / COLS);
+#pragma unroll
+      for (int i = 0; i < VPT; ++i)
+        o[u][i] = (res ? o[u][i] : 0.f) + rs * (g[i] * d[u][i] - s1 - xv[u][i] * s2);
+      store_row<TO, VPT>(dx + row * x_rs + lane * VPT, o[u]);
+    }
   }
   if (dgamma || dbeta) {
 #pragma unroll
@@ -460,7 +480,8 @@ static int ln_fwd_dispatch_warp(const void* x, int64_t x_rs, const float* g, con
                                 float* rstd, int64_t rows, int64_t cols, float eps, const float* w, void* dot,
                                 int64_t dot_hs, cudaStream_t st) {
   const int wpb = 8;
-  dim3 grid((unsigned)((rows + wpb - 1) / wpb));
+  int64_t need = (rows + 2 * wpb - 1) / (2 * wpb), cap = (int64_t)sm_count() * 8;
+  dim3 grid((unsigned)(need < cap ? need : cap));
 #define LNF(VPT)                                                                                             \
   ln_fwd_warp<TX, TY, VPT, K><<<grid, wpb * 32, 0, st>>>((const TX*)x, x_rs, g, b, (TY*)y, mean, rstd, rows, \
                                                          eps, w, (TY*)dot, dot_hs)
@@ -570,7 +591,7 @@ static int ln_bwd_impl(const void* dy, const void* x, int64_t x_rs, int64_t x_cs
                        const float* rstd, void* dx, const void* res, float* dg, float* db, int64_t rows, int64_t cols,
                        cudaStream_t st) {
   if (x_cs == 1 && cols % 32 == 0 && cols <= 1024) {
-    int64_t need = (rows + 63) / 64, cap = (int64_t)sm_count() * 2;  // >= 8 rows per warp, ~2 CTAs per SM
+    int64_t need = (rows + 127) / 128, cap = (int64_t)sm_count() * 4;  // 4-row batches per warp
     dim3 grid((unsigned)(need < cap ? need : cap));
     size_t sm = 16 * cols * sizeof(float);
 #define LNB(VPT)                                                                                            \
