@@ -154,7 +154,10 @@ __device__ __forceinline__ void bw_load(uint32_t sdst, const bf16* base, int64_t
 // A batch-shared bias (msa_row: dbias stride 0 over b) is handled by writing the
 // scaled dS (bf16) per batch and reducing over batches in attn_dbias_reduce
 // (deterministic, no atomics).
-template <int CP>
+// MODE: 0 = no bias (msa_col), 1 = per-key bias (pair_row / pair_col), 2 = full bias shared
+// over the batch with dS stored for the batch reduction (msa_row), 3 = generic full bias
+// (fp32 atomics).  Specialised so the per-element loop carries no dead predicated paths.
+template <int CP, int MODE>
 __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int G, int dq_partial) {
   using SM = BwdSmem<CP>;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -177,9 +180,9 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int G
   const int kr = wq * 32 + lane;  // key row of this thread (TMEM lane)
   const int kj = k0 + kr;
   const bool kvalid = kj < L;
-  const bool per_key_bias = F.bias && F.bs2 == 0;
-  const bool db_per_key = P.dbias && P.db2 == 0;
-  const bool db_store = P.dbias && P.dS != nullptr;  // batch-shared full bias -> dS workspace
+  constexpr bool per_key_bias = MODE == 1;
+  const bool db_per_key = MODE == 1 && P.dbias != nullptr;
+  constexpr bool db_store = MODE == 2;  // batch-shared full bias -> dS workspace
   const int nqt = (L + BW_BQ - 1) / BW_BQ;
   const int nkt = gridDim.x;
   const float LOG2E_ = 1.4426950408889634f;
@@ -269,12 +272,12 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int G
     for (int d = 0; d < CP; ++d) acc[d] = 0.f;
     float kbias = 0.f;
     if (per_key_bias && kvalid) kbias = bf2f(F.bias[b * F.bs0 + (int64_t)h * F.bs1 + (int64_t)kj * F.bs3]);
-    const bf16* bias_col = nullptr;
-    if (F.bias && !per_key_bias && kvalid) bias_col = F.bias + b * F.bs0 + (int64_t)h * F.bs1 + (int64_t)kj * F.bs3;
+    const bf16* bias_col = nullptr;  // full bias: element (q, kj) at bias_col[q * bs2]
+    if ((MODE == 2 || MODE == 3) && kvalid) bias_col = F.bias + b * F.bs0 + (int64_t)h * F.bs1 + (int64_t)kj * F.bs3;
     float* dbias_col = nullptr;
     if (P.dbias && kvalid) dbias_col = P.dbias + b * P.db0 + (int64_t)h * P.db1 + (int64_t)kj * P.db3;
-    bf16* ds_col = db_store && kvalid ? P.dS + ((b * H + h) * (int64_t)L) * L + kj : nullptr;
-
+    bf16* ds_col = (db_store && kvalid) ? P.dS + ((b * H + h) * (int64_t)L) * L + kj : nullptr;
+    const int bs2 = (int)F.bs2;  // full-bias query stride (< 2^31)
     for (int qt = 0; qt < nqt; ++qt, ++it) {
       const int q0 = qt * BW_BQ;
       cp_async_wait<0>();
@@ -304,28 +307,45 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int G
         tmem_ld16(t_lane + T_DP + qc, dp);
         tmem_ld_wait();
         float pv[16], dsv[16];
+        const bool all_valid = kvalid && q0 + qc + 16 <= L;
+        float bv[16];
+        if constexpr (MODE == 2 || MODE == 3) {
+          if (bias_col) {
+            const bf16* bp = bias_col + (q0 + qc) * bs2;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) bv[e] = (q0 + qc + e < L) ? bf2f(bp[e * bs2]) : 0.f;
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) bv[e] = 0.f;
+          }
+        }
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
-          const int ql = qc + e, qq = q0 + ql;
-          float x = s[e] + kbias;
-          if (bias_col && qq < L) x += bf2f(bias_col[(int64_t)qq * F.bs2]);
-          const bool ok = kvalid && qq < L;
+          const int ql = qc + e;
+          float x = s[e];
+          if constexpr (MODE == 1) x += kbias;
+          if constexpr (MODE == 2 || MODE == 3) x += bv[e];
+          const bool ok = all_valid || (kvalid && q0 + ql < L);
           const float p = ok ? exp2f(x * F.scale_log2 - s_lse[ql]) : 0.f;
-          const float ds = p * (dp[e] - s_D[ql]);
           pv[e] = p;
-          dsv[e] = ds;
+          dsv[e] = p * (dp[e] - s_D[ql]);
         }
-        if (ds_col) {
+        if constexpr (MODE == 2) {
+          if (ds_col) {
+            bf16* dp_ = ds_col + (q0 + qc) * L;
 #pragma unroll
-          for (int e = 0; e < 16; ++e)
-            if (q0 + qc + e < L) ds_col[(int64_t)(q0 + qc + e) * L] = f2bf(P.scale * dsv[e]);
-        } else if (db_per_key) {
+            for (int e = 0; e < 16; ++e)
+              if (q0 + qc + e < L) dp_[e * L] = f2bf(P.scale * dsv[e]);
+          }
+        } else if constexpr (MODE == 1) {
 #pragma unroll
           for (int e = 0; e < 16; ++e) kb_acc += dsv[e];
-        } else if (dbias_col) {
+        } else if constexpr (MODE == 3) {
+          if (dbias_col) {
 #pragma unroll
-          for (int e = 0; e < 16; ++e)
-            if (q0 + qc + e < L) atomicAdd(dbias_col + (int64_t)(q0 + qc + e) * P.db2, P.scale * dsv[e]);
+            for (int e = 0; e < 16; ++e)
+              if (q0 + qc + e < L) atomicAdd(dbias_col + (int64_t)(q0 + qc + e) * P.db2, P.scale * dsv[e]);
+          }
         }
 #pragma unroll
         for (int e = 0; e < 16; e += 8) {
@@ -471,12 +491,12 @@ static int64_t ws_layout(int64_t B, int64_t L, int H, int c, int bias_batch_redu
 
 int sm_count();
 
-template <int CP>
-static int launch_bwd(AttnBwdParams& p, int64_t B, int dq_partial, cudaStream_t st) {
+template <int CP, int MODE>
+static int launch_bwd_m(AttnBwdParams& p, int64_t B, int dq_partial, cudaStream_t st) {
   using SM = BwdSmem<CP>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel<CP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel<CP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)SM::TOTAL);
     if (e != cudaSuccess) return cuda_status(e, "attn bwd attr");
     attr = true;
@@ -487,9 +507,17 @@ static int launch_bwd(AttnBwdParams& p, int64_t B, int dq_partial, cudaStream_t 
   if (G < 1) G = 1;
   if (G > 16) G = 16;
   dim3 grid((unsigned)nkt, (unsigned)p.f.H, (unsigned)((B + G - 1) / G));
-  attn_bwd_kernel<CP><<<grid, 256, SM::TOTAL, st>>>(p, (int)G, dq_partial);
+  attn_bwd_kernel<CP, MODE><<<grid, 256, SM::TOTAL, st>>>(p, (int)G, dq_partial);
   EVO_LAUNCH_CHECK("attention bwd main");
   return EVO_OK;
+}
+
+template <int CP>
+static int launch_bwd(AttnBwdParams& p, int64_t B, int dq_partial, cudaStream_t st) {
+  if (!p.f.bias) return launch_bwd_m<CP, 0>(p, B, dq_partial, st);
+  if (p.f.bs2 == 0) return launch_bwd_m<CP, 1>(p, B, dq_partial, st);
+  if (p.dS) return launch_bwd_m<CP, 2>(p, B, dq_partial, st);
+  return launch_bwd_m<CP, 3>(p, B, dq_partial, st);
 }
 
 }  // namespace evo
