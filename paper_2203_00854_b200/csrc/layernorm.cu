@@ -300,6 +300,146 @@ __global__ void __launch_bounds__(256) ln_rowdot_bwd(const TX* __restrict__ x, c
   }
 }
 
+
+// ------------------------------------------------------------- lane-group rows (16-byte lanes)
+// Every lane owns 8 consecutive channels (one 16-byte bf16 vector); a row is handled by
+// LPR = COLS/8 lanes (4..32), so a warp covers 32/LPR rows per step and every load moves
+// 16 bytes per lane.  Reductions are xor-shuffles within the lane group.
+template <int LPR>
+__device__ __forceinline__ float group_sum(float v) {
+#pragma unroll
+  for (int o = LPR / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <typename TX, typename TY, int COLS, int U>
+__global__ void __launch_bounds__(256) ln_fwd_grp(const TX* __restrict__ x, int64_t x_rs,
+                                                  const float* __restrict__ gamma, const float* __restrict__ beta,
+                                                  TY* __restrict__ y, float* __restrict__ mean_out,
+                                                  float* __restrict__ rstd_out, int64_t rows, float eps) {
+  constexpr int LPR = COLS / 8, RPW = 32 / LPR;  // lanes per row, rows per warp step
+  const int lane = threadIdx.x & 31, sub = lane / LPR, cl = (lane % LPR) * 8;
+  float g[8], b[8];
+  load_row<float, 8>(gamma + cl, g);
+  load_row<float, 8>(beta + cl, b);
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t rb = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * RPW * U; rb < rows;
+       rb += nw * RPW * U) {
+    float v[U][8];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t row = rb + u * RPW + sub;
+      if (row < rows) load_row<TX, 8>(x + row * x_rs + cl, v[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t row = rb + u * RPW + sub;
+      float s = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s += v[u][i];
+      const float mu = group_sum<LPR>(s) * (1.0f / COLS);
+      float q = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        v[u][i] -= mu;
+        q += v[u][i] * v[u][i];
+      }
+      const float rs = rsqrtf(group_sum<LPR>(q) * (1.0f / COLS) + eps);
+      if (row < rows) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[u][i] = v[u][i] * rs * g[i] + b[i];
+        if (y) store_row<TY, 8>(y + row * COLS + cl, v[u]);
+        if (cl == 0 && mean_out) {
+          mean_out[row] = mu;
+          rstd_out[row] = rs;
+        }
+      }
+    }
+  }
+}
+
+template <typename TD, typename TX, typename TO, int COLS, int U>
+__global__ void __launch_bounds__(256) ln_bwd_grp(const TD* __restrict__ dy, const TX* __restrict__ x, int64_t x_rs,
+                                                  const float* __restrict__ gamma, const float* __restrict__ mean,
+                                                  const float* __restrict__ rstd, TO* dx, const TO* res,
+                                                  float* __restrict__ dgamma, float* __restrict__ dbeta,
+                                                  int64_t rows) {
+  constexpr int LPR = COLS / 8, RPW = 32 / LPR;
+  __shared__ float red[8][2][COLS];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, sub = lane / LPR, cl = (lane % LPR) * 8;
+  float g[8], dg[8], db[8];
+  load_row<float, 8>(gamma + cl, g);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) dg[i] = db[i] = 0.f;
+  const int64_t slab = (rows + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = blockIdx.x * slab, r1 = r0 + slab < rows ? r0 + slab : rows;
+  for (int64_t rb = r0 + wid * RPW * U; rb < r1; rb += 8 * RPW * U) {
+    float xv[U][8], d[U][8], o[U][8];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t row = rb + u * RPW + sub;
+      if (row < r1) {
+        load_row<TX, 8>(x + row * x_rs + cl, xv[u]);
+        load_row<TD, 8>(dy + row * COLS + cl, d[u]);
+        if (res) load_row<TO, 8>(res + row * x_rs + cl, o[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t row = rb + u * RPW + sub;
+      const bool ok = row < r1;
+      const float mu = ok ? mean[row] : 0.f, rs = ok ? rstd[row] : 0.f;
+      float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (!ok) xv[u][i] = d[u][i] = 0.f;
+        xv[u][i] = (xv[u][i] - mu) * rs;  // xhat
+        const float gd = g[i] * d[u][i];
+        s1 += gd;
+        s2 += gd * xv[u][i];
+        dg[i] += d[u][i] * xv[u][i];
+        db[i] += d[u][i];
+      }
+      s1 = group_sum<LPR>(s1) * (1.0f / COLS);
+      s2 = group_sum<LPR>(s2) * (1.0f / COLS);
+      if (ok) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[u][i] = (res ? o[u][i] : 0.f) + rs * (g[i] * d[u][i] - s1 - xv[u][i] * s2);
+        store_row<TO, 8>(dx + row * x_rs + cl, o[u]);
+      }
+    }
+  }
+  if (dgamma || dbeta) {
+    // lanes of different row-groups hold partials of the same channels: fold them first
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+#pragma unroll
+      for (int o = LPR; o < 32; o <<= 1) {
+        dg[i] += __shfl_xor_sync(0xffffffffu, dg[i], o);
+        db[i] += __shfl_xor_sync(0xffffffffu, db[i], o);
+      }
+    }
+    if (sub == 0) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        red[wid][0][cl + i] = dg[i];
+        red[wid][1][cl + i] = db[i];
+      }
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < COLS; c += blockDim.x) {
+      float a = 0.f, b = 0.f;
+#pragma unroll
+      for (int ww = 0; ww < 8; ++ww) {
+        a += red[ww][0][c];
+        b += red[ww][1][c];
+      }
+      if (dgamma) atomicAdd(dgamma + c, a);
+      if (dbeta) atomicAdd(dbeta + c, b);
+    }
+  }
+}
+
 // ------------------------------------------------------------- strided rows, thread per row
 template <typename TX, typename TY, int MAXC>
 __global__ void __launch_bounds__(256) ln_fwd_thread(const TX* __restrict__ x, int64_t x_rs, int64_t x_cs,
@@ -479,6 +619,21 @@ template <typename TX, typename TY, int K>
 static int ln_fwd_dispatch_warp(const void* x, int64_t x_rs, const float* g, const float* b, void* y, float* mean,
                                 float* rstd, int64_t rows, int64_t cols, float eps, const float* w, void* dot,
                                 int64_t dot_hs, cudaStream_t st) {
+  if (cols == 32 || cols == 64 || cols == 128 || cols == 256) {
+    const int64_t rpw = 32 / (cols / 8);
+    int64_t need = (rows + 8 * rpw * 2 - 1) / (8 * rpw * 2), cap = (int64_t)sm_count() * 8;
+    dim3 g2((unsigned)(need < cap ? need : cap));
+#define LNG(CC) ln_fwd_grp<TX, TY, CC, 2><<<g2, 256, 0, st>>>((const TX*)x, x_rs, g, b, (TY*)y, mean, rstd, rows, eps)
+    switch (cols) {
+      case 32: LNG(32); break;
+      case 64: LNG(64); break;
+      case 128: LNG(128); break;
+      default: LNG(256); break;
+    }
+#undef LNG
+    EVO_LAUNCH_CHECK("layernorm fwd");
+    return EVO_OK;
+  }
   const int wpb = 8;
   int64_t need = (rows + 2 * wpb - 1) / (2 * wpb), cap = (int64_t)sm_count() * 8;
   dim3 grid((unsigned)(need < cap ? need : cap));
@@ -590,6 +745,23 @@ template <typename TD, typename TX, typename TO>
 static int ln_bwd_impl(const void* dy, const void* x, int64_t x_rs, int64_t x_cs, const float* g, const float* mean,
                        const float* rstd, void* dx, const void* res, float* dg, float* db, int64_t rows, int64_t cols,
                        cudaStream_t st) {
+  if (x_cs == 1 && (cols == 32 || cols == 64 || cols == 128 || cols == 256)) {
+    const int64_t rpw = 32 / (cols / 8);
+    int64_t need = (rows + 8 * rpw * 4 - 1) / (8 * rpw * 4), cap = (int64_t)sm_count() * 4;
+    dim3 grid((unsigned)(need < cap ? need : cap));
+#define LBG(CC)                                                                                               \
+  ln_bwd_grp<TD, TX, TO, CC, (CC >= 256 ? 2 : 4)><<<grid, 256, 0, st>>>((const TD*)dy, (const TX*)x, x_rs, g, mean, \
+                                                                        rstd, (TO*)dx, (const TO*)res, dg, db, rows)
+    switch (cols) {
+      case 32: LBG(32); break;
+      case 64: LBG(64); break;
+      case 128: LBG(128); break;
+      default: LBG(256); break;
+    }
+#undef LBG
+    EVO_LAUNCH_CHECK("layernorm bwd");
+    return EVO_OK;
+  }
   if (x_cs == 1 && cols % 32 == 0 && cols <= 1024) {
     int64_t need = (rows + 127) / 128, cap = (int64_t)sm_count() * 4;  // 4-row batches per warp
     dim3 grid((unsigned)(need < cap ? need : cap));
