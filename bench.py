@@ -344,7 +344,14 @@ def main():
             ach = byts / sec / 1e9
             roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                     "frac": round(ach / hbm, 4)}
-        roof.update({"traffic": None, "kernel": dominant, "peak_source": peak_src,
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+        if os.path.exists(tpath):  # ncu --set full measurement of the same entry point (scripts/make_traffic.py)
+            tdoc = json.load(open(tpath)).get(dominant)
+            if tdoc:
+                traffic = round(tdoc["traffic_bytes_per_launch"])
+        roof.update({"traffic": traffic, "traffic_unit": "bytes/launch (DRAM read+write, ncu)",
+                     "kernel": dominant, "peak_source": peak_src,
                      "launches_per_step": dom["launches"] if use_graph else dom["launches"] / args.steps,
                      "avg_launch_ms": round(dom["avg_ms"], 4),
                      "share_of_step": round((dom["step_ms"] / ms_step) if use_graph else (dom["total_ms"] / total_ms), 4),
