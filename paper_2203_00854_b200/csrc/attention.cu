@@ -25,11 +25,11 @@ constexpr float LOG2E = 1.4426950408889634f;
 template <int CP>
 struct AttnSmem {
   static constexpr uint32_t Q = 0;
-  static constexpr uint32_t KT = Q + ATT_BQ * CP * 2;          // 3-stage ring
-  static constexpr uint32_t VT = KT + 3 * ATT_BK * CP * 2;     // 3-stage ring
-  static constexpr uint32_t P = VT + 3 * ATT_BK * CP * 2;
-  static constexpr uint32_t BIAS = P + ATT_BQ * ATT_BK * 2;    // 3 x 64 fp32 (per-key bias)
-  static constexpr uint32_t TOTAL = BIAS + 3 * ATT_BK * 4;
+  static constexpr uint32_t KT = Q + ATT_BQ * CP * 2;          // 2 stages
+  static constexpr uint32_t VT = KT + 2 * ATT_BK * CP * 2;     // 2 stages
+  static constexpr uint32_t P = VT + 2 * ATT_BK * CP * 2;
+  static constexpr uint32_t BIAS = P + ATT_BQ * ATT_BK * 2;    // 2 x 128 fp32 (per-key bias)
+  static constexpr uint32_t TOTAL = BIAS + 2 * ATT_BK * 4;
 };
 
 // ROWS x CP K-major tile from a strided [row][col] source (cols contiguous)
@@ -61,16 +61,11 @@ __device__ __forceinline__ void att_load_v(uint32_t sdst, const bf16* base, int6
   }
 }
 
-// lazy rescaling threshold (log2 units): the running max is only raised - and the
-// TMEM accumulator rescaled - when a tile's max exceeds it by more than 2^8, so P
-// values stay <= 256 (exact in bf16's exponent range) and rescales are rare.
-constexpr float RESCALE_LOG2 = 8.0f;
-
 template <int CP>
-__global__ void __launch_bounds__(128, CP == 64 ? 3 : 4) attn_fwd_kernel(AttnParams P) {
+__global__ void __launch_bounds__(128, CP == 32 ? 4 : 3) attn_fwd_kernel(AttnParams P) {
   using SM = AttnSmem<CP>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar_s, bar_o;
   __shared__ uint32_t tmem_sh;
   const uint32_t sb = smem_u32(smem);
   float* sbias = reinterpret_cast<float*>(smem + SM::BIAS);
@@ -83,38 +78,22 @@ __global__ void __launch_bounds__(128, CP == 64 ? 3 : 4) attn_fwd_kernel(AttnPar
   const int r = warp * 32 + lane;  // query row inside the tile
   const int qi = q0 + r;
   const bool per_key_bias = P.bias && P.bs2 == 0;
-  constexpr uint32_t T_S = 0, T_O = ATT_BK;  // TMEM: S [64 cols] | O [CP cols]
-  constexpr uint32_t TCOLS = ATT_BK + CP <= 128 ? 128 : 256;
 
-  if (warp == 0) tmem_alloc(&tmem_sh, TCOLS);
+  if (warp == 0) tmem_alloc(&tmem_sh, ATT_BK);
   if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
+    mbar_init(&bar_s, 1);
+    mbar_init(&bar_o, 1);
     fence_mbar_init();
   }
 
   const bf16* qb = P.q + b * P.q_sb + (int64_t)h * c;
   const bf16* kb = P.k + b * P.k_sb + (int64_t)h * c;
   const bf16* vb = P.v + b * P.v_sb + (int64_t)h * c;
-  const bf16* bkey = per_key_bias ? P.bias + b * P.bs0 + (int64_t)h * P.bs1 : nullptr;
-  const int nkt = (L + ATT_BK - 1) / ATT_BK;
-  // K/V ring: tile t lives in stage t % 3; tiles 0 and 1 are requested up front
-  auto load_kv = [&](int t) {
-    const int st3 = t % 3, kk0 = t * ATT_BK;
-    att_load_kmajor<CP, ATT_BK>(sb + SM::KT + st3 * ATT_BK * CP * 2, kb, P.k_sl, kk0, L - kk0, c);
-    att_load_v<CP>(sb + SM::VT + st3 * ATT_BK * CP * 2, vb, P.v_sl, kk0, L - kk0, c);
-    if (bkey && threadIdx.x < ATT_BK) {
-      const int kk = kk0 + threadIdx.x;
-      sbias[st3 * ATT_BK + threadIdx.x] = kk < L ? bf2f(bkey[(int64_t)kk * P.bs3]) : 0.f;
-    }
-  };
   att_load_kmajor<CP, ATT_BQ>(sb + SM::Q, qb, P.q_sl, q0, L - q0, c);
-  load_kv(0);
+  att_load_kmajor<CP, ATT_BK>(sb + SM::KT, kb, P.k_sl, 0, L, c);
+  att_load_v<CP>(sb + SM::VT, vb, P.v_sl, 0, L, c);
   cp_async_commit();
-  if (nkt > 1) load_kv(1);
-  cp_async_commit();
-  cp_async_wait<1>();  // Q and tile 0
-  cp_async_wait<0>();
-  fence_async_smem();
+
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -123,37 +102,52 @@ __global__ void __launch_bounds__(128, CP == 64 ? 3 : 4) attn_fwd_kernel(AttnPar
 
   constexpr uint32_t IDESC_S = make_idesc_bf16(128, ATT_BK, 0, 0);
   constexpr uint32_t IDESC_O = make_idesc_bf16(128, CP, 0, 1);
-  auto issue_s = [&](int st) {  // st = ring stage (tile % 3)
-#pragma unroll
-    for (int kk = 0; kk < CP / 16; ++kk) {
-      uint64_t ad = make_sdesc(sb + SM::Q + kk * 2 * (128 / 8) * 128, (128 / 8) * 128, 128);
-      uint64_t bd = make_sdesc(sb + SM::KT + st * ATT_BK * CP * 2 + kk * 2 * (ATT_BK / 8) * 128,
-                               (ATT_BK / 8) * 128, 128);
-      mma_bf16(tmem + T_S, ad, bd, IDESC_S, kk != 0);
-    }
-  };
-  if (threadIdx.x == 0) {
-    tc_fence_after();
-    issue_s(0);
-    mma_commit(&bar);
-  }
 
+  float m_run = -INFINITY, l_run = 0.f;
+  float o_acc[CP];
+#pragma unroll
+  for (int d = 0; d < CP; ++d) o_acc[d] = 0.f;
+
+  const int nkt = (L + ATT_BK - 1) / ATT_BK;
   const bf16* brow = nullptr;
   if (P.bias && !per_key_bias && qi < L) brow = P.bias + b * P.bs0 + (int64_t)h * P.bs1 + (int64_t)qi * P.bs2;
-  float m_run = -INFINITY, l_run = 0.f;
 
   for (int j = 0; j < nkt; ++j) {
     const int k0 = j * ATT_BK;
-    const int st = j % 3;
-    mbar_wait(&bar, j & 1);  // S(j) is in TMEM and PV(j-1) has landed in O
-    tc_fence_after();
-    // request tile j+2 (its stage was last read by PV(j-1) / S(j-1), both complete)
-    if (j + 2 < nkt) load_kv(j + 2);
+    const int st = j & 1;
+    if (per_key_bias) {
+      const bf16* bp = P.bias + b * P.bs0 + (int64_t)h * P.bs1;
+      const int kk = threadIdx.x;
+      if (kk < ATT_BK) sbias[st * ATT_BK + kk] = (k0 + kk < L) ? bf2f(bp[(int64_t)(k0 + kk) * P.bs3]) : 0.f;
+    }
+    cp_async_wait<0>();
+    fence_async_smem();
+    __syncthreads();
+    // prefetch the next K/V tile into the other stage (its MMAs finished last iteration)
+    if (j + 1 < nkt) {
+      att_load_kmajor<CP, ATT_BK>(sb + SM::KT + (st ^ 1) * ATT_BK * CP * 2, kb, P.k_sl, k0 + ATT_BK,
+                                  L - k0 - ATT_BK, c);
+      att_load_v<CP>(sb + SM::VT + (st ^ 1) * ATT_BK * CP * 2, vb, P.v_sl, k0 + ATT_BK, L - k0 - ATT_BK, c);
+    }
     cp_async_commit();
+
+    if (threadIdx.x == 0) {
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < CP / 16; ++kk) {
+        uint64_t ad = make_sdesc(sb + SM::Q + kk * 2 * (128 / 8) * 128, (128 / 8) * 128, 128);
+        uint64_t bd = make_sdesc(sb + SM::KT + st * ATT_BK * CP * 2 + kk * 2 * (ATT_BK / 8) * 128,
+                                 (ATT_BK / 8) * 128, 128);
+        mma_bf16(tmem, ad, bd, IDESC_S, kk != 0);
+      }
+      mma_commit(&bar_s);
+    }
+    mbar_wait(&bar_s, j & 1);
+    tc_fence_after();
 
     float s[ATT_BK];
 #pragma unroll
-    for (int cc = 0; cc < ATT_BK; cc += 32) tmem_ld32(t_row + T_S + cc, s + cc);
+    for (int cc = 0; cc < ATT_BK; cc += 32) tmem_ld32(t_row + cc, s + cc);
     tmem_ld_wait();
 
     // bias (before the scale, G1), scale, key masking
@@ -183,29 +177,13 @@ __global__ void __launch_bounds__(128, CP == 64 ? 3 : 4) attn_fwd_kernel(AttnPar
 #pragma unroll
       for (int kk = 0; kk < ATT_BK; ++kk) s[kk] += sbias[st * ATT_BK + kk];
     }
-    float mt = -INFINITY;
+    float mx = m_run;
 #pragma unroll
     for (int kk = 0; kk < ATT_BK; ++kk) {
       s[kk] = (k0 + kk < L) ? s[kk] * P.scale_log2 : -INFINITY;
-      mt = fmaxf(mt, s[kk]);
+      mx = fmaxf(mx, s[kk]);
     }
-    if (j == 0) {
-      m_run = mt;
-    } else if (mt > m_run + RESCALE_LOG2) {  // rare: raise the max, rescale O (TMEM) and l
-      const float corr = exp2f(m_run - mt);
-#pragma unroll
-      for (int cc = 0; cc < CP; cc += 16) {
-        float o[16];
-        tmem_ld16(t_row + T_O + cc, o);
-        tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 16; ++e) o[e] *= corr;
-        tmem_st16(t_row + T_O + cc, o);
-      }
-      tmem_st_wait();
-      l_run *= corr;
-      m_run = mt;
-    }
+    const float corr = exp2f(m_run - mx);  // m_run = -inf on the first tile -> 0
     float lsum = 0.f;
     const uint32_t prow = sb + SM::P;
 #pragma unroll
@@ -213,36 +191,45 @@ __global__ void __launch_bounds__(128, CP == 64 ? 3 : 4) attn_fwd_kernel(AttnPar
       float pv[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        pv[e] = exp2f(s[kk + e] - m_run);
+        pv[e] = exp2f(s[kk + e] - mx);
         lsum += pv[e];
       }
       st_shared_v4(prow + kmajor_off(r, kk, ATT_BQ), pack_bf16x2(pv[0], pv[1]), pack_bf16x2(pv[2], pv[3]),
                    pack_bf16x2(pv[4], pv[5]), pack_bf16x2(pv[6], pv[7]));
     }
-    l_run += lsum;
+    l_run = l_run * corr + lsum;
+    m_run = mx;
+#pragma unroll
+    for (int d = 0; d < CP; ++d) o_acc[d] *= corr;
 
-    cp_async_wait<1>();  // tile j+1 landed (requested an iteration ago); tile j+2 may be in flight
     fence_async_smem();
     tc_fence_before();
     __syncthreads();
     if (threadIdx.x == 0) {
       tc_fence_after();
 #pragma unroll
-      for (int kk = 0; kk < ATT_BK / 16; ++kk) {  // O += P V  (accumulates across key tiles)
+      for (int kk = 0; kk < ATT_BK / 16; ++kk) {
         uint64_t ad = make_sdesc(sb + SM::P + kk * 2 * (128 / 8) * 128, (128 / 8) * 128, 128);
         uint64_t bd = make_sdesc(sb + SM::VT + st * ATT_BK * CP * 2 + kk * 2 * (CP / 8) * 128, (CP / 8) * 128, 128);
-        mma_bf16(tmem + T_O, ad, bd, IDESC_O, (j | kk) != 0);
+        mma_bf16(tmem, ad, bd, IDESC_O, kk != 0);
       }
-      if (j + 1 < nkt) issue_s((j + 1) % 3);  // queued behind PV(j)
-      mma_commit(&bar);
+      mma_commit(&bar_o);
     }
-  }
-  mbar_wait(&bar, nkt & 1);  // final PV
-  tc_fence_after();
-  float o_acc[CP];
+    mbar_wait(&bar_o, j & 1);
+    tc_fence_after();
+    float ov[CP];
+    if constexpr (CP == 16) {
+      tmem_ld16(t_row, ov);
+    } else {
 #pragma unroll
-  for (int cc = 0; cc < CP; cc += 16) tmem_ld16(t_row + T_O + cc, o_acc + cc);
-  tmem_ld_wait();
+      for (int cc = 0; cc < CP; cc += 32) tmem_ld32(t_row + cc, ov + cc);
+    }
+    tmem_ld_wait();
+#pragma unroll
+    for (int d = 0; d < CP; ++d) o_acc[d] += ov[d];
+    tc_fence_before();
+    __syncthreads();  // all TMEM reads done before the next S MMA overwrites the columns
+  }
 
   if (qi < L) {
     const float inv = 1.f / l_run;
@@ -277,7 +264,7 @@ __global__ void __launch_bounds__(128, CP == 64 ? 3 : 4) attn_fwd_kernel(AttnPar
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, TCOLS);
+  if (warp == 0) tmem_dealloc(tmem, ATT_BK);
 }
 
 static bool a16(const void* p) { return ((uintptr_t)p & 15) == 0; }

@@ -195,20 +195,10 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int G
   }
   const int64_t HC = (int64_t)H * c;
   // gate backward fused into the tile load: dO = dout * sigmoid(g) (staged in smem),
-  // D = rowsum(dO * O), and - by the key-tile-0 CTAs only - dg = dout * O * s(1-s).
-  // Split in two so the raw dout/g/o loads are in flight while TMEM is drained:
-  //   prefetch(): cp.async for Q (+K, V) and plain loads of dout/g/o/lse into registers;
-  //   finish():   compute dO / D / dg and stage them.
-  constexpr int CPR = CP / 8;
-  constexpr int NCH = BW_BQ * CPR / 256;  // 16-byte chunks per thread
-  uint4 r_do[NCH], r_g[NCH], r_o[NCH];
-  float r_lse = 0.f;
-  int64_t pf_b = 0;
-  int pf_q0 = 0;
-  auto prefetch = [&](int64_t b, int qt, bool with_kv) {
+  // D = rowsum(dO * O) (4 lanes per row for c = 32), and - by the key-tile-0 CTAs only -
+  // dg = dout * O * s(1-s) written once per query row.
+  auto issue_loads = [&](int64_t b, int qt, bool with_kv) {
     const int q0 = qt * BW_BQ;
-    pf_b = b;
-    pf_q0 = q0;
     if (with_kv) {
       bw_load<CP>(sb + SM::K, F.k + b * F.k_sb + (int64_t)h * c, F.k_sl, k0, L - k0, c);
       bw_load<CP>(sb + SM::V, F.v + b * F.v_sb + (int64_t)h * c, F.v_sl, k0, L - k0, c);
@@ -217,58 +207,52 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int G
     cp_async_commit();
     if (threadIdx.x < BW_BQ) {
       const int qq = q0 + threadIdx.x;
-      r_lse = qq < L ? F.lse[(b * H + h) * (int64_t)L + qq] * LOG2E_ : 0.f;
+      s_lse[threadIdx.x] = qq < L ? F.lse[(b * H + h) * (int64_t)L + qq] * LOG2E_ : 0.f;
     }
-#pragma unroll
-    for (int n = 0; n < NCH; ++n) {
-      const int ch = threadIdx.x + n * 256;
+    constexpr int CPR = CP / 8;
+    for (int ch = threadIdx.x; ch < BW_BQ * CPR; ch += 256) {
       const int r = ch / CPR, d0 = (ch % CPR) * 8, qq = q0 + r;
+      float dO[8], part = 0.f;
       if (qq < L && d0 < c) {
-        r_do[n] = *reinterpret_cast<const uint4*>(P.dout + b * P.do_sb + (int64_t)qq * P.do_sl + h * c + d0);
-        r_g[n] = *reinterpret_cast<const uint4*>(F.g + b * F.g_sb + (int64_t)qq * F.g_sl + h * c + d0);
-        r_o[n] = *reinterpret_cast<const uint4*>(F.orw + b * F.r_sb + (int64_t)qq * F.r_sl + h * c + d0);
+        float dout[8], g[8], o[8];
+        const uint4 ud = *reinterpret_cast<const uint4*>(P.dout + b * P.do_sb + (int64_t)qq * P.do_sl + h * c + d0);
+        const uint4 ug = *reinterpret_cast<const uint4*>(F.g + b * F.g_sb + (int64_t)qq * F.g_sl + h * c + d0);
+        const uint4 uo = *reinterpret_cast<const uint4*>(F.orw + b * F.r_sb + (int64_t)qq * F.r_sl + h * c + d0);
+        unpack_bf16x2(ud.x, dout[0], dout[1]); unpack_bf16x2(ud.y, dout[2], dout[3]);
+        unpack_bf16x2(ud.z, dout[4], dout[5]); unpack_bf16x2(ud.w, dout[6], dout[7]);
+        unpack_bf16x2(ug.x, g[0], g[1]); unpack_bf16x2(ug.y, g[2], g[3]);
+        unpack_bf16x2(ug.z, g[4], g[5]); unpack_bf16x2(ug.w, g[6], g[7]);
+        unpack_bf16x2(uo.x, o[0], o[1]); unpack_bf16x2(uo.y, o[2], o[3]);
+        unpack_bf16x2(uo.z, o[4], o[5]); unpack_bf16x2(uo.w, o[6], o[7]);
+        float dg[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float sg = sigmoidf_(g[e]);
+          dO[e] = dout[e] * sg;
+          dg[e] = dout[e] * o[e] * sg * (1.f - sg);
+        }
+        // D uses the bf16-rounded dO that the MMAs see
+#pragma unroll
+        for (int e = 0; e < 8; ++e) part += bf2f(f2bf(dO[e])) * o[e];
+        if (blockIdx.x == 0) {
+          uint4 w;
+          w.x = pack_bf16x2(dg[0], dg[1]); w.y = pack_bf16x2(dg[2], dg[3]);
+          w.z = pack_bf16x2(dg[4], dg[5]); w.w = pack_bf16x2(dg[6], dg[7]);
+          *reinterpret_cast<uint4*>(P.dg + b * P.dg_sb + (int64_t)qq * P.dg_sl + h * c + d0) = w;
+        }
       } else {
-        r_do[n] = r_g[n] = r_o[n] = make_uint4(0, 0, 0, 0);
-      }
-    }
-  };
-  auto finish = [&]() {
-    const int64_t b = pf_b;
-    const int q0 = pf_q0;
-    if (threadIdx.x < BW_BQ) s_lse[threadIdx.x] = r_lse;
 #pragma unroll
-    for (int n = 0; n < NCH; ++n) {
-      const int ch = threadIdx.x + n * 256;
-      const int r = ch / CPR, d0 = (ch % CPR) * 8, qq = q0 + r;
-      float dout[8], g[8], o[8], dO[8], dg[8], part = 0.f;
-      unpack_bf16x2(r_do[n].x, dout[0], dout[1]); unpack_bf16x2(r_do[n].y, dout[2], dout[3]);
-      unpack_bf16x2(r_do[n].z, dout[4], dout[5]); unpack_bf16x2(r_do[n].w, dout[6], dout[7]);
-      unpack_bf16x2(r_g[n].x, g[0], g[1]); unpack_bf16x2(r_g[n].y, g[2], g[3]);
-      unpack_bf16x2(r_g[n].z, g[4], g[5]); unpack_bf16x2(r_g[n].w, g[6], g[7]);
-      unpack_bf16x2(r_o[n].x, o[0], o[1]); unpack_bf16x2(r_o[n].y, o[2], o[3]);
-      unpack_bf16x2(r_o[n].z, o[4], o[5]); unpack_bf16x2(r_o[n].w, o[6], o[7]);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float sg = sigmoidf_(g[e]);
-        dO[e] = dout[e] * sg;
-        dg[e] = dout[e] * o[e] * sg * (1.f - sg);
-        part += bf2f(f2bf(dO[e])) * o[e];  // D from the bf16 dO the MMAs see
-      }
-      if (blockIdx.x == 0 && qq < L && d0 < c) {
-        uint4 w;
-        w.x = pack_bf16x2(dg[0], dg[1]); w.y = pack_bf16x2(dg[2], dg[3]);
-        w.z = pack_bf16x2(dg[4], dg[5]); w.w = pack_bf16x2(dg[6], dg[7]);
-        *reinterpret_cast<uint4*>(P.dg + b * P.dg_sb + (int64_t)qq * P.dg_sl + h * c + d0) = w;
+        for (int e = 0; e < 8; ++e) dO[e] = 0.f;
       }
       st_shared_v4(sb + SM::DO + kmajor_off(r, d0, 128), pack_bf16x2(dO[0], dO[1]), pack_bf16x2(dO[2], dO[3]),
                    pack_bf16x2(dO[4], dO[5]), pack_bf16x2(dO[6], dO[7]));
+      // the CPR chunks of a row sit on consecutive lanes
 #pragma unroll
-      for (int o2 = 1; o2 < CPR; o2 <<= 1) part += __shfl_xor_sync(0xffffffffu, part, o2);
+      for (int o = 1; o < CPR; o <<= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
       if (ch % CPR == 0) s_D[r] = part;
     }
   };
-  prefetch(b_begin, 0, true);
-  finish();
+  issue_loads(b_begin, 0, true);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -402,8 +386,7 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int G
       tc_fence_after();
       // the tiles are free: prefetch the next (batch, query tile) while draining TMEM
       const bool last_q = qt + 1 == nqt;
-      const bool more = !(last_q && b + 1 == b_end);
-      if (more) prefetch(last_q ? b + 1 : b, last_q ? 0 : qt + 1, last_q);
+      if (!(last_q && b + 1 == b_end)) issue_loads(last_q ? b + 1 : b, last_q ? 0 : qt + 1, last_q);
       {
 #pragma unroll
         for (int cc = 0; cc < CP; cc += 16) {
@@ -440,7 +423,6 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int G
           }
         }
       }
-      if (more) finish();
       tc_fence_before();
       __syncthreads();
     }
