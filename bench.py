@@ -179,10 +179,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        # NCCL over NVLink; EVO_DIST_BACKEND=gloo only for functional checks with ranks sharing a GPU
+        backend = os.environ.get("EVO_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     _lib.load()
     longseq = args.workload == "longseq"
     cfg = EvoConfig(*TRAIN_DIMS) if not longseq else EvoConfig(128, args.n_res, 256, 128, 8, 4, 32)
