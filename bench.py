@@ -379,7 +379,7 @@ def main():
         else:
             metric, value, unit = METRIC, round(ms_step / nb, 4), UNIT
             workload = "evoformer_stack_fwd_bwd_training_shape"
-            step_desc = "48-block forward + backward incl. all weight gradients; no optimizer"
+            step_desc = f"{nb}-block forward + backward incl. all weight gradients; no optimizer"
         line = {
             "metric": metric, "value": value, "unit": unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),

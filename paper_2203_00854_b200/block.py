@@ -34,20 +34,56 @@ def _mm(a, b):
     return torch.mm(a, b)
 
 
+class SideStream:
+    """Parameter-gradient work (weight GEMMs, bias column sums) is off the critical
+    path of the input-gradient chain: it is forked onto a side CUDA stream (event
+    fork/join, also captured into CUDA graphs) so it fills the gaps left by the
+    latency-bound kernels of the main stream.  ``join()`` before reading grads."""
+
+    enabled = True
+    stream = None
+
+    @classmethod
+    def run(cls, fn, *keep):
+        if not (cls.enabled and keep and keep[0].is_cuda):
+            return fn()
+        if cls.stream is None:
+            cls.stream = torch.cuda.Stream()
+        main = torch.cuda.current_stream()
+        cls.stream.wait_stream(main)
+        with torch.cuda.stream(cls.stream):
+            fn()
+        for t in keep:  # the main stream's allocator must not recycle these before the side work ran
+            t.record_stream(cls.stream)
+
+    @classmethod
+    def join(cls):
+        if cls.stream is not None and torch.cuda.is_available():
+            torch.cuda.current_stream().wait_stream(cls.stream)
+
+
 def _wgrad(x, dy, out):
-    """out (fp32) = x^T @ dy with fp32 accumulation and output."""
+    """out (fp32) = x^T @ dy with fp32 accumulation and output (side stream)."""
     if x.is_cuda:  # cuBLAS writes the fp32 result straight into the grad buffer view
-        torch.mm(x.t(), dy, out_dtype=F32, out=out)
+        SideStream.run(lambda: torch.mm(x.t(), dy, out_dtype=F32, out=out), x, dy)
     else:  # CPU only in the host-logic tests (fake kernel backend)
         out.copy_(x.t().float() @ dy.float())
 
 
 def _bgrad(dy, out):
-    """bias gradient (accumulated into the zeroed fp32 grad view)"""
+    """bias gradient (accumulated into the zeroed fp32 grad view; side stream)"""
     if dy.is_cuda:
-        ops.colsum(dy, out)
+        SideStream.run(lambda: ops.colsum(dy, out), dy)
     else:  # CPU only in the host-logic tests (fake kernel backend)
         out += dy.float().sum(0)
+
+
+def _dbias_only(dx_new, rows, cols, out):
+    """dbias = column sums of the residual-stream gradient (side stream)"""
+    if dx_new.is_cuda:
+        SideStream.run(lambda: ops.colsum(dx_new, out, rows, cols), dx_new)
+    else:
+        ops.gated_residual_bwd(dx_new, rows, cols, dbias=out)
 
 
 class Saved(dict):
@@ -110,7 +146,7 @@ def attention_bwd(bp: BlockParams, sv: Saved, dx_new):
     rows = B * L
     h, f, g = bp.h, bp.f, bp.g
     dev = dx_new.device
-    ops.gated_residual_bwd(dx_new, rows, H, dbias=g[f"{mod}.b_o"])  # db_o = sum_r dx_new
+    _dbias_only(dx_new, rows, H, g[f"{mod}.b_o"])  # db_o = sum_r dx_new
     dog = _mm(dx_new, h[f"{mod}.w_o"].t())
     _wgrad(sv["og"], dx_new, g[f"{mod}.w_o"])
     sbr, slr = _attn_geometry(kind, B, L)
@@ -210,7 +246,7 @@ def transition_bwd(bp: BlockParams, sv: Saved, dx_new):
     mod = sv["mod"]
     rows, H = dx_new.shape
     h, f, g = bp.h, bp.f, bp.g
-    ops.gated_residual_bwd(dx_new, rows, H, dbias=g[f"{mod}.b2"])
+    _dbias_only(dx_new, rows, H, g[f"{mod}.b2"])
     _wgrad(sv["hid"], dx_new, g[f"{mod}.w2"])
     dhid = _mm(dx_new, h[f"{mod}.w2"].t())
     dpre = ops.bias_act_bwd(dhid, sv["hid"], rows, dhid.shape[1], dy=dhid, dbias=g[f"{mod}.b1"])
@@ -263,7 +299,7 @@ def opm_bwd(bp: BlockParams, sv: Saved, dz_new, dm, reduce_scatter=None):
     P, Hm, Hz = cfg.hidden_proj, cfg.h_msa, cfg.h_pair
     S, R, Rj = sv["S"], sv["R"], sv["Rj"]
     h, f, g = bp.h, bp.f, bp.g
-    ops.gated_residual_bwd(dz_new, R * Rj, Hz, dbias=g["opm.b_o"])
+    _dbias_only(dz_new, R * Rj, Hz, g["opm.b_o"])
     _wgrad(sv["o"].view(R * Rj, P * P), dz_new, g["opm.w_o"])
     do = _mm(dz_new, h["opm.w_o"].t())                               # [R*Rj, P*P] == [i][j][p][q]
     dab = torch.empty(S * R, 2 * P, device=dz_new.device, dtype=BF16)
@@ -459,4 +495,5 @@ def block_bwd(bp: BlockParams, saved, dm, dz):
     dm2, _ = attention_bwd(bp, s2, dm2)
     dm2, dbias = attention_bwd(bp, s1, dm2)
     msa_row_bias_bwd(bp, sv_b, dbias, dz2)
+    SideStream.join()
     return dm2.view(S, R, cfg.h_msa), dz2.view(R, R, cfg.h_pair)
