@@ -150,23 +150,18 @@ __global__ void __launch_bounds__(128, CP == 32 ? 4 : 3) attn_fwd_kernel(AttnPar
     for (int cc = 0; cc < ATT_BK; cc += 32) tmem_ld32(t_row + cc, s + cc);
     tmem_ld_wait();
 
-    // bias (before the scale, G1), scale, key masking
+    // bias (before the scale, G1); keys >= L masked on the last tile only
+    const bool full_tile = k0 + ATT_BK <= L;
     if (brow) {
-      if (P.bias_vec) {
+      if (P.bias_vec && full_tile) {
 #pragma unroll
         for (int kk = 0; kk < ATT_BK; kk += 8) {
-          if (k0 + kk + 8 <= L) {
-            uint4 u = *reinterpret_cast<const uint4*>(brow + k0 + kk);
-            float t[8];
-            unpack_bf16x2(u.x, t[0], t[1]); unpack_bf16x2(u.y, t[2], t[3]);
-            unpack_bf16x2(u.z, t[4], t[5]); unpack_bf16x2(u.w, t[6], t[7]);
+          uint4 u = *reinterpret_cast<const uint4*>(brow + k0 + kk);
+          float t[8];
+          unpack_bf16x2(u.x, t[0], t[1]); unpack_bf16x2(u.y, t[2], t[3]);
+          unpack_bf16x2(u.z, t[4], t[5]); unpack_bf16x2(u.w, t[6], t[7]);
 #pragma unroll
-            for (int e = 0; e < 8; ++e) s[kk + e] += t[e];
-          } else {
-#pragma unroll
-            for (int e = 0; e < 8; ++e)
-              if (k0 + kk + e < L) s[kk + e] += bf2f(brow[k0 + kk + e]);
-          }
+          for (int e = 0; e < 8; ++e) s[kk + e] += t[e];
         }
       } else {
 #pragma unroll
@@ -175,15 +170,22 @@ __global__ void __launch_bounds__(128, CP == 32 ? 4 : 3) attn_fwd_kernel(AttnPar
       }
     } else if (per_key_bias) {
 #pragma unroll
-      for (int kk = 0; kk < ATT_BK; ++kk) s[kk] += sbias[st * ATT_BK + kk];
+      for (int kk = 0; kk < ATT_BK; kk += 4) {
+        const float4 bv = *reinterpret_cast<const float4*>(sbias + st * ATT_BK + kk);
+        s[kk] += bv.x; s[kk + 1] += bv.y; s[kk + 2] += bv.z; s[kk + 3] += bv.w;
+      }
     }
+    if (!full_tile) {
+#pragma unroll
+      for (int kk = 0; kk < ATT_BK; ++kk)
+        if (k0 + kk >= L) s[kk] = -INFINITY;
+    }
+    // running max on the unscaled logits (scale > 0), p = 2^(s*scale*log2e - m*scale*log2e)
     float mx = m_run;
 #pragma unroll
-    for (int kk = 0; kk < ATT_BK; ++kk) {
-      s[kk] = (k0 + kk < L) ? s[kk] * P.scale_log2 : -INFINITY;
-      mx = fmaxf(mx, s[kk]);
-    }
-    const float corr = exp2f(m_run - mx);  // m_run = -inf on the first tile -> 0
+    for (int kk = 0; kk < ATT_BK; kk += 2) mx = fmaxf(mx, fmaxf(s[kk], s[kk + 1]));
+    const float corr = ex2f((m_run - mx) * P.scale_log2);  // m_run = -inf on the first tile -> 0
+    const float mxs = mx * P.scale_log2;
     float lsum = 0.f;
     const uint32_t prow = sb + SM::P;
 #pragma unroll
@@ -191,7 +193,7 @@ __global__ void __launch_bounds__(128, CP == 32 ? 4 : 3) attn_fwd_kernel(AttnPar
       float pv[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        pv[e] = exp2f(s[kk + e] - mx);
+        pv[e] = ex2f(fmaf(s[kk + e], P.scale_log2, -mxs));
         lsum += pv[e];
       }
       st_shared_v4(prow + kmajor_off(r, kk, ATT_BQ), pack_bf16x2(pv[0], pv[1]), pack_bf16x2(pv[2], pv[3]),
@@ -232,7 +234,7 @@ __global__ void __launch_bounds__(128, CP == 32 ? 4 : 3) attn_fwd_kernel(AttnPar
   }
 
   if (qi < L) {
-    const float inv = 1.f / l_run;
+    const float inv = rcpf(l_run);
     const bf16* gp = P.g + b * P.g_sb + (int64_t)qi * P.g_sl + (int64_t)h * c;
     bf16* og = P.og + b * P.o_sb + (int64_t)qi * P.o_sl + (int64_t)h * c;
     bf16* orw = P.orw ? P.orw + b * P.r_sb + (int64_t)qi * P.r_sl + (int64_t)h * c : nullptr;
@@ -259,7 +261,7 @@ __global__ void __launch_bounds__(128, CP == 32 ? 4 : 3) attn_fwd_kernel(AttnPar
         *reinterpret_cast<uint4*>(og + d) = w;
       }
     }
-    if (P.lse) P.lse[(b * P.H + h) * (int64_t)L + qi] = (m_run + log2f(l_run)) * 0.6931471805599453f;
+    if (P.lse) P.lse[(b * P.H + h) * (int64_t)L + qi] = (m_run * P.scale_log2 + log2f(l_run)) * 0.6931471805599453f;
   }
 
   tc_fence_before();
@@ -289,6 +291,7 @@ int attn_params_from_desc(const EvoAttnDesc* d, AttnParams& p) {
   EVO_CHECK_ARG(d->B >= 1 && d->L >= 1 && d->H >= 1 && d->c >= 8, EVO_ERR_SHAPE, "attention: bad extents");
   EVO_CHECK_ARG(d->c % 8 == 0 && d->c <= 64, EVO_ERR_SHAPE, "attention: head dim must be a multiple of 8, <= 64 (got %d)", d->c);
   EVO_CHECK_ARG(d->B < 65536 && d->H < 65536 && d->L < (1 << 30), EVO_ERR_SHAPE, "attention: extents too large");
+  EVO_CHECK_ARG(d->scale > 0.f, EVO_ERR_ARG, "attention: scale must be positive");
   const int64_t strides[] = {d->q_sb, d->q_sl, d->k_sb, d->k_sl, d->v_sb, d->v_sl, d->g_sb, d->g_sl,
                              d->o_sb, d->o_sl, d->r_sb, d->r_sl};
   for (int64_t s : strides) EVO_CHECK_ARG(s % 8 == 0, EVO_ERR_ALIGN, "attention: strides must be multiples of 8");

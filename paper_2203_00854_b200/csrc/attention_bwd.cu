@@ -319,17 +319,26 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int G
             for (int e = 0; e < 16; ++e) bv[e] = 0.f;
           }
         }
+        float lse16[16], D16[16];
+#pragma unroll
+        for (int e = 0; e < 16; e += 4) {
+          *reinterpret_cast<float4*>(lse16 + e) = *reinterpret_cast<const float4*>(s_lse + qc + e);
+          *reinterpret_cast<float4*>(D16 + e) = *reinterpret_cast<const float4*>(s_D + qc + e);
+        }
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
-          const int ql = qc + e;
           float x = s[e];
           if constexpr (MODE == 1) x += kbias;
           if constexpr (MODE == 2 || MODE == 3) x += bv[e];
-          const bool ok = all_valid || (kvalid && q0 + ql < L);
-          const float p = ok ? exp2f(x * F.scale_log2 - s_lse[ql]) : 0.f;
-          pv[e] = p;
-          dsv[e] = p * (dp[e] - s_D[ql]);
+          pv[e] = ex2f(fmaf(x, F.scale_log2, -lse16[e]));
         }
+        if (!all_valid) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            if (!(kvalid && q0 + qc + e < L)) pv[e] = 0.f;
+        }
+#pragma unroll
+        for (int e = 0; e < 16; ++e) dsv[e] = pv[e] * (dp[e] - D16[e]);
         if constexpr (MODE == 2) {
           if (ds_col) {
             bf16* dp_ = ds_col + (q0 + qc) * L;

@@ -45,9 +45,8 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&t);
 }
 __device__ __forceinline__ void unpack_bf16x2(uint32_t u, float& lo, float& hi) {
-  __nv_bfloat162 t = *reinterpret_cast<__nv_bfloat162*>(&u);
-  lo = __low2float(t);
-  hi = __high2float(t);
+  lo = __uint_as_float(u << 16);  // bf16 -> f32 is a 16-bit shift (one ALU op per value)
+  hi = __uint_as_float(u & 0xffff0000u);
 }
 
 template <typename T> __device__ __forceinline__ float ldf(const T* p);
@@ -68,7 +67,18 @@ __device__ __forceinline__ float warp_max(float v) {
   return v;
 }
 
-__device__ __forceinline__ float sigmoidf_(float x) { return 1.0f / (1.0f + __expf(-x)); }
+// MUFU fast paths without the denormal fix-up sequences exp2f / 1.f/x compile to
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcpf(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float sigmoidf_(float x) { return rcpf(1.0f + ex2f(-1.4426950408889634f * x)); }
 
 // ---------------------------------------------------------------- smem / async
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

@@ -16,6 +16,8 @@
 // TMEM accumulator (tcgen05.ld 32x32b) in the epilogue.  Operands may be K-major
 // or MN-major (instruction-descriptor major bits), so no transpose copies are
 // ever made.  Addressing is 2-level per dim (see EvoMat in include/evo.h).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace evo {
@@ -26,12 +28,18 @@ struct MatArg {
   const char* ptr;
   int64_t bs;                 // batch stride (elements)
   uint32_t split0, split1;
+  uint32_t mul0, sh0, mul1, sh1;  // magic numbers: i / split = umulhi(i, mul) >> sh (mul = 0: split 1)
   int64_t hi0, lo0, hi1, lo1;
 };
 
+// round-up magic-number division, exact for dividends < 2^31 (all indices are)
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, uint32_t mul, uint32_t sh) {
+  return mul == 0 ? n : (__umulhi(n, mul) >> sh);
+}
+
 __device__ __forceinline__ int64_t mat_off(const MatArg& m, uint32_t i0, uint32_t i1) {
-  uint32_t q0 = i0 / m.split0, r0 = i0 - q0 * m.split0;
-  uint32_t q1 = i1 / m.split1, r1 = i1 - q1 * m.split1;
+  uint32_t q0 = fdiv(i0, m.mul0, m.sh0), r0 = i0 - q0 * m.split0;
+  uint32_t q1 = fdiv(i1, m.mul1, m.sh1), r1 = i1 - q1 * m.split1;
   return (int64_t)q0 * m.hi0 + (int64_t)r0 * m.lo0 + (int64_t)q1 * m.hi1 + (int64_t)r1 * m.lo1;
 }
 
@@ -177,8 +185,8 @@ __global__ void __launch_bounds__(128) bgemm_kernel(MatArg A, MatArg B, MatArg C
       const int r = ch / CPR, cc = ch % CPR;
       const uint32_t grow = m0 + r, gcol = n0 + cc * EPC;
       if (grow >= M || gcol >= N) continue;
-      const uint32_t qr = grow / C.split0, rr = grow - qr * C.split0;
-      const uint32_t qc = gcol / C.split1, rc = gcol - qc * C.split1;
+      const uint32_t qr = fdiv(grow, C.mul0, C.sh0), rr = grow - qr * C.split0;
+      const uint32_t qc = fdiv(gcol, C.mul1, C.sh1), rc = gcol - qc * C.split1;
       TC* p = reinterpret_cast<TC*>(Cbase) + (int64_t)qr * C.hi0 + (int64_t)rr * C.lo0 + (int64_t)qc * C.hi1 + rc;
       uint4 val = *reinterpret_cast<const uint4*>(stile + r * PITCH + cc * 16);
       if (beta != 0.f) {
@@ -194,7 +202,7 @@ __global__ void __launch_bounds__(128) bgemm_kernel(MatArg A, MatArg B, MatArg C
   } else {
     int64_t roff = 0;
     if (row_ok) {
-      uint32_t q = row / C.split0, r = row - q * C.split0;
+      uint32_t q = fdiv(row, C.mul0, C.sh0), r = row - q * C.split0;
       roff = (int64_t)q * C.hi0 + (int64_t)r * C.lo0;
     }
 #pragma unroll 1
@@ -220,7 +228,7 @@ __global__ void __launch_bounds__(128) bgemm_kernel(MatArg A, MatArg B, MatArg C
       for (int j = 0; j < 32; ++j) {  // generic addressing (e.g. rows contiguous: coalesced per column)
         uint32_t col = n0 + c0 + j;
         if (col >= N) break;
-        uint32_t q = col / C.split1, r = col - q * C.split1;
+        uint32_t q = fdiv(col, C.mul1, C.sh1), r = col - q * C.split1;
         TC* p = crow + (int64_t)q * C.hi1 + (int64_t)r * C.lo1;
         float o = alpha * v[j];
         if (beta != 0.f) o += beta * ldf<TC>(p);
@@ -268,13 +276,313 @@ __global__ void __launch_bounds__(256) bgemm_splitk_reduce(const float* __restri
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       const uint32_t r = (uint32_t)(rows_contig ? r0 + e : r0), c = (uint32_t)(rows_contig ? c0 : c0 + e);
-      const uint32_t qr = r / C.split0, rr = r - qr * C.split0, qc = c / C.split1, rc = c - qc * C.split1;
+      const uint32_t qr = fdiv(r, C.mul0, C.sh0), rr = r - qr * C.split0, qc = fdiv(c, C.mul1, C.sh1), rc = c - qc * C.split1;
       TC* p = cb + (int64_t)qr * C.hi0 + (int64_t)rr * C.lo0 + (int64_t)qc * C.hi1 + (int64_t)rc * C.lo1;
       float o = alpha * acc[e];
       if (beta != 0.f) o += beta * ldf<TC>(p);
       stf<TC>(p, o);
     }
   }
+}
+
+
+// =====================================================================================
+// Warp-specialised persistent variant (the default path):
+//   warps 0..3  producers: cp.async ring of STAGES (A,B) k-tiles, completion signalled with
+//               cp.async.mbarrier.arrive.noinc on full[stage] (128 arrivals)
+//   warp 4      MMA issuer: waits full[stage], issues tcgen05.mma into one of two TMEM
+//               accumulators, tcgen05.commit -> empty[stage]; after the last k-tile of a
+//               tile, commit -> tmem_full[buf]
+//   warps 5..8  epilogue: wait tmem_full[buf], TMEM -> regs -> smem staging -> coalesced
+//               16-byte global stores (or split-K fp32 partials), arrive tmem_empty[buf]
+// The CTA loops over tiles (tile += gridDim.x), so the loads and MMAs of tile t+1 run
+// under the epilogue of tile t.
+// =====================================================================================
+__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
+
+__device__ __forceinline__ int64_t off_dim0(const MatArg& m, uint32_t i) {
+  uint32_t q = fdiv(i, m.mul0, m.sh0);
+  return (int64_t)q * m.hi0 + (int64_t)(i - q * m.split0) * m.lo0;
+}
+__device__ __forceinline__ int64_t off_dim1(const MatArg& m, uint32_t i) {
+  uint32_t q = fdiv(i, m.mul1, m.sh1);
+  return (int64_t)q * m.hi1 + (int64_t)(i - q * m.split1) * m.lo1;
+}
+
+// ROWS x 64 operand tile loader for the 128 producer threads.  The row (M/N) part of every
+// address is computed once per output tile, the K part once per k-tile, so the inner loop
+// is one add + one cp.async per 16-byte chunk.
+template <int ROWS, bool MN>
+struct TileLoader {
+  static constexpr int IT = ROWS / 16;  // chunks per thread per k-tile
+  int64_t roff[MN ? 1 : IT];            // element offset of the row part, -1 = out of range
+
+  __device__ __forceinline__ void setup(const MatArg& m, uint32_t r0, uint32_t R, int tid) {
+    if constexpr (!MN) {
+#pragma unroll
+      for (int it = 0; it < IT; ++it) {
+        const uint32_t r = r0 + (tid >> 3) + it * 16;
+        roff[it] = r < R ? off_dim0(m, r) : -1;
+      }
+    } else {
+      const uint32_t r = r0 + (tid % (ROWS / 8)) * 8;
+      roff[0] = r < R ? off_dim0(m, r) : -1;
+    }
+  }
+  // smem offsets: chunk it sits a constant stride after chunk 0 (16 rows = 2 core-matrix
+  // rows for K-major; KSTEP k = KSTEP/8 core-matrix columns = 2048 B for MN-major)
+  __device__ __forceinline__ void load(uint32_t sdst, const MatArg& m, const char* base, uint32_t k0, uint32_t K,
+                                       int tid) const {
+    if constexpr (!MN) {
+      const int k = (tid & 7) * 8;
+      const uint32_t kk = k0 + k;
+      const bool kok = kk < K;
+      const int64_t koff = kok ? off_dim1(m, kk) : 0;
+      const uint32_t s0 = sdst + kmajor_off(tid >> 3, k, ROWS);
+#pragma unroll
+      for (int it = 0; it < IT; ++it) {
+        const bool pred = kok && roff[it] >= 0;
+        cp_async16(s0 + it * 256, pred ? base + (roff[it] + koff) * 2 : base, pred);
+      }
+    } else {
+      constexpr int KSTEP = 128 / (ROWS / 8);
+      const int kb = tid / (ROWS / 8);
+      const uint32_t s0 = sdst + mnmajor_off((tid % (ROWS / 8)) * 8, kb, ROWS);
+      const bool rok = roff[0] >= 0;
+#pragma unroll
+      for (int it = 0; it < IT; ++it) {
+        const uint32_t kk = k0 + kb + it * KSTEP;
+        const bool pred = rok && kk < K;
+        cp_async16(s0 + it * 2048, pred ? base + (roff[0] + off_dim1(m, kk)) * 2 : base, pred);
+      }
+    }
+  }
+};
+
+template <int BN, bool A_MN, bool B_MN, int STAGES, typename TC>
+__global__ void __launch_bounds__(288, 1) bgemm_ws_kernel(MatArg A, MatArg B, MatArg C, uint32_t M, uint32_t N,
+                                                          uint32_t K, float alpha, float beta, int c_mode, int splits,
+                                                          float* __restrict__ ws, int batch) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_sh;
+  constexpr uint32_t A_BYTES = GEMM_BM * GEMM_BK * 2;
+  constexpr uint32_t B_BYTES = BN * GEMM_BK * 2;
+  constexpr int PITCH = BN * (int)sizeof(TC) + 16;
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t sA = sbase, sB = sbase + STAGES * A_BYTES;
+  uint8_t* stile = smem + STAGES * (A_BYTES + B_BYTES);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  const uint32_t mt = (M + GEMM_BM - 1) / GEMM_BM, nt = (N + BN - 1) / BN;
+  const uint32_t total = mt * nt * (uint32_t)batch * (uint32_t)splits;
+  const int KT_all = (K + GEMM_BK - 1) / GEMM_BK;
+  const int KT_per = (KT_all + splits - 1) / splits;
+  // tile id -> (batch, split, m-tile, n-tile); n fastest so consecutive CTAs share the A rows
+  auto decode = [&](uint32_t t, uint32_t& b, int& sp, uint32_t& m0, uint32_t& n0, int& kt0, int& ktn) {
+    const uint32_t n_i = t % nt;
+    t /= nt;
+    const uint32_t m_i = t % mt;
+    t /= mt;
+    sp = (int)(t % splits);
+    b = t / splits;
+    m0 = m_i * GEMM_BM;
+    n0 = n_i * BN;
+    kt0 = sp * KT_per;
+    ktn = KT_all - kt0 < KT_per ? KT_all - kt0 : KT_per;
+  };
+
+  if (warp == 0) tmem_alloc(&tmem_sh, 2 * BN);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 128);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 128);
+    }
+    fence_mbar_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_sh;
+
+  if (warp < 4) {
+    // ---------------- producers (warps 0..3)
+    const int tid = threadIdx.x;
+    int stage = 0;
+    uint32_t phase = 0;
+    TileLoader<GEMM_BM, A_MN> la;
+    TileLoader<BN, B_MN> lb;
+    for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
+      uint32_t b, m0, n0;
+      int sp, kt0, ktn;
+      decode(t, b, sp, m0, n0, kt0, ktn);
+      const char* Abase = A.ptr + (int64_t)b * A.bs * 2;
+      const char* Bbase = B.ptr + (int64_t)b * B.bs * 2;
+      la.setup(A, m0, M, tid);
+      lb.setup(B, n0, N, tid);
+      for (int kt = 0; kt < ktn; ++kt) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        la.load(sA + stage * A_BYTES, A, Abase, (kt0 + kt) * GEMM_BK, K, tid);
+        lb.load(sB + stage * B_BYTES, B, Bbase, (kt0 + kt) * GEMM_BK, K, tid);
+        cp_async_mbar_arrive_noinc(&full[stage]);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    cp_async_wait<0>();
+  } else if (warp == 4) {
+    // ---------------- MMA issuer
+    constexpr uint32_t IDESC = make_idesc_bf16(GEMM_BM, BN, A_MN, B_MN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (uint32_t t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+      uint32_t b, m0, n0;
+      int sp, kt0, ktn;
+      decode(t, b, sp, m0, n0, kt0, ktn);
+      const int buf = it & 1;
+      mbar_wait(&tempty[buf], ((it >> 1) & 1) ^ 1);  // epilogue drained this accumulator
+      tc_fence_after();
+      for (int kt = 0; kt < ktn; ++kt) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+#pragma unroll
+          for (int kk = 0; kk < GEMM_BK / 16; ++kk) {
+            uint64_t ad = make_sdesc(sA + stage * A_BYTES + kk * 2 * (GEMM_BM / 8) * 128, (GEMM_BM / 8) * 128, 128);
+            uint64_t bd = make_sdesc(sB + stage * B_BYTES + kk * 2 * (BN / 8) * 128, (BN / 8) * 128, 128);
+            mma_bf16(tmem + buf * BN, ad, bd, IDESC, (kt | kk) != 0);
+          }
+          mma_commit(&empty[stage]);
+          if (kt == ktn - 1) mma_commit(&tfull[buf]);
+        }
+        __syncwarp();
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 5..8 -> TMEM lane quarters 1,2,3,0)
+    const int q = warp & 3;            // lane quarter of this warp
+    const int et = threadIdx.x - 160;  // 0..127 epilogue thread id
+    int it = 0;
+    for (uint32_t t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+      uint32_t b, m0, n0;
+      int sp, kt0, ktn;
+      decode(t, b, sp, m0, n0, kt0, ktn);
+      const int buf = it & 1;
+      mbar_wait(&tfull[buf], (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t row = m0 + q * 32 + lane;
+      const bool row_ok = row < M;
+      char* Cbase = const_cast<char*>(C.ptr) + (int64_t)b * C.bs * (int64_t)sizeof(TC);
+      const uint32_t tbase = tmem + buf * BN + ((uint32_t)(q * 32) << 16);
+      if (c_mode == 1 && ws == nullptr) {
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          float v[32];
+          tmem_ld32(tbase + c0, v);
+          tmem_ld_wait();
+          uint8_t* dst = stile + (q * 32 + lane) * PITCH + c0 * (int)sizeof(TC);
+#pragma unroll
+          for (int j = 0; j < 32; j += 8) {
+            if constexpr (sizeof(TC) == 2) {
+              *reinterpret_cast<uint4*>(dst + j * 2) = make_uint4(
+                  pack_bf16x2(alpha * v[j], alpha * v[j + 1]), pack_bf16x2(alpha * v[j + 2], alpha * v[j + 3]),
+                  pack_bf16x2(alpha * v[j + 4], alpha * v[j + 5]), pack_bf16x2(alpha * v[j + 6], alpha * v[j + 7]));
+            } else {
+              *reinterpret_cast<float4*>(dst + j * 4) =
+                  make_float4(alpha * v[j], alpha * v[j + 1], alpha * v[j + 2], alpha * v[j + 3]);
+              *reinterpret_cast<float4*>(dst + j * 4 + 16) =
+                  make_float4(alpha * v[j + 4], alpha * v[j + 5], alpha * v[j + 6], alpha * v[j + 7]);
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[buf]);  // accumulator free for tile t + 2*gridDim.x
+        named_sync(1, 128);
+        constexpr int CPR = BN * (int)sizeof(TC) / 16;
+        constexpr int EPC = 16 / (int)sizeof(TC);
+        constexpr int RSTEP = 128 / CPR;
+        const int cc = et % CPR;
+        const uint32_t gcol = n0 + cc * EPC;
+        const bool col_ok = gcol < N;
+        TC* cbase = reinterpret_cast<TC*>(Cbase) + (col_ok ? off_dim1(C, gcol) : 0);
+        for (int r = et / CPR; r < GEMM_BM; r += RSTEP) {
+          const uint32_t grow = m0 + r;
+          if (grow >= M || !col_ok) continue;
+          TC* p = cbase + off_dim0(C, grow);
+          uint4 val = *reinterpret_cast<const uint4*>(stile + r * PITCH + cc * 16);
+          if (beta != 0.f) {
+            const TC* sv = reinterpret_cast<const TC*>(&val);
+            uint4 outv;
+            TC* ov = reinterpret_cast<TC*>(&outv);
+#pragma unroll
+            for (int e = 0; e < EPC; ++e) stf<TC>(ov + e, ldf<TC>(sv + e) + beta * ldf<TC>(p + e));
+            val = outv;
+          }
+          *reinterpret_cast<uint4*>(p) = val;
+        }
+        named_sync(1, 128);  // staging tile reusable
+      } else {
+        int64_t roff = 0;
+        if (row_ok) {
+          uint32_t qq = fdiv(row, C.mul0, C.sh0), r = row - qq * C.split0;
+          roff = (int64_t)qq * C.hi0 + (int64_t)r * C.lo0;
+        }
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          float v[32];
+          tmem_ld32(tbase + c0, v);
+          tmem_ld_wait();
+          if (!row_ok) continue;
+          if (ws != nullptr) {
+            float* wrow = ws + (((int64_t)sp * batch + b) * M + row) * N;
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              const uint32_t col = n0 + c0 + j;
+              if (col + 4 <= N)
+                *reinterpret_cast<float4*>(wrow + col) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+              else
+                for (int e = 0; e < 4; ++e)
+                  if (col + e < N) wrow[col + e] = v[j + e];
+            }
+            continue;
+          }
+          TC* crow = reinterpret_cast<TC*>(Cbase) + roff;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            uint32_t col = n0 + c0 + j;
+            if (col >= N) break;
+            uint32_t qq = fdiv(col, C.mul1, C.sh1), r = col - qq * C.split1;
+            TC* p = crow + (int64_t)qq * C.hi1 + (int64_t)r * C.lo1;
+            float o = alpha * v[j];
+            if (beta != 0.f) o += beta * ldf<TC>(p);
+            stf<TC>(p, o);
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[buf]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 2 * BN);
 }
 
 static MatArg to_arg(const EvoMat* m, int64_t ext0, int64_t ext1) {
@@ -288,6 +596,19 @@ static MatArg to_arg(const EvoMat* m, int64_t ext0, int64_t ext1) {
   };
   a.split0 = sp(m->split[0], ext0);
   a.split1 = sp(m->split[1], ext1);
+  auto magic = [](uint32_t d, uint32_t& mul, uint32_t& sh) {
+    if (d == 1) {
+      mul = sh = 0;
+      return;
+    }
+    uint32_t l = 0;
+    while ((1ull << l) < d) ++l;  // ceil(log2 d)
+    const uint64_t p = 31 + l;
+    mul = (uint32_t)(((1ull << p) + d - 1) / d);
+    sh = (uint32_t)(p - 32);
+  };
+  magic(a.split0, a.mul0, a.sh0);
+  magic(a.split1, a.mul1, a.sh1);
   a.hi0 = m->stride_hi[0];
   a.lo0 = m->stride_lo[0];
   a.hi1 = m->stride_hi[1];
@@ -331,11 +652,50 @@ static int launch_bgemm_s(MatArg A, MatArg B, MatArg C, int64_t batch, int64_t M
   return EVO_OK;
 }
 
+template <int BN, bool AM, bool BMN, typename TC>
+static int launch_bgemm_ws(MatArg A, MatArg B, MatArg C, int64_t batch, int64_t M, int64_t N, int64_t K, float alpha,
+                           float beta, int c_mode, int splits, float* ws, cudaStream_t st) {
+  constexpr int STAGES = 4;
+  const size_t smem = STAGES * (GEMM_BM * GEMM_BK * 2 + BN * GEMM_BK * 2) + (size_t)GEMM_BM * (BN * sizeof(TC) + 16);
+  auto kern = bgemm_ws_kernel<BN, AM, BMN, STAGES, TC>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_status(e, "bgemm_ws attr");
+    attr_set = true;
+  }
+  const int64_t tiles = ((M + GEMM_BM - 1) / GEMM_BM) * ((N + BN - 1) / BN) * batch * splits;
+  const int64_t grid = tiles < sm_count() ? tiles : sm_count();
+  kern<<<(unsigned)grid, 288, smem, st>>>(A, B, C, (uint32_t)M, (uint32_t)N, (uint32_t)K, alpha, beta, c_mode, splits,
+                                          splits > 1 ? ws : nullptr, (int)batch);
+  EVO_LAUNCH_CHECK("bgemm_ws launch");
+  if (splits > 1) {
+    const bool rows_contig = C.lo0 == 1 && C.split0 % 8 == 0 && M % 8 == 0;
+    EVO_CHECK_ARG(rows_contig || N % 8 == 0, EVO_ERR_ALIGN, "bgemm split-K: M or N must be a multiple of 8");
+    int64_t n8 = batch * M * N / 8;
+    int64_t g = (n8 + 255) / 256, cap = (int64_t)sm_count() * 16;
+    bgemm_splitk_reduce<TC><<<(unsigned)(g < cap ? g : cap), 256, 0, st>>>(ws, C, (uint32_t)M, (uint32_t)N, batch,
+                                                                           splits, alpha, beta, rows_contig ? 1 : 0);
+    EVO_LAUNCH_CHECK("bgemm split-K reduce");
+  }
+  return EVO_OK;
+}
+
+static bool use_v1() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("EVO_BGEMM_V1");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 // short K (<= 2 k-tiles, e.g. the OPM contraction over N_s = 128): 2 stages -> 64 KB smem,
 // 3 CTAs per SM so one CTA's epilogue overlaps another's main loop
 template <int BN, bool AM, bool BMN, typename TC>
 static int launch_bgemm(MatArg A, MatArg B, MatArg C, int64_t batch, int64_t M, int64_t N, int64_t K, float alpha,
                         float beta, int c_mode, int splits, float* ws, cudaStream_t st) {
+  if (!use_v1()) return launch_bgemm_ws<BN, AM, BMN, TC>(A, B, C, batch, M, N, K, alpha, beta, c_mode, splits, ws, st);
   const int64_t kt = (K + GEMM_BK - 1) / GEMM_BK / splits;
   if (kt <= 2) return launch_bgemm_s<BN, AM, BMN, TC, 2>(A, B, C, batch, M, N, K, alpha, beta, c_mode, splits, ws, st);
   return launch_bgemm_s<BN, AM, BMN, TC, 3>(A, B, C, batch, M, N, K, alpha, beta, c_mode, splits, ws, st);
