@@ -13,7 +13,7 @@ import threading
 
 from .errors import DimensionError, DomainError, KernelError, NativeLibraryMissing
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libevo.so")
+LIB_PATH = os.environ.get("EVO_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libevo.so")
 
 EVO_OK, EVO_ERR_SHAPE, EVO_ERR_DTYPE, EVO_ERR_ALIGN, EVO_ERR_CUDA, EVO_ERR_ARG, EVO_ERR_DOMAIN = range(7)
 EVO_BF16, EVO_F32 = 0, 1
@@ -126,8 +126,8 @@ def check(rc: int) -> None:
     raise KernelError(f"libevo error {rc}: {msg}")
 
 
-# kernels launched per C-ABI call (evo_gated_attention_bwd = main + dq finish [+ dbias reduce])
-LAUNCHES = {"evo_gated_attention_bwd": 2, "evo_bgemm_ws": 2}
+# kernels launched per C-ABI call (evo_gated_attention_bwd = prep + main + dq finish [+ dbias reduce])
+LAUNCHES = {"evo_gated_attention_bwd": 3, "evo_bgemm_ws": 2}
 
 
 class Instrument:

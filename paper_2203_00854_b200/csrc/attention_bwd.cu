@@ -2,9 +2,10 @@
 // tcgen05.  The reference has no backward; the gradient oracle is
 // the torch float64 restatement in oracle/evoformer_torch.py.
 //
-//   main   one CTA = (batch, head, 128-key tile), 8 warps, loops over 128-query tiles; the
-//          gate backward is fused into the query-tile load (dO = dout*sigmoid(g) staged in
-//          smem, D = rowsum(dO*O), dg = dout*O*s(1-s) written by the key-tile-0 CTAs):
+//   prep   one warp per (batch, position) row: dO = dout*sigmoid(g) (bf16), dg = dout*O*s(1-s),
+//          D = rowsum(dO*O) and lse*log2(e) per (batch, head, query), so the main loop's
+//          per-tile operands are all plain cp.async copies prefetched behind the TMEM drain
+//   main   one CTA = (batch, head, 128-key tile), 8 warps, loops over 128-query tiles:
 //            S^T  = K Q^T            (tcgen05, M=keys N=queries)  -> TMEM cols [0,128)
 //            dP^T = V dO^T           (tcgen05)                    -> TMEM cols [128,256)
 //            P^T  = exp2(S^T*scale + bias - lse), dS^T = P^T (dP^T - D)   (registers)
@@ -12,9 +13,15 @@
 //            dV  += P^T dO,  dK += dS^T Q   (accumulated in TMEM over query tiles)
 //            dQ_t = dS K  (same smem tile read as its transpose by swapping the
 //                   descriptor's LBO/SBO and the major bit) -> fp32 atomics
-//            dbias += scale * dS (atomics; per-key bias pre-reduced over queries)
+//            dbias: per-key bias pre-reduced over queries (one atomic per key); a bias shared
+//            over the batch (msa_row) copies the dS^T smem tile to a bf16 workspace with
+//            16-byte stores and attn_dbias_reduce sums it over the batch (deterministic)
 //   finish dq = bf16(dQ accumulator)
 #include "attn.cuh"
+
+#ifndef EVO_EXP
+#define EVO_EXP 0
+#endif
 
 namespace evo {
 
@@ -30,37 +37,69 @@ struct AttnBwdParams {
   bf16* dO;      // workspace [B][L][H*c]
   float* dQacc;  // workspace [B][L][H*c]
   float* Dsum;   // workspace [B][H][L]
-  bf16* dS;      // workspace [B][H][L][L] (batch-shared bias only) or null
+  float* lse2;   // workspace [B][H][L]: lse * log2(e)
+  bf16* dS;      // workspace [B][H][key][query] (batch-shared bias only, unscaled) or null
   float scale;
   int64_t B;
 };
 
-// dbias[h][q][k] += sum_b dS[b][h][q][k]   (batch-shared bias: msa_row, evoformer.py:214)
-template <int VEC>
+// dbias[h][q][k] += scale * sum_b dS[b][h][k][q]   (batch-shared bias: msa_row, evoformer.py:214).
+// Thread = 8 consecutive queries of one (h, key): 16-byte loads, B of them in flight.
 __global__ void __launch_bounds__(256) attn_dbias_reduce(const bf16* __restrict__ dS, float* __restrict__ dbias,
-                                                         int64_t B, int H, int L, int64_t d1, int64_t d2, int64_t d3) {
+                                                         int64_t B, int H, int L, int64_t d1, int64_t d2, int64_t d3,
+                                                         float scale) {
   const int64_t per = (int64_t)H * L * L;
-  const int64_t nv = per / VEC;
+  const int64_t nv = per / 8;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = i * VEC;
-    float acc[VEC];
+    const int64_t e = i * 8;
+    float acc[8];
 #pragma unroll
-    for (int k = 0; k < VEC; ++k) acc[k] = 0.f;
-    for (int64_t b = 0; b < B; ++b) {
-      if constexpr (VEC == 8) {
-        const uint4 u = *reinterpret_cast<const uint4*>(dS + b * per + e);
-        float t[8];
-        unpack_bf16x2(u.x, t[0], t[1]); unpack_bf16x2(u.y, t[2], t[3]);
-        unpack_bf16x2(u.z, t[4], t[5]); unpack_bf16x2(u.w, t[6], t[7]);
+    for (int k = 0; k < 8; ++k) acc[k] = 0.f;
+    int64_t b = 0;
+    for (; b + 4 <= B; b += 4) {
+      uint4 u[4];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) acc[k] += t[k];
-      } else {
-        acc[0] += bf2f(dS[b * per + e]);
+      for (int t = 0; t < 4; ++t) u[t] = *reinterpret_cast<const uint4*>(dS + (b + t) * per + e);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        float v[8];
+        unpack_bf16x2(u[t].x, v[0], v[1]); unpack_bf16x2(u[t].y, v[2], v[3]);
+        unpack_bf16x2(u[t].z, v[4], v[5]); unpack_bf16x2(u[t].w, v[6], v[7]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] += v[k];
       }
     }
-    const int64_t h = e / ((int64_t)L * L), q = (e / L) % L, k = e % L;
+    for (; b < B; ++b) {
+      const uint4 u = *reinterpret_cast<const uint4*>(dS + b * per + e);
+      float v[8];
+      unpack_bf16x2(u.x, v[0], v[1]); unpack_bf16x2(u.y, v[2], v[3]);
+      unpack_bf16x2(u.z, v[4], v[5]); unpack_bf16x2(u.w, v[6], v[7]);
 #pragma unroll
-    for (int t = 0; t < VEC; ++t) dbias[h * d1 + q * d2 + (k + t) * d3] += acc[t];
+      for (int k = 0; k < 8; ++k) acc[k] += v[k];
+    }
+    const int64_t h = e / ((int64_t)L * L), kk = (e / L) % L, q = e % L;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) dbias[h * d1 + (q + t) * d2 + kk * d3] += scale * acc[t];
+  }
+}
+
+// bias_t[h][k][q] = bias[h*s1 + q*s2 + k]  (batch-shared full bias, keys contiguous in the
+// source): the backward's threads own keys, so the transposed copy turns 16 strided 2-byte
+// loads per thread and query group into two 16-byte loads.  32x32 tiles through smem.
+__global__ void __launch_bounds__(256) attn_bias_transpose(const bf16* __restrict__ bias, int64_t s1, int64_t s2,
+                                                           bf16* __restrict__ bias_t, int L) {
+  __shared__ bf16 tile[32][33];
+  const int h = blockIdx.z;
+  const int q0 = blockIdx.y * 32, k0 = blockIdx.x * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int r = ty; r < 32; r += 8) {
+    const int q = q0 + r, k = k0 + tx;
+    tile[r][tx] = (q < L && k < L) ? bias[h * s1 + (int64_t)q * s2 + k] : f2bf(0.f);
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int k = k0 + r, q = q0 + tx;
+    if (q < L && k < L) bias_t[((int64_t)h * L + k) * L + q] = tile[tx][r];
   }
 }
 
@@ -72,36 +111,56 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
 }
 
 // ---------------------------------------------------------------------------------- prep
-// one warp per (b, l) row; lanes walk the H*c channels in 8-element chunks
+// The (row = (b, l), 8-channel chunk) pairs are flattened; a warp owns PREP_PASSES x 32
+// consecutive pairs (no idle lanes for any H*c), and issues every global load of them (dout,
+// g, o, lse) before any math, so it pays one memory latency per PREP_PASSES passes.  The
+// lanes of one head are consecutive and never straddle rows (c/8 divides 32 and H*c/8).
+constexpr int PREP_PASSES = 4;
 __global__ void __launch_bounds__(256) attn_bwd_prep(AttnBwdParams P, int64_t B) {
   const int lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int L = P.f.L, H = P.f.H, c = P.f.c;
-  if (row >= B * L) return;
-  const int64_t b = row / L, l = row % L;
   const int nch = H * c / 8;
+  const int64_t total = B * L * nch;
+  const int64_t f0 = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * (PREP_PASSES * 32);
+  if (f0 >= total) return;
   const int lanes_per_head = c / 8;  // 1, 2, 4 or 8
-  for (int base = 0; base < nch; base += 32) {
-    const int ch = base + lane;
+  uint4 ud[PREP_PASSES], ug[PREP_PASSES], uo[PREP_PASSES];
+  float lse[PREP_PASSES];
+#pragma unroll
+  for (int t = 0; t < PREP_PASSES; ++t) {
+    const int64_t f = f0 + t * 32 + lane;
+    if (f < total) {
+      const int64_t row = f / nch;
+      const int col = (int)(f - row * nch) * 8;
+      const int64_t b = row / L, l = row - b * L;
+      ud[t] = *reinterpret_cast<const uint4*>(P.dout + b * P.do_sb + l * P.do_sl + col);
+      ug[t] = *reinterpret_cast<const uint4*>(P.f.g + b * P.f.g_sb + l * P.f.g_sl + col);
+      uo[t] = *reinterpret_cast<const uint4*>(P.f.orw + b * P.f.r_sb + l * P.f.r_sl + col);
+      lse[t] = (lane % lanes_per_head) == 0 ? P.f.lse[(b * H + col / c) * (int64_t)L + l] : 0.f;
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < PREP_PASSES; ++t) {
+    const int64_t f = f0 + t * 32 + lane;
+    const bool ok = f < total;
+    const int64_t row = ok ? f / nch : 0;
+    const int col = (int)(f - row * nch) * 8;
+    const int64_t b = row / L, l = row - b * L;
     float dsum = 0.f;
-    if (ch < nch) {
-      const int col = ch * 8;
+    if (ok) {
       float dout[8], g[8], o[8], dO[8], dg[8];
-      const uint4 ud = *reinterpret_cast<const uint4*>(P.dout + b * P.do_sb + l * P.do_sl + col);
-      const uint4 ug = *reinterpret_cast<const uint4*>(P.f.g + b * P.f.g_sb + l * P.f.g_sl + col);
-      const uint4 uo = *reinterpret_cast<const uint4*>(P.f.orw + b * P.f.r_sb + l * P.f.r_sl + col);
-      unpack_bf16x2(ud.x, dout[0], dout[1]); unpack_bf16x2(ud.y, dout[2], dout[3]);
-      unpack_bf16x2(ud.z, dout[4], dout[5]); unpack_bf16x2(ud.w, dout[6], dout[7]);
-      unpack_bf16x2(ug.x, g[0], g[1]); unpack_bf16x2(ug.y, g[2], g[3]);
-      unpack_bf16x2(ug.z, g[4], g[5]); unpack_bf16x2(ug.w, g[6], g[7]);
-      unpack_bf16x2(uo.x, o[0], o[1]); unpack_bf16x2(uo.y, o[2], o[3]);
-      unpack_bf16x2(uo.z, o[4], o[5]); unpack_bf16x2(uo.w, o[6], o[7]);
+      unpack_bf16x2(ud[t].x, dout[0], dout[1]); unpack_bf16x2(ud[t].y, dout[2], dout[3]);
+      unpack_bf16x2(ud[t].z, dout[4], dout[5]); unpack_bf16x2(ud[t].w, dout[6], dout[7]);
+      unpack_bf16x2(ug[t].x, g[0], g[1]); unpack_bf16x2(ug[t].y, g[2], g[3]);
+      unpack_bf16x2(ug[t].z, g[4], g[5]); unpack_bf16x2(ug[t].w, g[6], g[7]);
+      unpack_bf16x2(uo[t].x, o[0], o[1]); unpack_bf16x2(uo[t].y, o[2], o[3]);
+      unpack_bf16x2(uo[t].z, o[4], o[5]); unpack_bf16x2(uo[t].w, o[6], o[7]);
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        const float s = sigmoidf_(g[e]);
-        dO[e] = dout[e] * s;
-        dg[e] = dout[e] * o[e] * s * (1.f - s);
-        dsum += dO[e] * o[e];
+        const float sg = sigmoidf_(g[e]);
+        dO[e] = dout[e] * sg;
+        dg[e] = dout[e] * o[e] * sg * (1.f - sg);
+        dsum += bf2f(f2bf(dO[e])) * o[e];  // D of the bf16 dO the MMAs see
       }
       uint4 w;
       w.x = pack_bf16x2(dO[0], dO[1]); w.y = pack_bf16x2(dO[2], dO[3]);
@@ -113,9 +172,10 @@ __global__ void __launch_bounds__(256) attn_bwd_prep(AttnBwdParams P, int64_t B)
     }
     // segmented reduction over the lanes of one head (lanes_per_head is a power of 2)
     for (int o = 1; o < lanes_per_head; o <<= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
-    if (ch < nch && (lane % lanes_per_head) == 0) {
-      const int h = (ch * 8) / c;
-      P.Dsum[(b * H + h) * (int64_t)L + l] = dsum;
+    if (ok && (lane % lanes_per_head) == 0) {
+      const int64_t ix = (b * H + col / c) * (int64_t)L + l;
+      P.Dsum[ix] = dsum;
+      P.lse2[ix] = lse[t] * 1.4426950408889634f;
     }
   }
 }
@@ -185,7 +245,6 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int G
   constexpr bool db_store = MODE == 2;  // batch-shared full bias -> dS workspace
   const int nqt = (L + BW_BQ - 1) / BW_BQ;
   const int nkt = gridDim.x;
-  const float LOG2E_ = 1.4426950408889634f;
 
   if (warp == 0) tmem_alloc(&tmem_sh, 256);
   if (threadIdx.x == 0) {
@@ -194,9 +253,8 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int G
     fence_mbar_init();
   }
   const int64_t HC = (int64_t)H * c;
-  // gate backward fused into the tile load: dO = dout * sigmoid(g) (staged in smem),
-  // D = rowsum(dO * O) (4 lanes per row for c = 32), and - by the key-tile-0 CTAs only -
-  // dg = dout * O * s(1-s) written once per query row.
+  // every per-tile operand is a cp.async copy (dO, D and lse*log2e come from the prep kernel)
+  const bool vec_stats = (L & 3) == 0;
   auto issue_loads = [&](int64_t b, int qt, bool with_kv) {
     const int q0 = qt * BW_BQ;
     if (with_kv) {
@@ -204,53 +262,21 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int G
       bw_load<CP>(sb + SM::V, F.v + b * F.v_sb + (int64_t)h * c, F.v_sl, k0, L - k0, c);
     }
     bw_load<CP>(sb + SM::Q, F.q + b * F.q_sb + (int64_t)h * c, F.q_sl, q0, L - q0, c);
-    cp_async_commit();
-    if (threadIdx.x < BW_BQ) {
-      const int qq = q0 + threadIdx.x;
-      s_lse[threadIdx.x] = qq < L ? F.lse[(b * H + h) * (int64_t)L + qq] * LOG2E_ : 0.f;
-    }
-    constexpr int CPR = CP / 8;
-    for (int ch = threadIdx.x; ch < BW_BQ * CPR; ch += 256) {
-      const int r = ch / CPR, d0 = (ch % CPR) * 8, qq = q0 + r;
-      float dO[8], part = 0.f;
-      if (qq < L && d0 < c) {
-        float dout[8], g[8], o[8];
-        const uint4 ud = *reinterpret_cast<const uint4*>(P.dout + b * P.do_sb + (int64_t)qq * P.do_sl + h * c + d0);
-        const uint4 ug = *reinterpret_cast<const uint4*>(F.g + b * F.g_sb + (int64_t)qq * F.g_sl + h * c + d0);
-        const uint4 uo = *reinterpret_cast<const uint4*>(F.orw + b * F.r_sb + (int64_t)qq * F.r_sl + h * c + d0);
-        unpack_bf16x2(ud.x, dout[0], dout[1]); unpack_bf16x2(ud.y, dout[2], dout[3]);
-        unpack_bf16x2(ud.z, dout[4], dout[5]); unpack_bf16x2(ud.w, dout[6], dout[7]);
-        unpack_bf16x2(ug.x, g[0], g[1]); unpack_bf16x2(ug.y, g[2], g[3]);
-        unpack_bf16x2(ug.z, g[4], g[5]); unpack_bf16x2(ug.w, g[6], g[7]);
-        unpack_bf16x2(uo.x, o[0], o[1]); unpack_bf16x2(uo.y, o[2], o[3]);
-        unpack_bf16x2(uo.z, o[4], o[5]); unpack_bf16x2(uo.w, o[6], o[7]);
-        float dg[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float sg = sigmoidf_(g[e]);
-          dO[e] = dout[e] * sg;
-          dg[e] = dout[e] * o[e] * sg * (1.f - sg);
-        }
-        // D uses the bf16-rounded dO that the MMAs see
-#pragma unroll
-        for (int e = 0; e < 8; ++e) part += bf2f(f2bf(dO[e])) * o[e];
-        if (blockIdx.x == 0) {
-          uint4 w;
-          w.x = pack_bf16x2(dg[0], dg[1]); w.y = pack_bf16x2(dg[2], dg[3]);
-          w.z = pack_bf16x2(dg[4], dg[5]); w.w = pack_bf16x2(dg[6], dg[7]);
-          *reinterpret_cast<uint4*>(P.dg + b * P.dg_sb + (int64_t)qq * P.dg_sl + h * c + d0) = w;
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) dO[e] = 0.f;
+    bw_load<CP>(sb + SM::DO, P.dO + b * L * HC + (int64_t)h * c, HC, q0, L - q0, c);
+    const int64_t st0 = (b * H + h) * (int64_t)L + q0;
+    if (vec_stats) {
+      if (threadIdx.x < 2 * BW_BQ / 4) {
+        const int t = threadIdx.x & (BW_BQ / 4 - 1);
+        const bool ok = q0 + 4 * t < L;
+        const float* src = threadIdx.x < BW_BQ / 4 ? P.lse2 : P.Dsum;
+        cp_async16(sb + (threadIdx.x < BW_BQ / 4 ? SM::LSE : SM::DD) + 16 * t, ok ? src + st0 + 4 * t : src, ok);
       }
-      st_shared_v4(sb + SM::DO + kmajor_off(r, d0, 128), pack_bf16x2(dO[0], dO[1]), pack_bf16x2(dO[2], dO[3]),
-                   pack_bf16x2(dO[4], dO[5]), pack_bf16x2(dO[6], dO[7]));
-      // the CPR chunks of a row sit on consecutive lanes
-#pragma unroll
-      for (int o = 1; o < CPR; o <<= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-      if (ch % CPR == 0) s_D[r] = part;
+    } else if (threadIdx.x < BW_BQ) {
+      const bool ok = q0 + (int)threadIdx.x < L;
+      s_lse[threadIdx.x] = ok ? P.lse2[st0 + threadIdx.x] : 0.f;
+      s_D[threadIdx.x] = ok ? P.Dsum[st0 + threadIdx.x] : 0.f;
     }
+    cp_async_commit();
   };
   issue_loads(b_begin, 0, true);
   tc_fence_before();
@@ -276,7 +302,6 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int G
     if ((MODE == 2 || MODE == 3) && kvalid) bias_col = F.bias + b * F.bs0 + (int64_t)h * F.bs1 + (int64_t)kj * F.bs3;
     float* dbias_col = nullptr;
     if (P.dbias && kvalid) dbias_col = P.dbias + b * P.db0 + (int64_t)h * P.db1 + (int64_t)kj * P.db3;
-    bf16* ds_col = (db_store && kvalid) ? P.dS + ((b * H + h) * (int64_t)L) * L + kj : nullptr;
     const int bs2 = (int)F.bs2;  // full-bias query stride (< 2^31)
     for (int qt = 0; qt < nqt; ++qt, ++it) {
       const int q0 = qt * BW_BQ;
@@ -309,7 +334,25 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int G
         float pv[16], dsv[16];
         const bool all_valid = kvalid && q0 + qc + 16 <= L;
         float bv[16];
-        if constexpr (MODE == 2 || MODE == 3) {
+        if constexpr (MODE == 2) {  // transposed batch-shared bias: 16 consecutive queries per key
+          if (bias_col) {
+            const bf16* bp = bias_col + (q0 + qc);
+#pragma unroll
+            for (int e = 0; e < 16; e += 8) {
+              if (q0 + qc + e < L) {
+                const uint4 u = *reinterpret_cast<const uint4*>(bp + e);
+                unpack_bf16x2(u.x, bv[e], bv[e + 1]); unpack_bf16x2(u.y, bv[e + 2], bv[e + 3]);
+                unpack_bf16x2(u.z, bv[e + 4], bv[e + 5]); unpack_bf16x2(u.w, bv[e + 6], bv[e + 7]);
+              } else {
+#pragma unroll
+                for (int t = 0; t < 8; ++t) bv[e + t] = 0.f;
+              }
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) bv[e] = 0.f;
+          }
+        } else if constexpr (MODE == 3) {
           if (bias_col) {
             const bf16* bp = bias_col + (q0 + qc) * bs2;
 #pragma unroll
@@ -339,14 +382,11 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int G
         }
 #pragma unroll
         for (int e = 0; e < 16; ++e) dsv[e] = pv[e] * (dp[e] - D16[e]);
-        if constexpr (MODE == 2) {
-          if (ds_col) {
-            bf16* dp_ = ds_col + (q0 + qc) * L;
+#if EVO_EXP == 1
 #pragma unroll
-            for (int e = 0; e < 16; ++e)
-              if (q0 + qc + e < L) dp_[e * L] = f2bf(P.scale * dsv[e]);
-          }
-        } else if constexpr (MODE == 1) {
+        for (int e = 0; e < 16; ++e) { pv[e] = s[e]; dsv[e] = dp[e]; }
+#endif
+        if constexpr (MODE == 1) {
 #pragma unroll
           for (int e = 0; e < 16; ++e) kb_acc += dsv[e];
         } else if constexpr (MODE == 3) {
@@ -374,6 +414,7 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int G
       if (db_per_key && wg == 0 && dbias_col) atomicAdd(dbias_col, P.scale * (s_kb[kr] + s_kb[BW_BK + kr]));
       if (threadIdx.x == 0) {
         tc_fence_after();
+#if EVO_EXP != 2
 #pragma unroll
         for (int kk = 0; kk < BW_BQ / 16; ++kk) {
           const uint32_t aoff = kk * 2 * LBO_ROWS;
@@ -389,6 +430,7 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int G
           mma_bf16(tmem + T_DQ, make_sdesc(sb + SM::DST + off, 128, LBO_ROWS),
                    make_sdesc(sb + SM::K + off, 128, LBO_ROWS), ID_Q, kk != 0);
         }
+#endif
         mma_commit(&bar2);
       }
       mbar_wait(&bar2, it & 1);
@@ -396,6 +438,24 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int G
       // the tiles are free: prefetch the next (batch, query tile) while draining TMEM
       const bool last_q = qt + 1 == nqt;
       if (!(last_q && b + 1 == b_end)) issue_loads(last_q ? b + 1 : b, last_q ? 0 : qt + 1, last_q);
+      if constexpr (db_store) {
+        // dS^T tile (unscaled bf16, canonical K-major [key][query]) -> workspace [b][h][key][query]:
+        // lane = (query group % 4, key % 8) so each smem phase reads 128 contiguous bytes and
+        // each key row gets 64 contiguous bytes per store (requires L % 8 == 0)
+        bf16* wsb = P.dS + ((b * H + h) * (int64_t)L + k0) * L + q0;
+#pragma unroll
+        for (int i = 0; i < (BW_BK * BW_BQ / 8) / 256; ++i) {
+          const int ch = threadIdx.x + i * 256;
+          const int r = ((ch >> 5) & 15) * 8 + (ch & 7);
+          const int g = (ch >> 9) * 4 + ((ch >> 3) & 3);
+          if (k0 + r < L && q0 + g * 8 < L) {
+            const uint4 v = *reinterpret_cast<const uint4*>(smem + SM::DST + (g * (BW_BK / 8) + (r >> 3)) * 128 +
+                                                            (r & 7) * 16);
+            *reinterpret_cast<uint4*>(wsb + (int64_t)r * L + g * 8) = v;
+          }
+        }
+      }
+#if EVO_EXP != 3
       {
 #pragma unroll
         for (int cc = 0; cc < CP; cc += 16) {
@@ -412,7 +472,24 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int G
         tmem_ld_wait();
         const int qq = q0 + kr;  // dQ: TMEM lane = query row
         if (qq < L) {
-          if (dq_partial) {
+          if (dq_partial == 2) {  // one key tile: dQ is final, written as bf16 (no finish pass)
+            bf16* dst = P.dq + b * P.dq_sb + (int64_t)qq * P.dq_sl + (int64_t)h * c + wg * (CP / 2);
+            if (wg * (CP / 2) + CP / 2 <= c && (CP / 2) % 8 == 0) {
+#pragma unroll
+              for (int e = 0; e < CP / 2; e += 8) {
+                uint4 u;
+                u.x = pack_bf16x2(P.scale * w[e], P.scale * w[e + 1]);
+                u.y = pack_bf16x2(P.scale * w[e + 2], P.scale * w[e + 3]);
+                u.z = pack_bf16x2(P.scale * w[e + 4], P.scale * w[e + 5]);
+                u.w = pack_bf16x2(P.scale * w[e + 6], P.scale * w[e + 7]);
+                *reinterpret_cast<uint4*>(dst + e) = u;
+              }
+            } else {
+#pragma unroll
+              for (int e = 0; e < CP / 2; ++e)
+                if (wg * (CP / 2) + e < c) dst[e] = f2bf(P.scale * w[e]);
+            }
+          } else if (dq_partial) {
             float* dst = P.dQacc + (((int64_t)blockIdx.x * Btot + b) * L + qq) * HC + (int64_t)h * c + wg * (CP / 2);
             if (wg * (CP / 2) + CP / 2 <= c) {
 #pragma unroll
@@ -432,6 +509,7 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int G
           }
         }
       }
+#endif
       tc_fence_before();
       __syncthreads();
     }
@@ -485,17 +563,21 @@ __global__ void __launch_bounds__(256) attn_bwd_dq_finish(AttnBwdParams P, int64
 constexpr int DQ_MAX_PARTS = 4;  // <= 4 key tiles (L <= 512): per-tile dQ partials, plain stores
 
 static int64_t ws_layout(int64_t B, int64_t L, int H, int c, int bias_batch_reduced, int64_t* off_dq, int64_t* off_D,
-                         int64_t* off_dS) {
+                         int64_t* off_lse2, int64_t* off_dS) {
   const int64_t n = B * L * (int64_t)H * c;
   const int64_t nkt = (L + BW_BK - 1) / BW_BK;
-  const int64_t parts = nkt <= DQ_MAX_PARTS ? nkt : 1;
+  const int64_t parts = nkt == 1 ? 0 : (nkt <= DQ_MAX_PARTS ? nkt : 1);
+  const int64_t stats = ((B * H * L * 4 + 255) / 256) * 256;
   int64_t o1 = ((n * 2 + 255) / 256) * 256;
   int64_t o2 = o1 + ((parts * n * 4 + 255) / 256) * 256;
-  int64_t o3 = o2 + ((B * H * L * 4 + 255) / 256) * 256;
+  int64_t o3 = o2 + stats;
+  int64_t o4 = o3 + stats;
   if (off_dq) *off_dq = o1;
   if (off_D) *off_D = o2;
-  if (off_dS) *off_dS = o3;
-  return o3 + (bias_batch_reduced ? ((B * H * L * L * 2 + 255) / 256) * 256 : 0);
+  if (off_lse2) *off_lse2 = o3;
+  if (off_dS) *off_dS = o4;
+  // batch-shared bias: dS^T workspace [B][H][L][L] + the transposed bias [H][L][L]
+  return o4 + (bias_batch_reduced ? ((B * H * L * L * 2 + 255) / 256) * 256 + ((H * L * L * 2 + 255) / 256) * 256 : 0);
 }
 
 int sm_count();
@@ -512,9 +594,11 @@ static int launch_bwd_m(AttnBwdParams& p, int64_t B, int dq_partial, cudaStream_
   }
   const int64_t nkt = (p.f.L + BW_BK - 1) / BW_BK;
   const int64_t units = B * p.f.H * nkt;
-  int64_t G = units / ((int64_t)sm_count() * 2 * 2);  // ~2 waves at 2 CTAs/SM
-  if (G < 1) G = 1;
-  if (G > 16) G = 16;
+  // one batch per CTA: the hardware block scheduler then balances the (batch, head, key
+  // tile) units over the 2-CTA/SM slots with at most one partial tail (grouping batches per
+  // CTA left a 1/3-full third wave at the training shape)
+  const int64_t G = 1;
+  (void)units;
   dim3 grid((unsigned)nkt, (unsigned)p.f.H, (unsigned)((B + G - 1) / G));
   attn_bwd_kernel<CP, MODE><<<grid, 256, SM::TOTAL, st>>>(p, (int)G, dq_partial);
   EVO_LAUNCH_CHECK("attention bwd main");
@@ -534,7 +618,7 @@ static int launch_bwd(AttnBwdParams& p, int64_t B, int dq_partial, cudaStream_t 
 using namespace evo;
 
 extern "C" int64_t evo_gated_attention_bwd_workspace(int64_t B, int64_t L, int H, int c, int bias_batch_reduced) {
-  return ws_layout(B, L, H, c, bias_batch_reduced, nullptr, nullptr, nullptr);
+  return ws_layout(B, L, H, c, bias_batch_reduced && L % 8 == 0, nullptr, nullptr, nullptr, nullptr);
 }
 
 extern "C" int evo_gated_attention_bwd(const EvoAttnBwdDesc* d, void* stream) {
@@ -546,9 +630,12 @@ extern "C" int evo_gated_attention_bwd(const EvoAttnBwdDesc* d, void* stream) {
                 "attention bwd: null pointer (o_raw, lse, dout, dq, dk, dv, dg, workspace are required)");
   const int64_t B = d->f.B, L = d->f.L;
   const int H = d->f.H, c = d->f.c;
-  int64_t off_dq, off_D, off_dS;
-  const int batch_reduced = d->dbias && d->f.bias && d->dbias_s[0] == 0 && d->dbias_s[2] != 0;
-  const int64_t need = ws_layout(B, L, H, c, batch_reduced, &off_dq, &off_D, &off_dS);
+  EVO_CHECK_ARG((c & (c - 1)) == 0, EVO_ERR_SHAPE, "attention bwd: head dim must be 8, 16, 32 or 64 (got %d)", c);
+  int64_t off_dq, off_D, off_lse2, off_dS;
+  // batch-shared full bias (msa_row): dS^T tiles to a workspace, reduced over the batch after
+  // (16-byte tile copies need L % 8 == 0; otherwise the generic atomic path)
+  const int batch_reduced = d->dbias && d->f.bias && d->dbias_s[0] == 0 && d->dbias_s[2] != 0 && L % 8 == 0;
+  const int64_t need = ws_layout(B, L, H, c, batch_reduced, &off_dq, &off_D, &off_lse2, &off_dS);
   EVO_CHECK_ARG(d->workspace_bytes >= need, EVO_ERR_ARG, "attention bwd: workspace %lld < %lld bytes",
                 (long long)d->workspace_bytes, (long long)need);
   const int64_t strides[] = {d->do_sb, d->do_sl, d->dq_sb, d->dq_sl, d->dk_sb, d->dk_sl, d->dv_sb, d->dv_sl,
@@ -565,29 +652,50 @@ extern "C" int evo_gated_attention_bwd(const EvoAttnBwdDesc* d, void* stream) {
   p.dO = (bf16*)ws;
   p.dQacc = (float*)(ws + off_dq);
   p.Dsum = (float*)(ws + off_D);
+  p.lse2 = (float*)(ws + off_lse2);
   p.dS = batch_reduced ? (bf16*)(ws + off_dS) : nullptr;
+  // MODE 2 reads the batch-shared bias transposed ([h][key][query], queries contiguous)
+  const bool bias_shared = batch_reduced && d->f.bias_s[0] == 0 && d->f.bias_s[3] == 1 && d->f.bias_s[1] % 8 == 0 &&
+                           d->f.bias_s[2] % 8 == 0;
+  if (batch_reduced && !bias_shared) p.dS = nullptr;  // generic atomic path (MODE 3)
+
   p.scale = d->f.scale;
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t nkt = (L + BW_BK - 1) / BW_BK;
-  const int dq_partial = nkt <= DQ_MAX_PARTS ? 1 : 0;
+  // 1 key tile: final bf16 dQ from the main kernel; <= 4: per-tile fp32 partials summed by the
+  // finish pass; more: fp32 atomics into one accumulator
+  const int dq_partial = nkt == 1 ? 2 : (nkt <= DQ_MAX_PARTS ? 1 : 0);
   p.B = B;
   if (!dq_partial) {
     cudaError_t e = cudaMemsetAsync(p.dQacc, 0, (size_t)(B * L * H * c) * 4, st);
     if (e != cudaSuccess) return cuda_status(e, "attention bwd memset");
   }
+  {
+    const int64_t rows = B * L;
+    const int64_t pairs = rows * (H * c / 8), per_cta = 8 * PREP_PASSES * 32;
+    attn_bwd_prep<<<(unsigned)((pairs + per_cta - 1) / per_cta), 256, 0, st>>>(p, B);
+    EVO_LAUNCH_CHECK("attention bwd prep");
+  }
+  if (p.dS) {
+    bf16* bias_t = (bf16*)(ws + off_dS + ((B * H * L * L * 2 + 255) / 256) * 256);
+    dim3 tg((unsigned)((L + 31) / 32), (unsigned)((L + 31) / 32), (unsigned)H);
+    attn_bias_transpose<<<tg, 256, 0, st>>>(p.f.bias, p.f.bs1, p.f.bs2, bias_t, (int)L);
+    EVO_LAUNCH_CHECK("attention bwd bias transpose");
+    p.f.bias = bias_t;
+    p.f.bs0 = 0; p.f.bs1 = L * L; p.f.bs2 = 1; p.f.bs3 = L;
+  }
   if (c <= 16) rc = launch_bwd<16>(p, B, dq_partial, st);
   else if (c <= 32) rc = launch_bwd<32>(p, B, dq_partial, st);
   else rc = launch_bwd<64>(p, B, dq_partial, st);
   if (rc) return rc;
-  if (batch_reduced) {
-    const int vec = L % 8 == 0 ? 8 : 1;
-    int64_t nv = (int64_t)H * L * L / vec;
+  if (p.dS) {
+    int64_t nv = (int64_t)H * L * L / 8;
     int64_t g2 = (nv + 255) / 256, cap2 = (int64_t)sm_count() * 8;
     unsigned g2u = (unsigned)(g2 < cap2 ? g2 : cap2);
-    if (vec == 8) attn_dbias_reduce<8><<<g2u, 256, 0, st>>>(p.dS, p.dbias, B, H, L, p.db1, p.db2, p.db3);
-    else attn_dbias_reduce<1><<<g2u, 256, 0, st>>>(p.dS, p.dbias, B, H, L, p.db1, p.db2, p.db3);
+    attn_dbias_reduce<<<g2u, 256, 0, st>>>(p.dS, p.dbias, B, H, L, p.db1, p.db2, p.db3, p.scale);
     EVO_LAUNCH_CHECK("attention bwd dbias reduce");
   }
+  if (dq_partial == 2) return EVO_OK;
   int64_t n8 = B * L * H * c / 8;
   int64_t g = (n8 + 255) / 256, cap = (int64_t)sm_count() * 16;
   attn_bwd_dq_finish<<<(unsigned)(g < cap ? g : cap), 256, 0, st>>>(p, B, dq_partial ? (int)nkt : 1);

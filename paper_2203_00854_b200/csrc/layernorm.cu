@@ -358,12 +358,39 @@ __global__ void __launch_bounds__(256) ln_fwd_grp(const TX* __restrict__ x, int6
   }
 }
 
+// 8 consecutive elements kept as raw bits until used (bf16: one 16-byte register quad), so
+// U row-groups of x, dy and res can be in flight without spilling the unpacked floats.
+template <typename T> struct Raw8;
+template <> struct Raw8<bf16> {
+  uint4 u;
+  __device__ __forceinline__ void load(const bf16* p) { u = *reinterpret_cast<const uint4*>(p); }
+  __device__ __forceinline__ void zero() { u = make_uint4(0, 0, 0, 0); }
+  __device__ __forceinline__ void get(float* v) const {
+    unpack_bf16x2(u.x, v[0], v[1]); unpack_bf16x2(u.y, v[2], v[3]);
+    unpack_bf16x2(u.z, v[4], v[5]); unpack_bf16x2(u.w, v[6], v[7]);
+  }
+};
+template <> struct Raw8<float> {
+  float4 a, b;
+  __device__ __forceinline__ void load(const float* p) {
+    a = *reinterpret_cast<const float4*>(p);
+    b = *reinterpret_cast<const float4*>(p + 4);
+  }
+  __device__ __forceinline__ void zero() { a = b = make_float4(0.f, 0.f, 0.f, 0.f); }
+  __device__ __forceinline__ void get(float* v) const {
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+};
+
+// LPR = COLS/8 lanes per row, each owning 8 channels; a CTA walks one contiguous slab of
+// rows, U row-groups per warp step with every load of the step issued before any math.
+// <= 128 registers (2 CTAs = 16 warps per SM) keep ~100 KB of loads in flight per SM.
 template <typename TD, typename TX, typename TO, int COLS, int U>
-__global__ void __launch_bounds__(256) ln_bwd_grp(const TD* __restrict__ dy, const TX* __restrict__ x, int64_t x_rs,
-                                                  const float* __restrict__ gamma, const float* __restrict__ mean,
-                                                  const float* __restrict__ rstd, TO* dx, const TO* res,
-                                                  float* __restrict__ dgamma, float* __restrict__ dbeta,
-                                                  int64_t rows) {
+__global__ void __launch_bounds__(256, 2) ln_bwd_grp(const TD* __restrict__ dy, const TX* __restrict__ x, int64_t x_rs,
+                                                     const float* __restrict__ gamma, const float* __restrict__ mean,
+                                                     const float* __restrict__ rstd, TO* dx, const TO* res,
+                                                     float* __restrict__ dgamma, float* __restrict__ dbeta,
+                                                     int64_t rows) {
   constexpr int LPR = COLS / 8, RPW = 32 / LPR;
   __shared__ float red[8][2][COLS];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, sub = lane / LPR, cl = (lane % LPR) * 8;
@@ -374,38 +401,49 @@ __global__ void __launch_bounds__(256) ln_bwd_grp(const TD* __restrict__ dy, con
   const int64_t slab = (rows + gridDim.x - 1) / gridDim.x;
   const int64_t r0 = blockIdx.x * slab, r1 = r0 + slab < rows ? r0 + slab : rows;
   for (int64_t rb = r0 + wid * RPW * U; rb < r1; rb += 8 * RPW * U) {
-    float xv[U][8], d[U][8], o[U][8];
+    Raw8<TX> rx[U];
+    Raw8<TD> rd[U];
+    Raw8<TO> rr[U];
+    float mu[U], rs[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t row = rb + u * RPW + sub;
       if (row < r1) {
-        load_row<TX, 8>(x + row * x_rs + cl, xv[u]);
-        load_row<TD, 8>(dy + row * COLS + cl, d[u]);
-        if (res) load_row<TO, 8>(res + row * x_rs + cl, o[u]);
+        rx[u].load(x + row * x_rs + cl);
+        rd[u].load(dy + row * COLS + cl);
+        if (res) rr[u].load(res + row * x_rs + cl);
+        mu[u] = mean[row];
+        rs[u] = rstd[row];
+      } else {
+        rx[u].zero();
+        rd[u].zero();
+        mu[u] = rs[u] = 0.f;
       }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t row = rb + u * RPW + sub;
-      const bool ok = row < r1;
-      const float mu = ok ? mean[row] : 0.f, rs = ok ? rstd[row] : 0.f;
+      float xv[8], d[8];
+      rx[u].get(xv);
+      rd[u].get(d);
       float s1 = 0.f, s2 = 0.f;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        if (!ok) xv[u][i] = d[u][i] = 0.f;
-        xv[u][i] = (xv[u][i] - mu) * rs;  // xhat
-        const float gd = g[i] * d[u][i];
+        xv[i] = (xv[i] - mu[u]) * rs[u];  // xhat
+        const float gd = g[i] * d[i];
         s1 += gd;
-        s2 += gd * xv[u][i];
-        dg[i] += d[u][i] * xv[u][i];
-        db[i] += d[u][i];
+        s2 += gd * xv[i];
+        dg[i] += d[i] * xv[i];
+        db[i] += d[i];
       }
       s1 = group_sum<LPR>(s1) * (1.0f / COLS);
       s2 = group_sum<LPR>(s2) * (1.0f / COLS);
-      if (ok) {
+      if (row < r1) {
+        float o[8];
+        if (res) rr[u].get(o);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) o[u][i] = (res ? o[u][i] : 0.f) + rs * (g[i] * d[u][i] - s1 - xv[u][i] * s2);
-        store_row<TO, 8>(dx + row * x_rs + cl, o[u]);
+        for (int i = 0; i < 8; ++i) o[i] = (res ? o[i] : 0.f) + rs[u] * (g[i] * d[i] - s1 - xv[i] * s2);
+        store_row<TO, 8>(dx + row * x_rs + cl, o);
       }
     }
   }
@@ -747,10 +785,10 @@ static int ln_bwd_impl(const void* dy, const void* x, int64_t x_rs, int64_t x_cs
                        cudaStream_t st) {
   if (x_cs == 1 && (cols == 32 || cols == 64 || cols == 128 || cols == 256)) {
     const int64_t rpw = 32 / (cols / 8);
-    int64_t need = (rows + 8 * rpw * 4 - 1) / (8 * rpw * 4), cap = (int64_t)sm_count() * 4;
+    int64_t need = (rows + 8 * rpw * 3 - 1) / (8 * rpw * 3), cap = (int64_t)sm_count() * 2;  // resident
     dim3 grid((unsigned)(need < cap ? need : cap));
 #define LBG(CC)                                                                                               \
-  ln_bwd_grp<TD, TX, TO, CC, (CC >= 256 ? 2 : 4)><<<grid, 256, 0, st>>>((const TD*)dy, (const TX*)x, x_rs, g, mean, \
+  ln_bwd_grp<TD, TX, TO, CC, 3><<<grid, 256, 0, st>>>((const TD*)dy, (const TX*)x, x_rs, g, mean, \
                                                                         rstd, (TO*)dx, (const TO*)res, dg, db, rows)
     switch (cols) {
       case 32: LBG(32); break;

@@ -215,9 +215,11 @@ def attention_bwd(fdesc: EvoAttnDesc, dout: Strided, dq: Strided, dk: Strided, d
     d.dbias_s = (C.c_int64 * 4)(*dbias_s)
     d.workspace = workspace.data_ptr()
     d.workspace_bytes = workspace.numel() * workspace.element_size()
-    batch_reduced = dbias is not None and fdesc.bias and dbias_s[0] == 0 and dbias_s[2] != 0
+    batch_reduced = (dbias is not None and fdesc.bias and dbias_s[0] == 0 and dbias_s[2] != 0
+                     and fdesc.L % 8 == 0)
     nkt = (fdesc.L + 127) // 128
-    launches = 2 + (1 if batch_reduced else 0) + (1 if nkt > 4 else 0)   # + dbias reduce, + dQ memset
+    # prep + main (+ dq finish when > 1 key tile), + bias transpose & dbias reduce, + dQ memset
+    launches = 2 + (1 if nkt > 1 else 0) + (2 if batch_reduced else 0) + (1 if nkt > 4 else 0)
     call("evo_gated_attention_bwd", C.byref(d), stream_handle(), work=_attn_work(fdesc, bwd=True),
          launches=launches)
 

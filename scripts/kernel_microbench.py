@@ -1,0 +1,138 @@
+"""Kernel microbench (BASELINE.json configs[4]): the fused bias+mask softmax (K2) and
+LayerNorm (K1) over pair-representation shapes, against the HBM roofline.
+
+    python scripts/kernel_microbench.py [--iters 50] [--out profiles/rNN_kernel_microbench.jsonl]
+
+Shapes:
+  K2 softmax: x [B=N_r, H=4, L=N_r, L] bf16 with a per-key bias [N_r, 4, 1, N_r] and a
+              key mask [N_r, 1, 1, N_r] (engine.fused_softmax_mask_bias_raw, engine.py:193-203),
+              and the msa_row shape [128, 8, 256, 256] with a batch-shared bias [1, 8, 256, 256];
+  K1 LayerNorm: [65536, 128], [32768, 256], [65536, 32] bf16 (engine.layernorm_raw, engine.py:206-217).
+Algorithmic bytes = every input read once + every output written once (bf16 activations,
+fp32 gamma/beta/statistics).  Each timed launch reads a fresh buffer from a rotating set
+larger than L2 (126 MB), so no launch hits warm L2.  Times: CUDA events on the launching
+stream, warm, mean over --iters launches.  Peak: MEASURED_PEAKS.json hbm_gbs (else the
+B200_PROFILING.md fallback).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2203_00854_b200 import _lib, ops  # noqa: E402
+
+L2_BYTES = 126 * 2**20
+
+
+def peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        return float(json.load(open(p)).get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def rotating(make, nbytes_each):
+    """enough independent copies that consecutive launches never see warm L2"""
+    n = max(2, int(2 * L2_BYTES // max(nbytes_each, 1)) + 1)
+    return [make() for _ in range(min(n, 8))]
+
+
+def time_launches(fn, sets, iters):
+    for s in sets[:2]:
+        fn(*s)
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(st)
+    for i in range(iters):
+        fn(*sets[i % len(sets)])
+    b.record(st)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / iters
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--iters", type=int, default=50)
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    _lib.load()
+    dev = torch.device("cuda")
+    peak, src = peak_hbm()
+    lines = []
+    g = torch.Generator(device=dev).manual_seed(0)
+
+    def emit(kernel, shape, ms, nbytes, extra=None):
+        gbs = nbytes / (ms * 1e-3) / 1e9
+        d = {"kernel": kernel, "shape": shape, "us_per_launch": round(ms * 1e3, 2),
+             "algorithmic_bytes": int(nbytes), "achieved_gbs": round(gbs, 1), "peak_gbs": peak,
+             "frac": round(gbs / peak, 4), "peak_source": src}
+        if extra:
+            d.update(extra)
+        lines.append(d)
+        print(json.dumps(d), flush=True)
+
+    # ------------------------------------------------------------------ K2 fused softmax
+    cases = [
+        ("pair[N_r=256]: x[256,4,256,256], bias[256,4,1,256], mask[256,1,1,256]", (256, 4, 256, 256),
+         (256, 4, 1, 256), (256, 1, 1, 256)),
+        ("msa_row: x[128,8,256,256], bias[1,8,256,256]", (128, 8, 256, 256), (1, 8, 256, 256), None),
+        ("pair[N_r=512]: x[512,4,512,512], bias[512,4,1,512], mask[512,1,1,512]", (512, 4, 512, 512),
+         (512, 4, 1, 512), (512, 1, 1, 512)),
+    ]
+    for name, xs, bs, ms_ in cases:
+        nx = xs[0] * xs[1] * xs[2] * xs[3]
+        bias = torch.randn(bs, device=dev, generator=g).bfloat16()
+        mask = None
+        if ms_ is not None:
+            mask = torch.zeros(ms_, device=dev, dtype=torch.bfloat16)
+            mask[..., -7:] = -1e30  # engine.py:31 masked keys
+        sets = rotating(lambda: (torch.randn(xs, device=dev, generator=g).bfloat16(),
+                                 torch.empty(xs, device=dev, dtype=torch.bfloat16)), nx * 4)
+        scale = 32 ** -0.5
+        t = time_launches(lambda x, y: ops.softmax_fwd(x, bias, mask, scale, out=y), sets, a.iters)
+        nbytes = nx * 2 * 2 + bias.numel() * 2 + (mask.numel() * 2 if mask is not None else 0)
+        emit("evo_softmax_fwd", name, t, nbytes)
+        bsets = [(y, x, torch.empty_like(x)) for (x, y) in sets]  # y = softmax out, dy = x reused
+        t = time_launches(lambda y, dy, dx: ops.softmax_bwd(y, dy, scale, out=dx), bsets, a.iters)
+        emit("evo_softmax_bwd", name, t, nx * 2 * 3)
+        del sets, bsets
+        torch.cuda.empty_cache()
+
+    # ------------------------------------------------------------------ K1 LayerNorm
+    for rows, cols in ((65536, 128), (32768, 256), (65536, 32), (1048576, 128)):
+        gam = torch.randn(cols, device=dev, generator=g)
+        bet = torch.randn(cols, device=dev, generator=g)
+        n = rows * cols
+        sets = rotating(lambda: (torch.randn(rows, cols, device=dev, generator=g).bfloat16(),
+                                 torch.empty(rows, cols, device=dev, dtype=torch.bfloat16),
+                                 torch.empty(rows, device=dev), torch.empty(rows, device=dev)), n * 4)
+        t = time_launches(lambda x, y, mu, rs: ops.layernorm_fwd(x, gam, bet, rows, cols, out=y, mean=mu, rstd=rs),
+                          sets, a.iters)
+        emit("evo_layernorm_fwd", f"[{rows},{cols}]", t, n * 2 * 2 + rows * 8 + cols * 8)
+        dgam = torch.zeros(cols, device=dev)
+        dbet = torch.zeros(cols, device=dev)
+        # backward: dy = y buffer, x, stats from the forward; dx written into a fresh buffer
+        bsets = [(y, x, mu, rs, torch.empty_like(x)) for (x, y, mu, rs) in sets]
+        t = time_launches(lambda dy, x, mu, rs, dx: ops.layernorm_bwd(dy, x, gam, mu, rs, rows, cols, dx=dx,
+                                                                     dgamma=dgam, dbeta=dbet),
+                          bsets, a.iters)
+        emit("evo_layernorm_bwd", f"[{rows},{cols}] (+dgamma/dbeta)", t, n * 2 * 3 + rows * 8 + cols * 12)
+        del sets, bsets
+        torch.cuda.empty_cache()
+
+    if a.out:
+        with open(a.out, "w") as f:
+            for d in lines:
+                f.write(json.dumps(d) + "\n")
+
+
+if __name__ == "__main__":
+    main()
