@@ -65,6 +65,7 @@ _SIGS = {
     "evo_softmax_bwd": [vp, C.c_int, vp, C.c_int, vp, C.c_int, i64, i64, C.c_float, vp],
     "evo_gated_attention_fwd": [C.POINTER(EvoAttnDesc), vp],
     "evo_gated_attention_bwd": [C.POINTER(EvoAttnBwdDesc), vp],
+    "evo_attention_fwd_ws_min_len": [C.c_int],
     "evo_gated_attention_bwd_workspace": [i64, i64, C.c_int, C.c_int, C.c_int],
     "evo_bgemm": [C.POINTER(EvoMat), C.POINTER(EvoMat), C.POINTER(EvoMat), i64, i64, i64, i64,
                   C.c_float, C.c_float, vp],

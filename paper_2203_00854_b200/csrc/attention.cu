@@ -315,11 +315,30 @@ int attn_params_from_desc(const EvoAttnDesc* d, AttnParams& p) {
 
 using namespace evo;
 
+namespace evo {
+template <int CP>
+int launch_attn_fwd_ws(const AttnParams& p, int64_t B, cudaStream_t st);
+// sequences at least this long take the warp-specialised kernel (attention_ws.cu)
+static int g_ws_min_len = 2048;  // measured: faster than attn_fwd_kernel from N_r = 2048 on
+}  // namespace evo
+
+extern "C" int evo_attention_fwd_ws_min_len(int len) {
+  const int old = g_ws_min_len;
+  if (len > 0) g_ws_min_len = len;
+  return old;
+}
+
 extern "C" int evo_gated_attention_fwd(const EvoAttnDesc* d, void* stream) {
   AttnParams p;
   int rc = attn_params_from_desc(d, p);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
+  const bool ws_bias_ok = true;
+  if (p.L >= g_ws_min_len && ws_bias_ok) {
+    if (p.c <= 16) return launch_attn_fwd_ws<16>(p, d->B, st);
+    if (p.c <= 32) return launch_attn_fwd_ws<32>(p, d->B, st);
+    return launch_attn_fwd_ws<64>(p, d->B, st);
+  }
   if (p.c <= 16) return launch_attn_fwd<16>(p, d->B, st);
   if (p.c <= 32) return launch_attn_fwd<32>(p, d->B, st);
   return launch_attn_fwd<64>(p, d->B, st);

@@ -11,7 +11,7 @@ pytestmark = pytest.mark.gpu
 if not torch.cuda.is_available():  # collected on CPU too; the gpu marker deselects
     pytest.skip("needs CUDA", allow_module_level=True)
 
-from paper_2203_00854_b200 import ops  # noqa: E402
+from paper_2203_00854_b200 import _lib, ops  # noqa: E402
 from paper_2203_00854_b200.ops import Mat, Strided  # noqa: E402
 
 DEV = "cuda"
@@ -170,6 +170,22 @@ def _attn_ref(q, k, v, g, bias, scale):
     a = torch.softmax(s * scale, -1)
     o = a @ v
     return torch.sigmoid(g) * o, o
+
+
+@pytest.fixture
+def ws_forward():
+    """force the warp-specialised long-sequence forward (attention_ws.cu) for every L"""
+    lib = _lib.load()
+    old = lib.evo_attention_fwd_ws_min_len(1)
+    yield
+    lib.evo_attention_fwd_ws_min_len(old)
+
+
+@pytest.mark.parametrize("L,c,H,mode", [(256, 32, 8, "full"), (128, 32, 8, "none"), (256, 32, 4, "key"),
+                                        (100, 16, 2, "full"), (300, 64, 2, "key"), (40, 8, 4, "none"),
+                                        (600, 32, 2, "key"), (1024, 32, 1, "full")])
+def test_attention_fwd_bwd_ws(L, c, H, mode, ws_forward):
+    test_attention_fwd_bwd(L, c, H, mode)
 
 
 @pytest.mark.parametrize("L,c,H,mode", [(256, 32, 8, "full"), (128, 32, 8, "none"), (256, 32, 4, "key"),
