@@ -44,10 +44,12 @@ struct AttnBwdParams {
 };
 
 // dbias[h][q][k] += scale * sum_b dS[b][h][k][q]   (batch-shared bias: msa_row, evoformer.py:214).
-// Thread = 8 consecutive queries of one (h, key): 16-byte loads, B of them in flight.
+// Thread = 8 consecutive queries of one (h, key); 8 batches' 16-byte loads in flight per
+// thread (the read of the B x H x L x L workspace is the whole cost, so it must saturate HBM).
 __global__ void __launch_bounds__(256) attn_dbias_reduce(const bf16* __restrict__ dS, float* __restrict__ dbias,
                                                          int64_t B, int H, int L, int64_t d1, int64_t d2, int64_t d3,
                                                          float scale) {
+  constexpr int U = 8;
   const int64_t per = (int64_t)H * L * L;
   const int64_t nv = per / 8;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
@@ -56,12 +58,12 @@ __global__ void __launch_bounds__(256) attn_dbias_reduce(const bf16* __restrict_
 #pragma unroll
     for (int k = 0; k < 8; ++k) acc[k] = 0.f;
     int64_t b = 0;
-    for (; b + 4 <= B; b += 4) {
-      uint4 u[4];
+    for (; b + U <= B; b += U) {  // unguarded: all U loads issue back to back
+      uint4 u[U];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) u[t] = *reinterpret_cast<const uint4*>(dS + (b + t) * per + e);
+      for (int t = 0; t < U; ++t) u[t] = *reinterpret_cast<const uint4*>(dS + (b + t) * per + e);
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
+      for (int t = 0; t < U; ++t) {
         float v[8];
         unpack_bf16x2(u[t].x, v[0], v[1]); unpack_bf16x2(u[t].y, v[2], v[3]);
         unpack_bf16x2(u[t].z, v[4], v[5]); unpack_bf16x2(u[t].w, v[6], v[7]);
@@ -218,7 +220,7 @@ __device__ __forceinline__ void bw_load(uint32_t sdst, const bf16* base, int64_t
 // over the batch with dS stored for the batch reduction (msa_row), 3 = generic full bias
 // (fp32 atomics).  Specialised so the per-element loop carries no dead predicated paths.
 template <int CP, int MODE>
-__global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int G, int dq_partial) {
+__global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int nkt, int dq_partial) {
   using SM = BwdSmem<CP>;
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar1, bar2;
@@ -230,21 +232,17 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int G
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wq = warp & 3, wg = warp >> 2;
-  const int k0 = blockIdx.x * BW_BK;
-  const int h = blockIdx.y;
   const AttnParams& F = P.f;
   const int L = F.L, c = F.c, H = F.H;
   const int64_t Btot = P.B;
-  const int64_t b_begin = (int64_t)blockIdx.z * G;
-  const int64_t b_end = b_begin + G < Btot ? b_begin + G : Btot;
   const int kr = wq * 32 + lane;  // key row of this thread (TMEM lane)
-  const int kj = k0 + kr;
-  const bool kvalid = kj < L;
   constexpr bool per_key_bias = MODE == 1;
   const bool db_per_key = MODE == 1 && P.dbias != nullptr;
   constexpr bool db_store = MODE == 2;  // batch-shared full bias -> dS workspace
   const int nqt = (L + BW_BQ - 1) / BW_BQ;
-  const int nkt = gridDim.x;
+  // persistent CTAs walk the (batch, head, key tile) units; the first query tile of the next
+  // unit (and its K/V) is prefetched under the TMEM drain of the current unit's last tile
+  const int64_t units = Btot * H * nkt;
 
   if (warp == 0) tmem_alloc(&tmem_sh, 256);
   if (threadIdx.x == 0) {
@@ -255,7 +253,7 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int G
   const int64_t HC = (int64_t)H * c;
   // every per-tile operand is a cp.async copy (dO, D and lse*log2e come from the prep kernel)
   const bool vec_stats = (L & 3) == 0;
-  auto issue_loads = [&](int64_t b, int qt, bool with_kv) {
+  auto issue_loads = [&](int64_t b, int h, int k0, int qt, bool with_kv) {
     const int q0 = qt * BW_BQ;
     if (with_kv) {
       bw_load<CP>(sb + SM::K, F.k + b * F.k_sb + (int64_t)h * c, F.k_sl, k0, L - k0, c);
@@ -278,7 +276,18 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int G
     }
     cp_async_commit();
   };
-  issue_loads(b_begin, 0, true);
+  auto decode = [&](int64_t u, int64_t& b, int& h, int& kt) {
+    kt = (int)(u % nkt);
+    const int64_t t = u / nkt;
+    h = (int)(t % H);
+    b = t / H;
+  };
+  {
+    int64_t b0;
+    int h0, kt0;
+    decode(blockIdx.x, b0, h0, kt0);
+    if ((int64_t)blockIdx.x < units) issue_loads(b0, h0, kt0 * BW_BK, 0, true);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -292,7 +301,13 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int G
   constexpr uint32_t LBO_ROWS = (128 / 8) * 128;               // 2048: next 8-k group of a 128-row K-major tile
 
   int it = 0;
-  for (int64_t b = b_begin; b < b_end; ++b) {
+  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+    int64_t b;
+    int h, kt;
+    decode(u, b, h, kt);
+    const int k0 = kt * BW_BK;
+    const int kj = k0 + kr;
+    const bool kvalid = kj < L;
     float acc[CP];  // dV (warpgroup 0) or dK (warpgroup 1) of this key row, summed over query tiles
 #pragma unroll
     for (int d = 0; d < CP; ++d) acc[d] = 0.f;
@@ -437,7 +452,14 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int G
       tc_fence_after();
       // the tiles are free: prefetch the next (batch, query tile) while draining TMEM
       const bool last_q = qt + 1 == nqt;
-      if (!(last_q && b + 1 == b_end)) issue_loads(last_q ? b + 1 : b, last_q ? 0 : qt + 1, last_q);
+      if (!last_q) {
+        issue_loads(b, h, k0, qt + 1, false);
+      } else if (u + gridDim.x < units) {
+        int64_t nb;
+        int nh, nkt_;
+        decode(u + gridDim.x, nb, nh, nkt_);
+        issue_loads(nb, nh, nkt_ * BW_BK, 0, true);
+      }
       if constexpr (db_store) {
         // dS^T tile (unscaled bf16, canonical K-major [key][query]) -> workspace [b][h][key][query]:
         // lane = (query group % 4, key % 8) so each smem phase reads 128 contiguous bytes and
@@ -490,7 +512,7 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int G
                 if (wg * (CP / 2) + e < c) dst[e] = f2bf(P.scale * w[e]);
             }
           } else if (dq_partial) {
-            float* dst = P.dQacc + (((int64_t)blockIdx.x * Btot + b) * L + qq) * HC + (int64_t)h * c + wg * (CP / 2);
+            float* dst = P.dQacc + (((int64_t)kt * Btot + b) * L + qq) * HC + (int64_t)h * c + wg * (CP / 2);
             if (wg * (CP / 2) + CP / 2 <= c) {
 #pragma unroll
               for (int e = 0; e < CP / 2; e += 4)
@@ -531,13 +553,14 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int G
       }
     }
   }
-  (void)nkt;
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc(tmem, 256);
 }
 
-__global__ void __launch_bounds__(256) attn_bwd_dq_finish(AttnBwdParams P, int64_t B, int nparts) {
+// dq = bf16(sum of the NP per-key-tile fp32 partials); all 2*NP loads of a thread in flight
+template <int NP>
+__global__ void __launch_bounds__(256) attn_bwd_dq_finish(AttnBwdParams P, int64_t B) {
   const int L = P.f.L, H = P.f.H, c = P.f.c;
   const int64_t n = B * L * (int64_t)H * c;
   const int64_t n8 = n / 8;
@@ -545,17 +568,20 @@ __global__ void __launch_bounds__(256) attn_bwd_dq_finish(AttnBwdParams P, int64
     const int64_t e = i * 8;
     const int64_t row = e / (H * c), col = e % (H * c);
     const int64_t b = row / L, l = row % L;
-    float4 a = *reinterpret_cast<const float4*>(P.dQacc + e);
-    float4 bq = *reinterpret_cast<const float4*>(P.dQacc + e + 4);
-    for (int p = 1; p < nparts; ++p) {
-      const float4 a2 = *reinterpret_cast<const float4*>(P.dQacc + p * n + e);
-      const float4 b2 = *reinterpret_cast<const float4*>(P.dQacc + p * n + e + 4);
-      a.x += a2.x; a.y += a2.y; a.z += a2.z; a.w += a2.w;
-      bq.x += b2.x; bq.y += b2.y; bq.z += b2.z; bq.w += b2.w;
+    float4 a[NP], q[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      a[p] = __ldcs(reinterpret_cast<const float4*>(P.dQacc + p * n + e));
+      q[p] = __ldcs(reinterpret_cast<const float4*>(P.dQacc + p * n + e + 4));
+    }
+#pragma unroll
+    for (int p = 1; p < NP; ++p) {
+      a[0].x += a[p].x; a[0].y += a[p].y; a[0].z += a[p].z; a[0].w += a[p].w;
+      q[0].x += q[p].x; q[0].y += q[p].y; q[0].z += q[p].z; q[0].w += q[p].w;
     }
     uint4 w;
-    w.x = pack_bf16x2(a.x, a.y); w.y = pack_bf16x2(a.z, a.w);
-    w.z = pack_bf16x2(bq.x, bq.y); w.w = pack_bf16x2(bq.z, bq.w);
+    w.x = pack_bf16x2(a[0].x, a[0].y); w.y = pack_bf16x2(a[0].z, a[0].w);
+    w.z = pack_bf16x2(q[0].x, q[0].y); w.w = pack_bf16x2(q[0].z, q[0].w);
     *reinterpret_cast<uint4*>(P.dq + b * P.dq_sb + l * P.dq_sl + col) = w;
   }
 }
@@ -594,13 +620,10 @@ static int launch_bwd_m(AttnBwdParams& p, int64_t B, int dq_partial, cudaStream_
   }
   const int64_t nkt = (p.f.L + BW_BK - 1) / BW_BK;
   const int64_t units = B * p.f.H * nkt;
-  // one batch per CTA: the hardware block scheduler then balances the (batch, head, key
-  // tile) units over the 2-CTA/SM slots with at most one partial tail (grouping batches per
-  // CTA left a 1/3-full third wave at the training shape)
-  const int64_t G = 1;
-  (void)units;
-  dim3 grid((unsigned)nkt, (unsigned)p.f.H, (unsigned)((B + G - 1) / G));
-  attn_bwd_kernel<CP, MODE><<<grid, 256, SM::TOTAL, st>>>(p, (int)G, dq_partial);
+  // persistent: 2 CTAs per SM, units handed out round-robin
+  const int64_t slots = (int64_t)sm_count() * 2;
+  dim3 grid((unsigned)(units < slots ? units : slots));
+  attn_bwd_kernel<CP, MODE><<<grid, 256, SM::TOTAL, st>>>(p, (int)nkt, dq_partial);
   EVO_LAUNCH_CHECK("attention bwd main");
   return EVO_OK;
 }
@@ -690,15 +713,22 @@ extern "C" int evo_gated_attention_bwd(const EvoAttnBwdDesc* d, void* stream) {
   if (rc) return rc;
   if (p.dS) {
     int64_t nv = (int64_t)H * L * L / 8;
-    int64_t g2 = (nv + 255) / 256, cap2 = (int64_t)sm_count() * 8;
+    // 128-thread CTAs: H*L*L/8 threads spread evenly over the SMs (each keeps 8 loads in flight)
+    int64_t g2 = (nv + 127) / 128, cap2 = (int64_t)sm_count() * 16;
     unsigned g2u = (unsigned)(g2 < cap2 ? g2 : cap2);
-    attn_dbias_reduce<<<g2u, 256, 0, st>>>(p.dS, p.dbias, B, H, L, p.db1, p.db2, p.db3, p.scale);
+    attn_dbias_reduce<<<g2u, 128, 0, st>>>(p.dS, p.dbias, B, H, L, p.db1, p.db2, p.db3, p.scale);
     EVO_LAUNCH_CHECK("attention bwd dbias reduce");
   }
   if (dq_partial == 2) return EVO_OK;
   int64_t n8 = B * L * H * c / 8;
   int64_t g = (n8 + 255) / 256, cap = (int64_t)sm_count() * 16;
-  attn_bwd_dq_finish<<<(unsigned)(g < cap ? g : cap), 256, 0, st>>>(p, B, dq_partial ? (int)nkt : 1);
+  const unsigned gf = (unsigned)(g < cap ? g : cap);
+  switch (dq_partial ? (int)nkt : 1) {
+    case 1: attn_bwd_dq_finish<1><<<gf, 256, 0, st>>>(p, B); break;
+    case 2: attn_bwd_dq_finish<2><<<gf, 256, 0, st>>>(p, B); break;
+    case 3: attn_bwd_dq_finish<3><<<gf, 256, 0, st>>>(p, B); break;
+    default: attn_bwd_dq_finish<4><<<gf, 256, 0, st>>>(p, B); break;
+  }
   EVO_LAUNCH_CHECK("attention bwd finish");
   return EVO_OK;
 }
