@@ -1,0 +1,159 @@
+"""Command-line front-end of the GPU path (the hot-path subset of the reference CLI,
+cli.py:1-312).
+
+  simulate    run one Evoformer block sharded over N DAP ranks on the GPU - one process per
+              GPU under torchrun (NCCL), otherwise the ranks run as threads on the current GPU
+              - compare it with the single-device GPU block, and check the MEASURED collective
+              ledger (bytes handed to NCCL, reference convention) against
+              predict_block_ledger (cli.py:119-138, commcost.py:126-158)
+  commvolume  closed-form tensor- vs axial-parallel volumes (cli.py:112-116)
+
+Same envelope as the reference: one JSON document {"schema": "evoplan-cli-v1", "command",
+"result"[, "timestamp"]}, sorted keys, --no-timestamp for byte-identical reruns; same exit
+codes (0 ok, 2 bad arguments, 3 constraint violated).  The numeric check differs by
+construction: the GPU block computes in bf16 with fp32 accumulation, so simulate compares
+DAP with the single-device GPU block (same kernels, different reduction order) against a
+relative tolerance instead of the reference's 1e-9 float64 bound.
+
+    python -m paper_2203_00854_b200.cli --no-timestamp simulate --devices 4 --n-seq 8 --n-res 16
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+from dataclasses import asdict
+from datetime import datetime, timezone
+
+EXIT_OK, EXIT_USAGE, EXIT_CONSTRAINT = 0, 2, 3
+DAP_REL_TOL = 5e-3  # DAP vs single device on the GPU
+
+
+def _emit(args, command: str, result: dict) -> None:
+    doc = {"schema": "evoplan-cli-v1", "command": command, "result": result}
+    if not args.no_timestamp:
+        doc["timestamp"] = datetime.now(timezone.utc).isoformat()
+    text = json.dumps(doc, sort_keys=True, indent=2)
+    if getattr(args, "out", None):
+        with open(args.out, "w") as fh:
+            fh.write(text + "\n")
+    else:
+        print(text)
+
+
+def _config(args):
+    from .config import EvoConfig
+    return EvoConfig(n_seq=args.n_seq, n_res=args.n_res, h_msa=args.h_msa, h_pair=args.h_pair,
+                     n_head_msa=args.heads_msa, n_head_pair=args.heads_pair, hidden_proj=args.hidden_proj)
+
+
+def cmd_commvolume(args) -> int:
+    from .commcost import CommModel
+    _emit(args, "commvolume", CommModel(n_heads=args.heads).compare(args.k, args.devices).as_dict())
+    return EXIT_OK
+
+
+def cmd_simulate(args) -> int:
+    import numpy as np
+    import torch
+
+    from .config import init_block_params
+    from .dap import CommLedger, DeviceMesh, dap_evoformer_block, predict_block_ledger
+    from .errors import ShardError
+    from .evoformer import evoformer_block
+
+    cfg = _config(args)
+    if cfg.n_seq % args.devices or cfg.n_res % args.devices:
+        raise ShardError(f"n_seq={cfg.n_seq} / n_res={cfg.n_res} not divisible by {args.devices} devices")
+    params = init_block_params(cfg, args.seed)
+    rng = np.random.default_rng(args.seed)  # the reference's draw order (cli.py:112-114)
+    m = rng.normal(size=(cfg.n_seq, cfg.n_res, cfg.h_msa))
+    z = rng.normal(size=(cfg.n_res, cfg.n_res, cfg.h_pair))
+    order = tuple(int(x) for x in args.device_order.split(",")) if args.device_order else ()
+    mesh = DeviceMesh(args.devices, order)
+    ledger = CommLedger(args.devices, element_size=args.element_size)
+    m_ref, z_ref = evoformer_block(m, z, params, cfg)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record()
+    m_dap, z_dap = dap_evoformer_block(m, z, params, cfg, mesh, ledger)
+    ev[1].record()
+    torch.cuda.synchronize()
+    err = max(float(np.max(np.abs(m_dap - m_ref))), float(np.max(np.abs(z_dap - z_ref))))
+    rel = max(float(np.linalg.norm(m_dap - m_ref) / np.linalg.norm(m_ref)),
+              float(np.linalg.norm(z_dap - z_ref) / np.linalg.norm(z_ref)))
+    predicted = predict_block_ledger(cfg, args.devices, args.element_size)
+    measured = {cat: {"count": ledger.counts[cat], "bytes": sum(ledger.bytes[cat])} for cat in sorted(ledger.counts)}
+    import torch.distributed as dist
+    distributed = dist.is_available() and dist.is_initialized() and dist.get_world_size() == args.devices
+    if not distributed or dist.get_rank() == 0:
+        _emit(args, "simulate", {
+            "config": asdict(cfg),
+            "n_devices": args.devices,
+            "device_order": list(mesh.device_order),
+            "max_abs_error": err,
+            "rel_error": rel,
+            "rel_tolerance": DAP_REL_TOL,
+            "ledger": measured,
+            "predicted": predicted,
+            "ledger_matches_prediction": measured == predicted,
+            "ranks": "processes (torch.distributed)" if distributed else "threads on one GPU",
+            "dap_block_ms": round(ev[0].elapsed_time(ev[1]), 3),
+        })
+    return EXIT_OK if rel <= DAP_REL_TOL and measured == predicted else EXIT_CONSTRAINT
+
+
+def _add_config_args(p: argparse.ArgumentParser) -> None:
+    # the reference's flags (cli.py:56-63) with GPU-sized defaults: the kernels need head dims
+    # and projection widths that are multiples of 8 (also per DAP shard: n_res/N >= 8) and a
+    # pair width of 32/64/128 (fused LN + bias-dot kernel)
+    p.add_argument("--n-seq", type=int, default=16)
+    p.add_argument("--n-res", type=int, default=32)
+    p.add_argument("--h-msa", type=int, default=32)
+    p.add_argument("--h-pair", type=int, default=32)
+    p.add_argument("--heads-msa", type=int, default=2)
+    p.add_argument("--heads-pair", type=int, default=2)
+    p.add_argument("--hidden-proj", type=int, default=16)
+    p.add_argument("--seed", type=int, default=0)
+
+
+def build_parser() -> argparse.ArgumentParser:
+    parser = argparse.ArgumentParser(prog="evo-b200", description="GPU Evoformer block: DAP simulation and "
+                                     "communication-volume reports (reference CLI subset)")
+    parser.add_argument("--no-timestamp", action="store_true", help="omit the timestamp for reproducible output")
+    sub = parser.add_subparsers(dest="command", required=True)
+    p = sub.add_parser("commvolume", help="closed-form volume comparison")
+    p.add_argument("--k", type=float, default=1.0)
+    p.add_argument("--devices", type=int, required=True)
+    p.add_argument("--heads", type=int, default=4)
+    p.add_argument("--out")
+    p.set_defaults(fn=cmd_commvolume)
+    p = sub.add_parser("simulate", help="run the DAP-sharded block on the GPU")
+    _add_config_args(p)
+    p.add_argument("--devices", type=int, required=True)
+    p.add_argument("--device-order", default="")
+    p.add_argument("--element-size", type=int, default=2)
+    p.add_argument("--out")
+    p.set_defaults(fn=cmd_simulate)
+    return parser
+
+
+def main(argv: list[str] | None = None) -> int:
+    from .errors import EvoplanError, HeadLimitError
+    parser = build_parser()
+    try:
+        args = parser.parse_args(argv)
+    except SystemExit as exc:
+        return EXIT_USAGE if exc.code not in (0, None) else 0
+    try:
+        return args.fn(args)
+    except HeadLimitError as exc:
+        print(json.dumps({"error": str(exc)}, sort_keys=True), file=sys.stderr)
+        return EXIT_CONSTRAINT
+    except (EvoplanError, FileNotFoundError) as exc:
+        print(json.dumps({"error": str(exc)}, sort_keys=True), file=sys.stderr)
+        return EXIT_USAGE
+
+
+if __name__ == "__main__":
+    sys.exit(main())

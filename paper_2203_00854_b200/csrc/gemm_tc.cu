@@ -365,8 +365,11 @@ struct TileLoader {
   }
 };
 
+constexpr int WS_EPI_WARPS = 8;                       // two epilogue warps per TMEM lane quarter
+constexpr int WS_GEMM_THREADS = 160 + 32 * WS_EPI_WARPS;  // 4 producer warps + MMA warp + epilogue
+
 template <int BN, bool A_MN, bool B_MN, int STAGES, typename TC>
-__global__ void __launch_bounds__(288, 1) bgemm_ws_kernel(MatArg A, MatArg B, MatArg C, uint32_t M, uint32_t N,
+__global__ void __launch_bounds__(WS_GEMM_THREADS, 1) bgemm_ws_kernel(MatArg A, MatArg B, MatArg C, uint32_t M, uint32_t N,
                                                           uint32_t K, float alpha, float beta, int c_mode, int splits,
                                                           float* __restrict__ ws, int batch) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -406,7 +409,7 @@ __global__ void __launch_bounds__(288, 1) bgemm_ws_kernel(MatArg A, MatArg B, Ma
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 128);
+      mbar_init(&tempty[i], 32 * WS_EPI_WARPS);
     }
     fence_mbar_init();
   }
@@ -476,9 +479,13 @@ __global__ void __launch_bounds__(288, 1) bgemm_ws_kernel(MatArg A, MatArg B, Ma
       }
     }
   } else {
-    // ---------------- epilogue (warps 5..8 -> TMEM lane quarters 1,2,3,0)
+    // ---------------- epilogue (warps 5..12 -> TMEM lane quarters 1,2,3,0,1,2,3,0; the two
+    // warps of a quarter split the tile's columns)
+    constexpr int NE = 32 * WS_EPI_WARPS;
+    constexpr int CH = BN / (WS_EPI_WARPS / 4);  // columns per epilogue warp
     const int q = warp & 3;            // lane quarter of this warp
-    const int et = threadIdx.x - 160;  // 0..127 epilogue thread id
+    const int c_lo = ((warp - 5) / 4) * CH;
+    const int et = threadIdx.x - 160;  // 0..NE-1 epilogue thread id
     int it = 0;
     for (uint32_t t = blockIdx.x; t < total; t += gridDim.x, ++it) {
       uint32_t b, m0, n0;
@@ -493,7 +500,7 @@ __global__ void __launch_bounds__(288, 1) bgemm_ws_kernel(MatArg A, MatArg B, Ma
       const uint32_t tbase = tmem + buf * BN + ((uint32_t)(q * 32) << 16);
       if (c_mode == 1 && ws == nullptr) {
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
+        for (int c0 = c_lo; c0 < c_lo + CH; c0 += 32) {
           float v[32];
           tmem_ld32(tbase + c0, v);
           tmem_ld_wait();
@@ -514,10 +521,10 @@ __global__ void __launch_bounds__(288, 1) bgemm_ws_kernel(MatArg A, MatArg B, Ma
         }
         tc_fence_before();
         mbar_arrive(&tempty[buf]);  // accumulator free for tile t + 2*gridDim.x
-        named_sync(1, 128);
+        named_sync(1, NE);
         constexpr int CPR = BN * (int)sizeof(TC) / 16;
         constexpr int EPC = 16 / (int)sizeof(TC);
-        constexpr int RSTEP = 128 / CPR;
+        constexpr int RSTEP = NE / CPR;
         const int cc = et % CPR;
         const uint32_t gcol = n0 + cc * EPC;
         const bool col_ok = gcol < N;
@@ -537,7 +544,7 @@ __global__ void __launch_bounds__(288, 1) bgemm_ws_kernel(MatArg A, MatArg B, Ma
           }
           *reinterpret_cast<uint4*>(p) = val;
         }
-        named_sync(1, 128);  // staging tile reusable
+        named_sync(1, NE);  // staging tile reusable
       } else {
         int64_t roff = 0;
         if (row_ok) {
@@ -545,7 +552,7 @@ __global__ void __launch_bounds__(288, 1) bgemm_ws_kernel(MatArg A, MatArg B, Ma
           roff = (int64_t)qq * C.hi0 + (int64_t)r * C.lo0;
         }
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
+        for (int c0 = c_lo; c0 < c_lo + CH; c0 += 32) {
           float v[32];
           tmem_ld32(tbase + c0, v);
           tmem_ld_wait();
@@ -666,7 +673,7 @@ static int launch_bgemm_ws(MatArg A, MatArg B, MatArg C, int64_t batch, int64_t 
   }
   const int64_t tiles = ((M + GEMM_BM - 1) / GEMM_BM) * ((N + BN - 1) / BN) * batch * splits;
   const int64_t grid = tiles < sm_count() ? tiles : sm_count();
-  kern<<<(unsigned)grid, 288, smem, st>>>(A, B, C, (uint32_t)M, (uint32_t)N, (uint32_t)K, alpha, beta, c_mode, splits,
+  kern<<<(unsigned)grid, WS_GEMM_THREADS, smem, st>>>(A, B, C, (uint32_t)M, (uint32_t)N, (uint32_t)K, alpha, beta, c_mode, splits,
                                           splits > 1 ? ws : nullptr, (int)batch);
   EVO_LAUNCH_CHECK("bgemm_ws launch");
   if (splits > 1) {

@@ -35,3 +35,13 @@ class KernelError(EvoplanError):
 
 class NativeLibraryMissing(KernelError):
     """libevo.so is not built / not loadable.  There is no CPU fallback."""
+
+
+class HeadLimitError(EvoplanError):
+    """Head-sharded (tensor) parallelism cannot use more devices than attention heads
+    (errors.py:44-53); raised by the closed-form volume model."""
+
+    def __init__(self, n_devices: int, n_heads: int):
+        self.n_devices = n_devices
+        self.n_heads = n_heads
+        super().__init__(f"tensor parallelism over {n_devices} devices exceeds the head-count limit of {n_heads}")
