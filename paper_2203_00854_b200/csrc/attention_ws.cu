@@ -10,7 +10,8 @@
 //     warp  9     loader: cp.async K/V (+ per-key bias) ring of WS_NS stages, completion
 //                 tracked by cp.async.mbarrier.arrive.noinc
 //   K/V tiles (64 keys) are loaded once and shared by both query tiles.  S is double
-//   buffered per warpgroup in TMEM and P double buffered in smem, so the tensor core works
+//   buffered per warpgroup in TMEM and P (bf16) is written back over S in TMEM and read from
+//   there by the PV MMA (A operand in tensor memory), so the tensor core works
 //   on tile j+1 while the warpgroups run the softmax of tile j, and the two warpgroups
 //   interleave on the MUFU/FMA pipes.  O accumulates in TMEM; a row's O is rescaled (TMEM
 //   load-scale-store, warp-uniform) only when its running max grows by more than 2^8, so the
@@ -43,8 +44,7 @@ struct WsSmem {
   static constexpr uint32_t Q = 0;                                  // 2 x [128][CQ] K-major
   static constexpr uint32_t K = Q + 2 * WS_BQ * CQ * 2;             // NS x [64][CQ] K-major
   static constexpr uint32_t V = K + NS * WS_BK * CQ * 2;         // NS x [64 keys][CV] MN-major over d
-  static constexpr uint32_t P = V + NS * WS_BK * CV * 2;         // [2 wg][2 buf] x [128][64] K-major
-  static constexpr uint32_t TOTAL = P + 4 * WS_BQ * WS_BK * 2;
+  static constexpr uint32_t TOTAL = V + NS * WS_BK * CV * 2;  // (P lives in TMEM, over S)
   static constexpr uint32_t Q_BYTES = WS_BQ * CQ * 2, K_BYTES = WS_BK * CQ * 2, V_BYTES = WS_BK * CV * 2;
 };
 
@@ -68,6 +68,31 @@ __device__ __forceinline__ void ws_tmem_st8(uint32_t taddr, const float* v) {
                : "memory");
 }
 
+// D[tmem] (+)= A[tmem] * B[smem]^T: the A operand (M = 128 lanes, K packed 2 bf16 per 32-bit
+// column) is read from tensor memory - P never leaves TMEM
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void ws_tmem_st32(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+
 // O row (NC fp32 columns, row sum included) scaled in place: warp-collective TMEM load/store
 template <int NC>
 __device__ __forceinline__ void ws_scale_o(uint32_t taddr, float f) {
@@ -88,8 +113,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) attn_fwd_ws_kernel(AttnParams P
   using SM = WsSmem<CP>;
   constexpr int CQ = SM::CQ, CV = SM::CV, WS_NS = SM::NS;
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t q_full, kv_full[WS_NS], kv_empty[WS_NS], s_full[2][2], s_free[2][2], p_full[2][2],
-      o_done[2][2];
+  __shared__ uint64_t q_full, kv_full[WS_NS], kv_empty[WS_NS], s_full[2][2], p_full[2][2], o_done[2][2];
   __shared__ uint32_t tmem_sh;
   const uint32_t sb = smem_u32(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -112,7 +136,6 @@ __global__ void __launch_bounds__(WS_THREADS, 1) attn_fwd_ws_kernel(AttnParams P
     for (int w = 0; w < 2; ++w)
       for (int i = 0; i < 2; ++i) {
         mbar_init(&s_full[w][i], 1);
-        mbar_init(&s_free[w][i], WS_BQ);
         mbar_init(&p_full[w][i], WS_BQ);
         mbar_init(&o_done[w][i], 1);
       }
@@ -213,8 +236,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) attn_fwd_ws_kernel(AttnParams P
           const int s = j % WS_NS, buf = j & 1;
           mbar_wait(&kv_full[s], (j / WS_NS) & 1);
           fence_async_smem();
-          // S[w][buf] last held tile j-2: its s_free completion is #((j-2)/2)
-          if (j >= 2) mbar_wait(&s_free[w][buf], ((j - 2) >> 1) & 1);
+          // S[w][buf] last held P_{j-2} (written over S_{j-2}), read by PV_{j-2}: completion
+          // #((j-2)/2) of o_done[w][buf]; the softmax read of S_{j-2} preceded its p_full
+          if (j >= 2) mbar_wait(&o_done[w][buf], ((j - 2) >> 1) & 1);
           tc_fence_after();
           for (int kk = 0; kk < ksteps; ++kk) {
             const uint64_t ad = make_sdesc(sb + SM::Q + w * SM::Q_BYTES + kk * 2 * (WS_BQ / 8) * 128,
@@ -230,11 +254,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1) attn_fwd_ws_kernel(AttnParams P
           mbar_wait(&p_full[w][buf], (jj >> 1) & 1);
           tc_fence_after();
 #pragma unroll
-          for (int kk = 0; kk < WS_BK / 16; ++kk) {
-            const uint64_t ad = make_sdesc(sb + SM::P + (2 * w + buf) * WS_BQ * WS_BK * 2 + kk * 2 * (WS_BQ / 8) * 128,
-                                           (WS_BQ / 8) * 128, 128);
+          for (int kk = 0; kk < WS_BK / 16; ++kk) {  // A = P_jj in TMEM: 16 keys per 8 columns
             const uint64_t bd = make_sdesc(sb + SM::V + s * SM::V_BYTES + kk * 2 * (CV / 8) * 128, (CV / 8) * 128, 128);
-            mma_bf16(tmem + 256 + w * 128, ad, bd, IDESC_O, (jj > 0 || kk > 0) ? 1u : 0u);
+            mma_bf16_ts(tmem + 256 + w * 128, tmem + (2 * w + buf) * WS_BK + kk * 8, bd, IDESC_O,
+                        (jj > 0 || kk > 0) ? 1u : 0u);
           }
           mma_commit(&o_done[w][buf]);
           mma_commit(&kv_empty[s]);  // this warpgroup is done with K_jj (S_jj) and V_jj
@@ -278,8 +301,6 @@ __global__ void __launch_bounds__(WS_THREADS, 1) attn_fwd_ws_kernel(AttnParams P
       tmem_ld32(t_lane + (2 * w + buf) * WS_BK, sv);
       tmem_ld32(t_lane + (2 * w + buf) * WS_BK + 32, sv + 32);
       tmem_ld_wait();
-      tc_fence_before();
-      ws_arrive(&s_free[w][buf]);
 
       if (brow) {
 #pragma unroll
@@ -318,20 +339,16 @@ __global__ void __launch_bounds__(WS_THREADS, 1) attn_fwd_ws_kernel(AttnParams P
         m_run = m_new;
       }
       const float mref = m_run == -INFINITY ? 0.f : m_run;
-      // P buffer `buf` was last read by PV_{j-2}: completion #((j-2)/2) of o_done[w][buf]
-      if (j >= 2) mbar_wait(&o_done[w][buf], ((j - 2) >> 1) & 1);
-      const uint32_t prow = sb + SM::P + (2 * w + buf) * WS_BQ * WS_BK * 2;
+      // P_j (bf16, 2 keys per 32-bit column) overwrites S_j in TMEM columns [0, 32) of the
+      // buffer: this thread's row was read above, and S_{j+2} will not be issued into the
+      // buffer before PV_j (which reads P_j) completes
+      uint32_t pk[WS_BK / 2];
 #pragma unroll
-      for (int kk = 0; kk < WS_BK; kk += 8) {
-        float pv[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          pv[e] = ex2f(fmaf(sv[kk + e], sl2, -mref));
-        }
-        st_shared_v4(prow + kmajor_off(r, kk, WS_BQ), pack_bf16x2(pv[0], pv[1]), pack_bf16x2(pv[2], pv[3]),
-                     pack_bf16x2(pv[4], pv[5]), pack_bf16x2(pv[6], pv[7]));
-      }
-      fence_async_smem();
+      for (int kk = 0; kk < WS_BK; kk += 2)
+        pk[kk / 2] = pack_bf16x2(ex2f(fmaf(sv[kk], sl2, -mref)), ex2f(fmaf(sv[kk + 1], sl2, -mref)));
+      ws_tmem_st32(t_lane + (2 * w + buf) * WS_BK, pk);
+      tmem_st_wait();
+      tc_fence_before();
       ws_arrive(&p_full[w][buf]);
     }
     // epilogue: the last PV (j = nkt-1) is completion #((nkt-1)/2) of o_done[w][(nkt-1)&1]
