@@ -118,9 +118,10 @@ typedef struct EvoAttnDesc {
   float scale;
 } EvoAttnDesc;
 int evo_gated_attention_fwd(const EvoAttnDesc* d, void* stream);
-/* Sequences with L >= len use the warp-specialised long-sequence forward (1 CTA/SM:
- * loader warp, MMA warp, two softmax warpgroups; default len 512).  Returns the previous
- * threshold; len <= 0 only queries it.  Both kernels compute the same function. */
+/* Sequences with L >= len and a per-key (or no) bias use the warp-specialised forward
+ * (attention_ws.cu: 1 CTA/SM, loader warp, per-warpgroup MMA warps, two softmax
+ * warpgroups); default len 4096.  Returns the previous threshold; len <= 0 only queries
+ * it; len == 1 forces it for every input (tests).  Both kernels compute the same function. */
 int evo_attention_fwd_ws_min_len(int len);
 
 /* Backward of the same op (flash-style: P is recomputed from q, k, bias and lse).

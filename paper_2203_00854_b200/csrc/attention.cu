@@ -3,13 +3,16 @@
 //
 // One CTA (4 warps, 128 threads) owns 128 queries of one (batch, head) and streams
 // the keys in tiles of 64 (flash-style online softmax, so N_r = 4096 never
-// materialises a logit matrix).  <= 128 registers, 64 TMEM columns and ~41 KB of
+// materialises a logit matrix).  <= 128 registers, 128 TMEM columns and ~34 KB of
 // shared memory per CTA -> 4 CTAs (16 warps) per SM hide each other's latency:
-//   S   = Q K^T                 tcgen05.mma M=128 N=64 K=16..64   -> TMEM (fp32)
-//   s   = (S + bias) * scale    thread r owns query row r (tcgen05.ld 32x32b),
-//   p   = exp2(s - m)           running max / sum in registers (no shuffles)
-//   P  -> smem (bf16, canonical K-major, conflict-free 16-byte stores)
-//   O  += P V                   tcgen05.mma M=128 N=c K=64 -> TMEM -> registers
+//   S   = [Q | 1] [K | b]^T       tcgen05.mma M=128 N=64 -> TMEM cols [0,64) (fp32); a per-key
+//                                 bias b (pair_row / pair_col) rides in an extra K group
+//   s   = S * scale (+ full bias)  thread r owns query row r (tcgen05.ld 32x32b), running
+//   p   = exp2(s - m)              max in registers (no shuffles)
+//   P  -> TMEM cols [0,32) as bf16 pairs over S (tcgen05.st) - never touches smem
+//   O_t = P [V | 1]                tcgen05.mma with the A operand in TMEM, N = CP + 8 ->
+//                                 TMEM cols [64, 64+CP+8): column CP is the row sum of P
+//   O  += O_t, l += O_t[CP]        in registers, rescaled by the running-max correction
 // Epilogue: o = O / l, out = sigmoid(g) * o (gate on raw x, G2), log-sum-exp saved.
 // K/V tiles are double-buffered with cp.async; several CTAs per SM overlap the
 // MMA of one CTA with the softmax of another.
@@ -24,12 +27,13 @@ constexpr float LOG2E = 1.4426950408889634f;
 
 template <int CP>
 struct AttnSmem {
+  static constexpr int CQ = CP + 16;  // Q / K K-extent: data + [1 | per-key bias] group + zero group
+  static constexpr int CV = CP + 8;   // V N-extent: data + [1, 0 x 7] (row sums of P)
   static constexpr uint32_t Q = 0;
-  static constexpr uint32_t KT = Q + ATT_BQ * CP * 2;          // 2 stages
-  static constexpr uint32_t VT = KT + 2 * ATT_BK * CP * 2;     // 2 stages
-  static constexpr uint32_t P = VT + 2 * ATT_BK * CP * 2;
-  static constexpr uint32_t BIAS = P + ATT_BQ * ATT_BK * 2;    // 2 x 128 fp32 (per-key bias)
-  static constexpr uint32_t TOTAL = BIAS + 2 * ATT_BK * 4;
+  static constexpr uint32_t KT = Q + ATT_BQ * CQ * 2;          // 2 stages
+  static constexpr uint32_t VT = KT + 2 * ATT_BK * CQ * 2;     // 2 stages
+  static constexpr uint32_t TOTAL = VT + 2 * ATT_BK * CV * 2;
+  static constexpr uint32_t K_BYTES = ATT_BK * CQ * 2, V_BYTES = ATT_BK * CV * 2;
 };
 
 // ROWS x CP K-major tile from a strided [row][col] source (cols contiguous)
@@ -46,8 +50,8 @@ __device__ __forceinline__ void att_load_kmajor(uint32_t sdst, const bf16* base,
     cp_async16(sdst + kmajor_off(r, d, ROWS), src, ok);
   }
 }
-// keys x CP tile stored MN-major over d (the PV B operand: N = d, K = key)
-template <int CP>
+// keys x CP tile stored MN-major over d (the PV B operand: N = d, K = key; N extent NV)
+template <int CP, int NV>
 __device__ __forceinline__ void att_load_v(uint32_t sdst, const bf16* base, int64_t row_stride, int row0,
                                            int nrows_valid, int c) {
   constexpr int CPR = CP / 8;
@@ -57,18 +61,53 @@ __device__ __forceinline__ void att_load_v(uint32_t sdst, const bf16* base, int6
     const int r = ch / CPR, d = (ch % CPR) * 8;
     const bool ok = (r < nrows_valid) && (d < c);
     const bf16* src = ok ? base + (int64_t)(row0 + r) * row_stride + d : base;
-    cp_async16(sdst + mnmajor_off(d, r, CP), src, ok);
+    cp_async16(sdst + mnmajor_off(d, r, NV), src, ok);
   }
+}
+__device__ __forceinline__ void att_tmem_st32(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void att_tmem_ld8(uint32_t taddr, float* v) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void att_tmem_st8(uint32_t taddr, const float* v) {
+  const uint32_t* r = reinterpret_cast<const uint32_t*>(v);
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+// O (+)= P[tmem] * V[smem]^T: A operand (M = 128 lanes, 2 bf16 per 32-bit column) in TMEM
+__device__ __forceinline__ void att_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
 }
 
 template <int CP>
-__global__ void __launch_bounds__(128, CP == 32 ? 4 : 3) attn_fwd_kernel(AttnParams P) {
+__global__ void __launch_bounds__(128, CP == 64 ? 2 : 4) attn_fwd_kernel(AttnParams P) {
   using SM = AttnSmem<CP>;
+  constexpr int CQ = SM::CQ, CV = SM::CV;
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar_s, bar_o;
   __shared__ uint32_t tmem_sh;
   const uint32_t sb = smem_u32(smem);
-  float* sbias = reinterpret_cast<float*>(smem + SM::BIAS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q0 = blockIdx.x * ATT_BQ;
@@ -78,8 +117,10 @@ __global__ void __launch_bounds__(128, CP == 32 ? 4 : 3) attn_fwd_kernel(AttnPar
   const int r = warp * 32 + lane;  // query row inside the tile
   const int qi = q0 + r;
   const bool per_key_bias = P.bias && P.bs2 == 0;
+  constexpr uint32_t ONE_BF16 = 0x3F80u;
 
-  if (warp == 0) tmem_alloc(&tmem_sh, ATT_BK);
+  constexpr uint32_t TCOLS = 64 + CV <= 128 ? 128 : 256;
+  if (warp == 0) tmem_alloc(&tmem_sh, TCOLS);
   if (threadIdx.x == 0) {
     mbar_init(&bar_s, 1);
     mbar_init(&bar_o, 1);
@@ -89,10 +130,24 @@ __global__ void __launch_bounds__(128, CP == 32 ? 4 : 3) attn_fwd_kernel(AttnPar
   const bf16* qb = P.q + b * P.q_sb + (int64_t)h * c;
   const bf16* kb = P.k + b * P.k_sb + (int64_t)h * c;
   const bf16* vb = P.v + b * P.v_sb + (int64_t)h * c;
+  const unsigned short* kbias =
+      per_key_bias ? reinterpret_cast<const unsigned short*>(P.bias + b * P.bs0 + (int64_t)h * P.bs1) : nullptr;
   att_load_kmajor<CP, ATT_BQ>(sb + SM::Q, qb, P.q_sl, q0, L - q0, c);
   att_load_kmajor<CP, ATT_BK>(sb + SM::KT, kb, P.k_sl, 0, L, c);
-  att_load_v<CP>(sb + SM::VT, vb, P.v_sl, 0, L, c);
+  att_load_v<CP, CV>(sb + SM::VT, vb, P.v_sl, 0, L, c);
   cp_async_commit();
+  // constant parts of the augmented operands: Q row [.. | 1 or 0, 0 x 7 | 0 x 8], K rows'
+  // zero group (the bias group is written per tile), V rows' [1, 0 x 7] row-sum column
+  st_shared_v4(sb + SM::Q + kmajor_off(r, CP, ATT_BQ), per_key_bias ? ONE_BF16 : 0u, 0u, 0u, 0u);
+  st_shared_v4(sb + SM::Q + kmajor_off(r, CP + 8, ATT_BQ), 0u, 0u, 0u, 0u);
+  {
+    const int st = r / ATT_BK, kr = r % ATT_BK;  // 128 threads = 2 stages x 64 keys
+    st_shared_v4(sb + SM::KT + st * SM::K_BYTES + kmajor_off(kr, CP + 8, ATT_BK), 0u, 0u, 0u, 0u);
+    st_shared_v4(sb + SM::VT + st * SM::V_BYTES + mnmajor_off(CP, kr, CV), ONE_BF16, 0u, 0u, 0u);
+    if (st == 0)
+      st_shared_v4(sb + SM::KT + kmajor_off(kr, CP, ATT_BK),
+                   (per_key_bias && kr < L) ? (uint32_t)kbias[(int64_t)kr * P.bs3] : 0u, 0u, 0u, 0u);
+  }
 
   tc_fence_before();
   __syncthreads();
@@ -101,47 +156,47 @@ __global__ void __launch_bounds__(128, CP == 32 ? 4 : 3) attn_fwd_kernel(AttnPar
   const uint32_t t_row = tmem + ((uint32_t)(warp * 32) << 16);
 
   constexpr uint32_t IDESC_S = make_idesc_bf16(128, ATT_BK, 0, 0);
-  constexpr uint32_t IDESC_O = make_idesc_bf16(128, CP, 0, 1);
+  constexpr uint32_t IDESC_O = make_idesc_bf16(128, CV, 0, 1);
+  constexpr uint32_t T_O = 64;  // O and its row sum (column CP) accumulate in TMEM [64, 64 + CV)
+  const int ksteps = per_key_bias ? CQ / 16 : CP / 16;
 
-  float m_run = -INFINITY, l_run = 0.f;
-  float o_acc[CP];
-#pragma unroll
-  for (int d = 0; d < CP; ++d) o_acc[d] = 0.f;
+  float m_run = -INFINITY;  // running max, scaled log2 units
 
   const int nkt = (L + ATT_BK - 1) / ATT_BK;
   const bf16* brow = nullptr;
   if (P.bias && !per_key_bias && qi < L) brow = P.bias + b * P.bs0 + (int64_t)h * P.bs1 + (int64_t)qi * P.bs2;
+  uint32_t nb = 0;  // next tile's per-key bias (threads 0..63), stored with its K tile
 
   for (int j = 0; j < nkt; ++j) {
     const int k0 = j * ATT_BK;
     const int st = j & 1;
-    if (per_key_bias) {
-      const bf16* bp = P.bias + b * P.bs0 + (int64_t)h * P.bs1;
-      const int kk = threadIdx.x;
-      if (kk < ATT_BK) sbias[st * ATT_BK + kk] = (k0 + kk < L) ? bf2f(bp[(int64_t)(k0 + kk) * P.bs3]) : 0.f;
-    }
     cp_async_wait<0>();
     fence_async_smem();
     __syncthreads();
     // prefetch the next K/V tile into the other stage (its MMAs finished last iteration)
     if (j + 1 < nkt) {
-      att_load_kmajor<CP, ATT_BK>(sb + SM::KT + (st ^ 1) * ATT_BK * CP * 2, kb, P.k_sl, k0 + ATT_BK,
-                                  L - k0 - ATT_BK, c);
-      att_load_v<CP>(sb + SM::VT + (st ^ 1) * ATT_BK * CP * 2, vb, P.v_sl, k0 + ATT_BK, L - k0 - ATT_BK, c);
+      att_load_kmajor<CP, ATT_BK>(sb + SM::KT + (st ^ 1) * SM::K_BYTES, kb, P.k_sl, k0 + ATT_BK, L - k0 - ATT_BK, c);
+      att_load_v<CP, CV>(sb + SM::VT + (st ^ 1) * SM::V_BYTES, vb, P.v_sl, k0 + ATT_BK, L - k0 - ATT_BK, c);
+      if (per_key_bias && threadIdx.x < ATT_BK) {
+        const int k = k0 + ATT_BK + threadIdx.x;
+        nb = k < L ? (uint32_t)kbias[(int64_t)k * P.bs3] : 0u;
+      }
     }
     cp_async_commit();
 
     if (threadIdx.x == 0) {
+      // S_j overwrites the columns P_{j-1} was read from: PV_{j-1} must be complete
+      if (j > 0) mbar_wait(&bar_o, (j - 1) & 1);
       tc_fence_after();
-#pragma unroll
-      for (int kk = 0; kk < CP / 16; ++kk) {
+      for (int kk = 0; kk < ksteps; ++kk) {
         uint64_t ad = make_sdesc(sb + SM::Q + kk * 2 * (128 / 8) * 128, (128 / 8) * 128, 128);
-        uint64_t bd = make_sdesc(sb + SM::KT + st * ATT_BK * CP * 2 + kk * 2 * (ATT_BK / 8) * 128,
-                                 (ATT_BK / 8) * 128, 128);
+        uint64_t bd = make_sdesc(sb + SM::KT + st * SM::K_BYTES + kk * 2 * (ATT_BK / 8) * 128, (ATT_BK / 8) * 128,
+                                 128);
         mma_bf16(tmem, ad, bd, IDESC_S, kk != 0);
       }
       mma_commit(&bar_s);
     }
+    // bar_s completes after S_j, which was issued after PV_{j-1} completed: O is stable here
     mbar_wait(&bar_s, j & 1);
     tc_fence_after();
 
@@ -150,7 +205,7 @@ __global__ void __launch_bounds__(128, CP == 32 ? 4 : 3) attn_fwd_kernel(AttnPar
     for (int cc = 0; cc < ATT_BK; cc += 32) tmem_ld32(t_row + cc, s + cc);
     tmem_ld_wait();
 
-    // bias (before the scale, G1); keys >= L masked on the last tile only
+    // full bias (before the scale, G1); keys >= L masked on the last tile only
     const bool full_tile = k0 + ATT_BK <= L;
     if (brow) {
       if (P.bias_vec && full_tile) {
@@ -168,70 +223,77 @@ __global__ void __launch_bounds__(128, CP == 32 ? 4 : 3) attn_fwd_kernel(AttnPar
         for (int kk = 0; kk < ATT_BK; ++kk)
           if (k0 + kk < L) s[kk] += bf2f(brow[(int64_t)(k0 + kk) * P.bs3]);
       }
-    } else if (per_key_bias) {
-#pragma unroll
-      for (int kk = 0; kk < ATT_BK; kk += 4) {
-        const float4 bv = *reinterpret_cast<const float4*>(sbias + st * ATT_BK + kk);
-        s[kk] += bv.x; s[kk + 1] += bv.y; s[kk + 2] += bv.z; s[kk + 3] += bv.w;
-      }
     }
     if (!full_tile) {
 #pragma unroll
       for (int kk = 0; kk < ATT_BK; ++kk)
         if (k0 + kk >= L) s[kk] = -INFINITY;
     }
-    // running max on the unscaled logits (scale > 0), p = 2^(s*scale*log2e - m*scale*log2e)
-    float mx = m_run;
+    float m8[8];
 #pragma unroll
-    for (int kk = 0; kk < ATT_BK; kk += 2) mx = fmaxf(mx, fmaxf(s[kk], s[kk + 1]));
-    const float corr = ex2f((m_run - mx) * P.scale_log2);  // m_run = -inf on the first tile -> 0
-    const float mxs = mx * P.scale_log2;
-    float lsum = 0.f;
-    const uint32_t prow = sb + SM::P;
+    for (int e = 0; e < 8; ++e) m8[e] = fmaxf(s[e], s[e + 8]);
 #pragma unroll
-    for (int kk = 0; kk < ATT_BK; kk += 8) {
-      float pv[8];
+    for (int kk = 16; kk < ATT_BK; kk += 16) {
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        pv[e] = ex2f(fmaf(s[kk + e], P.scale_log2, -mxs));
-        lsum += pv[e];
-      }
-      st_shared_v4(prow + kmajor_off(r, kk, ATT_BQ), pack_bf16x2(pv[0], pv[1]), pack_bf16x2(pv[2], pv[3]),
-                   pack_bf16x2(pv[4], pv[5]), pack_bf16x2(pv[6], pv[7]));
+      for (int e = 0; e < 8; ++e) m8[e] = fmaxf(m8[e], fmaxf(s[kk + e], s[kk + 8 + e]));
     }
-    l_run = l_run * corr + lsum;
-    m_run = mx;
+    const float mxs = P.scale_log2 * fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                                           fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+    // lazy rescale: O (and l) in TMEM are rescaled only when a row's max grows by > 2^8
+    // (warp-uniform: TMEM loads/stores are warp-collective); P <= 2^8 is exact enough in bf16
+    const bool grow = mxs > m_run + 8.0f;
+    if (__any_sync(0xffffffffu, grow)) {
+      const float m_new = grow ? mxs : m_run;
+      if (j > 0) {
+        const float f = ex2f(m_run - m_new);
 #pragma unroll
-    for (int d = 0; d < CP; ++d) o_acc[d] *= corr;
-
-    fence_async_smem();
+        for (int cc = 0; cc < CV; cc += 8) {
+          float v[8];
+          att_tmem_ld8(t_row + T_O + cc, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] *= f;
+          att_tmem_st8(t_row + T_O + cc, v);
+        }
+      }
+      m_run = m_new;
+    }
+    const float mref = m_run == -INFINITY ? 0.f : m_run;
+    // P over S in TMEM columns [0, 32): this thread's row of S was read above
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {  // 16 packed columns at a time (register budget)
+      uint32_t pk[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int kk = half * 32 + 2 * e;
+        pk[e] = pack_bf16x2(ex2f(fmaf(s[kk], P.scale_log2, -mref)), ex2f(fmaf(s[kk + 1], P.scale_log2, -mref)));
+      }
+      tmem_st16(t_row + half * 16, reinterpret_cast<const float*>(pk));
+    }
+    // the next tile's per-key bias into its K tile's bias group (stage st^1, loaded above)
+    if (per_key_bias && threadIdx.x < ATT_BK && j + 1 < nkt)
+      st_shared_v4(sb + SM::KT + (st ^ 1) * SM::K_BYTES + kmajor_off(threadIdx.x, CP, ATT_BK), nb, 0u, 0u, 0u);
+    tmem_st_wait();
     tc_fence_before();
     __syncthreads();
     if (threadIdx.x == 0) {
       tc_fence_after();
 #pragma unroll
       for (int kk = 0; kk < ATT_BK / 16; ++kk) {
-        uint64_t ad = make_sdesc(sb + SM::P + kk * 2 * (128 / 8) * 128, (128 / 8) * 128, 128);
-        uint64_t bd = make_sdesc(sb + SM::VT + st * ATT_BK * CP * 2 + kk * 2 * (CP / 8) * 128, (CP / 8) * 128, 128);
-        mma_bf16(tmem, ad, bd, IDESC_O, kk != 0);
+        uint64_t bd = make_sdesc(sb + SM::VT + st * SM::V_BYTES + kk * 2 * (CV / 8) * 128, (CV / 8) * 128, 128);
+        att_mma_ts(tmem + T_O, tmem + kk * 8, bd, IDESC_O, (j > 0 || kk > 0) ? 1u : 0u);
       }
       mma_commit(&bar_o);
     }
-    mbar_wait(&bar_o, j & 1);
-    tc_fence_after();
-    float ov[CP];
-    if constexpr (CP == 16) {
-      tmem_ld16(t_row, ov);
-    } else {
-#pragma unroll
-      for (int cc = 0; cc < CP; cc += 32) tmem_ld32(t_row + cc, ov + cc);
-    }
-    tmem_ld_wait();
-#pragma unroll
-    for (int d = 0; d < CP; ++d) o_acc[d] += ov[d];
-    tc_fence_before();
-    __syncthreads();  // all TMEM reads done before the next S MMA overwrites the columns
   }
+  // O and l of this row
+  mbar_wait(&bar_o, (nkt - 1) & 1);
+  tc_fence_after();
+  float o_acc[CV];
+#pragma unroll
+  for (int cc = 0; cc < CV; cc += 8) att_tmem_ld8(t_row + T_O + cc, o_acc + cc);
+  tmem_ld_wait();
+  const float l_run = o_acc[CP];
 
   if (qi < L) {
     const float inv = rcpf(l_run);
@@ -261,12 +323,12 @@ __global__ void __launch_bounds__(128, CP == 32 ? 4 : 3) attn_fwd_kernel(AttnPar
         *reinterpret_cast<uint4*>(og + d) = w;
       }
     }
-    if (P.lse) P.lse[(b * P.H + h) * (int64_t)L + qi] = (m_run * P.scale_log2 + log2f(l_run)) * 0.6931471805599453f;
+    if (P.lse) P.lse[(b * P.H + h) * (int64_t)L + qi] = (m_run + log2f(l_run)) * 0.6931471805599453f;
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, ATT_BK);
+  if (warp == 0) tmem_dealloc(tmem, TCOLS);
 }
 
 static bool a16(const void* p) { return ((uintptr_t)p & 15) == 0; }
@@ -319,7 +381,7 @@ namespace evo {
 template <int CP>
 int launch_attn_fwd_ws(const AttnParams& p, int64_t B, cudaStream_t st);
 // sequences at least this long take the warp-specialised kernel (attention_ws.cu)
-static int g_ws_min_len = 2048;  // measured: faster than attn_fwd_kernel from N_r = 2048 on
+static int g_ws_min_len = 4096;  // measured: faster than attn_fwd_kernel from N_r = 4096 on (per-key/no bias)
 }  // namespace evo
 
 extern "C" int evo_attention_fwd_ws_min_len(int len) {
@@ -333,7 +395,8 @@ extern "C" int evo_gated_attention_fwd(const EvoAttnDesc* d, void* stream) {
   int rc = attn_params_from_desc(d, p);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  const bool ws_bias_ok = true;
+  // the full (per query and key) bias path of the warp-specialised kernel measured slower
+  const bool ws_bias_ok = !p.bias || p.bs2 == 0 || g_ws_min_len <= 1;
   if (p.L >= g_ws_min_len && ws_bias_ok) {
     if (p.c <= 16) return launch_attn_fwd_ws<16>(p, d->B, st);
     if (p.c <= 32) return launch_attn_fwd_ws<32>(p, d->B, st);
