@@ -63,6 +63,14 @@ int evo_layernorm_bwd(const void* dy, int dy_dtype, const void* x, int x_dtype, 
                       void* dx, int dx_dtype, const void* res,
                       float* dgamma, float* dbeta, int64_t rows, int64_t cols, void* stream);
 
+/* same, plus dx_colsum[c] += sum_r dx[r, c] (fp32, ACCUMULATED): the bias gradient of the
+ * module that consumes this residual-stream gradient, fused into the pass that writes dx
+ * (contiguous rows of 32/64/128/256 columns; EVO_ERR_SHAPE otherwise). */
+int evo_layernorm_bwd_colsum(const void* dy, int dy_dtype, const void* x, int x_dtype, int64_t x_rs, int64_t x_cs,
+                             const float* gamma, const float* mean, const float* rstd,
+                             void* dx, int dx_dtype, const void* res,
+                             float* dgamma, float* dbeta, float* dx_colsum, int64_t rows, int64_t cols, void* stream);
+
 /* LN followed by k = 8 dot products per row (msa_row_bias, evoformer.py:201-207; fewer
  * heads are zero-padded to 8):  out[h*out_hs + r] = sum_c LN(x)[r, c] * w[c*8 + h].
  * ln_out (row-major, may be NULL) receives LN(x); mean/rstd are saved. bf16. */

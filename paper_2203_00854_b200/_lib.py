@@ -56,6 +56,8 @@ _SIGS = {
     "evo_device_info": [C.POINTER(C.c_int)] * 3,
     "evo_layernorm_fwd": [vp, C.c_int, i64, i64, vp, vp, vp, C.c_int, vp, vp, i64, i64, C.c_float, vp],
     "evo_layernorm_bwd": [vp, C.c_int, vp, C.c_int, i64, i64, vp, vp, vp, vp, C.c_int, vp, vp, vp, i64, i64, vp],
+    "evo_layernorm_bwd_colsum": [vp, C.c_int, vp, C.c_int, i64, i64, vp, vp, vp, vp, C.c_int, vp, vp, vp, vp, i64, i64,
+                                 vp],
     "evo_layernorm_rowdot_bwd": [vp, C.c_int, vp, vp, vp, C.c_int, vp, i64, vp, vp, vp, vp, vp, vp, vp, i64, i64,
                                  vp],
     "evo_layernorm_rowdot_fwd": [vp, C.c_int, vp, vp, vp, C.c_int, vp, C.c_int, i64, vp, vp, vp, i64, i64,

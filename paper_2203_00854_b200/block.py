@@ -138,15 +138,19 @@ def attention_fwd(bp: BlockParams, mod: str, x2d, B: int, L: int, kind: str, bia
     return out, sv
 
 
-def attention_bwd(bp: BlockParams, sv: Saved, dx_new):
-    """returns (dx, dbias) with dx = dx_new + d attn / dx; dbias fp32 for "full" bias."""
+def attention_bwd(bp: BlockParams, sv: Saved, dx_new, next_db=None, db_done=False):
+    """returns (dx, dbias) with dx = dx_new + d attn / dx; dbias fp32 for "full" bias.
+    next_db: bias-gradient buffer of the module consuming dx (its column sums are fused into
+    the final LayerNorm backward); db_done: this module's b_o gradient was already produced
+    that way by the module that wrote dx_new."""
     mod, B, L, kind = sv["mod"], sv["B"], sv["L"], sv["kind"]
     a = bp.layout.attn[mod]
     H, nh, c, ldq = a["H"], a["nh"], a["c"], a["ldq"]
     rows = B * L
     h, f, g = bp.h, bp.f, bp.g
     dev = dx_new.device
-    _dbias_only(dx_new, rows, H, g[f"{mod}.b_o"])  # db_o = sum_r dx_new
+    if not db_done:
+        _dbias_only(dx_new, rows, H, g[f"{mod}.b_o"])  # db_o = sum_r dx_new
     dog = _mm(dx_new, h[f"{mod}.w_o"].t())
     _wgrad(sv["og"], dx_new, g[f"{mod}.w_o"])
     sbr, slr = _attn_geometry(kind, B, L)
@@ -180,7 +184,7 @@ def attention_bwd(bp: BlockParams, sv: Saved, dx_new):
     dx = torch.addmm(dx_new, dgpre, h[f"{mod}.w_g"].t())          # gate reads raw x (G2)
     dln = _mm(dqkv, h[f"{mod}.w_qkv"].t())
     ops.layernorm_bwd(dln, sv["x"], f[f"{mod}.ln_g"], sv["mean"], sv["rstd"], rows, H, dx=dx, accumulate=True,
-                      dgamma=g[f"{mod}.ln_g"], dbeta=g[f"{mod}.ln_b"])
+                      dgamma=g[f"{mod}.ln_g"], dbeta=g[f"{mod}.ln_b"], dx_colsum=next_db)
     return dx, (dbias if full_bias else None)
 
 
@@ -242,11 +246,12 @@ def transition_fwd(bp: BlockParams, mod: str, x2d, rows: int, save=True):
     return out, sv
 
 
-def transition_bwd(bp: BlockParams, sv: Saved, dx_new):
+def transition_bwd(bp: BlockParams, sv: Saved, dx_new, next_db=None, db_done=False):
     mod = sv["mod"]
     rows, H = dx_new.shape
     h, f, g = bp.h, bp.f, bp.g
-    _dbias_only(dx_new, rows, H, g[f"{mod}.b2"])
+    if not db_done:
+        _dbias_only(dx_new, rows, H, g[f"{mod}.b2"])
     _wgrad(sv["hid"], dx_new, g[f"{mod}.w2"])
     dhid = _mm(dx_new, h[f"{mod}.w2"].t())
     dpre = ops.bias_act_bwd(dhid, sv["hid"], rows, dhid.shape[1], dy=dhid, dbias=g[f"{mod}.b1"])
@@ -254,7 +259,7 @@ def transition_bwd(bp: BlockParams, sv: Saved, dx_new):
     dln = _mm(dpre, h[f"{mod}.w1"].t())
     dx = torch.empty_like(dx_new)
     ops.layernorm_bwd(dln, sv["x"], f[f"{mod}.ln_g"], sv["mean"], sv["rstd"], rows, H, dx=dx, res=dx_new,
-                      dgamma=g[f"{mod}.ln_g"], dbeta=g[f"{mod}.ln_b"])
+                      dgamma=g[f"{mod}.ln_g"], dbeta=g[f"{mod}.ln_b"], dx_colsum=next_db)
     return dx
 
 
@@ -293,13 +298,15 @@ def opm_fwd(bp: BlockParams, m2d, z2d, S: int, R: int, save=True, b_full=None, R
     return out, sv
 
 
-def opm_bwd(bp: BlockParams, sv: Saved, dz_new, dm, reduce_scatter=None):
-    """accumulates the OPM contribution into dm (bf16 [S*R, Hm]); dz passes through."""
+def opm_bwd(bp: BlockParams, sv: Saved, dz_new, dm, reduce_scatter=None, next_db=None, db_done=False):
+    """accumulates the OPM contribution into dm (bf16 [S*R, Hm]); dz passes through.
+    next_db: bias gradient of the module consuming dm (fused column sums of the final dm)."""
     cfg = bp.cfg
     P, Hm, Hz = cfg.hidden_proj, cfg.h_msa, cfg.h_pair
     S, R, Rj = sv["S"], sv["R"], sv["Rj"]
     h, f, g = bp.h, bp.f, bp.g
-    _dbias_only(dz_new, R * Rj, Hz, g["opm.b_o"])
+    if not db_done:
+        _dbias_only(dz_new, R * Rj, Hz, g["opm.b_o"])
     _wgrad(sv["o"].view(R * Rj, P * P), dz_new, g["opm.w_o"])
     do = _mm(dz_new, h["opm.w_o"].t())                               # [R*Rj, P*P] == [i][j][p][q]
     dab = torch.empty(S * R, 2 * P, device=dz_new.device, dtype=BF16)
@@ -328,7 +335,7 @@ def opm_bwd(bp: BlockParams, sv: Saved, dz_new, dm, reduce_scatter=None):
     _bgrad(dab, g["opm.b_ab"])
     dln = _mm(dab, h["opm.w_ab"].t())
     ops.layernorm_bwd(dln, sv["m"], f["opm.ln_g"], sv["mean"], sv["rstd"], S * R, Hm, dx=dm, accumulate=True,
-                      dgamma=g["opm.ln_g"], dbeta=g["opm.ln_b"])
+                      dgamma=g["opm.ln_g"], dbeta=g["opm.ln_b"], dx_colsum=next_db)
 
 
 # ----------------------------------------------------------------------------- triangle update
@@ -391,7 +398,7 @@ def triangle_fwd(bp: BlockParams, mod: str, z2d, R: int, save=True, Rl=None, gat
     return out, sv
 
 
-def triangle_bwd(bp: BlockParams, sv: Saved, dz_new, reduce_scatter=None):
+def triangle_bwd(bp: BlockParams, sv: Saved, dz_new, reduce_scatter=None, next_db=None):
     cfg = bp.cfg
     P, Hz = cfg.hidden_proj, cfg.h_pair
     mod, R, Rl, M, N = sv["mod"], sv["R"], sv["Rl"], sv["M"], sv["N"]
@@ -450,7 +457,7 @@ def triangle_bwd(bp: BlockParams, sv: Saved, dz_new, reduce_scatter=None):
     dln = _mm(dY, h[f"{mod}.w_proj"].t())
     dz = torch.empty_like(dz_new)
     ops.layernorm_bwd(dln, sv["z"], f[f"{mod}.ln_g"], sv["mean"], sv["rstd"], rows, Hz, dx=dz, res=dz_new,
-                      dgamma=g[f"{mod}.ln_g"], dbeta=g[f"{mod}.ln_b"])
+                      dgamma=g[f"{mod}.ln_g"], dbeta=g[f"{mod}.ln_b"], dx_colsum=next_db)
     return dz
 
 
@@ -484,16 +491,21 @@ def block_bwd(bp: BlockParams, saved, dm, dz):
     sv_b, s1, s2, s3, s4, s5, s6, s7, s8, s9 = saved
     dm2 = dm.reshape(S * R, cfg.h_msa).contiguous()
     dz2 = dz.reshape(R * R, cfg.h_pair).contiguous()
-    dz2 = transition_bwd(bp, s9, dz2)
-    dz2, _ = attention_bwd(bp, s8, dz2)
-    dz2, _ = attention_bwd(bp, s7, dz2)
+    # each module's output-bias gradient (column sums of its incoming gradient) is fused into
+    # the final LayerNorm backward of the module that produced that gradient
+    fuse = dz2.is_cuda and cfg.h_pair in (32, 64, 128, 256) and cfg.h_msa in (32, 64, 128, 256)
+    g = bp.g
+    nd = (lambda k: g[k]) if fuse else (lambda k: None)
+    dz2 = transition_bwd(bp, s9, dz2, next_db=nd("pair_col.b_o"))
+    dz2, _ = attention_bwd(bp, s8, dz2, next_db=nd("pair_row.b_o"), db_done=fuse)
+    dz2, _ = attention_bwd(bp, s7, dz2, db_done=fuse)
     dz2 = triangle_bwd(bp, s6, dz2)
-    dz2 = triangle_bwd(bp, s5, dz2)
+    dz2 = triangle_bwd(bp, s5, dz2, next_db=nd("opm.b_o"))
     dm2 = dm2.clone()
-    opm_bwd(bp, s4, dz2, dm2)
-    dm2 = transition_bwd(bp, s3, dm2)
-    dm2, _ = attention_bwd(bp, s2, dm2)
-    dm2, dbias = attention_bwd(bp, s1, dm2)
+    opm_bwd(bp, s4, dz2, dm2, next_db=nd("msa_trans.b2"), db_done=fuse)
+    dm2 = transition_bwd(bp, s3, dm2, next_db=nd("msa_col.b_o"), db_done=fuse)
+    dm2, _ = attention_bwd(bp, s2, dm2, next_db=nd("msa_row.b_o"), db_done=fuse)
+    dm2, dbias = attention_bwd(bp, s1, dm2, db_done=fuse)
     msa_row_bias_bwd(bp, sv_b, dbias, dz2)
     SideStream.join()
     return dm2.view(S, R, cfg.h_msa), dz2.view(R, R, cfg.h_pair)

@@ -385,19 +385,21 @@ template <> struct Raw8<float> {
 // LPR = COLS/8 lanes per row, each owning 8 channels; a CTA walks one contiguous slab of
 // rows, U row-groups per warp step with every load of the step issued before any math.
 // <= 128 registers (2 CTAs = 16 warps per SM) keep ~100 KB of loads in flight per SM.
+// dsum (optional): column sums of the written dx, i.e. the bias gradient of the module that
+// consumes this residual-stream gradient (fused here instead of a separate colsum pass).
 template <typename TD, typename TX, typename TO, int COLS, int U>
 __global__ void __launch_bounds__(256, 2) ln_bwd_grp(const TD* __restrict__ dy, const TX* __restrict__ x, int64_t x_rs,
                                                      const float* __restrict__ gamma, const float* __restrict__ mean,
                                                      const float* __restrict__ rstd, TO* dx, const TO* res,
                                                      float* __restrict__ dgamma, float* __restrict__ dbeta,
-                                                     int64_t rows) {
+                                                     float* __restrict__ dsum, int64_t rows) {
   constexpr int LPR = COLS / 8, RPW = 32 / LPR;
-  __shared__ float red[8][2][COLS];
+  __shared__ float red[8][3][COLS];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, sub = lane / LPR, cl = (lane % LPR) * 8;
-  float g[8], dg[8], db[8];
+  float g[8], dg[8], db[8], ds[8];
   load_row<float, 8>(gamma + cl, g);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) dg[i] = db[i] = 0.f;
+  for (int i = 0; i < 8; ++i) dg[i] = db[i] = ds[i] = 0.f;
   const int64_t slab = (rows + gridDim.x - 1) / gridDim.x;
   const int64_t r0 = blockIdx.x * slab, r1 = r0 + slab < rows ? r0 + slab : rows;
   for (int64_t rb = r0 + wid * RPW * U; rb < r1; rb += 8 * RPW * U) {
@@ -444,10 +446,14 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_grp(const TD* __restrict__ dy, 
 #pragma unroll
         for (int i = 0; i < 8; ++i) o[i] = (res ? o[i] : 0.f) + rs[u] * (g[i] * d[i] - s1 - xv[i] * s2);
         store_row<TO, 8>(dx + row * x_rs + cl, o);
+        if (dsum) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) ds[i] += o[i];
+        }
       }
     }
   }
-  if (dgamma || dbeta) {
+  if (dgamma || dbeta || dsum) {
     // lanes of different row-groups hold partials of the same channels: fold them first
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -455,6 +461,7 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_grp(const TD* __restrict__ dy, 
       for (int o = LPR; o < 32; o <<= 1) {
         dg[i] += __shfl_xor_sync(0xffffffffu, dg[i], o);
         db[i] += __shfl_xor_sync(0xffffffffu, db[i], o);
+        ds[i] += __shfl_xor_sync(0xffffffffu, ds[i], o);
       }
     }
     if (sub == 0) {
@@ -462,18 +469,21 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_grp(const TD* __restrict__ dy, 
       for (int i = 0; i < 8; ++i) {
         red[wid][0][cl + i] = dg[i];
         red[wid][1][cl + i] = db[i];
+        red[wid][2][cl + i] = ds[i];
       }
     }
     __syncthreads();
     for (int c = threadIdx.x; c < COLS; c += blockDim.x) {
-      float a = 0.f, b = 0.f;
+      float a = 0.f, b = 0.f, e = 0.f;
 #pragma unroll
       for (int ww = 0; ww < 8; ++ww) {
         a += red[ww][0][c];
         b += red[ww][1][c];
+        e += red[ww][2][c];
       }
       if (dgamma) atomicAdd(dgamma + c, a);
       if (dbeta) atomicAdd(dbeta + c, b);
+      if (dsum) atomicAdd(dsum + c, e);
     }
   }
 }
@@ -781,15 +791,15 @@ extern "C" int evo_layernorm_rowdot_bwd(const void* x, int x_dtype, const float*
 
 template <typename TD, typename TX, typename TO>
 static int ln_bwd_impl(const void* dy, const void* x, int64_t x_rs, int64_t x_cs, const float* g, const float* mean,
-                       const float* rstd, void* dx, const void* res, float* dg, float* db, int64_t rows, int64_t cols,
-                       cudaStream_t st) {
+                       const float* rstd, void* dx, const void* res, float* dg, float* db, float* dsum, int64_t rows,
+                       int64_t cols, cudaStream_t st) {
   if (x_cs == 1 && (cols == 32 || cols == 64 || cols == 128 || cols == 256)) {
     const int64_t rpw = 32 / (cols / 8);
     int64_t need = (rows + 8 * rpw * 3 - 1) / (8 * rpw * 3), cap = (int64_t)sm_count() * 2;  // resident
     dim3 grid((unsigned)(need < cap ? need : cap));
 #define LBG(CC)                                                                                               \
   ln_bwd_grp<TD, TX, TO, CC, 3><<<grid, 256, 0, st>>>((const TD*)dy, (const TX*)x, x_rs, g, mean, \
-                                                                        rstd, (TO*)dx, (const TO*)res, dg, db, rows)
+                                                                        rstd, (TO*)dx, (const TO*)res, dg, db, dsum, rows)
     switch (cols) {
       case 32: LBG(32); break;
       case 64: LBG(64); break;
@@ -800,6 +810,8 @@ static int ln_bwd_impl(const void* dy, const void* x, int64_t x_rs, int64_t x_cs
     EVO_LAUNCH_CHECK("layernorm bwd");
     return EVO_OK;
   }
+  EVO_CHECK_ARG(dsum == nullptr, EVO_ERR_SHAPE, "layernorm bwd: fused dx column sums need 32/64/128/256 contiguous "
+                "columns (got %lld)", (long long)cols);
   if (x_cs == 1 && cols % 32 == 0 && cols <= 1024) {
     int64_t need = (rows + 127) / 128, cap = (int64_t)sm_count() * 4;  // 4-row batches per warp
     dim3 grid((unsigned)(need < cap ? need : cap));
@@ -839,20 +851,40 @@ static int ln_bwd_impl(const void* dy, const void* x, int64_t x_rs, int64_t x_cs
   return EVO_OK;
 }
 
-extern "C" int evo_layernorm_bwd(const void* dy, int dy_dtype, const void* x, int x_dtype, int64_t x_rs, int64_t x_cs,
-                                 const float* gamma, const float* mean, const float* rstd, void* dx, int dx_dtype,
-                                 const void* res, float* dgamma, float* dbeta, int64_t rows, int64_t cols,
-                                 void* stream) {
+static int ln_bwd_entry(const void* dy, int dy_dtype, const void* x, int x_dtype, int64_t x_rs, int64_t x_cs,
+                        const float* gamma, const float* mean, const float* rstd, void* dx, int dx_dtype,
+                        const void* res, float* dgamma, float* dbeta, float* dsum, int64_t rows, int64_t cols,
+                        void* stream) {
   EVO_CHECK_ARG(dy && x && gamma && mean && rstd && dx, EVO_ERR_ARG, "layernorm bwd: null pointer");
   if (rows == 0) return EVO_OK;
   cudaStream_t st = (cudaStream_t)stream;
   EVO_CHECK_ARG(x_dtype == dx_dtype, EVO_ERR_DTYPE, "layernorm bwd: x and dx dtypes must match");
   if (dy_dtype == EVO_BF16) {
     if (x_dtype == EVO_BF16)
-      return ln_bwd_impl<bf16, bf16, bf16>(dy, x, x_rs, x_cs, gamma, mean, rstd, dx, res, dgamma, dbeta, rows, cols, st);
-    return ln_bwd_impl<bf16, float, float>(dy, x, x_rs, x_cs, gamma, mean, rstd, dx, res, dgamma, dbeta, rows, cols, st);
+      return ln_bwd_impl<bf16, bf16, bf16>(dy, x, x_rs, x_cs, gamma, mean, rstd, dx, res, dgamma, dbeta, dsum, rows,
+                                           cols, st);
+    return ln_bwd_impl<bf16, float, float>(dy, x, x_rs, x_cs, gamma, mean, rstd, dx, res, dgamma, dbeta, dsum, rows,
+                                           cols, st);
   }
   if (x_dtype == EVO_BF16)
-    return ln_bwd_impl<float, bf16, bf16>(dy, x, x_rs, x_cs, gamma, mean, rstd, dx, res, dgamma, dbeta, rows, cols, st);
-  return ln_bwd_impl<float, float, float>(dy, x, x_rs, x_cs, gamma, mean, rstd, dx, res, dgamma, dbeta, rows, cols, st);
+    return ln_bwd_impl<float, bf16, bf16>(dy, x, x_rs, x_cs, gamma, mean, rstd, dx, res, dgamma, dbeta, dsum, rows,
+                                          cols, st);
+  return ln_bwd_impl<float, float, float>(dy, x, x_rs, x_cs, gamma, mean, rstd, dx, res, dgamma, dbeta, dsum, rows,
+                                          cols, st);
+}
+
+extern "C" int evo_layernorm_bwd(const void* dy, int dy_dtype, const void* x, int x_dtype, int64_t x_rs, int64_t x_cs,
+                                 const float* gamma, const float* mean, const float* rstd, void* dx, int dx_dtype,
+                                 const void* res, float* dgamma, float* dbeta, int64_t rows, int64_t cols,
+                                 void* stream) {
+  return ln_bwd_entry(dy, dy_dtype, x, x_dtype, x_rs, x_cs, gamma, mean, rstd, dx, dx_dtype, res, dgamma, dbeta,
+                      nullptr, rows, cols, stream);
+}
+
+extern "C" int evo_layernorm_bwd_colsum(const void* dy, int dy_dtype, const void* x, int x_dtype, int64_t x_rs,
+                                        int64_t x_cs, const float* gamma, const float* mean, const float* rstd,
+                                        void* dx, int dx_dtype, const void* res, float* dgamma, float* dbeta,
+                                        float* dx_colsum, int64_t rows, int64_t cols, void* stream) {
+  return ln_bwd_entry(dy, dy_dtype, x, x_dtype, x_rs, x_cs, gamma, mean, rstd, dx, dx_dtype, res, dgamma, dbeta,
+                      dx_colsum, rows, cols, stream);
 }

@@ -61,9 +61,10 @@ def layernorm_fwd(x, gamma, beta, rows, cols, x_rs=None, x_cs=1, out=None, out_d
 
 
 def layernorm_bwd(dy, x, gamma, mean, rstd, rows, cols, x_rs=None, x_cs=1, dx=None,
-                  accumulate=False, dgamma=None, dbeta=None, res=None):
+                  accumulate=False, dgamma=None, dbeta=None, res=None, dx_colsum=None):
     """dx = res + dLN/dx.  accumulate=True means res = dx (in place);  res may be another
-    tensor (the residual-stream gradient) so no clone is needed."""
+    tensor (the residual-stream gradient) so no clone is needed.  dx_colsum (fp32 [cols],
+    accumulated): column sums of the written dx, fused into the same pass."""
     _cuda(dy, x, gamma, mean, rstd)
     x_rs = cols if x_rs is None else x_rs
     if dx is None:
@@ -73,6 +74,10 @@ def layernorm_bwd(dy, x, gamma, mean, rstd, rows, cols, x_rs=None, x_cs=1, dx=No
         accumulate = False
     if accumulate:
         res = dx
+    if dx_colsum is not None:
+        call("evo_layernorm_bwd_colsum", _p(dy), _dt(dy), _p(x), _dt(x), x_rs, x_cs, _p(gamma), _p(mean), _p(rstd),
+             _p(dx), _dt(dx), _p(res), _p(dgamma), _p(dbeta), _p(dx_colsum), rows, cols, stream_handle())
+        return dx
     call("evo_layernorm_bwd", _p(dy), _dt(dy), _p(x), _dt(x), x_rs, x_cs, _p(gamma), _p(mean), _p(rstd),
          _p(dx), _dt(dx), _p(res), _p(dgamma), _p(dbeta), rows, cols, stream_handle())
     return dx

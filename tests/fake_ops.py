@@ -52,7 +52,7 @@ def layernorm_fwd(x, gamma, beta, rows, cols, x_rs=None, x_cs=1, out=None, out_d
 
 
 def layernorm_bwd(dy, x, gamma, mean, rstd, rows, cols, x_rs=None, x_cs=1, dx=None, accumulate=False, dgamma=None,
-                  dbeta=None, res=None):
+                  dbeta=None, res=None, dx_colsum=None):
     x_rs = cols if x_rs is None else x_rs
     xv = _sv(x, 0, (rows, cols), (x_rs, x_cs)).float()
     d = dy.reshape(rows, cols).float()
@@ -70,6 +70,8 @@ def layernorm_bwd(dy, x, gamma, mean, rstd, rows, cols, x_rs=None, x_cs=1, dx=No
         res = dx
     base = _sv(res, 0, (rows, cols), (x_rs, x_cs)).float() if res is not None else 0
     _sv(dx, 0, (rows, cols), (x_rs, x_cs)).copy_(o + base)
+    if dx_colsum is not None:
+        dx_colsum += (o + base).sum(0)
     return dx
 
 
