@@ -323,11 +323,16 @@ struct TileLoader {
   static constexpr int IT = ROWS / 16;  // chunks per thread per k-tile
   int64_t roff[MN ? 1 : IT];            // element offset of the row part, -1 = out of range
 
+  // K-major thread map: lane = (k chunk of a pair, row of 16); warp w owns k chunks 2w, 2w+1.
+  // Global: 32 contiguous bytes (one sector) per row; smem: each half-warp writes 256
+  // contiguous bytes (two core matrices) -> conflict-free 16-byte cp.async stores.
+  static __device__ __forceinline__ int krow(int tid) { return tid & 15; }
+  static __device__ __forceinline__ int kcol(int tid) { return ((tid >> 5) * 2 + ((tid >> 4) & 1)) * 8; }
   __device__ __forceinline__ void setup(const MatArg& m, uint32_t r0, uint32_t R, int tid) {
     if constexpr (!MN) {
 #pragma unroll
       for (int it = 0; it < IT; ++it) {
-        const uint32_t r = r0 + (tid >> 3) + it * 16;
+        const uint32_t r = r0 + krow(tid) + it * 16;
         roff[it] = r < R ? off_dim0(m, r) : -1;
       }
     } else {
@@ -340,11 +345,11 @@ struct TileLoader {
   __device__ __forceinline__ void load(uint32_t sdst, const MatArg& m, const char* base, uint32_t k0, uint32_t K,
                                        int tid) const {
     if constexpr (!MN) {
-      const int k = (tid & 7) * 8;
+      const int k = kcol(tid);
       const uint32_t kk = k0 + k;
       const bool kok = kk < K;
       const int64_t koff = kok ? off_dim1(m, kk) : 0;
-      const uint32_t s0 = sdst + kmajor_off(tid >> 3, k, ROWS);
+      const uint32_t s0 = sdst + kmajor_off(krow(tid), k, ROWS);
 #pragma unroll
       for (int it = 0; it < IT; ++it) {
         const bool pred = kok && roff[it] >= 0;
@@ -662,7 +667,9 @@ static int launch_bgemm_s(MatArg A, MatArg B, MatArg C, int64_t batch, int64_t M
 template <int BN, bool AM, bool BMN, typename TC>
 static int launch_bgemm_ws(MatArg A, MatArg B, MatArg C, int64_t batch, int64_t M, int64_t N, int64_t K, float alpha,
                            float beta, int c_mode, int splits, float* ws, cudaStream_t st) {
-  constexpr int STAGES = 4;
+  // 256-wide N tiles (long-K, large problems) halve the A-tile re-reads per FLOP; 3 stages
+  // keep the ring + staging tile within shared memory
+  constexpr int STAGES = BN >= 256 ? 3 : 4;
   const size_t smem = STAGES * (GEMM_BM * GEMM_BK * 2 + BN * GEMM_BK * 2) + (size_t)GEMM_BM * (BN * sizeof(TC) + 16);
   auto kern = bgemm_ws_kernel<BN, AM, BMN, STAGES, TC>;
   static bool attr_set = false;
@@ -760,12 +767,15 @@ static int bgemm_entry(const EvoMat* A, const EvoMat* B, const EvoMat* C, int64_
   cudaStream_t st = (cudaStream_t)stream;
   // wide N tiles amortise the A-tile loads; N=64 keeps small problems parallel
   bool small = ((M + 127) / 128) * ((N + 127) / 128) * batch < 148;
-  const int bn = (small || N <= 64) ? 64 : 128;
+  const bool wide = !small && C->dtype == EVO_BF16 && N >= 256 && K >= 512 && !use_v1() &&
+                    ((M + 127) / 128) * ((N + 255) / 256) * batch >= 2 * 148;
+  const int bn = (small || N <= 64) ? 64 : (wide ? 256 : 128);
   int splits = pick_splits(batch, M, N, K, bn);
   if (splits > 1 && (!workspace || ws_bytes < splits * batch * M * N * 4)) splits = 1;
   float* ws = (float*)workspace;
   if (C->dtype == EVO_BF16) {
     if (bn == 64) return dispatch_major<64, bf16>(am, bm, a, b, c, batch, M, N, K, alpha, beta, c_mode, splits, ws, st);
+    if (bn == 256) return dispatch_major<256, bf16>(am, bm, a, b, c, batch, M, N, K, alpha, beta, c_mode, splits, ws, st);
     return dispatch_major<128, bf16>(am, bm, a, b, c, batch, M, N, K, alpha, beta, c_mode, splits, ws, st);
   }
   if (bn == 64) return dispatch_major<64, float>(am, bm, a, b, c, batch, M, N, K, alpha, beta, c_mode, splits, ws, st);
