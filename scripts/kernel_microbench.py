@@ -10,8 +10,8 @@ Shapes:
   K1 LayerNorm: [65536, 128], [32768, 256], [65536, 32] bf16 (engine.layernorm_raw, engine.py:206-217).
 Algorithmic bytes = every input read once + every output written once (bf16 activations,
 fp32 gamma/beta/statistics).  Each timed launch reads a fresh buffer from a rotating set
-larger than L2 (126 MB), so no launch hits warm L2.  Times: CUDA events on the launching
-stream, warm, mean over --iters launches.  Peak: MEASURED_PEAKS.json hbm_gbs (else the
+larger than L2 (126 MB), so no launch hits warm L2.  Times: the --iters launches are captured
+in one CUDA graph and replayed (no host launch overhead), CUDA events on the stream.  Peak: MEASURED_PEAKS.json hbm_gbs (else the
 B200_PROFILING.md fallback).
 """
 from __future__ import annotations
@@ -45,14 +45,21 @@ def rotating(make, nbytes_each):
 
 
 def time_launches(fn, sets, iters):
+    """device time per launch: the launches are captured in a CUDA graph and replayed, so
+    host (ctypes) launch overhead is not measured"""
     for s in sets[:2]:
         fn(*s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for i in range(iters):
+            fn(*sets[i % len(sets)])
+    g.replay()
     torch.cuda.synchronize()
     st = torch.cuda.current_stream()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(st)
-    for i in range(iters):
-        fn(*sets[i % len(sets)])
+    g.replay()
     b.record(st)
     torch.cuda.synchronize()
     return a.elapsed_time(b) / iters
