@@ -669,7 +669,6 @@ static int ln_fwd_dispatch_warp(const void* x, int64_t x_rs, const float* g, con
                                 int64_t dot_hs, cudaStream_t st) {
   if (cols == 32 || cols == 64 || cols == 128 || cols == 256) {
     const int64_t rpw = 32 / (cols / 8);
-    // 4 row groups per warp step: 4 16-byte loads in flight per thread before any math
     int64_t need = (rows + 8 * rpw * 2 - 1) / (8 * rpw * 2), cap = (int64_t)sm_count() * 8;
     dim3 g2((unsigned)(need < cap ? need : cap));
 #define LNG(CC) ln_fwd_grp<TX, TY, CC, 2><<<g2, 256, 0, st>>>((const TX*)x, x_rs, g, b, (TY*)y, mean, rstd, rows, eps)
