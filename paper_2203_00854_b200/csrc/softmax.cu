@@ -82,7 +82,10 @@ __global__ void __launch_bounds__(256) softmax_fwd_kernel(const void* __restrict
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= rows) return;
-  const int64_t q = row % Q, bh = row / Q, h = bh % H, b = bh / H;
+  // 32-bit index math (rows < 2^31, host-checked): 64-bit divisions per row cost more issue
+  // slots than the row's arithmetic
+  const uint32_t r32 = (uint32_t)row, q = r32 % (uint32_t)Q, bh = r32 / (uint32_t)Q;
+  const uint32_t h = bh % (uint32_t)H, b = bh / (uint32_t)H;
   const int64_t boff = bias.p ? b * bias.s0 + h * bias.s1 + q * bias.s2 : 0;
   const int64_t moff = mask.p ? b * mask.s0 + h * mask.s1 + q * mask.s2 : 0;
   const bool bvec = bias.s3 == 1, mvec = mask.s3 == 1;
@@ -119,12 +122,12 @@ __global__ void __launch_bounds__(256) softmax_fwd_kernel(const void* __restrict
     if (k0 < K) {
 #pragma unroll
       for (int i = 0; i < VEC; ++i) {
-        v[j][i] = exp2f(v[j][i] - mx);
+        v[j][i] = ex2f(v[j][i] - mx);
         s += v[j][i];
       }
     }
   }
-  const float inv = 1.0f / warp_sum(s);
+  const float inv = rcpf(warp_sum(s));
 #pragma unroll
   for (int j = 0; j < NCH; ++j) {
     const int k0 = (j * 32 + lane) * VEC;
@@ -231,6 +234,7 @@ extern "C" int evo_softmax_fwd(const void* x, int x_dtype, const void* bias, int
   };
   EVO_CHECK_ARG(vec_ok(bb) && vec_ok(mm), EVO_ERR_ALIGN, "softmax: bias/mask rows must be vector aligned");
   cudaStream_t st = (cudaStream_t)stream;
+  EVO_CHECK_ARG(rows < (1LL << 31), EVO_ERR_SHAPE, "softmax: more than 2^31 rows");
   dim3 grid((unsigned)((rows + 7) / 8));
   const float sl2 = scale * 1.4426950408889634f;
   SM_DISPATCH(softmax_fwd_kernel, x, x_dtype, bb, mm, y, y_dtype, H, Q, rows, (int)K, sl2);
