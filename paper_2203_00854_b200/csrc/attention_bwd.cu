@@ -79,7 +79,8 @@ __global__ void __launch_bounds__(256) attn_dbias_reduce(const bf16* __restrict_
 #pragma unroll
       for (int k = 0; k < 8; ++k) acc[k] += v[k];
     }
-    const int64_t h = e / ((int64_t)L * L), kk = (e / L) % L, q = e % L;
+    const uint32_t eu = (uint32_t)e, LL = (uint32_t)L * (uint32_t)L;  // H*L*L < 2^31 (host-checked)
+    const int64_t h = eu / LL, kk = (eu / (uint32_t)L) % (uint32_t)L, q = eu % (uint32_t)L;
 #pragma unroll
     for (int t = 0; t < 8; ++t) dbias[h * d1 + (q + t) * d2 + kk * d3] += scale * acc[t];
   }
@@ -121,20 +122,22 @@ constexpr int PREP_PASSES = 4;
 __global__ void __launch_bounds__(256) attn_bwd_prep(AttnBwdParams P, int64_t B) {
   const int lane = threadIdx.x & 31;
   const int L = P.f.L, H = P.f.H, c = P.f.c;
-  const int nch = H * c / 8;
-  const int64_t total = B * L * nch;
-  const int64_t f0 = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * (PREP_PASSES * 32);
+  const uint32_t nch = H * c / 8;
+  // 32-bit (row, chunk) / (b, l) divisions: the host guarantees B*L*nch < 2^31
+  const uint32_t total = (uint32_t)(B * L * nch);
+  const uint32_t f0 = ((uint32_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * (PREP_PASSES * 32);
   if (f0 >= total) return;
   const int lanes_per_head = c / 8;  // 1, 2, 4 or 8
   uint4 ud[PREP_PASSES], ug[PREP_PASSES], uo[PREP_PASSES];
   float lse[PREP_PASSES];
 #pragma unroll
   for (int t = 0; t < PREP_PASSES; ++t) {
-    const int64_t f = f0 + t * 32 + lane;
+    const uint32_t f = f0 + t * 32 + lane;
     if (f < total) {
-      const int64_t row = f / nch;
+      const uint32_t row = f / nch;
       const int col = (int)(f - row * nch) * 8;
-      const int64_t b = row / L, l = row - b * L;
+      const uint32_t bu = row / (uint32_t)L;
+      const int64_t b = bu, l = row - bu * (uint32_t)L;
       ud[t] = *reinterpret_cast<const uint4*>(P.dout + b * P.do_sb + l * P.do_sl + col);
       ug[t] = *reinterpret_cast<const uint4*>(P.f.g + b * P.f.g_sb + l * P.f.g_sl + col);
       uo[t] = *reinterpret_cast<const uint4*>(P.f.orw + b * P.f.r_sb + l * P.f.r_sl + col);
@@ -143,11 +146,12 @@ __global__ void __launch_bounds__(256) attn_bwd_prep(AttnBwdParams P, int64_t B)
   }
 #pragma unroll
   for (int t = 0; t < PREP_PASSES; ++t) {
-    const int64_t f = f0 + t * 32 + lane;
+    const uint32_t f = f0 + t * 32 + lane;
     const bool ok = f < total;
-    const int64_t row = ok ? f / nch : 0;
+    const uint32_t row = ok ? f / nch : 0;
     const int col = (int)(f - row * nch) * 8;
-    const int64_t b = row / L, l = row - b * L;
+    const uint32_t bu = row / (uint32_t)L;
+    const int64_t b = bu, l = row - bu * (uint32_t)L;
     float dsum = 0.f;
     if (ok) {
       float dout[8], g[8], o[8], dO[8], dg[8];
@@ -167,7 +171,7 @@ __global__ void __launch_bounds__(256) attn_bwd_prep(AttnBwdParams P, int64_t B)
       uint4 w;
       w.x = pack_bf16x2(dO[0], dO[1]); w.y = pack_bf16x2(dO[2], dO[3]);
       w.z = pack_bf16x2(dO[4], dO[5]); w.w = pack_bf16x2(dO[6], dO[7]);
-      *reinterpret_cast<uint4*>(P.dO + row * (int64_t)(H * c) + col) = w;
+      *reinterpret_cast<uint4*>(P.dO + (int64_t)row * (H * c) + col) = w;
       w.x = pack_bf16x2(dg[0], dg[1]); w.y = pack_bf16x2(dg[2], dg[3]);
       w.z = pack_bf16x2(dg[4], dg[5]); w.w = pack_bf16x2(dg[6], dg[7]);
       *reinterpret_cast<uint4*>(P.dg + b * P.dg_sb + l * P.dg_sl + col) = w;
@@ -566,8 +570,9 @@ __global__ void __launch_bounds__(256) attn_bwd_dq_finish(AttnBwdParams P, int64
   const int64_t n8 = n / 8;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = i * 8;
-    const int64_t row = e / (H * c), col = e % (H * c);
-    const int64_t b = row / L, l = row % L;
+    const uint32_t eu = (uint32_t)e, hc = (uint32_t)(H * c);  // n < 2^31 (host-checked)
+    const uint32_t rowu = eu / hc, bu = rowu / (uint32_t)L;
+    const int64_t col = eu - rowu * hc, b = bu, l = rowu - bu * (uint32_t)L;
     float4 a[NP], q[NP];
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
@@ -654,6 +659,8 @@ extern "C" int evo_gated_attention_bwd(const EvoAttnBwdDesc* d, void* stream) {
   const int64_t B = d->f.B, L = d->f.L;
   const int H = d->f.H, c = d->f.c;
   EVO_CHECK_ARG((c & (c - 1)) == 0, EVO_ERR_SHAPE, "attention bwd: head dim must be 8, 16, 32 or 64 (got %d)", c);
+  EVO_CHECK_ARG(B * L * H * c < (1LL << 31) && (int64_t)H * L * L < (1LL << 31), EVO_ERR_SHAPE,
+                "attention bwd: B*L*H*c and H*L*L must be < 2^31 (32-bit index math)");
   int64_t off_dq, off_D, off_lse2, off_dS;
   // batch-shared full bias (msa_row): dS^T tiles to a workspace, reduced over the batch after
   // (16-byte tile copies need L % 8 == 0; otherwise the generic atomic path)

@@ -38,15 +38,18 @@ __device__ __forceinline__ void st8(T* p, const float* v) {
 }
 
 // ------------------------------------------------------------------ gated residual
-template <typename T>
+// IDX: uint32_t when rows*cols/8 < 2^31 (one 32-bit division per vector instead of a 64-bit
+// one, which costs more issue slots than the vector's arithmetic), else int64_t
+template <typename T, typename IDX>
 __global__ void __launch_bounds__(256) gated_residual_fwd_k(const T* __restrict__ res, const T* __restrict__ y,
                                                             int64_t y_rs, const float* __restrict__ bias,
                                                             const T* __restrict__ gp, int64_t gp_rs,
                                                             T* __restrict__ out, int64_t rows, int64_t cols) {
-  const int64_t cpr = cols / 8;
-  const int64_t n = rows * cpr;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / cpr, c = (i - r * cpr) * 8;
+  const IDX cpr = (IDX)(cols / 8);
+  const IDX n = (IDX)(rows * (cols / 8));
+  for (IDX i = (IDX)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (IDX)gridDim.x * blockDim.x) {
+    const IDX rr = i / cpr;
+    const int64_t r = rr, c = (int64_t)(i - rr * cpr) * 8;
     float rv[8], yv[8];
     ld8<T>(res + r * cols + c, rv);
     ld8<T>(y + r * y_rs + c, yv);
@@ -167,12 +170,13 @@ __global__ void __launch_bounds__(256) colsum_k(const T* __restrict__ x, int64_t
 }
 
 // ------------------------------------------------------------------ bias + activation
-template <typename T>
+template <typename T, typename IDX>
 __global__ void __launch_bounds__(256) bias_act_fwd_k(T* __restrict__ y, const float* __restrict__ bias, int64_t rows,
                                                       int64_t cols, int act) {
-  const int64_t cpr = cols / 8, n = rows * cpr;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / cpr, c = (i - r * cpr) * 8;
+  const IDX cpr = (IDX)(cols / 8), n = (IDX)(rows * (cols / 8));
+  for (IDX i = (IDX)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (IDX)gridDim.x * blockDim.x) {
+    const IDX rr = i / cpr;
+    const int64_t r = rr, c = (int64_t)(i - rr * cpr) * 8;
     float v[8];
     ld8<T>(y + r * cols + c, v);
 #pragma unroll
@@ -308,12 +312,15 @@ extern "C" int evo_gated_residual_fwd(const void* res, const void* y, int64_t y_
   if (rows == 0) return EVO_OK;
   cudaStream_t st = (cudaStream_t)stream;
   unsigned g = grid_for(rows * cols / 8, 256);
-  if (dtype == EVO_BF16)
-    gated_residual_fwd_k<bf16><<<g, 256, 0, st>>>((const bf16*)res, (const bf16*)y, y_rs, bias, (const bf16*)gp,
-                                                  gp_rs, (bf16*)out, rows, cols);
-  else
-    gated_residual_fwd_k<float><<<g, 256, 0, st>>>((const float*)res, (const float*)y, y_rs, bias, (const float*)gp,
-                                                   gp_rs, (float*)out, rows, cols);
+  const bool i32 = rows * (cols / 8) < (1LL << 31);
+#define GRF(T, I) gated_residual_fwd_k<T, I><<<g, 256, 0, st>>>((const T*)res, (const T*)y, y_rs, bias, (const T*)gp, \
+                                                                gp_rs, (T*)out, rows, cols)
+  if (dtype == EVO_BF16) {
+    if (i32) GRF(bf16, uint32_t); else GRF(bf16, int64_t);
+  } else {
+    if (i32) GRF(float, uint32_t); else GRF(float, int64_t);
+  }
+#undef GRF
   EVO_LAUNCH_CHECK("gated_residual fwd");
   return EVO_OK;
 }
@@ -376,8 +383,14 @@ extern "C" int evo_bias_act_fwd(void* y, const float* bias, int64_t rows, int64_
   if (rows == 0) return EVO_OK;
   cudaStream_t st = (cudaStream_t)stream;
   unsigned g = grid_for(rows * cols / 8, 256);
-  if (dtype == EVO_BF16) bias_act_fwd_k<bf16><<<g, 256, 0, st>>>((bf16*)y, bias, rows, cols, act);
-  else bias_act_fwd_k<float><<<g, 256, 0, st>>>((float*)y, bias, rows, cols, act);
+  const bool i32 = rows * (cols / 8) < (1LL << 31);
+  if (dtype == EVO_BF16) {
+    if (i32) bias_act_fwd_k<bf16, uint32_t><<<g, 256, 0, st>>>((bf16*)y, bias, rows, cols, act);
+    else bias_act_fwd_k<bf16, int64_t><<<g, 256, 0, st>>>((bf16*)y, bias, rows, cols, act);
+  } else {
+    if (i32) bias_act_fwd_k<float, uint32_t><<<g, 256, 0, st>>>((float*)y, bias, rows, cols, act);
+    else bias_act_fwd_k<float, int64_t><<<g, 256, 0, st>>>((float*)y, bias, rows, cols, act);
+  }
   EVO_LAUNCH_CHECK("bias_act fwd");
   return EVO_OK;
 }
