@@ -20,6 +20,10 @@
 
 #include "common.cuh"
 
+#include <cuda.h>  // CUtensorMap (the encoder is fetched at run time via cudaGetDriverEntryPoint)
+#include <cstdlib>
+#include <cstring>
+
 namespace evo {
 
 int sm_count();
@@ -370,13 +374,52 @@ struct TileLoader {
   }
 };
 
-constexpr int WS_EPI_WARPS = 8;                       // two epilogue warps per TMEM lane quarter
+// ---------------------------------------------------------------- TMA (K-major operands)
+// A / B tiles arrive by cp.async.bulk.tensor with the 128-byte swizzle: BM (BN) rows of 64
+// bf16 = 128 B each, 8-row atoms of 1 KB.  One elected producer thread per stage instead of
+// 128 threads x 12 cp.async with per-chunk address arithmetic.
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+// MN-major SWIZZLE_128B descriptor: tile = (rows/64) TMA boxes of [64 k][64 mn] (8 KB each);
+// LBO = 8 KB (next 64-element MN atom), SBO = 1 KB (next 8 k rows)
+__device__ __forceinline__ uint64_t make_sdesc_sw128_mn(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)(8192 >> 4) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+// K-major SWIZZLE_128B descriptor: LBO = 16 B (unused within the atom), SBO = 1 KB (8 rows)
+__device__ __forceinline__ uint64_t make_sdesc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;  // version
+  d |= (uint64_t)2 << 61;  // layout SWIZZLE_128B
+  return d;
+}
+
+constexpr int WS_EPI_WARPS = 4;  // one epilogue warp per TMEM lane quarter (8 measured no faster)
 constexpr int WS_GEMM_THREADS = 160 + 32 * WS_EPI_WARPS;  // 4 producer warps + MMA warp + epilogue
 
-template <int BN, bool A_MN, bool B_MN, int STAGES, typename TC>
+template <int BN, bool A_MN, bool B_MN, int STAGES, typename TC, bool TMA>
 __global__ void __launch_bounds__(WS_GEMM_THREADS, 1) bgemm_ws_kernel(MatArg A, MatArg B, MatArg C, uint32_t M, uint32_t N,
                                                           uint32_t K, float alpha, float beta, int c_mode, int splits,
-                                                          float* __restrict__ ws, int batch) {
+                                                          float* __restrict__ ws, int batch,
+                                                          const __grid_constant__ CUtensorMap tmA,
+                                                          const __grid_constant__ CUtensorMap tmB) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
   __shared__ uint32_t tmem_sh;
@@ -409,7 +452,7 @@ __global__ void __launch_bounds__(WS_GEMM_THREADS, 1) bgemm_ws_kernel(MatArg A, 
   if (warp == 0) tmem_alloc(&tmem_sh, 2 * BN);
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 128);
+      mbar_init(&full[s], TMA ? 1 : 128);
       mbar_init(&empty[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -423,7 +466,41 @@ __global__ void __launch_bounds__(WS_GEMM_THREADS, 1) bgemm_ws_kernel(MatArg A, 
   tc_fence_after();
   const uint32_t tmem = tmem_sh;
 
-  if (warp < 4) {
+  if (TMA && warp < 4) {
+    // ---------------- TMA producer (one thread)
+    if (threadIdx.x == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
+        uint32_t b, m0, n0;
+        int sp, kt0, ktn;
+        decode(t, b, sp, m0, n0, kt0, ktn);
+        for (int kt = 0; kt < ktn; ++kt) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], A_BYTES + B_BYTES);
+          const int k0 = (kt0 + kt) * GEMM_BK;
+          if constexpr (A_MN) {
+#pragma unroll
+            for (int j = 0; j < GEMM_BM / 64; ++j)
+              tma_load_3d(sA + stage * A_BYTES + j * 8192, &tmA, (int)m0 + 64 * j, k0, (int)b, &full[stage]);
+          } else {
+            tma_load_3d(sA + stage * A_BYTES, &tmA, k0, (int)m0, (int)b, &full[stage]);
+          }
+          if constexpr (B_MN) {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_3d(sB + stage * B_BYTES + j * 8192, &tmB, (int)n0 + 64 * j, k0, (int)b, &full[stage]);
+          } else {
+            tma_load_3d(sB + stage * B_BYTES, &tmB, k0, (int)n0, (int)b, &full[stage]);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp < 4) {
     // ---------------- producers (warps 0..3)
     const int tid = threadIdx.x;
     int stage = 0;
@@ -469,8 +546,16 @@ __global__ void __launch_bounds__(WS_GEMM_THREADS, 1) bgemm_ws_kernel(MatArg A, 
         if (lane == 0) {
 #pragma unroll
           for (int kk = 0; kk < GEMM_BK / 16; ++kk) {
-            uint64_t ad = make_sdesc(sA + stage * A_BYTES + kk * 2 * (GEMM_BM / 8) * 128, (GEMM_BM / 8) * 128, 128);
-            uint64_t bd = make_sdesc(sB + stage * B_BYTES + kk * 2 * (BN / 8) * 128, (BN / 8) * 128, 128);
+            uint64_t ad, bd;
+            if constexpr (TMA) {  // K = 16 step: 32 B along K-major rows / 16 k rows (2 KB) MN-major
+              ad = A_MN ? make_sdesc_sw128_mn(sA + stage * A_BYTES + kk * 2048)
+                        : make_sdesc_sw128(sA + stage * A_BYTES + kk * 32);
+              bd = B_MN ? make_sdesc_sw128_mn(sB + stage * B_BYTES + kk * 2048)
+                        : make_sdesc_sw128(sB + stage * B_BYTES + kk * 32);
+            } else {
+              ad = make_sdesc(sA + stage * A_BYTES + kk * 2 * (GEMM_BM / 8) * 128, (GEMM_BM / 8) * 128, 128);
+              bd = make_sdesc(sB + stage * B_BYTES + kk * 2 * (BN / 8) * 128, (BN / 8) * 128, 128);
+            }
             mma_bf16(tmem + buf * BN, ad, bd, IDESC, (kt | kk) != 0);
           }
           mma_commit(&empty[stage]);
@@ -664,6 +749,56 @@ static int launch_bgemm_s(MatArg A, MatArg B, MatArg C, int64_t batch, int64_t M
   return EVO_OK;
 }
 
+// cuTensorMapEncodeTiled from the driver, fetched once through the runtime (no -lcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// K-major operand with plain [batch][rows][K] addressing (no split levels) -> 3-D map with a
+// {64 k, box_rows rows, 1} box and the 128-byte swizzle
+static bool tma_map_kmajor(CUtensorMap* map, const MatArg& a, int64_t rows, int64_t K, int64_t batch, int box_rows) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return false;
+  if (!(a.lo1 == 1 && a.split1 >= (uint32_t)K && a.split0 >= (uint32_t)rows)) return false;
+  if ((a.lo0 * 2) % 16 || (batch > 1 && (a.bs * 2) % 16) || ((uintptr_t)a.ptr & 15) || K % 8) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)batch};
+  cuuint64_t strides[2] = {(cuuint64_t)a.lo0 * 2, (cuuint64_t)(batch > 1 ? a.bs * 2 : a.lo0 * 2 * rows)};
+  cuuint32_t box[3] = {(cuuint32_t)GEMM_BK, (cuuint32_t)box_rows, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<char*>(a.ptr), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// MN-major operand with plain [batch][K][rows] addressing -> 3-D map {rows, K, batch} with a
+// {64 mn, 64 k, 1} box (one 128-byte swizzle atom column)
+static bool tma_map_mnmajor(CUtensorMap* map, const MatArg& a, int64_t rows, int64_t K, int64_t batch) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return false;
+  if (!(a.lo0 == 1 && a.split0 >= (uint32_t)rows && a.split1 >= (uint32_t)K)) return false;
+  if ((a.lo1 * 2) % 16 || (batch > 1 && (a.bs * 2) % 16) || ((uintptr_t)a.ptr & 15) || rows % 8) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)rows, (cuuint64_t)K, (cuuint64_t)batch};
+  cuuint64_t strides[2] = {(cuuint64_t)a.lo1 * 2, (cuuint64_t)(batch > 1 ? a.bs * 2 : a.lo1 * 2 * K)};
+  cuuint32_t box[3] = {64, (cuuint32_t)GEMM_BK, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<char*>(a.ptr), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int BN, bool AM, bool BMN, typename TC>
 static int launch_bgemm_ws(MatArg A, MatArg B, MatArg C, int64_t batch, int64_t M, int64_t N, int64_t K, float alpha,
                            float beta, int c_mode, int splits, float* ws, cudaStream_t st) {
@@ -671,17 +806,30 @@ static int launch_bgemm_ws(MatArg A, MatArg B, MatArg C, int64_t batch, int64_t 
   // keep the ring + staging tile within shared memory
   constexpr int STAGES = BN >= 256 ? 3 : 4;
   const size_t smem = STAGES * (GEMM_BM * GEMM_BK * 2 + BN * GEMM_BK * 2) + (size_t)GEMM_BM * (BN * sizeof(TC) + 16);
-  auto kern = bgemm_ws_kernel<BN, AM, BMN, STAGES, TC>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return cuda_status(e, "bgemm_ws attr");
-    attr_set = true;
-  }
+  // operands with plain strides (no split levels) take the TMA producer (128-byte swizzled tiles)
+  CUtensorMap ta, tb;
+  memset(&ta, 0, sizeof(ta));
+  memset(&tb, 0, sizeof(tb));
+  static const bool tma_off = [] { const char* e = getenv("EVO_BGEMM_NO_TMA"); return e && e[0] == '1'; }();
+  const bool tma = !tma_off && (AM ? tma_map_mnmajor(&ta, A, M, K, batch) : tma_map_kmajor(&ta, A, M, K, batch, GEMM_BM)) &&
+                   (BMN ? tma_map_mnmajor(&tb, B, N, K, batch) : tma_map_kmajor(&tb, B, N, K, batch, BN));
   const int64_t tiles = ((M + GEMM_BM - 1) / GEMM_BM) * ((N + BN - 1) / BN) * batch * splits;
   const int64_t grid = tiles < sm_count() ? tiles : sm_count();
-  kern<<<(unsigned)grid, WS_GEMM_THREADS, smem, st>>>(A, B, C, (uint32_t)M, (uint32_t)N, (uint32_t)K, alpha, beta, c_mode, splits,
-                                          splits > 1 ? ws : nullptr, (int)batch);
+  auto run = [&](auto kern, bool& attr_set) -> int {
+    if (!attr_set) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return cuda_status(e, "bgemm_ws attr");
+      attr_set = true;
+    }
+    kern<<<(unsigned)grid, WS_GEMM_THREADS, smem, st>>>(A, B, C, (uint32_t)M, (uint32_t)N, (uint32_t)K, alpha, beta,
+                                                        c_mode, splits, splits > 1 ? ws : nullptr, (int)batch, ta, tb);
+    return EVO_OK;
+  };
+  static bool attr_plain = false, attr_tma = false;
+  int rc;
+  if (tma) rc = run(bgemm_ws_kernel<BN, AM, BMN, STAGES, TC, true>, attr_tma);
+  else rc = run(bgemm_ws_kernel<BN, AM, BMN, STAGES, TC, false>, attr_plain);
+  if (rc) return rc;
   EVO_LAUNCH_CHECK("bgemm_ws launch");
   if (splits > 1) {
     const bool rows_contig = C.lo0 == 1 && C.split0 % 8 == 0 && M % 8 == 0;
