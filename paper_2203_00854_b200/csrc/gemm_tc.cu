@@ -382,13 +382,42 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
-                                            uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
-      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-      : "memory");
+__device__ __forceinline__ void tma_ld3(uint32_t dst, uint64_t m, int c0, int c1, int c2, uint32_t b) {
+  asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
+               ::"r"(dst), "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(b) : "memory");
 }
+__device__ __forceinline__ void tma_ld4(uint32_t dst, uint64_t m, int c0, int c1, int c2, int c3, uint32_t b) {
+  asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];\n"
+               ::"r"(dst), "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(b) : "memory");
+}
+__device__ __forceinline__ void tma_ld5(uint32_t dst, uint64_t m, int c0, int c1, int c2, int c3, int c4, uint32_t b) {
+  asm volatile("cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n"
+               ::"r"(dst), "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(b) : "memory");
+}
+
+// How the producer addresses one operand's tensor map.  The map's dims are, in order: the
+// contiguous dim (K for K-major, rows for MN-major) as [lo] or [lo = 32, hi], the other dim
+// as [lo] or [lo = split, hi], then [batch] (MatArg's two-level addressing, e.g. the OPM
+// [i][j][p][q] layout, maps onto dims of the tensor map).
+struct TmaOp {
+  int nd, c2, o2, batched;
+  int split_o;
+};
+// issue the box whose contiguous-dim start is cs and other-dim start is os (coordinates stay in
+// registers: the producer is a single thread, so no local-memory coordinate arrays).  Maps are
+// always >= 3-D (a unit batch dim is kept for 1-level operands).
+__device__ __forceinline__ void tma_issue(const TmaOp& op, uint32_t dst, const CUtensorMap* map, int cs, int os, int b,
+                                          uint64_t* bar) {
+  const uint64_t m = reinterpret_cast<uint64_t>(map);
+  const uint32_t br = smem_u32(bar);
+  const int cl = op.c2 ? (cs & 31) : cs, ch = cs >> 5;
+  const int ol = op.o2 ? os % op.split_o : os, oh = op.o2 ? os / op.split_o : 0;
+  if (!op.c2 && !op.o2) tma_ld3(dst, m, cl, ol, b, br);
+  else if (op.c2 && !op.o2) tma_ld4(dst, m, cl, ch, ol, b, br);
+  else if (!op.c2 && op.o2) tma_ld4(dst, m, cl, ol, oh, b, br);
+  else tma_ld5(dst, m, cl, ch, ol, oh, b, br);
+}
+
 // MN-major SWIZZLE_128B descriptor: tile = (rows/64) TMA boxes of [64 k][64 mn] (8 KB each);
 // LBO = 8 KB (next 64-element MN atom), SBO = 1 KB (next 8 k rows)
 __device__ __forceinline__ uint64_t make_sdesc_sw128_mn(uint32_t saddr) {
@@ -410,6 +439,33 @@ __device__ __forceinline__ uint64_t make_sdesc_sw128(uint32_t saddr) {
   d |= (uint64_t)2 << 61;  // layout SWIZZLE_128B
   return d;
 }
+// SWIZZLE_64B variants for operands whose contiguous dim comes in 32-element (64 B) runs:
+// K-major: [rows][32 k] blocks, 8-row atoms of 512 B (SBO); MN-major: [64 k][32 mn] atoms
+// of 4 KB (LBO) with 8 k rows = 512 B (SBO)
+__device__ __forceinline__ uint64_t make_sdesc_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)4 << 61;  // layout SWIZZLE_64B
+  return d;
+}
+__device__ __forceinline__ uint64_t make_sdesc_sw64_mn(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)(4096 >> 4) << 16;
+  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)4 << 61;
+  return d;
+}
+// descriptor of K-step kk (16 k) of an operand tile of `rows` rows at `base`
+__device__ __forceinline__ uint64_t tma_desc(bool mn, bool sw64, uint32_t base, int kk, int rows) {
+  if (!sw64) return mn ? make_sdesc_sw128_mn(base + kk * 2048) : make_sdesc_sw128(base + kk * 32);
+  if (mn) return make_sdesc_sw64_mn(base + kk * 1024);
+  return make_sdesc_sw64(base + (kk >> 1) * rows * 64 + (kk & 1) * 32);
+}
 
 constexpr int WS_EPI_WARPS = 4;  // one epilogue warp per TMEM lane quarter (8 measured no faster)
 constexpr int WS_GEMM_THREADS = 160 + 32 * WS_EPI_WARPS;  // 4 producer warps + MMA warp + epilogue
@@ -419,7 +475,8 @@ __global__ void __launch_bounds__(WS_GEMM_THREADS, 1) bgemm_ws_kernel(MatArg A, 
                                                           uint32_t K, float alpha, float beta, int c_mode, int splits,
                                                           float* __restrict__ ws, int batch,
                                                           const __grid_constant__ CUtensorMap tmA,
-                                                          const __grid_constant__ CUtensorMap tmB) {
+                                                          const __grid_constant__ CUtensorMap tmB, TmaOp opA,
+                                                          TmaOp opB) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
   __shared__ uint32_t tmem_sh;
@@ -479,19 +536,38 @@ __global__ void __launch_bounds__(WS_GEMM_THREADS, 1) bgemm_ws_kernel(MatArg A, 
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], A_BYTES + B_BYTES);
           const int k0 = (kt0 + kt) * GEMM_BK;
+          // 128-byte swizzle: MN-major one [64 k][64 mn] box per 64 rows, K-major one box;
+          // 64-byte swizzle (32-element runs): MN-major one [64 k][32 mn] box per 32 rows,
+          // K-major one [rows][32 k] box per 32 k
           if constexpr (A_MN) {
+            if (opA.c2) {
+              for (int j = 0; j < GEMM_BM / 32; ++j)
+                tma_issue(opA, sA + stage * A_BYTES + j * 4096, &tmA, (int)m0 + 32 * j, k0, (int)b, &full[stage]);
+            } else {
 #pragma unroll
-            for (int j = 0; j < GEMM_BM / 64; ++j)
-              tma_load_3d(sA + stage * A_BYTES + j * 8192, &tmA, (int)m0 + 64 * j, k0, (int)b, &full[stage]);
+              for (int j = 0; j < GEMM_BM / 64; ++j)
+                tma_issue(opA, sA + stage * A_BYTES + j * 8192, &tmA, (int)m0 + 64 * j, k0, (int)b, &full[stage]);
+            }
+          } else if (opA.c2) {
+            for (int j = 0; j < 2; ++j)
+              tma_issue(opA, sA + stage * A_BYTES + j * GEMM_BM * 64, &tmA, k0 + 32 * j, (int)m0, (int)b, &full[stage]);
           } else {
-            tma_load_3d(sA + stage * A_BYTES, &tmA, k0, (int)m0, (int)b, &full[stage]);
+            tma_issue(opA, sA + stage * A_BYTES, &tmA, k0, (int)m0, (int)b, &full[stage]);
           }
           if constexpr (B_MN) {
+            if (opB.c2) {
+              for (int j = 0; j < BN / 32; ++j)
+                tma_issue(opB, sB + stage * B_BYTES + j * 4096, &tmB, (int)n0 + 32 * j, k0, (int)b, &full[stage]);
+            } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              tma_load_3d(sB + stage * B_BYTES + j * 8192, &tmB, (int)n0 + 64 * j, k0, (int)b, &full[stage]);
+              for (int j = 0; j < BN / 64; ++j)
+                tma_issue(opB, sB + stage * B_BYTES + j * 8192, &tmB, (int)n0 + 64 * j, k0, (int)b, &full[stage]);
+            }
+          } else if (opB.c2) {
+            for (int j = 0; j < 2; ++j)
+              tma_issue(opB, sB + stage * B_BYTES + j * BN * 64, &tmB, k0 + 32 * j, (int)n0, (int)b, &full[stage]);
           } else {
-            tma_load_3d(sB + stage * B_BYTES, &tmB, k0, (int)n0, (int)b, &full[stage]);
+            tma_issue(opB, sB + stage * B_BYTES, &tmB, k0, (int)n0, (int)b, &full[stage]);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -547,11 +623,9 @@ __global__ void __launch_bounds__(WS_GEMM_THREADS, 1) bgemm_ws_kernel(MatArg A, 
 #pragma unroll
           for (int kk = 0; kk < GEMM_BK / 16; ++kk) {
             uint64_t ad, bd;
-            if constexpr (TMA) {  // K = 16 step: 32 B along K-major rows / 16 k rows (2 KB) MN-major
-              ad = A_MN ? make_sdesc_sw128_mn(sA + stage * A_BYTES + kk * 2048)
-                        : make_sdesc_sw128(sA + stage * A_BYTES + kk * 32);
-              bd = B_MN ? make_sdesc_sw128_mn(sB + stage * B_BYTES + kk * 2048)
-                        : make_sdesc_sw128(sB + stage * B_BYTES + kk * 32);
+            if constexpr (TMA) {
+              ad = tma_desc(A_MN, opA.c2, sA + stage * A_BYTES, kk, GEMM_BM);
+              bd = tma_desc(B_MN, opB.c2, sB + stage * B_BYTES, kk, BN);
             } else {
               ad = make_sdesc(sA + stage * A_BYTES + kk * 2 * (GEMM_BM / 8) * 128, (GEMM_BM / 8) * 128, 128);
               bd = make_sdesc(sB + stage * B_BYTES + kk * 2 * (BN / 8) * 128, (BN / 8) * 128, 128);
@@ -767,36 +841,62 @@ static EncodeTiledFn encode_tiled() {
   return fn;
 }
 
-// K-major operand with plain [batch][rows][K] addressing (no split levels) -> 3-D map with a
-// {64 k, box_rows rows, 1} box and the 128-byte swizzle
-static bool tma_map_kmajor(CUtensorMap* map, const MatArg& a, int64_t rows, int64_t K, int64_t batch, int box_rows) {
+// Tensor map of one operand (rows = M or N extent).  K-major: box [box_rows][64 k];
+// MN-major: box [64 k][64 rows] (128-byte swizzle).  The contiguous dim may be plain (one run)
+// or two-level with runs of exactly 32 elements (64 B: 64-byte swizzle, one box per run); the
+// other dim may be plain or two-level with a split dividing the box extent.  Returns false (-> cp.async
+// producer) for anything else.
+static bool tma_map(CUtensorMap* map, TmaOp* op, const MatArg& a, bool mn_major, int64_t rows, int64_t K,
+                    int64_t batch, int box_rows) {
   EncodeTiledFn enc = encode_tiled();
-  if (!enc) return false;
-  if (!(a.lo1 == 1 && a.split1 >= (uint32_t)K && a.split0 >= (uint32_t)rows)) return false;
-  if ((a.lo0 * 2) % 16 || (batch > 1 && (a.bs * 2) % 16) || ((uintptr_t)a.ptr & 15) || K % 8) return false;
-  cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)batch};
-  cuuint64_t strides[2] = {(cuuint64_t)a.lo0 * 2, (cuuint64_t)(batch > 1 ? a.bs * 2 : a.lo0 * 2 * rows)};
-  cuuint32_t box[3] = {(cuuint32_t)GEMM_BK, (cuuint32_t)box_rows, 1};
-  cuuint32_t es[3] = {1, 1, 1};
-  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<char*>(a.ptr), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-// MN-major operand with plain [batch][K][rows] addressing -> 3-D map {rows, K, batch} with a
-// {64 mn, 64 k, 1} box (one 128-byte swizzle atom column)
-static bool tma_map_mnmajor(CUtensorMap* map, const MatArg& a, int64_t rows, int64_t K, int64_t batch) {
-  EncodeTiledFn enc = encode_tiled();
-  if (!enc) return false;
-  if (!(a.lo0 == 1 && a.split0 >= (uint32_t)rows && a.split1 >= (uint32_t)K)) return false;
-  if ((a.lo1 * 2) % 16 || (batch > 1 && (a.bs * 2) % 16) || ((uintptr_t)a.ptr & 15) || rows % 8) return false;
-  cuuint64_t dims[3] = {(cuuint64_t)rows, (cuuint64_t)K, (cuuint64_t)batch};
-  cuuint64_t strides[2] = {(cuuint64_t)a.lo1 * 2, (cuuint64_t)(batch > 1 ? a.bs * 2 : a.lo1 * 2 * K)};
-  cuuint32_t box[3] = {64, (cuuint32_t)GEMM_BK, 1};
-  cuuint32_t es[3] = {1, 1, 1};
-  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<char*>(a.ptr), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  if (!enc || ((uintptr_t)a.ptr & 15)) return false;
+  // contiguous (c) and other (o) dims of the MatArg
+  const int64_t ext_c = mn_major ? rows : K, ext_o = mn_major ? K : rows;
+  const uint32_t split_c = mn_major ? a.split0 : a.split1, split_o = mn_major ? a.split1 : a.split0;
+  const int64_t lo_c = mn_major ? a.lo0 : a.lo1, hi_c = mn_major ? a.hi0 : a.hi1;
+  const int64_t lo_o = mn_major ? a.lo1 : a.lo0, hi_o = mn_major ? a.hi1 : a.hi0;
+  const int box_o = mn_major ? GEMM_BK : box_rows;
+  if (lo_c != 1) return false;
+  cuuint64_t dims[5], strides[4];
+  cuuint32_t box[5], es[5] = {1, 1, 1, 1, 1};
+  int nd = 0;
+  auto stride_ok = [](int64_t el) { return el > 0 && (el * 2) % 16 == 0 && el * 2 < (1LL << 40); };
+  TmaOp o{};
+  if ((int64_t)split_c >= ext_c) {
+    dims[nd] = (cuuint64_t)ext_c; box[nd] = 64; ++nd;
+  } else if (split_c == 32 && ext_c % 32 == 0 && stride_ok(hi_c)) {  // 64-byte runs: SWIZZLE_64B boxes
+    dims[nd] = 32; box[nd] = 32; ++nd;
+    dims[nd] = (cuuint64_t)(ext_c / 32); strides[nd - 1] = (cuuint64_t)hi_c * 2; box[nd] = 1; ++nd;
+    o.c2 = 1;
+  } else {
+    return false;
+  }
+  if ((int64_t)split_o >= ext_o) {
+    if (!stride_ok(lo_o)) return false;
+    dims[nd] = (cuuint64_t)ext_o; strides[nd - 1] = (cuuint64_t)lo_o * 2; box[nd] = (cuuint32_t)box_o; ++nd;
+    o.split_o = 1 << 30;
+  } else if (box_o % split_o == 0 && ext_o % split_o == 0 && stride_ok(lo_o) && stride_ok(hi_o)) {
+    dims[nd] = split_o; strides[nd - 1] = (cuuint64_t)lo_o * 2; box[nd] = split_o; ++nd;
+    dims[nd] = (cuuint64_t)(ext_o / split_o); strides[nd - 1] = (cuuint64_t)hi_o * 2;
+    box[nd] = (cuuint32_t)(box_o / split_o); ++nd;
+    o.o2 = 1;
+    o.split_o = (int)split_o;
+  } else {
+    return false;
+  }
+  // batch dim always present (unit extent when batch == 1) so every map is 3-, 4- or 5-D
+  if (batch > 1 && !stride_ok(a.bs)) return false;
+  dims[nd] = (cuuint64_t)batch;
+  strides[nd - 1] = batch > 1 ? (cuuint64_t)a.bs * 2 : strides[nd - 2] * (cuuint64_t)dims[nd - 1];
+  box[nd] = 1;
+  ++nd;
+  o.batched = 1;
+  if (nd < 3 || nd > 5) return false;
+  o.nd = nd;
+  *op = o;
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, (cuuint32_t)nd, const_cast<char*>(a.ptr), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, o.c2 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 template <int BN, bool AM, bool BMN, typename TC>
@@ -806,13 +906,13 @@ static int launch_bgemm_ws(MatArg A, MatArg B, MatArg C, int64_t batch, int64_t 
   // keep the ring + staging tile within shared memory
   constexpr int STAGES = BN >= 256 ? 3 : 4;
   const size_t smem = STAGES * (GEMM_BM * GEMM_BK * 2 + BN * GEMM_BK * 2) + (size_t)GEMM_BM * (BN * sizeof(TC) + 16);
-  // operands with plain strides (no split levels) take the TMA producer (128-byte swizzled tiles)
+  // operands whose addressing maps onto a tensor map take the TMA producer (128-byte swizzle)
   CUtensorMap ta, tb;
   memset(&ta, 0, sizeof(ta));
   memset(&tb, 0, sizeof(tb));
   static const bool tma_off = [] { const char* e = getenv("EVO_BGEMM_NO_TMA"); return e && e[0] == '1'; }();
-  const bool tma = !tma_off && (AM ? tma_map_mnmajor(&ta, A, M, K, batch) : tma_map_kmajor(&ta, A, M, K, batch, GEMM_BM)) &&
-                   (BMN ? tma_map_mnmajor(&tb, B, N, K, batch) : tma_map_kmajor(&tb, B, N, K, batch, BN));
+  TmaOp oa{}, ob{};
+  const bool tma = !tma_off && tma_map(&ta, &oa, A, AM, M, K, batch, GEMM_BM) && tma_map(&tb, &ob, B, BMN, N, K, batch, BN);
   const int64_t tiles = ((M + GEMM_BM - 1) / GEMM_BM) * ((N + BN - 1) / BN) * batch * splits;
   const int64_t grid = tiles < sm_count() ? tiles : sm_count();
   auto run = [&](auto kern, bool& attr_set) -> int {
@@ -822,7 +922,8 @@ static int launch_bgemm_ws(MatArg A, MatArg B, MatArg C, int64_t batch, int64_t 
       attr_set = true;
     }
     kern<<<(unsigned)grid, WS_GEMM_THREADS, smem, st>>>(A, B, C, (uint32_t)M, (uint32_t)N, (uint32_t)K, alpha, beta,
-                                                        c_mode, splits, splits > 1 ? ws : nullptr, (int)batch, ta, tb);
+                                                        c_mode, splits, splits > 1 ? ws : nullptr, (int)batch, ta, tb,
+                                                        oa, ob);
     return EVO_OK;
   };
   static bool attr_plain = false, attr_tma = false;

@@ -162,6 +162,31 @@ def test_bgemm_opm_layout():
     assert rel(o, ref) < 1e-2
 
 
+@pytest.mark.parametrize("S,R,P", [(64, 48, 16), (64, 64, 32)])
+def test_bgemm_opm_fwd_bwd_layouts(S, R, P):
+    """the three OPM contractions with block.py's exact views; P = 32 takes the TMA path with
+    64-byte swizzled boxes (32-element runs), P = 16 the cp.async path"""
+    g = torch.Generator(device=DEV).manual_seed(11)
+    ab = _mk((S * R, 2 * P), g)
+    a3, b3 = ab.view(S, R, 2 * P)[..., :P].float(), ab.view(S, R, 2 * P)[..., P:].float()
+    o = torch.empty(R, R, P, P, device=DEV, dtype=torch.bfloat16)
+    ops.bgemm(Mat(ab, lo=(1, R * 2 * P), split=(P, 0), hi=(2 * P, 0)),
+              Mat(ab, lo=(1, R * 2 * P), split=(P, 0), hi=(2 * P, 0), offset=P),
+              Mat(o, lo=(P, 1), split=(P, P), hi=(R * P * P, P * P)), 1, R * P, R * P, S, alpha=1.0 / S)
+    assert rel(o, torch.einsum("sip,sjq->ijpq", a3, b3) / S) < 1e-2
+    do = _mk((R * R, P * P), g)
+    do4 = do.view(R, R, P, P).float()
+    dab = torch.zeros(S * R, 2 * P, device=DEV, dtype=torch.bfloat16)
+    ops.bgemm(Mat(do, lo=(P, 1), split=(P, P), hi=(R * P * P, P * P)),
+              Mat(ab, lo=(R * 2 * P, 1), split=(0, P), hi=(0, 2 * P), offset=P),
+              Mat(dab, lo=(1, R * 2 * P), split=(P, 0), hi=(2 * P, 0)), 1, R * P, S, R * P, alpha=1.0 / S)
+    assert rel(dab.view(S, R, 2 * P)[..., :P], torch.einsum("ijpq,sjq->sip", do4, b3) / S) < 1e-2
+    ops.bgemm(Mat(do, lo=(1, P), split=(P, P), hi=(P * P, R * P * P)),
+              Mat(ab, lo=(R * 2 * P, 1), split=(0, P), hi=(0, 2 * P)),
+              Mat(dab, lo=(1, R * 2 * P), split=(P, 0), hi=(2 * P, 0), offset=P), 1, R * P, S, R * P, alpha=1.0 / S)
+    assert rel(dab.view(S, R, 2 * P)[..., P:], torch.einsum("ijpq,sip->sjq", do4, a3) / S) < 1e-2
+
+
 def _attn_ref(q, k, v, g, bias, scale):
     # q,k,v,g: [B, H, L, c] fp32; bias broadcastable to [B, H, L, L]
     s = q @ k.transpose(-1, -2)
