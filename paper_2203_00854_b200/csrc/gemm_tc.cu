@@ -400,7 +400,11 @@ __device__ __forceinline__ void tma_ld5(uint32_t dst, uint64_t m, int c0, int c1
 // as [lo] or [lo = split, hi], then [batch] (MatArg's two-level addressing, e.g. the OPM
 // [i][j][p][q] layout, maps onto dims of the tensor map).
 struct TmaOp {
-  int nd, c2, o2, batched;
+  int c2;       // contiguous dim in 32-element runs (64-byte swizzle)
+  int chi;      // the map has a contiguous-hi dim (placed after the other dim): the whole stage
+                // tile is ONE box; otherwise one box per 64-row atom (MN-major, ragged rows)
+  int cw;       // contiguous-lo width of the map (32 or 64, or the full extent when !chi)
+  int o2;       // other dim two-level
   int split_o;
 };
 // issue the box whose contiguous-dim start is cs and other-dim start is os (coordinates stay in
@@ -408,14 +412,15 @@ struct TmaOp {
 // always >= 3-D (a unit batch dim is kept for 1-level operands).
 __device__ __forceinline__ void tma_issue(const TmaOp& op, uint32_t dst, const CUtensorMap* map, int cs, int os, int b,
                                           uint64_t* bar) {
+  // map dims: [c_lo, o_lo, (o_hi), (c_hi), batch]
   const uint64_t m = reinterpret_cast<uint64_t>(map);
   const uint32_t br = smem_u32(bar);
-  const int cl = op.c2 ? (cs & 31) : cs, ch = cs >> 5;
+  const int cl = op.chi ? cs % op.cw : cs, ch = op.chi ? cs / op.cw : 0;
   const int ol = op.o2 ? os % op.split_o : os, oh = op.o2 ? os / op.split_o : 0;
-  if (!op.c2 && !op.o2) tma_ld3(dst, m, cl, ol, b, br);
-  else if (op.c2 && !op.o2) tma_ld4(dst, m, cl, ch, ol, b, br);
-  else if (!op.c2 && op.o2) tma_ld4(dst, m, cl, ol, oh, b, br);
-  else tma_ld5(dst, m, cl, ch, ol, oh, b, br);
+  if (!op.o2 && !op.chi) tma_ld3(dst, m, cl, ol, b, br);
+  else if (!op.o2) tma_ld4(dst, m, cl, ol, ch, b, br);
+  else if (!op.chi) tma_ld4(dst, m, cl, ol, oh, b, br);
+  else tma_ld5(dst, m, cl, ol, oh, ch, b, br);
 }
 
 // MN-major SWIZZLE_128B descriptor: tile = (rows/64) TMA boxes of [64 k][64 mn] (8 KB each);
@@ -536,38 +541,22 @@ __global__ void __launch_bounds__(WS_GEMM_THREADS, 1) bgemm_ws_kernel(MatArg A, 
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], A_BYTES + B_BYTES);
           const int k0 = (kt0 + kt) * GEMM_BK;
-          // 128-byte swizzle: MN-major one [64 k][64 mn] box per 64 rows, K-major one box;
-          // 64-byte swizzle (32-element runs): MN-major one [64 k][32 mn] box per 32 rows,
-          // K-major one [rows][32 k] box per 32 k
-          if constexpr (A_MN) {
-            if (opA.c2) {
-              for (int j = 0; j < GEMM_BM / 32; ++j)
-                tma_issue(opA, sA + stage * A_BYTES + j * 4096, &tmA, (int)m0 + 32 * j, k0, (int)b, &full[stage]);
-            } else {
-#pragma unroll
-              for (int j = 0; j < GEMM_BM / 64; ++j)
-                tma_issue(opA, sA + stage * A_BYTES + j * 8192, &tmA, (int)m0 + 64 * j, k0, (int)b, &full[stage]);
-            }
-          } else if (opA.c2) {
-            for (int j = 0; j < 2; ++j)
-              tma_issue(opA, sA + stage * A_BYTES + j * GEMM_BM * 64, &tmA, k0 + 32 * j, (int)m0, (int)b, &full[stage]);
+          // one box per operand and stage when the map has a contiguous-hi dim (the box then
+          // spans the atoms: [atom][64 k][mn run] MN-major, [k run][rows][32 k] K-major);
+          // otherwise MN-major tiles take one [64 k][64 mn] box per 64 rows
+          if (!A_MN || opA.chi) {
+            tma_issue(opA, sA + stage * A_BYTES, &tmA, A_MN ? (int)m0 : k0, A_MN ? k0 : (int)m0, (int)b, &full[stage]);
           } else {
-            tma_issue(opA, sA + stage * A_BYTES, &tmA, k0, (int)m0, (int)b, &full[stage]);
+#pragma unroll
+            for (int j = 0; j < GEMM_BM / 64; ++j)
+              tma_issue(opA, sA + stage * A_BYTES + j * 8192, &tmA, (int)m0 + 64 * j, k0, (int)b, &full[stage]);
           }
-          if constexpr (B_MN) {
-            if (opB.c2) {
-              for (int j = 0; j < BN / 32; ++j)
-                tma_issue(opB, sB + stage * B_BYTES + j * 4096, &tmB, (int)n0 + 32 * j, k0, (int)b, &full[stage]);
-            } else {
-#pragma unroll
-              for (int j = 0; j < BN / 64; ++j)
-                tma_issue(opB, sB + stage * B_BYTES + j * 8192, &tmB, (int)n0 + 64 * j, k0, (int)b, &full[stage]);
-            }
-          } else if (opB.c2) {
-            for (int j = 0; j < 2; ++j)
-              tma_issue(opB, sB + stage * B_BYTES + j * BN * 64, &tmB, k0 + 32 * j, (int)n0, (int)b, &full[stage]);
+          if (!B_MN || opB.chi) {
+            tma_issue(opB, sB + stage * B_BYTES, &tmB, B_MN ? (int)n0 : k0, B_MN ? k0 : (int)n0, (int)b, &full[stage]);
           } else {
-            tma_issue(opB, sB + stage * B_BYTES, &tmB, k0, (int)n0, (int)b, &full[stage]);
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              tma_issue(opB, sB + stage * B_BYTES + j * 8192, &tmB, (int)n0 + 64 * j, k0, (int)b, &full[stage]);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -855,22 +844,30 @@ static bool tma_map(CUtensorMap* map, TmaOp* op, const MatArg& a, bool mn_major,
   const uint32_t split_c = mn_major ? a.split0 : a.split1, split_o = mn_major ? a.split1 : a.split0;
   const int64_t lo_c = mn_major ? a.lo0 : a.lo1, hi_c = mn_major ? a.hi0 : a.hi1;
   const int64_t lo_o = mn_major ? a.lo1 : a.lo0, hi_o = mn_major ? a.hi1 : a.hi0;
-  const int box_o = mn_major ? GEMM_BK : box_rows;
+  const int box_o = mn_major ? GEMM_BK : box_rows;     // other-dim extent of one stage tile
+  const int tile_c = mn_major ? box_rows : GEMM_BK;    // contiguous-dim extent of one stage tile
   if (lo_c != 1) return false;
-  cuuint64_t dims[5], strides[4];
-  cuuint32_t box[5], es[5] = {1, 1, 1, 1, 1};
-  int nd = 0;
   auto stride_ok = [](int64_t el) { return el > 0 && (el * 2) % 16 == 0 && el * 2 < (1LL << 40); };
   TmaOp o{};
-  if ((int64_t)split_c >= ext_c) {
-    dims[nd] = (cuuint64_t)ext_c; box[nd] = 64; ++nd;
-  } else if (split_c == 32 && ext_c % 32 == 0 && stride_ok(hi_c)) {  // 64-byte runs: SWIZZLE_64B boxes
-    dims[nd] = 32; box[nd] = 32; ++nd;
-    dims[nd] = (cuuint64_t)(ext_c / 32); strides[nd - 1] = (cuuint64_t)hi_c * 2; box[nd] = 1; ++nd;
-    o.c2 = 1;
+  cuuint64_t cdim_lo, cdim_hi = 0, cstride_hi = 0;
+  cuuint32_t cbox_lo, cbox_hi = 1;
+  if ((int64_t)split_c >= ext_c) {                 // one run
+    if (mn_major && ext_c % 64 == 0) {             // split into 64-wide atoms, one box per tile
+      o.chi = 1; o.cw = 64;
+      cdim_lo = 64; cbox_lo = 64; cdim_hi = ext_c / 64; cstride_hi = 64; cbox_hi = tile_c / 64;
+    } else {
+      cdim_lo = ext_c; cbox_lo = 64; o.cw = 1 << 30;
+    }
+  } else if (split_c == 32 && ext_c % 32 == 0 && stride_ok(hi_c)) {  // 64-byte runs: SWIZZLE_64B
+    o.c2 = 1; o.chi = 1; o.cw = 32;
+    cdim_lo = 32; cbox_lo = 32; cdim_hi = ext_c / 32; cstride_hi = hi_c; cbox_hi = tile_c / 32;
   } else {
     return false;
   }
+  cuuint64_t dims[5], strides[4];
+  cuuint32_t box[5], es[5] = {1, 1, 1, 1, 1};
+  int nd = 0;
+  dims[nd] = cdim_lo; box[nd] = cbox_lo; ++nd;
   if ((int64_t)split_o >= ext_o) {
     if (!stride_ok(lo_o)) return false;
     dims[nd] = (cuuint64_t)ext_o; strides[nd - 1] = (cuuint64_t)lo_o * 2; box[nd] = (cuuint32_t)box_o; ++nd;
@@ -884,15 +881,17 @@ static bool tma_map(CUtensorMap* map, TmaOp* op, const MatArg& a, bool mn_major,
   } else {
     return false;
   }
+  if (o.chi) {
+    if (!stride_ok((int64_t)cstride_hi)) return false;
+    dims[nd] = cdim_hi; strides[nd - 1] = cstride_hi * 2; box[nd] = cbox_hi; ++nd;
+  }
   // batch dim always present (unit extent when batch == 1) so every map is 3-, 4- or 5-D
   if (batch > 1 && !stride_ok(a.bs)) return false;
   dims[nd] = (cuuint64_t)batch;
   strides[nd - 1] = batch > 1 ? (cuuint64_t)a.bs * 2 : strides[nd - 2] * (cuuint64_t)dims[nd - 1];
   box[nd] = 1;
   ++nd;
-  o.batched = 1;
   if (nd < 3 || nd > 5) return false;
-  o.nd = nd;
   *op = o;
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, (cuuint32_t)nd, const_cast<char*>(a.ptr), dims, strides, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, o.c2 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
