@@ -120,24 +120,39 @@ __global__ void __launch_bounds__(256) gated_residual_bwd_k(const T* __restrict_
 #pragma unroll
       for (int e = 0; e < 8; ++e) b[e] = bias[c + e];
     }
-    for (int64_t r = t.r0 + t.tr; r < t.r1; r += t.rpi) {
-      float d[8];
-      ld8<T>(dout + r * cols + c, d);
-      if (gp) {
-        float gv[8], yv[8], dg[8];
-        ld8<T>(gp + r * gp_rs + c, gv);
-        ld8<T>(y + r * y_rs + c, yv);
+    // two rows per step with all loads first (outputs may alias inputs)
+    int64_t r = t.r0 + t.tr;
+    for (; r < t.r1; r += 2 * t.rpi) {
+      const bool two = r + t.rpi < t.r1;
+      float d[2][8], gv[2][8], yv[2][8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          float s = sigmoidf_(gv[e]);
-          dg[e] = d[e] * (yv[e] + b[e]) * s * (1.f - s);
-          d[e] *= s;
+      for (int u = 0; u < 2; ++u) {
+        if (u == 1 && !two) break;
+        const int64_t ru = r + u * t.rpi;
+        ld8<T>(dout + ru * cols + c, d[u]);
+        if (gp) {
+          ld8<T>(gp + ru * gp_rs + c, gv[u]);
+          ld8<T>(y + ru * y_rs + c, yv[u]);
         }
-        st8<T>(dgp + r * dgp_rs + c, dg);
       }
-      if (dy) st8<T>(dy + r * cols + c, d);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc[e] += d[e];
+      for (int u = 0; u < 2; ++u) {
+        if (u == 1 && !two) break;
+        const int64_t ru = r + u * t.rpi;
+        if (gp) {
+          float dg[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            float s = sigmoidf_(gv[u][e]);
+            dg[e] = d[u][e] * (yv[u][e] + b[e]) * s * (1.f - s);
+            d[u][e] *= s;
+          }
+          st8<T>(dgp + ru * dgp_rs + c, dg);
+        }
+        if (dy) st8<T>(dy + ru * cols + c, d[u]);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] += d[u][e];
+      }
     }
   }
   if (dbias) col_flush(red, t, acc, cols, dbias);
@@ -152,14 +167,14 @@ __global__ void __launch_bounds__(256) colsum_k(const T* __restrict__ x, int64_t
   if (t.active()) {
     const int64_t c = t.tc * 8;
     int64_t r = t.r0 + t.tr;
-    for (; r + t.rpi < t.r1; r += 2 * t.rpi) {  // two rows in flight
-      float u[8], v[8];
-      ld8<T>(x + r * ld + c, u);
-      ld8<T>(x + (r + t.rpi) * ld + c, v);
+    for (; r + 3 * t.rpi < t.r1; r += 4 * t.rpi) {  // four rows in flight
+      float u[4][8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc[e] += u[e] + v[e];
+      for (int q = 0; q < 4; ++q) ld8<T>(x + (r + q * t.rpi) * ld + c, u[q]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += (u[0][e] + u[1][e]) + (u[2][e] + u[3][e]);
     }
-    if (r < t.r1) {
+    for (; r < t.r1; r += t.rpi) {
       float u[8];
       ld8<T>(x + r * ld + c, u);
 #pragma unroll
@@ -197,7 +212,29 @@ __global__ void __launch_bounds__(256) bias_act_bwd_k(const T* __restrict__ dh, 
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   if (t.active()) {
     const int64_t c = t.tc * 8;
-    for (int64_t r = t.r0 + t.tr; r < t.r1; r += t.rpi) {
+    // U rows per step with every load issued before the (possibly in-place) stores: dy may
+    // alias dh, so without this the compiler keeps one row in flight per thread
+    constexpr int U = 4;
+    int64_t r = t.r0 + t.tr;
+    for (; r + (U - 1) * t.rpi < t.r1; r += U * t.rpi) {
+      float d[U][8], hv[U][8];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        ld8<T>(dh + (r + u * t.rpi) * cols + c, d[u]);
+        if (act == 1) ld8<T>(h + (r + u * t.rpi) * cols + c, hv[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (act == 1) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) d[u][e] = hv[u][e] > 0.f ? d[u][e] : 0.f;
+        }
+        st8<T>(dy + (r + u * t.rpi) * cols + c, d[u]);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] += d[u][e];
+      }
+    }
+    for (; r < t.r1; r += t.rpi) {
       float d[8], hv[8];
       ld8<T>(dh + r * cols + c, d);
       if (act == 1) {
