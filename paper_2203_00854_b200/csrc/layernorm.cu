@@ -514,9 +514,20 @@ __global__ void __launch_bounds__(256) ln_fwd_thread(const TX* __restrict__ x, i
       q += v[c] * v[c];
     }
   const float rstd = rsqrtf(q / cols + eps);
+  if (sizeof(TY) == 2 && MAXC % 8 == 0 && cols == MAXC) {
+    // the row-major output row (MAXC bf16) as 16-byte stores instead of MAXC 2-byte ones
 #pragma unroll
-  for (int c = 0; c < MAXC; ++c)
-    if (c < cols) stf<TY>(y + row * cols + c, v[c] * rstd * gamma[c] + beta[c]);
+    for (int c = 0; c < MAXC; c += 8) {
+      float o[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] = v[c + e] * rstd * gamma[c + e] + beta[c + e];
+      store_row<TY, 8>(y + row * cols + c, o);
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c)
+      if (c < cols) stf<TY>(y + row * cols + c, v[c] * rstd * gamma[c] + beta[c]);
+  }
   if (mean_out) mean_out[row] = mu;
   if (rstd_out) rstd_out[row] = rstd;
 }
@@ -609,10 +620,16 @@ __global__ void __launch_bounds__(256) ln_bwd_thread(const TD* __restrict__ dy, 
     float xh[C], d[C];
     const float mu = mean[row], rs = rstd[row];
     float s1 = 0.f, s2 = 0.f;
+    if (sizeof(TD) == 2 && C % 8 == 0) {  // the row-major dy row as 16-byte loads
+#pragma unroll
+      for (int c = 0; c < C; c += 8) load_row<TD, 8>(dy + row * C + c, d + c);
+    } else {
+#pragma unroll
+      for (int c = 0; c < C; ++c) d[c] = ldf<TD>(dy + row * C + c);
+    }
 #pragma unroll
     for (int c = 0; c < C; ++c) {
       xh[c] = (ldf<TX>(x + row * x_rs + c * x_cs) - mu) * rs;
-      d[c] = ldf<TD>(dy + row * C + c);
       const float gd = gamma[c] * d[c];
       s1 += gd;
       s2 += gd * xh[c];
@@ -721,8 +738,14 @@ static int ln_fwd_impl(const void* x, int64_t x_rs, int64_t x_cs, const float* g
   }
   EVO_CHECK_ARG(cols <= 64, EVO_ERR_SHAPE, "layernorm: strided rows support cols <= 64 (got %lld)", (long long)cols);
   dim3 grid((unsigned)((rows + 255) / 256));
-  ln_fwd_thread<TX, TY, 64><<<grid, 256, 0, st>>>((const TX*)x, x_rs, x_cs, g, b, (TY*)y, mean, rstd, rows,
-                                                  (int)cols, eps);
+  // exact widths get the 16-byte row stores (cols == MAXC)
+#define LFT(MC) ln_fwd_thread<TX, TY, MC><<<grid, 256, 0, st>>>((const TX*)x, x_rs, x_cs, g, b, (TY*)y, mean, rstd, \
+                                                                rows, (int)cols, eps)
+  if (cols == 32) LFT(32);
+  else if (cols == 16) LFT(16);
+  else if (cols == 8) LFT(8);
+  else LFT(64);
+#undef LFT
   EVO_LAUNCH_CHECK("layernorm fwd strided");
   return EVO_OK;
 }
