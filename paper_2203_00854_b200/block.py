@@ -190,43 +190,42 @@ def attention_bwd(bp: BlockParams, sv: Saved, dx_new, next_db=None, db_done=Fals
 
 # ----------------------------------------------------------------------------- msa_row bias
 def msa_row_bias_fwd(bp: BlockParams, z2d, n_i: int, n_j: int | None = None, save=True):
-    """msa_row_bias (evoformer.py:201-207) -> bias[h][i][j] bf16, one fused kernel
-    (LayerNorm + n_head dot products per pair row).  n_i rows of z (an i-shard under DAP)."""
+    """msa_row_bias (evoformer.py:201-207) -> bias[h][i][j] bf16.  n_i rows of z (an i-shard
+    under DAP).  LN_z on the lane-group LayerNorm kernel, then the 8 (padded) head dots as one
+    GEMM producing the head-major layout directly: bias = W^T LN(z)^T  ([8, rows])."""
     cfg = bp.cfg
     n_j = n_i if n_j is None else n_j
-    nh, k = cfg.n_head_msa, bp.layout.rowdot_k
+    nh = cfg.n_head_msa
     rows = n_i * n_j
-    out = torch.empty(k, n_i, n_j, device=z2d.device, dtype=BF16)
-    ln = torch.empty(rows, cfg.h_pair, device=z2d.device, dtype=BF16) if save else None
-    mean = torch.empty(rows, device=z2d.device, dtype=F32) if save else None
-    rstd = torch.empty_like(mean) if save else None
-    ops.layernorm_rowdot_fwd(z2d, bp.f["msa_row.lnz_g"], bp.f["msa_row.lnz_b"], bp.f["msa_row.w_bias"], rows,
-                             cfg.h_pair, out, rows, ln_out=ln, mean=mean, rstd=rstd)
+    ln, mean, rstd = ops.layernorm_fwd(z2d, bp.f["msa_row.lnz_g"], bp.f["msa_row.lnz_b"], rows, cfg.h_pair)
+    if ln.is_cuda:
+        out = torch.mm(bp.h["msa_row.w_bias"].t(), ln.t())            # [8, rows] bf16
+    else:  # CPU host-logic tests (fake kernel backend)
+        out = (bp.f["msa_row.w_bias"].t() @ ln.float().t()).to(ln.dtype)
+    out = out.view(-1, n_i, n_j)
     sv = Saved(z=z2d, ln=ln, mean=mean, rstd=rstd) if save else None
     return out[:nh], sv
 
 
 def msa_row_bias_bwd(bp: BlockParams, sv: Saved, dbias, dz):
-    """dbias fp32 [nh, n_i, n_j]; accumulates into dz (bf16 [n_i*n_j, Hz]) in one fused pass
-    (w . dbias, LayerNorm backward, dW_bias, dgamma, dbeta)."""
+    """dbias fp32 [nh, n_i, n_j]; accumulates into dz (bf16 [n_i*n_j, Hz]):
+    d LN = dbias^T W^T (one K = nh GEMM), dW = LN^T dbias^T (side stream), LN backward with
+    the residual-stream accumulate and dgamma / dbeta fused."""
     cfg = bp.cfg
-    nh, Hz, k = cfg.n_head_msa, cfg.h_pair, bp.layout.rowdot_k
+    nh, Hz = cfg.n_head_msa, cfg.h_pair
     rows = dbias[0].numel()
-    if nh < k:  # zero-padded heads
-        full = torch.zeros(k, rows, device=dbias.device, dtype=F32)
-        full[:nh].copy_(dbias.reshape(nh, rows))
-        dbias = full
-    db2 = dbias.reshape(k, rows)
+    db2 = dbias.reshape(nh, rows)
+    w = bp.f["msa_row.w_bias"][:, :nh]                                   # fp32 [Hz, nh]
     if not dz.is_cuda:  # CPU host-logic tests (fake kernel backend)
-        w = bp.f["msa_row.w_bias"]
         dln = db2.t() @ w.t()
-        bp.g["msa_row.w_bias"] += sv["ln"].float().t() @ db2.t()
-        ops.layernorm_bwd(dln, sv["z"], bp.f["msa_row.lnz_g"], sv["mean"], sv["rstd"], rows, Hz, dx=dz,
-                          accumulate=True, dgamma=bp.g["msa_row.lnz_g"], dbeta=bp.g["msa_row.lnz_b"])
-        return
-    ops.layernorm_rowdot_bwd(sv["z"], bp.f["msa_row.lnz_g"], bp.f["msa_row.lnz_b"], bp.f["msa_row.w_bias"], db2,
-                             rows, sv["mean"], sv["rstd"], rows, Hz, dz, dz, bp.g["msa_row.lnz_g"],
-                             bp.g["msa_row.lnz_b"], bp.g["msa_row.w_bias"])
+        bp.g["msa_row.w_bias"][:, :nh] += sv["ln"].float().t() @ db2.t()
+    else:
+        dln = torch.mm(db2.t(), w.t())                                  # fp32 [rows, Hz]
+        db2h = db2.to(torch.bfloat16)
+        gw = bp.g["msa_row.w_bias"]
+        SideStream.run(lambda: gw[:, :nh].add_(torch.mm(sv["ln"].t(), db2h.t(), out_dtype=F32)), sv["ln"], db2h)
+    ops.layernorm_bwd(dln, sv["z"], bp.f["msa_row.lnz_g"], sv["mean"], sv["rstd"], rows, Hz, dx=dz,
+                      accumulate=True, dgamma=bp.g["msa_row.lnz_g"], dbeta=bp.g["msa_row.lnz_b"])
 
 
 # ----------------------------------------------------------------------------- transition
