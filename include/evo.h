@@ -85,6 +85,15 @@ int evo_layernorm_rowdot_bwd(const void* x, int x_dtype, const float* gamma, con
                              const float* mean, const float* rstd, const void* res, void* dx,
                              float* dgamma, float* dbeta, float* dw, int64_t rows, int64_t cols, void* stream);
 
+/* Residual epilogue fused with the NEXT module's LayerNorm (bf16 only, cols 32/64/128/256):
+ *   out = res + [sigmoid(gp) *] (y + bias)      (evoformer.py:316-324 residual adds; gp may be NULL)
+ *   ln  = LayerNorm(out) with gamma/beta, mean/rstd saved (engine.py:206-217; stats of the
+ *         bf16-rounded out, exactly what a separate evo_layernorm_fwd of out would see)   */
+int evo_residual_layernorm_fwd(const void* res, const void* y, int64_t y_rs, const float* bias,
+                               const void* gp, int64_t gp_rs, void* out, const float* gamma,
+                               const float* beta, void* ln, float* mean, float* rstd, int64_t rows,
+                               int64_t cols, float eps, void* stream);
+
 /* ------------------------------------------------------------------ fused softmax
  * Replaces engine.fused_softmax_mask_bias_raw (engine.py:193-203) and the block's
  * softmax (evoformer.py:186-190):  y = softmax((x + bias) * scale + mask) over the

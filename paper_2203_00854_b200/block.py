@@ -90,6 +90,32 @@ class Saved(dict):
     """activations saved by a forward for its backward"""
 
 
+class LnChain:
+    """The next module's LayerNorm parameters handed to a module's residual epilogue: the
+    residual add and that LayerNorm run as one kernel (evo_residual_layernorm_fwd) and the
+    result (ln, mean, rstd) is picked up by the next module instead of recomputing it."""
+
+    def __init__(self, gamma, beta):
+        self.gamma, self.beta, self.result = gamma, beta, None
+
+
+def _layernorm_in(x2d, gamma, beta, rows, cols, pre_ln):
+    """the module's input LayerNorm: the chained result when the previous epilogue made it"""
+    if pre_ln is not None and pre_ln.result is not None:
+        return pre_ln.result
+    return ops.layernorm_fwd(x2d, gamma, beta, rows, cols)
+
+
+def _residual_out(res, y, bias, rows, cols, next_ln, gp=None, gp_rs=0):
+    """residual epilogue, fused with the next module's LayerNorm when chained"""
+    if next_ln is not None and res.is_cuda and cols in (32, 64, 128, 256):
+        out, ln, mean, rstd = ops.residual_layernorm_fwd(res, y, bias, rows, cols, next_ln.gamma, next_ln.beta, gp=gp,
+                                                         gp_rs=gp_rs)
+        next_ln.result = (ln, mean, rstd)
+        return out
+    return ops.gated_residual_fwd(res, y, bias, rows, cols, gp=gp, gp_rs=gp_rs)
+
+
 # ----------------------------------------------------------------------------- attention
 def _attn_geometry(kind: str, B: int, L: int):
     """rows of the [rows, C] view for attention batch b / position l:
@@ -97,7 +123,8 @@ def _attn_geometry(kind: str, B: int, L: int):
     return (L, 1) if kind == "row" else (1, B)
 
 
-def attention_fwd(bp: BlockParams, mod: str, x2d, B: int, L: int, kind: str, bias=None, save=True):
+def attention_fwd(bp: BlockParams, mod: str, x2d, B: int, L: int, kind: str, bias=None, save=True, pre_ln=None,
+                  next_ln=None):
     """_attention_core (evoformer.py:173-198) + residual: returns x + attn(x).
 
     kind "row": attention along the second axis of [B, L, C]; "col": x2d is
@@ -109,7 +136,7 @@ def attention_fwd(bp: BlockParams, mod: str, x2d, B: int, L: int, kind: str, bia
     H, nh, c, ldq = a["H"], a["nh"], a["c"], a["ldq"]
     rows = B * L
     h, f = bp.h, bp.f
-    ln, mean, rstd = ops.layernorm_fwd(x2d, f[f"{mod}.ln_g"], f[f"{mod}.ln_b"], rows, H)
+    ln, mean, rstd = _layernorm_in(x2d, f[f"{mod}.ln_g"], f[f"{mod}.ln_b"], rows, H, pre_ln)
     qkv = torch.addmm(h[f"{mod}.b_qkv"], ln, h[f"{mod}.w_qkv"])
     gpre = torch.addmm(h[f"{mod}.b_g"], x2d, h[f"{mod}.w_g"])
     og = torch.empty(rows, nh * c, device=x2d.device, dtype=BF16)
@@ -130,7 +157,7 @@ def attention_fwd(bp: BlockParams, mod: str, x2d, B: int, L: int, kind: str, bia
                               bias=bt, bias_s=bs, bias_off=boff)
     ops.attention_fwd(desc)
     y = _mm(og, h[f"{mod}.w_o"])
-    out = ops.gated_residual_fwd(x2d, y, f[f"{mod}.b_o"], rows, H)
+    out = _residual_out(x2d, y, f[f"{mod}.b_o"], rows, H, next_ln)
     sv = None
     if save:
         sv = Saved(x=x2d, ln=ln, mean=mean, rstd=rstd, qkv=qkv, gpre=gpre, og=og, orw=orw, lse=lse,
@@ -229,18 +256,18 @@ def msa_row_bias_bwd(bp: BlockParams, sv: Saved, dbias, dz):
 
 
 # ----------------------------------------------------------------------------- transition
-def transition_fwd(bp: BlockParams, mod: str, x2d, rows: int, save=True):
+def transition_fwd(bp: BlockParams, mod: str, x2d, rows: int, save=True, pre_ln=None, next_ln=None):
     """transition (evoformer.py:237-240) + residual."""
     H = x2d.shape[1]
     h, f = bp.h, bp.f
-    ln, mean, rstd = ops.layernorm_fwd(x2d, f[f"{mod}.ln_g"], f[f"{mod}.ln_b"], rows, H)
+    ln, mean, rstd = _layernorm_in(x2d, f[f"{mod}.ln_g"], f[f"{mod}.ln_b"], rows, H, pre_ln)
     if ln.is_cuda:  # bias + ReLU in the cuBLASLt epilogue (RELU_BIAS): hid is written once
         hid = torch._addmm_activation(h[f"{mod}.b1"], ln, h[f"{mod}.w1"])
     else:
         hid = _mm(ln, h[f"{mod}.w1"])
         ops.bias_act_fwd(hid, f[f"{mod}.b1"], rows, hid.shape[1], relu=True)
     y = _mm(hid, h[f"{mod}.w2"])
-    out = ops.gated_residual_fwd(x2d, y, f[f"{mod}.b2"], rows, H)
+    out = _residual_out(x2d, y, f[f"{mod}.b2"], rows, H, next_ln)
     sv = Saved(x=x2d, ln=ln, mean=mean, rstd=rstd, hid=hid, mod=mod) if save else None
     return out, sv
 
@@ -263,7 +290,8 @@ def transition_bwd(bp: BlockParams, sv: Saved, dx_new, next_db=None, db_done=Fal
 
 
 # ----------------------------------------------------------------------------- outer product mean
-def opm_fwd(bp: BlockParams, m2d, z2d, S: int, R: int, save=True, b_full=None, Rj=None, gather=None):
+def opm_fwd(bp: BlockParams, m2d, z2d, S: int, R: int, save=True, b_full=None, Rj=None, gather=None, pre_ln=None,
+            next_ln=None):
     """outer_product_mean (evoformer.py:243-255) + residual into z.
 
     o[i][j][p][q] = sum_s a[s,i,p] b[s,j,q] / S is ONE tcgen05 GEMM with M = i*p,
@@ -275,7 +303,7 @@ def opm_fwd(bp: BlockParams, m2d, z2d, S: int, R: int, save=True, b_full=None, R
     P, Hm, Hz = cfg.hidden_proj, cfg.h_msa, cfg.h_pair
     rows_m = S * R
     h, f = bp.h, bp.f
-    ln, mean, rstd = ops.layernorm_fwd(m2d, f["opm.ln_g"], f["opm.ln_b"], rows_m, Hm)
+    ln, mean, rstd = _layernorm_in(m2d, f["opm.ln_g"], f["opm.ln_b"], rows_m, Hm, pre_ln)
     ab = torch.addmm(h["opm.b_ab"], ln, h["opm.w_ab"])              # [S*R, 2P] = [a | b]
     A = Mat(ab, lo=(1, R * 2 * P), split=(P, 0), hi=(2 * P, 0))
     if gather is None:
@@ -291,7 +319,7 @@ def opm_fwd(bp: BlockParams, m2d, z2d, S: int, R: int, save=True, b_full=None, R
     Cm = Mat(o, lo=(P, 1), split=(P, P), hi=(Rj * P * P, P * P))
     ops.bgemm(A, B, Cm, 1, R * P, Rj * P, S, alpha=1.0 / S)
     y = _mm(o.view(R * Rj, P * P), h["opm.w_o"])
-    out = ops.gated_residual_fwd(z2d, y, f["opm.b_o"], R * Rj, Hz)
+    out = _residual_out(z2d, y, f["opm.b_o"], R * Rj, Hz, next_ln)
     sv = Saved(m=m2d, ln=ln, mean=mean, rstd=rstd, ab=ab, bsrc=bsrc, o=o, S=S, R=R, Rj=Rj,
                gathered=gather is not None) if save else None
     return out, sv
@@ -338,7 +366,7 @@ def opm_bwd(bp: BlockParams, sv: Saved, dz_new, dm, reduce_scatter=None, next_db
 
 
 # ----------------------------------------------------------------------------- triangle update
-def triangle_fwd(bp: BlockParams, mod: str, z2d, R: int, save=True, Rl=None, gather=None):
+def triangle_fwd(bp: BlockParams, mod: str, z2d, R: int, save=True, Rl=None, gather=None, pre_ln=None, next_ln=None):
     """tri_update_outgoing / incoming (evoformer.py:258-284) + residual.
 
     Y = LN(z) @ [W_g|W_as|W_al|W_bs|W_bl] + b (cuBLAS);  a, b = sigmoid gating
@@ -356,7 +384,7 @@ def triangle_fwd(bp: BlockParams, mod: str, z2d, R: int, save=True, Rl=None, gat
     Rl = R if Rl is None else Rl
     rows = R * Rl
     h, f = bp.h, bp.f
-    ln, mean, rstd = ops.layernorm_fwd(z2d, f[f"{mod}.ln_g"], f[f"{mod}.ln_b"], rows, Hz)
+    ln, mean, rstd = _layernorm_in(z2d, f[f"{mod}.ln_g"], f[f"{mod}.ln_b"], rows, Hz, pre_ln)
     Y = torch.addmm(h[f"{mod}.b_proj"], ln, h[f"{mod}.w_proj"])       # [rows, Hz + 4P]
     a_cm = torch.empty(P, rows, device=z2d.device, dtype=BF16)
     b_cm = torch.empty_like(a_cm)
@@ -390,7 +418,7 @@ def triangle_fwd(bp: BlockParams, mod: str, z2d, R: int, save=True, Rl=None, gat
         bfull = b_cm
     ln2, mean2, rstd2 = ops.layernorm_fwd(t_cm, f[f"{mod}.ln2_g"], f[f"{mod}.ln2_b"], rows, P, x_rs=1, x_cs=rows)
     y2 = _mm(ln2, h[f"{mod}.w_o"])
-    out = ops.gated_residual_fwd(z2d, y2, f[f"{mod}.b_o"], rows, Hz, gp=Y, gp_rs=Hz + 4 * P)
+    out = _residual_out(z2d, y2, f[f"{mod}.b_o"], rows, Hz, next_ln, gp=Y, gp_rs=Hz + 4 * P)
     sv = Saved(z=z2d, ln=ln, mean=mean, rstd=rstd, Y=Y, a_cm=a_cm, b_cm=b_cm, afull=afull, bfull=bfull,
                t_cm=t_cm, ln2=ln2, mean2=mean2, rstd2=rstd2, y2=y2, mod=mod, R=R, Rl=Rl, M=M, N=N,
                gathered=gather is not None) if save else None
@@ -468,16 +496,22 @@ def block_fwd(bp: BlockParams, m, z, save=True):
     m2 = m.reshape(S * R, cfg.h_msa)
     z2 = z.reshape(R * R, cfg.h_pair)
     saved = [] if save else None
+    # each residual epilogue also produces the next module's input LayerNorm (LnChain)
+    f = bp.f
+    c = {k: LnChain(f[f"{k}.ln_g"], f[f"{k}.ln_b"]) for k in
+         ("msa_col", "msa_trans", "opm", "tri_out", "tri_in", "pair_row", "pair_col", "pair_trans")}
     bias, sv_b = msa_row_bias_fwd(bp, z2, R, R, save)
-    m2, s1 = attention_fwd(bp, "msa_row", m2, S, R, "row", bias=bias, save=save)
-    m2, s2 = attention_fwd(bp, "msa_col", m2, R, S, "col", save=save)
-    m2, s3 = transition_fwd(bp, "msa_trans", m2, S * R, save)
-    z2, s4 = opm_fwd(bp, m2, z2, S, R, save)
-    z2, s5 = triangle_fwd(bp, "tri_out", z2, R, save)
-    z2, s6 = triangle_fwd(bp, "tri_in", z2, R, save)
-    z2, s7 = attention_fwd(bp, "pair_row", z2, R, R, "row", bias="pair", save=save)
-    z2, s8 = attention_fwd(bp, "pair_col", z2, R, R, "col", bias="pair", save=save)
-    z2, s9 = transition_fwd(bp, "pair_trans", z2, R * R, save)
+    m2, s1 = attention_fwd(bp, "msa_row", m2, S, R, "row", bias=bias, save=save, next_ln=c["msa_col"])
+    m2, s2 = attention_fwd(bp, "msa_col", m2, R, S, "col", save=save, pre_ln=c["msa_col"], next_ln=c["msa_trans"])
+    m2, s3 = transition_fwd(bp, "msa_trans", m2, S * R, save, pre_ln=c["msa_trans"], next_ln=c["opm"])
+    z2, s4 = opm_fwd(bp, m2, z2, S, R, save, pre_ln=c["opm"], next_ln=c["tri_out"])
+    z2, s5 = triangle_fwd(bp, "tri_out", z2, R, save, pre_ln=c["tri_out"], next_ln=c["tri_in"])
+    z2, s6 = triangle_fwd(bp, "tri_in", z2, R, save, pre_ln=c["tri_in"], next_ln=c["pair_row"])
+    z2, s7 = attention_fwd(bp, "pair_row", z2, R, R, "row", bias="pair", save=save, pre_ln=c["pair_row"],
+                           next_ln=c["pair_col"])
+    z2, s8 = attention_fwd(bp, "pair_col", z2, R, R, "col", bias="pair", save=save, pre_ln=c["pair_col"],
+                           next_ln=c["pair_trans"])
+    z2, s9 = transition_fwd(bp, "pair_trans", z2, R * R, save, pre_ln=c["pair_trans"])
     if save:
         saved.extend([sv_b, s1, s2, s3, s4, s5, s6, s7, s8, s9])
     return m2.view(S, R, cfg.h_msa), z2.view(R, R, cfg.h_pair), saved

@@ -61,8 +61,8 @@ __global__ void __launch_bounds__(256) gated_residual_fwd_k(const T* __restrict_
       float gv[8];
       ld8<T>(gp + r * gp_rs + c, gv);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) yv[e] *= sigmoidf_(gv[e]);
-    }
+      for (int e = 0; e < 8; ++e) yv[e] = __fmul_rn(yv[e], sigmoidf_(gv[e]));  // no FMA contraction: bitwise
+    }                                                                        // equal to residual_ln_k
 #pragma unroll
     for (int e = 0; e < 8; ++e) rv[e] += yv[e];
     st8<T>(out + r * cols + c, rv);
@@ -327,6 +327,108 @@ __global__ void count_nonfinite_k(const T* __restrict__ x, int64_t n, unsigned i
   if ((threadIdx.x & 31) == 0 && local) atomicAdd(counter, local);
 }
 
+// ------------------------------------------------------------------ residual + LayerNorm
+// out = res + [sigmoid(gp) *] (y + bias)   (the module's residual epilogue), then the next
+// module's LayerNorm of out (engine.layernorm_raw, engine.py:206-217) in the same pass:
+// ln = (out - mean) * rstd * gamma + beta, mean/rstd saved.  Saves the LayerNorm's re-read
+// of out and a launch per module boundary.  LPR = COLS/8 lanes per row (16-byte lanes),
+// U rows per lane group per step with every load issued first.
+template <int COLS, int U>
+__global__ void __launch_bounds__(256, 2) residual_ln_k(const bf16* __restrict__ res, const bf16* __restrict__ y,
+                                                        int64_t y_rs, const float* __restrict__ bias,
+                                                        const bf16* __restrict__ gp, int64_t gp_rs,
+                                                        bf16* __restrict__ out, const float* __restrict__ gamma,
+                                                        const float* __restrict__ beta, bf16* __restrict__ ln,
+                                                        float* __restrict__ mean, float* __restrict__ rstd,
+                                                        int64_t rows, float eps) {
+  // loads stay raw (one uint4 per 8 bf16) until used and the per-column vectors are re-read
+  // through L1 at use: 2 CTAs per SM, U = 4 row-groups of 3 loads in flight per lane
+  constexpr int LPR = COLS / 8, RPW = 32 / LPR;
+  __shared__ float4 cv[3][COLS / 4];  // bias, gamma, beta (volatile reads: not hoisted into registers)
+  for (int i = threadIdx.x; i < COLS; i += blockDim.x) {
+    reinterpret_cast<float*>(cv[0])[i] = bias ? bias[i] : 0.f;
+    reinterpret_cast<float*>(cv[1])[i] = gamma[i];
+    reinterpret_cast<float*>(cv[2])[i] = beta[i];
+  }
+  __syncthreads();
+  const volatile float4* vb = cv[0];
+  const volatile float4* vg = cv[1];
+  const volatile float4* vt = cv[2];
+  const int lane = threadIdx.x & 31, sub = lane / LPR, cl = (lane % LPR) * 8;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t rb = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * RPW * U; rb < rows;
+       rb += nw * RPW * U) {
+    uint4 rr[U], yr[U], gr[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t row = rb + u * RPW + sub;
+      if (row < rows) {
+        rr[u] = __ldcs(reinterpret_cast<const uint4*>(res + row * COLS + cl));
+        yr[u] = __ldcs(reinterpret_cast<const uint4*>(y + row * y_rs + cl));
+        if (gp) gr[u] = __ldcs(reinterpret_cast<const uint4*>(gp + row * gp_rs + cl));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t row = rb + u * RPW + sub;
+      float o[8], t[8], s = 0.f;
+      unpack_bf16x2(rr[u].x, o[0], o[1]); unpack_bf16x2(rr[u].y, o[2], o[3]);
+      unpack_bf16x2(rr[u].z, o[4], o[5]); unpack_bf16x2(rr[u].w, o[6], o[7]);
+      unpack_bf16x2(yr[u].x, t[0], t[1]); unpack_bf16x2(yr[u].y, t[2], t[3]);
+      unpack_bf16x2(yr[u].z, t[4], t[5]); unpack_bf16x2(yr[u].w, t[6], t[7]);
+      {
+        const float4 b0 = const_cast<const float4&>(vb[cl / 4]);
+        const float4 b1 = const_cast<const float4&>(vb[cl / 4 + 1]);
+        t[0] += b0.x; t[1] += b0.y; t[2] += b0.z; t[3] += b0.w;
+        t[4] += b1.x; t[5] += b1.y; t[6] += b1.z; t[7] += b1.w;
+      }
+      if (gp) {
+        float gv[8];
+        unpack_bf16x2(gr[u].x, gv[0], gv[1]); unpack_bf16x2(gr[u].y, gv[2], gv[3]);
+        unpack_bf16x2(gr[u].z, gv[4], gv[5]); unpack_bf16x2(gr[u].w, gv[6], gv[7]);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) t[e] = __fmul_rn(t[e], sigmoidf_(gv[e]));
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] += t[e];
+      // LayerNorm statistics of the bf16-rounded residual stream (what the next module reads)
+      uint4 w;
+      w.x = pack_bf16x2(o[0], o[1]); w.y = pack_bf16x2(o[2], o[3]);
+      w.z = pack_bf16x2(o[4], o[5]); w.w = pack_bf16x2(o[6], o[7]);
+      unpack_bf16x2(w.x, o[0], o[1]); unpack_bf16x2(w.y, o[2], o[3]);
+      unpack_bf16x2(w.z, o[4], o[5]); unpack_bf16x2(w.w, o[6], o[7]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s += o[e];
+#pragma unroll
+      for (int off = LPR / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      const float mu = s * (1.0f / COLS);
+      float q = 0.f;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) q += (o[e] - mu) * (o[e] - mu);
+#pragma unroll
+      for (int off = LPR / 2; off > 0; off >>= 1) q += __shfl_xor_sync(0xffffffffu, q, off);
+      const float rs = rsqrtf(q * (1.0f / COLS) + eps);
+      if (row < rows) {
+        *reinterpret_cast<uint4*>(out + row * COLS + cl) = w;
+        const float4 g0 = const_cast<const float4&>(vg[cl / 4]);
+        const float4 g1 = const_cast<const float4&>(vg[cl / 4 + 1]);
+        const float4 c0 = const_cast<const float4&>(vt[cl / 4]);
+        const float4 c1 = const_cast<const float4&>(vt[cl / 4 + 1]);
+        const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+        const float bb[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+        float lv[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) lv[e] = (o[e] - mu) * rs * gg[e] + bb[e];
+        st8<bf16>(ln + row * COLS + cl, lv);
+        if (cl == 0 && mean) {
+          mean[row] = mu;
+          rstd[row] = rs;
+        }
+      }
+    }
+  }
+}
+
 static unsigned grid_for(int64_t work, int threads) {
   int64_t need = (work + threads - 1) / threads;
   int64_t cap = (int64_t)sm_count() * 16;
@@ -506,5 +608,33 @@ extern "C" int evo_count_nonfinite(const void* x, int dtype, int64_t n, unsigned
   if (dtype == EVO_BF16) count_nonfinite_k<bf16><<<g, 256, 0, st>>>((const bf16*)x, n, counter);
   else count_nonfinite_k<float><<<g, 256, 0, st>>>((const float*)x, n, counter);
   EVO_LAUNCH_CHECK("count_nonfinite");
+  return EVO_OK;
+}
+
+extern "C" int evo_residual_layernorm_fwd(const void* res, const void* y, int64_t y_rs, const float* bias,
+                                          const void* gp, int64_t gp_rs, void* out, const float* gamma,
+                                          const float* beta, void* ln, float* mean, float* rstd, int64_t rows,
+                                          int64_t cols, float eps, void* stream) {
+  EVO_CHECK_ARG(res && y && out && gamma && beta && ln, EVO_ERR_ARG, "residual_layernorm: null pointer");
+  EVO_CHECK_ARG(cols == 32 || cols == 64 || cols == 128 || cols == 256, EVO_ERR_SHAPE,
+                "residual_layernorm: cols must be 32/64/128/256 (got %lld)", (long long)cols);
+  EVO_CHECK_ARG(y_rs % 8 == 0 && (!gp || gp_rs % 8 == 0) && al16(res) && al16(y) && al16(out) && al16(ln) &&
+                    (!gp || al16(gp)),
+                EVO_ERR_ALIGN, "residual_layernorm: 16-byte aligned rows required");
+  if (rows == 0) return EVO_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t rpw = 32 / (cols / 8);
+  int64_t need = (rows + 8 * rpw * 4 - 1) / (8 * rpw * 4), cap = (int64_t)sm_count() * 2;
+  dim3 g((unsigned)(need < cap ? need : cap));
+#define RLN(CC) residual_ln_k<CC, 4><<<g, 256, 0, st>>>((const bf16*)res, (const bf16*)y, y_rs, bias, (const bf16*)gp, \
+                                                        gp_rs, (bf16*)out, gamma, beta, (bf16*)ln, mean, rstd, rows, eps)
+  switch (cols) {
+    case 32: RLN(32); break;
+    case 64: RLN(64); break;
+    case 128: RLN(128); break;
+    default: RLN(256); break;
+  }
+#undef RLN
+  EVO_LAUNCH_CHECK("residual_layernorm fwd");
   return EVO_OK;
 }

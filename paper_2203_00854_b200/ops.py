@@ -292,6 +292,21 @@ def gated_residual_fwd(res, y, bias, rows, cols, y_rs=None, gp=None, gp_rs=0, ou
     return out
 
 
+def residual_layernorm_fwd(res, y, bias, rows, cols, gamma, beta, y_rs=None, gp=None, gp_rs=0, eps=1e-5):
+    """out = res + [sigmoid(gp) *] (y + bias) and the next module's LayerNorm of out in one pass
+    -> (out, ln, mean, rstd)"""
+    _cuda(res, y, gamma, beta)
+    y_rs = cols if y_rs is None else y_rs
+    out = torch.empty(rows, cols, device=res.device, dtype=res.dtype)
+    ln = torch.empty_like(out)
+    mean = torch.empty(rows, device=res.device, dtype=torch.float32)
+    rstd = torch.empty_like(mean)
+    call("evo_residual_layernorm_fwd", _p(res), _p(y), y_rs, _p(bias), _p(gp), gp_rs, _p(out), _p(gamma), _p(beta),
+         _p(ln), _p(mean), _p(rstd), rows, cols, eps, stream_handle(),
+         work=(0, rows * cols * 2 * (4 + (1 if gp is not None else 0)) + 8 * rows))
+    return out, ln, mean, rstd
+
+
 def gated_residual_bwd(dout, rows, cols, y=None, y_rs=None, bias=None, gp=None, gp_rs=0, dy=None, dgp=None,
                        dgp_rs=0, dbias=None):
     call("evo_gated_residual_bwd", _p(dout), _p(y), cols if y_rs is None else y_rs, _p(bias), _p(gp), gp_rs,

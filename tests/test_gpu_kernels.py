@@ -336,6 +336,28 @@ def test_tri_gate_and_residuals():
     assert rel(dyy, want) < 1e-2 and rel(db1, want.sum(0)) < 1e-3
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("cols,gated,rows", [(32, False, 1000), (64, False, 777), (128, False, 4099), (128, True, 513),
+                                             (256, False, 300)])
+def test_residual_layernorm_fwd(cols, gated, rows):
+    """fused residual epilogue + next module's LayerNorm == gated_residual_fwd then layernorm_fwd"""
+    gen = torch.Generator(device=DEV).manual_seed(cols + rows)
+    res = _mk((rows, cols), gen)
+    y = _mk((rows, cols + 16), gen)[:, :cols]
+    bias = torch.randn(cols, device=DEV, generator=gen)
+    gp = _mk((rows, 2 * cols), gen) if gated else None
+    gam = torch.randn(cols, device=DEV, generator=gen)
+    bet = torch.randn(cols, device=DEV, generator=gen)
+    kw = dict(gp=gp, gp_rs=2 * cols) if gated else {}
+    want = ops.gated_residual_fwd(res, y, bias, rows, cols, y_rs=cols + 16, **kw)
+    wln, wmu, wrs = ops.layernorm_fwd(want, gam, bet, rows, cols)
+    out, ln, mu, rs = ops.residual_layernorm_fwd(res, y, bias, rows, cols, gam, bet, y_rs=cols + 16, **kw)
+    assert torch.equal(out, want)
+    assert torch.allclose(mu, wmu, atol=1e-5, rtol=1e-5) and torch.allclose(rs, wrs, atol=1e-3, rtol=1e-4)
+    assert rel(ln, wln) < 1e-2
+
+
+@pytest.mark.gpu
 def test_count_nonfinite():
     x = torch.zeros(1000, device=DEV)
     x[3] = float("inf")
