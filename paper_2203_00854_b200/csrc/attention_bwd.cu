@@ -44,24 +44,30 @@ struct AttnBwdParams {
 };
 
 // dbias[h][q][k] += scale * sum_b dS[b][h][k][q]   (batch-shared bias: msa_row, evoformer.py:214).
-// Thread = 8 consecutive queries of one (h, key); 8 batches' 16-byte loads in flight per
-// thread (the read of the B x H x L x L workspace is the whole cost, so it must saturate HBM).
+// CTA = 8 warps x 32 lanes over 32 consecutive 16-byte vectors (256 elements): warp w sums the
+// batches b = w, w + 8, ... (U loads in flight per lane), then the 8 partial sums meet in smem
+// in a fixed order (deterministic).  H*L*L/8 * 8 threads keep enough bytes in flight to stream
+// the B x H x L x L workspace at HBM speed.
 __global__ void __launch_bounds__(256) attn_dbias_reduce(const bf16* __restrict__ dS, float* __restrict__ dbias,
                                                          int64_t B, int H, int L, int64_t d1, int64_t d2, int64_t d3,
                                                          float scale) {
-  constexpr int U = 8;
+  constexpr int U = 4, NW = 8;
+  __shared__ float part[NW][8][33];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t per = (int64_t)H * L * L;
   const int64_t nv = per / 8;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = i * 8;
+  for (int64_t v0 = (int64_t)blockIdx.x * 32; v0 < nv; v0 += (int64_t)gridDim.x * 32) {
+    const int64_t i = v0 + lane;
+    const bool ok = i < nv;
+    const bf16* src = dS + (ok ? i * 8 : 0);
     float acc[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) acc[k] = 0.f;
-    int64_t b = 0;
-    for (; b + U <= B; b += U) {  // unguarded: all U loads issue back to back
+    int64_t b = warp;
+    for (; b + (U - 1) * NW < B; b += U * NW) {
       uint4 u[U];
 #pragma unroll
-      for (int t = 0; t < U; ++t) u[t] = *reinterpret_cast<const uint4*>(dS + (b + t) * per + e);
+      for (int t = 0; t < U; ++t) u[t] = __ldcs(reinterpret_cast<const uint4*>(src + (b + t * NW) * per));
 #pragma unroll
       for (int t = 0; t < U; ++t) {
         float v[8];
@@ -71,18 +77,31 @@ __global__ void __launch_bounds__(256) attn_dbias_reduce(const bf16* __restrict_
         for (int k = 0; k < 8; ++k) acc[k] += v[k];
       }
     }
-    for (; b < B; ++b) {
-      const uint4 u = *reinterpret_cast<const uint4*>(dS + b * per + e);
+    for (; b < B; b += NW) {
+      const uint4 u = __ldcs(reinterpret_cast<const uint4*>(src + b * per));
       float v[8];
       unpack_bf16x2(u.x, v[0], v[1]); unpack_bf16x2(u.y, v[2], v[3]);
       unpack_bf16x2(u.z, v[4], v[5]); unpack_bf16x2(u.w, v[6], v[7]);
 #pragma unroll
       for (int k = 0; k < 8; ++k) acc[k] += v[k];
     }
-    const uint32_t eu = (uint32_t)e, LL = (uint32_t)L * (uint32_t)L;  // H*L*L < 2^31 (host-checked)
-    const int64_t h = eu / LL, kk = (eu / (uint32_t)L) % (uint32_t)L, q = eu % (uint32_t)L;
 #pragma unroll
-    for (int t = 0; t < 8; ++t) dbias[h * d1 + (q + t) * d2 + kk * d3] += scale * acc[t];
+    for (int k = 0; k < 8; ++k) part[warp][k][lane] = acc[k];
+    __syncthreads();
+    // 256 threads = 32 vectors x 8 elements: thread (lane', k) sums element k of vector lane'
+    {
+      const int vl = threadIdx.x >> 3, k = threadIdx.x & 7;
+      const int64_t iv = v0 + vl;
+      if (iv < nv) {
+        float t = 0.f;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) t += part[w][k][vl];
+        const uint32_t eu = (uint32_t)(iv * 8 + k), LL = (uint32_t)L * (uint32_t)L;  // H*L*L < 2^31 (host-checked)
+        const int64_t h = eu / LL, kk = (eu / (uint32_t)L) % (uint32_t)L, q = eu % (uint32_t)L;
+        dbias[h * d1 + q * d2 + kk * d3] += scale * t;
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -720,10 +739,9 @@ extern "C" int evo_gated_attention_bwd(const EvoAttnBwdDesc* d, void* stream) {
   if (rc) return rc;
   if (p.dS) {
     int64_t nv = (int64_t)H * L * L / 8;
-    // 128-thread CTAs: H*L*L/8 threads spread evenly over the SMs (each keeps 8 loads in flight)
-    int64_t g2 = (nv + 127) / 128, cap2 = (int64_t)sm_count() * 16;
+    int64_t g2 = (nv + 31) / 32, cap2 = (int64_t)sm_count() * 8;
     unsigned g2u = (unsigned)(g2 < cap2 ? g2 : cap2);
-    attn_dbias_reduce<<<g2u, 128, 0, st>>>(p.dS, p.dbias, B, H, L, p.db1, p.db2, p.db3, p.scale);
+    attn_dbias_reduce<<<g2u, 256, 0, st>>>(p.dS, p.dbias, B, H, L, p.db1, p.db2, p.db3, p.scale);
     EVO_LAUNCH_CHECK("attention bwd dbias reduce");
   }
   if (dq_partial == 2) return EVO_OK;
