@@ -140,6 +140,9 @@ int evo_gated_attention_fwd(const EvoAttnDesc* d, void* stream);
  * warpgroups); default len 4096.  Returns the previous threshold; len <= 0 only queries
  * it; len == 1 forces it for every input (tests).  Both kernels compute the same function. */
 int evo_attention_fwd_ws_min_len(int len);
+/* A/B switch: stage a full (per query and key) bias through shared memory in the forward
+   (default 1); on < 0 only queries.  Returns the previous setting. */
+int evo_attention_fwd_full_bias_smem(int on);
 
 /* Backward of the same op (flash-style: P is recomputed from q, k, bias and lse).
  * Inputs: the forward descriptor (q,k,v,g,bias,o_raw,lse) plus dout (gradient of

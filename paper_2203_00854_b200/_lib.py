@@ -68,6 +68,7 @@ _SIGS = {
     "evo_gated_attention_fwd": [C.POINTER(EvoAttnDesc), vp],
     "evo_gated_attention_bwd": [C.POINTER(EvoAttnBwdDesc), vp],
     "evo_attention_fwd_ws_min_len": [C.c_int],
+    "evo_attention_fwd_full_bias_smem": [C.c_int],
     "evo_residual_layernorm_fwd": [vp, vp, i64, vp, vp, i64, vp, vp, vp, vp, vp, vp, i64, i64, C.c_float, vp],
     "evo_gated_attention_bwd_workspace": [i64, i64, C.c_int, C.c_int, C.c_int],
     "evo_bgemm": [C.POINTER(EvoMat), C.POINTER(EvoMat), C.POINTER(EvoMat), i64, i64, i64, i64,

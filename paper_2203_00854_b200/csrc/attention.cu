@@ -17,6 +17,7 @@
 // K/V tiles are double-buffered with cp.async; several CTAs per SM overlap the
 // MMA of one CTA with the softmax of another.
 #include "attn.cuh"
+#include <cstdlib>
 
 namespace evo {
 
@@ -29,12 +30,32 @@ template <int CP>
 struct AttnSmem {
   static constexpr int CQ = CP + 16;  // Q / K K-extent: data + [1 | per-key bias] group + zero group
   static constexpr int CV = CP + 8;   // V N-extent: data + [1, 0 x 7] (row sums of P)
-  static constexpr uint32_t Q = 0;
-  static constexpr uint32_t KT = Q + ATT_BQ * CQ * 2;          // 2 stages
+  static constexpr uint32_t Q = 0, Q_BYTES = ATT_BQ * CQ * 2;
+  static constexpr uint32_t KT = Q + Q_BYTES;                  // 2 stages
   static constexpr uint32_t VT = KT + 2 * ATT_BK * CQ * 2;     // 2 stages
   static constexpr uint32_t TOTAL = VT + 2 * ATT_BK * CV * 2;
   static constexpr uint32_t K_BYTES = ATT_BK * CQ * 2, V_BYTES = ATT_BK * CV * 2;
+  // full (per query and key) bias tiles, 2 stages, rows padded to 72 elements (conflict-free
+  // 16-byte row reads): only with the FB variant
+  static constexpr int BROW = ATT_BK + 8;
+  static constexpr uint32_t BS = TOTAL, BS_BYTES = ATT_BQ * BROW * 2;
+  static constexpr uint32_t TOTAL_FB = BS + 2 * BS_BYTES;
 };
+
+// 128 query rows x 64 keys of a full bias into smem (rows padded to BROW): 4 rows of 128
+// contiguous bytes per warp instruction
+template <int BROW>
+__device__ __forceinline__ void att_load_bias(uint32_t sdst, const bf16* base, int64_t row_stride, int q0, int k0,
+                                              int L) {
+#pragma unroll
+  for (int it = 0; it < ATT_BQ * 8 / 128; ++it) {
+    const int ch = threadIdx.x + it * 128;
+    const int rr = ch >> 3, cc = (ch & 7) * 8;
+    const bool ok = (q0 + rr < L) && (k0 + cc < L);
+    const bf16* src = ok ? base + (int64_t)(q0 + rr) * row_stride + k0 + cc : base;
+    cp_async16(sdst + rr * (BROW * 2) + (ch & 7) * 16, src, ok);
+  }
+}
 
 // ROWS x CP K-major tile from a strided [row][col] source (cols contiguous)
 template <int CP, int ROWS>
@@ -100,8 +121,22 @@ __device__ __forceinline__ void att_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uin
       : "memory");
 }
 
-template <int CP>
-__global__ void __launch_bounds__(128, CP == 64 ? 2 : 4) attn_fwd_kernel(AttnParams P) {
+#ifndef EVO_EXP
+#define EVO_EXP 0
+#endif
+int sm_count();
+
+// FB: full bias staged through smem with the K/V tiles (msa_row: [1, H, L, L] shared over the
+// batch, so the tile loads hit L2) instead of 16-byte global loads after the S wait.
+//
+// Persistent: each CTA walks units u = (batch, head, query tile) with stride gridDim.x.  The
+// K/V stage and the mbarrier phases follow a CTA-wide tile counter, so the last key tile of a
+// unit already prefetches the next unit's first K/V tile, and the next unit's Q follows as
+// soon as this unit's last S MMA has read Q: the next unit's load latency hides under this
+// unit's last softmax and epilogue.
+template <int CP, bool FB>
+__global__ void __launch_bounds__(128, CP == 64 ? 2 : ((FB || EVO_EXP == 1) ? 3 : 4)) attn_fwd_kernel(AttnParams P,
+                                                                                                      int nunits) {
   using SM = AttnSmem<CP>;
   constexpr int CQ = SM::CQ, CV = SM::CV;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -110,14 +145,12 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : 4) attn_fwd_kernel(AttnPar
   const uint32_t sb = smem_u32(smem);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int q0 = blockIdx.x * ATT_BQ;
-  const int h = blockIdx.y;
-  const int64_t b = blockIdx.z;
-  const int L = P.L, c = P.c;
+  const int L = P.L, c = P.c, H = P.H;
+  const int nqt = (L + ATT_BQ - 1) / ATT_BQ;
   const int r = warp * 32 + lane;  // query row inside the tile
-  const int qi = q0 + r;
   const bool per_key_bias = P.bias && P.bs2 == 0;
   constexpr uint32_t ONE_BF16 = 0x3F80u;
+  const int nkt = (L + ATT_BK - 1) / ATT_BK;
 
   constexpr uint32_t TCOLS = 64 + CV <= 128 ? 128 : 256;
   if (warp == 0) tmem_alloc(&tmem_sh, TCOLS);
@@ -127,17 +160,43 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : 4) attn_fwd_kernel(AttnPar
     fence_mbar_init();
   }
 
-  const bf16* qb = P.q + b * P.q_sb + (int64_t)h * c;
-  const bf16* kb = P.k + b * P.k_sb + (int64_t)h * c;
-  const bf16* vb = P.v + b * P.v_sb + (int64_t)h * c;
-  const unsigned short* kbias =
-      per_key_bias ? reinterpret_cast<const unsigned short*>(P.bias + b * P.bs0 + (int64_t)h * P.bs1) : nullptr;
-  att_load_kmajor<CP, ATT_BQ>(sb + SM::Q, qb, P.q_sl, q0, L - q0, c);
-  att_load_kmajor<CP, ATT_BK>(sb + SM::KT, kb, P.k_sl, 0, L, c);
-  att_load_v<CP, CV>(sb + SM::VT, vb, P.v_sl, 0, L, c);
+  struct Unit {
+    int q0, h;
+    int64_t b;
+  };
+  auto decode = [&](int u) {
+    Unit t;
+    const int qt = u % nqt, rest = u / nqt;
+    t.q0 = qt * ATT_BQ;
+    t.h = rest % H;
+    t.b = rest / H;
+    return t;
+  };
+  auto kbase = [&](const Unit& t) { return P.k + t.b * P.k_sb + (int64_t)t.h * c; };
+  auto vbase = [&](const Unit& t) { return P.v + t.b * P.v_sb + (int64_t)t.h * c; };
+  auto kbias_of = [&](const Unit& t) {
+    return per_key_bias ? reinterpret_cast<const unsigned short*>(P.bias + t.b * P.bs0 + (int64_t)t.h * P.bs1)
+                        : nullptr;
+  };
+  auto bfull_of = [&](const Unit& t) { return FB ? P.bias + t.b * P.bs0 + (int64_t)t.h * P.bs1 : nullptr; };
+
+  int u = blockIdx.x;
+  if (u >= nunits) {  // (grid <= nunits by construction)
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem_sh, TCOLS);
+    return;
+  }
+  Unit cur = decode(u);
+  // prologue: Q and tile 0 of the first unit into Q buffer 0 / stage 0
+  att_load_kmajor<CP, ATT_BQ>(sb + SM::Q, P.q + cur.b * P.q_sb + (int64_t)cur.h * c, P.q_sl, cur.q0, L - cur.q0, c);
+  att_load_kmajor<CP, ATT_BK>(sb + SM::KT, kbase(cur), P.k_sl, 0, L, c);
+  att_load_v<CP, CV>(sb + SM::VT, vbase(cur), P.v_sl, 0, L, c);
+  if (FB) att_load_bias<SM::BROW>(sb + SM::BS, bfull_of(cur), P.bs2, cur.q0, 0, L);
   cp_async_commit();
-  // constant parts of the augmented operands: Q row [.. | 1 or 0, 0 x 7 | 0 x 8], K rows'
-  // zero group (the bias group is written per tile), V rows' [1, 0 x 7] row-sum column
+  // constant parts of the augmented operands (Q, both K/V stages): Q rows
+  // [.. | 1 or 0, 0 x 7 | 0 x 8], K rows' zero group (the bias group is written per tile),
+  // V rows' [1, 0 x 7] row-sum column
   st_shared_v4(sb + SM::Q + kmajor_off(r, CP, ATT_BQ), per_key_bias ? ONE_BF16 : 0u, 0u, 0u, 0u);
   st_shared_v4(sb + SM::Q + kmajor_off(r, CP + 8, ATT_BQ), 0u, 0u, 0u, 0u);
   {
@@ -146,7 +205,7 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : 4) attn_fwd_kernel(AttnPar
     st_shared_v4(sb + SM::VT + st * SM::V_BYTES + mnmajor_off(CP, kr, CV), ONE_BF16, 0u, 0u, 0u);
     if (st == 0)
       st_shared_v4(sb + SM::KT + kmajor_off(kr, CP, ATT_BK),
-                   (per_key_bias && kr < L) ? (uint32_t)kbias[(int64_t)kr * P.bs3] : 0u, 0u, 0u, 0u);
+                   (per_key_bias && kr < L) ? (uint32_t)kbias_of(cur)[(int64_t)kr * P.bs3] : 0u, 0u, 0u, 0u);
   }
 
   tc_fence_before();
@@ -160,192 +219,253 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : 4) attn_fwd_kernel(AttnPar
   constexpr uint32_t T_O = 64;  // O and its row sum (column CP) accumulate in TMEM [64, 64 + CV)
   const int ksteps = per_key_bias ? CQ / 16 : CP / 16;
 
-  float m_run = -INFINITY;  // running max, scaled log2 units
+  uint32_t gt = 0;  // CTA-wide tile counter: K/V stage = gt & 1, mbarrier phase parity = gt & 1
+  while (u < nunits) {
+    const int nu = u + gridDim.x;
+    const bool has_next = nu < nunits;
+    const Unit nxt = decode(has_next ? nu : u);
+    const int q0 = cur.q0, h = cur.h;
+    const int64_t b = cur.b;
+    const int qi = q0 + r;
+    const bf16* kb = kbase(cur);
+    const bf16* vb = vbase(cur);
+    const unsigned short* kbias = kbias_of(cur);
+    const bf16* bfull = bfull_of(cur);
+    float m_run = -INFINITY;  // running max, scaled log2 units
+    const bf16* brow = nullptr;
+    if (!FB && P.bias && !per_key_bias && qi < L) brow = P.bias + b * P.bs0 + (int64_t)h * P.bs1 + (int64_t)qi * P.bs2;
+    uint32_t nb = 0;  // next tile's per-key bias (threads 0..63), stored with its K tile
 
-  const int nkt = (L + ATT_BK - 1) / ATT_BK;
-  const bf16* brow = nullptr;
-  if (P.bias && !per_key_bias && qi < L) brow = P.bias + b * P.bs0 + (int64_t)h * P.bs1 + (int64_t)qi * P.bs2;
-  uint32_t nb = 0;  // next tile's per-key bias (threads 0..63), stored with its K tile
-
-  for (int j = 0; j < nkt; ++j) {
-    const int k0 = j * ATT_BK;
-    const int st = j & 1;
-    cp_async_wait<0>();
-    fence_async_smem();
-    __syncthreads();
-    // prefetch the next K/V tile into the other stage (its MMAs finished last iteration)
-    if (j + 1 < nkt) {
-      att_load_kmajor<CP, ATT_BK>(sb + SM::KT + (st ^ 1) * SM::K_BYTES, kb, P.k_sl, k0 + ATT_BK, L - k0 - ATT_BK, c);
-      att_load_v<CP, CV>(sb + SM::VT + (st ^ 1) * SM::V_BYTES, vb, P.v_sl, k0 + ATT_BK, L - k0 - ATT_BK, c);
-      if (per_key_bias && threadIdx.x < ATT_BK) {
-        const int k = k0 + ATT_BK + threadIdx.x;
-        nb = k < L ? (uint32_t)kbias[(int64_t)k * P.bs3] : 0u;
+    for (int j = 0; j < nkt; ++j, ++gt) {
+      const int k0 = j * ATT_BK;
+      const int st = gt & 1;
+      cp_async_wait<0>();
+      fence_async_smem();
+      __syncthreads();
+      // prefetch into the other stage (its MMAs finished last iteration): this unit's next
+      // K/V tile, or on the last tile the next unit's first K/V tile
+      const uint32_t kdst = sb + SM::KT + (st ^ 1) * SM::K_BYTES, vdst = sb + SM::VT + (st ^ 1) * SM::V_BYTES;
+      if (j + 1 < nkt) {
+        att_load_kmajor<CP, ATT_BK>(kdst, kb, P.k_sl, k0 + ATT_BK, L - k0 - ATT_BK, c);
+        att_load_v<CP, CV>(vdst, vb, P.v_sl, k0 + ATT_BK, L - k0 - ATT_BK, c);
+        if (FB) att_load_bias<SM::BROW>(sb + SM::BS + (st ^ 1) * SM::BS_BYTES, bfull, P.bs2, q0, k0 + ATT_BK, L);
+        if (per_key_bias && threadIdx.x < ATT_BK) {
+          const int k = k0 + ATT_BK + threadIdx.x;
+          nb = k < L ? (uint32_t)kbias[(int64_t)k * P.bs3] : 0u;
+        }
+      } else if (has_next) {
+        att_load_kmajor<CP, ATT_BK>(kdst, kbase(nxt), P.k_sl, 0, L, c);
+        att_load_v<CP, CV>(vdst, vbase(nxt), P.v_sl, 0, L, c);
+        if (FB) att_load_bias<SM::BROW>(sb + SM::BS + (st ^ 1) * SM::BS_BYTES, bfull_of(nxt), P.bs2, nxt.q0, 0, L);
+        if (per_key_bias && threadIdx.x < ATT_BK)
+          nb = (int)threadIdx.x < L ? (uint32_t)kbias_of(nxt)[(int64_t)threadIdx.x * P.bs3] : 0u;
       }
-    }
-    cp_async_commit();
+      cp_async_commit();
 
-    if (threadIdx.x == 0) {
-      // S_j overwrites the columns P_{j-1} was read from: PV_{j-1} must be complete
-      if (j > 0) mbar_wait(&bar_o, (j - 1) & 1);
+      if (threadIdx.x == 0) {
+        // S overwrites the columns the previous tile's P was read from: its PV must be complete
+        if (gt > 0) mbar_wait(&bar_o, (gt - 1) & 1);
+        tc_fence_after();
+        for (int kk = 0; kk < ksteps; ++kk) {
+          uint64_t ad = make_sdesc(sb + SM::Q + kk * 2 * (128 / 8) * 128, (128 / 8) * 128, 128);
+          uint64_t bd = make_sdesc(sb + SM::KT + st * SM::K_BYTES + kk * 2 * (ATT_BK / 8) * 128, (ATT_BK / 8) * 128,
+                                   128);
+          mma_bf16(tmem, ad, bd, IDESC_S, kk != 0);
+        }
+        mma_commit(&bar_s);
+      }
+      // bar_s completes after S, which was issued after the previous PV completed: O is stable
+      mbar_wait(&bar_s, gt & 1);
       tc_fence_after();
-      for (int kk = 0; kk < ksteps; ++kk) {
-        uint64_t ad = make_sdesc(sb + SM::Q + kk * 2 * (128 / 8) * 128, (128 / 8) * 128, 128);
-        uint64_t bd = make_sdesc(sb + SM::KT + st * SM::K_BYTES + kk * 2 * (ATT_BK / 8) * 128, (ATT_BK / 8) * 128,
-                                 128);
-        mma_bf16(tmem, ad, bd, IDESC_S, kk != 0);
+      if (j + 1 == nkt && has_next) {  // Q is free: this unit's last S MMA has completed
+        att_load_kmajor<CP, ATT_BQ>(sb + SM::Q, P.q + nxt.b * P.q_sb + (int64_t)nxt.h * c, P.q_sl, nxt.q0,
+                                    L - nxt.q0, c);
+        cp_async_commit();
       }
-      mma_commit(&bar_s);
-    }
-    // bar_s completes after S_j, which was issued after PV_{j-1} completed: O is stable here
-    mbar_wait(&bar_s, j & 1);
-    tc_fence_after();
 
-    float s[ATT_BK];
+      float s[ATT_BK];
 #pragma unroll
-    for (int cc = 0; cc < ATT_BK; cc += 32) tmem_ld32(t_row + cc, s + cc);
-    tmem_ld_wait();
+      for (int cc = 0; cc < ATT_BK; cc += 32) tmem_ld32(t_row + cc, s + cc);
+      tmem_ld_wait();
 
-    // full bias (before the scale, G1); keys >= L masked on the last tile only
-    const bool full_tile = k0 + ATT_BK <= L;
-    if (brow) {
-      if (P.bias_vec && full_tile) {
+      // full bias (before the scale, G1); keys >= L masked on the last tile only
+      const bool full_tile = k0 + ATT_BK <= L;
+      if (FB) {
+        const uint32_t brs = sb + SM::BS + st * SM::BS_BYTES + r * (SM::BROW * 2);
 #pragma unroll
         for (int kk = 0; kk < ATT_BK; kk += 8) {
-          uint4 u = *reinterpret_cast<const uint4*>(brow + k0 + kk);
+          uint32_t u0, u1, u2, u3;
+          asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];\n" : "=r"(u0), "=r"(u1), "=r"(u2), "=r"(u3)
+                       : "r"(brs + kk * 2));
           float t[8];
-          unpack_bf16x2(u.x, t[0], t[1]); unpack_bf16x2(u.y, t[2], t[3]);
-          unpack_bf16x2(u.z, t[4], t[5]); unpack_bf16x2(u.w, t[6], t[7]);
+          unpack_bf16x2(u0, t[0], t[1]); unpack_bf16x2(u1, t[2], t[3]);
+          unpack_bf16x2(u2, t[4], t[5]); unpack_bf16x2(u3, t[6], t[7]);
 #pragma unroll
           for (int e = 0; e < 8; ++e) s[kk + e] += t[e];
         }
-      } else {
+      } else if (brow) {
+        if (P.bias_vec && full_tile) {
 #pragma unroll
-        for (int kk = 0; kk < ATT_BK; ++kk)
-          if (k0 + kk < L) s[kk] += bf2f(brow[(int64_t)(k0 + kk) * P.bs3]);
-      }
-    }
-    if (!full_tile) {
+          for (int kk = 0; kk < ATT_BK; kk += 8) {
+            uint4 w = *reinterpret_cast<const uint4*>(brow + k0 + kk);
+            float t[8];
+            unpack_bf16x2(w.x, t[0], t[1]); unpack_bf16x2(w.y, t[2], t[3]);
+            unpack_bf16x2(w.z, t[4], t[5]); unpack_bf16x2(w.w, t[6], t[7]);
 #pragma unroll
-      for (int kk = 0; kk < ATT_BK; ++kk)
-        if (k0 + kk >= L) s[kk] = -INFINITY;
-    }
-    float m8[8];
+            for (int e = 0; e < 8; ++e) s[kk + e] += t[e];
+          }
+        } else {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) m8[e] = fmaxf(s[e], s[e + 8]);
-#pragma unroll
-    for (int kk = 16; kk < ATT_BK; kk += 16) {
-#pragma unroll
-      for (int e = 0; e < 8; ++e) m8[e] = fmaxf(m8[e], fmaxf(s[kk + e], s[kk + 8 + e]));
-    }
-    const float mxs = P.scale_log2 * fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
-                                           fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
-    // lazy rescale: O (and l) in TMEM are rescaled only when a row's max grows by > 2^8
-    // (warp-uniform: TMEM loads/stores are warp-collective); P <= 2^8 is exact enough in bf16
-    const bool grow = mxs > m_run + 8.0f;
-    if (__any_sync(0xffffffffu, grow)) {
-      const float m_new = grow ? mxs : m_run;
-      if (j > 0) {
-        const float f = ex2f(m_run - m_new);
-#pragma unroll
-        for (int cc = 0; cc < CV; cc += 8) {
-          float v[8];
-          att_tmem_ld8(t_row + T_O + cc, v);
-          tmem_ld_wait();
-#pragma unroll
-          for (int e = 0; e < 8; ++e) v[e] *= f;
-          att_tmem_st8(t_row + T_O + cc, v);
+          for (int kk = 0; kk < ATT_BK; ++kk)
+            if (k0 + kk < L) s[kk] += bf2f(brow[(int64_t)(k0 + kk) * P.bs3]);
         }
       }
-      m_run = m_new;
-    }
-    const float mref = m_run == -INFINITY ? 0.f : m_run;
-    // P over S in TMEM columns [0, 32): this thread's row of S was read above
+      if (!full_tile) {
 #pragma unroll
-    for (int half = 0; half < 2; ++half) {  // 16 packed columns at a time (register budget)
-      uint32_t pk[16];
-#pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const int kk = half * 32 + 2 * e;
-        pk[e] = pack_bf16x2(ex2f(fmaf(s[kk], P.scale_log2, -mref)), ex2f(fmaf(s[kk + 1], P.scale_log2, -mref)));
+        for (int kk = 0; kk < ATT_BK; ++kk)
+          if (k0 + kk >= L) s[kk] = -INFINITY;
       }
-      tmem_st16(t_row + half * 16, reinterpret_cast<const float*>(pk));
+      float m8[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) m8[e] = fmaxf(s[e], s[e + 8]);
+#pragma unroll
+      for (int kk = 16; kk < ATT_BK; kk += 16) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) m8[e] = fmaxf(m8[e], fmaxf(s[kk + e], s[kk + 8 + e]));
+      }
+      const float mxs = P.scale_log2 * fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                                             fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+      // lazy rescale: O (and l) in TMEM are rescaled only when a row's max grows by > 2^8
+      // (warp-uniform: TMEM loads/stores are warp-collective); P <= 2^8 is exact enough in bf16
+      const bool grow = mxs > m_run + 8.0f;
+      if (__any_sync(0xffffffffu, grow)) {
+        const float m_new = grow ? mxs : m_run;
+        if (j > 0) {
+          const float f = ex2f(m_run - m_new);
+#pragma unroll
+          for (int cc = 0; cc < CV; cc += 8) {
+            float v[8];
+            att_tmem_ld8(t_row + T_O + cc, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[e] *= f;
+            att_tmem_st8(t_row + T_O + cc, v);
+          }
+        }
+        m_run = m_new;
+      }
+      const float mref = m_run == -INFINITY ? 0.f : m_run;
+      // P over S in TMEM columns [0, 32): this thread's row of S was read above
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {  // 16 packed columns at a time (register budget)
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const int kk = half * 32 + 2 * e;
+          pk[e] = pack_bf16x2(ex2f(fmaf(s[kk], P.scale_log2, -mref)), ex2f(fmaf(s[kk + 1], P.scale_log2, -mref)));
+        }
+        tmem_st16(t_row + half * 16, reinterpret_cast<const float*>(pk));
+      }
+      // the next tile's per-key bias into its K tile's bias group (stage st^1, loaded above)
+      if (per_key_bias && threadIdx.x < ATT_BK && (j + 1 < nkt || has_next))
+        st_shared_v4(sb + SM::KT + (st ^ 1) * SM::K_BYTES + kmajor_off(threadIdx.x, CP, ATT_BK), nb, 0u, 0u, 0u);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < ATT_BK / 16; ++kk) {
+          uint64_t bd = make_sdesc(sb + SM::VT + st * SM::V_BYTES + kk * 2 * (CV / 8) * 128, (CV / 8) * 128, 128);
+          att_mma_ts(tmem + T_O, tmem + kk * 8, bd, IDESC_O, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        mma_commit(&bar_o);
+      }
     }
-    // the next tile's per-key bias into its K tile's bias group (stage st^1, loaded above)
-    if (per_key_bias && threadIdx.x < ATT_BK && j + 1 < nkt)
-      st_shared_v4(sb + SM::KT + (st ^ 1) * SM::K_BYTES + kmajor_off(threadIdx.x, CP, ATT_BK), nb, 0u, 0u, 0u);
-    tmem_st_wait();
+    // O and l of this row (the next unit's first PV overwrites O only after the __syncthreads
+    // at the top of its first tile, which every thread reaches after these TMEM loads)
+    mbar_wait(&bar_o, (gt - 1) & 1);
+    tc_fence_after();
+    float o_acc[CV];
+#pragma unroll
+    for (int cc = 0; cc < CV; cc += 8) att_tmem_ld8(t_row + T_O + cc, o_acc + cc);
+    tmem_ld_wait();
     tc_fence_before();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      tc_fence_after();
-#pragma unroll
-      for (int kk = 0; kk < ATT_BK / 16; ++kk) {
-        uint64_t bd = make_sdesc(sb + SM::VT + st * SM::V_BYTES + kk * 2 * (CV / 8) * 128, (CV / 8) * 128, 128);
-        att_mma_ts(tmem + T_O, tmem + kk * 8, bd, IDESC_O, (j > 0 || kk > 0) ? 1u : 0u);
-      }
-      mma_commit(&bar_o);
-    }
-  }
-  // O and l of this row
-  mbar_wait(&bar_o, (nkt - 1) & 1);
-  tc_fence_after();
-  float o_acc[CV];
-#pragma unroll
-  for (int cc = 0; cc < CV; cc += 8) att_tmem_ld8(t_row + T_O + cc, o_acc + cc);
-  tmem_ld_wait();
-  const float l_run = o_acc[CP];
+    const float l_run = o_acc[CP];
 
-  if (qi < L) {
-    const float inv = rcpf(l_run);
-    const bf16* gp = P.g + b * P.g_sb + (int64_t)qi * P.g_sl + (int64_t)h * c;
-    bf16* og = P.og + b * P.o_sb + (int64_t)qi * P.o_sl + (int64_t)h * c;
-    bf16* orw = P.orw ? P.orw + b * P.r_sb + (int64_t)qi * P.r_sl + (int64_t)h * c : nullptr;
+    if (qi < L) {
+      const float inv = rcpf(l_run);
+      const bf16* gp = P.g + b * P.g_sb + (int64_t)qi * P.g_sl + (int64_t)h * c;
+      bf16* og = P.og + b * P.o_sb + (int64_t)qi * P.o_sl + (int64_t)h * c;
+      bf16* orw = P.orw ? P.orw + b * P.r_sb + (int64_t)qi * P.r_sl + (int64_t)h * c : nullptr;
 #pragma unroll
-    for (int d = 0; d < CP; d += 8) {
-      if (d < c) {
-        float o[8], gv[8];
-        uint4 u = *reinterpret_cast<const uint4*>(gp + d);
-        unpack_bf16x2(u.x, gv[0], gv[1]); unpack_bf16x2(u.y, gv[2], gv[3]);
-        unpack_bf16x2(u.z, gv[4], gv[5]); unpack_bf16x2(u.w, gv[6], gv[7]);
+      for (int d = 0; d < CP; d += 8) {
+        if (d < c) {
+          float o[8], gv[8];
+          uint4 w0 = *reinterpret_cast<const uint4*>(gp + d);
+          unpack_bf16x2(w0.x, gv[0], gv[1]); unpack_bf16x2(w0.y, gv[2], gv[3]);
+          unpack_bf16x2(w0.z, gv[4], gv[5]); unpack_bf16x2(w0.w, gv[6], gv[7]);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = o_acc[d + e] * inv;
-        if (orw) {
+          for (int e = 0; e < 8; ++e) o[e] = o_acc[d + e] * inv;
+          if (orw) {
+            uint4 w;
+            w.x = pack_bf16x2(o[0], o[1]); w.y = pack_bf16x2(o[2], o[3]);
+            w.z = pack_bf16x2(o[4], o[5]); w.w = pack_bf16x2(o[6], o[7]);
+            *reinterpret_cast<uint4*>(orw + d) = w;
+          }
+#pragma unroll
+          for (int e = 0; e < 8; ++e) o[e] *= sigmoidf_(gv[e]);
           uint4 w;
           w.x = pack_bf16x2(o[0], o[1]); w.y = pack_bf16x2(o[2], o[3]);
           w.z = pack_bf16x2(o[4], o[5]); w.w = pack_bf16x2(o[6], o[7]);
-          *reinterpret_cast<uint4*>(orw + d) = w;
+          *reinterpret_cast<uint4*>(og + d) = w;
         }
-#pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] *= sigmoidf_(gv[e]);
-        uint4 w;
-        w.x = pack_bf16x2(o[0], o[1]); w.y = pack_bf16x2(o[2], o[3]);
-        w.z = pack_bf16x2(o[4], o[5]); w.w = pack_bf16x2(o[6], o[7]);
-        *reinterpret_cast<uint4*>(og + d) = w;
       }
+      if (P.lse) P.lse[(b * P.H + h) * (int64_t)L + qi] = (m_run + log2f(l_run)) * 0.6931471805599453f;
     }
-    if (P.lse) P.lse[(b * P.H + h) * (int64_t)L + qi] = (m_run + log2f(l_run)) * 0.6931471805599453f;
+    u = nu;
+    cur = nxt;
   }
 
-  tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc(tmem, TCOLS);
 }
 
 static bool a16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
-template <int CP>
-static int launch_attn_fwd(const AttnParams& p, int64_t B, cudaStream_t st) {
+template <int CP, bool FB>
+static int launch_attn_fwd_v(const AttnParams& p, int64_t B, cudaStream_t st) {
   using SM = AttnSmem<CP>;
+  constexpr uint32_t bytes = FB ? SM::TOTAL_FB : SM::TOTAL;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<CP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM::TOTAL);
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<CP, FB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return cuda_status(e, "attn fwd attr");
     attr = true;
   }
-  dim3 grid((unsigned)((p.L + ATT_BQ - 1) / ATT_BQ), (unsigned)p.H, (unsigned)B);
-  attn_fwd_kernel<CP><<<grid, 128, SM::TOTAL, st>>>(p);
+  // resident CTAs per SM: the launch bound (registers; TMEM 4 x 128 columns) or what fits in
+  // 228 KB of shared memory (1 KB reserved per CTA), whichever is smaller.  The persistent grid
+  // is exactly one wave: measured, a grid above the resident count is slower (uneven tails).
+  constexpr int occ_lb = CP == 64 ? 2 : ((FB || EVO_EXP == 1) ? 3 : 4);
+  constexpr int occ_sm = (int)((228u * 1024u) / (bytes + 1024u + 64u));
+  static int occ = occ_lb < occ_sm ? occ_lb : occ_sm;
+  if (EVO_EXP == 2) {
+    if (const char* ev = getenv("EVO_FWD_OCC")) occ = atoi(ev);
+  }
+  const int64_t nunits = (int64_t)((p.L + ATT_BQ - 1) / ATT_BQ) * p.H * B;
+  EVO_CHECK_ARG(nunits < (1ll << 31), EVO_ERR_SHAPE, "attention fwd: too many (batch, head, query tile) units");
+  const int64_t cap = (int64_t)occ * sm_count();
+  attn_fwd_kernel<CP, FB><<<(unsigned)(nunits < cap ? nunits : cap), 128, bytes, st>>>(p, (int)nunits);
   EVO_LAUNCH_CHECK("attention fwd");
   return EVO_OK;
+}
+
+static int g_fwd_fb = 1;  // stage a full bias through smem (evo_attention_fwd_full_bias_smem: A/B switch)
+
+template <int CP>
+static int launch_attn_fwd(const AttnParams& p, int64_t B, cudaStream_t st) {
+  if (g_fwd_fb && p.bias && p.bs2 != 0 && p.bias_vec) return launch_attn_fwd_v<CP, true>(p, B, st);
+  return launch_attn_fwd_v<CP, false>(p, B, st);
 }
 
 int attn_params_from_desc(const EvoAttnDesc* d, AttnParams& p) {
@@ -383,6 +503,12 @@ int launch_attn_fwd_ws(const AttnParams& p, int64_t B, cudaStream_t st);
 // sequences at least this long take the warp-specialised kernel (attention_ws.cu)
 static int g_ws_min_len = 4096;  // measured: faster than attn_fwd_kernel from N_r = 4096 on (per-key/no bias)
 }  // namespace evo
+
+extern "C" int evo_attention_fwd_full_bias_smem(int on) {
+  const int old = g_fwd_fb;
+  if (on >= 0) g_fwd_fb = on;
+  return old;
+}
 
 extern "C" int evo_attention_fwd_ws_min_len(int len) {
   const int old = g_ws_min_len;

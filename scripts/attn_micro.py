@@ -10,7 +10,10 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--variant", default="all")
 ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--bwd", type=int, default=1)
+ap.add_argument("--fb", type=int, default=1, help="forward: stage a full bias through smem (A/B switch)")
 a = ap.parse_args()
+from paper_2203_00854_b200 import _lib
+_lib.load().evo_attention_fwd_full_bias_smem(a.fb)
 # (name, B, L, H, c, kind, bias)
 V = [("msa_row", 128, 256, 8, 32, "row", "full"), ("msa_col", 256, 128, 8, 32, "col", None),
      ("pair_row", 256, 256, 4, 32, "row", "key"), ("pair_col", 256, 256, 4, 32, "col", "key")]
