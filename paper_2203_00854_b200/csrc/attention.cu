@@ -40,6 +40,9 @@ struct AttnSmem {
   static constexpr int BROW = ATT_BK + 8;
   static constexpr uint32_t BS = TOTAL, BS_BYTES = ATT_BQ * BROW * 2;
   static constexpr uint32_t TOTAL_FB = BS + 2 * BS_BYTES;
+  // gate rows of the unit's queries for the epilogue (non-FB variant only: FB needs the room)
+  static constexpr uint32_t GT = TOTAL, GT_BYTES = ATT_BQ * CP * 2;
+  static constexpr uint32_t TOTAL_G = GT + GT_BYTES;
 };
 
 // 128 query rows x 64 keys of a full bias into smem (rows padded to BROW): 4 rows of 128
@@ -134,9 +137,12 @@ int sm_count();
 // unit already prefetches the next unit's first K/V tile, and the next unit's Q follows as
 // soon as this unit's last S MMA has read Q: the next unit's load latency hides under this
 // unit's last softmax and epilogue.
-template <int CP, bool FB>
-__global__ void __launch_bounds__(128, CP == 64 ? 2 : ((FB || EVO_EXP == 1) ? 3 : 4)) attn_fwd_kernel(AttnParams P,
-                                                                                                      int nunits) {
+// VAR: 0 = no bias (gate rows prefetched into smem for the epilogue), 1 = per-key bias or a
+// generic full bias (global loads), 2 = full bias staged through smem (FB)
+template <int CP, int VAR>
+__global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1) ? 3 : 4)) attn_fwd_kernel(AttnParams P,
+                                                                                                          int nunits) {
+  constexpr bool FB = VAR == 2, GS = VAR == 0;
   using SM = AttnSmem<CP>;
   constexpr int CQ = SM::CQ, CV = SM::CV;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -148,7 +154,7 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((FB || EVO_EXP == 1) ? 3 
   const int L = P.L, c = P.c, H = P.H;
   const int nqt = (L + ATT_BQ - 1) / ATT_BQ;
   const int r = warp * 32 + lane;  // query row inside the tile
-  const bool per_key_bias = P.bias && P.bs2 == 0;
+  const bool per_key_bias = VAR == 1 && P.bias && P.bs2 == 0;
   constexpr uint32_t ONE_BF16 = 0x3F80u;
   const int nkt = (L + ATT_BK - 1) / ATT_BK;
 
@@ -233,7 +239,7 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((FB || EVO_EXP == 1) ? 3 
     const bf16* bfull = bfull_of(cur);
     float m_run = -INFINITY;  // running max, scaled log2 units
     const bf16* brow = nullptr;
-    if (!FB && P.bias && !per_key_bias && qi < L) brow = P.bias + b * P.bs0 + (int64_t)h * P.bs1 + (int64_t)qi * P.bs2;
+    if (VAR == 1 && P.bias && !per_key_bias && qi < L) brow = P.bias + b * P.bs0 + (int64_t)h * P.bs1 + (int64_t)qi * P.bs2;
     uint32_t nb = 0;  // next tile's per-key bias (threads 0..63), stored with its K tile
 
     for (int j = 0; j < nkt; ++j, ++gt) {
@@ -261,6 +267,13 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((FB || EVO_EXP == 1) ? 3 
           nb = (int)threadIdx.x < L ? (uint32_t)kbias_of(nxt)[(int64_t)threadIdx.x * P.bs3] : 0u;
       }
       cp_async_commit();
+      if (GS && j + 1 == nkt && qi < L) {  // this unit's gate rows (own row: no barrier needed)
+        const bf16* gsrc = P.g + b * P.g_sb + (int64_t)qi * P.g_sl + (int64_t)h * c;
+#pragma unroll
+        for (int d = 0; d < CP; d += 8)
+          if (d < c) cp_async16(sb + SM::GT + r * (CP * 2) + d * 2, gsrc + d, true);
+      }
+      if (GS) cp_async_commit();
 
       if (threadIdx.x == 0) {
         // S overwrites the columns the previous tile's P was read from: its PV must be complete
@@ -393,6 +406,10 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((FB || EVO_EXP == 1) ? 3 
     tc_fence_before();
     const float l_run = o_acc[CP];
 
+    if (GS) {  // the gate group: only the next unit's Q group may still be in flight
+      if (has_next) cp_async_wait<1>();
+      else cp_async_wait<0>();
+    }
     if (qi < L) {
       const float inv = rcpf(l_run);
       const bf16* gp = P.g + b * P.g_sb + (int64_t)qi * P.g_sl + (int64_t)h * c;
@@ -402,7 +419,13 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((FB || EVO_EXP == 1) ? 3 
       for (int d = 0; d < CP; d += 8) {
         if (d < c) {
           float o[8], gv[8];
-          uint4 w0 = *reinterpret_cast<const uint4*>(gp + d);
+          uint4 w0;
+          if (!GS) {
+            w0 = *reinterpret_cast<const uint4*>(gp + d);
+          } else {
+            asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];\n" : "=r"(w0.x), "=r"(w0.y), "=r"(w0.z), "=r"(w0.w)
+                         : "r"(sb + SM::GT + r * (CP * 2) + d * 2));
+          }
           unpack_bf16x2(w0.x, gv[0], gv[1]); unpack_bf16x2(w0.y, gv[2], gv[3]);
           unpack_bf16x2(w0.z, gv[4], gv[5]); unpack_bf16x2(w0.w, gv[6], gv[7]);
 #pragma unroll
@@ -433,13 +456,14 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((FB || EVO_EXP == 1) ? 3 
 
 static bool a16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
-template <int CP, bool FB>
+template <int CP, int VAR>
 static int launch_attn_fwd_v(const AttnParams& p, int64_t B, cudaStream_t st) {
   using SM = AttnSmem<CP>;
-  constexpr uint32_t bytes = FB ? SM::TOTAL_FB : SM::TOTAL;
+  constexpr bool FB = VAR == 2;
+  constexpr uint32_t bytes = FB ? SM::TOTAL_FB : (VAR == 0 ? SM::TOTAL_G : SM::TOTAL);
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<CP, FB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<CP, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return cuda_status(e, "attn fwd attr");
     attr = true;
   }
@@ -455,7 +479,7 @@ static int launch_attn_fwd_v(const AttnParams& p, int64_t B, cudaStream_t st) {
   const int64_t nunits = (int64_t)((p.L + ATT_BQ - 1) / ATT_BQ) * p.H * B;
   EVO_CHECK_ARG(nunits < (1ll << 31), EVO_ERR_SHAPE, "attention fwd: too many (batch, head, query tile) units");
   const int64_t cap = (int64_t)occ * sm_count();
-  attn_fwd_kernel<CP, FB><<<(unsigned)(nunits < cap ? nunits : cap), 128, bytes, st>>>(p, (int)nunits);
+  attn_fwd_kernel<CP, VAR><<<(unsigned)(nunits < cap ? nunits : cap), 128, bytes, st>>>(p, (int)nunits);
   EVO_LAUNCH_CHECK("attention fwd");
   return EVO_OK;
 }
@@ -464,8 +488,9 @@ static int g_fwd_fb = 1;  // stage a full bias through smem (evo_attention_fwd_f
 
 template <int CP>
 static int launch_attn_fwd(const AttnParams& p, int64_t B, cudaStream_t st) {
-  if (g_fwd_fb && p.bias && p.bs2 != 0 && p.bias_vec) return launch_attn_fwd_v<CP, true>(p, B, st);
-  return launch_attn_fwd_v<CP, false>(p, B, st);
+  if (!p.bias) return launch_attn_fwd_v<CP, 0>(p, B, st);
+  if (g_fwd_fb && p.bs2 != 0 && p.bias_vec) return launch_attn_fwd_v<CP, 2>(p, B, st);
+  return launch_attn_fwd_v<CP, 1>(p, B, st);
 }
 
 int attn_params_from_desc(const EvoAttnDesc* d, AttnParams& p) {
