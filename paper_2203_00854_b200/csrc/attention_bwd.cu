@@ -211,17 +211,41 @@ constexpr int BW_BQ = 128;  // queries per iteration
 
 template <int CP>
 struct BwdSmem {
+  // PTM (head dim <= 32): P^T lives in TMEM (the dV MMA reads its A operand from there), and
+  // the freed 32 KB double-buffer the per-query-tile operands (Q, dO, lse, D), so the next
+  // query tile is loaded while this one computes.  Head dim 64 keeps P^T in smem.
+  static constexpr bool PTM = CP <= 32;
+  static constexpr int NB = PTM ? 2 : 1;                    // query-tile operand buffers
   static constexpr uint32_t K = 0;                          // [key][d] K-major
   static constexpr uint32_t V = K + BW_BK * CP * 2;         // [key][d] K-major
-  static constexpr uint32_t Q = V + BW_BK * CP * 2;         // [query][d] K-major
-  static constexpr uint32_t DO = Q + BW_BQ * CP * 2;        // [query][d] K-major
-  static constexpr uint32_t PT = DO + BW_BQ * CP * 2;       // [key][query] K-major
-  static constexpr uint32_t DST = PT + BW_BK * BW_BQ * 2;   // [key][query] K-major
-  static constexpr uint32_t LSE = DST + BW_BK * BW_BQ * 2;  // fp32 [128]
-  static constexpr uint32_t DD = LSE + BW_BQ * 4;           // fp32 [128]
-  static constexpr uint32_t KB = DD + BW_BQ * 4;            // fp32 [2][128] per-key dbias partials
+  static constexpr uint32_t Q = V + BW_BK * CP * 2;         // NB x [query][d] K-major
+  static constexpr uint32_t QD_BYTES = BW_BQ * CP * 2;
+  static constexpr uint32_t DO = Q + NB * QD_BYTES;         // NB x [query][d] K-major
+  static constexpr uint32_t PT = DO + NB * QD_BYTES;        // [key][query] K-major (!PTM)
+  static constexpr uint32_t DST = PT + (PTM ? 0 : BW_BK * BW_BQ * 2);  // [key][query] K-major
+  static constexpr uint32_t LSE = DST + BW_BK * BW_BQ * 2;  // NB x fp32 [128]
+  static constexpr uint32_t DD = LSE + NB * BW_BQ * 4;      // NB x fp32 [128]
+  static constexpr uint32_t KB = DD + NB * BW_BQ * 4;       // fp32 [2][128] per-key dbias partials
   static constexpr uint32_t TOTAL = KB + 2 * BW_BK * 4;
 };
+
+__device__ __forceinline__ void bw_tmem_st8(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+// D (+)= A[tmem] * B[smem]: A operand (M = 128 lanes, 2 bf16 per 32-bit column) in TMEM
+__device__ __forceinline__ void bw_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 
 template <int CP>
 __device__ __forceinline__ void bw_load(uint32_t sdst, const bf16* base, int64_t row_stride, int row0, int nvalid,
@@ -249,8 +273,7 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
   __shared__ uint64_t bar1, bar2;
   __shared__ uint32_t tmem_sh;
   const uint32_t sb = smem_u32(smem);
-  float* s_lse = reinterpret_cast<float*>(smem + SM::LSE);
-  float* s_D = reinterpret_cast<float*>(smem + SM::DD);
+  constexpr bool PTM = SM::PTM;
   float* s_kb = reinterpret_cast<float*>(smem + SM::KB);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -276,26 +299,27 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
   const int64_t HC = (int64_t)H * c;
   // every per-tile operand is a cp.async copy (dO, D and lse*log2e come from the prep kernel)
   const bool vec_stats = (L & 3) == 0;
-  auto issue_loads = [&](int64_t b, int h, int k0, int qt, bool with_kv) {
+  auto issue_loads = [&](int64_t b, int h, int k0, int qt, bool with_kv, int buf) {
     const int q0 = qt * BW_BQ;
     if (with_kv) {
       bw_load<CP>(sb + SM::K, F.k + b * F.k_sb + (int64_t)h * c, F.k_sl, k0, L - k0, c);
       bw_load<CP>(sb + SM::V, F.v + b * F.v_sb + (int64_t)h * c, F.v_sl, k0, L - k0, c);
     }
-    bw_load<CP>(sb + SM::Q, F.q + b * F.q_sb + (int64_t)h * c, F.q_sl, q0, L - q0, c);
-    bw_load<CP>(sb + SM::DO, P.dO + b * L * HC + (int64_t)h * c, HC, q0, L - q0, c);
+    bw_load<CP>(sb + SM::Q + buf * SM::QD_BYTES, F.q + b * F.q_sb + (int64_t)h * c, F.q_sl, q0, L - q0, c);
+    bw_load<CP>(sb + SM::DO + buf * SM::QD_BYTES, P.dO + b * L * HC + (int64_t)h * c, HC, q0, L - q0, c);
     const int64_t st0 = (b * H + h) * (int64_t)L + q0;
+    const uint32_t lse_b = SM::LSE + buf * BW_BQ * 4, dd_b = SM::DD + buf * BW_BQ * 4;
     if (vec_stats) {
       if (threadIdx.x < 2 * BW_BQ / 4) {
         const int t = threadIdx.x & (BW_BQ / 4 - 1);
         const bool ok = q0 + 4 * t < L;
         const float* src = threadIdx.x < BW_BQ / 4 ? P.lse2 : P.Dsum;
-        cp_async16(sb + (threadIdx.x < BW_BQ / 4 ? SM::LSE : SM::DD) + 16 * t, ok ? src + st0 + 4 * t : src, ok);
+        cp_async16(sb + (threadIdx.x < BW_BQ / 4 ? lse_b : dd_b) + 16 * t, ok ? src + st0 + 4 * t : src, ok);
       }
     } else if (threadIdx.x < BW_BQ) {
       const bool ok = q0 + (int)threadIdx.x < L;
-      s_lse[threadIdx.x] = ok ? P.lse2[st0 + threadIdx.x] : 0.f;
-      s_D[threadIdx.x] = ok ? P.Dsum[st0 + threadIdx.x] : 0.f;
+      reinterpret_cast<float*>(smem + lse_b)[threadIdx.x] = ok ? P.lse2[st0 + threadIdx.x] : 0.f;
+      reinterpret_cast<float*>(smem + dd_b)[threadIdx.x] = ok ? P.Dsum[st0 + threadIdx.x] : 0.f;
     }
     cp_async_commit();
   };
@@ -309,14 +333,17 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
     int64_t b0;
     int h0, kt0;
     decode(blockIdx.x, b0, h0, kt0);
-    if ((int64_t)blockIdx.x < units) issue_loads(b0, h0, kt0 * BW_BK, 0, true);
+    if ((int64_t)blockIdx.x < units) issue_loads(b0, h0, kt0 * BW_BK, 0, true, 0);
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_sh;
   const uint32_t t_lane = tmem + ((uint32_t)(wq * 32) << 16);
-  constexpr uint32_t T_S = 0, T_DP = 128, T_DV = 0, T_DK = CP, T_DQ = 2 * CP;
+  // S^T [0,128) (PTM: P^T packed bf16 over it at wg*64 + part*8), dP^T [128,256); the
+  // dV/dK/dQ products go where no operand of their own MMAs lives
+  constexpr uint32_t T_S = 0, T_DP = 128;
+  constexpr uint32_t T_DV = PTM ? 128 : 0, T_DK = T_DV + CP, T_DQ = T_DV + 2 * CP;
 
   constexpr uint32_t ID_SS = make_idesc_bf16(128, 128, 0, 0);  // S^T = K Q^T, dP^T = V dO^T
   constexpr uint32_t ID_KV = make_idesc_bf16(128, CP, 0, 1);   // dV = P^T dO, dK = dS^T Q  (B: MN-major view)
@@ -343,18 +370,25 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
     const int bs2 = (int)F.bs2;  // full-bias query stride (< 2^31)
     for (int qt = 0; qt < nqt; ++qt, ++it) {
       const int q0 = qt * BW_BQ;
+      const int buf = PTM ? (it & 1) : 0;
+      const uint32_t sQ = sb + SM::Q + buf * SM::QD_BYTES, sDO = sb + SM::DO + buf * SM::QD_BYTES;
+      const float* s_lse = reinterpret_cast<const float*>(smem + SM::LSE + buf * BW_BQ * 4);
+      const float* s_D = reinterpret_cast<const float*>(smem + SM::DD + buf * BW_BQ * 4);
       cp_async_wait<0>();
       fence_async_smem();
       __syncthreads();
+      // double-buffered: the next query tile of this unit loads while this one computes (the
+      // other buffer's last reader, the previous tile's MMAs, completed before this barrier)
+      if (PTM && qt + 1 < nqt) issue_loads(b, h, k0, qt + 1, false, buf ^ 1);
       if (threadIdx.x == 0) {
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < CP / 16; ++kk) {
           const uint32_t koff = kk * 2 * LBO_ROWS;
-          mma_bf16(tmem + T_S, make_sdesc(sb + SM::K + koff, LBO_ROWS, 128),
-                   make_sdesc(sb + SM::Q + koff, LBO_ROWS, 128), ID_SS, kk != 0);
-          mma_bf16(tmem + T_DP, make_sdesc(sb + SM::V + koff, LBO_ROWS, 128),
-                   make_sdesc(sb + SM::DO + koff, LBO_ROWS, 128), ID_SS, kk != 0);
+          mma_bf16(tmem + T_S, make_sdesc(sb + SM::K + koff, LBO_ROWS, 128), make_sdesc(sQ + koff, LBO_ROWS, 128),
+                   ID_SS, kk != 0);
+          mma_bf16(tmem + T_DP, make_sdesc(sb + SM::V + koff, LBO_ROWS, 128), make_sdesc(sDO + koff, LBO_ROWS, 128),
+                   ID_SS, kk != 0);
         }
         mma_commit(&bar1);
       }
@@ -434,11 +468,18 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
               if (q0 + qc + e < L) atomicAdd(dbias_col + (int64_t)(q0 + qc + e) * P.db2, P.scale * dsv[e]);
           }
         }
+        if constexpr (PTM) {  // P^T over the S^T columns this warp has already read
+          uint32_t pk[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) pk[e] = pack_bf16x2(pv[2 * e], pv[2 * e + 1]);
+          bw_tmem_st8(t_lane + T_S + wg * 64 + part * 8, pk);
+        }
 #pragma unroll
         for (int e = 0; e < 16; e += 8) {
-          st_shared_v4(sb + SM::PT + kmajor_off(kr, qc + e, 128), pack_bf16x2(pv[e], pv[e + 1]),
-                       pack_bf16x2(pv[e + 2], pv[e + 3]), pack_bf16x2(pv[e + 4], pv[e + 5]),
-                       pack_bf16x2(pv[e + 6], pv[e + 7]));
+          if constexpr (!PTM)
+            st_shared_v4(sb + SM::PT + kmajor_off(kr, qc + e, 128), pack_bf16x2(pv[e], pv[e + 1]),
+                         pack_bf16x2(pv[e + 2], pv[e + 3]), pack_bf16x2(pv[e + 4], pv[e + 5]),
+                         pack_bf16x2(pv[e + 6], pv[e + 7]));
           st_shared_v4(sb + SM::DST + kmajor_off(kr, qc + e, 128), pack_bf16x2(dsv[e], dsv[e + 1]),
                        pack_bf16x2(dsv[e + 2], dsv[e + 3]), pack_bf16x2(dsv[e + 4], dsv[e + 5]),
                        pack_bf16x2(dsv[e + 6], dsv[e + 7]));
@@ -446,6 +487,7 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
       }
       if (db_per_key) s_kb[wg * BW_BK + kr] = kb_acc;
 
+      if (PTM) tmem_st_wait();
       fence_async_smem();
       tc_fence_before();
       __syncthreads();
@@ -457,10 +499,14 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
         for (int kk = 0; kk < BW_BQ / 16; ++kk) {
           const uint32_t aoff = kk * 2 * LBO_ROWS;
           const uint32_t boff = kk * 2 * 128;
-          mma_bf16(tmem + T_DV, make_sdesc(sb + SM::PT + aoff, LBO_ROWS, 128),
-                   make_sdesc(sb + SM::DO + boff, 128, LBO_ROWS), ID_KV, kk != 0);
-          mma_bf16(tmem + T_DK, make_sdesc(sb + SM::DST + aoff, LBO_ROWS, 128),
-                   make_sdesc(sb + SM::Q + boff, 128, LBO_ROWS), ID_KV, kk != 0);
+          if constexpr (PTM)  // queries [0,64) at columns [0,32), [64,128) at [64,96)
+            bw_mma_ts(tmem + T_DV, tmem + T_S + (kk < 4 ? kk * 8 : 64 + (kk - 4) * 8),
+                      make_sdesc(sDO + boff, 128, LBO_ROWS), ID_KV, kk != 0);
+          else
+            mma_bf16(tmem + T_DV, make_sdesc(sb + SM::PT + aoff, LBO_ROWS, 128), make_sdesc(sDO + boff, 128, LBO_ROWS),
+                     ID_KV, kk != 0);
+          mma_bf16(tmem + T_DK, make_sdesc(sb + SM::DST + aoff, LBO_ROWS, 128), make_sdesc(sQ + boff, 128, LBO_ROWS),
+                   ID_KV, kk != 0);
         }
 #pragma unroll
         for (int kk = 0; kk < BW_BK / 16; ++kk) {
@@ -476,12 +522,12 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
       // the tiles are free: prefetch the next (batch, query tile) while draining TMEM
       const bool last_q = qt + 1 == nqt;
       if (!last_q) {
-        issue_loads(b, h, k0, qt + 1, false);
+        if (!PTM) issue_loads(b, h, k0, qt + 1, false, 0);
       } else if (u + gridDim.x < units) {
         int64_t nb;
         int nh, nkt_;
         decode(u + gridDim.x, nb, nh, nkt_);
-        issue_loads(nb, nh, nkt_ * BW_BK, 0, true);
+        issue_loads(nb, nh, nkt_ * BW_BK, 0, true, PTM ? (buf ^ 1) : 0);
       }
       if constexpr (db_store) {
         // dS^T tile (unscaled bf16, canonical K-major [key][query]) -> workspace [b][h][key][query]:
