@@ -138,15 +138,22 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
 // g, o, lse) before any math, so it pays one memory latency per PREP_PASSES passes.  The
 // lanes of one head are consecutive and never straddle rows (c/8 divides 32 and H*c/8).
 constexpr int PREP_PASSES = 4;
+// STAGED (when H*c/8 divides the CTA's 1024 chunks, i.e. the CTA covers whole rows): the
+// per-(b, h, l) statistics D and lse*log2e go through smem and are written (and lse read) as
+// runs of consecutive l per head instead of one scattered 4-byte access per head and row.
+template <bool STAGED>
 __global__ void __launch_bounds__(256) attn_bwd_prep(AttnBwdParams P, int64_t B) {
+  constexpr int PER_CTA = 8 * PREP_PASSES * 32;
+  __shared__ float s_D[STAGED ? PER_CTA : 1];
   const int lane = threadIdx.x & 31;
   const int L = P.f.L, H = P.f.H, c = P.f.c;
   const uint32_t nch = H * c / 8;
   // 32-bit (row, chunk) / (b, l) divisions: the host guarantees B*L*nch < 2^31
   const uint32_t total = (uint32_t)(B * L * nch);
   const uint32_t f0 = ((uint32_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * (PREP_PASSES * 32);
-  if (f0 >= total) return;
+  if (!STAGED && f0 >= total) return;
   const int lanes_per_head = c / 8;  // 1, 2, 4 or 8
+  const uint32_t row0 = (uint32_t)blockIdx.x * (PER_CTA / nch);  // STAGED: first row of this CTA
   uint4 ud[PREP_PASSES], ug[PREP_PASSES], uo[PREP_PASSES];
   float lse[PREP_PASSES];
 #pragma unroll
@@ -160,7 +167,7 @@ __global__ void __launch_bounds__(256) attn_bwd_prep(AttnBwdParams P, int64_t B)
       ud[t] = *reinterpret_cast<const uint4*>(P.dout + b * P.do_sb + l * P.do_sl + col);
       ug[t] = *reinterpret_cast<const uint4*>(P.f.g + b * P.f.g_sb + l * P.f.g_sl + col);
       uo[t] = *reinterpret_cast<const uint4*>(P.f.orw + b * P.f.r_sb + l * P.f.r_sl + col);
-      lse[t] = (lane % lanes_per_head) == 0 ? P.f.lse[(b * H + col / c) * (int64_t)L + l] : 0.f;
+      if (!STAGED) lse[t] = (lane % lanes_per_head) == 0 ? P.f.lse[(b * H + col / c) * (int64_t)L + l] : 0.f;
     }
   }
 #pragma unroll
@@ -198,9 +205,28 @@ __global__ void __launch_bounds__(256) attn_bwd_prep(AttnBwdParams P, int64_t B)
     // segmented reduction over the lanes of one head (lanes_per_head is a power of 2)
     for (int o = 1; o < lanes_per_head; o <<= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
     if (ok && (lane % lanes_per_head) == 0) {
-      const int64_t ix = (b * H + col / c) * (int64_t)L + l;
-      P.Dsum[ix] = dsum;
-      P.lse2[ix] = lse[t] * 1.4426950408889634f;
+      if (STAGED) {
+        s_D[(row - row0) * H + col / c] = dsum;
+      } else {
+        const int64_t ix = (b * H + col / c) * (int64_t)L + l;
+        P.Dsum[ix] = dsum;
+        P.lse2[ix] = lse[t] * 1.4426950408889634f;
+      }
+    }
+  }
+  if (STAGED) {
+    __syncthreads();
+    const int R = PER_CTA / (int)nch;
+    const uint32_t rows = (uint32_t)(B * L);
+    for (int i = threadIdx.x; i < R * H; i += 256) {
+      const int h = i / R, rl = i - h * R;
+      const uint32_t row = row0 + rl;
+      if (row < rows) {
+        const uint32_t bu = row / (uint32_t)L;
+        const int64_t ix = ((int64_t)bu * H + h) * L + (row - bu * (uint32_t)L);
+        P.Dsum[ix] = s_D[rl * H + h];
+        P.lse2[ix] = P.f.lse[ix] * 1.4426950408889634f;
+      }
     }
   }
 }
@@ -768,7 +794,9 @@ extern "C" int evo_gated_attention_bwd(const EvoAttnBwdDesc* d, void* stream) {
   {
     const int64_t rows = B * L;
     const int64_t pairs = rows * (H * c / 8), per_cta = 8 * PREP_PASSES * 32;
-    attn_bwd_prep<<<(unsigned)((pairs + per_cta - 1) / per_cta), 256, 0, st>>>(p, B);
+    const unsigned g = (unsigned)((pairs + per_cta - 1) / per_cta);
+    if (per_cta % (H * c / 8) == 0) attn_bwd_prep<true><<<g, 256, 0, st>>>(p, B);
+    else attn_bwd_prep<false><<<g, 256, 0, st>>>(p, B);
     EVO_LAUNCH_CHECK("attention bwd prep");
   }
   if (p.dS) {
