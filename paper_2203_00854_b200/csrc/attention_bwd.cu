@@ -137,8 +137,8 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
 // consecutive pairs (no idle lanes for any H*c), and issues every global load of them (dout,
 // g, o, lse) before any math, so it pays one memory latency per PREP_PASSES passes.  The
 // lanes of one head are consecutive and never straddle rows (c/8 divides 32 and H*c/8).
-constexpr int PREP_PASSES = 4;
-// STAGED (when H*c/8 divides the CTA's 1024 chunks, i.e. the CTA covers whole rows): the
+constexpr int PREP_PASSES = 2;  // measured: 2 beats 4 (more resident CTAs, load/store phases overlap) and 1
+// STAGED (when H*c/8 divides the CTA's 8*32*PREP_PASSES chunks: the CTA covers whole rows): the
 // per-(b, h, l) statistics D and lse*log2e go through smem and are written (and lse read) as
 // runs of consecutive l per head instead of one scattered 4-byte access per head and row.
 template <bool STAGED>
