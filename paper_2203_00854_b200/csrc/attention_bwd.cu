@@ -606,17 +606,23 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
               for (int e = 0; e < CP / 2; ++e)
                 if (wg * (CP / 2) + e < c) dst[e] = f2bf(P.scale * w[e]);
             }
-          } else if (dq_partial) {
-            float* dst = P.dQacc + (((int64_t)kt * Btot + b) * L + qq) * HC + (int64_t)h * c + wg * (CP / 2);
-            if (wg * (CP / 2) + CP / 2 <= c) {
+          } else if (dq_partial) {  // per-key-tile bf16 partial, summed in fp32 by the finish pass
+            bf16* dst = reinterpret_cast<bf16*>(P.dQacc) + (((int64_t)kt * Btot + b) * L + qq) * HC + (int64_t)h * c +
+                        wg * (CP / 2);
+            if (wg * (CP / 2) + CP / 2 <= c && (CP / 2) % 8 == 0) {
 #pragma unroll
-              for (int e = 0; e < CP / 2; e += 4)
-                *reinterpret_cast<float4*>(dst + e) =
-                    make_float4(P.scale * w[e], P.scale * w[e + 1], P.scale * w[e + 2], P.scale * w[e + 3]);
+              for (int e = 0; e < CP / 2; e += 8) {
+                uint4 u;
+                u.x = pack_bf16x2(P.scale * w[e], P.scale * w[e + 1]);
+                u.y = pack_bf16x2(P.scale * w[e + 2], P.scale * w[e + 3]);
+                u.z = pack_bf16x2(P.scale * w[e + 4], P.scale * w[e + 5]);
+                u.w = pack_bf16x2(P.scale * w[e + 6], P.scale * w[e + 7]);
+                *reinterpret_cast<uint4*>(dst + e) = u;
+              }
             } else {
 #pragma unroll
               for (int e = 0; e < CP / 2; ++e)
-                if (wg * (CP / 2) + e < c) dst[e] = P.scale * w[e];
+                if (wg * (CP / 2) + e < c) dst[e] = f2bf(P.scale * w[e]);
             }
           } else {
             float* dst = P.dQacc + (b * L + qq) * HC + (int64_t)h * c + wg * (CP / 2);
@@ -664,20 +670,27 @@ __global__ void __launch_bounds__(256) attn_bwd_dq_finish(AttnBwdParams P, int64
     const uint32_t eu = (uint32_t)e, hc = (uint32_t)(H * c);  // n < 2^31 (host-checked)
     const uint32_t rowu = eu / hc, bu = rowu / (uint32_t)L;
     const int64_t col = eu - rowu * hc, b = bu, l = rowu - bu * (uint32_t)L;
-    float4 a[NP], q[NP];
+    float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if constexpr (NP == 0) {  // one fp32 accumulator (atomics, > DQ_MAX_PARTS key tiles)
+      const float4 x0 = __ldcs(reinterpret_cast<const float4*>(P.dQacc + e));
+      const float4 x1 = __ldcs(reinterpret_cast<const float4*>(P.dQacc + e + 4));
+      a[0] = x0.x; a[1] = x0.y; a[2] = x0.z; a[3] = x0.w; a[4] = x1.x; a[5] = x1.y; a[6] = x1.z; a[7] = x1.w;
+    }
+    const bf16* part = reinterpret_cast<const bf16*>(P.dQacc);
+    uint4 raw[NP > 0 ? NP : 1];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) raw[p] = __ldcs(reinterpret_cast<const uint4*>(part + p * n + e));
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-      a[p] = __ldcs(reinterpret_cast<const float4*>(P.dQacc + p * n + e));
-      q[p] = __ldcs(reinterpret_cast<const float4*>(P.dQacc + p * n + e + 4));
-    }
+      float v[8];
+      unpack_bf16x2(raw[p].x, v[0], v[1]); unpack_bf16x2(raw[p].y, v[2], v[3]);
+      unpack_bf16x2(raw[p].z, v[4], v[5]); unpack_bf16x2(raw[p].w, v[6], v[7]);
 #pragma unroll
-    for (int p = 1; p < NP; ++p) {
-      a[0].x += a[p].x; a[0].y += a[p].y; a[0].z += a[p].z; a[0].w += a[p].w;
-      q[0].x += q[p].x; q[0].y += q[p].y; q[0].z += q[p].z; q[0].w += q[p].w;
+      for (int k = 0; k < 8; ++k) a[k] += v[k];
     }
     uint4 w;
-    w.x = pack_bf16x2(a[0].x, a[0].y); w.y = pack_bf16x2(a[0].z, a[0].w);
-    w.z = pack_bf16x2(q[0].x, q[0].y); w.w = pack_bf16x2(q[0].z, q[0].w);
+    w.x = pack_bf16x2(a[0], a[1]); w.y = pack_bf16x2(a[2], a[3]);
+    w.z = pack_bf16x2(a[4], a[5]); w.w = pack_bf16x2(a[6], a[7]);
     *reinterpret_cast<uint4*>(P.dq + b * P.dq_sb + l * P.dq_sl + col) = w;
   }
 }
@@ -691,7 +704,8 @@ static int64_t ws_layout(int64_t B, int64_t L, int H, int c, int bias_batch_redu
   const int64_t parts = nkt == 1 ? 0 : (nkt <= DQ_MAX_PARTS ? nkt : 1);
   const int64_t stats = ((B * H * L * 4 + 255) / 256) * 256;
   int64_t o1 = ((n * 2 + 255) / 256) * 256;
-  int64_t o2 = o1 + ((parts * n * 4 + 255) / 256) * 256;
+  // <= DQ_MAX_PARTS key tiles: bf16 partials; more: one fp32 atomic accumulator
+  int64_t o2 = o1 + ((parts * n * (nkt <= DQ_MAX_PARTS ? 2 : 4) + 255) / 256) * 256;
   int64_t o3 = o2 + stats;
   int64_t o4 = o3 + stats;
   if (off_dq) *off_dq = o1;
@@ -822,8 +836,8 @@ extern "C" int evo_gated_attention_bwd(const EvoAttnBwdDesc* d, void* stream) {
   int64_t n8 = B * L * H * c / 8;
   int64_t g = (n8 + 255) / 256, cap = (int64_t)sm_count() * 16;
   const unsigned gf = (unsigned)(g < cap ? g : cap);
-  switch (dq_partial ? (int)nkt : 1) {
-    case 1: attn_bwd_dq_finish<1><<<gf, 256, 0, st>>>(p, B); break;
+  switch (dq_partial ? (int)nkt : 0) {  // 0: fp32 atomic accumulator; 2..4: bf16 per-tile partials
+    case 0: attn_bwd_dq_finish<0><<<gf, 256, 0, st>>>(p, B); break;
     case 2: attn_bwd_dq_finish<2><<<gf, 256, 0, st>>>(p, B); break;
     case 3: attn_bwd_dq_finish<3><<<gf, 256, 0, st>>>(p, B); break;
     default: attn_bwd_dq_finish<4><<<gf, 256, 0, st>>>(p, B); break;
