@@ -235,9 +235,10 @@ def msa_row_bias_fwd(bp: BlockParams, z2d, n_i: int, n_j: int | None = None, sav
 
 
 def msa_row_bias_bwd(bp: BlockParams, sv: Saved, dbias, dz):
-    """dbias fp32 [nh, n_i, n_j]; accumulates into dz (bf16 [n_i*n_j, Hz]):
+    """dbias fp32 [nh, n_i, n_j]; returns dz + dLN/dz (bf16 [n_i*n_j, Hz]) as a NEW tensor:
     d LN = dbias^T W^T (one K = nh GEMM), dW = LN^T dbias^T (side stream), LN backward with
-    the residual-stream accumulate and dgamma / dbeta fused."""
+    the residual-stream add and dgamma / dbeta fused.  Out of place because dz may still be
+    read by side-stream weight-gradient GEMMs (opm's w_o) issued earlier in the block."""
     cfg = bp.cfg
     nh, Hz = cfg.n_head_msa, cfg.h_pair
     rows = dbias[0].numel()
@@ -251,8 +252,8 @@ def msa_row_bias_bwd(bp: BlockParams, sv: Saved, dbias, dz):
         db2h = db2.to(torch.bfloat16)
         gw = bp.g["msa_row.w_bias"]
         SideStream.run(lambda: gw[:, :nh].add_(torch.mm(sv["ln"].t(), db2h.t(), out_dtype=F32)), sv["ln"], db2h)
-    ops.layernorm_bwd(dln, sv["z"], bp.f["msa_row.lnz_g"], sv["mean"], sv["rstd"], rows, Hz, dx=dz,
-                      accumulate=True, dgamma=bp.g["msa_row.lnz_g"], dbeta=bp.g["msa_row.lnz_b"])
+    return ops.layernorm_bwd(dln, sv["z"], bp.f["msa_row.lnz_g"], sv["mean"], sv["rstd"], rows, Hz, res=dz,
+                             dgamma=bp.g["msa_row.lnz_g"], dbeta=bp.g["msa_row.lnz_b"])
 
 
 # ----------------------------------------------------------------------------- transition
@@ -517,7 +518,7 @@ def block_fwd(bp: BlockParams, m, z, save=True):
     return m2.view(S, R, cfg.h_msa), z2.view(R, R, cfg.h_pair), saved
 
 
-def block_bwd(bp: BlockParams, saved, dm, dz):
+def block_bwd(bp: BlockParams, saved, dm, dz, join=True):
     """gradients w.r.t. (m, z) of the block input; parameter grads accumulate into bp.grad."""
     cfg: EvoConfig = bp.cfg
     S, R = cfg.n_seq, cfg.n_res
@@ -539,6 +540,7 @@ def block_bwd(bp: BlockParams, saved, dm, dz):
     dm2 = transition_bwd(bp, s3, dm2, next_db=nd("msa_col.b_o"), db_done=fuse)
     dm2, _ = attention_bwd(bp, s2, dm2, next_db=nd("msa_row.b_o"), db_done=fuse)
     dm2, dbias = attention_bwd(bp, s1, dm2, db_done=fuse)
-    msa_row_bias_bwd(bp, sv_b, dbias, dz2)
-    SideStream.join()
+    dz2 = msa_row_bias_bwd(bp, sv_b, dbias, dz2)
+    if join:  # a stack joins once after its last block: side work then overlaps the next block
+        SideStream.join()
     return dm2.view(S, R, cfg.h_msa), dz2.view(R, R, cfg.h_pair)

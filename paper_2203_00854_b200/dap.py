@@ -377,7 +377,7 @@ def dap_block_bwd(bp, comm: DapComm, sv, dm_loc, dz_loc):
     dm2, dbias = B.attention_bwd(bp, sv["msa_row"], dm_s.reshape(Sl * R, Hm).contiguous())
     if N > 1:
         dbias = comm.reduce_scatter(dbias.view(nh, N, Rl, R).permute(1, 0, 2, 3))
-    B.msa_row_bias_bwd(bp, sv["bias"], dbias, dz2)
+    dz2 = B.msa_row_bias_bwd(bp, sv["bias"], dbias, dz2)
     B.SideStream.join()
     return dm2.view(Sl, R, Hm), dz2.view(Rl, R, Hz)
 

@@ -403,8 +403,12 @@ class EvoformerStack:
         return m, z, saved
 
     def backward(self, saved, dm, dz):
+        # parameter-gradient work of block i stays on the side stream while block i-1's
+        # backward runs (block_bwd never writes a tensor in place that side work may still
+        # read); one join at the end
         for b, s in zip(reversed(self.blocks), reversed(saved)):
-            dm, dz = _blk.block_bwd(b, s, dm, dz)
+            dm, dz = _blk.block_bwd(b, s, dm, dz, join=False)
+        _blk.SideStream.join()
         return dm, dz
 
     def forward_backward(self, m, z, gm, gz):

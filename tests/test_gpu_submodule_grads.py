@@ -62,7 +62,7 @@ def test_submodule_backward(mod):
         out, sv = B.attention_fwd(bp, "msa_row", dev(m).view(S * R, -1), S, R, "row", bias=bias)
         dx, dbias = B.attention_bwd(bp, sv, dev(g).view(S * R, -1))
         dz = torch.zeros(R * R, cfg.h_pair, device="cuda", dtype=torch.bfloat16)
-        B.msa_row_bias_bwd(bp, svb, dbias, dz)
+        dz = B.msa_row_bias_bwd(bp, svb, dbias, dz)
         # reference: d/dm and d/dz of <msa_row_attention(m, z), g>
         mt = torch.tensor(m, requires_grad=True)
         ztt = torch.tensor(z, requires_grad=True)
