@@ -235,13 +235,16 @@ __global__ void __launch_bounds__(256) attn_bwd_prep(AttnBwdParams P, int64_t B)
 constexpr int BW_BK = 128;  // keys per CTA
 constexpr int BW_BQ = 128;  // queries per iteration
 
-template <int CP>
+template <int CP, bool BIASS = false>
 struct BwdSmem {
   // PTM (head dim <= 32): P^T lives in TMEM (the dV MMA reads its A operand from there), and
   // the freed 32 KB double-buffer the per-query-tile operands (Q, dO, lse, D), so the next
   // query tile is loaded while this one computes.  Head dim 64 keeps P^T in smem.
+  // BIASS (msa_row's batch-shared full bias): the freed 32 KB hold the (key x query) bias tile
+  // instead, prefetched with the Q/dO tile (single-buffered) rather than loaded from global
+  // memory inside the softmax-backward loop.
   static constexpr bool PTM = CP <= 32;
-  static constexpr int NB = PTM ? 2 : 1;                    // query-tile operand buffers
+  static constexpr int NB = (PTM && !BIASS) ? 2 : 1;        // query-tile operand buffers
   static constexpr uint32_t K = 0;                          // [key][d] K-major
   static constexpr uint32_t V = K + BW_BK * CP * 2;         // [key][d] K-major
   static constexpr uint32_t Q = V + BW_BK * CP * 2;         // NB x [query][d] K-major
@@ -252,7 +255,9 @@ struct BwdSmem {
   static constexpr uint32_t LSE = DST + BW_BK * BW_BQ * 2;  // NB x fp32 [128]
   static constexpr uint32_t DD = LSE + NB * BW_BQ * 4;      // NB x fp32 [128]
   static constexpr uint32_t KB = DD + NB * BW_BQ * 4;       // fp32 [2][128] per-key dbias partials
-  static constexpr uint32_t TOTAL = KB + 2 * BW_BK * 4;
+  static constexpr int BROW = BW_BQ + 8;                    // bias tile row (key): 136 bf16, conflict-free
+  static constexpr uint32_t BT = KB + 2 * BW_BK * 4;        // [key][query] bias tile (BIASS)
+  static constexpr uint32_t TOTAL = BT + (BIASS ? BW_BK * BROW * 2 : 0);
 };
 
 __device__ __forceinline__ void bw_tmem_st8(uint32_t taddr, const uint32_t* r) {
@@ -294,12 +299,14 @@ __device__ __forceinline__ void bw_load(uint32_t sdst, const bf16* base, int64_t
 // (fp32 atomics).  Specialised so the per-element loop carries no dead predicated paths.
 template <int CP, int MODE>
 __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int nkt, int dq_partial) {
-  using SM = BwdSmem<CP>;
+  constexpr bool BIASS = MODE == 2 && CP <= 32;
+  using SM = BwdSmem<CP, BIASS>;
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar1, bar2;
   __shared__ uint32_t tmem_sh;
   const uint32_t sb = smem_u32(smem);
   constexpr bool PTM = SM::PTM;
+  constexpr bool DB = SM::NB == 2;  // double-buffered query-tile operands
   float* s_kb = reinterpret_cast<float*>(smem + SM::KB);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -335,6 +342,16 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
     bw_load<CP>(sb + SM::DO + buf * SM::QD_BYTES, P.dO + b * L * HC + (int64_t)h * c, HC, q0, L - q0, c);
     const int64_t st0 = (b * H + h) * (int64_t)L + q0;
     const uint32_t lse_b = SM::LSE + buf * BW_BQ * 4, dd_b = SM::DD + buf * BW_BQ * 4;
+    if constexpr (BIASS) {  // transposed bias [h][key][query] (query-contiguous, L % 8 == 0)
+      const bf16* bt = F.bias + (int64_t)h * F.bs1;
+#pragma unroll
+      for (int i = 0; i < BW_BK * (BW_BQ / 8) / 256; ++i) {
+        const int ch = threadIdx.x + i * 256;
+        const int r = ch >> 4, cq = (ch & 15) * 8;
+        const bool ok = (k0 + r < L) && (q0 + cq < L);
+        cp_async16(sb + SM::BT + r * (SM::BROW * 2) + cq * 2, ok ? bt + (int64_t)(k0 + r) * F.bs3 + q0 + cq : bt, ok);
+      }
+    }
     if (vec_stats) {
       if (threadIdx.x < 2 * BW_BQ / 4) {
         const int t = threadIdx.x & (BW_BQ / 4 - 1);
@@ -396,7 +413,7 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
     const int bs2 = (int)F.bs2;  // full-bias query stride (< 2^31)
     for (int qt = 0; qt < nqt; ++qt, ++it) {
       const int q0 = qt * BW_BQ;
-      const int buf = PTM ? (it & 1) : 0;
+      const int buf = DB ? (it & 1) : 0;
       const uint32_t sQ = sb + SM::Q + buf * SM::QD_BYTES, sDO = sb + SM::DO + buf * SM::QD_BYTES;
       const float* s_lse = reinterpret_cast<const float*>(smem + SM::LSE + buf * BW_BQ * 4);
       const float* s_D = reinterpret_cast<const float*>(smem + SM::DD + buf * BW_BQ * 4);
@@ -405,7 +422,7 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
       __syncthreads();
       // double-buffered: the next query tile of this unit loads while this one computes (the
       // other buffer's last reader, the previous tile's MMAs, completed before this barrier)
-      if (PTM && qt + 1 < nqt) issue_loads(b, h, k0, qt + 1, false, buf ^ 1);
+      if (DB && qt + 1 < nqt) issue_loads(b, h, k0, qt + 1, false, buf ^ 1);
       if (threadIdx.x == 0) {
         tc_fence_after();
 #pragma unroll
@@ -432,7 +449,16 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
         float pv[16], dsv[16];
         const bool all_valid = kvalid && q0 + qc + 16 <= L;
         float bv[16];
-        if constexpr (MODE == 2) {  // transposed batch-shared bias: 16 consecutive queries per key
+        if constexpr (BIASS) {  // this key row's 16 queries from the prefetched smem tile
+#pragma unroll
+          for (int e = 0; e < 16; e += 8) {
+            uint32_t u0, u1, u2, u3;
+            asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];\n" : "=r"(u0), "=r"(u1), "=r"(u2), "=r"(u3)
+                         : "r"(sb + SM::BT + kr * (SM::BROW * 2) + (qc + e) * 2));
+            unpack_bf16x2(u0, bv[e], bv[e + 1]); unpack_bf16x2(u1, bv[e + 2], bv[e + 3]);
+            unpack_bf16x2(u2, bv[e + 4], bv[e + 5]); unpack_bf16x2(u3, bv[e + 6], bv[e + 7]);
+          }
+        } else if constexpr (MODE == 2) {  // transposed batch-shared bias: 16 consecutive queries per key
           if (bias_col) {
             const bf16* bp = bias_col + (q0 + qc);
 #pragma unroll
@@ -548,12 +574,12 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
       // the tiles are free: prefetch the next (batch, query tile) while draining TMEM
       const bool last_q = qt + 1 == nqt;
       if (!last_q) {
-        if (!PTM) issue_loads(b, h, k0, qt + 1, false, 0);
+        if (!DB) issue_loads(b, h, k0, qt + 1, false, 0);
       } else if (u + gridDim.x < units) {
         int64_t nb;
         int nh, nkt_;
         decode(u + gridDim.x, nb, nh, nkt_);
-        issue_loads(nb, nh, nkt_ * BW_BK, 0, true, PTM ? (buf ^ 1) : 0);
+        issue_loads(nb, nh, nkt_ * BW_BK, 0, true, DB ? (buf ^ 1) : 0);
       }
       if constexpr (db_store) {
         // dS^T tile (unscaled bf16, canonical K-major [key][query]) -> workspace [b][h][key][query]:
@@ -720,7 +746,7 @@ int sm_count();
 
 template <int CP, int MODE>
 static int launch_bwd_m(AttnBwdParams& p, int64_t B, int dq_partial, cudaStream_t st) {
-  using SM = BwdSmem<CP>;
+  using SM = BwdSmem<CP, MODE == 2 && CP <= 32>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel<CP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
