@@ -137,8 +137,8 @@ int sm_count();
 // unit already prefetches the next unit's first K/V tile, and the next unit's Q follows as
 // soon as this unit's last S MMA has read Q: the next unit's load latency hides under this
 // unit's last softmax and epilogue.
-// VAR: 0 = no bias (gate rows prefetched into smem for the epilogue), 1 = per-key bias or a
-// generic full bias (global loads), 2 = full bias staged through smem (FB)
+// VAR: 0 = no bias (gate rows prefetched into smem for the epilogue), 1 = per-key bias,
+// 2 = full bias staged through smem (FB), 3 = generic full bias (strided global loads)
 template <int CP, int VAR>
 __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1) ? 3 : 4)) attn_fwd_kernel(AttnParams P,
                                                                                                           int nunits) {
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1
   const int L = P.L, c = P.c, H = P.H;
   const int nqt = (L + ATT_BQ - 1) / ATT_BQ;
   const int r = warp * 32 + lane;  // query row inside the tile
-  const bool per_key_bias = VAR == 1 && P.bias && P.bs2 == 0;
+  const bool per_key_bias = VAR == 1;
   constexpr uint32_t ONE_BF16 = 0x3F80u;
   const int nkt = (L + ATT_BK - 1) / ATT_BK;
 
@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1
     const bf16* bfull = bfull_of(cur);
     float m_run = -INFINITY;  // running max, scaled log2 units
     const bf16* brow = nullptr;
-    if (VAR == 1 && P.bias && !per_key_bias && qi < L) brow = P.bias + b * P.bs0 + (int64_t)h * P.bs1 + (int64_t)qi * P.bs2;
+    if (VAR == 3 && qi < L) brow = P.bias + b * P.bs0 + (int64_t)h * P.bs1 + (int64_t)qi * P.bs2;
     uint32_t nb = 0;  // next tile's per-key bias (threads 0..63), stored with its K tile
 
     for (int j = 0; j < nkt; ++j, ++gt) {
@@ -489,8 +489,9 @@ static int g_fwd_fb = 1;  // stage a full bias through smem (evo_attention_fwd_f
 template <int CP>
 static int launch_attn_fwd(const AttnParams& p, int64_t B, cudaStream_t st) {
   if (!p.bias) return launch_attn_fwd_v<CP, 0>(p, B, st);
-  if (g_fwd_fb && p.bs2 != 0 && p.bias_vec) return launch_attn_fwd_v<CP, 2>(p, B, st);
-  return launch_attn_fwd_v<CP, 1>(p, B, st);
+  if (p.bs2 == 0) return launch_attn_fwd_v<CP, 1>(p, B, st);
+  if (g_fwd_fb && p.bias_vec) return launch_attn_fwd_v<CP, 2>(p, B, st);
+  return launch_attn_fwd_v<CP, 3>(p, B, st);
 }
 
 int attn_params_from_desc(const EvoAttnDesc* d, AttnParams& p) {
