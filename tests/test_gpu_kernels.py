@@ -215,9 +215,8 @@ def test_attention_fwd_bwd_ws(L, c, H, mode, ws_forward):
 
 @pytest.mark.parametrize("L,c,H,mode", [(256, 32, 8, "full"), (128, 32, 8, "none"), (256, 32, 4, "key"),
                                         (100, 16, 2, "full"), (300, 64, 2, "key"), (40, 8, 4, "none")])
-def test_attention_fwd_bwd(L, c, H, mode):
+def test_attention_fwd_bwd(L, c, H, mode, B=3):
     gen = torch.Generator(device=DEV).manual_seed(L * c + H)
-    B = 3
     ld = 3 * H * c + (8 if mode == "key" else 0)
     qkv = _mk((B, L, ld), gen)
     gp = _mk((B, L, H * c), gen)
@@ -282,6 +281,44 @@ def test_attention_fwd_bwd(L, c, H, mode):
         assert rel(dbias, br.grad.sum(0)) < 2e-2
     elif mode == "key":
         assert rel(dbias, br.grad[:, :, 0, :]) < 2e-2
+
+
+@pytest.mark.parametrize("mode,H", [("none", 8), ("key", 4), ("full", 8)])
+def test_attention_persistent_units(mode, H):
+    """B*H*L/128 units well above the persistent forward grid (4 CTAs/SM) and the backward's
+    (2 CTAs/SM): the cross-unit prefetch paths (next unit's Q/K/V under the last tile, the
+    double-buffered query tiles) run many times per CTA"""
+    test_attention_fwd_bwd(256, 32, H, mode, B=160)
+
+
+def test_attention_fwd_full_bias_smem_switch():
+    """the smem-staged full-bias forward (msa_row) equals the global-load variant bitwise"""
+    lib = _lib.load()
+    gen = torch.Generator(device=DEV).manual_seed(5)
+    B, L, H, c = 40, 256, 8, 32
+    qkv = _mk((B, L, 3 * H * c), gen)
+    gp = _mk((B, L, H * c), gen)
+    bias = _mk((H, L, L), gen)
+    outs = []
+    old = lib.evo_attention_fwd_full_bias_smem(-1)
+    try:
+        for fb in (1, 0):
+            lib.evo_attention_fwd_full_bias_smem(fb)
+            og = torch.empty(B, L, H * c, device=DEV, dtype=torch.bfloat16)
+            orw = torch.empty_like(og)
+            lse = torch.empty(B, H, L, device=DEV)
+            ld = 3 * H * c
+            d = ops.attention_desc(Strided(qkv, L * ld, ld, 0), Strided(qkv, L * ld, ld, H * c),
+                                   Strided(qkv, L * ld, ld, 2 * H * c), Strided(gp, L * H * c, H * c),
+                                   Strided(og, L * H * c, H * c), Strided(orw, L * H * c, H * c), lse,
+                                   B, L, H, c, 1 / math.sqrt(c), bias=bias, bias_s=(0, L * L, L, 1))
+            ops.attention_fwd(d)
+            torch.cuda.synchronize()
+            outs.append((og, orw, lse))
+    finally:
+        lib.evo_attention_fwd_full_bias_smem(old)
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
 
 
 def test_tri_gate_and_residuals():
