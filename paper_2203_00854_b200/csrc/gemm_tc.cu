@@ -976,12 +976,26 @@ static int dispatch_major(bool am, bool bm, MatArg A, MatArg B, MatArg C, int64_
 }
 
 // split-K factor: only when the output tiles cannot fill the machine and K is long
+// N tile width.  A long-K product with 64 < N <= 128 (OPM backward: M = 8192, N = 128,
+// K = 8192) takes one 128-wide N tile so the (HBM-sized) A operand is streamed once rather
+// than once per 64-wide N tile; split-K restores the parallelism.
+static int pick_bn(int64_t batch, int64_t M, int64_t N, int64_t K, bool small, bool wide) {
+  if (N > 64 && N <= 128 && K >= 2048) return 128;
+  return (small || N <= 64) ? 64 : (wide ? 256 : 128);
+}
+
+// split-K for long-K products with fewer output tiles than SMs: the persistent grid is one
+// CTA per SM, so the split count keeps every (tile, split) unit in ONE wave (tiles * splits <=
+// SMs).  Measured on the OPM backward (64 tiles, K = 8192): 2 splits 56 us, 3 -> 71, 5 -> 77,
+// 9 -> 85, 16 -> 115 (more waves and more fp32 partial traffic).
 static int pick_splits(int64_t batch, int64_t M, int64_t N, int64_t K, int bn) {
+  static const int forced = [] { const char* e = getenv("EVO_BGEMM_SPLITS"); return e ? atoi(e) : 0; }();
+  if (forced > 0 && K >= 2048) return forced;
   const int64_t tiles = ((M + 127) / 128) * ((N + bn - 1) / bn) * batch;
   const int64_t kt = (K + GEMM_BK - 1) / GEMM_BK;
-  const int64_t target = 2 * (int64_t)sm_count();
-  if (tiles >= target || kt < 16) return 1;
-  int64_t s = (target + tiles - 1) / tiles;
+  const int64_t slots = (int64_t)sm_count();
+  if (tiles * 2 > slots || kt < 16) return 1;
+  int64_t s = slots / tiles;
   if (s > kt / 8) s = kt / 8;  // >= 8 k-tiles per split
   if (s > 16) s = 16;
   if (s < 1) s = 1;
@@ -1017,7 +1031,7 @@ static int bgemm_entry(const EvoMat* A, const EvoMat* B, const EvoMat* C, int64_
   bool small = ((M + 127) / 128) * ((N + 127) / 128) * batch < 148;
   const bool wide = !small && C->dtype == EVO_BF16 && N >= 256 && K >= 512 && !use_v1() &&
                     ((M + 127) / 128) * ((N + 255) / 256) * batch >= 2 * 148;
-  const int bn = (small || N <= 64) ? 64 : (wide ? 256 : 128);
+  const int bn = pick_bn(batch, M, N, K, small, wide);
   int splits = pick_splits(batch, M, N, K, bn);
   if (splits > 1 && (!workspace || ws_bytes < splits * batch * M * N * 4)) splits = 1;
   float* ws = (float*)workspace;
@@ -1039,7 +1053,7 @@ extern "C" int evo_bgemm(const EvoMat* A, const EvoMat* B, const EvoMat* C, int6
 
 extern "C" int64_t evo_bgemm_workspace(int64_t batch, int64_t M, int64_t N, int64_t K) {
   bool small = ((M + 127) / 128) * ((N + 127) / 128) * batch < 148;
-  const int bn = (small || N <= 64) ? 64 : 128;
+  const int bn = evo::pick_bn(batch, M, N, K, small, false);
   const int splits = evo::pick_splits(batch, M, N, K, bn);
   return splits > 1 ? (int64_t)splits * batch * M * N * 4 : 0;
 }
