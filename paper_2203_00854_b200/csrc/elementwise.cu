@@ -268,15 +268,23 @@ __global__ void __launch_bounds__(256) tri_gate_fwd_k(const bf16* __restrict__ y
     for (int e = 0; e < 8; ++e) ys[r][c + e] = v[e];
   }
   __syncthreads();
-  // write a[h][r], b[h][r]: consecutive threads -> consecutive rows (coalesced)
-  for (int i = threadIdx.x; i < 2 * P * RB; i += blockDim.x) {
-    const int r = i % RB, ch = i / RB;  // ch < 2P
+  // write a[h][r], b[h][r]: consecutive threads -> consecutive row pairs (coalesced 4-byte
+  // stores of two rows; scalar when rows is odd or at the ragged end)
+  const bool pairs = (rows & 1) == 0;
+  for (int i = threadIdx.x; i < P * RB; i += blockDim.x) {
+    const int r = (i % (RB / 2)) * 2, ch = i / (RB / 2);  // ch < 2P
     if (r0 + r >= rows) continue;
     const int h = ch % P, which = ch / P;  // 0 = a, 1 = b
-    const float s = ys[r][which * 2 * P + h], l = ys[r][which * 2 * P + P + h];
-    const float v = sigmoidf_(s) * l;
-    bf16* dst = which ? b_cm : a_cm;
-    dst[(int64_t)h * rows + r0 + r] = f2bf(v);
+    const int cs = which * 2 * P + h, cl = cs + P;
+    const float v0 = sigmoidf_(ys[r][cs]) * ys[r][cl];
+    const float v1 = sigmoidf_(ys[r + 1][cs]) * ys[r + 1][cl];
+    bf16* dst = (which ? b_cm : a_cm) + (int64_t)h * rows + r0 + r;
+    if (pairs && r0 + r + 1 < rows) {
+      *reinterpret_cast<uint32_t*>(dst) = pack_bf16x2(v0, v1);
+    } else {
+      dst[0] = f2bf(v0);
+      if (r0 + r + 1 < rows) dst[1] = f2bf(v1);
+    }
   }
 }
 
