@@ -133,16 +133,19 @@ typedef struct EvoAttnDesc {
   int64_t B, L;
   int H, c;
   float scale;
+  int flags;   /* EVO_ATTN_* kernel-selection hints (0 = automatic); per call, no global state */
 } EvoAttnDesc;
+/* Kernel selection is automatic: sequences with L >= 4096 and a per-key (or no) bias take
+ * the warp-specialised forward (attention_ws.cu: 1 CTA/SM, loader warp, per-warpgroup MMA
+ * warps, two softmax warpgroups), everything else the persistent flash kernel; a full
+ * bias is staged through shared memory when its rows are 16-byte aligned.  Every
+ * variant computes the same function; the flags force one for tests and A/B timing. */
+enum {
+  EVO_ATTN_FORCE_WS = 1,        /* warp-specialised forward at any L (any bias) */
+  EVO_ATTN_FORCE_FLASH = 2,     /* persistent flash forward at any L */
+  EVO_ATTN_NO_BIAS_SMEM = 4     /* full bias read from global memory, not staged in smem */
+};
 int evo_gated_attention_fwd(const EvoAttnDesc* d, void* stream);
-/* Sequences with L >= len and a per-key (or no) bias use the warp-specialised forward
- * (attention_ws.cu: 1 CTA/SM, loader warp, per-warpgroup MMA warps, two softmax
- * warpgroups); default len 4096.  Returns the previous threshold; len <= 0 only queries
- * it; len == 1 forces it for every input (tests).  Both kernels compute the same function. */
-int evo_attention_fwd_ws_min_len(int len);
-/* A/B switch: stage a full (per query and key) bias through shared memory in the forward
-   (default 1); on < 0 only queries.  Returns the previous setting. */
-int evo_attention_fwd_full_bias_smem(int on);
 
 /* Backward of the same op (flash-style: P is recomputed from q, k, bias and lse).
  * Inputs: the forward descriptor (q,k,v,g,bias,o_raw,lse) plus dout (gradient of
@@ -216,6 +219,14 @@ int evo_gated_residual_fwd(const void* res, const void* y, int64_t y_rs, const f
 int evo_gated_residual_bwd(const void* dout, const void* y, int64_t y_rs, const float* bias,
                            const void* gp, int64_t gp_rs, void* dy, void* dgp, int64_t dgp_rs,
                            float* dbias, int dtype, int64_t rows, int64_t cols, void* stream);
+
+/* out[r*out_rs + c] = act(gate[r*gate_rs + c]) * (y[r*y_rs + c] + bias[c]); act 0 = identity,
+ * 1 = sigmoid, 2 = ReLU; gate NULL -> 1, y NULL -> (y + bias) = 1, bias may be NULL.
+ * The reference-API helpers _triangle_projections / _triangle_finish (evoformer.py:258-270)
+ * and engine.sigmoid_raw / relu_raw (engine.py:220-225); any cols, any row strides.   */
+int evo_gate_mul_fwd(const void* gate, int64_t gate_rs, int gate_act, const void* y, int64_t y_rs,
+                     const float* bias, void* out, int64_t out_rs, int dtype, int64_t rows, int64_t cols,
+                     void* stream);
 
 /* out[c] += sum_r x[r*ld + c]  (fp32 out; bias gradients of the projection GEMMs) */
 int evo_colsum(const void* x, int dtype, int64_t ld, int64_t rows, int64_t cols, float* out, void* stream);

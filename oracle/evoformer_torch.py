@@ -73,9 +73,13 @@ def msa_col_attention(m, p, cfg):
     return gated_attention(m.transpose(0, 1), p, "msa_col", cfg.n_head_msa).transpose(0, 1)
 
 
-def transition(x, p, mod):
+def transition(x, p, mod, mask=None):
+    """evoformer.py:237-240.  mask (bool, the hidden layer's shape): use this ReLU pattern
+    instead of (pre > 0) - the mask-matched gradient oracle (see block_grads)."""
     ln = layernorm(x, p[f"{mod}/ln/g"], p[f"{mod}/ln/b"])
-    return torch.relu(ln @ p[f"{mod}/w1"] + p[f"{mod}/b1"]) @ p[f"{mod}/w2"] + p[f"{mod}/b2"]
+    pre = ln @ p[f"{mod}/w1"] + p[f"{mod}/b1"]
+    hid = torch.relu(pre) if mask is None else pre * mask.to(pre.dtype)
+    return hid @ p[f"{mod}/w2"] + p[f"{mod}/b2"]
 
 
 def opm_projections(m, p):
@@ -143,29 +147,39 @@ def pair_attention_col(z, p, cfg):
                            pair_key_bias(zt, p, "pair_col", cfg.n_head_pair)).transpose(0, 1)
 
 
-def evoformer_block(m, z, p, cfg):
-    """evoformer.py:314-325."""
+def evoformer_block(m, z, p, cfg, masks=None):
+    """evoformer.py:314-325.  masks: optional {"msa_trans": bool, "pair_trans": bool} ReLU
+    patterns for the two transitions (mask-matched oracle)."""
+    masks = masks or {}
     m = m + msa_row_attention(m, z, p, cfg)
     m = m + msa_col_attention(m, p, cfg)
-    m = m + transition(m, p, "msa_trans")
+    m = m + transition(m, p, "msa_trans", masks.get("msa_trans"))
     z = z + outer_product_mean(m, p, cfg)
     z = z + tri_update_outgoing(z, p, cfg)
     z = z + tri_update_incoming(z, p, cfg)
     z = z + pair_attention_row(z, p, cfg)
     z = z + pair_attention_col(z, p, cfg)
-    z = z + transition(z, p, "pair_trans")
+    z = z + transition(z, p, "pair_trans", masks.get("pair_trans"))
     return m, z
 
 
-def block_grads(m, z, params, cfg, gm, gz, dtype=torch.float64):
+def block_grads(m, z, params, cfg, gm, gz, dtype=torch.float64, masks=None):
     """Gradient oracle: d/d(m, z, params) of <m', gm> + <z', gz>.
 
     Inputs are numpy or torch; returns (m', z', dm, dz, dparams) as float64 numpy.
+    masks: the ReLU patterns the GPU run took in its two transitions.  A bf16 run flips the
+    pattern of units whose pre-activation lies within rounding distance of 0; each flip is an
+    O(1) change of that unit's gradient (~sqrt(fraction) relative error in dm/dz).  With the
+    GPU's own pattern the oracle differentiates the same piecewise-linear branch, so the
+    comparison measures the kernels' error, not the branch choice.  The forward is unchanged
+    up to the flipped units' |pre| ~ bf16 rounding.
     """
     t = lambda a: torch.as_tensor(a, dtype=dtype).clone().requires_grad_(True)
     mt, zt = t(m), t(z)
     pt = {k: t(v) for k, v in params.items()}
-    mo, zo = evoformer_block(mt, zt, pt, cfg)
+    if masks is not None:
+        masks = {k: torch.as_tensor(v).bool() for k, v in masks.items()}
+    mo, zo = evoformer_block(mt, zt, pt, cfg, masks)
     loss = (mo * torch.as_tensor(gm, dtype=dtype)).sum() + (zo * torch.as_tensor(gz, dtype=dtype)).sum()
     keys = list(pt)
     grads = torch.autograd.grad(loss, [mt, zt] + [pt[k] for k in keys], allow_unused=True)

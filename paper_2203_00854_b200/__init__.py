@@ -32,9 +32,12 @@ __version__ = "0.1.0"
 def __getattr__(name):
     # heavy (torch / CUDA) modules load lazily so that `import` works on CPU-only hosts
     if name in ("evoformer_block", "msa_row_attention", "msa_row_bias", "msa_row_attention_with_bias",
-                "msa_col_attention", "transition", "outer_product_mean", "tri_update_outgoing",
-                "tri_update_incoming", "pair_attention_row", "pair_attention_col",
-                "fused_softmax_mask_bias", "layernorm", "EvoformerStack", "BlockParams"):
+                "msa_col_attention", "transition", "outer_product_mean", "outer_product_mean_from_projections",
+                "tri_update_outgoing", "tri_update_incoming", "pair_attention_row", "pair_attention_col",
+                "fused_softmax_mask_bias", "fused_softmax_mask_bias_raw", "layernorm", "layernorm_raw",
+                "softmax_raw", "sigmoid_raw", "relu_raw", "EvoformerStack", "BlockParams", "GraphedStep",
+                "EvoformerBlockFunction", "_attention_core", "_triangle_projections", "_triangle_finish",
+                "_pair_bias_fn", "_check_msa", "_check_pair", "check_supported"):
         from . import evoformer
         return getattr(evoformer, name)
     if name in ("dap_evoformer_block", "DeviceMesh", "CommLedger", "predict_block_ledger", "dap_block"):

@@ -33,7 +33,11 @@ class EvoAttnDesc(C.Structure):
                 ("lse", vp),
                 ("B", i64), ("L", i64),
                 ("H", C.c_int), ("c", C.c_int),
-                ("scale", C.c_float)]
+                ("scale", C.c_float), ("flags", C.c_int)]
+
+
+# EvoAttnDesc.flags (include/evo.h): per-call kernel-selection hints, 0 = automatic
+EVO_ATTN_FORCE_WS, EVO_ATTN_FORCE_FLASH, EVO_ATTN_NO_BIAS_SMEM = 1, 2, 4
 
 
 class EvoAttnBwdDesc(C.Structure):
@@ -67,8 +71,6 @@ _SIGS = {
     "evo_softmax_bwd": [vp, C.c_int, vp, C.c_int, vp, C.c_int, i64, i64, C.c_float, vp],
     "evo_gated_attention_fwd": [C.POINTER(EvoAttnDesc), vp],
     "evo_gated_attention_bwd": [C.POINTER(EvoAttnBwdDesc), vp],
-    "evo_attention_fwd_ws_min_len": [C.c_int],
-    "evo_attention_fwd_full_bias_smem": [C.c_int],
     "evo_residual_layernorm_fwd": [vp, vp, i64, vp, vp, i64, vp, vp, vp, vp, vp, vp, i64, i64, C.c_float, vp],
     "evo_gated_attention_bwd_workspace": [i64, i64, C.c_int, C.c_int, C.c_int],
     "evo_bgemm": [C.POINTER(EvoMat), C.POINTER(EvoMat), C.POINTER(EvoMat), i64, i64, i64, i64,
@@ -84,6 +86,7 @@ _SIGS = {
     "evo_bias_act_bwd": [vp, vp, vp, vp, i64, i64, C.c_int, C.c_int, vp],
     "evo_count_nonfinite": [vp, C.c_int, i64, vp, vp],
     "evo_colsum": [vp, C.c_int, i64, i64, i64, vp, vp],
+    "evo_gate_mul_fwd": [vp, i64, C.c_int, vp, i64, vp, vp, i64, C.c_int, i64, i64, vp],
 }
 
 _lib = None

@@ -63,11 +63,12 @@ class SideStream:
 
 
 def _wgrad(x, dy, out):
-    """out (fp32) = x^T @ dy with fp32 accumulation and output (side stream)."""
-    if x.is_cuda:  # cuBLAS writes the fp32 result straight into the grad buffer view
-        SideStream.run(lambda: torch.mm(x.t(), dy, out_dtype=F32, out=out), x, dy)
+    """out (fp32) += x^T @ dy with fp32 accumulation (side stream).  Every parameter gradient
+    ACCUMULATES into bp.grad (micro-batch accumulation works; zero_grad() between steps)."""
+    if x.is_cuda:  # cuBLAS, beta = 1: the fp32 result is added straight into the grad buffer view
+        SideStream.run(lambda: torch.addmm(out, x.t(), dy, out_dtype=F32, out=out), x, dy)
     else:  # CPU only in the host-logic tests (fake kernel backend)
-        out.copy_(x.t().float() @ dy.float())
+        out += x.t().float() @ dy.float()
 
 
 def _bgrad(dy, out):
@@ -124,8 +125,9 @@ def _attn_geometry(kind: str, B: int, L: int):
 
 
 def attention_fwd(bp: BlockParams, mod: str, x2d, B: int, L: int, kind: str, bias=None, save=True, pre_ln=None,
-                  next_ln=None):
+                  next_ln=None, flags=0):
     """_attention_core (evoformer.py:173-198) + residual: returns x + attn(x).
+    flags: EVO_ATTN_* kernel-selection hints (0 = automatic; tests force each variant).
 
     kind "row": attention along the second axis of [B, L, C]; "col": x2d is
     [L, B, C] and attention runs along the first axis (msa_col / pair_col).
@@ -154,7 +156,7 @@ def attention_fwd(bp: BlockParams, mod: str, x2d, B: int, L: int, kind: str, bia
         bt, bs, boff = bias, (0, L * L, L, 1), 0
     desc = ops.attention_desc(S(qkv, ldq, 0), S(qkv, ldq, nh * c), S(qkv, ldq, 2 * nh * c), S(gpre, nh * c),
                               S(og, nh * c), S(orw, nh * c), lse, B, L, nh, c, 1.0 / math.sqrt(c),
-                              bias=bt, bias_s=bs, bias_off=boff)
+                              bias=bt, bias_s=bs, bias_off=boff, flags=flags)
     ops.attention_fwd(desc)
     y = _mm(og, h[f"{mod}.w_o"])
     out = _residual_out(x2d, y, f[f"{mod}.b_o"], rows, H, next_ln)
@@ -326,6 +328,18 @@ def opm_fwd(bp: BlockParams, m2d, z2d, S: int, R: int, save=True, b_full=None, R
     return out, sv
 
 
+def opm_contract(a2d, b2d, S: int, I: int, J: int, P: int):
+    """o[i][j][p][q] = sum_s a[s, i, p] b[s, j, q] / S (evoformer.py:253) for separate projections
+    a [S, I*P], b [S, J*P] (outer_product_mean_from_projections): one tcgen05 GEMM with M = (i,p),
+    N = (j,q), K = s, both operands MN-major, written straight into the [i][j][p][q] layout."""
+    o = torch.empty(I, J, P, P, device=a2d.device, dtype=BF16)
+    A = Mat(a2d, lo=(1, a2d.stride(0)))
+    B = Mat(b2d, lo=(1, b2d.stride(0)))
+    Cm = Mat(o, lo=(P, 1), split=(P, P), hi=(J * P * P, P * P))
+    ops.bgemm(A, B, Cm, 1, I * P, J * P, S, alpha=1.0 / S)
+    return o
+
+
 def opm_bwd(bp: BlockParams, sv: Saved, dz_new, dm, reduce_scatter=None, next_db=None, db_done=False):
     """accumulates the OPM contribution into dm (bf16 [S*R, Hm]); dz passes through.
     next_db: bias gradient of the module consuming dm (fused column sums of the final dm)."""
@@ -490,8 +504,9 @@ def triangle_bwd(bp: BlockParams, sv: Saved, dz_new, reduce_scatter=None, next_d
 
 
 # ----------------------------------------------------------------------------- block
-def block_fwd(bp: BlockParams, m, z, save=True):
-    """evoformer_block (evoformer.py:314-325) on bf16 device tensors m [S,R,Hm], z [R,R,Hz]."""
+def block_fwd(bp: BlockParams, m, z, save=True, attn_flags=0):
+    """evoformer_block (evoformer.py:314-325) on bf16 device tensors m [S,R,Hm], z [R,R,Hz].
+    attn_flags: EVO_ATTN_* hints for the four attention forwards (0 = automatic)."""
     cfg: EvoConfig = bp.cfg
     S, R = cfg.n_seq, cfg.n_res
     m2 = m.reshape(S * R, cfg.h_msa)
@@ -502,16 +517,18 @@ def block_fwd(bp: BlockParams, m, z, save=True):
     c = {k: LnChain(f[f"{k}.ln_g"], f[f"{k}.ln_b"]) for k in
          ("msa_col", "msa_trans", "opm", "tri_out", "tri_in", "pair_row", "pair_col", "pair_trans")}
     bias, sv_b = msa_row_bias_fwd(bp, z2, R, R, save)
-    m2, s1 = attention_fwd(bp, "msa_row", m2, S, R, "row", bias=bias, save=save, next_ln=c["msa_col"])
-    m2, s2 = attention_fwd(bp, "msa_col", m2, R, S, "col", save=save, pre_ln=c["msa_col"], next_ln=c["msa_trans"])
+    m2, s1 = attention_fwd(bp, "msa_row", m2, S, R, "row", bias=bias, save=save, next_ln=c["msa_col"],
+                           flags=attn_flags)
+    m2, s2 = attention_fwd(bp, "msa_col", m2, R, S, "col", save=save, pre_ln=c["msa_col"], next_ln=c["msa_trans"],
+                           flags=attn_flags)
     m2, s3 = transition_fwd(bp, "msa_trans", m2, S * R, save, pre_ln=c["msa_trans"], next_ln=c["opm"])
     z2, s4 = opm_fwd(bp, m2, z2, S, R, save, pre_ln=c["opm"], next_ln=c["tri_out"])
     z2, s5 = triangle_fwd(bp, "tri_out", z2, R, save, pre_ln=c["tri_out"], next_ln=c["tri_in"])
     z2, s6 = triangle_fwd(bp, "tri_in", z2, R, save, pre_ln=c["tri_in"], next_ln=c["pair_row"])
     z2, s7 = attention_fwd(bp, "pair_row", z2, R, R, "row", bias="pair", save=save, pre_ln=c["pair_row"],
-                           next_ln=c["pair_col"])
+                           next_ln=c["pair_col"], flags=attn_flags)
     z2, s8 = attention_fwd(bp, "pair_col", z2, R, R, "col", bias="pair", save=save, pre_ln=c["pair_col"],
-                           next_ln=c["pair_trans"])
+                           next_ln=c["pair_trans"], flags=attn_flags)
     z2, s9 = transition_fwd(bp, "pair_trans", z2, R * R, save, pre_ln=c["pair_trans"])
     if save:
         saved.extend([sv_b, s1, s2, s3, s4, s5, s6, s7, s8, s9])

@@ -484,13 +484,12 @@ static int launch_attn_fwd_v(const AttnParams& p, int64_t B, cudaStream_t st) {
   return EVO_OK;
 }
 
-static int g_fwd_fb = 1;  // stage a full bias through smem (evo_attention_fwd_full_bias_smem: A/B switch)
-
 template <int CP>
-static int launch_attn_fwd(const AttnParams& p, int64_t B, cudaStream_t st) {
+static int launch_attn_fwd(const AttnParams& p, int64_t B, int flags, cudaStream_t st) {
   if (!p.bias) return launch_attn_fwd_v<CP, 0>(p, B, st);
   if (p.bs2 == 0) return launch_attn_fwd_v<CP, 1>(p, B, st);
-  if (g_fwd_fb && p.bias_vec) return launch_attn_fwd_v<CP, 2>(p, B, st);
+  // a full bias is staged through smem with the K/V tiles unless EVO_ATTN_NO_BIAS_SMEM
+  if (!(flags & EVO_ATTN_NO_BIAS_SMEM) && p.bias_vec) return launch_attn_fwd_v<CP, 2>(p, B, st);
   return launch_attn_fwd_v<CP, 3>(p, B, st);
 }
 
@@ -527,34 +526,26 @@ namespace evo {
 template <int CP>
 int launch_attn_fwd_ws(const AttnParams& p, int64_t B, cudaStream_t st);
 // sequences at least this long take the warp-specialised kernel (attention_ws.cu)
-static int g_ws_min_len = 4096;  // measured: faster than attn_fwd_kernel from N_r = 4096 on (per-key/no bias)
+constexpr int kWsMinLen = 4096;  // measured: faster than attn_fwd_kernel from N_r = 4096 on (per-key/no bias)
 }  // namespace evo
-
-extern "C" int evo_attention_fwd_full_bias_smem(int on) {
-  const int old = g_fwd_fb;
-  if (on >= 0) g_fwd_fb = on;
-  return old;
-}
-
-extern "C" int evo_attention_fwd_ws_min_len(int len) {
-  const int old = g_ws_min_len;
-  if (len > 0) g_ws_min_len = len;
-  return old;
-}
 
 extern "C" int evo_gated_attention_fwd(const EvoAttnDesc* d, void* stream) {
   AttnParams p;
   int rc = attn_params_from_desc(d, p);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
+  const int flags = d->flags;
+  EVO_CHECK_ARG((flags & ~(EVO_ATTN_FORCE_WS | EVO_ATTN_FORCE_FLASH | EVO_ATTN_NO_BIAS_SMEM)) == 0 &&
+                    (flags & (EVO_ATTN_FORCE_WS | EVO_ATTN_FORCE_FLASH)) != (EVO_ATTN_FORCE_WS | EVO_ATTN_FORCE_FLASH),
+                EVO_ERR_ARG, "attention fwd: bad flags 0x%x", flags);
   // the full (per query and key) bias path of the warp-specialised kernel measured slower
-  const bool ws_bias_ok = !p.bias || p.bs2 == 0 || g_ws_min_len <= 1;
-  if (p.L >= g_ws_min_len && ws_bias_ok) {
+  const bool ws_auto = p.L >= kWsMinLen && (!p.bias || p.bs2 == 0);
+  if ((flags & EVO_ATTN_FORCE_WS) || (ws_auto && !(flags & EVO_ATTN_FORCE_FLASH))) {
     if (p.c <= 16) return launch_attn_fwd_ws<16>(p, d->B, st);
     if (p.c <= 32) return launch_attn_fwd_ws<32>(p, d->B, st);
     return launch_attn_fwd_ws<64>(p, d->B, st);
   }
-  if (p.c <= 16) return launch_attn_fwd<16>(p, d->B, st);
-  if (p.c <= 32) return launch_attn_fwd<32>(p, d->B, st);
-  return launch_attn_fwd<64>(p, d->B, st);
+  if (p.c <= 16) return launch_attn_fwd<16>(p, d->B, flags, st);
+  if (p.c <= 32) return launch_attn_fwd<32>(p, d->B, flags, st);
+  return launch_attn_fwd<64>(p, d->B, flags, st);
 }

@@ -254,7 +254,8 @@ __global__ void __launch_bounds__(256) bias_act_bwd_k(const T* __restrict__ dh, 
 // RB rows per CTA; Y row slice [hz, hz+4p) staged in shared memory as fp32
 template <int P>
 __global__ void __launch_bounds__(256) tri_gate_fwd_k(const bf16* __restrict__ y, int64_t rows, int hz,
-                                                      bf16* __restrict__ a_cm, bf16* __restrict__ b_cm) {
+                                                      bf16* __restrict__ a_cm, bf16* __restrict__ b_cm,
+                                                      bool pairs) {
   constexpr int W = 4 * P;
   constexpr int RB = P <= 32 ? 64 : 32;
   __shared__ float ys[RB][W + 1];
@@ -269,8 +270,8 @@ __global__ void __launch_bounds__(256) tri_gate_fwd_k(const bf16* __restrict__ y
   }
   __syncthreads();
   // write a[h][r], b[h][r]: consecutive threads -> consecutive row pairs (coalesced 4-byte
-  // stores of two rows; scalar when rows is odd or at the ragged end)
-  const bool pairs = (rows & 1) == 0;
+  // stores of two rows; scalar when the host found rows odd or a_cm / b_cm not 4-byte
+  // aligned, and at the ragged end)
   for (int i = threadIdx.x; i < P * RB; i += blockDim.x) {
     const int r = (i % (RB / 2)) * 2, ch = i / (RB / 2);  // ch < 2P
     if (r0 + r >= rows) continue;
@@ -569,7 +570,9 @@ extern "C" int evo_tri_gate_fwd(const void* y, int64_t rows, int hz, int p, void
   if (rows == 0) return EVO_OK;
   cudaStream_t st = (cudaStream_t)stream;
   unsigned g = (unsigned)((rows + (p <= 32 ? 63 : 31)) / (p <= 32 ? 64 : 32));
-#define TG(PP) tri_gate_fwd_k<PP><<<g, 256, 0, st>>>((const bf16*)y, rows, hz, (bf16*)a_cm, (bf16*)b_cm)
+  // paired 4-byte stores need an even row count and 4-byte aligned channel-major outputs
+  const bool pairs = (rows & 1) == 0 && ((uintptr_t)a_cm & 3) == 0 && ((uintptr_t)b_cm & 3) == 0;
+#define TG(PP) tri_gate_fwd_k<PP><<<g, 256, 0, st>>>((const bf16*)y, rows, hz, (bf16*)a_cm, (bf16*)b_cm, pairs)
   switch (p) {
     case 2: TG(2); break;
     case 4: TG(4); break;
@@ -647,5 +650,49 @@ extern "C" int evo_residual_layernorm_fwd(const void* res, const void* y, int64_
   }
 #undef RLN
   EVO_LAUNCH_CHECK("residual_layernorm fwd");
+  return EVO_OK;
+}
+
+// ------------------------------------------------------------------ gate multiply
+// out = act(gate) * (y + bias) elementwise over a [rows, cols] view with row strides;
+// gate NULL -> factor 1, y NULL -> (y + bias) = 1.  The reference's private triangle helpers
+// (_triangle_projections g = sigmoid(.), _triangle_finish g * (.), evoformer.py:258-270) and
+// the engine's sigmoid_raw / relu_raw (engine.py:220-225) on the reference-API path; the
+// block itself fuses these into its epilogues.
+template <typename T>
+__global__ void __launch_bounds__(256) gate_mul_k(const T* __restrict__ gate, int64_t gate_rs, int act,
+                                                  const T* __restrict__ y, int64_t y_rs,
+                                                  const float* __restrict__ bias, T* __restrict__ out,
+                                                  int64_t out_rs, int64_t rows, int64_t cols) {
+  const int64_t n = rows * cols;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i - r * cols;
+    float f = 1.f;
+    if (y) f = (float)y[r * y_rs + c] + (bias ? bias[c] : 0.f);
+    if (gate) {
+      float gv = (float)gate[r * gate_rs + c];
+      gv = act == 1 ? sigmoidf_(gv) : (act == 2 ? fmaxf(gv, 0.f) : gv);
+      f = __fmul_rn(gv, f);
+    }
+    out[r * out_rs + c] = (T)f;
+  }
+}
+
+extern "C" int evo_gate_mul_fwd(const void* gate, int64_t gate_rs, int gate_act, const void* y, int64_t y_rs,
+                                const float* bias, void* out, int64_t out_rs, int dtype, int64_t rows, int64_t cols,
+                                void* stream) {
+  EVO_CHECK_ARG(out && (gate || y), EVO_ERR_ARG, "gate_mul: need out and at least one of gate / y");
+  EVO_CHECK_ARG(gate_act >= 0 && gate_act <= 2, EVO_ERR_ARG, "gate_mul: act must be 0 (identity), 1 (sigmoid), 2 (relu)");
+  EVO_CHECK_ARG(rows >= 0 && cols >= 0, EVO_ERR_SHAPE, "gate_mul: negative extent");
+  if (rows == 0 || cols == 0) return EVO_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned g = grid_for(rows * cols, 256);
+  if (dtype == EVO_BF16)
+    gate_mul_k<bf16><<<g, 256, 0, st>>>((const bf16*)gate, gate_rs, gate_act, (const bf16*)y, y_rs, bias, (bf16*)out,
+                                        out_rs, rows, cols);
+  else
+    gate_mul_k<float><<<g, 256, 0, st>>>((const float*)gate, gate_rs, gate_act, (const float*)y, y_rs, bias,
+                                         (float*)out, out_rs, rows, cols);
+  EVO_LAUNCH_CHECK("gate_mul fwd");
   return EVO_OK;
 }

@@ -20,6 +20,10 @@ Training entry points (the reference has none): ``BlockParams``,
 
 from __future__ import annotations
 
+import hashlib
+import math
+from collections import OrderedDict
+
 import numpy as np
 import torch
 
@@ -27,24 +31,29 @@ from . import block as _blk
 from . import ops
 from .config import EvoConfig
 from .errors import DimensionError, DomainError, KernelError
+from .ops import Strided
 from .params import BlockLayout, BlockParams
 
 __all__ = ["evoformer_block", "msa_row_attention", "msa_row_bias", "msa_row_attention_with_bias",
-           "msa_col_attention", "transition", "outer_product_mean", "tri_update_outgoing",
-           "tri_update_incoming", "pair_attention_row", "pair_attention_col", "layernorm",
-           "fused_softmax_mask_bias", "BlockParams", "block_forward_backward", "EvoformerStack",
-           "EvoformerBlockFunction", "GraphedStep"]
+           "msa_col_attention", "transition", "outer_product_mean", "outer_product_mean_from_projections",
+           "tri_update_outgoing", "tri_update_incoming", "pair_attention_row", "pair_attention_col",
+           "layernorm", "layernorm_raw", "softmax_raw", "sigmoid_raw", "relu_raw", "fused_softmax_mask_bias",
+           "fused_softmax_mask_bias_raw", "_attention_core", "_triangle_projections", "_triangle_finish",
+           "_pair_bias_fn", "_check_msa", "_check_pair", "BlockParams", "block_forward_backward",
+           "EvoformerStack", "EvoformerBlockFunction", "GraphedStep"]
 
 _DEV = "cuda"
 
 
 def _check_msa(m, cfg):
+    """evoformer.py:328-332"""
     if tuple(m.shape) != (cfg.n_seq, cfg.n_res, cfg.h_msa):
         raise DimensionError(f"MSA tensor shape {tuple(m.shape)} does not match config "
                              f"({cfg.n_seq}, {cfg.n_res}, {cfg.h_msa})")
 
 
 def _check_pair(z, cfg):
+    """evoformer.py:335-339"""
     if tuple(z.shape) != (cfg.n_res, cfg.n_res, cfg.h_pair):
         raise DimensionError(f"pair tensor shape {tuple(z.shape)} does not match config "
                              f"({cfg.n_res}, {cfg.n_res}, {cfg.h_pair})")
@@ -55,15 +64,15 @@ def _require_cuda():
         raise KernelError("the B200 Evoformer engine needs a CUDA device (no CPU fallback)")
 
 
-def _to_dev(x):
-    """-> (bf16 contiguous CUDA tensor, was_numpy)"""
+def _to_dev(x, dtype=torch.bfloat16):
+    """-> (contiguous CUDA tensor of `dtype`, was_numpy)"""
     if isinstance(x, np.ndarray):
         _require_cuda()
-        return torch.from_numpy(np.ascontiguousarray(x)).to(_DEV).to(torch.bfloat16), True
+        return torch.from_numpy(np.ascontiguousarray(x)).to(_DEV).to(dtype), True
     if isinstance(x, torch.Tensor):
         if not x.is_cuda:
             raise KernelError("torch inputs must be CUDA tensors (no CPU fallback)")
-        return x.to(torch.bfloat16).contiguous(), False
+        return x.to(dtype).contiguous(), False
     raise TypeError(f"unsupported input type {type(x)}")
 
 
@@ -71,119 +80,217 @@ def _out(t, was_np):
     return t.double().cpu().numpy() if was_np else t
 
 
-_PARAM_CACHE: dict = {}
+# ----------------------------------------------------------------------------- parameter cache
+_PARAM_CACHE: OrderedDict = OrderedDict()
+_PARAM_CACHE_SIZE = 4
 
 
-def _block_params(p, cfg: EvoConfig) -> BlockParams:
+def _fingerprint(p) -> bytes:
+    """content hash of a reference parameter dict (keys, shapes, bytes): the packed device copy
+    is reused only while the weights are unchanged, so in-place edits of p (an optimizer step,
+    a finite-difference probe) are always seen - the reference re-reads p on every call."""
+    h = hashlib.blake2b(digest_size=20)
+    for k in sorted(p):
+        v = p[k]
+        a = v.detach().cpu().numpy() if isinstance(v, torch.Tensor) else np.asarray(v)
+        a = np.ascontiguousarray(a)
+        h.update(k.encode())
+        h.update(repr((a.shape, a.dtype.str)).encode())
+        h.update(memoryview(a).cast("B"))
+    return h.digest()
+
+
+def _block_params(p, cfg: EvoConfig, partial: bool = False) -> BlockParams:
     if isinstance(p, BlockParams):
         return p
-    key = (id(p), cfg)
+    key = (_fingerprint(p), cfg, partial)
     hit = _PARAM_CACHE.get(key)
-    if hit is not None and hit[0] is p:
-        return hit[1]
+    if hit is not None:
+        _PARAM_CACHE.move_to_end(key)
+        return hit
     _require_cuda()
-    bp = BlockParams(p, cfg, device=_DEV)
-    _PARAM_CACHE.clear()
-    _PARAM_CACHE[key] = (p, bp)
+    bp = BlockParams(p, cfg, device=_DEV, partial=partial)
+    _PARAM_CACHE[key] = bp
+    while len(_PARAM_CACHE) > _PARAM_CACHE_SIZE:
+        _PARAM_CACHE.popitem(last=False)
     return bp
+
+
+def _count_heads(p, mod):
+    n = 0
+    while f"{mod}/q/{n}/w" in p:
+        n += 1
+    return n
+
+
+def _infer_cfg(p, prefix: str | None = None, n_head: int | None = None, c: int | None = None) -> EvoConfig:
+    """EvoConfig for the parameter layout of ``p`` (the reference's private helpers take no
+    cfg).  Only the dimensions of the keys present matter; absent modules get placeholder
+    extents (their packed entries stay zero).  n_seq / n_res do not enter the layout."""
+    if isinstance(p, BlockParams):
+        return p.cfg
+    sh = lambda k, ax: int(np.shape(p[k])[ax]) if k in p else None
+    first = lambda *v: next((x for x in v if x), None)
+    h_msa = first(sh("msa_row/ln/g", 0), sh("msa_col/ln/g", 0), sh("msa_trans/ln/g", 0), sh("opm/ln/g", 0))
+    h_pair = first(sh("msa_row/ln_z/g", 0), sh("pair_row/ln/g", 0), sh("pair_col/ln/g", 0), sh("pair_trans/ln/g", 0),
+                   sh("tri_out/ln/g", 0), sh("tri_in/ln/g", 0), sh("opm/o/b", 0))
+    nh_m = first(_count_heads(p, "msa_row"), _count_heads(p, "msa_col"))
+    nh_p = first(_count_heads(p, "pair_row"), _count_heads(p, "pair_col"))
+    if prefix is not None and n_head is not None and c is not None:
+        if prefix.startswith("msa"):
+            h_msa, nh_m = n_head * c, n_head
+        else:
+            h_pair, nh_p = n_head * c, n_head
+    proj = first(sh("opm/a/w", 1), sh("tri_out/a_sig/w", 1), sh("tri_in/a_sig/w", 1))
+    h_msa = h_msa or 8 * (nh_m or 1)
+    h_pair = h_pair or 8 * (nh_p or 1)
+    nh_m = nh_m if nh_m and h_msa % nh_m == 0 else 1
+    nh_p = nh_p if nh_p and h_pair % nh_p == 0 else 1
+    tf = first(sh("msa_trans/w1", 1) and sh("msa_trans/w1", 1) // h_msa,
+               sh("pair_trans/w1", 1) and sh("pair_trans/w1", 1) // h_pair) or 4
+    return EvoConfig(1, 1, h_msa, h_pair, nh_m, nh_p, proj or 8, tf)
 
 
 # ----------------------------------------------------------------------------- engine ops
 def layernorm(x, gamma, beta, eps: float = 1e-5):
-    """engine.layernorm (engine.py:206-217) on the GPU; returns the input's type."""
-    xt, was_np = _to_dev(x) if isinstance(x, np.ndarray) else (x.contiguous(), False)
-    if xt.dtype not in (torch.float32, torch.bfloat16):
-        xt = xt.float()
+    """engine.layernorm_raw (engine.py:206-217) on the GPU (fp32 math); returns the input's type."""
+    if isinstance(x, np.ndarray):
+        xt, was_np = _to_dev(x, torch.float32)
+    else:
+        xt, was_np = x.contiguous(), False
+        if xt.dtype not in (torch.float32, torch.bfloat16):
+            xt = xt.float()
     if tuple(np.shape(gamma)) != (xt.shape[-1],) or tuple(np.shape(beta)) != (xt.shape[-1],):
-        raise DimensionError(f"layernorm params must match last extent {xt.shape[-1]}")
-    if was_np:
-        xt = torch.from_numpy(np.ascontiguousarray(x)).to(_DEV).float()
+        raise DimensionError(f"layernorm params must match last extent {xt.shape[-1]}, "
+                             f"got gamma {tuple(np.shape(gamma))}, beta {tuple(np.shape(beta))}")
     g = torch.as_tensor(np.asarray(gamma) if not isinstance(gamma, torch.Tensor) else gamma,
                         dtype=torch.float32, device=xt.device)
     b = torch.as_tensor(np.asarray(beta) if not isinstance(beta, torch.Tensor) else beta,
                         dtype=torch.float32, device=xt.device)
     C = xt.shape[-1]
     y, _, _ = ops.layernorm_fwd(xt, g, b, xt.numel() // C, C, eps=eps, save_stats=False)
-    y = y.view(xt.shape)
-    return _out(y, was_np)
+    return _out(y.view(xt.shape), was_np)
+
+
+layernorm_raw = layernorm
+
+
+def _elementwise(x, act):
+    xt, was_np = _to_dev(x, torch.float32) if isinstance(x, np.ndarray) else (x.contiguous(), False)
+    if xt.numel() == 0:
+        return _out(xt.clone(), was_np)
+    C = xt.shape[-1] if xt.dim() else 1
+    y = ops.gate_mul(xt.reshape(-1, C), act=act)
+    return _out(y.view(xt.shape), was_np)
+
+
+def sigmoid_raw(x):
+    """engine.sigmoid_raw (engine.py:220-221)"""
+    return _elementwise(x, 1)
+
+
+def relu_raw(x):
+    """engine.relu_raw (engine.py:224-225)"""
+    return _elementwise(x, 2)
 
 
 def fused_softmax_mask_bias(x, mask, bias, axis: int = -1, check_finite: bool = True):
-    """engine.fused_softmax_mask_bias (engine.py:291-298): softmax(x + mask + bias, axis).
+    """engine.fused_softmax_mask_bias(_raw) (engine.py:193-203, 291-298): softmax(x + mask + bias, axis).
 
-    One fused kernel; the only allocation is the output.  Like the reference,
-    non-finite input raises ``DomainError`` (checked on the device).
-    """
+    One fused kernel (fp32 math); mask and bias broadcast right-aligned exactly as numpy
+    does.  Like the reference: an out-of-range axis raises ``DimensionError``, a
+    non-finite operand raises ``DomainError`` (checked on the device)."""
     def dev(a):
-        if isinstance(a, np.ndarray):
+        if isinstance(a, np.ndarray) or np.isscalar(a):
             _require_cuda()
-            return torch.from_numpy(np.ascontiguousarray(a)).to(_DEV).float(), True
-        return a, False
+            return torch.as_tensor(np.asarray(a, dtype=np.float64)).to(_DEV).float(), True
+        return a.float(), False
 
     xt, was_np = dev(x)
     mt, _ = dev(mask)
     bt, _ = dev(bias)
     try:
-        shape = torch.broadcast_shapes(xt.shape, mt.shape, bt.shape)
+        shape = tuple(torch.broadcast_shapes(xt.shape, mt.shape, bt.shape))
     except RuntimeError as exc:
-        raise DimensionError(f"mask/bias not broadcastable to {tuple(xt.shape)}") from exc
-    if tuple(shape) != tuple(xt.shape):
-        raise DimensionError(f"mask/bias broadcast would change the shape of x {tuple(xt.shape)}")
-    nd = xt.dim()
-    ax = axis % nd
-    if ax != nd - 1:
-        xt, mt, bt = (t.movedim(ax, -1) if t.dim() == nd else t for t in (xt, mt, bt))
-    if check_finite and ops.count_nonfinite(xt.contiguous()) > 0:
+        raise DimensionError(f"mask/bias not broadcastable to {tuple(xt.shape)}: mask {tuple(mt.shape)}, "
+                             f"bias {tuple(bt.shape)}") from exc
+    nd = len(shape)
+    if not -nd <= axis < nd:
+        raise DimensionError(f"softmax axis {axis} out of range for rank {nd}")
+    if check_finite and sum(ops.count_nonfinite(t.contiguous()) for t in (xt, mt, bt) if t.numel()) > 0:
         raise DomainError("softmax input contains non-finite values")
+    if tuple(xt.shape) != shape:   # the reference's x + mask + bias broadcasts x up as well
+        xt = xt.expand(shape)
+    # operands at x's rank (leading 1s), the softmax axis moved last
+    full = lambda t: t.reshape((1,) * (nd - t.dim()) + tuple(t.shape))
+    ax = axis % nd
+    xt, mt, bt = (full(t).movedim(ax, -1) for t in (xt, mt, bt))
+    xt = xt.contiguous()
     lead = xt.shape[:-1]
-    x4 = xt.contiguous().reshape((-1,) + (1, 1) + (xt.shape[-1],)) if len(lead) > 3 else xt
-    if len(lead) > 3:
-        raise DimensionError("fused_softmax_mask_bias supports rank <= 4")
-    y = ops.softmax_fwd(x4, bt if bt.dim() <= 4 else None, mt if mt.dim() <= 4 else None, 1.0)
-    if ax != nd - 1:
-        y = y.movedim(-1, ax)
-    return _out(y.float().contiguous(), was_np) if was_np else y
+    if nd > 4:   # collapse leading axes into one (mask/bias materialised at x's shape)
+        mt, bt = (t.expand(xt.shape).reshape(-1, xt.shape[-1]) for t in (mt, bt))
+        xt = xt.reshape(-1, xt.shape[-1])
+    y = ops.softmax_fwd(xt, bt, mt, 1.0)
+    y = y.reshape(tuple(lead) + (shape[ax],)).movedim(-1, ax)
+    return _out(y.contiguous(), was_np) if was_np else y
 
 
-# ----------------------------------------------------------------------------- sub-modules
-def msa_row_bias(z, p, cfg: EvoConfig):
-    """evoformer.py:201-207 -> [N_r, N_r, n_head] (reference layout)."""
-    _check_pair(z, cfg)
-    zt, was_np = _to_dev(z)
-    bp = _block_params(p, cfg)
-    bias, _ = _blk.msa_row_bias_fwd(bp, zt.view(-1, cfg.h_pair), cfg.n_res, save=False)
-    return _out(bias.permute(1, 2, 0).contiguous(), was_np)
+fused_softmax_mask_bias_raw = fused_softmax_mask_bias
 
 
-def msa_row_attention_with_bias(m, bias, p, cfg: EvoConfig, return_weights: bool = False):
-    """evoformer.py:210-216; bias [N_r, N_r, n_head] (reference layout)."""
-    _check_msa(m, cfg)
-    mt, was_np = _to_dev(m)
-    bt, _ = _to_dev(bias)
-    bp = _block_params(p, cfg)
-    S, R = cfg.n_seq, cfg.n_res
-    bh = bt.permute(2, 0, 1).contiguous()
-    x2 = mt.view(S * R, cfg.h_msa)
-    res = _update_exact(bp, "msa_row", x2, S, R, "row", bh)
-    if return_weights:
-        _, sv = _blk.attention_fwd(bp, "msa_row", x2, S, R, "row", bias=bh, save=True)
-        return _out(res, was_np), _attention_weights(bp, sv)
-    return _out(res, was_np)
+def softmax_raw(x, axis: int):
+    """engine.softmax_raw (engine.py:183-190) incl. its DimensionError / DomainError."""
+    z = np.zeros(()) if isinstance(x, np.ndarray) else torch.zeros((), device=x.device)
+    return fused_softmax_mask_bias(x, z, z, axis)
 
 
-def _update_exact(bp, mod, x2d, B, L, kind, bias):
-    """the sub-module update f(x) itself (reference returns f(x), not x + f(x)):
-    run with a zero residual so no bf16 cancellation happens."""
-    a = bp.layout.attn[mod]
-    out, _ = _attention_update(bp, mod, x2d, torch.zeros_like(x2d), B, L, kind, bias)
-    if kind == "row":
-        return out.view(B, L, a["H"])
-    return out.view(L, B, a["H"])
+# ----------------------------------------------------------------------------- attention core
+class _PairBias:
+    """``_pair_bias_fn(p, prefix)`` (evoformer.py:287-292): per-key bias (LN(x) . w_h)[:, None, :].
+    Callable like the reference's closure; ``_attention_core`` recognises it and runs the
+    fused per-key path (the bias is an extra column group of the q/k/v GEMM)."""
+
+    def __init__(self, p, prefix):
+        self.p, self.prefix = p, prefix
+
+    def __call__(self, ln, hh):
+        w = self.p[f"{self.prefix}/bias/{hh}/w"]
+        if isinstance(ln, torch.Tensor):
+            return (ln.float() @ torch.as_tensor(np.asarray(w), dtype=torch.float32, device=ln.device))[:, None, :]
+        return (ln @ w)[:, None, :]
 
 
-def _attention_update(bp, mod, x2d, res, B, L, kind, bias):
-    import math
-    from .ops import Strided
+def _pair_bias_fn(p, prefix):
+    return _PairBias(p, prefix)
+
+
+def _bias_from_fn(bias_fn, ln2d, B, L, nh, was_np):
+    """a generic bias_fn(ln, head) (anything broadcastable to [B, L, L]) -> a bf16 tensor
+    [Bb, nh, Lq, L] (Bb in {1, B}, Lq in {1, L}) and its (batch, head, query, key) strides."""
+    ln = ln2d.view(B, L, -1)
+    ln_arg = ln.double().cpu().numpy() if was_np else ln.float()
+    heads = []
+    for hh in range(nh):
+        b = bias_fn(ln_arg, hh)
+        b = torch.as_tensor(np.asarray(b) if not isinstance(b, torch.Tensor) else b, device=ln.device).float()
+        if b.dim() > 3:
+            raise DimensionError(f"bias of rank {b.dim()} does not broadcast against [B, L, L] logits")
+        b = b.reshape((1,) * (3 - b.dim()) + tuple(b.shape))
+        try:
+            torch.broadcast_shapes(tuple(b.shape), (B, L, L))
+        except RuntimeError as exc:
+            raise DimensionError(f"bias {tuple(b.shape)} not broadcastable to logits {(B, L, L)}") from exc
+        heads.append(b)
+    bb = max(h.shape[0] for h in heads)
+    bq = max(h.shape[1] for h in heads)
+    t = torch.stack([h.expand(bb, bq, L) for h in heads], 1).to(torch.bfloat16).contiguous()  # [bb, nh, bq, L]
+    strides = (nh * bq * L if bb > 1 else 0, bq * L, L if bq > 1 else 0, 1)
+    return t, strides
+
+
+def _attention_update(bp, mod, x2d, res, B, L, kind, bias_t=None, bias_s=(0, 0, 0, 0), bias_off=0):
+    """res + (gated attention of mod over the [B, L, H] view of x2d); bias_t may be the string
+    "pair" (per-key bias from the merged projection)."""
     a = bp.layout.attn[mod]
     H, nh, c, ldq = a["H"], a["nh"], a["c"], a["ldq"]
     rows = B * L
@@ -194,44 +301,113 @@ def _attention_update(bp, mod, x2d, res, B, L, kind, bias):
     og = torch.empty(rows, nh * c, device=x2d.device, dtype=torch.bfloat16)
     sbr, slr = _blk._attn_geometry(kind, B, L)
     S_ = lambda t, ld, off=0: Strided(t, sbr * ld, slr * ld, off)
-    if bias is None:
-        bt, bs, boff = None, (0, 0, 0, 0), 0
-    elif isinstance(bias, str):
-        bt, bs, boff = qkv, (sbr * ldq, 1, 0, slr * ldq), 3 * nh * c
-    else:
-        bt, bs, boff = bias, (0, L * L, L, 1), 0
+    if isinstance(bias_t, str):
+        bias_t, bias_s, bias_off = qkv, (sbr * ldq, 1, 0, slr * ldq), 3 * nh * c
     desc = ops.attention_desc(S_(qkv, ldq, 0), S_(qkv, ldq, nh * c), S_(qkv, ldq, 2 * nh * c), S_(gpre, nh * c),
                               S_(og, nh * c), None, None, B, L, nh, c, 1.0 / math.sqrt(c),
-                              bias=bt, bias_s=bs, bias_off=boff)
+                              bias=bias_t, bias_s=bias_s, bias_off=bias_off)
     ops.attention_fwd(desc)
     y = torch.mm(og, h[f"{mod}.w_o"])
-    return ops.gated_residual_fwd(res, y, f[f"{mod}.b_o"], rows, H), None
+    out = ops.gated_residual_fwd(res, y, f[f"{mod}.b_o"], rows, H) if res is not None else \
+        ops.gate_mul(None, y=y, bias=f[f"{mod}.b_o"])
+    return out, (ln, qkv)
 
 
-def _attention_weights(bp, sv):
+def _attention_weights(bp, mod, qkv, B, L, kind, bias_t=None, bias_s=None, pair=False):
     """debug path for return_weights=True: softmax((qk^T + bias)/sqrt(c)) per head, materialised
     with the fused softmax kernel (the flash kernel never materialises them)."""
-    import math
-    mod, B, L, kind = sv["mod"], sv["B"], sv["L"], sv["kind"]
     a = bp.layout.attn[mod]
     nh, c, ldq = a["nh"], a["c"], a["ldq"]
-    qkv = sv["qkv"].float()
-    if kind == "row":
-        qkv = qkv.view(B, L, ldq)
-    else:
-        qkv = qkv.view(L, B, ldq).transpose(0, 1)
+    qkv = qkv.float()
+    qkv = qkv.view(B, L, ldq) if kind == "row" else qkv.view(L, B, ldq).transpose(0, 1)
     q = qkv[..., :nh * c].reshape(B, L, nh, c).permute(0, 2, 1, 3)
     k = qkv[..., nh * c:2 * nh * c].reshape(B, L, nh, c).permute(0, 2, 1, 3)
     logits = (q @ k.transpose(-1, -2)).contiguous()
-    bias = sv["bias"]
-    if bias is None:
-        bt = None
-    elif isinstance(bias, str):
+    if pair:
         bt = qkv[..., 3 * nh * c:3 * nh * c + nh].permute(0, 2, 1)[:, :, None, :].contiguous()
+    elif bias_t is not None:
+        bt = torch.as_strided(bias_t, (B, nh, L, L), bias_s).float()
     else:
-        bt = bias.float()[None]
+        bt = None
     w = ops.softmax_fwd(logits, bt, None, 1.0 / math.sqrt(c))
-    return [w[:, hh].double().cpu().numpy() for hh in range(nh)]
+    return [w[:, hh] for hh in range(nh)]
+
+
+def _attn_api(x, p, cfg, mod, kind, bias=None, return_weights=False, bias_fn=None, partial=False):
+    """the reference's attention sub-modules: f(x) (not x + f(x)).  x [B, L, H] for kind "row";
+    for "col" x is [L, B, H] and attention runs along its first axis (no transpose copy).
+    bias: None, "pair", or a bf16 tensor [nh, L, L] shared over the batch; bias_fn: a
+    generic reference bias_fn(ln, head)."""
+    xt, was_np = _to_dev(x)
+    if xt.dim() != 3:
+        raise DimensionError(f"attention input must be [B, L, H], got {tuple(xt.shape)}")
+    bp = _block_params(p, cfg, partial=partial)
+    a = bp.layout.attn[mod]
+    if xt.shape[-1] != a["H"]:
+        raise DimensionError(f"{mod}: input channels {xt.shape[-1]} != {a['H']}")
+    B, L = (xt.shape[0], xt.shape[1]) if kind == "row" else (xt.shape[1], xt.shape[0])
+    x2 = xt.view(B * L, a["H"])
+    bias_t, bias_s = None, (0, 0, 0, 0)
+    if isinstance(bias, str):
+        bias_t = bias
+    elif bias is not None:
+        bias_t, bias_s = bias, (0, L * L, L, 1)
+    elif bias_fn is not None:
+        ln, _, _ = ops.layernorm_fwd(x2, bp.f[f"{mod}.ln_g"], bp.f[f"{mod}.ln_b"], B * L, a["H"], save_stats=False)
+        bias_t, bias_s = _bias_from_fn(bias_fn, ln, B, L, a["nh"], was_np)
+    out, (_, qkv) = _attention_update(bp, mod, x2, None, B, L, kind, bias_t, bias_s)
+    res = _out(out.view(xt.shape), was_np)
+    if not return_weights:
+        return res
+    w = _attention_weights(bp, mod, qkv, B, L, kind, None if isinstance(bias_t, str) else bias_t, bias_s,
+                           pair=isinstance(bias_t, str))
+    return res, [_out(t, was_np) for t in w]
+
+
+def _attention_core(x, p, prefix, n_head, c, bias_fn=None, return_weights=False):
+    """evoformer.py:173-198: gated multi-head attention over the middle axis of x [B, L, H];
+    bias_fn(ln, head) broadcastable to [B, L, L] is added before the 1/sqrt(c) scale.  Works
+    on shards (the reference's DAP block calls it per device, dap_block.py:72-75, 133-145)."""
+    if prefix not in BlockLayout.ATTN:
+        raise DimensionError(f"unknown attention module {prefix!r} (one of {BlockLayout.ATTN})")
+    if not isinstance(p, BlockParams):
+        w = p.get(f"{prefix}/q/0/w")
+        if _count_heads(p, prefix) != n_head or w is None or int(np.shape(w)[1]) != c:
+            raise DimensionError(f"{prefix}: n_head={n_head}, c={c} do not match the parameters "
+                                 f"({_count_heads(p, prefix)} heads, q/0/w {None if w is None else np.shape(w)})")
+    cfg = _infer_cfg(p, prefix, n_head, c)
+    bp = _block_params(p, cfg, partial=True)
+    a = bp.layout.attn[prefix]
+    if (a["nh"], a["c"]) != (n_head, c):
+        raise DimensionError(f"{prefix}: n_head={n_head}, c={c} do not match the parameters ({a['nh']}, {a['c']})")
+    if isinstance(bias_fn, _PairBias) and bias_fn.prefix == prefix and a["pair_bias"]:
+        return _attn_api(x, bp, cfg, prefix, "row", bias="pair", return_weights=return_weights)
+    return _attn_api(x, bp, cfg, prefix, "row", bias_fn=bias_fn, return_weights=return_weights)
+
+
+# ----------------------------------------------------------------------------- sub-modules
+def msa_row_bias(z, p, cfg: EvoConfig):
+    """evoformer.py:201-207: [.., .., H_z] -> [.., .., n_head] (any pair rows: a DAP row shard
+    gives its rows of the bias, dap_block.py:63)."""
+    zt, was_np = _to_dev(z)
+    if zt.dim() != 3 or zt.shape[-1] != cfg.h_pair:
+        raise DimensionError(f"pair tensor {tuple(zt.shape)} must be [n_i, n_j, {cfg.h_pair}]")
+    bp = _block_params(p, cfg)
+    n_i, n_j = zt.shape[0], zt.shape[1]
+    bias, _ = _blk.msa_row_bias_fwd(bp, zt.view(-1, cfg.h_pair), n_i, n_j, save=False)
+    return _out(bias.permute(1, 2, 0).contiguous(), was_np)
+
+
+def msa_row_attention_with_bias(m, bias, p, cfg: EvoConfig, return_weights: bool = False):
+    """evoformer.py:210-216; bias [N_r, N_r, n_head] (reference layout) shared by every sequence
+    of m [B, N_r, H_m] (a DAP sequence shard is fine, dap_block.py:65-66)."""
+    bt, _ = _to_dev(bias)
+    L = m.shape[1] if len(m.shape) == 3 else -1
+    if bt.dim() == 3 and tuple(bt.shape) == (L, L, cfg.n_head_msa):
+        return _attn_api(m, p, cfg, "msa_row", "row", bias=bt.permute(2, 0, 1).contiguous(),
+                         return_weights=return_weights)
+    return _attn_api(m, p, cfg, "msa_row", "row", bias_fn=lambda _ln, hh: bias[..., hh],
+                     return_weights=return_weights)
 
 
 def msa_row_attention(m, z, p, cfg: EvoConfig, return_weights: bool = False):
@@ -241,65 +417,38 @@ def msa_row_attention(m, z, p, cfg: EvoConfig, return_weights: bool = False):
     zt, _ = _to_dev(z)
     bp = _block_params(p, cfg)
     bias, _ = _blk.msa_row_bias_fwd(bp, zt.view(-1, cfg.h_pair), cfg.n_res, save=False)
-    mt, was_np = _to_dev(m)
-    S, R = cfg.n_seq, cfg.n_res
-    x2 = mt.view(S * R, cfg.h_msa)
-    res = _update_exact(bp, "msa_row", x2, S, R, "row", bias)
-    if return_weights:
-        _, sv = _blk.attention_fwd(bp, "msa_row", x2, S, R, "row", bias=bias, save=True)
-        return _out(res, was_np), _attention_weights(bp, sv)
-    return _out(res, was_np)
+    return _attn_api(m, bp, cfg, "msa_row", "row", bias=bias.contiguous(), return_weights=return_weights)
 
 
 def msa_col_attention(m, p, cfg: EvoConfig, return_weights: bool = False):
     """evoformer.py:226-234 (no bias, G5); no transpose copy is made."""
     _check_msa(m, cfg)
-    mt, was_np = _to_dev(m)
-    bp = _block_params(p, cfg)
-    S, R = cfg.n_seq, cfg.n_res
-    x2 = mt.view(S * R, cfg.h_msa)
-    res = _update_exact(bp, "msa_col", x2, R, S, "col", None)   # [S, R, H] already
-    if return_weights:
-        _, sv = _blk.attention_fwd(bp, "msa_col", x2, R, S, "col", save=True)
-        return _out(res, was_np), _attention_weights(bp, sv)
-    return _out(res, was_np)
+    return _attn_api(m, p, cfg, "msa_col", "col", return_weights=return_weights)
 
 
 def pair_attention_row(z, p, cfg: EvoConfig, return_weights: bool = False):
     """evoformer.py:295-299 (per-key self bias, G4)."""
     _check_pair(z, cfg)
-    zt, was_np = _to_dev(z)
-    bp = _block_params(p, cfg)
-    R = cfg.n_res
-    x2 = zt.view(R * R, cfg.h_pair)
-    res = _update_exact(bp, "pair_row", x2, R, R, "row", "pair")
-    if return_weights:
-        _, sv = _blk.attention_fwd(bp, "pair_row", x2, R, R, "row", bias="pair", save=True)
-        return _out(res, was_np), _attention_weights(bp, sv)
-    return _out(res, was_np)
+    return _attn_api(z, p, cfg, "pair_row", "row", bias="pair", return_weights=return_weights)
 
 
 def pair_attention_col(z, p, cfg: EvoConfig, return_weights: bool = False):
     """evoformer.py:302-311."""
     _check_pair(z, cfg)
-    zt, was_np = _to_dev(z)
-    bp = _block_params(p, cfg)
-    R = cfg.n_res
-    x2 = zt.view(R * R, cfg.h_pair)
-    res = _update_exact(bp, "pair_col", x2, R, R, "col", "pair")
-    if return_weights:
-        _, sv = _blk.attention_fwd(bp, "pair_col", x2, R, R, "col", bias="pair", save=True)
-        return _out(res, was_np), _attention_weights(bp, sv)
-    return _out(res, was_np)
+    return _attn_api(z, p, cfg, "pair_col", "col", bias="pair", return_weights=return_weights)
 
 
 def transition(x, p, prefix: str, cfg: EvoConfig | None = None):
-    """evoformer.py:237-240.  cfg may be omitted when p is a reference dict."""
+    """evoformer.py:237-240: LN -> W1 + b1 -> ReLU -> W2 + b2 over the last axis of x (any
+    leading shape).  The widths come from p[f"{prefix}/ln/g"] and p[f"{prefix}/w1"] as in the
+    reference; cfg is accepted for symmetry and ignored."""
+    if prefix not in ("msa_trans", "pair_trans"):
+        raise DimensionError(f"unknown transition {prefix!r}")
     xt, was_np = _to_dev(x)
-    if cfg is None:
-        cfg = _infer_cfg(p)
-    bp = _block_params(p, cfg)
-    H = xt.shape[-1]
+    H = int(np.shape(p[f"{prefix}/ln/g"])[0])
+    if xt.shape[-1] != H:
+        raise DimensionError(f"{prefix}: input channels {xt.shape[-1]} != {H}")
+    bp = _block_params(p, _infer_cfg(p), partial=True)
     rows = xt.numel() // H
     x2 = xt.view(rows, H)
     f, h = bp.f, bp.h
@@ -307,12 +456,12 @@ def transition(x, p, prefix: str, cfg: EvoConfig | None = None):
     hid = torch.mm(ln, h[f"{prefix}.w1"])
     ops.bias_act_fwd(hid, f[f"{prefix}.b1"], rows, hid.shape[1])
     y = torch.mm(hid, h[f"{prefix}.w2"])
-    out = ops.gated_residual_fwd(torch.zeros_like(x2), y, f[f"{prefix}.b2"], rows, H)
+    out = ops.gate_mul(None, y=y, bias=f[f"{prefix}.b2"])
     return _out(out.view(xt.shape), was_np)
 
 
 def outer_product_mean(m, p, cfg: EvoConfig):
-    """evoformer.py:243-255."""
+    """evoformer.py:243-248."""
     _check_msa(m, cfg)
     mt, was_np = _to_dev(m)
     bp = _block_params(p, cfg)
@@ -322,16 +471,73 @@ def outer_product_mean(m, p, cfg: EvoConfig):
     return _out(out.view(R, R, cfg.h_pair), was_np)
 
 
+def outer_product_mean_from_projections(a, b, p, cfg: EvoConfig):
+    """evoformer.py:251-255: mean over sequences of the outer product of a [S, I, P] and
+    b [S, J, P] (one tcgen05 GEMM), then @ W_o + b_o -> [I, J, H_z]."""
+    at, was_np = _to_dev(a)
+    bt, _ = _to_dev(b)
+    if at.dim() != 3 or bt.dim() != 3 or at.shape[0] != bt.shape[0] or at.shape[2] != bt.shape[2]:
+        raise DimensionError(f"projections {tuple(at.shape)} / {tuple(bt.shape)} must be [S, I, P] / [S, J, P]")
+    bp = _block_params(p, cfg, partial=True)
+    S, I, P = at.shape
+    J = bt.shape[1]
+    if P != cfg.hidden_proj:
+        raise DimensionError(f"projection width {P} != hidden_proj {cfg.hidden_proj}")
+    o = _blk.opm_contract(at.view(S, I * P), bt.view(S, J * P), S, I, J, P)
+    y = torch.mm(o.view(I * J, P * P), bp.h["opm.w_o"])
+    out = ops.gate_mul(None, y=y, bias=bp.f["opm.b_o"])
+    return _out(out.view(I, J, cfg.h_pair), was_np)
+
+
+def _triangle_projections(z, p, prefix):
+    """evoformer.py:258-265 -> (g = sigmoid(.), a, b) over the last axis of z (any leading shape;
+    a DAP shard is fine, dap_block.py:98, 115): the merged [g|a_sig|a_lin|b_sig|b_lin] GEMM."""
+    if prefix not in ("tri_out", "tri_in"):
+        raise DimensionError(f"unknown triangle module {prefix!r}")
+    zt, was_np = _to_dev(z)
+    bp = _block_params(p, _infer_cfg(p), partial=True)
+    Hz, P = bp.cfg.h_pair, bp.cfg.hidden_proj
+    if zt.shape[-1] != Hz:
+        raise DimensionError(f"{prefix}: input channels {zt.shape[-1]} != {Hz}")
+    lead = tuple(zt.shape[:-1])
+    rows = zt.numel() // Hz
+    ln, _, _ = ops.layernorm_fwd(zt.view(rows, Hz), bp.f[f"{prefix}.ln_g"], bp.f[f"{prefix}.ln_b"], rows, Hz,
+                                 save_stats=False)
+    Y = torch.addmm(bp.h[f"{prefix}.b_proj"], ln, bp.h[f"{prefix}.w_proj"])     # [rows, Hz + 4P]
+    g = ops.gate_mul(Y[:, :Hz], act=1)
+    a = ops.gate_mul(Y[:, Hz:Hz + P], y=Y[:, Hz + P:Hz + 2 * P], act=1)
+    b = ops.gate_mul(Y[:, Hz + 2 * P:Hz + 3 * P], y=Y[:, Hz + 3 * P:], act=1)
+    return (_out(g.view(lead + (Hz,)), was_np), _out(a.view(lead + (P,)), was_np), _out(b.view(lead + (P,)), was_np))
+
+
+def _triangle_finish(g, t, p, prefix):
+    """evoformer.py:268-270: g * (LN2(t) @ W_o + b_o), g already activated."""
+    if prefix not in ("tri_out", "tri_in"):
+        raise DimensionError(f"unknown triangle module {prefix!r}")
+    gt, was_np = _to_dev(g)
+    tt, _ = _to_dev(t)
+    bp = _block_params(p, _infer_cfg(p), partial=True)
+    Hz, P = bp.cfg.h_pair, bp.cfg.hidden_proj
+    if gt.shape[-1] != Hz or tt.shape[-1] != P or gt.shape[:-1] != tt.shape[:-1]:
+        raise DimensionError(f"{prefix}: g {tuple(gt.shape)} / t {tuple(tt.shape)} do not match ({Hz}, {P})")
+    rows = tt.numel() // P
+    ln2, _, _ = ops.layernorm_fwd(tt.view(rows, P), bp.f[f"{prefix}.ln2_g"], bp.f[f"{prefix}.ln2_b"], rows, P,
+                                  save_stats=False)
+    y = torch.mm(ln2, bp.h[f"{prefix}.w_o"])
+    out = ops.gate_mul(gt.view(rows, Hz), y=y, bias=bp.f[f"{prefix}.b_o"], act=0)
+    return _out(out.view(gt.shape), was_np)
+
+
 def _triangle(z, p, cfg, mod):
     _check_pair(z, cfg)
     zt, was_np = _to_dev(z)
     bp = _block_params(p, cfg)
     R = cfg.n_res
     x2 = zt.view(R * R, cfg.h_pair)
-    # residual-free update: run the fused epilogue against a zero residual
+    # residual-free update: the fused epilogue's gate applied without the residual stream
     out, sv = _blk.triangle_fwd(bp, mod, x2, R, save=True)
-    upd = ops.gated_residual_fwd(torch.zeros_like(x2), sv["y2"], bp.f[f"{mod}.b_o"], R * R, cfg.h_pair,
-                                 gp=sv["Y"], gp_rs=cfg.h_pair + 4 * cfg.hidden_proj)
+    upd = ops.gate_mul(sv["Y"], y=sv["y2"], bias=bp.f[f"{mod}.b_o"], act=1, rows=R * R, cols=cfg.h_pair,
+                       gate_rs=cfg.h_pair + 4 * cfg.hidden_proj)
     return _out(upd.view(R, R, cfg.h_pair), was_np)
 
 
@@ -345,16 +551,27 @@ def tri_update_incoming(z, p, cfg: EvoConfig):
     return _triangle(z, p, cfg, "tri_in")
 
 
-def _infer_cfg(p) -> EvoConfig:
-    if isinstance(p, BlockParams):
-        return p.cfg
-    raise DimensionError("pass cfg= when calling transition() with a plain parameter dict")
+def check_supported(cfg: EvoConfig) -> None:
+    """the kernels' granularity (a DimensionError, never a launch failure): n_seq and n_res are
+    multiples of 8 (tcgen05 K-steps of the OPM / triangle contractions, 16-byte rows), head
+    dims multiples of 8 up to 64, hidden_proj in {8, 16, 32, 64}."""
+    bad = []
+    if cfg.n_seq % 8 or cfg.n_res % 8:
+        bad.append(f"n_seq={cfg.n_seq}, n_res={cfg.n_res} must be multiples of 8")
+    for name, c in (("c_msa", cfg.c_msa), ("c_pair", cfg.c_pair)):
+        if c % 8 or c > 64:
+            bad.append(f"{name}={c} must be a multiple of 8 and <= 64")
+    if cfg.hidden_proj not in (8, 16, 32, 64):
+        bad.append(f"hidden_proj={cfg.hidden_proj} must be 8, 16, 32 or 64")
+    if bad:
+        raise DimensionError("config below the B200 kernels' granularity: " + "; ".join(bad))
 
 
 def evoformer_block(m, z, p, cfg: EvoConfig):
     """evoformer.py:314-325: (m, z) -> (m', z'), nine residual sub-modules."""
     _check_msa(m, cfg)
     _check_pair(z, cfg)
+    check_supported(cfg)
     mt, was_np = _to_dev(m)
     zt, _ = _to_dev(z)
     bp = _block_params(p, cfg)
@@ -363,19 +580,26 @@ def evoformer_block(m, z, p, cfg: EvoConfig):
 
 
 # ----------------------------------------------------------------------------- training API
-def block_forward_backward(bp: BlockParams, m, z, gm, gz):
+def block_forward_backward(bp: BlockParams, m, z, gm, gz, return_masks=False):
     """one block forward + backward of loss = <m', gm> + <z', gz> (the gradient
     oracle's loss, oracle/evoformer_torch.block_grads).  numpy in, numpy out:
-    (m', z', dm, dz, dparams[reference keys])."""
+    (m', z', dm, dz, dparams[reference keys]) [+ the transitions' ReLU patterns
+    {"msa_trans": bool [S, R, 4H_m], "pair_trans": bool [R, R, 4H_z]} with return_masks]."""
     cfg = bp.cfg
     mt, _ = _to_dev(m)
     zt, _ = _to_dev(z)
     bp.zero_grad()
     mo, zo, saved = _blk.block_fwd(bp, mt, zt, save=True)
+    masks = None
+    if return_masks:
+        S, R = cfg.n_seq, cfg.n_res
+        masks = {"msa_trans": (saved[3]["hid"] > 0).view(S, R, -1).cpu().numpy(),
+                 "pair_trans": (saved[9]["hid"] > 0).view(R, R, -1).cpu().numpy()}
     dm, dz = _blk.block_bwd(bp, saved, _to_dev(gm)[0], _to_dev(gz)[0])
     torch.cuda.synchronize()
     f = lambda t: t.double().cpu().numpy()
-    return f(mo), f(zo), f(dm), f(dz), bp.grads_to_reference()
+    out = (f(mo), f(zo), f(dm), f(dz), bp.grads_to_reference())
+    return out + (masks,) if return_masks else out
 
 
 class EvoformerStack:
@@ -456,11 +680,16 @@ class GraphedStep:
 
 
 class EvoformerBlockFunction(torch.autograd.Function):
-    """autograd wrapper: (m, z, flat_params) -> (m', z'); backward fills flat_params.grad
-    through the packed-gradient buffer of the BlockParams."""
+    """autograd wrapper: (m, z, flat, bp) -> (m', z') with flat = bp.flat (the block's fp32 master
+    weights).  forward re-derives the bf16 tensor-core copy from flat (so an optimizer step on
+    flat between calls is always seen); backward returns d flat through the packed-gradient
+    buffer of the BlockParams."""
 
     @staticmethod
     def forward(ctx, m, z, flat, bp):
+        if flat is not bp.flat and flat.data_ptr() != bp.flat.data_ptr():
+            raise KernelError("EvoformerBlockFunction: flat must be bp.flat (the tensor the kernels read)")
+        bp.refresh()
         mo, zo, saved = _blk.block_fwd(bp, m.to(torch.bfloat16).contiguous(), z.to(torch.bfloat16).contiguous())
         ctx.bp, ctx.saved = bp, saved
         ctx.dtypes = (m.dtype, z.dtype)

@@ -173,7 +173,8 @@ class Strided:
 
 
 def attention_desc(q: Strided, k: Strided, v: Strided, g: Strided, og: Strided, orw: Strided, lse,
-                   B, L, H, c, scale, bias=None, bias_s=(0, 0, 0, 0), bias_off=0):
+                   B, L, H, c, scale, bias=None, bias_s=(0, 0, 0, 0), bias_off=0, flags=0):
+    """flags: EVO_ATTN_* kernel-selection hints (include/evo.h), 0 = automatic"""
     d = EvoAttnDesc()
     d.q, d.k, d.v, d.g = q.ptr(), k.ptr(), v.ptr(), g.ptr()
     d.q_sb, d.q_sl, d.k_sb, d.k_sl = q.sb, q.sl, k.sb, k.sl
@@ -185,6 +186,7 @@ def attention_desc(q: Strided, k: Strided, v: Strided, g: Strided, og: Strided, 
         d.o_raw, d.r_sb, d.r_sl = orw.ptr(), orw.sb, orw.sl
     d.lse = _p(lse)
     d.B, d.L, d.H, d.c, d.scale = B, L, H, c, float(scale)
+    d.flags = int(flags)
     return d
 
 
@@ -324,6 +326,24 @@ def bias_act_bwd(dh, h, rows, cols, dy=None, dbias=None, relu=True):
     call("evo_bias_act_bwd", _p(dh), _p(h), _p(dy), _p(dbias), rows, cols, 1 if relu else 0, _dt(dh),
          stream_handle())
     return dy
+
+
+def gate_mul(gate, y=None, bias=None, act=1, rows=None, cols=None, gate_rs=None, y_rs=None, out=None):
+    """out = act(gate) * (y + bias) over a [rows, cols] view (evo_gate_mul_fwd); gate or y may be None
+    (factor 1).  act: 0 identity, 1 sigmoid, 2 ReLU."""
+    ref = gate if gate is not None else y
+    _cuda(ref, y, bias)
+    rows = ref.shape[0] if rows is None else rows
+    cols = ref.shape[-1] if cols is None else cols
+    if out is None:
+        out = torch.empty(rows, cols, device=ref.device, dtype=ref.dtype)
+    for t in (gate, y):
+        if t is not None and t.dtype != out.dtype:
+            raise KernelError("gate_mul: gate / y / out must share a dtype")
+    call("evo_gate_mul_fwd", _p(gate), gate.stride(0) if gate_rs is None and gate is not None else (gate_rs or 0),
+         int(act), _p(y), y.stride(0) if y_rs is None and y is not None else (y_rs or 0), _p(bias), _p(out),
+         out.stride(0), _dt(out), rows, cols, stream_handle())
+    return out
 
 
 def colsum(x, out, rows=None, cols=None, ld=None):

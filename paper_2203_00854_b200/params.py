@@ -119,11 +119,15 @@ class BlockLayout:
         self.entries.append((name, tuple(shape)))
         self.maps[name] = refs
 
-    def pack(self, params) -> np.ndarray:
+    def pack(self, params, strict: bool = True) -> np.ndarray:
+        """reference-keyed dict -> packed flat vector; strict=False leaves the entries of
+        absent keys zero (a caller holding only one module's weights)."""
         flat = np.zeros(self.numel, dtype=np.float64)
         for name, shape in self.entries:
             view = np.zeros(shape)
             for key, idx in self.maps[name]:
+                if not strict and key not in params:
+                    continue
                 view[idx] = np.asarray(params[key], dtype=np.float64)
             o = self.offsets[name]
             flat[o:o + view.size] = view.reshape(-1)
@@ -147,12 +151,16 @@ class BlockParams:
     """Packed device parameters of one block (fp32 master, bf16 compute copy, fp32 grads)."""
 
     def __init__(self, params=None, cfg: EvoConfig | None = None, device="cuda", layout: BlockLayout | None = None,
-                 flat: torch.Tensor | None = None):
+                 flat: torch.Tensor | None = None, partial: bool = False):
+        """partial=True: params may hold a subset of the block's keys (the reference's module
+        functions only read their own prefix); absent entries are zero."""
         self.cfg = cfg
         self.layout = layout or BlockLayout(cfg)
         if flat is None:
-            check_params(params, cfg)
-            flat = torch.from_numpy(self.layout.pack(params)).to(device=device, dtype=torch.float32)
+            if not partial:
+                check_params(params, cfg)
+            flat = torch.from_numpy(self.layout.pack(params, strict=not partial)).to(device=device,
+                                                                                    dtype=torch.float32)
         self.flat = flat
         self.device = flat.device
         self.flat_h = torch.empty(self.layout.numel, device=self.device, dtype=torch.bfloat16)

@@ -26,11 +26,11 @@ for n in a.n:
             bias = torch.randn(H, L, L, device="cuda").bfloat16(); bs = (0, L * L, L, 1); boff = 0
         else:
             bias = qkv; bs = (L * ld, 1, 0, ld); boff = 3 * H * c
-        d = ops.attention_desc(S(qkv, ld, 0), S(qkv, ld, H * c), S(qkv, ld, 2 * H * c), S(gp, H * c), S(og, H * c),
-                               S(orw, H * c), lse, B, L, H, c, 1 / math.sqrt(c), bias=bias, bias_s=bs, bias_off=boff)
         res = {}
-        for kern, thr in (("ws", 1), ("flash", 1 << 30)):
-            lib.evo_attention_fwd_ws_min_len(thr)
+        for kern, fl_ in (("ws", _lib.EVO_ATTN_FORCE_WS), ("flash", _lib.EVO_ATTN_FORCE_FLASH)):
+            d = ops.attention_desc(S(qkv, ld, 0), S(qkv, ld, H * c), S(qkv, ld, 2 * H * c), S(gp, H * c),
+                                   S(og, H * c), S(orw, H * c), lse, B, L, H, c, 1 / math.sqrt(c), bias=bias,
+                                   bias_s=bs, bias_off=boff, flags=fl_)
             ops.attention_fwd(d)
             torch.cuda.synchronize()
             ref = og.clone() if kern == "ws" else None
@@ -48,6 +48,5 @@ for n in a.n:
         fl = 4 * B * H * L * L * c
         print(f"N_r={n:5d} {name:8s} ws {res['ws']:8.2f} ms ({fl/res['ws']/1e9:6.1f} TFLOP/s)   "
               f"flash {res['flash']:8.2f} ms ({fl/res['flash']/1e9:6.1f} TFLOP/s)   rel diff {diff:.2e}", flush=True)
-        lib.evo_attention_fwd_ws_min_len(512)
         del qkv, gp, og, orw, lse, bias
         torch.cuda.empty_cache()

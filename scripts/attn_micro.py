@@ -13,7 +13,7 @@ ap.add_argument("--bwd", type=int, default=1)
 ap.add_argument("--fb", type=int, default=1, help="forward: stage a full bias through smem (A/B switch)")
 a = ap.parse_args()
 from paper_2203_00854_b200 import _lib
-_lib.load().evo_attention_fwd_full_bias_smem(a.fb)
+FLAGS = 0 if a.fb else _lib.EVO_ATTN_NO_BIAS_SMEM
 # (name, B, L, H, c, kind, bias)
 V = [("msa_row", 128, 256, 8, 32, "row", "full"), ("msa_col", 256, 128, 8, 32, "col", None),
      ("pair_row", 256, 256, 4, 32, "row", "key"), ("pair_col", 256, 256, 4, 32, "col", "key")]
@@ -35,7 +35,8 @@ for name, B, L, H, c, kind, bmode in V:
     else:
         bias, bs, boff = None, (0, 0, 0, 0), 0
     d = ops.attention_desc(S(qkv, ld, 0), S(qkv, ld, H * c), S(qkv, ld, 2 * H * c), S(gp, H * c), S(og, H * c),
-                           S(orw, H * c), lse, B, L, H, c, 1 / math.sqrt(c), bias=bias, bias_s=bs, bias_off=boff)
+                           S(orw, H * c), lse, B, L, H, c, 1 / math.sqrt(c), bias=bias, bias_s=bs, bias_off=boff,
+                           flags=FLAGS)
     dout = torch.randn(rows, H * c, device="cuda").bfloat16()
     dqkv = torch.zeros_like(qkv); dgp = torch.empty_like(gp)
     if bmode == "full":

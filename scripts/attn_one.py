@@ -12,7 +12,6 @@ ap.add_argument("--kind", default="pair")
 ap.add_argument("--iters", type=int, default=3)
 a = ap.parse_args()
 lib = _lib.load()
-lib.evo_attention_fwd_ws_min_len(1 if a.ws else 1 << 30)
 L, c = a.n, 32
 B, H, bmode = ((a.batch or L), 4, "key") if a.kind == "pair" else ((a.batch or 128), 8, "full")
 ld = 3 * H * c + (8 if bmode == "key" else 0)
@@ -26,7 +25,8 @@ if bmode == "full":
 else:
     bias = qkv; bs = (L * ld, 1, 0, ld); boff = 3 * H * c
 d = ops.attention_desc(S(qkv, ld, 0), S(qkv, ld, H * c), S(qkv, ld, 2 * H * c), S(gp, H * c), S(og, H * c),
-                       S(orw, H * c), lse, B, L, H, c, 1 / math.sqrt(c), bias=bias, bias_s=bs, bias_off=boff)
+                       S(orw, H * c), lse, B, L, H, c, 1 / math.sqrt(c), bias=bias, bias_s=bs, bias_off=boff,
+                       flags=_lib.EVO_ATTN_FORCE_WS if a.ws else _lib.EVO_ATTN_FORCE_FLASH)
 for _ in range(a.iters):
     ops.attention_fwd(d)
 torch.cuda.synchronize()

@@ -88,7 +88,8 @@ def layernorm_rowdot_fwd(x, gamma, beta, w, rows, cols, out, out_hs, ln_out=None
 
 
 # ------------------------------------------------------------------ attention
-def attention_desc(q, k, v, g, og, orw, lse, B, L, H, c, scale, bias=None, bias_s=(0, 0, 0, 0), bias_off=0):
+def attention_desc(q, k, v, g, og, orw, lse, B, L, H, c, scale, bias=None, bias_s=(0, 0, 0, 0), bias_off=0,
+                   flags=0):
     return SimpleNamespace(q=q, k=k, v=v, g=g, og=og, orw=orw, lse=lse, B=B, L=L, H=H, c=c, scale=scale,
                            bias=bias, bias_s=tuple(bias_s), bias_off=bias_off)
 
@@ -227,7 +228,26 @@ def bias_act_bwd(dh, h, rows, cols, dy=None, dbias=None, relu=True):
     return dy
 
 
-NAMES = ["layernorm_fwd", "layernorm_bwd", "layernorm_rowdot_fwd", "attention_desc", "attention_fwd",
+def gate_mul(gate, y=None, bias=None, act=1, rows=None, cols=None, gate_rs=None, y_rs=None, out=None):
+    ref = gate if gate is not None else y
+    rows = ref.shape[0] if rows is None else rows
+    cols = ref.shape[-1] if cols is None else cols
+    f = torch.ones(rows, cols)
+    if y is not None:
+        f = _sv(y, 0, (rows, cols), (y.stride(0) if y_rs is None else y_rs, 1)).float()
+        if bias is not None:
+            f = f + bias.float()
+    if gate is not None:
+        gv = _sv(gate, 0, (rows, cols), (gate.stride(0) if gate_rs is None else gate_rs, 1)).float()
+        gv = torch.sigmoid(gv) if act == 1 else (torch.relu(gv) if act == 2 else gv)
+        f = gv * f
+    if out is None:
+        out = torch.empty(rows, cols, dtype=ref.dtype)
+    out.copy_(f)
+    return out
+
+
+NAMES = ["gate_mul", "layernorm_fwd", "layernorm_bwd", "layernorm_rowdot_fwd", "attention_desc", "attention_fwd",
          "attention_bwd_workspace", "attention_bwd", "bgemm", "tri_gate_fwd", "tri_gate_bwd",
          "gated_residual_fwd", "gated_residual_bwd", "bias_act_fwd", "bias_act_bwd"]
 

@@ -197,25 +197,17 @@ def _attn_ref(q, k, v, g, bias, scale):
     return torch.sigmoid(g) * o, o
 
 
-@pytest.fixture
-def ws_forward():
-    """force the warp-specialised long-sequence forward (attention_ws.cu) for every L"""
-    lib = _lib.load()
-    old = lib.evo_attention_fwd_ws_min_len(1)
-    yield
-    lib.evo_attention_fwd_ws_min_len(old)
-
-
 @pytest.mark.parametrize("L,c,H,mode", [(256, 32, 8, "full"), (128, 32, 8, "none"), (256, 32, 4, "key"),
                                         (100, 16, 2, "full"), (300, 64, 2, "key"), (40, 8, 4, "none"),
                                         (600, 32, 2, "key"), (1024, 32, 1, "full")])
-def test_attention_fwd_bwd_ws(L, c, H, mode, ws_forward):
-    test_attention_fwd_bwd(L, c, H, mode)
+def test_attention_fwd_bwd_ws(L, c, H, mode):
+    """the warp-specialised long-sequence forward (attention_ws.cu) forced at every L"""
+    test_attention_fwd_bwd(L, c, H, mode, flags=_lib.EVO_ATTN_FORCE_WS)
 
 
 @pytest.mark.parametrize("L,c,H,mode", [(256, 32, 8, "full"), (128, 32, 8, "none"), (256, 32, 4, "key"),
                                         (100, 16, 2, "full"), (300, 64, 2, "key"), (40, 8, 4, "none")])
-def test_attention_fwd_bwd(L, c, H, mode, B=3):
+def test_attention_fwd_bwd(L, c, H, mode, B=3, flags=0):
     gen = torch.Generator(device=DEV).manual_seed(L * c + H)
     ld = 3 * H * c + (8 if mode == "key" else 0)
     qkv = _mk((B, L, ld), gen)
@@ -239,7 +231,7 @@ def test_attention_fwd_bwd(L, c, H, mode, B=3):
                            Strided(qkv, L * ld, ld, 2 * H * c), Strided(gp, L * H * c, H * c),
                            Strided(og, L * H * c, H * c), Strided(orw, L * H * c, H * c), lse,
                            B, L, H, c, scale, bias=bias_t, bias_s=bias_s,
-                           bias_off=3 * H * c if mode == "key" else 0)
+                           bias_off=3 * H * c if mode == "key" else 0, flags=flags)
     ops.attention_fwd(d)
     torch.cuda.synchronize()
     split = lambda t, i: t[..., i * H * c:(i + 1) * H * c].float().reshape(B, L, H, c).permute(0, 2, 1, 3)
@@ -291,32 +283,26 @@ def test_attention_persistent_units(mode, H):
     test_attention_fwd_bwd(256, 32, H, mode, B=160)
 
 
-def test_attention_fwd_full_bias_smem_switch():
+def test_attention_fwd_full_bias_smem_flag():
     """the smem-staged full-bias forward (msa_row) equals the global-load variant bitwise"""
-    lib = _lib.load()
     gen = torch.Generator(device=DEV).manual_seed(5)
     B, L, H, c = 40, 256, 8, 32
     qkv = _mk((B, L, 3 * H * c), gen)
     gp = _mk((B, L, H * c), gen)
     bias = _mk((H, L, L), gen)
     outs = []
-    old = lib.evo_attention_fwd_full_bias_smem(-1)
-    try:
-        for fb in (1, 0):
-            lib.evo_attention_fwd_full_bias_smem(fb)
-            og = torch.empty(B, L, H * c, device=DEV, dtype=torch.bfloat16)
-            orw = torch.empty_like(og)
-            lse = torch.empty(B, H, L, device=DEV)
-            ld = 3 * H * c
-            d = ops.attention_desc(Strided(qkv, L * ld, ld, 0), Strided(qkv, L * ld, ld, H * c),
-                                   Strided(qkv, L * ld, ld, 2 * H * c), Strided(gp, L * H * c, H * c),
-                                   Strided(og, L * H * c, H * c), Strided(orw, L * H * c, H * c), lse,
-                                   B, L, H, c, 1 / math.sqrt(c), bias=bias, bias_s=(0, L * L, L, 1))
-            ops.attention_fwd(d)
-            torch.cuda.synchronize()
-            outs.append((og, orw, lse))
-    finally:
-        lib.evo_attention_fwd_full_bias_smem(old)
+    for flags in (0, _lib.EVO_ATTN_NO_BIAS_SMEM):
+        og = torch.empty(B, L, H * c, device=DEV, dtype=torch.bfloat16)
+        orw = torch.empty_like(og)
+        lse = torch.empty(B, H, L, device=DEV)
+        ld = 3 * H * c
+        d = ops.attention_desc(Strided(qkv, L * ld, ld, 0), Strided(qkv, L * ld, ld, H * c),
+                               Strided(qkv, L * ld, ld, 2 * H * c), Strided(gp, L * H * c, H * c),
+                               Strided(og, L * H * c, H * c), Strided(orw, L * H * c, H * c), lse,
+                               B, L, H, c, 1 / math.sqrt(c), bias=bias, bias_s=(0, L * L, L, 1), flags=flags)
+        ops.attention_fwd(d)
+        torch.cuda.synchronize()
+        outs.append((og, orw, lse))
     for a, b in zip(*outs):
         assert torch.equal(a, b)
 

@@ -17,12 +17,12 @@ from paper_2203_00854_b200.config import EvoConfig, init_block_params, synthetic
 from paper_2203_00854_b200.params import BlockParams  # noqa: E402
 
 CFG = EvoConfig(16, 32, 64, 32, 2, 1, 16)
-# Gradient tolerance (relative Frobenius per tensor).  bf16 storage of activations
-# and weights flips the ReLU mask of the transitions for pre-activations within
-# rounding distance of 0; each flip is an O(1) change of that unit's gradient, so
-# a fraction f of flips gives ~sqrt(f) relative error (measured 2-4.6% on the
-# transitions, <1.5% everywhere else).  Forward outputs keep the 2e-2 bound.
-GRAD_TOL = 5e-2
+# Gradient tolerance (relative Frobenius per tensor), SURVEY.md 8c.  The transitions are
+# compared against the MASK-MATCHED oracle (the GPU's own ReLU pattern, see
+# oracle/evoformer_torch.block_grads): bf16 rounding otherwise flips units whose
+# pre-activation lies within rounding distance of 0, an O(1) change each (~sqrt(fraction)
+# relative error, 2-4.6 % measured) that would hide a kernel error of that size.
+GRAD_TOL = 2e-2
 
 
 def rel(a, b):
@@ -99,13 +99,16 @@ def test_submodule_backward(mod):
             errs = {"dx": rel(dm.double().cpu().view(x.shape), ref_dx)}
         else:
             g = rng.normal(size=x.shape)
-            ref_dx, ref_p = _ref_grads(fn, x, p, g, keys)
             x2 = dev(x).view(-1, x.shape[-1])
+            if mod in ("msa_trans", "pair_trans"):   # mask-matched: the GPU's ReLU pattern
+                out, sv = B.transition_fwd(bp, mod, x2, x2.shape[0])
+                mask = torch.tensor((sv["hid"] > 0).view(x.shape[:-1] + (-1,)).cpu().numpy())
+                fn = (lambda xx, q, mod=mod, mask=mask: T.transition(xx, q, mod, mask))
+            ref_dx, ref_p = _ref_grads(fn, x, p, g, keys)
             if mod == "msa_col":
                 out, sv = B.attention_fwd(bp, "msa_col", x2, R, S, "col")
                 dx, _ = B.attention_bwd(bp, sv, dev(g).view(S * R, -1))
             elif mod in ("msa_trans", "pair_trans"):
-                out, sv = B.transition_fwd(bp, mod, x2, x2.shape[0])
                 dx = B.transition_bwd(bp, sv, dev(g).view(x2.shape))
             elif mod in ("tri_out", "tri_in"):
                 out, sv = B.triangle_fwd(bp, mod, x2, R)
