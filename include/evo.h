@@ -203,9 +203,11 @@ int evo_bgemm_ws(const EvoMat* A, const EvoMat* B, const EvoMat* C,
  * written CHANNEL-MAJOR (a_cm[h*rows + r]) so that the einsum is a plain batched
  * GEMM over h.  The g gate stays in Y (sigmoid applied by evo_gated_residual_fwd). */
 int evo_tri_gate_fwd(const void* y, int64_t rows, int hz, int p, void* a_cm, void* b_cm, void* stream);
-/* dY[:, hz:] from da_cm, db_cm (channel-major fp32 or bf16); writes bf16 dY row-major */
+/* dY[:, hz:] from da_cm, db_cm (channel-major fp32 or bf16); writes bf16 dY row-major;
+ * dsum (fp32 [4p], may be NULL): += column sums of dY[:, hz:] in fp32 (the bias gradient of
+ * the a/b projections, before the bf16 rounding of dY) */
 int evo_tri_gate_bwd(const void* y, const void* da_cm, const void* db_cm, int d_dtype,
-                     int64_t rows, int hz, int p, void* dy, void* stream);
+                     int64_t rows, int hz, int p, void* dy, float* dsum, void* stream);
 
 /* ------------------------------------------------------------------ residual epilogues
  * out = res + gate(gp) * (y + bias), gate(gp) = sigmoid(gp) or 1 when gp == NULL.
@@ -215,10 +217,11 @@ int evo_tri_gate_bwd(const void* y, const void* da_cm, const void* db_cm, int d_
 int evo_gated_residual_fwd(const void* res, const void* y, int64_t y_rs, const float* bias,
                            const void* gp, int64_t gp_rs, void* out, int dtype,
                            int64_t rows, int64_t cols, void* stream);
-/* dy = dout * gate, dgp = dout * (y+bias) * gate*(1-gate) (if gp), dbias += sum_r dy (fp32). */
+/* dy = dout * gate, dgp = dout * (y+bias) * gate*(1-gate) (if gp), dbias += sum_r dy (fp32),
+ * dgp_sum += sum_r dgp (fp32, may be NULL: the gate projection's bias gradient). */
 int evo_gated_residual_bwd(const void* dout, const void* y, int64_t y_rs, const float* bias,
                            const void* gp, int64_t gp_rs, void* dy, void* dgp, int64_t dgp_rs,
-                           float* dbias, int dtype, int64_t rows, int64_t cols, void* stream);
+                           float* dbias, float* dgp_sum, int dtype, int64_t rows, int64_t cols, void* stream);
 
 /* out[r*out_rs + c] = act(gate[r*gate_rs + c]) * (y[r*y_rs + c] + bias[c]); act 0 = identity,
  * 1 = sigmoid, 2 = ReLU; gate NULL -> 1, y NULL -> (y + bias) = 1, bias may be NULL.

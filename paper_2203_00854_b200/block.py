@@ -451,8 +451,10 @@ def triangle_bwd(bp: BlockParams, sv: Saved, dz_new, reduce_scatter=None, next_d
     ld = Hz + 4 * P
     dY = torch.empty(rows, ld, device=dev, dtype=BF16)
     dy2 = torch.empty(rows, Hz, device=dev, dtype=BF16)
+    # the merged projection's bias gradient comes out of the two epilogues in fp32 (before
+    # dY is rounded to bf16): g part here, a/b part in tri_gate_bwd
     ops.gated_residual_bwd(dz_new, rows, Hz, y=sv["y2"], bias=f[f"{mod}.b_o"], gp=sv["Y"], gp_rs=ld, dy=dy2,
-                           dgp=dY, dgp_rs=ld, dbias=g[f"{mod}.b_o"])
+                           dgp=dY, dgp_rs=ld, dbias=g[f"{mod}.b_o"], dgp_sum=g[f"{mod}.b_proj"][:Hz])
     _wgrad(sv["ln2"], dy2, g[f"{mod}.w_o"])
     dln2 = _mm(dy2, h[f"{mod}.w_o"].t())                              # [rows, P]
     dt_cm = torch.empty(P, rows, device=dev, dtype=BF16)
@@ -493,9 +495,8 @@ def triangle_bwd(bp: BlockParams, sv: Saved, dz_new, reduce_scatter=None, next_d
             da_cm.copy_(reduce_scatter(daf).view(P, rows))
             Aa = Mat(sv["afull"], lo=(Rl, 1), split=(0, Rl), hi=(0, P * R * Rl), batch_stride=R * Rl)
         ops.bgemm(Aa, dTt, Mat(db_cm, lo=(Rl, 1), batch_stride=rows), P, R, N, M)
-    ops.tri_gate_bwd(sv["Y"], da_cm, db_cm, rows, Hz, P, dY)
+    ops.tri_gate_bwd(sv["Y"], da_cm, db_cm, rows, Hz, P, dY, dsum=g[f"{mod}.b_proj"][Hz:])
     _wgrad(sv["ln"], dY, g[f"{mod}.w_proj"])
-    _bgrad(dY, g[f"{mod}.b_proj"])
     dln = _mm(dY, h[f"{mod}.w_proj"].t())
     dz = torch.empty_like(dz_new)
     ops.layernorm_bwd(dln, sv["z"], f[f"{mod}.ln_g"], sv["mean"], sv["rstd"], rows, Hz, dx=dz, res=dz_new,

@@ -44,64 +44,55 @@ struct AttnBwdParams {
 };
 
 // dbias[h][q][k] += scale * sum_b dS[b][h][k][q]   (batch-shared bias: msa_row, evoformer.py:214).
-// CTA = 8 warps x 32 lanes over 32 consecutive 16-byte vectors (256 elements): warp w sums the
-// batches b = w, w + 8, ... (U loads in flight per lane), then the 8 partial sums meet in smem
-// in a fixed order (deterministic).  H*L*L/8 * 8 threads keep enough bytes in flight to stream
-// the B x H x L x L workspace at HBM speed.
+// CTA = one (head, 32-key, 32-query) tile; 256 threads = 2 batch slices x 32 keys x 4 16-byte query
+// vectors, each thread keeping U loads of its slice's batches in flight (each warp reads 8 key rows
+// x 64 contiguous bytes).  The two slices meet in smem in a fixed order (deterministic, no
+// atomics) and the tile leaves transposed: a warp writes 32 consecutive keys of one query
+// (coalesced; the dS^T workspace is key-major because the backward's threads own keys).
 __global__ void __launch_bounds__(256) attn_dbias_reduce(const bf16* __restrict__ dS, float* __restrict__ dbias,
                                                          int64_t B, int H, int L, int64_t d1, int64_t d2, int64_t d3,
                                                          float scale) {
-  constexpr int U = 4, NW = 8;
-  __shared__ float part[NW][8][33];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int U = 8;
+  __shared__ float part[2][32][33];
+  const int h = blockIdx.z, k0 = blockIdx.y * 32, q0 = blockIdx.x * 32;
+  const int t = threadIdx.x, slice = t >> 7, key = (t >> 2) & 31, qv = t & 3;
   const int64_t per = (int64_t)H * L * L;
-  const int64_t nv = per / 8;
-  for (int64_t v0 = (int64_t)blockIdx.x * 32; v0 < nv; v0 += (int64_t)gridDim.x * 32) {
-    const int64_t i = v0 + lane;
-    const bool ok = i < nv;
-    const bf16* src = dS + (ok ? i * 8 : 0);
-    float acc[8];
+  float acc[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) acc[k] = 0.f;
-    int64_t b = warp;
-    for (; b + (U - 1) * NW < B; b += U * NW) {
+  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+  if (k0 + key < L && q0 + qv * 8 < L) {  // L % 8 == 0 (host-checked): whole vectors
+    const bf16* src = dS + ((int64_t)h * L + k0 + key) * L + q0 + qv * 8;
+    int64_t b = slice;
+    for (; b + 2 * (U - 1) < B; b += 2 * U) {
       uint4 u[U];
 #pragma unroll
-      for (int t = 0; t < U; ++t) u[t] = __ldcs(reinterpret_cast<const uint4*>(src + (b + t * NW) * per));
+      for (int i = 0; i < U; ++i) u[i] = __ldcs(reinterpret_cast<const uint4*>(src + (b + 2 * i) * per));
 #pragma unroll
-      for (int t = 0; t < U; ++t) {
+      for (int i = 0; i < U; ++i) {
         float v[8];
-        unpack_bf16x2(u[t].x, v[0], v[1]); unpack_bf16x2(u[t].y, v[2], v[3]);
-        unpack_bf16x2(u[t].z, v[4], v[5]); unpack_bf16x2(u[t].w, v[6], v[7]);
+        unpack_bf16x2(u[i].x, v[0], v[1]); unpack_bf16x2(u[i].y, v[2], v[3]);
+        unpack_bf16x2(u[i].z, v[4], v[5]); unpack_bf16x2(u[i].w, v[6], v[7]);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) acc[k] += v[k];
+        for (int e = 0; e < 8; ++e) acc[e] += v[e];
       }
     }
-    for (; b < B; b += NW) {
+    for (; b < B; b += 2) {
       const uint4 u = __ldcs(reinterpret_cast<const uint4*>(src + b * per));
       float v[8];
       unpack_bf16x2(u.x, v[0], v[1]); unpack_bf16x2(u.y, v[2], v[3]);
       unpack_bf16x2(u.z, v[4], v[5]); unpack_bf16x2(u.w, v[6], v[7]);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) acc[k] += v[k];
+      for (int e = 0; e < 8; ++e) acc[e] += v[e];
     }
+  }
 #pragma unroll
-    for (int k = 0; k < 8; ++k) part[warp][k][lane] = acc[k];
-    __syncthreads();
-    // 256 threads = 32 vectors x 8 elements: thread (lane', k) sums element k of vector lane'
-    {
-      const int vl = threadIdx.x >> 3, k = threadIdx.x & 7;
-      const int64_t iv = v0 + vl;
-      if (iv < nv) {
-        float t = 0.f;
+  for (int e = 0; e < 8; ++e) part[slice][key][qv * 8 + e] = acc[e];
+  __syncthreads();
 #pragma unroll
-        for (int w = 0; w < NW; ++w) t += part[w][k][vl];
-        const uint32_t eu = (uint32_t)(iv * 8 + k), LL = (uint32_t)L * (uint32_t)L;  // H*L*L < 2^31 (host-checked)
-        const int64_t h = eu / LL, kk = (eu / (uint32_t)L) % (uint32_t)L, q = eu % (uint32_t)L;
-        dbias[h * d1 + q * d2 + kk * d3] += scale * t;
-      }
-    }
-    __syncthreads();
+  for (int i = 0; i < 4; ++i) {
+    const int q = (t >> 5) + 8 * i, k = t & 31;
+    if (q0 + q < L && k0 + k < L)
+      dbias[h * d1 + (int64_t)(q0 + q) * d2 + (int64_t)(k0 + k) * d3] += scale * (part[0][k][q] + part[1][k][q]);
   }
 }
 
@@ -394,6 +385,8 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
   constexpr uint32_t LBO_ROWS = (128 / 8) * 128;               // 2048: next 8-k group of a 128-row K-major tile
 
   int it = 0;
+  bf16 kb_next = f2bf(0.f);  // per-key bias of the next unit (MODE 1)
+  bool first_unit = true;
   for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
     int64_t b;
     int h, kt;
@@ -405,7 +398,11 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
 #pragma unroll
     for (int d = 0; d < CP; ++d) acc[d] = 0.f;
     float kbias = 0.f;
-    if (per_key_bias && kvalid) kbias = bf2f(F.bias[b * F.bs0 + (int64_t)h * F.bs1 + (int64_t)kj * F.bs3]);
+    if constexpr (per_key_bias) {
+      if (first_unit) kb_next = kvalid ? F.bias[b * F.bs0 + (int64_t)h * F.bs1 + (int64_t)kj * F.bs3] : f2bf(0.f);
+      kbias = bf2f(kb_next);  // loaded with this unit's prefetch, under the previous unit's drain
+      first_unit = false;
+    }
     const bf16* bias_col = nullptr;  // full bias: element (q, kj) at bias_col[q * bs2]
     if ((MODE == 2 || MODE == 3) && kvalid) bias_col = F.bias + b * F.bs0 + (int64_t)h * F.bs1 + (int64_t)kj * F.bs3;
     float* dbias_col = nullptr;
@@ -569,6 +566,30 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
 #endif
         mma_commit(&bar2);
       }
+      if constexpr (db_store) {
+        // dS^T tile (unscaled bf16, canonical K-major [key][query]) -> workspace [b][h][key][query],
+        // under the dV/dK/dQ MMAs (which only read the tile): all 8 smem reads of a thread first,
+        // then its 8 16-byte stores (no register-reuse serialisation between load and store).
+        // lane = (query group % 4, key % 8): each smem phase reads 128 contiguous bytes and each key
+        // row gets 64 contiguous bytes per store (requires L % 8 == 0)
+        bf16* wsb = P.dS + ((b * H + h) * (int64_t)L + k0) * L + q0;
+        constexpr int NCP = (BW_BK * BW_BQ / 8) / 256;
+        uint4 cv[NCP];
+#pragma unroll
+        for (int i = 0; i < NCP; ++i) {
+          const int ch = threadIdx.x + i * 256;
+          const int r = ((ch >> 5) & 15) * 8 + (ch & 7);
+          const int g = (ch >> 9) * 4 + ((ch >> 3) & 3);
+          cv[i] = *reinterpret_cast<const uint4*>(smem + SM::DST + (g * (BW_BK / 8) + (r >> 3)) * 128 + (r & 7) * 16);
+        }
+#pragma unroll
+        for (int i = 0; i < NCP; ++i) {
+          const int ch = threadIdx.x + i * 256;
+          const int r = ((ch >> 5) & 15) * 8 + (ch & 7);
+          const int g = (ch >> 9) * 4 + ((ch >> 3) & 3);
+          if (k0 + r < L && q0 + g * 8 < L) *reinterpret_cast<uint4*>(wsb + (int64_t)r * L + g * 8) = cv[i];
+        }
+      }
       mbar_wait(&bar2, it & 1);
       tc_fence_after();
       // the tiles are free: prefetch the next (batch, query tile) while draining TMEM
@@ -580,22 +601,9 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
         int nh, nkt_;
         decode(u + gridDim.x, nb, nh, nkt_);
         issue_loads(nb, nh, nkt_ * BW_BK, 0, true, DB ? (buf ^ 1) : 0);
-      }
-      if constexpr (db_store) {
-        // dS^T tile (unscaled bf16, canonical K-major [key][query]) -> workspace [b][h][key][query]:
-        // lane = (query group % 4, key % 8) so each smem phase reads 128 contiguous bytes and
-        // each key row gets 64 contiguous bytes per store (requires L % 8 == 0)
-        bf16* wsb = P.dS + ((b * H + h) * (int64_t)L + k0) * L + q0;
-#pragma unroll
-        for (int i = 0; i < (BW_BK * BW_BQ / 8) / 256; ++i) {
-          const int ch = threadIdx.x + i * 256;
-          const int r = ((ch >> 5) & 15) * 8 + (ch & 7);
-          const int g = (ch >> 9) * 4 + ((ch >> 3) & 3);
-          if (k0 + r < L && q0 + g * 8 < L) {
-            const uint4 v = *reinterpret_cast<const uint4*>(smem + SM::DST + (g * (BW_BK / 8) + (r >> 3)) * 128 +
-                                                            (r & 7) * 16);
-            *reinterpret_cast<uint4*>(wsb + (int64_t)r * L + g * 8) = v;
-          }
+        if constexpr (per_key_bias) {
+          const int nkj = nkt_ * BW_BK + kr;
+          kb_next = nkj < L ? F.bias[nb * F.bs0 + (int64_t)nh * F.bs1 + (int64_t)nkj * F.bs3] : f2bf(0.f);
         }
       }
 #if EVO_EXP != 3
@@ -852,10 +860,8 @@ extern "C" int evo_gated_attention_bwd(const EvoAttnBwdDesc* d, void* stream) {
   else rc = launch_bwd<64>(p, B, dq_partial, st);
   if (rc) return rc;
   if (p.dS) {
-    int64_t nv = (int64_t)H * L * L / 8;
-    int64_t g2 = (nv + 31) / 32, cap2 = (int64_t)sm_count() * 8;
-    unsigned g2u = (unsigned)(g2 < cap2 ? g2 : cap2);
-    attn_dbias_reduce<<<g2u, 256, 0, st>>>(p.dS, p.dbias, B, H, L, p.db1, p.db2, p.db3, p.scale);
+    const dim3 g2((unsigned)((L + 31) / 32), (unsigned)((L + 31) / 32), (unsigned)H);
+    attn_dbias_reduce<<<g2, 256, 0, st>>>(p.dS, p.dbias, B, H, L, p.db1, p.db2, p.db3, p.scale);
     EVO_LAUNCH_CHECK("attention bwd dbias reduce");
   }
   if (dq_partial == 2) return EVO_OK;

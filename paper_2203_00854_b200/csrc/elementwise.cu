@@ -109,10 +109,12 @@ __global__ void __launch_bounds__(256) gated_residual_bwd_k(const T* __restrict_
                                                             int64_t y_rs, const float* __restrict__ bias,
                                                             const T* __restrict__ gp, int64_t gp_rs, T* __restrict__ dy,
                                                             T* __restrict__ dgp, int64_t dgp_rs,
-                                                            float* __restrict__ dbias, int64_t rows, int64_t cols) {
+                                                            float* __restrict__ dbias, float* __restrict__ dgp_sum,
+                                                            int64_t rows, int64_t cols) {
   extern __shared__ float red[];
   const ColTile t(rows, cols);
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  float acc_g[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // fp32 column sums of dgp (its bias gradient, pre-rounding)
   if (t.active()) {
     const int64_t c = t.tc * 8;
     float b[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -146,6 +148,7 @@ __global__ void __launch_bounds__(256) gated_residual_bwd_k(const T* __restrict_
             float s = sigmoidf_(gv[u][e]);
             dg[e] = d[u][e] * (yv[u][e] + b[e]) * s * (1.f - s);
             d[u][e] *= s;
+            acc_g[e] += dg[e];
           }
           st8<T>(dgp + ru * dgp_rs + c, dg);
         }
@@ -156,6 +159,10 @@ __global__ void __launch_bounds__(256) gated_residual_bwd_k(const T* __restrict_
     }
   }
   if (dbias) col_flush(red, t, acc, cols, dbias);
+  if (dgp_sum) {
+    if (dbias) __syncthreads();  // red reused
+    col_flush(red, t, acc_g, cols, dgp_sum);
+  }
 }
 
 template <typename T>
@@ -292,9 +299,11 @@ __global__ void __launch_bounds__(256) tri_gate_fwd_k(const bf16* __restrict__ y
 template <int P, typename TD>
 __global__ void __launch_bounds__(256) tri_gate_bwd_k(const bf16* __restrict__ y, const TD* __restrict__ da,
                                                       const TD* __restrict__ db, int64_t rows, int hz,
-                                                      bf16* __restrict__ dy) {
+                                                      bf16* __restrict__ dy, float* __restrict__ dsum) {
   constexpr int W = 4 * P;
   __shared__ float gs[64][2 * P + 1];
+  __shared__ float cs[256 / (W / 8 < 256 ? W / 8 : 256)][W + 1];  // per row-group column partials
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};                         // fp32 sums of dY[:, hz:] (its bias grad)
   const int64_t r0 = (int64_t)blockIdx.x * 64;
   const int64_t ld = hz + W;
   for (int i = threadIdx.x; i < 2 * P * 64; i += blockDim.x) {
@@ -322,8 +331,21 @@ __global__ void __launch_bounds__(256) tri_gate_bwd_k(const bf16* __restrict__ y
       const float sg = sigmoidf_(s);
       const float g = gs[r][which * P + h];
       o[e] = cc < P ? g * l * sg * (1.f - sg) : g * sg;
+      acc[e] += o[e];
     }
     st8<bf16>(dy + (r0 + r) * ld + hz + c, o);
+  }
+  if (dsum) {  // the thread's column chunk is fixed (256 % (W/8) == 0): one smem pass, one atomic per column
+    constexpr int CPR = W / 8, RG = 256 / CPR;
+    const int rg = threadIdx.x / CPR, c = (threadIdx.x % CPR) * 8;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) cs[rg][c + e] = acc[e];
+    __syncthreads();
+    for (int col = threadIdx.x; col < W; col += blockDim.x) {
+      float sum = 0.f;
+      for (int g2 = 0; g2 < RG; ++g2) sum += cs[g2][col];
+      atomicAdd(dsum + col, sum);
+    }
   }
 }
 
@@ -490,10 +512,11 @@ static int col_grid(int64_t rows, int64_t cols, dim3& grid, size_t& smem) {
 }
 
 extern "C" int evo_gated_residual_bwd(const void* dout, const void* y, int64_t y_rs, const float* bias, const void* gp,
-                                      int64_t gp_rs, void* dy, void* dgp, int64_t dgp_rs, float* dbias, int dtype,
-                                      int64_t rows, int64_t cols, void* stream) {
+                                      int64_t gp_rs, void* dy, void* dgp, int64_t dgp_rs, float* dbias,
+                                      float* dgp_sum, int dtype, int64_t rows, int64_t cols, void* stream) {
   EVO_CHECK_ARG(dout, EVO_ERR_ARG, "gated_residual bwd: null dout");
   EVO_CHECK_ARG(!gp || (y && dgp), EVO_ERR_ARG, "gated_residual bwd: gp needs y and dgp");
+  EVO_CHECK_ARG(!dgp_sum || gp, EVO_ERR_ARG, "gated_residual bwd: dgp_sum needs gp");
   if (rows == 0) return EVO_OK;
   cudaStream_t st = (cudaStream_t)stream;
   dim3 grid;
@@ -503,11 +526,11 @@ extern "C" int evo_gated_residual_bwd(const void* dout, const void* y, int64_t y
   if (dtype == EVO_BF16)
     gated_residual_bwd_k<bf16><<<grid, 256, smem, st>>>((const bf16*)dout, (const bf16*)y, y_rs, bias,
                                                         (const bf16*)gp, gp_rs, (bf16*)dy, (bf16*)dgp, dgp_rs, dbias,
-                                                        rows, cols);
+                                                        dgp_sum, rows, cols);
   else
     gated_residual_bwd_k<float><<<grid, 256, smem, st>>>((const float*)dout, (const float*)y, y_rs, bias,
                                                          (const float*)gp, gp_rs, (float*)dy, (float*)dgp, dgp_rs,
-                                                         dbias, rows, cols);
+                                                         dbias, dgp_sum, rows, cols);
   EVO_LAUNCH_CHECK("gated_residual bwd");
   return EVO_OK;
 }
@@ -588,7 +611,7 @@ extern "C" int evo_tri_gate_fwd(const void* y, int64_t rows, int hz, int p, void
 }
 
 extern "C" int evo_tri_gate_bwd(const void* y, const void* da_cm, const void* db_cm, int d_dtype, int64_t rows, int hz,
-                                int p, void* dy, void* stream) {
+                                int p, void* dy, float* dsum, void* stream) {
   EVO_CHECK_ARG(y && da_cm && db_cm && dy, EVO_ERR_ARG, "tri_gate bwd: null pointer");
   EVO_CHECK_ARG(hz % 8 == 0 && al16(y) && al16(dy), EVO_ERR_ALIGN, "tri_gate bwd: alignment");
   if (rows == 0) return EVO_OK;
@@ -597,9 +620,9 @@ extern "C" int evo_tri_gate_bwd(const void* y, const void* da_cm, const void* db
 #define TGB(PP)                                                                                                  \
   (d_dtype == EVO_BF16                                                                                           \
        ? tri_gate_bwd_k<PP, bf16><<<g, 256, 0, st>>>((const bf16*)y, (const bf16*)da_cm, (const bf16*)db_cm, rows, \
-                                                     hz, (bf16*)dy)                                              \
+                                                     hz, (bf16*)dy, dsum)                                        \
        : tri_gate_bwd_k<PP, float><<<g, 256, 0, st>>>((const bf16*)y, (const float*)da_cm, (const float*)db_cm,    \
-                                                      rows, hz, (bf16*)dy))
+                                                      rows, hz, (bf16*)dy, dsum))
   switch (p) {
     case 2: TGB(2); break;
     case 4: TGB(4); break;

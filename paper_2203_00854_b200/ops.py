@@ -281,8 +281,9 @@ def tri_gate_fwd(y, rows, hz, p, a_cm, b_cm):
     call("evo_tri_gate_fwd", _p(y), rows, hz, p, _p(a_cm), _p(b_cm), stream_handle())
 
 
-def tri_gate_bwd(y, da_cm, db_cm, rows, hz, p, dy):
-    call("evo_tri_gate_bwd", _p(y), _p(da_cm), _p(db_cm), _dt(da_cm), rows, hz, p, _p(dy), stream_handle())
+def tri_gate_bwd(y, da_cm, db_cm, rows, hz, p, dy, dsum=None):
+    """dsum (fp32 [4p]): += fp32 column sums of dY[:, hz:] (the a/b projection bias gradient)"""
+    call("evo_tri_gate_bwd", _p(y), _p(da_cm), _p(db_cm), _dt(da_cm), rows, hz, p, _p(dy), _p(dsum), stream_handle())
 
 
 def gated_residual_fwd(res, y, bias, rows, cols, y_rs=None, gp=None, gp_rs=0, out=None):
@@ -310,9 +311,10 @@ def residual_layernorm_fwd(res, y, bias, rows, cols, gamma, beta, y_rs=None, gp=
 
 
 def gated_residual_bwd(dout, rows, cols, y=None, y_rs=None, bias=None, gp=None, gp_rs=0, dy=None, dgp=None,
-                       dgp_rs=0, dbias=None):
+                       dgp_rs=0, dbias=None, dgp_sum=None):
+    """dgp_sum (fp32 [cols]): += fp32 column sums of dgp (the gate projection's bias gradient)"""
     call("evo_gated_residual_bwd", _p(dout), _p(y), cols if y_rs is None else y_rs, _p(bias), _p(gp), gp_rs,
-         _p(dy), _p(dgp), dgp_rs, _p(dbias), _dt(dout), rows, cols, stream_handle())
+         _p(dy), _p(dgp), dgp_rs, _p(dbias), _p(dgp_sum), _dt(dout), rows, cols, stream_handle())
 
 
 def bias_act_fwd(y, bias, rows, cols, relu=True):

@@ -175,7 +175,7 @@ def tri_gate_fwd(y, rows, hz, p, a_cm, b_cm):
     b_cm.view(p, rows).copy_(b.t())
 
 
-def tri_gate_bwd(y, da_cm, db_cm, rows, hz, p, dy):
+def tri_gate_bwd(y, da_cm, db_cm, rows, hz, p, dy, dsum=None):
     yv = y.float()
     da, db = da_cm.reshape(p, rows).float().t(), db_cm.reshape(p, rows).float().t()
     for j, dd in ((0, da), (1, db)):
@@ -184,6 +184,9 @@ def tri_gate_bwd(y, da_cm, db_cm, rows, hz, p, dy):
         sg = torch.sigmoid(s)
         dy[:, hz + 2 * j * p:hz + (2 * j + 1) * p] = dd * lin * sg * (1 - sg)
         dy[:, hz + (2 * j + 1) * p:hz + (2 * j + 2) * p] = dd * sg
+        if dsum is not None:
+            dsum[2 * j * p:(2 * j + 1) * p] += (dd * lin * sg * (1 - sg)).sum(0)
+            dsum[(2 * j + 1) * p:(2 * j + 2) * p] += (dd * sg).sum(0)
 
 
 def gated_residual_fwd(res, y, bias, rows, cols, y_rs=None, gp=None, gp_rs=0, out=None):
@@ -198,13 +201,16 @@ def gated_residual_fwd(res, y, bias, rows, cols, y_rs=None, gp=None, gp_rs=0, ou
 
 
 def gated_residual_bwd(dout, rows, cols, y=None, y_rs=None, bias=None, gp=None, gp_rs=0, dy=None, dgp=None,
-                       dgp_rs=0, dbias=None):
+                       dgp_rs=0, dbias=None, dgp_sum=None):
     d = dout.reshape(rows, cols).float()
     if gp is not None:
         y_rs = cols if y_rs is None else y_rs
         yv = _sv(y, 0, (rows, cols), (y_rs, 1)).float() + (bias if bias is not None else 0)
         s = torch.sigmoid(_sv(gp, 0, (rows, cols), (gp_rs, 1)).float())
-        _sv(dgp, 0, (rows, cols), (dgp_rs, 1)).copy_(d * yv * s * (1 - s))
+        dg = d * yv * s * (1 - s)
+        _sv(dgp, 0, (rows, cols), (dgp_rs, 1)).copy_(dg)
+        if dgp_sum is not None:
+            dgp_sum += dg.sum(0)
         d = d * s
     if dy is not None:
         dy.copy_(d)

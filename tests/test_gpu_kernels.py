@@ -322,9 +322,11 @@ def test_tri_gate_and_residuals(rows):
     da = torch.randn(p, rows, device=DEV, generator=gen)
     db = torch.randn(p, rows, device=DEV, generator=gen)
     dy = torch.zeros_like(y)
-    ops.tri_gate_bwd(y, da, db, rows, hz, p, dy)
+    dsum = torch.zeros(4 * p, device=DEV)
+    ops.tri_gate_bwd(y, da, db, rows, hz, p, dy, dsum=dsum)
     (a * da.t()).sum().add((b * db.t()).sum()).backward()
     assert rel(dy[:, hz:], yf.grad[:, hz:]) < 1e-2
+    assert rel(dsum, yf.grad[:, hz:].sum(0)) < 1e-4      # fp32 sums of the unrounded values
 
     # gated residual with the g gate stored in Y (row stride hz + 4p)
     res = _mk((rows, hz), gen)
@@ -341,11 +343,13 @@ def test_tri_gate_and_residuals(rows):
     dy2 = torch.empty_like(y2)
     dgp = torch.zeros_like(y)
     dbias = torch.zeros(hz, device=DEV)
+    dgsum = torch.zeros(hz, device=DEV)
     ops.gated_residual_bwd(dout, rows, hz, y=y2, bias=bias, gp=y, gp_rs=hz + 4 * p, dy=dy2, dgp=dgp,
-                           dgp_rs=hz + 4 * p, dbias=dbias)
+                           dgp_rs=hz + 4 * p, dbias=dbias, dgp_sum=dgsum)
     assert rel(dy2, y2f.grad) < 1e-2
     assert rel(dgp[:, :hz], gpf.grad) < 1e-2
     assert rel(dbias, bf.grad) < 1e-3
+    assert rel(dgsum, gpf.grad.sum(0)) < 1e-4
 
     # bias + relu
     h = _mk((rows, 64), gen)
