@@ -243,10 +243,19 @@ def main():
     dominant = max(census, key=lambda k: census[k]["total_ms"]) if census else None
 
     # ------------------------------------------------------------------ CUDA graph of the step
-    use_graph = bool(args.graph) and world == 1 and not longseq
+    # the whole fwd+bwd step as one CUDA graph; under DAP the NCCL collectives (async, waited on
+    # the compute stream) are captured with it.  A backend that cannot be captured (gloo) falls
+    # back to eager launches and says so in the JSON line.
+    use_graph = bool(args.graph) and not longseq
+    graph_note = None
     if use_graph:
         from paper_2203_00854_b200.evoformer import GraphedStep
-        gstep = GraphedStep(stack, m, z, gm, gz)
+        try:
+            gstep = GraphedStep(stack, m, z, gm, gz)
+        except Exception as exc:  # noqa: BLE001 - reported, eager fallback
+            use_graph, graph_note = False, f"capture failed, eager: {type(exc).__name__}: {str(exc)[:120]}"
+            torch.cuda.synchronize()
+    if use_graph:
         launches_eager = inst.launches()
         run_step = gstep.replay
     else:
@@ -410,6 +419,7 @@ def main():
                        "l2": "per-step working set >> 126 MB L2 (no flush needed)", "step": step_desc},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches_per_step * args.steps),
             "gpu_launches_per_step": launches_per_step, "clocks": clk, "cuda_graph": use_graph,
+            **({"cuda_graph_note": graph_note} if graph_note else {}),
             "kernel_census_ms_per_step": {k: round(v["total_ms"], 3) for k, v in census.items()},
         }
         print(json.dumps(line), flush=True)

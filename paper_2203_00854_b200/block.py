@@ -307,14 +307,21 @@ def opm_fwd(bp: BlockParams, m2d, z2d, S: int, R: int, save=True, b_full=None, R
     rows_m = S * R
     h, f = bp.h, bp.f
     ln, mean, rstd = _layernorm_in(m2d, f["opm.ln_g"], f["opm.ln_b"], rows_m, Hm, pre_ln)
-    ab = torch.addmm(h["opm.b_ab"], ln, h["opm.w_ab"])              # [S*R, 2P] = [a | b]
-    A = Mat(ab, lo=(1, R * 2 * P), split=(P, 0), hi=(2 * P, 0))
     if gather is None:
+        ab = torch.addmm(h["opm.b_ab"], ln, h["opm.w_ab"])          # [S*R, 2P] = [a | b]
+        A = Mat(ab, lo=(1, R * 2 * P), split=(P, 0), hi=(2 * P, 0))
         Rj = R
         bsrc = ab
         B = Mat(ab, lo=(1, R * 2 * P), split=(P, 0), hi=(2 * P, 0), offset=P)
     else:
-        bsrc = gather(ab[:, P:].contiguous())                      # [N, S, R_loc, P]
+        # DAP: the right projection first; its all-gather is in flight on the communicator's
+        # stream while the left projection runs (DAO).  a and b are separate
+        # [S*R, P] buffers, so the overlapped and the synchronous schedules compute the same bits.
+        bl = torch.addmm(h["opm.b_ab"][P:], ln, h["opm.w_ab"][:, P:])
+        pending = gather(bl, async_op=True)                         # -> [N, S, R_loc, P]
+        ab = torch.addmm(h["opm.b_ab"][:P], ln, h["opm.w_ab"][:, :P])   # a only
+        A = Mat(ab, lo=(1, R * P))
+        bsrc = pending()
         nd = bsrc.shape[0]
         Rj = nd * R
         B = Mat(bsrc, lo=(1, R * P), split=(R * P, 0), hi=(S * R * P, 0))
@@ -352,27 +359,28 @@ def opm_bwd(bp: BlockParams, sv: Saved, dz_new, dm, reduce_scatter=None, next_db
     _wgrad(sv["o"].view(R * Rj, P * P), dz_new, g["opm.w_o"])
     do = _mm(dz_new, h["opm.w_o"].t())                               # [R*Rj, P*P] == [i][j][p][q]
     dab = torch.empty(S * R, 2 * P, device=dz_new.device, dtype=BF16)
-    ab = sv["ab"]
-    # da[s,i,p] = sum_{j,q} do[i,j,p,q] b[s,j,q] / S      (M = (i,p), N = s, K = (j,q))
+    ab = sv["ab"]                                                    # [a | b], or a alone under DAP
     dO_A = Mat(do, lo=(P, 1), split=(P, P), hi=(Rj * P * P, P * P))
-    if not sv["gathered"]:
-        Bb = Mat(ab, lo=(R * 2 * P, 1), split=(0, P), hi=(0, 2 * P), offset=P)
-    else:
-        Bb = Mat(sv["bsrc"], lo=(R * P, 1), split=(0, R * P), hi=(0, S * R * P))
     Cda = Mat(dab, lo=(1, R * 2 * P), split=(P, 0), hi=(2 * P, 0))
-    ops.bgemm(dO_A, Bb, Cda, 1, R * P, S, Rj * P, alpha=1.0 / S)
-    # db[s,j,q] = sum_{i,p} a[s,i,p] do[i,j,p,q] / S      (M = (j,q), N = s, K = (i,p))
     dO_T = Mat(do, lo=(1, P), split=(P, P), hi=(P * P, Rj * P * P))
-    Ba = Mat(ab, lo=(R * 2 * P, 1), split=(0, P), hi=(0, 2 * P))
     if not sv["gathered"]:
+        # da[s,i,p] = sum_{j,q} do[i,j,p,q] b[s,j,q] / S      (M = (i,p), N = s, K = (j,q))
+        Bb = Mat(ab, lo=(R * 2 * P, 1), split=(0, P), hi=(0, 2 * P), offset=P)
+        ops.bgemm(dO_A, Bb, Cda, 1, R * P, S, Rj * P, alpha=1.0 / S)
+        # db[s,j,q] = sum_{i,p} a[s,i,p] do[i,j,p,q] / S      (M = (j,q), N = s, K = (i,p))
+        Ba = Mat(ab, lo=(R * 2 * P, 1), split=(0, P), hi=(0, 2 * P))
         Cdb = Mat(dab, lo=(1, R * 2 * P), split=(P, 0), hi=(2 * P, 0), offset=P)
         ops.bgemm(dO_T, Ba, Cdb, 1, Rj * P, S, R * P, alpha=1.0 / S)
     else:
+        # the gathered factor's partial gradient first: its reduce-scatter overlaps the da GEMM
         nd = sv["bsrc"].shape[0]
         dbf = torch.empty(nd, S, R, P, device=dz_new.device, dtype=F32)   # rank-major partials
         Cdb = Mat(dbf, lo=(1, R * P), split=(R * P, 0), hi=(S * R * P, 0))
-        ops.bgemm(dO_T, Ba, Cdb, 1, Rj * P, S, R * P, alpha=1.0 / S)
-        dab[:, P:].copy_(reduce_scatter(dbf).view(S * R, P))
+        ops.bgemm(dO_T, Mat(ab, lo=(R * P, 1)), Cdb, 1, Rj * P, S, R * P, alpha=1.0 / S)
+        pending = reduce_scatter(dbf, async_op=True)
+        Bb = Mat(sv["bsrc"], lo=(R * P, 1), split=(0, R * P), hi=(0, S * R * P))
+        ops.bgemm(dO_A, Bb, Cda, 1, R * P, S, Rj * P, alpha=1.0 / S)
+        dab[:, P:].copy_(pending().view(S * R, P))
     _wgrad(sv["ln"], dab, g["opm.w_ab"])
     _bgrad(dab, g["opm.b_ab"])
     dln = _mm(dab, h["opm.w_ab"].t())
@@ -471,16 +479,19 @@ def triangle_bwd(bp: BlockParams, sv: Saved, dz_new, reduce_scatter=None, next_d
             Bb = Mat(bfull, lo=(1, R), batch_stride=rows)             # [N=k][K=j] MN-major
         else:
             Bb = Mat(bfull, lo=(1, R), split=(0, Rl), hi=(0, P * Rl * R), batch_stride=Rl * R)
-        ops.bgemm(dT, Bb, Mat(da_cm, lo=(R, 1), batch_stride=rows), P, M, R, N)
         Aa = Mat(sv["a_cm"], lo=(1, R), batch_stride=rows)            # [N=k][K=i] MN-major
         if not sv["gathered"]:
+            ops.bgemm(dT, Bb, Mat(da_cm, lo=(R, 1), batch_stride=rows), P, M, R, N)
             ops.bgemm(dTt, Aa, Mat(db_cm, lo=(R, 1), batch_stride=rows), P, N, R, M)
         else:
+            # the gathered factor's partial gradient first: its reduce-scatter overlaps the da GEMM
             nd = N // Rl
             dbf = torch.empty(nd, P, Rl, R, device=dev, dtype=F32)
             ops.bgemm(dTt, Aa, Mat(dbf, lo=(R, 1), split=(Rl, 0), hi=(P * Rl * R, 0), batch_stride=Rl * R),
                       P, N, R, M)
-            db_cm.copy_(reduce_scatter(dbf).view(P, rows))
+            pending = reduce_scatter(dbf, async_op=True)
+            ops.bgemm(dT, Bb, Mat(da_cm, lo=(R, 1), batch_stride=rows), P, M, R, N)
+            db_cm.copy_(pending().view(P, rows))
     else:
         # t[i][j] = sum_k a[k][i] b[k][j]:  da[k][i] = sum_j b[k][j] dT[i][j],  db[k][j] = sum_i a[k][i] dT[i][j]
         Ab = Mat(sv["b_cm"], lo=(Rl, 1), batch_stride=rows)           # [M=k][K=j] K-major
@@ -492,9 +503,11 @@ def triangle_bwd(bp: BlockParams, sv: Saved, dz_new, reduce_scatter=None, next_d
             daf = torch.empty(nd, P, R, Rl, device=dev, dtype=F32)
             ops.bgemm(Ab, dT, Mat(daf, lo=(Rl, 1), split=(0, Rl), hi=(0, P * R * Rl), batch_stride=R * Rl),
                       P, R, M, N)
-            da_cm.copy_(reduce_scatter(daf).view(P, rows))
+            pending = reduce_scatter(daf, async_op=True)             # overlaps the db GEMM below
             Aa = Mat(sv["afull"], lo=(Rl, 1), split=(0, Rl), hi=(0, P * R * Rl), batch_stride=R * Rl)
         ops.bgemm(Aa, dTt, Mat(db_cm, lo=(Rl, 1), batch_stride=rows), P, R, N, M)
+        if sv["gathered"]:
+            da_cm.copy_(pending().view(P, rows))
     ops.tri_gate_bwd(sv["Y"], da_cm, db_cm, rows, Hz, P, dY, dsum=g[f"{mod}.b_proj"][Hz:])
     _wgrad(sv["ln"], dY, g[f"{mod}.w_proj"])
     dln = _mm(dY, h[f"{mod}.w_proj"].t())

@@ -116,10 +116,15 @@ class DapComm:
     chunk d to rank d and returns [N(src), ...]; reduce_scatter(t [N, ...]) -> sum over
     ranks of chunk `rank`."""
 
-    def __init__(self, group=None, ledger: CommLedger | None = None):
+    def __init__(self, group=None, ledger: CommLedger | None = None, overlap: bool = True):
+        """overlap: asynchronous collectives (DAO) - the projection all-gathers,
+        the backward reduce-scatters and the gradient all-reduce run on the communicator's stream
+        under independent compute.  overlap=False issues the same collectives synchronously (same
+        buffers, same order, same bits: tests/test_dap_gloo.py compares the two schedules)."""
         import torch.distributed as dist
         self.dist = dist
         self.group = group
+        self.overlap = overlap
         if dist.is_available() and dist.is_initialized():
             self.N = dist.get_world_size(group)
             self.rank = dist.get_rank(group)
@@ -144,14 +149,45 @@ class DapComm:
         self._rec(category, t.numel() * (self.N - 1))
         return (out, work) if async_op else out
 
-    def reduce_scatter(self, t, category="reduce_scatter"):
+    def reduce_scatter(self, t, category="reduce_scatter", async_op=False):
+        """sum over ranks of chunk `rank` of t [N, ...]; async_op: returns a zero-argument callable
+        that waits and returns the result (the caller runs independent work in between)."""
         t = t.contiguous()
         if self.N == 1:
-            return t[0]
+            return (lambda: t[0]) if async_op else t[0]
         out = torch.empty(tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
-        self.dist.reduce_scatter_tensor(out, t.flatten(0, 1), op=self.dist.ReduceOp.SUM, group=self.group)
+        work = self.dist.reduce_scatter_tensor(out, t.flatten(0, 1), op=self.dist.ReduceOp.SUM, group=self.group,
+                                               async_op=async_op and self.overlap)
         self._rec(category, t[0].numel() * (self.N - 1))
-        return out
+        if not async_op:
+            return out
+        if work is None:
+            return lambda: out
+
+        def finish():
+            work.wait()
+            return out
+        return finish
+
+    def gather_fn(self, category="all_gather"):
+        """the ``gather`` callable block.py takes: gather(t) -> [N, *t.shape]; gather(t, async_op=True)
+        -> zero-argument callable returning it after the collective completed"""
+        def gather(t, async_op=False):
+            if not async_op:
+                return self.all_gather(t, category)
+            if not self.overlap:
+                out = self.all_gather(t, category)
+                return lambda: out
+            out, work = self.all_gather(t, category, async_op=True)
+
+            def finish():
+                work.wait()
+                return out
+            return finish
+        return gather
+
+    def reduce_scatter_fn(self, category="reduce_scatter"):
+        return lambda t, async_op=False: self.reduce_scatter(t, category, async_op=async_op)
 
     def all_to_all(self, t, category="all_to_all", async_op=False):
         t = t.contiguous()
@@ -162,11 +198,16 @@ class DapComm:
         self._rec(category, t.numel() - t.numel() // self.N)
         return (out, work) if async_op else out
 
-    def all_reduce_(self, t, category="grad_all_reduce"):
+    def all_reduce_(self, t, category="grad_all_reduce", async_op=False):
+        """in-place sum over ranks; async_op: returns a handle with wait() (the gradient all-reduce
+        of block i runs under block i-1's backward)"""
         if self.N == 1:
-            return t
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+            return _Done() if async_op else t
+        work = self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group,
+                                    async_op=async_op and self.overlap)
         self._rec(category, 2 * t.numel() * (self.N - 1) // self.N)
+        if async_op:
+            return work if work is not None else _Done()
         return t
 
     def all_reduce_max(self, x: float) -> float:
@@ -211,6 +252,7 @@ class ThreadComm(DapComm):
     def __init__(self, mesh: ThreadMesh, rank: int, ledger: CommLedger | None = None):
         self.mesh, self.N, self.rank, self.ledger = mesh, mesh.n, rank, ledger
         self.group = None
+        self.overlap = False  # rendezvous collectives complete on return
 
     def _rec(self, category, elems):
         # one ledger shared by the virtual ranks: rank 0 records for all (symmetric shards)
@@ -224,14 +266,14 @@ class ThreadComm(DapComm):
         out = torch.stack(parts, 0)
         return (out, _Done()) if async_op else out
 
-    def reduce_scatter(self, t, category="reduce_scatter"):
+    def reduce_scatter(self, t, category="reduce_scatter", async_op=False):
         parts = self.mesh.exchange(self.rank, t.contiguous())
         if self.N > 1:
             self._rec(category, t[0].numel() * (self.N - 1))
         out = parts[0][self.rank].clone()
         for p in parts[1:]:
             out += p[self.rank]
-        return out
+        return (lambda: out) if async_op else out
 
     def all_to_all(self, t, category="all_to_all", async_op=False):
         parts = self.mesh.exchange(self.rank, t.contiguous())
@@ -240,12 +282,12 @@ class ThreadComm(DapComm):
         out = torch.stack([p[self.rank] for p in parts], 0)
         return (out, _Done()) if async_op else out
 
-    def all_reduce_(self, t, category="grad_all_reduce"):
+    def all_reduce_(self, t, category="grad_all_reduce", async_op=False):
         parts = self.mesh.exchange(self.rank, t.clone())
         if self.N > 1:
             self._rec(category, 2 * t.numel() * (self.N - 1) // self.N)
         t.copy_(sum(parts[1:], parts[0]))
-        return t
+        return _Done() if async_op else t
 
     def all_reduce_max(self, x: float) -> float:
         return max(self.mesh.exchange(self.rank, x))
@@ -325,7 +367,7 @@ def dap_block_fwd(bp, comm: DapComm, m_loc, z_loc, save=True):
     # DAO: m is final here; its switch back to the sequence shard overlaps the pair stack
     m_out_ready = None  # issued after the OPM (which still reads m2)
     # 3) outer product mean: right projection gathered (dap_block.py:81-94)
-    gat = (lambda t: comm.all_gather(t)) if N > 1 else None
+    gat = comm.gather_fn() if N > 1 else None
     z2, sv["opm"] = B.opm_fwd(bp, m2, z_loc.reshape(Rl * R, Hz), S, Rl, save, gather=gat)
     m_out_ready = switch_cols_to_rows(comm, m2.view(S, Rl, Hm), async_op=True)
     # 4) outgoing triangle: b gathered across the row shard (dap_block.py:98-111)
@@ -358,7 +400,7 @@ def dap_block_bwd(bp, comm: DapComm, sv, dm_loc, dz_loc):
     S, R, Hm, Hz = cfg.n_seq, cfg.n_res, cfg.h_msa, cfg.h_pair
     Sl, Rl = S // N, R // N
     nh = cfg.n_head_msa
-    rs = (lambda t: comm.reduce_scatter(t)) if N > 1 else None
+    rs = comm.reduce_scatter_fn() if N > 1 else None
     dm_r_ready = switch_rows_to_cols(comm, dm_loc.view(Sl, R, Hm), async_op=True)  # overlaps the pair stack
     dz_c = switch_rows_to_cols(comm, dz_loc.view(Rl, R, Hz))          # inverse of step 8
     dz2 = B.transition_bwd(bp, sv["pair_trans"], dz_c.reshape(R * Rl, Hz).contiguous())
@@ -422,9 +464,15 @@ class DapStack:
         return m, z, saved
 
     def backward(self, saved, dm, dz):
+        # one gradient all-reduce per block (a 6.8 MB bucket at the training shape), issued async
+        # as soon as the block's parameter gradients are final: it runs on the communicator's
+        # stream under the previous block's backward; all are waited for before returning
+        pending = []
         for b, s in zip(reversed(self.blocks), reversed(saved)):
             dm, dz = dap_block_bwd(b, self.comm, s, dm, dz)
-            self.comm.all_reduce_(b.grad)
+            pending.append(self.comm.all_reduce_(b.grad, async_op=True))
+        for w in pending:
+            w.wait()
         return dm, dz
 
     def forward_backward(self, m, z, gm, gz):

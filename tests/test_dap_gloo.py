@@ -73,6 +73,19 @@ def _worker(rank, world, port):
         comm.all_reduce_(bp.grad)
         comm.ledger = None
         full = [comm.all_gather(a).flatten(0, 1) for a in (ml, zl, dm, dz)]
+        # the overlapped (DAO) schedule == the synchronous one, bit for bit, same ledgers
+        for overlap in (False, True):
+            bq = BlockParams(p, CFG, device="cpu")
+            bq.zero_grad()
+            led_f, led_b = CommLedger(world, element_size=2), CommLedger(world, element_size=2)
+            cq = DapComm(ledger=led_f, overlap=overlap)
+            ml2, zl2, sv2 = dap_block_fwd(bq, cq, shard_of(t(m), 0, cq), shard_of(t(z), 0, cq))
+            cq.ledger = led_b
+            dm2, dz2 = dap_block_bwd(bq, cq, sv2, shard_of(t(gm), 0, cq), shard_of(t(gz), 0, cq))
+            cq.all_reduce_(bq.grad, async_op=True).wait()
+            for a, b_ in ((ml2, ml), (zl2, zl), (dm2, dm), (dz2, dz), (bq.grad, bp.grad)):
+                assert torch.equal(a, b_), overlap
+            assert led_f.to_json() == fwd_led.to_json() and led_b.to_json() == bwd_led.to_json()
         if rank == 0:
             assert fwd_led.summary() == predict_block_ledger(CFG, world, 2), fwd_led.summary()
             assert bwd_led.counts == {"all_to_all": 6, "reduce_scatter": 4, "grad_all_reduce": 1}, bwd_led.counts
