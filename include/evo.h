@@ -195,6 +195,26 @@ int evo_bgemm_ws(const EvoMat* A, const EvoMat* B, const EvoMat* C,
                  int64_t batch, int64_t M, int64_t N, int64_t K,
                  float alpha, float beta, void* workspace, int64_t workspace_bytes, void* stream);
 
+/* ------------------------------------------------------------------ fused OuterProductMean
+ * outer_product_mean (evoformer.py:243-255) after its projections: with
+ *   o[i,j,p,q] = alpha * sum_s a[s,i,p] b[s,j,q]     (alpha = 1/N_s, evoformer.py:253)
+ * writes y[(i*J + j)*y_ld + c] = sum_{p,q} o[i,j,p,q] W_o[p*P+q, c] (bf16, before the output bias
+ * and the residual add of evoformer.py:255/318) as two back-to-back tcgen05 GEMMs per tile: o
+ * stays on chip.  o_save (may be NULL): also store o, bf16 [I][J][P][P] (the backward's operand).
+ * a_t: a as bf16 [I][P][N_s] (sequence-contiguous, evo_opm_transpose), b_t: b as [J][P][N_s]
+ * (a DAP all-gather of per-rank [J/N][P][N_s] blocks is already in this layout).
+ * W_o bf16 [P*P][Hz] row-major.  Supported extents: evo_opm_fused_supported() != 0 (P = 32,
+ * N_s <= 128 and a multiple of 8, I % 32 == 0, J % 8 == 0, Hz in {32, 64, 128}); the caller
+ * composes evo_bgemm + a projection GEMM otherwise.
+ * Replaces: the einsum + reshape + matmul of outer_product_mean, evoformer.py:251-255. */
+int evo_opm_fused_supported(int64_t I, int64_t J, int64_t S, int64_t P, int64_t Hz);
+int evo_opm_fused_fwd(const void* a_t, const void* b_t, const void* w_o, void* y, int64_t y_ld, void* o_save,
+                      int64_t I, int64_t J, int64_t S, int64_t P, int64_t Hz, float alpha, void* stream);
+/* The OPM projections [N_s*R][ld] (rows (s, r); channels col0 .. col0+P, and col0+P .. col0+2P
+ * when out_b != NULL) to the sequence-contiguous layout out[r][p][s] the fused kernel reads (bf16). */
+int evo_opm_transpose(const void* x, int64_t ld, int64_t col0, int64_t S, int64_t R, int64_t P, void* out_a,
+                      void* out_b, void* stream);
+
 /* ------------------------------------------------------------------ triangle gating
  * _triangle_projections epilogue (evoformer.py:260-264) for the merged projection
  * Y = LN(z) @ [W_g | W_a_sig | W_a_lin | W_b_sig | W_b_lin] + bias, Y bf16

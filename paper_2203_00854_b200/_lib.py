@@ -78,6 +78,9 @@ _SIGS = {
     "evo_bgemm_workspace": [i64, i64, i64, i64],
     "evo_bgemm_ws": [C.POINTER(EvoMat), C.POINTER(EvoMat), C.POINTER(EvoMat), i64, i64, i64, i64,
                      C.c_float, C.c_float, vp, i64, vp],
+    "evo_opm_fused_supported": [i64, i64, i64, i64, i64],
+    "evo_opm_fused_fwd": [vp, vp, vp, vp, i64, vp, i64, i64, i64, i64, i64, C.c_float, vp],
+    "evo_opm_transpose": [vp, i64, i64, i64, i64, i64, vp, vp, vp],
     "evo_tri_gate_fwd": [vp, i64, C.c_int, C.c_int, vp, vp, vp],
     "evo_tri_gate_bwd": [vp, vp, vp, C.c_int, i64, C.c_int, C.c_int, vp, vp, vp],
     "evo_gated_residual_fwd": [vp, vp, i64, vp, vp, i64, vp, C.c_int, i64, i64, vp],

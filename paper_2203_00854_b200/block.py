@@ -297,41 +297,62 @@ def opm_fwd(bp: BlockParams, m2d, z2d, S: int, R: int, save=True, b_full=None, R
             next_ln=None):
     """outer_product_mean (evoformer.py:243-255) + residual into z.
 
-    o[i][j][p][q] = sum_s a[s,i,p] b[s,j,q] / S is ONE tcgen05 GEMM with M = i*p,
-    N = j*q, K = s written straight into the [i][j][p][q] layout; then o @ W_o.
-    Under DAP, a is local ([S, R_loc, p]) and b is gathered (``gather(b_local)``
-    returns [N_dev, S, R_loc, p] rank-major), addressed without unpacking.
+    Fused path (evo_opm_fused_fwd, P = 32, N_s <= 128, R % 32 == 0): the projections are turned
+    sequence-contiguous ([R, P, S], evo_opm_transpose) and o[i][j][p][q] = sum_s a b / S is
+    contracted with W_o tile by tile on chip; o reaches HBM only when ``save`` (the backward's
+    operand).  Otherwise o is ONE tcgen05 GEMM (M = i*p, N = j*q, K = s) written straight into
+    the [i][j][p][q] layout, then o @ W_o.
+    Under DAP, a is local and b is all-gathered (rank-major [N_dev, R_loc, P, S] = [J, P, S] for
+    the fused kernel, [N_dev, S, R_loc, P] otherwise), addressed without unpacking.
     """
     cfg = bp.cfg
     P, Hm, Hz = cfg.hidden_proj, cfg.h_msa, cfg.h_pair
     rows_m = S * R
     h, f = bp.h, bp.f
     ln, mean, rstd = _layernorm_in(m2d, f["opm.ln_g"], f["opm.ln_b"], rows_m, Hm, pre_ln)
+    # evo_opm_fused_fwd when the extents allow it (J = N_dev * R is then a multiple of 8 as well)
+    fused = ops.opm_fused_supported(R, R, S, P, Hz)
     if gather is None:
         ab = torch.addmm(h["opm.b_ab"], ln, h["opm.w_ab"])          # [S*R, 2P] = [a | b]
-        A = Mat(ab, lo=(1, R * 2 * P), split=(P, 0), hi=(2 * P, 0))
-        Rj = R
-        bsrc = ab
-        B = Mat(ab, lo=(1, R * 2 * P), split=(P, 0), hi=(2 * P, 0), offset=P)
+        pending = None
     else:
         # DAP: the right projection first; its all-gather is in flight on the communicator's
         # stream while the left projection runs (DAO, PAPER.md:69-80).  a and b are separate
         # [S*R, P] buffers, so the overlapped and the synchronous schedules compute the same bits.
         bl = torch.addmm(h["opm.b_ab"][P:], ln, h["opm.w_ab"][:, P:])
-        pending = gather(bl, async_op=True)                         # -> [N, S, R_loc, P]
+        # the fused kernel reads b sequence-contiguous: the gathered blocks [R_loc][P][S] stack into [J][P][S]
+        pending = gather(ops.opm_transpose(bl, S, R, P) if fused else bl, async_op=True)
         ab = torch.addmm(h["opm.b_ab"][:P], ln, h["opm.w_ab"][:, :P])   # a only
-        A = Mat(ab, lo=(1, R * P))
-        bsrc = pending()
-        nd = bsrc.shape[0]
-        Rj = nd * R
-        B = Mat(bsrc, lo=(1, R * P), split=(R * P, 0), hi=(S * R * P, 0))
-    o = torch.empty(R, Rj, P, P, device=m2d.device, dtype=BF16)
-    Cm = Mat(o, lo=(P, 1), split=(P, P), hi=(Rj * P * P, P * P))
-    ops.bgemm(A, B, Cm, 1, R * P, Rj * P, S, alpha=1.0 / S)
-    y = _mm(o.view(R * Rj, P * P), h["opm.w_o"])
+    if fused:
+        if pending is None:
+            a_t, b_t = ops.opm_transpose(ab, S, R, P, both=True)    # [R, P, S] each
+            bsrc = None
+        else:
+            a_t = ops.opm_transpose(ab, S, R, P)
+            b_t = pending().reshape(-1, P, S)                       # [J, P, S]
+            bsrc = b_t
+        Rj = b_t.shape[0]
+        # evo_opm_fused_fwd: o stays on chip; training also stores it (bf16) for the backward
+        o = torch.empty(R, Rj, P, P, device=m2d.device, dtype=BF16) if save else None
+        y = ops.opm_fused_fwd(a_t, b_t, h["opm.w_o"], R, Rj, S, P, Hz, 1.0 / S, o_save=o)
+    else:  # tcgen05 contraction into o [R, Rj, P, P], then o @ W_o
+        if pending is None:
+            A = Mat(ab, lo=(1, R * 2 * P), split=(P, 0), hi=(2 * P, 0))
+            Rj = R
+            bsrc = ab
+            B = Mat(ab, lo=(1, R * 2 * P), split=(P, 0), hi=(2 * P, 0), offset=P)
+        else:
+            A = Mat(ab, lo=(1, R * P))
+            bsrc = pending()
+            Rj = bsrc.shape[0] * R
+            B = Mat(bsrc, lo=(1, R * P), split=(R * P, 0), hi=(S * R * P, 0))
+        o = torch.empty(R, Rj, P, P, device=m2d.device, dtype=BF16)
+        Cm = Mat(o, lo=(P, 1), split=(P, P), hi=(Rj * P * P, P * P))
+        ops.bgemm(A, B, Cm, 1, R * P, Rj * P, S, alpha=1.0 / S)
+        y = _mm(o.view(R * Rj, P * P), h["opm.w_o"])
     out = _residual_out(z2d, y, f["opm.b_o"], R * Rj, Hz, next_ln)
     sv = Saved(m=m2d, ln=ln, mean=mean, rstd=rstd, ab=ab, bsrc=bsrc, o=o, S=S, R=R, Rj=Rj,
-               gathered=gather is not None) if save else None
+               gathered=gather is not None, b_seq=fused and gather is not None) if save else None
     return out, sv
 
 
@@ -373,12 +394,15 @@ def opm_bwd(bp: BlockParams, sv: Saved, dz_new, dm, reduce_scatter=None, next_db
         ops.bgemm(dO_T, Ba, Cdb, 1, Rj * P, S, R * P, alpha=1.0 / S)
     else:
         # the gathered factor's partial gradient first: its reduce-scatter overlaps the da GEMM
-        nd = sv["bsrc"].shape[0]
+        nd = Rj // R
         dbf = torch.empty(nd, S, R, P, device=dz_new.device, dtype=F32)   # rank-major partials
         Cdb = Mat(dbf, lo=(1, R * P), split=(R * P, 0), hi=(S * R * P, 0))
         ops.bgemm(dO_T, Mat(ab, lo=(R * P, 1)), Cdb, 1, Rj * P, S, R * P, alpha=1.0 / S)
         pending = reduce_scatter(dbf, async_op=True)
-        Bb = Mat(sv["bsrc"], lo=(R * P, 1), split=(0, R * P), hi=(0, S * R * P))
+        if sv["b_seq"]:  # gathered b sequence-contiguous [J][P][S] (fused forward): (n = s, k = (j, q))
+            Bb = Mat(sv["bsrc"], lo=(1, S))
+        else:
+            Bb = Mat(sv["bsrc"], lo=(R * P, 1), split=(0, R * P), hi=(0, S * R * P))
         ops.bgemm(dO_A, Bb, Cda, 1, R * P, S, Rj * P, alpha=1.0 / S)
         dab[:, P:].copy_(pending().view(S * R, P))
     _wgrad(sv["ln"], dab, g["opm.w_ab"])

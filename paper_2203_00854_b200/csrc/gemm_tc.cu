@@ -19,8 +19,8 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "tma.cuh"
 
-#include <cuda.h>  // CUtensorMap (the encoder is fetched at run time via cudaGetDriverEntryPoint)
 #include <cstdlib>
 #include <cstring>
 
@@ -305,10 +305,6 @@ __global__ void __launch_bounds__(256) bgemm_splitk_reduce(const float* __restri
 __device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
 
 __device__ __forceinline__ int64_t off_dim0(const MatArg& m, uint32_t i) {
   uint32_t q = fdiv(i, m.mul0, m.sh0);
@@ -378,23 +374,6 @@ struct TileLoader {
 // A / B tiles arrive by cp.async.bulk.tensor with the 128-byte swizzle: BM (BN) rows of 64
 // bf16 = 128 B each, 8-row atoms of 1 KB.  One elected producer thread per stage instead of
 // 128 threads x 12 cp.async with per-chunk address arithmetic.
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void tma_ld3(uint32_t dst, uint64_t m, int c0, int c1, int c2, uint32_t b) {
-  asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
-               ::"r"(dst), "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(b) : "memory");
-}
-__device__ __forceinline__ void tma_ld4(uint32_t dst, uint64_t m, int c0, int c1, int c2, int c3, uint32_t b) {
-  asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];\n"
-               ::"r"(dst), "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(b) : "memory");
-}
-__device__ __forceinline__ void tma_ld5(uint32_t dst, uint64_t m, int c0, int c1, int c2, int c3, int c4, uint32_t b) {
-  asm volatile("cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n"
-               ::"r"(dst), "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(b) : "memory");
-}
-
 // How the producer addresses one operand's tensor map.  The map's dims are, in order: the
 // contiguous dim (K for K-major, rows for MN-major) as [lo] or [lo = 32, hi], the other dim
 // as [lo] or [lo = split, hi], then [batch] (MatArg's two-level addressing, e.g. the OPM
@@ -813,10 +792,7 @@ static int launch_bgemm_s(MatArg A, MatArg B, MatArg C, int64_t batch, int64_t M
 }
 
 // cuTensorMapEncodeTiled from the driver, fetched once through the runtime (no -lcuda)
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-static EncodeTiledFn encode_tiled() {
+EncodeTiledFn encode_tiled() {
   static EncodeTiledFn fn = nullptr;
   static bool tried = false;
   if (!tried) {

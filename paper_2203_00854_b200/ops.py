@@ -275,6 +275,37 @@ def bgemm(A: Mat, B: Mat, Cm: Mat, batch, M, N, K, alpha=1.0, beta=0.0):
          stream_handle(), work=work)
 
 
+def opm_fused_supported(I, J, S, P, Hz) -> bool:
+    return bool(_lib.load().evo_opm_fused_supported(I, J, S, P, Hz))
+
+
+def opm_transpose(x, S, R, P, col0=0, both=False):
+    """[S*R, ld] projection rows (s, r) -> sequence-contiguous [R, P, S] (and the next P channels
+    as a second [R, P, S] when both) for the fused OPM (evo_opm_transpose)."""
+    _cuda(x)
+    out_a = torch.empty(R, P, S, device=x.device, dtype=torch.bfloat16)
+    out_b = torch.empty_like(out_a) if both else None
+    call("evo_opm_transpose", _p(x), x.stride(0), col0, S, R, P, _p(out_a), _p(out_b), stream_handle(),
+         work=(0, 4 * S * R * P * (2 if both else 1)))
+    return (out_a, out_b) if both else out_a
+
+
+def opm_fused_fwd(a_t, b_t, w_o, I, J, S, P, Hz, alpha, y=None, o_save=None):
+    """outer_product_mean contraction + output projection (evoformer.py:251-255) with o kept on chip:
+    y[(i, j), c] = sum_{p,q} (alpha * sum_s a[s,i,p] b[s,j,q]) W_o[p*P+q, c]  (evo_opm_fused_fwd).
+    a_t: [I, P, S], b_t: [J, P, S] bf16 contiguous (opm_transpose); w_o: [P*P, Hz] bf16.
+    o_save: optional [I, J, P, P] bf16 output of o (kept for the backward)."""
+    _cuda(a_t, b_t, w_o)
+    if not (a_t.is_contiguous() and b_t.is_contiguous() and w_o.is_contiguous()):
+        raise KernelError("opm_fused_fwd: a_t, b_t and w_o must be contiguous")
+    if y is None:
+        y = torch.empty(I * J, Hz, device=a_t.device, dtype=torch.bfloat16)
+    call("evo_opm_fused_fwd", _p(a_t), _p(b_t), _p(w_o), _p(y), y.stride(0), _p(o_save), I, J, S, P, Hz,
+         float(alpha), stream_handle(),
+         work=(2 * I * J * P * P * (S + Hz), 2 * (S * I * P + S * J * P + P * P * Hz + I * J * Hz)))
+    return y
+
+
 # ------------------------------------------------------------------ elementwise epilogues
 
 def tri_gate_fwd(y, rows, hz, p, a_cm, b_cm):

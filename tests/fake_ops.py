@@ -155,6 +155,32 @@ def _idx(m: Mat, n0, n1, batch):
             + dim(0, n0)[None, :, None] + dim(1, n1)[None, None, :])
 
 
+def opm_fused_supported(I, J, S, P, Hz):
+    return P == 32 and 8 <= S <= 128 and S % 8 == 0 and I % 32 == 0 and I >= 32 and J % 8 == 0 and J >= 8 and \
+        Hz in (32, 64, 128)
+
+
+def opm_transpose(x, S, R, P, col0=0, both=False):
+    v = _sv(x, col0, (S, R, (2 if both else 1) * P), (R * x.stride(0), x.stride(0), 1))
+    a = v[..., :P].permute(1, 2, 0).contiguous()
+    return (a, v[..., P:].permute(1, 2, 0).contiguous()) if both else a
+
+
+CALLS = {"opm_fused_fwd": 0}
+
+
+def opm_fused_fwd(a_t, b_t, w_o, I, J, S, P, Hz, alpha, y=None, o_save=None):
+    CALLS["opm_fused_fwd"] += 1
+    o = (torch.einsum("ips,jqs->ijpq", a_t.float(), b_t.float()) * alpha).to(a_t.dtype)
+    if o_save is not None:
+        o_save.copy_(o)
+    out = o.reshape(I * J, P * P).float() @ w_o.float()
+    if y is None:
+        y = torch.empty(I * J, Hz, dtype=a_t.dtype)
+    y.copy_(out)
+    return y
+
+
 def bgemm(A: Mat, B: Mat, Cm: Mat, batch, M, N, K, alpha=1.0, beta=0.0):
     a = _flat(A.t)[_idx(A, M, K, batch)].float()
     b = _flat(B.t)[_idx(B, N, K, batch)].float()
@@ -254,7 +280,8 @@ def gate_mul(gate, y=None, bias=None, act=1, rows=None, cols=None, gate_rs=None,
 
 
 NAMES = ["gate_mul", "layernorm_fwd", "layernorm_bwd", "layernorm_rowdot_fwd", "attention_desc", "attention_fwd",
-         "attention_bwd_workspace", "attention_bwd", "bgemm", "tri_gate_fwd", "tri_gate_bwd",
+         "attention_bwd_workspace", "attention_bwd", "bgemm", "opm_fused_supported", "opm_transpose",
+         "opm_fused_fwd", "tri_gate_fwd", "tri_gate_bwd",
          "gated_residual_fwd", "gated_residual_bwd", "bias_act_fwd", "bias_act_bwd"]
 
 

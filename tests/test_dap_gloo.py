@@ -21,6 +21,9 @@ import torch.multiprocessing as mp
 from paper_2203_00854_b200.config import EvoConfig, init_block_params, synthetic_inputs
 
 CFG = EvoConfig(16, 32, 64, 32, 2, 1, 16)
+# hidden_proj 32 and R_loc % 32 == 0 at world 2: the OPM takes the fused-kernel host path (sequence-contiguous
+# projections, gathered [J, P, S] b, the backward's b_seq operand)
+CFG_FUSED_OPM = EvoConfig(16, 64, 64, 32, 2, 1, 32)
 
 
 def _port():
@@ -36,7 +39,8 @@ def _rel(a, b):
     return float((a - b).norm() / b.norm().clamp_min(1e-30))
 
 
-def _worker(rank, world, port):
+def _worker(rank, world, port, dims=None):
+    CFG = EvoConfig(*dims) if dims else globals()["CFG"]
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.set_num_threads(1)
@@ -96,6 +100,8 @@ def _worker(rank, world, port):
             errs = [_rel(full[0], mo), _rel(full[1], zo), _rel(full[2], dm1), _rel(full[3], dz1),
                     _rel(bp.grad, ref.grad)]
             assert max(errs[:2]) <= 1e-2 and max(errs[2:]) <= 2e-2, errs
+            if dims:  # the fused-OPM host path ran (sharded and single-device)
+                assert fake_ops.CALLS["opm_fused_fwd"] >= 2, fake_ops.CALLS
     finally:
         dist.destroy_process_group()
 
@@ -103,3 +109,9 @@ def _worker(rank, world, port):
 @pytest.mark.parametrize("world", [2, 4])
 def test_dap_block_gloo(world):
     mp.spawn(_worker, args=(world, _port()), nprocs=world, join=True)
+
+
+def test_dap_block_gloo_fused_opm_layout():
+    import dataclasses
+    dims = tuple(dataclasses.astuple(CFG_FUSED_OPM))
+    mp.spawn(_worker, args=(2, _port(), dims), nprocs=2, join=True)

@@ -445,3 +445,41 @@ def test_layernorm_rowdot_bwd():
     y.backward(dout.t())
     assert rel(dx.float() - res.float(), xr.grad) < 2e-2
     assert rel(dg, gr.grad) < 1e-2 and rel(db, br.grad) < 1e-2 and rel(dw, wr.grad) < 1e-2
+
+
+@pytest.mark.parametrize("I,J,S,Hz", [(32, 32, 16, 32), (32, 64, 48, 64), (64, 32, 128, 128), (32, 40, 96, 64),
+                                      (256, 256, 128, 128)])
+def test_opm_fused_fwd(I, J, S, Hz):
+    """evo_opm_fused_fwd (+ evo_opm_transpose) vs fp32 torch: o = einsum(sip,sjq->ijpq)/S rounded to bf16 (as
+    the unfused path stores it), y = o @ W_o.  The stored o is the same bf16 tensor up to fp32 summation order."""
+    P = 32
+    g = torch.Generator(device=DEV).manual_seed(I * 7 + J + S + Hz)
+    a = torch.randn(S, I, P, device=DEV, generator=g).bfloat16()
+    b = torch.randn(S, J, P, device=DEV, generator=g).bfloat16()
+    w = (torch.randn(P * P, Hz, device=DEV, generator=g) / 32).bfloat16()
+    assert ops.opm_fused_supported(I, J, S, P, Hz)
+    a_t = ops.opm_transpose(a.view(S * I, P), S, I, P)
+    b_t = ops.opm_transpose(b.view(S * J, P), S, J, P)
+    assert torch.equal(a_t, a.permute(1, 2, 0)) and torch.equal(b_t, b.permute(1, 2, 0))
+    n = min(I, J)
+    ab = torch.cat([a[:, :n], b[:, :n]], -1).reshape(S * n, 2 * P)  # merged [a | b] rows: both outputs of one call
+    a2, b2 = ops.opm_transpose(ab, S, n, P, both=True)
+    assert torch.equal(a2, a_t[:n]) and torch.equal(b2, b_t[:n])
+    o_ref = (torch.einsum("sip,sjq->ijpq", a.float(), b.float()) / S).bfloat16().contiguous()
+    y_ref = o_ref.view(I * J, P * P).float() @ w.float()
+    o = torch.empty(I, J, P, P, device=DEV, dtype=torch.bfloat16)
+    y = ops.opm_fused_fwd(a_t, b_t, w, I, J, S, P, Hz, 1.0 / S, o_save=o)
+    y2 = ops.opm_fused_fwd(a_t, b_t, w, I, J, S, P, Hz, 1.0 / S)  # inference form: no o
+    torch.cuda.synchronize()
+    assert rel(o, o_ref) < 1e-3, rel(o, o_ref)
+    assert rel(y, y_ref) < 5e-3, rel(y, y_ref)
+    assert torch.equal(y, y2)
+
+
+def test_opm_fused_rejects_unsupported():
+    t = torch.zeros(32, 16, 32, device=DEV, dtype=torch.bfloat16)
+    assert not ops.opm_fused_supported(32, 32, 32, 16, 64)   # hidden_proj 16
+    assert not ops.opm_fused_supported(48, 32, 32, 32, 64)   # I % 32
+    assert not ops.opm_fused_supported(32, 32, 256, 32, 64)  # N_s > 128
+    with pytest.raises(Exception):
+        ops.opm_fused_fwd(t, t, torch.zeros(256, 64, device=DEV, dtype=torch.bfloat16), 32, 32, 32, 16, 64, 1.0)

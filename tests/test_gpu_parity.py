@@ -35,7 +35,9 @@ from paper_2203_00854_b200.ops import Strided  # noqa: E402
 GRAD_TOL = 2e-2
 TOL = 2e-2
 STACK_TOL = 5e-2
-CFGS = {"c1": EvoConfig(16, 32, 64, 32, 2, 1, 16), "h84": EvoConfig(16, 32, 64, 32, 8, 4, 8)}
+CFGS = {"c1": EvoConfig(16, 32, 64, 32, 2, 1, 16), "h84": EvoConfig(16, 32, 64, 32, 8, 4, 8),
+        # hidden_proj 32, N_r % 32 == 0: the fused OuterProductMean kernel (evo_opm_fused_fwd) runs
+        "p32": EvoConfig(32, 64, 64, 64, 2, 2, 32)}
 TRAIN = EvoConfig(128, 256, 256, 128, 8, 4, 32)
 
 
@@ -75,7 +77,7 @@ def _grad_check(cfg, seed):
     return errs, keys
 
 
-@pytest.mark.parametrize("name,seed", [("c1", 7), ("c1", 31), ("h84", 101)])
+@pytest.mark.parametrize("name,seed", [("c1", 7), ("c1", 31), ("h84", 101), ("p32", 5)])
 def test_block_gradients_mask_matched(name, seed):
     errs, keys = _grad_check(CFGS[name], seed)
     print(name, seed, {k: round(v, 5) for k, v in errs.items()}, "worst key", max(keys.items(), key=lambda kv: kv[1][0]))
