@@ -7,6 +7,10 @@ cli.py:1-312).
               ledger (bytes handed to NCCL, reference convention) against
               predict_block_ledger (cli.py:119-138, commcost.py:126-158)
   commvolume  closed-form tensor- vs axial-parallel volumes (cli.py:112-116)
+  schedule    the reference's timeline simulation (cli.py:205-225, scheduling.py:91-111) of a timeline
+              document, in sync and async modes
+  timeline    the DAP block's MEASURED timeline: one rank's forward timed segment by segment on the
+              GPU (collectives modelled from their bytes), simulated sync vs async (timeline.py)
 
 Same envelope as the reference: one JSON document {"schema": "evoplan-cli-v1", "command",
 "result"[, "timestamp"]}, sorted keys, --no-timestamp for byte-identical reruns; same exit
@@ -103,6 +107,24 @@ def cmd_simulate(args) -> int:
     return EXIT_OK if rel <= DAP_REL_TOL and measured == predicted else EXIT_CONSTRAINT
 
 
+def cmd_schedule(args) -> int:
+    from .timeline import events_from_json, simulate_schedule
+    with open(args.timeline) as fh:
+        events = events_from_json(fh.read())
+    res = {m: {"makespan": r.makespan, "timeline": {k: list(v) for k, v in r.timeline.items()}}
+           for m in ("sync", "async") for r in [simulate_schedule(events, m)]}
+    _emit(args, "schedule", res)
+    return EXIT_OK
+
+
+def cmd_timeline(args) -> int:
+    from .timeline import measure_dap_forward, overlap_report
+    events, info = measure_dap_forward(_config(args), args.devices, seed=args.seed, link_gbps=args.link_gbps,
+                                       latency_us=args.latency_us)
+    _emit(args, "timeline", overlap_report(events, info))
+    return EXIT_OK
+
+
 def _add_config_args(p: argparse.ArgumentParser) -> None:
     # the reference's flags (cli.py:56-63) with GPU-sized defaults: the kernels need head dims
     # and projection widths that are multiples of 8 (also per DAP shard: n_res/N >= 8) and a
@@ -135,6 +157,17 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--element-size", type=int, default=2)
     p.add_argument("--out")
     p.set_defaults(fn=cmd_simulate)
+    p = sub.add_parser("schedule", help="simulate a comm/compute timeline document (sync and async)")
+    p.add_argument("--timeline", required=True)
+    p.add_argument("--out")
+    p.set_defaults(fn=cmd_schedule)
+    p = sub.add_parser("timeline", help="measured DAP block timeline on the GPU, sync vs async")
+    _add_config_args(p)
+    p.add_argument("--devices", type=int, required=True)
+    p.add_argument("--link-gbps", type=float, default=900.0, help="modelled per-device collective bandwidth")
+    p.add_argument("--latency-us", type=float, default=10.0, help="modelled per-collective latency")
+    p.add_argument("--out")
+    p.set_defaults(fn=cmd_timeline)
     return parser
 
 

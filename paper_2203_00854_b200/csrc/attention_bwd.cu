@@ -384,6 +384,13 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
   constexpr uint32_t ID_Q = make_idesc_bf16(128, CP, 1, 1);    // dQ = dS K  (A and B: MN-major views)
   constexpr uint32_t LBO_ROWS = (128 / 8) * 128;               // 2048: next 8-k group of a 128-row K-major tile
 
+#if EVO_EXP == 4 || EVO_EXP == 5
+  if (blockIdx.x & 1) {  // experiment: offset the two co-resident CTAs by part of an iteration
+    const long long t0 = clock64();
+    while (clock64() - t0 < (EVO_EXP == 4 ? 1500 : 3000)) {
+    }
+  }
+#endif
   int it = 0;
   bf16 kb_next = f2bf(0.f);  // per-key bias of the next unit (MODE 1)
   bool first_unit = true;

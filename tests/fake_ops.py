@@ -155,6 +155,25 @@ def _idx(m: Mat, n0, n1, batch):
             + dim(0, n0)[None, :, None] + dim(1, n1)[None, None, :])
 
 
+def softmax_fwd(x, bias=None, mask=None, scale=1.0, out=None):
+    """softmax((x + bias) * scale + mask) over the last axis, operands broadcast right-aligned"""
+    v = x.to(torch.float64 if x.dtype == torch.float64 else F32)
+    if bias is not None:
+        v = v + bias
+    v = v * scale
+    if mask is not None:
+        v = v + mask
+    y = torch.softmax(v, -1).to(x.dtype)
+    if out is not None:
+        out.copy_(y.reshape(out.shape))
+        return out
+    return y
+
+
+def count_nonfinite(x) -> int:
+    return int((~torch.isfinite(x)).sum())
+
+
 def opm_fused_supported(I, J, S, P, Hz):
     return P == 32 and 8 <= S <= 128 and S % 8 == 0 and I % 32 == 0 and I >= 32 and J % 8 == 0 and J >= 8 and \
         Hz in (32, 64, 128)
@@ -280,7 +299,7 @@ def gate_mul(gate, y=None, bias=None, act=1, rows=None, cols=None, gate_rs=None,
 
 
 NAMES = ["gate_mul", "layernorm_fwd", "layernorm_bwd", "layernorm_rowdot_fwd", "attention_desc", "attention_fwd",
-         "attention_bwd_workspace", "attention_bwd", "bgemm", "opm_fused_supported", "opm_transpose",
+         "attention_bwd_workspace", "attention_bwd", "bgemm", "softmax_fwd", "count_nonfinite", "opm_fused_supported", "opm_transpose",
          "opm_fused_fwd", "tri_gate_fwd", "tri_gate_bwd",
          "gated_residual_fwd", "gated_residual_bwd", "bias_act_fwd", "bias_act_bwd"]
 
@@ -290,6 +309,21 @@ def install():
     g = globals()
     for n in NAMES:
         setattr(_real, n, g[n])
+
+
+class installed:
+    """context manager: the CPU stand-ins for the duration of a block, the real ops restored after
+    (for tests sharing a process with GPU tests)"""
+
+    def __enter__(self):
+        self.saved = {n: getattr(_real, n) for n in NAMES}
+        install()
+        return self
+
+    def __exit__(self, *exc):
+        for n, f in self.saved.items():
+            setattr(_real, n, f)
+        return False
 
 
 _ = math  # (kept for parity with the CUDA module's imports)
