@@ -194,7 +194,8 @@ class TimingComm:
 
 def measure_dap_forward(cfg, N: int, seed: int = 0, warmup: int = 2, link_gbps: float = 900.0,
                         latency_us: float = 10.0):
-    """Time one rank's DAP block forward (dap.dap_block_fwd) at mesh size N on the current GPU and
+    """Time one rank's DAP block forward (dap.dap_block_fwd) at mesh size N on the current GPU (device
+    time: the launches are queued behind a spin kernel before the first mark) and
     build the timeline: compute segments (measured, ms) and collectives (modelled at ``link_gbps``
     GB/s per device plus ``latency_us``).  Returns (events, info)."""
     import numpy as np
@@ -211,6 +212,10 @@ def measure_dap_forward(cfg, N: int, seed: int = 0, warmup: int = 2, link_gbps: 
     z = torch.tensor(rng.normal(size=(R // N, R, cfg.h_pair)), device="cuda").bfloat16()
     for _ in range(warmup):
         dap.dap_block_fwd(bp, TimingComm(N), m, z, save=False)
+    # the device first spins while the host enqueues the whole forward, so the segment times are
+    # device execution times, not the host's launch rate
+    torch.cuda.synchronize()
+    torch.cuda._sleep(int(4e8))
     comm = TimingComm(N)
     dap.dap_block_fwd(bp, comm, m, z, save=False)
     comm.marks.append(comm._ev())
