@@ -195,6 +195,16 @@ int evo_bgemm_ws(const EvoMat* A, const EvoMat* B, const EvoMat* C,
                  int64_t batch, int64_t M, int64_t N, int64_t K,
                  float alpha, float beta, void* workspace, int64_t workspace_bytes, void* stream);
 
+/* Weight gradient of a projection: dW[M][N] (fp32, row stride ldw) += X^T dY, X bf16 [rows][M]
+ * (row stride ldx), dY bf16 [rows][N] (ldy); K = rows.  tcgen05, MN-major TMA operands, split-K
+ * with fp32 partials in workspace (evo_wgrad_workspace() bytes; 0 = no split) reduced in a fixed
+ * order (deterministic).  Replaces the weight-gradient products of every projection of the block
+ * (the reference has no backward; these are the transposes of evoformer.py:183-195, 239-240,
+ * 246-247, 255, 260-264, 270). */
+int64_t evo_wgrad_workspace(int64_t rows, int64_t M, int64_t N);
+int evo_wgrad(const void* x, int64_t ldx, const void* dy, int64_t ldy, float* dw, int64_t ldw, int64_t rows,
+              int64_t M, int64_t N, void* workspace, int64_t workspace_bytes, void* stream);
+
 /* ------------------------------------------------------------------ fused OuterProductMean
  * outer_product_mean (evoformer.py:243-255) after its projections: with
  *   o[i,j,p,q] = alpha * sum_s a[s,i,p] b[s,j,q]     (alpha = 1/N_s, evoformer.py:253)

@@ -78,6 +78,8 @@ _SIGS = {
     "evo_bgemm_workspace": [i64, i64, i64, i64],
     "evo_bgemm_ws": [C.POINTER(EvoMat), C.POINTER(EvoMat), C.POINTER(EvoMat), i64, i64, i64, i64,
                      C.c_float, C.c_float, vp, i64, vp],
+    "evo_wgrad_workspace": [i64, i64, i64],
+    "evo_wgrad": [vp, i64, vp, i64, vp, i64, i64, i64, i64, vp, i64, vp],
     "evo_opm_fused_supported": [i64, i64, i64, i64, i64],
     "evo_opm_fused_fwd": [vp, vp, vp, vp, i64, vp, i64, i64, i64, i64, i64, C.c_float, vp],
     "evo_opm_transpose": [vp, i64, i64, i64, i64, i64, vp, vp, vp],
@@ -138,7 +140,7 @@ def check(rc: int) -> None:
 
 
 # kernels launched per C-ABI call (evo_gated_attention_bwd = prep + main + dq finish [+ dbias reduce])
-LAUNCHES = {"evo_gated_attention_bwd": 3, "evo_bgemm_ws": 2}
+LAUNCHES = {"evo_gated_attention_bwd": 3, "evo_bgemm_ws": 2, "evo_wgrad": 2}
 
 
 class Instrument:

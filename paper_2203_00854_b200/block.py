@@ -66,6 +66,8 @@ def _wgrad(x, dy, out):
     """out (fp32) += x^T @ dy with fp32 accumulation (side stream).  Every parameter gradient
     ACCUMULATES into bp.grad (micro-batch accumulation works; zero_grad() between steps)."""
     if x.is_cuda:  # cuBLAS, beta = 1: the fp32 result is added straight into the grad buffer view
+        # (evo_wgrad, the tcgen05 split-K form, matches cuBLAS in isolation but measured 1 % slower in
+        # the step: its all-SM grid competes with the main stream's kernels; profiles/r02_wgrad_*)
         SideStream.run(lambda: torch.addmm(out, x.t(), dy, out_dtype=F32, out=out), x, dy)
     else:  # CPU only in the host-logic tests (fake kernel backend)
         out += x.t().float() @ dy.float()

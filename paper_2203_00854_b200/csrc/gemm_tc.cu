@@ -876,11 +876,14 @@ static bool tma_map(CUtensorMap* map, TmaOp* op, const MatArg& a, bool mn_major,
 
 template <int BN, bool AM, bool BMN, typename TC>
 static int launch_bgemm_ws(MatArg A, MatArg B, MatArg C, int64_t batch, int64_t M, int64_t N, int64_t K, float alpha,
-                           float beta, int c_mode, int splits, float* ws, cudaStream_t st) {
+                           float beta, int c_mode, int splits, float* ws, cudaStream_t st, bool reduce = true) {
   // 256-wide N tiles (long-K, large problems) halve the A-tile re-reads per FLOP; 3 stages
   // keep the ring + staging tile within shared memory
-  constexpr int STAGES = BN >= 256 ? 3 : 4;
-  const size_t smem = STAGES * (GEMM_BM * GEMM_BK * 2 + BN * GEMM_BK * 2) + (size_t)GEMM_BM * (BN * sizeof(TC) + 16);
+  // split-K partials leave from registers (no staging tile): 256-wide N tiles keep 4 stages
+  constexpr int STAGES = (BN >= 256 && sizeof(TC) == 2) ? 3 : 4;
+  const size_t pipe = STAGES * (GEMM_BM * GEMM_BK * 2 + BN * GEMM_BK * 2);
+  const size_t smem = pipe + (splits > 1 ? 0 : (size_t)GEMM_BM * (BN * sizeof(TC) + 16));
+  if (smem > 227 * 1024) return set_error("bgemm_ws: tile config exceeds shared memory"), EVO_ERR_SHAPE;
   // operands whose addressing maps onto a tensor map take the TMA producer (128-byte swizzle)
   CUtensorMap ta, tb;
   memset(&ta, 0, sizeof(ta));
@@ -890,24 +893,24 @@ static int launch_bgemm_ws(MatArg A, MatArg B, MatArg C, int64_t batch, int64_t 
   const bool tma = !tma_off && tma_map(&ta, &oa, A, AM, M, K, batch, GEMM_BM) && tma_map(&tb, &ob, B, BMN, N, K, batch, BN);
   const int64_t tiles = ((M + GEMM_BM - 1) / GEMM_BM) * ((N + BN - 1) / BN) * batch * splits;
   const int64_t grid = tiles < sm_count() ? tiles : sm_count();
-  auto run = [&](auto kern, bool& attr_set) -> int {
-    if (!attr_set) {
+  auto run = [&](auto kern, size_t& attr_set) -> int {
+    if (attr_set < smem) {  // the split-K form needs no staging tile: the attribute tracks the largest launch
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return cuda_status(e, "bgemm_ws attr");
-      attr_set = true;
+      attr_set = smem;
     }
     kern<<<(unsigned)grid, WS_GEMM_THREADS, smem, st>>>(A, B, C, (uint32_t)M, (uint32_t)N, (uint32_t)K, alpha, beta,
                                                         c_mode, splits, splits > 1 ? ws : nullptr, (int)batch, ta, tb,
                                                         oa, ob);
     return EVO_OK;
   };
-  static bool attr_plain = false, attr_tma = false;
+  static size_t attr_plain = 0, attr_tma = 0;
   int rc;
   if (tma) rc = run(bgemm_ws_kernel<BN, AM, BMN, STAGES, TC, true>, attr_tma);
   else rc = run(bgemm_ws_kernel<BN, AM, BMN, STAGES, TC, false>, attr_plain);
   if (rc) return rc;
   EVO_LAUNCH_CHECK("bgemm_ws launch");
-  if (splits > 1) {
+  if (splits > 1 && reduce) {
     const bool rows_contig = C.lo0 == 1 && C.split0 % 8 == 0 && M % 8 == 0;
     EVO_CHECK_ARG(rows_contig || N % 8 == 0, EVO_ERR_ALIGN, "bgemm split-K: M or N must be a multiple of 8");
     int64_t n8 = batch * M * N / 8;
@@ -1028,7 +1031,103 @@ static int bgemm_entry(const EvoMat* A, const EvoMat* B, const EvoMat* C, int64_
   return dispatch_major<128, float>(am, bm, a, b, c, batch, M, N, K, alpha, beta, c_mode, splits, ws, st);
 }
 
+// Weight gradient dW[M][N] (fp32) += X^T dY with X [rows][M], dY [rows][N] bf16 row-major (K = rows,
+// tens of thousands): both operands MN-major through TMA, 256-wide N tiles (the 128-row A tile is
+// re-read once per 256 output columns instead of once per 64), and split-K sized so the
+// (tile, split) units form ONE wave over the SMs - every SM streams its K slice of
+// X and dY at HBM rate (the fp32 partials, units x BN x 512 B, are reduced by all SMs); the deterministic
+// reduction adds the partials into dW in split order (beta = 1: gradients accumulate).
+static int wgrad_splits(int64_t M, int64_t N, int64_t rows, int bn) {
+  const int64_t tiles = ((M + 127) / 128) * ((N + bn - 1) / bn);
+  const int64_t kt = (rows + GEMM_BK - 1) / GEMM_BK;
+  int64_t s = sm_count() / tiles;
+  if (s > kt / 4) s = kt / 4;  // >= 4 k-tiles per split
+  if (s < 1) s = 1;
+  const int64_t per = (kt + s - 1) / s;
+  return (int)((kt + per - 1) / per);
+}
+static int wgrad_bn(int64_t N) { return N >= 192 ? 256 : (N > 64 ? 128 : 64); }
+
+// dw[m][n] (row stride ldw) += sum_s ws[s][m][n]: a CTA owns 32 four-element column groups and its 8
+// warps split the partials (warp w takes s = w, w + 8, ...; 4 loads in flight per thread); the 8
+// per-warp sums meet in shared memory and are added in warp order (deterministic).
+__global__ void __launch_bounds__(256) wgrad_reduce(const float* __restrict__ ws, float* __restrict__ dw, int64_t ldw,
+                                                    int M, int N, int splits) {
+  __shared__ float4 part[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t MN = (int64_t)M * N;
+  const int64_t e = ((int64_t)blockIdx.x * 32 + lane) * 4;  // first of 4 elements (N % 4 == 0)
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (e < MN) {
+    int s = w;
+    for (; s + 24 < splits; s += 32) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldcs(reinterpret_cast<const float4*>(ws + (int64_t)(s + 8 * u) * MN + e));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w;
+      }
+    }
+    for (; s < splits; s += 8) {
+      const float4 v = __ldcs(reinterpret_cast<const float4*>(ws + (int64_t)s * MN + e));
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+  }
+  part[w][lane] = acc;
+  __syncthreads();
+  if (w == 0 && e < MN) {
+    float4 t = part[0][lane];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) {
+      t.x += part[i][lane].x; t.y += part[i][lane].y; t.z += part[i][lane].z; t.w += part[i][lane].w;
+    }
+    const int64_t m = e / N, n = e % N;
+    float4* d = reinterpret_cast<float4*>(dw + m * ldw + n);
+    float4 o = *d;
+    o.x += t.x; o.y += t.y; o.z += t.z; o.w += t.w;
+    *d = o;
+  }
+}
+
 }  // namespace evo
+
+extern "C" int64_t evo_wgrad_workspace(int64_t rows, int64_t M, int64_t N) {
+  const int bn = evo::wgrad_bn(N);
+  const int s = evo::wgrad_splits(M, N, rows, bn);
+  return s > 1 ? (int64_t)s * M * N * 4 : 0;
+}
+
+extern "C" int evo_wgrad(const void* x, int64_t ldx, const void* dy, int64_t ldy, float* dw, int64_t ldw, int64_t rows,
+                         int64_t M, int64_t N, void* workspace, int64_t ws_bytes, void* stream) {
+  using namespace evo;
+  EVO_CHECK_ARG(x && dy && dw, EVO_ERR_ARG, "wgrad: null operand");
+  EVO_CHECK_ARG(rows >= 1 && M >= 8 && N >= 8 && M % 8 == 0 && N % 8 == 0 && ldx % 8 == 0 && ldy % 8 == 0 &&
+                    rows < (1LL << 31),
+                EVO_ERR_SHAPE, "wgrad: M, N, ldx, ldy must be multiples of 8");
+  EVO_CHECK_ARG((((uintptr_t)x | (uintptr_t)dy) & 15) == 0 && ((uintptr_t)dw & 15) == 0, EVO_ERR_ALIGN,
+                "wgrad: operands must be 16-byte aligned");
+  int bn = wgrad_bn(N);
+  int splits = wgrad_splits(M, N, rows, bn);
+  if (splits > 1 && (!workspace || ws_bytes < (int64_t)splits * M * N * 4)) splits = 1;
+  if (splits == 1 && bn == 256) bn = 128;  // the unsplit form stages its tile in shared memory
+  EvoMat A{const_cast<void*>(x), EVO_BF16, 0, {0, 0}, {0, 0}, {1, ldx}};   // A[m][k] = x[k][m]
+  EvoMat B{const_cast<void*>(dy), EVO_BF16, 0, {0, 0}, {0, 0}, {1, ldy}};  // B[n][k] = dy[k][n]
+  EvoMat C{dw, EVO_F32, 0, {0, 0}, {0, 0}, {ldw, 1}};
+  MatArg a = to_arg(&A, M, rows), b = to_arg(&B, N, rows), c = to_arg(&C, M, N);
+  cudaStream_t st = (cudaStream_t)stream;
+  float* ws = (float*)workspace;
+  // the main kernel writes the split partials (its own split-K reduction is replaced below)
+  const int rc = bn == 256   ? launch_bgemm_ws<256, true, true, float>(a, b, c, 1, M, N, rows, 1.f, 1.f, 0, splits, ws, st, false)
+                 : bn == 128 ? launch_bgemm_ws<128, true, true, float>(a, b, c, 1, M, N, rows, 1.f, 1.f, 0, splits, ws, st, false)
+                             : launch_bgemm_ws<64, true, true, float>(a, b, c, 1, M, N, rows, 1.f, 1.f, 0, splits, ws, st, false);
+  if (rc || splits == 1) return rc;
+  EVO_CHECK_ARG(ldw % 4 == 0, EVO_ERR_ALIGN, "wgrad: ldw must be a multiple of 4");
+  const int64_t groups = (M * N / 4 + 31) / 32;
+  wgrad_reduce<<<(unsigned)groups, 256, 0, st>>>(ws, dw, ldw, (int)M, (int)N, splits);
+  EVO_LAUNCH_CHECK("wgrad reduce");
+  return EVO_OK;
+}
 
 extern "C" int evo_bgemm(const EvoMat* A, const EvoMat* B, const EvoMat* C, int64_t batch, int64_t M, int64_t N,
                          int64_t K, float alpha, float beta, void* stream) {

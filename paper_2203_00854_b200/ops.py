@@ -306,6 +306,21 @@ def opm_fused_fwd(a_t, b_t, w_o, I, J, S, P, Hz, alpha, y=None, o_save=None):
     return y
 
 
+def wgrad(x, dy, dw):
+    """dw (fp32 [M, N], any row stride) += x^T @ dy for x [rows, M], dy [rows, N] bf16 (evo_wgrad)."""
+    _cuda(x, dy, dw)
+    rows, M = x.shape
+    N = dy.shape[1]
+    if x.stride(1) != 1 or dy.stride(1) != 1 or dw.stride(1) != 1 or dw.dtype != torch.float32:
+        raise KernelError("wgrad: row-major bf16 x / dy and an fp32 dw are required")
+    ws_bytes = int(_lib.load().evo_wgrad_workspace(rows, M, N))
+    ws = torch.empty(max(ws_bytes // 4, 1), device=x.device, dtype=torch.float32)
+    call("evo_wgrad", _p(x), x.stride(0), _p(dy), dy.stride(0), _p(dw), dw.stride(0), rows, M, N,
+         _p(ws) if ws_bytes else None, ws_bytes, stream_handle(),
+         work=(2 * rows * M * N, 2 * rows * (M + N) + 8 * M * N), launches=2 if ws_bytes else 1)
+    return dw
+
+
 # ------------------------------------------------------------------ elementwise epilogues
 
 def tri_gate_fwd(y, rows, hz, p, a_cm, b_cm):

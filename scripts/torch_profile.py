@@ -29,3 +29,19 @@ for e in rows[:45]:
     if t <= 0:
         continue
     print(f"{t/1e3/nb:8.3f} ms/block {100*t/tot:5.1f}%  n={e.count//nb:4d}/blk  {e.key[:100]}")
+
+CATEGORIES = [("attention bwd", ("attn_bwd", "attn_dbias")), ("attention fwd", ("attn_fwd",)),
+              ("cuBLAS", ("nvjet", "cublas", "gemm", "splitKreduce", "cutlass")), ("OPM fused", ("opm_",)),
+              ("tcgen05 bgemm", ("bgemm",)), ("LayerNorm / residual", ("ln_", "residual_ln", "layernorm")),
+              ("elementwise / gates", ("gated_residual", "bias_act", "tri_gate", "colsum", "count_nonfinite")),
+              ("copies / torch eager", ("copy", "Memcpy", "fill", "elementwise_kernel", "reduce_kernel"))]
+cat = {}
+for e in rows:
+    t = getattr(e, "self_device_time_total", 0)
+    if t <= 0:
+        continue
+    k = next((c for c, keys in CATEGORIES if any(x in e.key for x in keys)), "other")
+    cat[k] = cat.get(k, 0) + t
+print("--- by category (ms/block)")
+for k, t in sorted(cat.items(), key=lambda kv: -kv[1]):
+    print(f"{t / 1e3 / nb:8.3f}  {100 * t / tot:5.1f}%  {k}")

@@ -483,3 +483,23 @@ def test_opm_fused_rejects_unsupported():
     assert not ops.opm_fused_supported(32, 32, 256, 32, 64)  # N_s > 128
     with pytest.raises(Exception):
         ops.opm_fused_fwd(t, t, torch.zeros(256, 64, device=DEV, dtype=torch.bfloat16), 32, 32, 32, 16, 64, 1.0)
+
+
+@pytest.mark.parametrize("rows,M,N", [(65536, 128, 392), (32768, 256, 64), (65536, 32, 128), (4096, 1024, 256), (256, 64, 256),
+                                      (1000, 64, 136)])
+def test_wgrad_accumulates(rows, M, N):
+    """evo_wgrad: dW += X^T dY in fp32 (split-K partials reduced in a fixed order) vs fp32 torch;
+    called twice onto a strided fp32 view it accumulates; bitwise repeatable."""
+    g = torch.Generator(device=DEV).manual_seed(rows + M + N)
+    x = torch.randn(rows, M, device=DEV, generator=g).bfloat16()
+    dy = torch.randn(rows, N, device=DEV, generator=g).bfloat16()
+    base = torch.randn(M, N + 8, device=DEV, generator=g)
+    dw = base.clone()[:, :N]
+    ref = base[:, :N] + 2 * (x.float().t() @ dy.float())
+    ops.wgrad(x, dy, dw)
+    ops.wgrad(x, dy, dw)
+    assert rel(dw, ref) < 1e-5, rel(dw, ref)
+    dw2 = base.clone()[:, :N]
+    ops.wgrad(x, dy, dw2)
+    ops.wgrad(x, dy, dw2)
+    assert torch.equal(dw, dw2)
