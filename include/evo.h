@@ -220,6 +220,22 @@ int evo_wgrad(const void* x, int64_t ldx, const void* dy, int64_t ldy, float* dw
 int evo_opm_fused_supported(int64_t I, int64_t J, int64_t S, int64_t P, int64_t Hz);
 int evo_opm_fused_fwd(const void* a_t, const void* b_t, const void* w_o, void* y, int64_t y_ld, void* o_save,
                       int64_t I, int64_t J, int64_t S, int64_t P, int64_t Hz, float alpha, void* stream);
+/* Backward of the fused OPM for one factor, without materialising do = dy W_o^T:
+ *   role 0:  da[s,i,p] = alpha sum_{j,q} b[s,j,q] do[i,j,p,q]    (x = i, y = j, other_t = b_t [J][P][N_s])
+ *   role 1:  db[s,j,q] = alpha sum_{i,p} a[s,i,p] do[i,j,p,q]    (x = j, y = i, other_t = a_t [I][P][N_s])
+ * with do[i,j,p,q] = sum_c dy[(i*J + j)*ldy + c] W_o[p*P+q, c] (X = extent of x, Y = of y).  Output
+ * element (s, x, p) at out + s*o_ss + (x / x_split)*o_sr + (x % x_split)*o_sx + p, bf16 (out_f32 = 0)
+ * or fp32 (the rank-major partial a DAP reduce-scatter takes).  Two tcgen05 GEMMs per 128-pair step
+ * (dy W^T into TMEM, converted to bf16 in shared memory, times the other factor) accumulating in
+ * TMEM; fp32 partials over y splits in workspace (evo_opm_bwd_workspace(X) bytes) summed in order.
+ * Supported extents: evo_opm_bwd_supported(I, J, N_s, P, Hz) (P = 32, N_s <= 128, I, J % 32 == 0,
+ * Hz in {64, 128}).  Replaces the backward of the einsum + matmul of evoformer.py:251-255. */
+int evo_opm_bwd_supported(int64_t I, int64_t J, int64_t S, int64_t P, int64_t Hz);
+int64_t evo_opm_bwd_workspace(int64_t X);
+int evo_opm_bwd_factor(int role, const void* dy, int64_t ldy, const void* w_o, const void* other_t,
+                       int64_t X, int64_t Y, int64_t S, int64_t P, int64_t Hz, float alpha, void* out, int out_f32,
+                       int64_t o_ss, int64_t o_sr, int64_t o_sx, int64_t x_split, void* workspace,
+                       int64_t workspace_bytes, void* stream);
 /* The OPM projections [N_s*R][ld] (rows (s, r); channels col0 .. col0+P, and col0+P .. col0+2P
  * when out_b != NULL) to the sequence-contiguous layout out[r][p][s] the fused kernel reads (bf16). */
 int evo_opm_transpose(const void* x, int64_t ld, int64_t col0, int64_t S, int64_t R, int64_t P, void* out_a,

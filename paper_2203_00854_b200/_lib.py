@@ -82,6 +82,10 @@ _SIGS = {
     "evo_wgrad": [vp, i64, vp, i64, vp, i64, i64, i64, i64, vp, i64, vp],
     "evo_opm_fused_supported": [i64, i64, i64, i64, i64],
     "evo_opm_fused_fwd": [vp, vp, vp, vp, i64, vp, i64, i64, i64, i64, i64, C.c_float, vp],
+    "evo_opm_bwd_supported": [i64, i64, i64, i64, i64],
+    "evo_opm_bwd_workspace": [i64],
+    "evo_opm_bwd_factor": [C.c_int, vp, i64, vp, vp, i64, i64, i64, i64, i64, C.c_float, vp, C.c_int, i64, i64, i64,
+                           i64, vp, i64, vp],
     "evo_opm_transpose": [vp, i64, i64, i64, i64, i64, vp, vp, vp],
     "evo_tri_gate_fwd": [vp, i64, C.c_int, C.c_int, vp, vp, vp],
     "evo_tri_gate_bwd": [vp, vp, vp, C.c_int, i64, C.c_int, C.c_int, vp, vp, vp],
@@ -140,7 +144,7 @@ def check(rc: int) -> None:
 
 
 # kernels launched per C-ABI call (evo_gated_attention_bwd = prep + main + dq finish [+ dbias reduce])
-LAUNCHES = {"evo_gated_attention_bwd": 3, "evo_bgemm_ws": 2, "evo_wgrad": 2}
+LAUNCHES = {"evo_gated_attention_bwd": 3, "evo_bgemm_ws": 2, "evo_wgrad": 2, "evo_opm_bwd_factor": 2}
 
 
 class Instrument:

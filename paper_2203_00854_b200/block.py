@@ -354,7 +354,8 @@ def opm_fwd(bp: BlockParams, m2d, z2d, S: int, R: int, save=True, b_full=None, R
         y = _mm(o.view(R * Rj, P * P), h["opm.w_o"])
     out = _residual_out(z2d, y, f["opm.b_o"], R * Rj, Hz, next_ln)
     sv = Saved(m=m2d, ln=ln, mean=mean, rstd=rstd, ab=ab, bsrc=bsrc, o=o, S=S, R=R, Rj=Rj,
-               gathered=gather is not None, b_seq=fused and gather is not None) if save else None
+               gathered=gather is not None, b_seq=fused and gather is not None,
+               a_t=a_t if fused else None, b_t=b_t if fused else None) if save else None
     return out, sv
 
 
@@ -380,8 +381,25 @@ def opm_bwd(bp: BlockParams, sv: Saved, dz_new, dm, reduce_scatter=None, next_db
     if not db_done:
         _dbias_only(dz_new, R * Rj, Hz, g["opm.b_o"])
     _wgrad(sv["o"].view(R * Rj, P * P), dz_new, g["opm.w_o"])
-    do = _mm(dz_new, h["opm.w_o"].t())                               # [R*Rj, P*P] == [i][j][p][q]
     dab = torch.empty(S * R, 2 * P, device=dz_new.device, dtype=BF16)
+    if sv.get("a_t") is not None and ops.opm_bwd_supported(R, Rj, S, P, Hz):
+        # evo_opm_bwd_factor: da and db straight from dz and W_o - do = dz W_o^T is never materialised
+        w_o = h["opm.w_o"]
+        if not sv["gathered"]:
+            ops.opm_bwd_factor(0, dz_new, w_o, sv["b_t"], R, Rj, S, P, Hz, 1.0 / S, dab, R * 2 * P, 0, 2 * P)
+            ops.opm_bwd_factor(1, dz_new, w_o, sv["a_t"], Rj, R, S, P, Hz, 1.0 / S, dab[:, P:], R * 2 * P, 0, 2 * P)
+        else:
+            # the gathered factor's rank-major fp32 partial first: its reduce-scatter overlaps da
+            nd = Rj // R
+            dbf = torch.empty(nd, S, R, P, device=dz_new.device, dtype=F32)
+            ops.opm_bwd_factor(1, dz_new, w_o, sv["a_t"], Rj, R, S, P, Hz, 1.0 / S, dbf, R * P, S * R * P, P,
+                               x_split=R)
+            pending = reduce_scatter(dbf, async_op=True)
+            ops.opm_bwd_factor(0, dz_new, w_o, sv["b_t"], R, Rj, S, P, Hz, 1.0 / S, dab, R * 2 * P, 0, 2 * P)
+            dab[:, P:].copy_(pending().view(S * R, P))
+        _opm_proj_bwd(bp, sv, dab, dm, next_db)
+        return
+    do = _mm(dz_new, h["opm.w_o"].t())                               # [R*Rj, P*P] == [i][j][p][q]
     ab = sv["ab"]                                                    # [a | b], or a alone under DAP
     dO_A = Mat(do, lo=(P, 1), split=(P, P), hi=(Rj * P * P, P * P))
     Cda = Mat(dab, lo=(1, R * 2 * P), split=(P, 0), hi=(2 * P, 0))
@@ -407,6 +425,13 @@ def opm_bwd(bp: BlockParams, sv: Saved, dz_new, dm, reduce_scatter=None, next_db
             Bb = Mat(sv["bsrc"], lo=(R * P, 1), split=(0, R * P), hi=(0, S * R * P))
         ops.bgemm(dO_A, Bb, Cda, 1, R * P, S, Rj * P, alpha=1.0 / S)
         dab[:, P:].copy_(pending().view(S * R, P))
+    _opm_proj_bwd(bp, sv, dab, dm, next_db)
+
+
+def _opm_proj_bwd(bp: BlockParams, sv: Saved, dab, dm, next_db):
+    """backward of the [a | b] projection and the OPM's input LayerNorm (dm accumulates)"""
+    Hm, S, R = bp.cfg.h_msa, sv["S"], sv["R"]
+    h, f, g = bp.h, bp.f, bp.g
     _wgrad(sv["ln"], dab, g["opm.w_ab"])
     _bgrad(dab, g["opm.b_ab"])
     dln = _mm(dab, h["opm.w_ab"].t())

@@ -379,6 +379,270 @@ __global__ void __launch_bounds__(256) opm_transpose_kernel(const bf16* __restri
   }
 }
 
+
+// ===================================================================================== backward
+// Gradients of the OPM factors without materialising do[i,j,p,q] = sum_c dy[i,j,c] W_o[pq,c]:
+//
+//   da[s,i,p] = alpha sum_{j,q} b[s,j,q] do[i,j,p,q]        db[s,j,q] = alpha sum_{i,p} a[s,i,p] do[i,j,p,q]
+//
+// are the same contraction with the roles of (i, p, a) and (j, q, b) exchanged, so one kernel runs
+// both (the caller swaps the tensor maps).  In da's terms: a unit = (32 x-rows [i], 4 p of a chunk,
+// a range of y [j]); per step of 4 y (128 (y, x) pairs):
+//   GEMM_A   D_A[(y_l, x_l)][(p_l, q)] = dy[(x, y)][c] . W[(p_l, q)][c]^T        M = 128 pairs, N = 128, K = Hz
+//   convert  D_A -> bf16 shared memory, rows (p_l, x_l), K = (y_l, q) (128-byte swizzle, conflict-free)
+//   GEMM_B   acc[(p_l, x_l)][s] += A_B . other[y][q][s]^T                        M = 128, N = N_s, K = 128
+// acc stays in TMEM over the unit's y range and leaves as fp32 partials [split][x][p][s];
+// opm_bwd_finish sums the splits in order, scales by alpha and writes the factor gradient in the
+// projection's row layout (or the rank-major layout a DAP reduce-scatter takes).
+constexpr int OB_THREADS = 384;
+constexpr uint32_t OB_T = 128 * 64 * 2;  // one 128-row x 64-element swizzle column: 16 KB
+
+struct OpmBwdArgs {
+  int X, Y, S, units_x, units, nsplit, ysteps_per_split, hz_halves;
+  float* part;  // [nsplit][X][P][128] fp32
+};
+
+__global__ void __launch_bounds__(OB_THREADS, 1)
+    opm_bwd_contract_kernel(const __grid_constant__ CUtensorMap tmDY, const __grid_constant__ CUtensorMap tmW,
+                            const __grid_constant__ CUtensorMap tmO, OpmBwdArgs g) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t w_full, w_empty, dy_full[2], dy_empty[2], ot_full[2], ot_empty[2], da_full[2], da_empty[2],
+      ab_full[2], ab_empty[2], acc_full, acc_empty;
+  __shared__ uint32_t tmem_sh;
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t sW = sbase, sDY = sW + 2 * OB_T, sOT = sDY + 4 * OB_T, sAB = sOT + 4 * OB_T;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int HH = g.hz_halves;  // Hz / 64: K of GEMM_A in 64-element swizzle columns
+
+  if (threadIdx.x == 0) {
+    mbar_init(&w_full, 1);
+    mbar_init(&w_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&dy_full[i], 1);
+      mbar_init(&dy_empty[i], 1);
+      mbar_init(&ot_full[i], 1);
+      mbar_init(&ot_empty[i], 1);
+      mbar_init(&da_full[i], 1);
+      mbar_init(&da_empty[i], 128);
+      mbar_init(&ab_full[i], 128);
+      mbar_init(&ab_empty[i], 1);
+    }
+    mbar_init(&acc_full, 1);
+    mbar_init(&acc_empty, 128);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(&tmem_sh, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_sh;  // D_A[b] at b*128, acc at 256
+
+  auto decode = [&](int u, int& x0, int& p0, int& sp) {
+    x0 = (u % g.units_x) * 32;
+    const int r = u / g.units_x;
+    p0 = (r % 8) * 4;
+    sp = r / 8;
+  };
+  auto ysteps = [&](int sp) {
+    const int y_total = g.Y / 4, lo = sp * g.ysteps_per_split;
+    const int hi = lo + g.ysteps_per_split < y_total ? lo + g.ysteps_per_split : y_total;
+    return hi > lo ? hi - lo : 0;
+  };
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const uint64_t mdy = reinterpret_cast<uint64_t>(&tmDY), mw = reinterpret_cast<uint64_t>(&tmW),
+                     mo = reinterpret_cast<uint64_t>(&tmO);
+      int st = 0, it = 0;
+      for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++it) {
+        int x0, p0, sp;
+        decode(u, x0, p0, sp);
+        const int n = ysteps(sp), y0 = sp * g.ysteps_per_split * 4;
+        mbar_wait(&w_empty, (it & 1) ^ 1);
+        mbar_expect_tx(&w_full, HH * OB_T);
+        for (int hh = 0; hh < HH; ++hh) tma_ld3(sW + hh * OB_T, mw, hh * 64, 0, p0, smem_u32(&w_full));
+        for (int t = 0; t < n; ++t, ++st) {
+          const int b = st & 1;
+          const uint32_t ph = ((st >> 1) & 1) ^ 1;
+          const int yb = y0 + t * 4;
+          mbar_wait(&dy_empty[b], ph);
+          mbar_expect_tx(&dy_full[b], HH * OB_T);
+          for (int hh = 0; hh < HH; ++hh)
+            tma_ld3(sDY + (2 * b + hh) * OB_T, mdy, hh * 64, x0, yb, smem_u32(&dy_full[b]));
+          mbar_wait(&ot_empty[b], ph);
+          mbar_expect_tx(&ot_full[b], 2 * OB_T);
+          for (int sh = 0; sh < 2; ++sh)
+            tma_ld3(sOT + (2 * b + sh) * OB_T, mo, sh * 64, 0, yb, smem_u32(&ot_full[b]));
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t IDA = make_idesc_bf16(128, 128, 0, 0);  // dy (K-major) x W (K-major)
+    constexpr uint32_t IDB = make_idesc_bf16(128, 128, 0, 1);  // A_B (K-major) x other (MN-major over s)
+    int st = 0, it = 0;
+    for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++it) {
+      int x0, p0, sp;
+      decode(u, x0, p0, sp);
+      const int n = ysteps(sp);
+      mbar_wait(&w_full, it & 1);
+      for (int t = 0; t <= n; ++t) {
+        if (t < n) {  // GEMM_A of step t
+          const int s_ = st + t, b = s_ & 1;
+          mbar_wait(&dy_full[b], (s_ >> 1) & 1);
+          mbar_wait(&da_empty[b], ((s_ >> 1) & 1) ^ 1);
+          tc_fence_after();
+          if (lane == 0) {
+            for (int kk = 0; kk < 4 * HH; ++kk) {
+              const uint32_t off = (kk >> 2) * OB_T + (kk & 3) * 32;
+              mma_bf16(tmem + b * 128, sdesc(sDY + 2 * b * OB_T + off, 16, 1024, 2), sdesc(sW + off, 16, 1024, 2),
+                       IDA, kk != 0);
+            }
+            mma_commit(&dy_empty[b]);
+            mma_commit(&da_full[b]);
+            if (t == n - 1) mma_commit(&w_empty);
+          }
+          __syncwarp();
+        }
+        if (t > 0) {  // GEMM_B of step t-1 (its conversion overlapped GEMM_A of step t)
+          const int s_ = st + t - 1, b = s_ & 1;
+          if (t == 1) mbar_wait(&acc_empty, (it & 1) ^ 1);
+          mbar_wait(&ab_full[b], (s_ >> 1) & 1);
+          mbar_wait(&ot_full[b], (s_ >> 1) & 1);
+          tc_fence_after();
+          if (lane == 0) {
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+              const uint64_t ad = sdesc(sAB + (2 * b + (kk >> 2)) * OB_T + (kk & 3) * 32, 16, 1024, 2);
+              const uint64_t bd = sdesc(sOT + 2 * b * OB_T + kk * 2048, OB_T, 1024, 2);
+              mma_bf16(tmem + 256, ad, bd, IDB, (t > 1 || kk > 0) ? 1u : 0u);
+            }
+            mma_commit(&ab_empty[b]);
+            mma_commit(&ot_empty[b]);
+            if (t == n) mma_commit(&acc_full);
+          }
+          __syncwarp();
+        }
+      }
+      if (n == 0 && lane == 0) mma_commit(&w_empty);
+      st += n;
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ------------------------------------------------------------ converter: D_A -> A_B
+    const int yq = warp & 3;  // lane quarter = y_l of the pairs; lane = x_l
+    int st = 0;
+    for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
+      int x0, p0, sp;
+      decode(u, x0, p0, sp);
+      const int n = ysteps(sp);
+      for (int t = 0; t < n; ++t, ++st) {
+        const int b = st & 1;
+        const uint32_t ph = (st >> 1) & 1;
+        mbar_wait(&da_full[b], ph);
+        tc_fence_after();
+        mbar_wait(&ab_empty[b], ph ^ 1);
+        const uint32_t ab = sAB + (2 * b + (yq >> 1)) * OB_T;
+#pragma unroll
+        for (int pp = 0; pp < 4; pp += 2) {
+          float v[64];
+          tmem_ld32(tmem + b * 128 + ((uint32_t)(yq * 32) << 16) + pp * 32, v);
+          tmem_ld32(tmem + b * 128 + ((uint32_t)(yq * 32) << 16) + pp * 32 + 32, v + 32);
+          tmem_ld_wait();
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = (pp + h) * 32 + lane;  // row (p_l, x_l)
+            const uint32_t row = ab + r * 128;
+#pragma unroll
+            for (int t4 = 0; t4 < 4; ++t4) {
+              const int ch = ((yq & 1) * 4 + t4) ^ (r & 7);
+              const float* w = v + h * 32 + t4 * 8;
+              st_shared_v4(row + ch * 16, pack_bf16x2(w[0], w[1]), pack_bf16x2(w[2], w[3]), pack_bf16x2(w[4], w[5]),
+                           pack_bf16x2(w[6], w[7]));
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&da_empty[b]);
+        fence_async_smem();
+        mbar_arrive(&ab_full[b]);
+      }
+    }
+  } else if (warp >= 8) {
+    // ------------------------------------------------------------ epilogue: acc -> fp32 partials
+    const int pq = warp & 3;  // lane quarter = p_l; lane = x_l
+    int it = 0;
+    for (int u = blockIdx.x; u < g.units; u += gridDim.x, ++it) {
+      int x0, p0, sp;
+      decode(u, x0, p0, sp);
+      const int n = ysteps(sp);
+      float* dst = g.part + (((int64_t)sp * g.X + x0 + lane) * 32 + p0 + pq) * 128;
+      if (n == 0) {  // an empty y range contributes zeros
+        for (int c0 = 0; c0 < 128; c0 += 4) *reinterpret_cast<float4*>(dst + c0) = make_float4(0.f, 0.f, 0.f, 0.f);
+        continue;
+      }
+      mbar_wait(&acc_full, it & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c0 = 0; c0 < 128; c0 += 32) {
+        float v[32];
+        tmem_ld32(tmem + 256 + ((uint32_t)(pq * 32) << 16) + c0, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 32; e += 4)
+          *reinterpret_cast<float4*>(dst + c0 + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+      }
+      tc_fence_before();
+      mbar_arrive(&acc_empty);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc(tmem, 512);
+}
+
+// out(s, x, p) = alpha * sum_split part[split][x][p][s]  for s < S: one CTA per x, the [P][S] slab
+// transposed through shared memory; out element (s, x, p) at
+//   out + s*o_ss + (x / x_split)*o_sr + (x % x_split)*o_sx + p   (bf16 or fp32)
+template <typename TO>
+__global__ void __launch_bounds__(256) opm_bwd_finish(const float* __restrict__ part, int nsplit, int X, int S,
+                                                      float alpha, TO* __restrict__ out, int64_t o_ss, int64_t o_sr,
+                                                      int64_t o_sx, int x_split) {
+  __shared__ float t[32][129];
+  const int x = blockIdx.x;
+  // the [32 p][128 s] slab: 4 float4 per thread and split, every load of a thread in flight
+  float4 acc[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (k < nsplit) {
+      const float4* src = reinterpret_cast<const float4*>(part + ((int64_t)k * X + x) * 32 * 128);
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldcs(src + threadIdx.x + u * 256);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        acc[u].x += v[u].x; acc[u].y += v[u].y; acc[u].z += v[u].z; acc[u].w += v[u].w;
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int i = (threadIdx.x + u * 256) * 4, p = i >> 7, sq = i & 127;
+    t[p][sq] = alpha * acc[u].x;
+    t[p][sq + 1] = alpha * acc[u].y;
+    t[p][sq + 2] = alpha * acc[u].z;
+    t[p][sq + 3] = alpha * acc[u].w;
+  }
+  __syncthreads();
+  TO* base = out + (int64_t)(x / x_split) * o_sr + (int64_t)(x % x_split) * o_sx;
+  for (int i = threadIdx.x; i < S * 32; i += 256) {  // lanes = consecutive p: coalesced rows
+    const int sq = i >> 5, p = i & 31;
+    stf<TO>(base + (int64_t)sq * o_ss + p, t[p][sq]);
+  }
+}
+
 bool encode(CUtensorMap* map, const void* ptr, int nd, const cuuint64_t* dims, const cuuint64_t* strides_bytes,
             const cuuint32_t* box, CUtensorMapSwizzle sw) {
   EncodeTiledFn enc = encode_tiled();
@@ -499,4 +763,93 @@ extern "C" int evo_opm_transpose(const void* x, int64_t ld, int64_t col0, int64_
       static_cast<const bf16*>(x), ld, col0, (int)S, (int)R, (int)P, static_cast<bf16*>(out_a), static_cast<bf16*>(out_b));
   EVO_LAUNCH_CHECK("opm_transpose launch");
   return EVO_OK;
+}
+
+extern "C" int evo_opm_bwd_supported(int64_t I, int64_t J, int64_t S, int64_t P, int64_t Hz) {
+  return P == 32 && S >= 8 && S <= 128 && S % 8 == 0 && I >= 32 && I % 32 == 0 && J >= 32 && J % 32 == 0 &&
+         (Hz == 64 || Hz == 128);
+}
+
+// role 0: da (x = i over a's rows, y = j, other = b_t);  role 1: db (x = j, y = i, other = a_t, W with
+// (p, q) exchanged)
+static int opm_bwd_one(int role, const void* dy, int64_t ldy, const void* w_o, const void* other_t, int64_t X,
+                       int64_t Y, int64_t S, int64_t Hz, float alpha, void* out, int out_f32, int64_t o_ss,
+                       int64_t o_sr, int64_t o_sx, int64_t x_split, float* part, int nsplit, cudaStream_t st) {
+  using namespace evo;
+  CUtensorMap tdy, tw, to;
+  const int64_t I = role == 0 ? X : Y, J = role == 0 ? Y : X;
+  {  // dy (i, j, c) at (i*J + j)*ldy + c: dims {c, x, y}, box [64 c][32 x][4 y] -> rows (y_l, x_l)
+    const int64_t sx = role == 0 ? J * ldy : ldy, sy = role == 0 ? ldy : J * ldy;
+    cuuint64_t d[3] = {(cuuint64_t)Hz, (cuuint64_t)X, (cuuint64_t)Y};
+    cuuint64_t s[2] = {(cuuint64_t)sx * 2, (cuuint64_t)sy * 2};
+    cuuint32_t bx[3] = {64, 32, 4};
+    EVO_CHECK_ARG(encode(&tdy, dy, 3, d, s, bx, CU_TENSOR_MAP_SWIZZLE_128B), EVO_ERR_ARG, "opm_bwd: dy map");
+    (void)I;
+  }
+  {  // W rows (chunk-dim index, inner index): da (p, q) -> row p*32+q; db (q, p) -> row p*32+q
+    const int64_t s_in = role == 0 ? Hz : 32 * Hz, s_ch = role == 0 ? 32 * Hz : Hz;
+    cuuint64_t d[3] = {(cuuint64_t)Hz, 32, 32};
+    cuuint64_t s[2] = {(cuuint64_t)s_in * 2, (cuuint64_t)s_ch * 2};
+    cuuint32_t bx[3] = {64, 32, 4};
+    EVO_CHECK_ARG(encode(&tw, w_o, 3, d, s, bx, CU_TENSOR_MAP_SWIZZLE_128B), EVO_ERR_ARG, "opm_bwd: W map");
+  }
+  {  // other [y][q][s]: box [64 s][32 q][4 y]
+    cuuint64_t d[3] = {(cuuint64_t)S, 32, (cuuint64_t)Y};
+    cuuint64_t s[2] = {(cuuint64_t)S * 2, (cuuint64_t)32 * S * 2};
+    cuuint32_t bx[3] = {64, 32, 4};
+    EVO_CHECK_ARG(encode(&to, other_t, 3, d, s, bx, CU_TENSOR_MAP_SWIZZLE_128B), EVO_ERR_ARG, "opm_bwd: other map");
+  }
+  OpmBwdArgs a;
+  a.X = (int)X;
+  a.Y = (int)Y;
+  a.S = (int)S;
+  a.units_x = (int)(X / 32);
+  a.nsplit = nsplit;
+  a.ysteps_per_split = (int)((Y / 4 + nsplit - 1) / nsplit);
+  a.units = a.units_x * 8 * nsplit;
+  a.hz_halves = (int)(Hz / 64);
+  a.part = part;
+  constexpr size_t smem = 2 * OB_T + 4 * OB_T + 4 * OB_T + 4 * OB_T;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(opm_bwd_contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_status(e, "opm_bwd attr");
+    attr = true;
+  }
+  const int grid = a.units < sm_count() ? a.units : sm_count();
+  opm_bwd_contract_kernel<<<grid, OB_THREADS, smem, st>>>(tdy, tw, to, a);
+  EVO_LAUNCH_CHECK("opm_bwd contract launch");
+  if (out_f32)
+    opm_bwd_finish<float><<<(unsigned)X, 256, 0, st>>>(part, nsplit, (int)X, (int)S, alpha, static_cast<float*>(out),
+                                                       o_ss, o_sr, o_sx, (int)x_split);
+  else
+    opm_bwd_finish<bf16><<<(unsigned)X, 256, 0, st>>>(part, nsplit, (int)X, (int)S, alpha, static_cast<bf16*>(out),
+                                                      o_ss, o_sr, o_sx, (int)x_split);
+  EVO_LAUNCH_CHECK("opm_bwd finish launch");
+  return EVO_OK;
+}
+
+extern "C" int64_t evo_opm_bwd_workspace(int64_t X) { return 4 * X * 32 * 128 * 4; }
+
+extern "C" int evo_opm_bwd_factor(int role, const void* dy, int64_t ldy, const void* w_o, const void* other_t,
+                                  int64_t X, int64_t Y, int64_t S, int64_t P, int64_t Hz, float alpha, void* out,
+                                  int out_f32, int64_t o_ss, int64_t o_sr, int64_t o_sx, int64_t x_split,
+                                  void* workspace, int64_t ws_bytes, void* stream) {
+  using namespace evo;
+  EVO_CHECK_ARG(role == 0 || role == 1, EVO_ERR_ARG, "opm_bwd_factor: role must be 0 (da) or 1 (db)");
+  EVO_CHECK_ARG(dy && w_o && other_t && out && workspace, EVO_ERR_ARG, "opm_bwd_factor: null operand");
+  EVO_CHECK_ARG(evo_opm_bwd_supported(role == 0 ? X : Y, role == 0 ? Y : X, S, P, Hz), EVO_ERR_SHAPE,
+                "opm_bwd_factor: unsupported extents X=%lld Y=%lld S=%lld P=%lld Hz=%lld", (long long)X, (long long)Y,
+                (long long)S, (long long)P, (long long)Hz);
+  EVO_CHECK_ARG(ws_bytes >= evo_opm_bwd_workspace(X) && ldy % 8 == 0 && x_split >= 1, EVO_ERR_ARG,
+                "opm_bwd_factor: workspace too small or bad strides");
+  EVO_CHECK_ARG((((uintptr_t)dy | (uintptr_t)w_o | (uintptr_t)other_t | (uintptr_t)workspace) & 15) == 0,
+                EVO_ERR_ALIGN, "opm_bwd_factor: operands must be 16-byte aligned");
+  // y splits so the units (x blocks x 8 p-chunks x splits) fill one wave
+  // ONE wave: a second partial wave would double the time of the CTAs it lands on
+  int ns = (int)(sm_count() / (X / 32 * 8));
+  if (ns > 4) ns = 4;
+  while (ns > 1 && (Y / 4) / ns < 4) --ns;
+  return opm_bwd_one(role, dy, ldy, w_o, other_t, X, Y, S, Hz, alpha, out, out_f32, o_ss, o_sr, o_sx, x_split,
+                     static_cast<float*>(workspace), ns < 1 ? 1 : ns, (cudaStream_t)stream);
 }

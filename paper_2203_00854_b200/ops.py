@@ -321,6 +321,24 @@ def wgrad(x, dy, dw):
     return dw
 
 
+def opm_bwd_supported(I, J, S, P, Hz) -> bool:
+    return bool(_lib.load().evo_opm_bwd_supported(I, J, S, P, Hz))
+
+
+def opm_bwd_factor(role, dy, w_o, other_t, X, Y, S, P, Hz, alpha, out, o_ss, o_sr, o_sx, x_split=None):
+    """one factor gradient of the fused OPM (evo_opm_bwd_factor): role 0 -> da (x = i, other = b_t),
+    role 1 -> db (x = j, other = a_t); out element (s, x, p) at
+    out[s*o_ss + (x // x_split)*o_sr + (x % x_split)*o_sx + p] (out bf16 or fp32)."""
+    _cuda(dy, w_o, other_t, out)
+    ws_bytes = int(_lib.load().evo_opm_bwd_workspace(X))
+    ws = torch.empty(ws_bytes // 4, device=dy.device, dtype=torch.float32)
+    call("evo_opm_bwd_factor", role, _p(dy), dy.stride(0), _p(w_o), _p(other_t), X, Y, S, P, Hz, float(alpha),
+         _p(out), 1 if out.dtype == torch.float32 else 0, o_ss, o_sr, o_sx, X if x_split is None else x_split,
+         _p(ws), ws_bytes, stream_handle(),
+         work=(4 * X * Y * P * P * (Hz + S), 2 * (X * Y * Hz * P // 4 + P * P * Hz + Y * P * S)))
+    return out
+
+
 # ------------------------------------------------------------------ elementwise epilogues
 
 def tri_gate_fwd(y, rows, hz, p, a_cm, b_cm):

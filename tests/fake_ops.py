@@ -174,6 +174,29 @@ def count_nonfinite(x) -> int:
     return int((~torch.isfinite(x)).sum())
 
 
+def opm_bwd_supported(I, J, S, P, Hz):
+    return P == 32 and 8 <= S <= 128 and S % 8 == 0 and I % 32 == 0 and I >= 32 and J % 32 == 0 and J >= 32 and \
+        Hz in (64, 128)
+
+
+def opm_bwd_factor(role, dy, w_o, other_t, X, Y, S, P, Hz, alpha, out, o_ss, o_sr, o_sx, x_split=None):
+    x_split = X if x_split is None else x_split
+    I, J = (X, Y) if role == 0 else (Y, X)
+    do = (dy.float() @ w_o.float().t()).to(dy.dtype).float().view(I, J, P, P)
+    oth = other_t.float()                       # [Y][P][S]
+    if role == 0:
+        g = alpha * torch.einsum("ijpq,jqs->sip", do, oth)       # da [S, X, P]
+    else:
+        g = alpha * torch.einsum("ijpq,ips->sjq", do, oth)       # db [S, X, P]
+    CALLS["opm_bwd_factor"] += 1
+    flat = _flat(out)  # absolute storage offsets
+    for x in range(X):
+        off = out.storage_offset() + (x // x_split) * o_sr + (x % x_split) * o_sx
+        idx = off + torch.arange(S)[:, None] * o_ss + torch.arange(P)[None, :]
+        flat[idx.reshape(-1)] = g[:, x, :].reshape(-1).to(out.dtype)
+    return out
+
+
 def opm_fused_supported(I, J, S, P, Hz):
     return P == 32 and 8 <= S <= 128 and S % 8 == 0 and I % 32 == 0 and I >= 32 and J % 8 == 0 and J >= 8 and \
         Hz in (32, 64, 128)
@@ -185,7 +208,7 @@ def opm_transpose(x, S, R, P, col0=0, both=False):
     return (a, v[..., P:].permute(1, 2, 0).contiguous()) if both else a
 
 
-CALLS = {"opm_fused_fwd": 0}
+CALLS = {"opm_fused_fwd": 0, "opm_bwd_factor": 0}
 
 
 def opm_fused_fwd(a_t, b_t, w_o, I, J, S, P, Hz, alpha, y=None, o_save=None):
@@ -299,7 +322,7 @@ def gate_mul(gate, y=None, bias=None, act=1, rows=None, cols=None, gate_rs=None,
 
 
 NAMES = ["gate_mul", "layernorm_fwd", "layernorm_bwd", "layernorm_rowdot_fwd", "attention_desc", "attention_fwd",
-         "attention_bwd_workspace", "attention_bwd", "bgemm", "softmax_fwd", "count_nonfinite", "opm_fused_supported", "opm_transpose",
+         "attention_bwd_workspace", "attention_bwd", "bgemm", "softmax_fwd", "count_nonfinite", "opm_fused_supported", "opm_transpose", "opm_bwd_supported", "opm_bwd_factor",
          "opm_fused_fwd", "tri_gate_fwd", "tri_gate_bwd",
          "gated_residual_fwd", "gated_residual_bwd", "bias_act_fwd", "bias_act_bwd"]
 

@@ -23,7 +23,7 @@ from paper_2203_00854_b200.config import EvoConfig, init_block_params, synthetic
 CFG = EvoConfig(16, 32, 64, 32, 2, 1, 16)
 # hidden_proj 32 and R_loc % 32 == 0 at world 2: the OPM takes the fused-kernel host path (sequence-contiguous
 # projections, gathered [J, P, S] b, the backward's b_seq operand)
-CFG_FUSED_OPM = EvoConfig(16, 64, 64, 32, 2, 1, 32)
+CFG_FUSED_OPM = EvoConfig(16, 64, 64, 64, 2, 1, 32)
 
 
 def _port():
@@ -101,7 +101,7 @@ def _worker(rank, world, port, dims=None):
                     _rel(bp.grad, ref.grad)]
             assert max(errs[:2]) <= 1e-2 and max(errs[2:]) <= 2e-2, errs
             if dims:  # the fused-OPM host path ran (sharded and single-device)
-                assert fake_ops.CALLS["opm_fused_fwd"] >= 2, fake_ops.CALLS
+                assert fake_ops.CALLS["opm_fused_fwd"] >= 2 and fake_ops.CALLS["opm_bwd_factor"] >= 4, fake_ops.CALLS
     finally:
         dist.destroy_process_group()
 

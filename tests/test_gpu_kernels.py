@@ -503,3 +503,32 @@ def test_wgrad_accumulates(rows, M, N):
     ops.wgrad(x, dy, dw2)
     ops.wgrad(x, dy, dw2)
     assert torch.equal(dw, dw2)
+
+
+@pytest.mark.parametrize("I,J,S,Hz", [(32, 32, 16, 64), (64, 32, 128, 128), (32, 96, 96, 128), (256, 256, 128, 128)])
+def test_opm_bwd_factor(I, J, S, Hz):
+    """evo_opm_bwd_factor vs fp32 torch: da = alpha einsum(ijpq,sjq->sip), db = alpha einsum(ijpq,sip->sjq) with
+    do = bf16(dy W_o^T) (what the unfused path stores); da written bf16 into columns [0, P) of the [S*I, 2P]
+    projection-gradient buffer, db fp32 in the rank-major layout a DAP reduce-scatter takes (2 ranks)."""
+    P = 32
+    g = torch.Generator(device=DEV).manual_seed(I + 3 * J + S + Hz)
+    a = torch.randn(S, I, P, device=DEV, generator=g).bfloat16()
+    b = torch.randn(S, J, P, device=DEV, generator=g).bfloat16()
+    w = (torch.randn(P * P, Hz, device=DEV, generator=g) / 32).bfloat16()
+    dy = torch.randn(I * J, Hz, device=DEV, generator=g).bfloat16()
+    a_t, b_t = a.permute(1, 2, 0).contiguous(), b.permute(1, 2, 0).contiguous()
+    al = 1.0 / S
+    do = (dy.float() @ w.float().t()).bfloat16().float().view(I, J, P, P)
+    da_ref = al * torch.einsum("ijpq,sjq->sip", do, b.float())
+    db_ref = al * torch.einsum("ijpq,sip->sjq", do, a.float())
+    assert ops.opm_bwd_supported(I, J, S, P, Hz)
+    dab = torch.zeros(S, I, 2 * P, device=DEV, dtype=torch.bfloat16)
+    ops.opm_bwd_factor(0, dy, w, b_t, I, J, S, P, Hz, al, dab, I * 2 * P, 0, 2 * P)
+    Jl = J // 2
+    dbf = torch.empty(2, S, Jl, P, device=DEV)  # [rank][s][j_local][q]
+    ops.opm_bwd_factor(1, dy, w, a_t, J, I, S, P, Hz, al, dbf, Jl * P, S * Jl * P, P, x_split=Jl)
+    torch.cuda.synchronize()
+    assert rel(dab[..., :P], da_ref) < 5e-3, rel(dab[..., :P], da_ref)
+    assert torch.count_nonzero(dab[..., P:]) == 0  # the other half of the buffer untouched
+    db = torch.cat([dbf[0], dbf[1]], dim=1)
+    assert rel(db, db_ref) < 1e-4, rel(db, db_ref)
