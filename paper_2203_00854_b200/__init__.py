@@ -4,8 +4,10 @@ Drop-in for the reference package's Evoformer block / module API
 (/root/reference/pkg/src/evoplan/__init__.py:13-72, hot-path subset):
 ``EvoConfig``, ``param_shapes``, ``init_block_params``, ``params_to_json``,
 ``params_from_json``, ``evoformer_block`` and its sub-modules,
-``dap_evoformer_block`` with ``DeviceMesh`` / ``CommLedger``, and the
-reference's exception classes.  Compute runs in libevo.so (sm_100a CUDA,
+``dap_evoformer_block`` with ``DeviceMesh`` / ``CommLedger``, the reference's
+exception classes, the GPU executor of the reference's AutoChunk plans
+(``execute_chunked`` with ``graph_from_json`` / ``plan_from_json``) and the
+measured overlap timeline (``simulate_schedule``, ``measure_dap_forward``).  Compute runs in libevo.so (sm_100a CUDA,
 include/evo.h); there is no CPU fallback.
 """
 
@@ -43,4 +45,12 @@ def __getattr__(name):
     if name in ("dap_evoformer_block", "DeviceMesh", "CommLedger", "predict_block_ledger", "dap_block"):
         from . import dap
         return getattr(dap, name)
+    if name in ("execute_chunked", "graph_from_json", "graph_to_json", "plan_from_json", "plan_to_json",
+                "ByteTracker"):
+        from . import autochunk
+        return getattr(autochunk, name)
+    if name in ("TimelineEvent", "simulate_schedule", "events_from_json", "events_to_json", "measure_dap_forward",
+                "overlap_report"):
+        from . import timeline
+        return getattr(timeline, name)
     raise AttributeError(name)
