@@ -17,13 +17,31 @@
 //            over the batch (msa_row) copies the dS^T smem tile to a bf16 workspace with
 //            16-byte stores and attn_dbias_reduce sums it over the batch (deterministic)
 //   finish dq = bf16(dQ accumulator)
+#include <cstdlib>
+#include <cstring>
+
 #include "attn.cuh"
+#include "tma.cuh"
 
 #ifndef EVO_EXP
 #define EVO_EXP 0
 #endif
 
 namespace evo {
+
+#if EVO_EXP == 10 || EVO_EXP == 11
+__device__ unsigned long long g_bwd_trace[8192];
+#define BTRACE(i)                                                                              \
+  do {                                                                                         \
+    if (blockIdx.x == 0 && (threadIdx.x == 0 || threadIdx.x == 128) && (i) < 4096) {           \
+      unsigned long long t_;                                                                   \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                   \
+      g_bwd_trace[(threadIdx.x == 128 ? 4096 : 0) + (i)] = t_;                                 \
+    }                                                                                          \
+  } while (0)
+#else
+#define BTRACE(i) (void)0
+#endif
 
 
 struct AttnBwdParams {
@@ -115,6 +133,25 @@ __global__ void __launch_bounds__(256) attn_bias_transpose(const bf16* __restric
     if (q < L && k < L) bias_t[((int64_t)h * L + k) * L + q] = tile[tx][r];
   }
 }
+
+// 64-byte-swizzled operand tiles (TMA path, head dim 32): [128 rows][32 elements], 8-row atoms of 512 B.
+// K-major read (k = the 32 channels): k-step of 16 = +32 B inside the row; MN-major view of the same
+// tile (mn = channels, k = rows): k-step of 16 rows = +1024 B
+__device__ __forceinline__ uint64_t bw_sw64_k(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | (1ull << 16) | ((uint64_t)(512 >> 4) << 32) | (1ull << 46) | (4ull << 61);
+}
+__device__ __forceinline__ uint64_t bw_sw64_mn(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(4096 >> 4) << 16) | ((uint64_t)(512 >> 4) << 32) |
+         (1ull << 46) | (4ull << 61);
+}
+__device__ __forceinline__ void bulk_ld(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(dst), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+struct BwdMaps {  // tensor maps of the per-tile operands (TMA path): element (d, h, l, b)
+  CUtensorMap q, k, v, dO;
+};
 
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
   uint32_t* r = reinterpret_cast<uint32_t*>(v);
@@ -289,11 +326,12 @@ __device__ __forceinline__ void bw_load(uint32_t sdst, const bf16* base, int64_t
 // over the batch with dS stored for the batch reduction (msa_row), 3 = generic full bias
 // (fp32 atomics).  Specialised so the per-element loop carries no dead predicated paths.
 template <int CP, int MODE>
-__global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int nkt, int dq_partial) {
+__global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int nkt, int dq_partial,
+                                                          const __grid_constant__ BwdMaps maps, int tmaq) {
   constexpr bool BIASS = MODE == 2 && CP <= 32;
   using SM = BwdSmem<CP, BIASS>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bar1, bar2;
+  __shared__ uint64_t bar1, bar2, tbar[2];
   __shared__ uint32_t tmem_sh;
   const uint32_t sb = smem_u32(smem);
   constexpr bool PTM = SM::PTM;
@@ -318,21 +356,45 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
   if (threadIdx.x == 0) {
     mbar_init(&bar1, 1);
     mbar_init(&bar2, 1);
+    mbar_init(&tbar[0], 1);
+    mbar_init(&tbar[1], 1);
     fence_mbar_init();
   }
+  __syncthreads();  // the TMA path issues into tbar right below
+  uint32_t t_par = 0;  // TMA path: completion parity of tbar[0] / tbar[1] in bits 0 / 1 (uniform over threads)
   const int64_t HC = (int64_t)H * c;
   // every per-tile operand is a cp.async copy (dO, D and lse*log2e come from the prep kernel)
   const bool vec_stats = (L & 3) == 0;
   auto issue_loads = [&](int64_t b, int h, int k0, int qt, bool with_kv, int buf) {
     const int q0 = qt * BW_BQ;
-    if (with_kv) {
-      bw_load<CP>(sb + SM::K, F.k + b * F.k_sb + (int64_t)h * c, F.k_sl, k0, L - k0, c);
-      bw_load<CP>(sb + SM::V, F.v + b * F.v_sb + (int64_t)h * c, F.v_sl, k0, L - k0, c);
-    }
-    bw_load<CP>(sb + SM::Q + buf * SM::QD_BYTES, F.q + b * F.q_sb + (int64_t)h * c, F.q_sl, q0, L - q0, c);
-    bw_load<CP>(sb + SM::DO + buf * SM::QD_BYTES, P.dO + b * L * HC + (int64_t)h * c, HC, q0, L - q0, c);
     const int64_t st0 = (b * H + h) * (int64_t)L + q0;
     const uint32_t lse_b = SM::LSE + buf * BW_BQ * 4, dd_b = SM::DD + buf * BW_BQ * 4;
+    if (tmaq) {
+      // one thread: K/V (first tile of a unit), Q, dO by tensor maps (64-byte swizzle), lse / D rows
+      // by bulk copies; all of it completes on tbar[buf] (no per-thread cp.async address streams)
+      if (threadIdx.x == 0) {
+        const uint32_t tile = 128 * 32 * 2, vec = BW_BQ * 4;
+        const int nq = L - q0 < BW_BQ ? L - q0 : BW_BQ;
+        mbar_expect_tx(&tbar[buf], (with_kv ? 4 : 2) * tile + 2 * (uint32_t)nq * 4);
+        const uint32_t br = smem_u32(&tbar[buf]);
+        if (with_kv) {
+          tma_ld4(sb + SM::K, reinterpret_cast<uint64_t>(&maps.k), 0, h, k0, (int)b, br);
+          tma_ld4(sb + SM::V, reinterpret_cast<uint64_t>(&maps.v), 0, h, k0, (int)b, br);
+        }
+        tma_ld4(sb + SM::Q + buf * SM::QD_BYTES, reinterpret_cast<uint64_t>(&maps.q), 0, h, q0, (int)b, br);
+        tma_ld4(sb + SM::DO + buf * SM::QD_BYTES, reinterpret_cast<uint64_t>(&maps.dO), 0, h, q0, (int)b, br);
+        bulk_ld(sb + lse_b, P.lse2 + st0, (uint32_t)nq * 4, &tbar[buf]);
+        bulk_ld(sb + dd_b, P.Dsum + st0, (uint32_t)nq * 4, &tbar[buf]);
+        (void)vec;
+      }
+    } else {
+      if (with_kv) {
+        bw_load<CP>(sb + SM::K, F.k + b * F.k_sb + (int64_t)h * c, F.k_sl, k0, L - k0, c);
+        bw_load<CP>(sb + SM::V, F.v + b * F.v_sb + (int64_t)h * c, F.v_sl, k0, L - k0, c);
+      }
+      bw_load<CP>(sb + SM::Q + buf * SM::QD_BYTES, F.q + b * F.q_sb + (int64_t)h * c, F.q_sl, q0, L - q0, c);
+      bw_load<CP>(sb + SM::DO + buf * SM::QD_BYTES, P.dO + b * L * HC + (int64_t)h * c, HC, q0, L - q0, c);
+    }
     if constexpr (BIASS) {  // transposed bias [h][key][query] (query-contiguous, L % 8 == 0)
       const bf16* bt = F.bias + (int64_t)h * F.bs1;
 #pragma unroll
@@ -343,7 +405,9 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
         cp_async16(sb + SM::BT + r * (SM::BROW * 2) + cq * 2, ok ? bt + (int64_t)(k0 + r) * F.bs3 + q0 + cq : bt, ok);
       }
     }
-    if (vec_stats) {
+    if (tmaq) {
+      // lse / D were bulk-copied above
+    } else if (vec_stats) {
       if (threadIdx.x < 2 * BW_BQ / 4) {
         const int t = threadIdx.x & (BW_BQ / 4 - 1);
         const bool ok = q0 + 4 * t < L;
@@ -421,9 +485,15 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
       const uint32_t sQ = sb + SM::Q + buf * SM::QD_BYTES, sDO = sb + SM::DO + buf * SM::QD_BYTES;
       const float* s_lse = reinterpret_cast<const float*>(smem + SM::LSE + buf * BW_BQ * 4);
       const float* s_D = reinterpret_cast<const float*>(smem + SM::DD + buf * BW_BQ * 4);
+      BTRACE(it * 8 + 0);
       cp_async_wait<0>();
+      if (tmaq) {
+        mbar_wait(&tbar[buf], (t_par >> buf) & 1u);
+        t_par ^= 1u << buf;
+      }
       fence_async_smem();
       __syncthreads();
+      BTRACE(it * 8 + 1);
       // double-buffered: the next query tile of this unit loads while this one computes (the
       // other buffer's last reader, the previous tile's MMAs, completed before this barrier)
       if (DB && qt + 1 < nqt) issue_loads(b, h, k0, qt + 1, false, buf ^ 1);
@@ -432,15 +502,21 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
 #pragma unroll
         for (int kk = 0; kk < CP / 16; ++kk) {
           const uint32_t koff = kk * 2 * LBO_ROWS;
-          mma_bf16(tmem + T_S, make_sdesc(sb + SM::K + koff, LBO_ROWS, 128), make_sdesc(sQ + koff, LBO_ROWS, 128),
-                   ID_SS, kk != 0);
-          mma_bf16(tmem + T_DP, make_sdesc(sb + SM::V + koff, LBO_ROWS, 128), make_sdesc(sDO + koff, LBO_ROWS, 128),
-                   ID_SS, kk != 0);
+          if (tmaq) {
+            mma_bf16(tmem + T_S, bw_sw64_k(sb + SM::K + kk * 32), bw_sw64_k(sQ + kk * 32), ID_SS, kk != 0);
+            mma_bf16(tmem + T_DP, bw_sw64_k(sb + SM::V + kk * 32), bw_sw64_k(sDO + kk * 32), ID_SS, kk != 0);
+          } else {
+            mma_bf16(tmem + T_S, make_sdesc(sb + SM::K + koff, LBO_ROWS, 128), make_sdesc(sQ + koff, LBO_ROWS, 128),
+                     ID_SS, kk != 0);
+            mma_bf16(tmem + T_DP, make_sdesc(sb + SM::V + koff, LBO_ROWS, 128), make_sdesc(sDO + koff, LBO_ROWS, 128),
+                     ID_SS, kk != 0);
+          }
         }
         mma_commit(&bar1);
       }
       mbar_wait(&bar1, it & 1);
       tc_fence_after();
+      BTRACE(it * 8 + 2);
 
       float kb_acc = 0.f;
 #pragma unroll 1
@@ -542,6 +618,7 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
         }
       }
       if (db_per_key) s_kb[wg * BW_BK + kr] = kb_acc;
+      BTRACE(it * 8 + 3);
 
       if (PTM) tmem_st_wait();
       fence_async_smem();
@@ -555,20 +632,19 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
         for (int kk = 0; kk < BW_BQ / 16; ++kk) {
           const uint32_t aoff = kk * 2 * LBO_ROWS;
           const uint32_t boff = kk * 2 * 128;
+          const uint64_t d_do = tmaq ? bw_sw64_mn(sDO + kk * 1024) : make_sdesc(sDO + boff, 128, LBO_ROWS);
+          const uint64_t d_q = tmaq ? bw_sw64_mn(sQ + kk * 1024) : make_sdesc(sQ + boff, 128, LBO_ROWS);
           if constexpr (PTM)  // queries [0,64) at columns [0,32), [64,128) at [64,96)
-            bw_mma_ts(tmem + T_DV, tmem + T_S + (kk < 4 ? kk * 8 : 64 + (kk - 4) * 8),
-                      make_sdesc(sDO + boff, 128, LBO_ROWS), ID_KV, kk != 0);
+            bw_mma_ts(tmem + T_DV, tmem + T_S + (kk < 4 ? kk * 8 : 64 + (kk - 4) * 8), d_do, ID_KV, kk != 0);
           else
-            mma_bf16(tmem + T_DV, make_sdesc(sb + SM::PT + aoff, LBO_ROWS, 128), make_sdesc(sDO + boff, 128, LBO_ROWS),
-                     ID_KV, kk != 0);
-          mma_bf16(tmem + T_DK, make_sdesc(sb + SM::DST + aoff, LBO_ROWS, 128), make_sdesc(sQ + boff, 128, LBO_ROWS),
-                   ID_KV, kk != 0);
+            mma_bf16(tmem + T_DV, make_sdesc(sb + SM::PT + aoff, LBO_ROWS, 128), d_do, ID_KV, kk != 0);
+          mma_bf16(tmem + T_DK, make_sdesc(sb + SM::DST + aoff, LBO_ROWS, 128), d_q, ID_KV, kk != 0);
         }
 #pragma unroll
         for (int kk = 0; kk < BW_BK / 16; ++kk) {
           const uint32_t off = kk * 2 * 128;
-          mma_bf16(tmem + T_DQ, make_sdesc(sb + SM::DST + off, 128, LBO_ROWS),
-                   make_sdesc(sb + SM::K + off, 128, LBO_ROWS), ID_Q, kk != 0);
+          const uint64_t d_k = tmaq ? bw_sw64_mn(sb + SM::K + kk * 1024) : make_sdesc(sb + SM::K + off, 128, LBO_ROWS);
+          mma_bf16(tmem + T_DQ, make_sdesc(sb + SM::DST + off, 128, LBO_ROWS), d_k, ID_Q, kk != 0);
         }
 #endif
         mma_commit(&bar2);
@@ -597,8 +673,10 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
           if (k0 + r < L && q0 + g * 8 < L) *reinterpret_cast<uint4*>(wsb + (int64_t)r * L + g * 8) = cv[i];
         }
       }
+      BTRACE(it * 8 + 4);
       mbar_wait(&bar2, it & 1);
       tc_fence_after();
+      BTRACE(it * 8 + 5);
       // the tiles are free: prefetch the next (batch, query tile) while draining TMEM
       const bool last_q = qt + 1 == nqt;
       if (!last_q) {
@@ -607,12 +685,15 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
         int64_t nb;
         int nh, nkt_;
         decode(u + gridDim.x, nb, nh, nkt_);
+#if EVO_EXP != 11
         issue_loads(nb, nh, nkt_ * BW_BK, 0, true, DB ? (buf ^ 1) : 0);
+#endif
         if constexpr (per_key_bias) {
           const int nkj = nkt_ * BW_BK + kr;
           kb_next = nkj < L ? F.bias[nb * F.bs0 + (int64_t)nh * F.bs1 + (int64_t)nkj * F.bs3] : f2bf(0.f);
         }
       }
+      BTRACE(it * 8 + 7);
 #if EVO_EXP != 3
       {
 #pragma unroll
@@ -674,6 +755,7 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
         }
       }
 #endif
+      BTRACE(it * 8 + 6);
       tc_fence_before();
       __syncthreads();
     }
@@ -701,6 +783,11 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
 }
 
 // dq = bf16(sum of the NP per-key-tile fp32 partials); all 2*NP loads of a thread in flight
+#if EVO_EXP == 10 || EVO_EXP == 11
+}  // namespace evo
+extern "C" int evo_bwd_trace(void* dst) { return (int)cudaMemcpyFromSymbol(dst, evo::g_bwd_trace, sizeof(evo::g_bwd_trace)); }
+namespace evo {
+#endif
 template <int NP>
 __global__ void __launch_bounds__(256) attn_bwd_dq_finish(AttnBwdParams P, int64_t B) {
   const int L = P.f.L, H = P.f.H, c = P.f.c;
@@ -759,9 +846,32 @@ static int64_t ws_layout(int64_t B, int64_t L, int H, int c, int bias_batch_redu
 
 int sm_count();
 
+// tensor map of one per-tile operand: element (d, h, l, b) at base + b*sb + l*sl + h*c + d, box [32 d][1][128 l][1]
+static bool bw_map(CUtensorMap* m, const void* base, int c, int H, int64_t L, int64_t B, int64_t sl, int64_t sb) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc || ((uintptr_t)base & 15) || (sl * 2) % 16 || (sb * 2) % 16 || sl <= 0 || sb <= 0) return false;
+  cuuint64_t d[4] = {(cuuint64_t)c, (cuuint64_t)H, (cuuint64_t)L, (cuuint64_t)B};
+  cuuint64_t s[3] = {(cuuint64_t)c * 2, (cuuint64_t)sl * 2, (cuuint64_t)sb * 2};
+  cuuint32_t bx[4] = {32, 1, 128, 1}, es[4] = {1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), d, s, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
 template <int CP, int MODE>
 static int launch_bwd_m(AttnBwdParams& p, int64_t B, int dq_partial, cudaStream_t st) {
   using SM = BwdSmem<CP, MODE == 2 && CP <= 32>;
+  BwdMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  static const bool tma_off = [] { const char* e = getenv("EVO_ATTN_BWD_NO_TMA"); return e && e[0] == '1'; }();
+  const AttnParams& f = p.f;
+  const int64_t HC = (int64_t)f.H * f.c;
+  // TMA path: head dim exactly 32 (the 64-byte rows of the swizzled tiles) and 16-byte lse / D rows
+  const int tmaq = !tma_off && CP == 32 && f.c == 32 && f.L % 4 == 0 &&
+                   bw_map(&maps.q, f.q, f.c, f.H, f.L, B, f.q_sl, f.q_sb) &&
+                   bw_map(&maps.k, f.k, f.c, f.H, f.L, B, f.k_sl, f.k_sb) &&
+                   bw_map(&maps.v, f.v, f.c, f.H, f.L, B, f.v_sl, f.v_sb) &&
+                   bw_map(&maps.dO, p.dO, f.c, f.H, f.L, B, HC, f.L * HC);
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel<CP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -774,7 +884,7 @@ static int launch_bwd_m(AttnBwdParams& p, int64_t B, int dq_partial, cudaStream_
   // persistent: 2 CTAs per SM, units handed out round-robin
   const int64_t slots = (int64_t)sm_count() * 2;
   dim3 grid((unsigned)(units < slots ? units : slots));
-  attn_bwd_kernel<CP, MODE><<<grid, 256, SM::TOTAL, st>>>(p, (int)nkt, dq_partial);
+  attn_bwd_kernel<CP, MODE><<<grid, 256, SM::TOTAL, st>>>(p, (int)nkt, dq_partial, maps, tmaq);
   EVO_LAUNCH_CHECK("attention bwd main");
   return EVO_OK;
 }

@@ -11,6 +11,7 @@ ap.add_argument("--variant", default="all")
 ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--bwd", type=int, default=1)
 ap.add_argument("--fb", type=int, default=1, help="forward: stage a full bias through smem (A/B switch)")
+ap.add_argument("--trace-dump", default="", help="EVO_EXP=10 builds: dump the backward phase trace (numpy)")
 a = ap.parse_args()
 from paper_2203_00854_b200 import _lib
 FLAGS = 0 if a.fb else _lib.EVO_ATTN_NO_BIAS_SMEM
@@ -64,3 +65,9 @@ for name, B, L, H, c, kind, bmode in V:
         ms = e0.elapsed_time(e1) / a.iters
         fl = (4 if tag == "fwd" else 10) * B * H * L * L * c
         print(f"{name:9s} {tag}: {ms*1e3:8.1f} us  {fl/ms/1e9:7.1f} TFLOP/s")
+
+if a.trace_dump:
+    import ctypes, numpy as np
+    buf = np.zeros(8192, dtype=np.uint64)
+    _lib.load().evo_bwd_trace(buf.ctypes.data_as(ctypes.c_void_p))
+    np.save(a.trace_dump, buf)
