@@ -151,7 +151,13 @@ __device__ __forceinline__ void bulk_ld(uint32_t dst, const void* src, uint32_t 
 
 struct BwdMaps {  // tensor maps of the per-tile operands (TMA path): element (d, h, l, b)
   CUtensorMap q, k, v, dO;
+  CUtensorMap bt;  // msa_row: transposed batch-shared bias [h][key][query], box [136 q][128 keys]
+  CUtensorMap ws;  // msa_row: dS^T workspace [b*H + h][key][query] in the canonical tile order (store)
 };
+__device__ __forceinline__ void tma_st5(uint64_t m, uint32_t src, int c0, int c1, int c2, int c3, int c4) {
+  asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];\n"
+               ::"l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(src) : "memory");
+}
 
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
   uint32_t* r = reinterpret_cast<uint32_t*>(v);
@@ -375,12 +381,15 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
       if (threadIdx.x == 0) {
         const uint32_t tile = 128 * 32 * 2, vec = BW_BQ * 4;
         const int nq = L - q0 < BW_BQ ? L - q0 : BW_BQ;
-        mbar_expect_tx(&tbar[buf], (with_kv ? 4 : 2) * tile + 2 * (uint32_t)nq * 4);
+        mbar_expect_tx(&tbar[buf], (with_kv ? 4 : 2) * tile + 2 * (uint32_t)nq * 4 +
+                                       (BIASS ? (uint32_t)(BW_BK * SM::BROW * 2) : 0u));
         const uint32_t br = smem_u32(&tbar[buf]);
         if (with_kv) {
           tma_ld4(sb + SM::K, reinterpret_cast<uint64_t>(&maps.k), 0, h, k0, (int)b, br);
           tma_ld4(sb + SM::V, reinterpret_cast<uint64_t>(&maps.v), 0, h, k0, (int)b, br);
         }
+        if constexpr (BIASS)  // the padded 136-query rows of the smem tile ARE the box rows
+          tma_ld3(sb + SM::BT, reinterpret_cast<uint64_t>(&maps.bt), q0, k0, h, br);
         tma_ld4(sb + SM::Q + buf * SM::QD_BYTES, reinterpret_cast<uint64_t>(&maps.q), 0, h, q0, (int)b, br);
         tma_ld4(sb + SM::DO + buf * SM::QD_BYTES, reinterpret_cast<uint64_t>(&maps.dO), 0, h, q0, (int)b, br);
         bulk_ld(sb + lse_b, P.lse2 + st0, (uint32_t)nq * 4, &tbar[buf]);
@@ -395,7 +404,7 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
       bw_load<CP>(sb + SM::Q + buf * SM::QD_BYTES, F.q + b * F.q_sb + (int64_t)h * c, F.q_sl, q0, L - q0, c);
       bw_load<CP>(sb + SM::DO + buf * SM::QD_BYTES, P.dO + b * L * HC + (int64_t)h * c, HC, q0, L - q0, c);
     }
-    if constexpr (BIASS) {  // transposed bias [h][key][query] (query-contiguous, L % 8 == 0)
+    if constexpr (BIASS) if (!tmaq) {  // transposed bias [h][key][query] (query-contiguous, L % 8 == 0)
       const bf16* bt = F.bias + (int64_t)h * F.bs1;
 #pragma unroll
       for (int i = 0; i < BW_BK * (BW_BQ / 8) / 256; ++i) {
@@ -490,6 +499,7 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
       if (tmaq) {
         mbar_wait(&tbar[buf], (t_par >> buf) & 1u);
         t_par ^= 1u << buf;
+        if (db_store && threadIdx.x == 0) bulk_wait_read<0>();  // the dS^T store has read the tile
       }
       fence_async_smem();
       __syncthreads();
@@ -649,7 +659,14 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
 #endif
         mma_commit(&bar2);
       }
-      if constexpr (db_store) {
+      if (db_store && tmaq) {
+        // dS^T tile -> workspace by one TMA tensor store (the map walks the canonical tile order);
+        // the tile is re-read only after bulk_wait_read at the next loop top
+        if (threadIdx.x == 0) {
+          tma_st5(reinterpret_cast<uint64_t>(&maps.ws), sb + SM::DST, 0, 0, k0 / 8, q0 / 8, (int)(b * H + h));
+          bulk_commit();
+        }
+      } else if constexpr (db_store) {
         // dS^T tile (unscaled bf16, canonical K-major [key][query]) -> workspace [b][h][key][query],
         // under the dV/dK/dQ MMAs (which only read the tile): all 8 smem reads of a thread first,
         // then its 8 16-byte stores (no register-reuse serialisation between load and store).
@@ -777,6 +794,7 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
       }
     }
   }
+  if (db_store && tmaq && threadIdx.x == 0) bulk_wait<0>();
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc(tmem, 256);
@@ -858,6 +876,29 @@ static bool bw_map(CUtensorMap* m, const void* base, int c, int H, int64_t L, in
          CUDA_SUCCESS;
 }
 
+// msa_row: the transposed bias [H][L][L] (box [136 q][128 keys], the padded smem rows) and the dS^T
+// workspace [B*H][L][L] as 5-D (q % 8, key % 8, key / 8, q / 8, b*H + h) = the canonical tile order
+static bool bw_bias_maps(BwdMaps* m, const void* bias_t, const void* ds, int H, int64_t L, int64_t B) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc || !bias_t || !ds || L % 8 || ((uintptr_t)bias_t & 15) || ((uintptr_t)ds & 15)) return false;
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  {
+    cuuint64_t d[3] = {(cuuint64_t)L, (cuuint64_t)L, (cuuint64_t)H};
+    cuuint64_t s[2] = {(cuuint64_t)L * 2, (cuuint64_t)L * L * 2};
+    cuuint32_t bx[3] = {136, 128, 1};
+    if (enc(&m->bt, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(bias_t), d, s, bx, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  cuuint64_t d[5] = {8, 8, (cuuint64_t)(L / 8), (cuuint64_t)(L / 8), (cuuint64_t)(B * H)};
+  cuuint64_t s[4] = {(cuuint64_t)L * 2, (cuuint64_t)L * 16, 16, (cuuint64_t)L * L * 2};
+  cuuint32_t bx[5] = {8, 8, 16, 16, 1};
+  return enc(&m->ws, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(ds), d, s, bx, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int CP, int MODE>
 static int launch_bwd_m(AttnBwdParams& p, int64_t B, int dq_partial, cudaStream_t st) {
   using SM = BwdSmem<CP, MODE == 2 && CP <= 32>;
@@ -871,7 +912,8 @@ static int launch_bwd_m(AttnBwdParams& p, int64_t B, int dq_partial, cudaStream_
                    bw_map(&maps.q, f.q, f.c, f.H, f.L, B, f.q_sl, f.q_sb) &&
                    bw_map(&maps.k, f.k, f.c, f.H, f.L, B, f.k_sl, f.k_sb) &&
                    bw_map(&maps.v, f.v, f.c, f.H, f.L, B, f.v_sl, f.v_sb) &&
-                   bw_map(&maps.dO, p.dO, f.c, f.H, f.L, B, HC, f.L * HC);
+                   bw_map(&maps.dO, p.dO, f.c, f.H, f.L, B, HC, f.L * HC) &&
+                   (MODE != 2 || bw_bias_maps(&maps, f.bias, p.dS, f.H, f.L, B));
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel<CP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
