@@ -17,7 +17,9 @@
 // K/V tiles are double-buffered with cp.async; several CTAs per SM overlap the
 // MMA of one CTA with the softmax of another.
 #include "attn.cuh"
+#include "tma.cuh"
 #include <cstdlib>
+#include <cstring>
 
 namespace evo {
 
@@ -129,6 +131,18 @@ __device__ __forceinline__ void att_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uin
 #endif
 int sm_count();
 
+// TMA path (head dim 32): tensor maps whose boxes land exactly in the canonical (SWIZZLE_NONE)
+// operand layouts - Q / K [k/8][row/8][row%8][k%8] data groups, V as [d/8][key/8][key%8][d%8]
+// (the row-sum group d/8 = 4 stays a constant block after the data), the full-bias tile with its
+// padded 72-key rows and the gate rows - so one thread issues a unit's / a tile's loads
+struct AttnFwdMaps {
+  CUtensorMap q, k, v, bias, g;
+};
+// V (TMA layout): byte offset of element (key, d) in a stage
+__device__ __forceinline__ uint32_t vt_off(int key, int d) {
+  return (uint32_t)(((d >> 3) * (ATT_BK / 8) + (key >> 3)) * 128 + (key & 7) * 16 + (d & 7) * 2);
+}
+
 // FB: full bias staged through smem with the K/V tiles (msa_row: [1, H, L, L] shared over the
 // batch, so the tile loads hit L2) instead of 16-byte global loads after the S wait.
 //
@@ -140,13 +154,13 @@ int sm_count();
 // VAR: 0 = no bias (gate rows prefetched into smem for the epilogue), 1 = per-key bias,
 // 2 = full bias staged through smem (FB), 3 = generic full bias (strided global loads)
 template <int CP, int VAR>
-__global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1) ? 3 : 4)) attn_fwd_kernel(AttnParams P,
-                                                                                                          int nunits) {
+__global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1) ? 3 : 4)) attn_fwd_kernel(
+    AttnParams P, int nunits, const __grid_constant__ AttnFwdMaps maps, int tmaq) {
   constexpr bool FB = VAR == 2, GS = VAR == 0;
   using SM = AttnSmem<CP>;
   constexpr int CQ = SM::CQ, CV = SM::CV;
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bar_s, bar_o;
+  __shared__ uint64_t bar_s, bar_o, kv_full[2], q_full, g_full;
   __shared__ uint32_t tmem_sh;
   const uint32_t sb = smem_u32(smem);
 
@@ -163,8 +177,13 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1
   if (threadIdx.x == 0) {
     mbar_init(&bar_s, 1);
     mbar_init(&bar_o, 1);
+    mbar_init(&kv_full[0], 1);
+    mbar_init(&kv_full[1], 1);
+    mbar_init(&q_full, 1);
+    mbar_init(&g_full, 1);
     fence_mbar_init();
   }
+  __syncthreads();  // the TMA path issues into these barriers in the prologue
 
   struct Unit {
     int q0, h;
@@ -186,6 +205,30 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1
   };
   auto bfull_of = [&](const Unit& t) { return FB ? P.bias + t.b * P.bs0 + (int64_t)t.h * P.bs1 : nullptr; };
 
+  // TMA issue (thread 0): a K/V (+ full-bias) tile into a stage, a unit's Q, a unit's gate rows
+  auto tma_kv = [&](const Unit& t, int k0, int st) {
+    const uint32_t bytes = 2u * ATT_BK * CP * 2 + (FB ? (uint32_t)(ATT_BQ * SM::BROW * 2) : 0u);
+    mbar_expect_tx(&kv_full[st], bytes);
+    const uint32_t br = smem_u32(&kv_full[st]);
+    tma_ld5(sb + SM::KT + st * SM::K_BYTES, reinterpret_cast<uint64_t>(&maps.k), 0, 0, k0 / 8, t.h * (CP / 8),
+            (int)t.b, br);
+    tma_ld5(sb + SM::VT + st * SM::V_BYTES, reinterpret_cast<uint64_t>(&maps.v), 0, 0, k0 / 8, t.h * (CP / 8),
+            (int)t.b, br);
+    if (FB)
+      tma_ld4(sb + SM::BS + st * SM::BS_BYTES, reinterpret_cast<uint64_t>(&maps.bias), k0, t.q0, t.h,
+              P.bs0 == 0 ? 0 : (int)t.b, br);
+  };
+  auto tma_q = [&](const Unit& t) {
+    mbar_expect_tx(&q_full, (uint32_t)(ATT_BQ * CP * 2));
+    tma_ld5(sb + SM::Q, reinterpret_cast<uint64_t>(&maps.q), 0, 0, t.q0 / 8, t.h * (CP / 8), (int)t.b,
+            smem_u32(&q_full));
+  };
+  auto tma_g = [&](const Unit& t) {
+    mbar_expect_tx(&g_full, (uint32_t)(ATT_BQ * CP * 2));
+    tma_ld4(sb + SM::GT, reinterpret_cast<uint64_t>(&maps.g), 0, t.h, t.q0, (int)t.b, smem_u32(&g_full));
+  };
+  uint32_t ui = 0;  // CTA-local unit counter: q_full / g_full parity
+
   int u = blockIdx.x;
   if (u >= nunits) {  // (grid <= nunits by construction)
     tc_fence_before();
@@ -195,10 +238,17 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1
   }
   Unit cur = decode(u);
   // prologue: Q and tile 0 of the first unit into Q buffer 0 / stage 0
-  att_load_kmajor<CP, ATT_BQ>(sb + SM::Q, P.q + cur.b * P.q_sb + (int64_t)cur.h * c, P.q_sl, cur.q0, L - cur.q0, c);
-  att_load_kmajor<CP, ATT_BK>(sb + SM::KT, kbase(cur), P.k_sl, 0, L, c);
-  att_load_v<CP, CV>(sb + SM::VT, vbase(cur), P.v_sl, 0, L, c);
-  if (FB) att_load_bias<SM::BROW>(sb + SM::BS, bfull_of(cur), P.bs2, cur.q0, 0, L);
+  if (tmaq) {
+    if (threadIdx.x == 0) {
+      tma_q(cur);
+      tma_kv(cur, 0, 0);
+    }
+  } else {
+    att_load_kmajor<CP, ATT_BQ>(sb + SM::Q, P.q + cur.b * P.q_sb + (int64_t)cur.h * c, P.q_sl, cur.q0, L - cur.q0, c);
+    att_load_kmajor<CP, ATT_BK>(sb + SM::KT, kbase(cur), P.k_sl, 0, L, c);
+    att_load_v<CP, CV>(sb + SM::VT, vbase(cur), P.v_sl, 0, L, c);
+    if (FB) att_load_bias<SM::BROW>(sb + SM::BS, bfull_of(cur), P.bs2, cur.q0, 0, L);
+  }
   cp_async_commit();
   // constant parts of the augmented operands (Q, both K/V stages): Q rows
   // [.. | 1 or 0, 0 x 7 | 0 x 8], K rows' zero group (the bias group is written per tile),
@@ -208,7 +258,8 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1
   {
     const int st = r / ATT_BK, kr = r % ATT_BK;  // 128 threads = 2 stages x 64 keys
     st_shared_v4(sb + SM::KT + st * SM::K_BYTES + kmajor_off(kr, CP + 8, ATT_BK), 0u, 0u, 0u, 0u);
-    st_shared_v4(sb + SM::VT + st * SM::V_BYTES + mnmajor_off(CP, kr, CV), ONE_BF16, 0u, 0u, 0u);
+    st_shared_v4(sb + SM::VT + st * SM::V_BYTES + (tmaq ? vt_off(kr, CP) : mnmajor_off(CP, kr, CV)), ONE_BF16, 0u,
+                 0u, 0u);
     if (st == 0)
       st_shared_v4(sb + SM::KT + kmajor_off(kr, CP, ATT_BK),
                    (per_key_bias && kr < L) ? (uint32_t)kbias_of(cur)[(int64_t)kr * P.bs3] : 0u, 0u, 0u, 0u);
@@ -246,32 +297,48 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1
       const int k0 = j * ATT_BK;
       const int st = gt & 1;
       cp_async_wait<0>();
+      if (tmaq) {
+        mbar_wait(&kv_full[st], (gt >> 1) & 1);
+        if (j == 0) mbar_wait(&q_full, ui & 1);
+      }
       fence_async_smem();
       __syncthreads();
       // prefetch into the other stage (its MMAs finished last iteration): this unit's next
       // K/V tile, or on the last tile the next unit's first K/V tile
       const uint32_t kdst = sb + SM::KT + (st ^ 1) * SM::K_BYTES, vdst = sb + SM::VT + (st ^ 1) * SM::V_BYTES;
       if (j + 1 < nkt) {
-        att_load_kmajor<CP, ATT_BK>(kdst, kb, P.k_sl, k0 + ATT_BK, L - k0 - ATT_BK, c);
-        att_load_v<CP, CV>(vdst, vb, P.v_sl, k0 + ATT_BK, L - k0 - ATT_BK, c);
-        if (FB) att_load_bias<SM::BROW>(sb + SM::BS + (st ^ 1) * SM::BS_BYTES, bfull, P.bs2, q0, k0 + ATT_BK, L);
+        if (tmaq) {
+          if (threadIdx.x == 0) tma_kv(cur, k0 + ATT_BK, st ^ 1);
+        } else {
+          att_load_kmajor<CP, ATT_BK>(kdst, kb, P.k_sl, k0 + ATT_BK, L - k0 - ATT_BK, c);
+          att_load_v<CP, CV>(vdst, vb, P.v_sl, k0 + ATT_BK, L - k0 - ATT_BK, c);
+          if (FB) att_load_bias<SM::BROW>(sb + SM::BS + (st ^ 1) * SM::BS_BYTES, bfull, P.bs2, q0, k0 + ATT_BK, L);
+        }
         if (per_key_bias && threadIdx.x < ATT_BK) {
           const int k = k0 + ATT_BK + threadIdx.x;
           nb = k < L ? (uint32_t)kbias[(int64_t)k * P.bs3] : 0u;
         }
       } else if (has_next) {
-        att_load_kmajor<CP, ATT_BK>(kdst, kbase(nxt), P.k_sl, 0, L, c);
-        att_load_v<CP, CV>(vdst, vbase(nxt), P.v_sl, 0, L, c);
-        if (FB) att_load_bias<SM::BROW>(sb + SM::BS + (st ^ 1) * SM::BS_BYTES, bfull_of(nxt), P.bs2, nxt.q0, 0, L);
+        if (tmaq) {
+          if (threadIdx.x == 0) tma_kv(nxt, 0, st ^ 1);
+        } else {
+          att_load_kmajor<CP, ATT_BK>(kdst, kbase(nxt), P.k_sl, 0, L, c);
+          att_load_v<CP, CV>(vdst, vbase(nxt), P.v_sl, 0, L, c);
+          if (FB) att_load_bias<SM::BROW>(sb + SM::BS + (st ^ 1) * SM::BS_BYTES, bfull_of(nxt), P.bs2, nxt.q0, 0, L);
+        }
         if (per_key_bias && threadIdx.x < ATT_BK)
           nb = (int)threadIdx.x < L ? (uint32_t)kbias_of(nxt)[(int64_t)threadIdx.x * P.bs3] : 0u;
       }
       cp_async_commit();
-      if (GS && j + 1 == nkt && qi < L) {  // this unit's gate rows (own row: no barrier needed)
-        const bf16* gsrc = P.g + b * P.g_sb + (int64_t)qi * P.g_sl + (int64_t)h * c;
+      if (GS && j + 1 == nkt) {  // this unit's gate rows
+        if (tmaq) {
+          if (threadIdx.x == 0) tma_g(cur);
+        } else if (qi < L) {  // (own row: no barrier needed)
+          const bf16* gsrc = P.g + b * P.g_sb + (int64_t)qi * P.g_sl + (int64_t)h * c;
 #pragma unroll
-        for (int d = 0; d < CP; d += 8)
-          if (d < c) cp_async16(sb + SM::GT + r * (CP * 2) + d * 2, gsrc + d, true);
+          for (int d = 0; d < CP; d += 8)
+            if (d < c) cp_async16(sb + SM::GT + r * (CP * 2) + d * 2, gsrc + d, true);
+        }
       }
       if (GS) cp_async_commit();
 
@@ -291,9 +358,13 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1
       mbar_wait(&bar_s, gt & 1);
       tc_fence_after();
       if (j + 1 == nkt && has_next) {  // Q is free: this unit's last S MMA has completed
-        att_load_kmajor<CP, ATT_BQ>(sb + SM::Q, P.q + nxt.b * P.q_sb + (int64_t)nxt.h * c, P.q_sl, nxt.q0,
-                                    L - nxt.q0, c);
-        cp_async_commit();
+        if (tmaq) {
+          if (threadIdx.x == 0) tma_q(nxt);
+        } else {
+          att_load_kmajor<CP, ATT_BQ>(sb + SM::Q, P.q + nxt.b * P.q_sb + (int64_t)nxt.h * c, P.q_sl, nxt.q0,
+                                      L - nxt.q0, c);
+          cp_async_commit();
+        }
       }
 
       float s[ATT_BK];
@@ -389,7 +460,9 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < ATT_BK / 16; ++kk) {
-          uint64_t bd = make_sdesc(sb + SM::VT + st * SM::V_BYTES + kk * 2 * (CV / 8) * 128, (CV / 8) * 128, 128);
+          const uint64_t bd =
+              tmaq ? make_sdesc(sb + SM::VT + st * SM::V_BYTES + kk * 2 * 128, 128, (ATT_BK / 8) * 128)
+                   : make_sdesc(sb + SM::VT + st * SM::V_BYTES + kk * 2 * (CV / 8) * 128, (CV / 8) * 128, 128);
           att_mma_ts(tmem + T_O, tmem + kk * 8, bd, IDESC_O, (j > 0 || kk > 0) ? 1u : 0u);
         }
         mma_commit(&bar_o);
@@ -407,8 +480,13 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1
     const float l_run = o_acc[CP];
 
     if (GS) {  // the gate group: only the next unit's Q group may still be in flight
-      if (has_next) cp_async_wait<1>();
-      else cp_async_wait<0>();
+      if (tmaq) {
+        mbar_wait(&g_full, ui & 1);
+      } else if (has_next) {
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
     }
     if (qi < L) {
       const float inv = rcpf(l_run);
@@ -448,6 +526,7 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1
     }
     u = nu;
     cur = nxt;
+    ++ui;
   }
 
   __syncthreads();
@@ -455,6 +534,28 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1
 }
 
 static bool a16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+static bool fwd_map5(CUtensorMap* m, const void* base, int H, int64_t L, int64_t B, int64_t sl, int64_t sb, bool v) {
+  // Q / K: (d%8, row%8, row/8, d/8 over all heads, b) box [8][8][rows/8][4][1];  V: (d%8, key%8, key/8, d/8, b)
+  // with the boxes ordered so the smem image is [d/8][key/8][key%8][d%8]
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc || ((uintptr_t)base & 15) || (sl * 2) % 16 || (sb * 2) % 16) return false;
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  if (!v) {
+    cuuint64_t d[5] = {8, 8, (cuuint64_t)((L + 7) / 8), (cuuint64_t)(H * 4), (cuuint64_t)B};
+    cuuint64_t s[4] = {(cuuint64_t)sl * 2, (cuuint64_t)sl * 16, 16, (cuuint64_t)sb * 2};
+    cuuint32_t bx[5] = {8, 8, 16, 4, 1};  // Q box; K tiles use the first 8 row groups (set below)
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), d, s, bx, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  cuuint64_t d[5] = {8, 8, (cuuint64_t)((L + 7) / 8), (cuuint64_t)(H * 4), (cuuint64_t)B};
+  cuuint64_t s[4] = {(cuuint64_t)sl * 2, (cuuint64_t)sl * 16, 16, (cuuint64_t)sb * 2};
+  cuuint32_t bx[5] = {8, 8, 8, 4, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), d, s, bx, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 template <int CP, int VAR>
 static int launch_attn_fwd_v(const AttnParams& p, int64_t B, cudaStream_t st) {
@@ -479,7 +580,52 @@ static int launch_attn_fwd_v(const AttnParams& p, int64_t B, cudaStream_t st) {
   const int64_t nunits = (int64_t)((p.L + ATT_BQ - 1) / ATT_BQ) * p.H * B;
   EVO_CHECK_ARG(nunits < (1ll << 31), EVO_ERR_SHAPE, "attention fwd: too many (batch, head, query tile) units");
   const int64_t cap = (int64_t)occ * sm_count();
-  attn_fwd_kernel<CP, VAR><<<(unsigned)(nunits < cap ? nunits : cap), 128, bytes, st>>>(p, (int)nunits);
+  AttnFwdMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  static const bool tma_off = [] { const char* e = getenv("EVO_ATTN_FWD_NO_TMA"); return e && e[0] == '1'; }();
+  int tmaq = !tma_off && CP == 32 && p.c == 32 && p.L % 8 == 0 && fwd_map5(&maps.q, p.q, p.H, p.L, B, p.q_sl, p.q_sb, false) &&
+             fwd_map5(&maps.k, p.k, p.H, p.L, B, p.k_sl, p.k_sb, false) &&
+             fwd_map5(&maps.v, p.v, p.H, p.L, B, p.v_sl, p.v_sb, true);
+  if (tmaq) {  // K tiles: 64 rows (8 row groups); V box written in the [d/8][key/8][key%8][d%8] order
+    EncodeTiledFn enc = encode_tiled();
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    {
+      cuuint64_t d[5] = {8, 8, (cuuint64_t)(p.L / 8), (cuuint64_t)(p.H * 4), (cuuint64_t)B};
+      cuuint64_t s[4] = {(cuuint64_t)p.k_sl * 2, (cuuint64_t)p.k_sl * 16, 16, (cuuint64_t)p.k_sb * 2};
+      cuuint32_t bx[5] = {8, 8, 8, 4, 1};
+      tmaq = enc(&maps.k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<bf16*>(p.k), d, s, bx, es,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
+    if (tmaq) {  // V: dims reordered (d%8, key%8, key/8, d/8, b) -> smem [d/8][key/8][key%8][d%8]
+      cuuint64_t d[5] = {8, 8, (cuuint64_t)(p.L / 8), (cuuint64_t)(p.H * 4), (cuuint64_t)B};
+      cuuint64_t s[4] = {(cuuint64_t)p.v_sl * 2, (cuuint64_t)p.v_sl * 16, 16, (cuuint64_t)p.v_sb * 2};
+      cuuint32_t bx[5] = {8, 8, 8, 4, 1};
+      tmaq = enc(&maps.v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<bf16*>(p.v), d, s, bx, es,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
+    if (tmaq && FB) {  // full bias [b?][h][q][key]: box [72 keys][128 q] = the padded smem rows
+      cuuint64_t d[4] = {(cuuint64_t)p.L, (cuuint64_t)p.L, (cuuint64_t)p.H, (cuuint64_t)(p.bs0 == 0 ? 1 : B)};
+      cuuint64_t s[3] = {(cuuint64_t)p.bs2 * 2, (cuuint64_t)p.bs1 * 2,
+                         (cuuint64_t)(p.bs0 == 0 ? p.bs1 * p.H : p.bs0) * 2};
+      cuuint32_t bx[4] = {(cuuint32_t)SM::BROW, ATT_BQ, 1, 1};
+      tmaq = p.bs3 == 1 && (p.bs2 * 2) % 16 == 0 && (p.bs1 * 2) % 16 == 0 && (p.bs0 * 2) % 16 == 0 &&
+             enc(&maps.bias, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<bf16*>(p.bias), d, s, bx, es,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
+    if (tmaq && VAR == 0) {  // gate rows [b][l][h*c]: box [32 d][1 h][128 l][1 b]
+      cuuint64_t d[4] = {32, (cuuint64_t)p.H, (cuuint64_t)p.L, (cuuint64_t)B};
+      cuuint64_t s[3] = {64, (cuuint64_t)p.g_sl * 2, (cuuint64_t)p.g_sb * 2};
+      cuuint32_t bx[4] = {32, 1, ATT_BQ, 1};
+      tmaq = (p.g_sl * 2) % 16 == 0 && (p.g_sb * 2) % 16 == 0 && a16(p.g) &&
+             enc(&maps.g, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<bf16*>(p.g), d, s, bx, es,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
+  }
+  attn_fwd_kernel<CP, VAR><<<(unsigned)(nunits < cap ? nunits : cap), 128, bytes, st>>>(p, (int)nunits, maps, tmaq);
   EVO_LAUNCH_CHECK("attention fwd");
   return EVO_OK;
 }
