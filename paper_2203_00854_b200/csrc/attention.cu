@@ -583,7 +583,11 @@ static int launch_attn_fwd_v(const AttnParams& p, int64_t B, cudaStream_t st) {
   AttnFwdMaps maps;
   memset(&maps, 0, sizeof(maps));
   static const bool tma_off = [] { const char* e = getenv("EVO_ATTN_FWD_NO_TMA"); return e && e[0] == '1'; }();
-  int tmaq = !tma_off && CP == 32 && p.c == 32 && p.L % 8 == 0 && fwd_map5(&maps.q, p.q, p.H, p.L, B, p.q_sl, p.q_sb, false) &&
+  // rows more than 1 MB apart (the column variants at N_r >= 2048: every 16-byte box row of a tile in
+  // another 2 MB page) measured slower through TMA than through per-thread cp.async (pair_col at N_r =
+  // 2048: 2.3x; msa_col at 400 KB and pair_col at 800 KB are faster through TMA), so those keep cp.async
+  const bool near_rows = p.q_sl * 2 <= (1 << 20) && p.k_sl * 2 <= (1 << 20) && p.v_sl * 2 <= (1 << 20);
+  int tmaq = !tma_off && near_rows && CP == 32 && p.c == 32 && p.L % 8 == 0 && fwd_map5(&maps.q, p.q, p.H, p.L, B, p.q_sl, p.q_sb, false) &&
              fwd_map5(&maps.k, p.k, p.H, p.L, B, p.k_sl, p.k_sb, false) &&
              fwd_map5(&maps.v, p.v, p.H, p.L, B, p.v_sl, p.v_sb, true);
   if (tmaq) {  // K tiles: 64 rows (8 row groups); V box written in the [d/8][key/8][key%8][d%8] order

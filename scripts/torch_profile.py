@@ -30,9 +30,9 @@ for e in rows[:45]:
         continue
     print(f"{t/1e3/nb:8.3f} ms/block {100*t/tot:5.1f}%  n={e.count//nb:4d}/blk  {e.key[:100]}")
 
-CATEGORIES = [("attention bwd", ("attn_bwd", "attn_dbias")), ("attention fwd", ("attn_fwd",)),
-              ("cuBLAS", ("nvjet", "cublas", "gemm", "splitKreduce", "cutlass")), ("OPM fused", ("opm_",)),
-              ("tcgen05 bgemm", ("bgemm",)), ("LayerNorm / residual", ("ln_", "residual_ln", "layernorm")),
+CATEGORIES = [("attention bwd", ("attn_bwd", "attn_dbias", "attn_bias_transpose")), ("attention fwd", ("attn_fwd",)),
+              ("OPM fused", ("opm_",)), ("tcgen05 bgemm", ("bgemm",)),
+              ("cuBLAS", ("nvjet", "cublas", "gemm", "splitKreduce", "cutlass")), ("LayerNorm / residual", ("ln_", "residual_ln", "layernorm")),
               ("elementwise / gates", ("gated_residual", "bias_act", "tri_gate", "colsum", "count_nonfinite")),
               ("copies / torch eager", ("copy", "Memcpy", "fill", "elementwise_kernel", "reduce_kernel"))]
 cat = {}
