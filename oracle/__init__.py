@@ -11,8 +11,10 @@ it and fails loudly when its CUDA library is missing.
 * ``evoformer_torch`` - the same algorithm in torch float64 on CPU; its autograd
                         is the gradient oracle (the reference has no backward,
                         SPEC.md:224).
-* ``dap_np``          - float64 restatement of dap_block.py + sharding.py
-                        (sharded schedule, byte ledger).
+
+The DAP schedule (dap_block.py + sharding.py) has no separate restatement: the
+sharded GPU block is checked against the single-device oracle above, and its
+byte ledger against the reference-generated golden ledger.
 
 Parity is pinned: tests/test_oracle_golden.py checks these against golden
 vectors produced by importing the reference itself (tests/golden/make_golden.py).
