@@ -409,16 +409,17 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1
         for (int kk = 0; kk < ATT_BK; ++kk)
           if (k0 + kk >= L) s[kk] = -INFINITY;
       }
-      float m8[8];
+      float m8[8];  // row max: 8 chains of three-input max (FMNMX3)
 #pragma unroll
-      for (int e = 0; e < 8; ++e) m8[e] = fmaxf(s[e], s[e + 8]);
+      for (int e = 0; e < 8; ++e) m8[e] = fmax3f(s[e], s[e + 8], s[e + 16]);
 #pragma unroll
-      for (int kk = 16; kk < ATT_BK; kk += 16) {
+      for (int kk = 24; kk + 16 <= ATT_BK; kk += 16) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) m8[e] = fmaxf(m8[e], fmaxf(s[kk + e], s[kk + 8 + e]));
+        for (int e = 0; e < 8; ++e) m8[e] = fmax3f(m8[e], s[kk + e], s[kk + 8 + e]);
       }
-      const float mxs = P.scale_log2 * fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
-                                             fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+#pragma unroll
+      for (int e = 0; e < 8; ++e) m8[e] = fmaxf(m8[e], s[ATT_BK - 8 + e]);
+      const float mxs = P.scale_log2 * fmax3f(fmax3f(m8[0], m8[1], m8[2]), fmax3f(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
       // lazy rescale: O (and l) in TMEM are rescaled only when a row's max grows by > 2^8
       // (warp-uniform: TMEM loads/stores are warp-collective); P <= 2^8 is exact enough in bf16
       const bool grow = mxs > m_run + 8.0f;

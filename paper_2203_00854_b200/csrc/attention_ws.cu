@@ -9,6 +9,9 @@
 //                 one issuer per warpgroup so neither waits on the other's softmax
 //     warp  9     loader: cp.async K/V (+ per-key bias) ring of WS_NS stages, completion
 //                 tracked by cp.async.mbarrier.arrive.noinc
+//   The two warpgroups take turns on the exponential phase (named barriers 1/2, ping-pong):
+//   one warpgroup's TMEM load, row max and P store run under the other's MUFU work
+//   (in-kernel clock trace: tile period 2039 -> 1791 clk; profiles/r02_ws_pingpong_trace.txt).
 //   K/V tiles (64 keys) are loaded once and shared by both query tiles.  S is double
 //   buffered per warpgroup in TMEM and P (bf16) is written back over S in TMEM and read from
 //   there by the PV MMA (A operand in tensor memory), so the tensor core works
@@ -28,12 +31,28 @@
 // mbarrier phases are tracked per buffer so a waiter can never be lapped (see comments).
 #include "attn.cuh"
 
+#ifndef EVO_EXP
+#define EVO_EXP 0
+#endif
+
 namespace evo {
+
+#if EVO_EXP == 12
+__device__ long long g_ws_trace[3 * 4096];
+#define WTRACE(slot, i)                                                                         \
+  do {                                                                                          \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (i) < 4096) g_ws_trace[(slot) * 4096 + (i)] = clock64(); \
+  } while (0)
+#else
+#define WTRACE(slot, i) (void)0
+#endif
 
 constexpr int WS_BQ = 128;
 constexpr int WS_BK = 64;
 constexpr int WS_THREADS = 352;
-constexpr float WS_RESCALE = 8.0f;  // log2 units: rescale O when the max grows by > 2^8
+constexpr float WS_RESCALE = 8.0f;
+
+  // log2 units: rescale O when the max grows by > 2^8
 
 template <int CP>
 struct WsSmem {
@@ -235,10 +254,12 @@ __global__ void __launch_bounds__(WS_THREADS, 1) attn_fwd_ws_kernel(AttnParams P
         if (j < nkt) {
           const int s = j % WS_NS, buf = j & 1;
           mbar_wait(&kv_full[s], (j / WS_NS) & 1);
+          if (w == 0) WTRACE(2, j * 8 + 0);
           fence_async_smem();
           // S[w][buf] last held P_{j-2} (written over S_{j-2}), read by PV_{j-2}: completion
           // #((j-2)/2) of o_done[w][buf]; the softmax read of S_{j-2} preceded its p_full
           if (j >= 2) mbar_wait(&o_done[w][buf], ((j - 2) >> 1) & 1);
+          if (w == 0) WTRACE(2, j * 8 + 1);
           tc_fence_after();
           for (int kk = 0; kk < ksteps; ++kk) {
             const uint64_t ad = make_sdesc(sb + SM::Q + w * SM::Q_BYTES + kk * 2 * (WS_BQ / 8) * 128,
@@ -252,6 +273,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) attn_fwd_ws_kernel(AttnParams P
         if (j >= 1) {
           const int jj = j - 1, s = jj % WS_NS, buf = jj & 1;
           mbar_wait(&p_full[w][buf], (jj >> 1) & 1);
+          if (w == 0) WTRACE(2, jj * 8 + 2);
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < WS_BK / 16; ++kk) {  // A = P_jj in TMEM: 16 keys per 8 columns
@@ -276,6 +298,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) attn_fwd_ws_kernel(AttnParams P
     if (P.bias && !per_key_bias && qi < L) brow = P.bias + b * P.bs0 + (int64_t)h * P.bs1 + (int64_t)qi * P.bs2;
     const float sl2 = P.scale_log2;
     float m_run = -INFINITY;  // running max in scaled log2 units
+    if (w == 1) named_bar_arrive(1, 256);  // warpgroup 0 takes the first turn
 
     for (int j = 0; j < nkt; ++j) {
       const int buf = j & 1;
@@ -295,12 +318,15 @@ __global__ void __launch_bounds__(WS_THREADS, 1) attn_fwd_ws_kernel(AttnParams P
           for (int kk = 0; kk < WS_BK; ++kk) bv[kk] = k0 + kk < L ? bf2f(brow[(int64_t)(k0 + kk) * P.bs3]) : 0.f;
         }
       }
+      if ((threadIdx.x & 127) == 0) WTRACE(w, j * 8 + 0);
       mbar_wait(&s_full[w][buf], (j >> 1) & 1);
+      if ((threadIdx.x & 127) == 0) WTRACE(w, j * 8 + 1);
       tc_fence_after();
       float sv[WS_BK];
       tmem_ld32(t_lane + (2 * w + buf) * WS_BK, sv);
       tmem_ld32(t_lane + (2 * w + buf) * WS_BK + 32, sv + 32);
       tmem_ld_wait();
+      if ((threadIdx.x & 127) == 0) WTRACE(w, j * 8 + 2);
 
       if (brow) {
 #pragma unroll
@@ -313,15 +339,18 @@ __global__ void __launch_bounds__(WS_THREADS, 1) attn_fwd_ws_kernel(AttnParams P
       }
       // row max as a tree (8 independent chains): a serial chain of dependent max ops is
       // latency-bound with only two softmax warps per scheduler
+      // (three-input max: 36 FMNMX3 for 64 keys)
       float m8[8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) m8[e] = fmaxf(sv[e], sv[e + 8]);
+      for (int e = 0; e < 8; ++e) m8[e] = fmax3f(sv[e], sv[e + 8], sv[e + 16]);
 #pragma unroll
-      for (int kk = 16; kk < WS_BK; kk += 16) {
+      for (int kk = 24; kk + 16 <= WS_BK; kk += 16) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) m8[e] = fmaxf(m8[e], fmaxf(sv[kk + e], sv[kk + 8 + e]));
+        for (int e = 0; e < 8; ++e) m8[e] = fmax3f(m8[e], sv[kk + e], sv[kk + 8 + e]);
       }
-      const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+#pragma unroll
+      for (int e = 0; e < 8; ++e) m8[e] = fmaxf(m8[e], sv[WS_BK - 8 + e]);
+      const float mx = fmax3f(fmax3f(m8[0], m8[1], m8[2]), fmax3f(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
       const float mxs = mx * sl2;
       // lazy rescale: a row whose max grew by more than 2^8 rescales its O row (and its row
       // sum, column CP) - warp-uniform because TMEM loads/stores are warp-collective
@@ -338,6 +367,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1) attn_fwd_ws_kernel(AttnParams P
         }
         m_run = m_new;
       }
+      if ((threadIdx.x & 127) == 0) WTRACE(w, j * 8 + 3);
+      // ping-pong: the two warpgroups take turns on the exp phase (the MUFU pipe), so one
+      // warpgroup's TMEM round trips and row max run under the other's exponentials
+      named_bar_sync(1 + w, 256);
+      if ((threadIdx.x & 127) == 0) WTRACE(w, j * 8 + 6);
       const float mref = m_run == -INFINITY ? 0.f : m_run;
       // P_j (bf16, 2 keys per 32-bit column) overwrites S_j in TMEM columns [0, 32) of the
       // buffer: this thread's row was read above, and S_{j+2} will not be issued into the
@@ -346,10 +380,13 @@ __global__ void __launch_bounds__(WS_THREADS, 1) attn_fwd_ws_kernel(AttnParams P
 #pragma unroll
       for (int kk = 0; kk < WS_BK; kk += 2)
         pk[kk / 2] = pack_bf16x2(ex2f(fmaf(sv[kk], sl2, -mref)), ex2f(fmaf(sv[kk + 1], sl2, -mref)));
+      if ((threadIdx.x & 127) == 0) WTRACE(w, j * 8 + 4);
       ws_tmem_st32(t_lane + (2 * w + buf) * WS_BK, pk);
+      if (w == 0 || j + 1 < nkt) named_bar_arrive(2 - w, 256);  // hand the turn over
       tmem_st_wait();
       tc_fence_before();
       ws_arrive(&p_full[w][buf]);
+      if ((threadIdx.x & 127) == 0) WTRACE(w, j * 8 + 5);
     }
     // epilogue: the last PV (j = nkt-1) is completion #((nkt-1)/2) of o_done[w][(nkt-1)&1]
     mbar_wait(&o_done[w][(nkt - 1) & 1], ((nkt - 1) >> 1) & 1);
@@ -411,6 +448,9 @@ int launch_attn_fwd_ws(const AttnParams& p, int64_t B, cudaStream_t st) {
   EVO_LAUNCH_CHECK("attention fwd (warp-specialised)");
   return EVO_OK;
 }
+#if EVO_EXP == 12
+extern "C" int evo_ws_trace(void* dst) { return (int)cudaMemcpyFromSymbol(dst, g_ws_trace, sizeof(g_ws_trace)); }
+#endif
 template int launch_attn_fwd_ws<16>(const AttnParams&, int64_t, cudaStream_t);
 template int launch_attn_fwd_ws<32>(const AttnParams&, int64_t, cudaStream_t);
 template int launch_attn_fwd_ws<64>(const AttnParams&, int64_t, cudaStream_t);

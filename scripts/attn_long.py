@@ -14,18 +14,23 @@ ap.add_argument("--pair-batch", type=int, default=0, help="batch for pair shape 
 a = ap.parse_args()
 lib = _lib.load()
 for n in a.n:
-    for name, B, H, bmode in (("pair_row", a.pair_batch or n, 4, "key"), ("msa_row", 128, 8, "full")):
+    for name, B, H, bmode in (("pair_row", a.pair_batch or n, 4, "key"), ("pair_col", a.pair_batch or n, 4, "key"),
+                              ("msa_row", 128, 8, "full")):
         L, c = n, 32
         ld = 3 * H * c + (8 if bmode == "key" else 0)
         qkv = torch.randn(B * L, ld, device="cuda").bfloat16()
         gp = torch.randn(B * L, H * c, device="cuda").bfloat16()
         og = torch.empty(B * L, H * c, device="cuda", dtype=torch.bfloat16); orw = torch.empty_like(og)
         lse = torch.empty(B, H, L, device="cuda")
-        S = lambda t, w, off=0: Strided(t, L * w, w, off)
+        if name == "pair_col":  # rows of one sequence B * ld apart (the pair grid's column axis)
+            S = lambda t, w, off=0: Strided(t, w, B * w, off)
+        else:
+            S = lambda t, w, off=0: Strided(t, L * w, w, off)
         if bmode == "full":
             bias = torch.randn(H, L, L, device="cuda").bfloat16(); bs = (0, L * L, L, 1); boff = 0
         else:
-            bias = qkv; bs = (L * ld, 1, 0, ld); boff = 3 * H * c
+            bias = qkv; boff = 3 * H * c
+            bs = (ld, 1, 0, B * ld) if name == "pair_col" else (L * ld, 1, 0, ld)
         res = {}
         for kern, fl_ in (("ws", _lib.EVO_ATTN_FORCE_WS), ("flash", _lib.EVO_ATTN_FORCE_FLASH)):
             d = ops.attention_desc(S(qkv, ld, 0), S(qkv, ld, H * c), S(qkv, ld, 2 * H * c), S(gp, H * c),
