@@ -144,10 +144,6 @@ __device__ __forceinline__ uint64_t bw_sw64_mn(uint32_t saddr) {
   return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(4096 >> 4) << 16) | ((uint64_t)(512 >> 4) << 32) |
          (1ull << 46) | (4ull << 61);
 }
-__device__ __forceinline__ void bulk_ld(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-               ::"r"(dst), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
 
 struct BwdMaps {  // tensor maps of the per-tile operands (TMA path): element (d, h, l, b)
   CUtensorMap q, k, v, dO;

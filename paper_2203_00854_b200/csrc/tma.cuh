@@ -39,6 +39,11 @@ __device__ __forceinline__ void tma_st3(uint64_t m, uint32_t src, int c0, int c1
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n"
                ::"l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(src) : "memory");
 }
+// 1-D bulk copy global -> shared (16-byte aligned, size a multiple of 16), completing on bar
+__device__ __forceinline__ void bulk_ld(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(dst), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 // wait until at most N committed bulk groups still READ their shared-memory source
 template <int N>
