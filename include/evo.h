@@ -289,6 +289,11 @@ int evo_bias_act_bwd(const void* dh, const void* h, void* dy, float* dbias, int6
 /* number of non-finite elements of x (fp32 counter, accumulated) - the GPU twin of
  * softmax_raw's DomainError check (engine.py:186-187) */
 int evo_count_nonfinite(const void* x, int dtype, int64_t n, unsigned int* counter, void* stream);
+/* Per-key (pair) bias gradient into the bias columns of the fused qkv gradient (the per-key
+ * bias is the 4 extra projection columns of _pair_bias_fn, evoformer.py:287-292):
+ * dst[b*dst_sb + l*dst_sl + h] = bf16(dbias[(b*nh + h)*L + l]) for h < nh, 0 for nh <= h < cols. */
+int evo_key_bias_grad_cols(const float* dbias, int64_t B, int nh, int64_t L, void* dst, int64_t dst_sb,
+                           int64_t dst_sl, int cols, void* stream);
 
 #ifdef __cplusplus
 }

@@ -94,6 +94,7 @@ _SIGS = {
     "evo_bias_act_fwd": [vp, vp, i64, i64, C.c_int, C.c_int, vp],
     "evo_bias_act_bwd": [vp, vp, vp, vp, i64, i64, C.c_int, C.c_int, vp],
     "evo_count_nonfinite": [vp, C.c_int, i64, vp, vp],
+    "evo_key_bias_grad_cols": [vp, i64, C.c_int, i64, vp, i64, i64, C.c_int, vp],
     "evo_colsum": [vp, C.c_int, i64, i64, i64, vp, vp],
     "evo_gate_mul_fwd": [vp, i64, C.c_int, vp, i64, vp, vp, i64, C.c_int, i64, i64, vp],
 }

@@ -187,7 +187,8 @@ def attention_bwd(bp: BlockParams, sv: Saved, dx_new, next_db=None, db_done=Fals
     sbr, slr = _attn_geometry(kind, B, L)
     S = lambda t, ld, off=0: Strided(t, sbr * ld, slr * ld, off)
     dqkv = torch.empty(rows, ldq, device=dev, dtype=BF16)
-    if ldq > 3 * nh * c:
+    pair_bias = isinstance(sv["bias"], str) and sv["bias"] == "pair"
+    if ldq > 3 * nh * c and not pair_bias:  # (pair: the padding is written with the bias columns)
         dqkv[:, 3 * nh * c:].zero_()
     dgpre = torch.empty(rows, nh * c, device=dev, dtype=BF16)
     bias = sv["bias"]
@@ -202,12 +203,9 @@ def attention_bwd(bp: BlockParams, sv: Saved, dx_new, next_db=None, db_done=Fals
                      device=dev, dtype=torch.uint8)
     ops.attention_bwd(sv["desc"], S(dog, nh * c), S(dqkv, ldq, 0), S(dqkv, ldq, nh * c), S(dqkv, ldq, 2 * nh * c),
                       S(dgpre, nh * c), ws, dbias=dbias, dbias_s=dbs)
-    if isinstance(bias, str) and bias == "pair":
-        cols = dqkv[:, 3 * nh * c:3 * nh * c + nh]
-        if kind == "row":
-            cols.view(B, L, nh).copy_(dbias.permute(0, 2, 1))
-        else:
-            cols.view(L, B, nh).copy_(dbias.permute(2, 0, 1))
+    if pair_bias:
+        # fp32 [B, nh, L] -> the bias columns of dqkv (bf16) + zeroed row padding, one pass
+        ops.key_bias_grad_cols(dbias, B, nh, L, S(dqkv, ldq, 3 * nh * c), ldq - 3 * nh * c)
     _wgrad(sv["ln"], dqkv, g[f"{mod}.w_qkv"])
     _bgrad(dqkv, g[f"{mod}.b_qkv"])
     _wgrad(sv["x"], dgpre, g[f"{mod}.w_g"])
@@ -372,7 +370,8 @@ def opm_contract(a2d, b2d, S: int, I: int, J: int, P: int):
 
 
 def opm_bwd(bp: BlockParams, sv: Saved, dz_new, dm, reduce_scatter=None, next_db=None, db_done=False):
-    """accumulates the OPM contribution into dm (bf16 [S*R, Hm]); dz passes through.
+    """returns dm + the OPM's input gradient as a NEW bf16 [S*R, Hm] tensor (dm is only read, so
+    the caller's gradient needs no defensive copy); dz passes through.
     next_db: bias gradient of the module consuming dm (fused column sums of the final dm)."""
     cfg = bp.cfg
     P, Hm, Hz = cfg.hidden_proj, cfg.h_msa, cfg.h_pair
@@ -397,8 +396,7 @@ def opm_bwd(bp: BlockParams, sv: Saved, dz_new, dm, reduce_scatter=None, next_db
             pending = reduce_scatter(dbf, async_op=True)
             ops.opm_bwd_factor(0, dz_new, w_o, sv["b_t"], R, Rj, S, P, Hz, 1.0 / S, dab, R * 2 * P, 0, 2 * P)
             dab[:, P:].copy_(pending().view(S * R, P))
-        _opm_proj_bwd(bp, sv, dab, dm, next_db)
-        return
+        return _opm_proj_bwd(bp, sv, dab, dm, next_db)
     do = _mm(dz_new, h["opm.w_o"].t())                               # [R*Rj, P*P] == [i][j][p][q]
     ab = sv["ab"]                                                    # [a | b], or a alone under DAP
     dO_A = Mat(do, lo=(P, 1), split=(P, P), hi=(Rj * P * P, P * P))
@@ -425,18 +423,18 @@ def opm_bwd(bp: BlockParams, sv: Saved, dz_new, dm, reduce_scatter=None, next_db
             Bb = Mat(sv["bsrc"], lo=(R * P, 1), split=(0, R * P), hi=(0, S * R * P))
         ops.bgemm(dO_A, Bb, Cda, 1, R * P, S, Rj * P, alpha=1.0 / S)
         dab[:, P:].copy_(pending().view(S * R, P))
-    _opm_proj_bwd(bp, sv, dab, dm, next_db)
+    return _opm_proj_bwd(bp, sv, dab, dm, next_db)
 
 
 def _opm_proj_bwd(bp: BlockParams, sv: Saved, dab, dm, next_db):
-    """backward of the [a | b] projection and the OPM's input LayerNorm (dm accumulates)"""
+    """backward of the [a | b] projection and the OPM's input LayerNorm: returns dm + dLN/dm"""
     Hm, S, R = bp.cfg.h_msa, sv["S"], sv["R"]
     h, f, g = bp.h, bp.f, bp.g
     _wgrad(sv["ln"], dab, g["opm.w_ab"])
     _bgrad(dab, g["opm.b_ab"])
     dln = _mm(dab, h["opm.w_ab"].t())
-    ops.layernorm_bwd(dln, sv["m"], f["opm.ln_g"], sv["mean"], sv["rstd"], S * R, Hm, dx=dm, accumulate=True,
-                      dgamma=g["opm.ln_g"], dbeta=g["opm.ln_b"], dx_colsum=next_db)
+    return ops.layernorm_bwd(dln, sv["m"], f["opm.ln_g"], sv["mean"], sv["rstd"], S * R, Hm, res=dm,
+                             dgamma=g["opm.ln_g"], dbeta=g["opm.ln_b"], dx_colsum=next_db)
 
 
 # ----------------------------------------------------------------------------- triangle update
@@ -617,8 +615,7 @@ def block_bwd(bp: BlockParams, saved, dm, dz, join=True):
     dz2, _ = attention_bwd(bp, s7, dz2, db_done=fuse)
     dz2 = triangle_bwd(bp, s6, dz2)
     dz2 = triangle_bwd(bp, s5, dz2, next_db=nd("opm.b_o"))
-    dm2 = dm2.clone()
-    opm_bwd(bp, s4, dz2, dm2, next_db=nd("msa_trans.b2"), db_done=fuse)
+    dm2 = opm_bwd(bp, s4, dz2, dm2, next_db=nd("msa_trans.b2"), db_done=fuse)
     dm2 = transition_bwd(bp, s3, dm2, next_db=nd("msa_col.b_o"), db_done=fuse)
     dm2, _ = attention_bwd(bp, s2, dm2, next_db=nd("msa_row.b_o"), db_done=fuse)
     dm2, dbias = attention_bwd(bp, s1, dm2, db_done=fuse)

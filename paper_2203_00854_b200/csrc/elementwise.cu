@@ -719,3 +719,37 @@ extern "C" int evo_gate_mul_fwd(const void* gate, int64_t gate_rs, int gate_act,
   EVO_LAUNCH_CHECK("gate_mul fwd");
   return EVO_OK;
 }
+
+// Per-key bias gradient (fp32 [B][nh][L], accumulated by the attention backward) into the bias
+// columns of the qkv gradient: dst[b, l, h] = bf16(dbias[b, h, l]) for h < nh, 0 for nh <= h <
+// cols (the row padding of the fused projection).  One thread per (b, l): nh coalesced reads
+// across the warp, one 16-byte store for the usual 8 columns.
+__global__ void __launch_bounds__(256) key_bias_cols_k(const float* __restrict__ dbias, int64_t B, int nh, int64_t L,
+                                                       bf16* __restrict__ dst, int64_t sb, int64_t sl, int cols) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B * L) return;
+  const int64_t b = i / L, l = i - b * L;
+  bf16* d = dst + b * sb + l * sl;
+  float v[8];
+#pragma unroll
+  for (int h = 0; h < 8; ++h) v[h] = h < nh ? dbias[(b * nh + h) * L + l] : 0.f;
+  if (cols == 8 && ((uintptr_t)d & 15) == 0) {
+    uint4 u;
+    u.x = pack_bf16x2(v[0], v[1]); u.y = pack_bf16x2(v[2], v[3]);
+    u.z = pack_bf16x2(v[4], v[5]); u.w = pack_bf16x2(v[6], v[7]);
+    *reinterpret_cast<uint4*>(d) = u;
+  } else {
+    for (int h = 0; h < cols; ++h) d[h] = f2bf(h < 8 ? v[h] : (h < nh ? dbias[(b * nh + h) * L + l] : 0.f));
+  }
+}
+
+extern "C" int evo_key_bias_grad_cols(const float* dbias, int64_t B, int nh, int64_t L, void* dst, int64_t dst_sb,
+                                      int64_t dst_sl, int cols, void* stream) {
+  EVO_CHECK_ARG(dbias && dst, EVO_ERR_ARG, "key_bias_grad_cols: null pointer");
+  EVO_CHECK_ARG(B >= 0 && L >= 0 && nh >= 1 && cols >= nh, EVO_ERR_SHAPE, "key_bias_grad_cols: bad extents");
+  if (B * L == 0) return EVO_OK;
+  key_bias_cols_k<<<grid_for(B * L, 256), 256, 0, (cudaStream_t)stream>>>(dbias, B, nh, L, (bf16*)dst, dst_sb, dst_sl,
+                                                                          cols);
+  EVO_LAUNCH_CHECK("key_bias_grad_cols");
+  return EVO_OK;
+}

@@ -411,8 +411,7 @@ def dap_block_bwd(bp, comm: DapComm, sv, dm_loc, dz_loc):
     dz2 = B.triangle_bwd(bp, sv["tri_in"], dz_c.reshape(R * Rl, Hz).contiguous(), reduce_scatter=rs)
     dz_r = switch_cols_to_rows(comm, dz2.view(R, Rl, Hz))             # inverse of step 5
     dz2 = B.triangle_bwd(bp, sv["tri_out"], dz_r.reshape(Rl * R, Hz).contiguous(), reduce_scatter=rs)
-    dm2 = dm_r_ready().reshape(S * Rl, Hm).contiguous().clone()
-    B.opm_bwd(bp, sv["opm"], dz2, dm2, reduce_scatter=rs)
+    dm2 = B.opm_bwd(bp, sv["opm"], dz2, dm_r_ready().reshape(S * Rl, Hm).contiguous(), reduce_scatter=rs)
     dm2 = B.transition_bwd(bp, sv["msa_trans"], dm2)
     dm2, _ = B.attention_bwd(bp, sv["msa_col"], dm2)
     dm_s = switch_cols_to_rows(comm, dm2.view(S, Rl, Hm))             # inverse of step 2

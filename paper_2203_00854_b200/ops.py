@@ -206,6 +206,14 @@ def attention_fwd(desc: EvoAttnDesc):
     call("evo_gated_attention_fwd", C.byref(desc), stream_handle(), work=_attn_work(desc))
 
 
+def key_bias_grad_cols(dbias, B, nh, L, dst: Strided, cols: int):
+    """dst[b, l, h] = bf16(dbias[b, h, l]) for h < nh and 0 for nh <= h < cols (dbias fp32
+    [B, nh, L] contiguous): the per-key bias gradient into the bias columns of dqkv."""
+    _cuda(dbias)
+    call("evo_key_bias_grad_cols", _p(dbias), B, nh, L, dst.ptr(), dst.sb, dst.sl, cols, stream_handle())
+    return dst
+
+
 def attention_bwd_workspace(B, L, H, c, batch_reduced_bias=False) -> int:
     return int(_lib.load().evo_gated_attention_bwd_workspace(B, L, H, c, int(batch_reduced_bias)))
 

@@ -128,6 +128,17 @@ def attention_bwd_workspace(B, L, H, c, batch_reduced_bias=False):
     return 1
 
 
+def key_bias_grad_cols(dbias, B, nh, L, dst, cols):
+    v = torch.zeros(B, L, cols, dtype=torch.float32)
+    v[..., :nh] = dbias.permute(0, 2, 1)
+    _blhc_cols(dst, B, L, cols).copy_(v)
+    return dst
+
+
+def _blhc_cols(s, B, L, cols):
+    return _sv(s.t, s.offset, (B, L, cols), (s.sb, s.sl, 1))
+
+
 def attention_bwd(fdesc, dout, dq, dk, dv, dg, workspace, dbias=None, dbias_s=(0, 0, 0, 0)):
     d = fdesc
     B, L, H, c = d.B, d.L, d.H, d.c
@@ -324,7 +335,7 @@ def gate_mul(gate, y=None, bias=None, act=1, rows=None, cols=None, gate_rs=None,
 NAMES = ["gate_mul", "layernorm_fwd", "layernorm_bwd", "layernorm_rowdot_fwd", "attention_desc", "attention_fwd",
          "attention_bwd_workspace", "attention_bwd", "bgemm", "softmax_fwd", "count_nonfinite", "opm_fused_supported", "opm_transpose", "opm_bwd_supported", "opm_bwd_factor",
          "opm_fused_fwd", "tri_gate_fwd", "tri_gate_bwd",
-         "gated_residual_fwd", "gated_residual_bwd", "bias_act_fwd", "bias_act_bwd"]
+         "gated_residual_fwd", "gated_residual_bwd", "bias_act_fwd", "bias_act_bwd", "key_bias_grad_cols"]
 
 
 def install():

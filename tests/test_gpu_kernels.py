@@ -532,3 +532,18 @@ def test_opm_bwd_factor(I, J, S, Hz):
     assert torch.count_nonzero(dab[..., P:]) == 0  # the other half of the buffer untouched
     db = torch.cat([dbf[0], dbf[1]], dim=1)
     assert rel(db, db_ref) < 1e-4, rel(db, db_ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["row", "col"])
+def test_key_bias_grad_cols(kind, B=5, L=37, nh=4, ld=3 * 4 * 32 + 8):
+    """per-key bias gradient fp32 [B, nh, L] -> bias columns + zeroed padding of a strided dqkv"""
+    db = torch.randn(B, nh, L, device=DEV)
+    dqkv = torch.full((B * L, ld), float("nan"), device=DEV, dtype=torch.bfloat16)
+    sb, sl = (L * ld, ld) if kind == "row" else (ld, B * ld)
+    ops.key_bias_grad_cols(db, B, nh, L, Strided(dqkv, sb, sl, ld - 8), 8)
+    torch.cuda.synchronize()
+    v = dqkv.view(-1)[ld - 8:].as_strided((B, L, 8), (sb, sl, 1)).float()
+    assert torch.equal(v[..., :nh], db.permute(0, 2, 1).bfloat16().float())
+    assert (v[..., nh:] == 0).all()
+    assert torch.isnan(dqkv[:, :ld - 8].float()).all()

@@ -95,7 +95,7 @@ def test_submodule_backward(mod):
             zt = dev(z).view(R * R, -1)
             out, sv = B.opm_fwd(bp, dev(m).view(S * R, -1), zt, S, R)
             dm = torch.zeros(S * R, cfg.h_msa, device="cuda", dtype=torch.bfloat16)
-            B.opm_bwd(bp, sv, dev(g).view(R * R, -1), dm)
+            dm = B.opm_bwd(bp, sv, dev(g).view(R * R, -1), dm)
             errs = {"dx": rel(dm.double().cpu().view(x.shape), ref_dx)}
         else:
             g = rng.normal(size=x.shape)
