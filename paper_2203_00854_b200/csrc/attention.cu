@@ -396,7 +396,11 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1
             unpack_bf16x2(w.x, t[0], t[1]); unpack_bf16x2(w.y, t[2], t[3]);
             unpack_bf16x2(w.z, t[4], t[5]); unpack_bf16x2(w.w, t[6], t[7]);
 #pragma unroll
-            for (int e = 0; e < 8; ++e) s[kk + e] += t[e];
+            for (int e = 0; e < 8; e += 2) {  // FADD2
+              const float2 r = __fadd2_rn(make_float2(s[kk + e], s[kk + e + 1]), make_float2(t[e], t[e + 1]));
+              s[kk + e] = r.x;
+              s[kk + e + 1] = r.y;
+            }
           }
         } else {
 #pragma unroll
@@ -447,7 +451,9 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           const int kk = half * 32 + 2 * e;
-          pk[e] = pack_bf16x2(ex2f(fmaf(s[kk], P.scale_log2, -mref)), ex2f(fmaf(s[kk + 1], P.scale_log2, -mref)));
+          const float2 y = __ffma2_rn(make_float2(s[kk], s[kk + 1]), make_float2(P.scale_log2, P.scale_log2),
+                                      make_float2(-mref, -mref));  // FFMA2
+          pk[e] = pack_bf16x2(ex2f(y.x), ex2f(y.y));
         }
         tmem_st16(t_row + half * 16, reinterpret_cast<const float*>(pk));
       }

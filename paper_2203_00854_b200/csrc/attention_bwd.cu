@@ -578,12 +578,16 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
           *reinterpret_cast<float4*>(lse16 + e) = *reinterpret_cast<const float4*>(s_lse + qc + e);
           *reinterpret_cast<float4*>(D16 + e) = *reinterpret_cast<const float4*>(s_D + qc + e);
         }
+        // packed fp32x2 math (FFMA2 / FADD2 / FMUL2): half the issue slots of the scalar form
+        const float2 sl2 = make_float2(F.scale_log2, F.scale_log2);
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          float x = s[e];
-          if constexpr (MODE == 1) x += kbias;
-          if constexpr (MODE == 2 || MODE == 3) x += bv[e];
-          pv[e] = ex2f(fmaf(x, F.scale_log2, -lse16[e]));
+        for (int e = 0; e < 16; e += 2) {
+          float2 x = make_float2(s[e], s[e + 1]);
+          if constexpr (MODE == 1) x = __fadd2_rn(x, make_float2(kbias, kbias));
+          if constexpr (MODE == 2 || MODE == 3) x = __fadd2_rn(x, make_float2(bv[e], bv[e + 1]));
+          const float2 y = __ffma2_rn(x, sl2, make_float2(-lse16[e], -lse16[e + 1]));
+          pv[e] = ex2f(y.x);
+          pv[e + 1] = ex2f(y.y);
         }
         if (!all_valid) {
 #pragma unroll
@@ -591,14 +595,21 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
             if (!(kvalid && q0 + qc + e < L)) pv[e] = 0.f;
         }
 #pragma unroll
-        for (int e = 0; e < 16; ++e) dsv[e] = pv[e] * (dp[e] - D16[e]);
+        for (int e = 0; e < 16; e += 2) {
+          const float2 d = __fmul2_rn(make_float2(pv[e], pv[e + 1]),
+                                      f2sub(make_float2(dp[e], dp[e + 1]), make_float2(D16[e], D16[e + 1])));
+          dsv[e] = d.x;
+          dsv[e + 1] = d.y;
+        }
 #if EVO_EXP == 1
 #pragma unroll
         for (int e = 0; e < 16; ++e) { pv[e] = s[e]; dsv[e] = dp[e]; }
 #endif
         if constexpr (MODE == 1) {
+          float2 k2 = make_float2(0.f, 0.f);
 #pragma unroll
-          for (int e = 0; e < 16; ++e) kb_acc += dsv[e];
+          for (int e = 0; e < 16; e += 2) k2 = __fadd2_rn(k2, make_float2(dsv[e], dsv[e + 1]));
+          kb_acc += k2.x + k2.y;
         } else if constexpr (MODE == 3) {
           if (dbias_col) {
 #pragma unroll

@@ -379,7 +379,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1) attn_fwd_ws_kernel(AttnParams P
       uint32_t pk[WS_BK / 2];
 #pragma unroll
       for (int kk = 0; kk < WS_BK; kk += 2)
-        pk[kk / 2] = pack_bf16x2(ex2f(fmaf(sv[kk], sl2, -mref)), ex2f(fmaf(sv[kk + 1], sl2, -mref)));
+      {
+        const float2 y = __ffma2_rn(make_float2(sv[kk], sv[kk + 1]), make_float2(sl2, sl2), make_float2(-mref, -mref));
+        pk[kk / 2] = pack_bf16x2(ex2f(y.x), ex2f(y.y));
+      }
       if ((threadIdx.x & 127) == 0) WTRACE(w, j * 8 + 4);
       ws_tmem_st32(t_lane + (2 * w + buf) * WS_BK, pk);
       if (w == 0 || j + 1 < nkt) named_bar_arrive(2 - w, 256);  // hand the turn over

@@ -64,6 +64,15 @@ __device__ __forceinline__ void trace(int idx) {
 #else
 #define TRACE(i) (void)0
 #endif
+#if EVO_EXP == 4
+__device__ long long g_opmb_trace[4096];
+#define BTR(i)                                                          \
+  do {                                                                  \
+    if (blockIdx.x == 0 && (i) < 4096) g_opmb_trace[(i)] = clock64();   \
+  } while (0)
+#else
+#define BTR(i) (void)0
+#endif
 
 struct OpmArgs {
   int I, J, S;
@@ -490,8 +499,11 @@ __global__ void __launch_bounds__(OB_THREADS, 1)
       for (int t = 0; t <= n; ++t) {
         if (t < n) {  // GEMM_A of step t
           const int s_ = st + t, b = s_ & 1;
+          if (lane == 0) BTR(s_ * 8 + 0);
           mbar_wait(&dy_full[b], (s_ >> 1) & 1);
+          if (lane == 0) BTR(s_ * 8 + 1);
           mbar_wait(&da_empty[b], ((s_ >> 1) & 1) ^ 1);
+          if (lane == 0) BTR(s_ * 8 + 2);
           tc_fence_after();
           if (lane == 0) {
             for (int kk = 0; kk < 4 * HH; ++kk) {
@@ -507,9 +519,12 @@ __global__ void __launch_bounds__(OB_THREADS, 1)
         }
         if (t > 0) {  // GEMM_B of step t-1 (its conversion overlapped GEMM_A of step t)
           const int s_ = st + t - 1, b = s_ & 1;
+          if (lane == 0) BTR(s_ * 8 + 3);
           if (t == 1) mbar_wait(&acc_empty, (it & 1) ^ 1);
           mbar_wait(&ab_full[b], (s_ >> 1) & 1);
+          if (lane == 0) BTR(s_ * 8 + 4);
           mbar_wait(&ot_full[b], (s_ >> 1) & 1);
+          if (lane == 0) BTR(s_ * 8 + 5);
           tc_fence_after();
           if (lane == 0) {
 #pragma unroll
@@ -542,6 +557,7 @@ __global__ void __launch_bounds__(OB_THREADS, 1)
         mbar_wait(&da_full[b], ph);
         tc_fence_after();
         mbar_wait(&ab_empty[b], ph ^ 1);
+        if (threadIdx.x == 128) BTR(st * 8 + 6);
         const uint32_t ab = sAB + (2 * b + (yq >> 1)) * OB_T;
 #pragma unroll
         for (int pp = 0; pp < 4; pp += 2) {
@@ -563,6 +579,7 @@ __global__ void __launch_bounds__(OB_THREADS, 1)
           }
         }
         tc_fence_before();
+        if (threadIdx.x == 128) BTR(st * 8 + 7);
         mbar_arrive(&da_empty[b]);
         fence_async_smem();
         mbar_arrive(&ab_full[b]);
@@ -672,6 +689,9 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tw, 
 }  // namespace
 }  // namespace evo
 
+#if EVO_EXP == 4
+extern "C" int evo_opmb_trace(void* dst) { return (int)cudaMemcpyFromSymbol(dst, evo::g_opmb_trace, sizeof(evo::g_opmb_trace)); }
+#endif
 #if EVO_EXP == 3
 extern "C" int evo_opm_trace(void* dst) { return (int)cudaMemcpyFromSymbol(dst, evo::g_opm_trace, sizeof(evo::g_opm_trace)); }
 #endif
