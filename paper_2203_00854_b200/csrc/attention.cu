@@ -129,6 +129,15 @@ __device__ __forceinline__ void att_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uin
 #ifndef EVO_EXP
 #define EVO_EXP 0
 #endif
+#if EVO_EXP == 5
+__device__ long long g_fwd_trace[4096];
+#define FTR(i)                                                                              \
+  do {                                                                                      \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (i) < 4096) evo::g_fwd_trace[(i)] = clock64(); \
+  } while (0)
+#else
+#define FTR(i) (void)0
+#endif
 int sm_count();
 
 // TMA path (head dim 32): tensor maps whose boxes land exactly in the canonical (SWIZZLE_NONE)
@@ -296,6 +305,7 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1
     for (int j = 0; j < nkt; ++j, ++gt) {
       const int k0 = j * ATT_BK;
       const int st = gt & 1;
+      FTR(gt * 8 + 0);
       cp_async_wait<0>();
       if (tmaq) {
         mbar_wait(&kv_full[st], (gt >> 1) & 1);
@@ -303,6 +313,7 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1
       }
       fence_async_smem();
       __syncthreads();
+      FTR(gt * 8 + 1);
       // prefetch into the other stage (its MMAs finished last iteration): this unit's next
       // K/V tile, or on the last tile the next unit's first K/V tile
       const uint32_t kdst = sb + SM::KT + (st ^ 1) * SM::K_BYTES, vdst = sb + SM::VT + (st ^ 1) * SM::V_BYTES;
@@ -356,6 +367,7 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1
       }
       // bar_s completes after S, which was issued after the previous PV completed: O is stable
       mbar_wait(&bar_s, gt & 1);
+      FTR(gt * 8 + 2);
       tc_fence_after();
       if (j + 1 == nkt && has_next) {  // Q is free: this unit's last S MMA has completed
         if (tmaq) {
@@ -461,8 +473,10 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1
       if (per_key_bias && threadIdx.x < ATT_BK && (j + 1 < nkt || has_next))
         st_shared_v4(sb + SM::KT + (st ^ 1) * SM::K_BYTES + kmajor_off(threadIdx.x, CP, ATT_BK), nb, 0u, 0u, 0u);
       tmem_st_wait();
+      FTR(gt * 8 + 3);
       tc_fence_before();
       __syncthreads();
+      FTR(gt * 8 + 4);
       if (threadIdx.x == 0) {
         tc_fence_after();
 #pragma unroll
@@ -477,7 +491,9 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1
     }
     // O and l of this row (the next unit's first PV overwrites O only after the __syncthreads
     // at the top of its first tile, which every thread reaches after these TMEM loads)
+    FTR((gt - 1) * 8 + 5);
     mbar_wait(&bar_o, (gt - 1) & 1);
+    FTR((gt - 1) * 8 + 6);
     tc_fence_after();
     float o_acc[CV];
 #pragma unroll
@@ -531,6 +547,7 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1
       }
       if (P.lse) P.lse[(b * P.H + h) * (int64_t)L + qi] = (m_run + log2f(l_run)) * 0.6931471805599453f;
     }
+    FTR((gt - 1) * 8 + 7);
     u = nu;
     cur = nxt;
     ++ui;
@@ -686,6 +703,9 @@ int launch_attn_fwd_ws(const AttnParams& p, int64_t B, cudaStream_t st);
 constexpr int kWsMinLen = 4096;  // measured: faster than attn_fwd_kernel from N_r = 4096 on (per-key/no bias)
 }  // namespace evo
 
+#if EVO_EXP == 5
+extern "C" int evo_fwd_trace(void* dst) { return (int)cudaMemcpyFromSymbol(dst, evo::g_fwd_trace, sizeof(evo::g_fwd_trace)); }
+#endif
 extern "C" int evo_gated_attention_fwd(const EvoAttnDesc* d, void* stream) {
   AttnParams p;
   int rc = attn_params_from_desc(d, p);

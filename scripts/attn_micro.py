@@ -11,6 +11,7 @@ ap.add_argument("--variant", default="all")
 ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--bwd", type=int, default=1)
 ap.add_argument("--fb", type=int, default=1, help="forward: stage a full bias through smem (A/B switch)")
+ap.add_argument("--fwd-trace-dump", default="", help="EVO_EXP=5 builds: dump the forward tile trace (numpy)")
 ap.add_argument("--trace-dump", default="", help="EVO_EXP=10 builds: dump the backward phase trace (numpy)")
 a = ap.parse_args()
 from paper_2203_00854_b200 import _lib
@@ -71,3 +72,8 @@ if a.trace_dump:
     buf = np.zeros(8192, dtype=np.uint64)
     _lib.load().evo_bwd_trace(buf.ctypes.data_as(ctypes.c_void_p))
     np.save(a.trace_dump, buf)
+if a.fwd_trace_dump:
+    import ctypes, numpy as np
+    buf = np.zeros(4096, dtype=np.int64)
+    _lib.load().evo_fwd_trace(buf.ctypes.data_as(ctypes.c_void_p))
+    np.save(a.fwd_trace_dump, buf)
