@@ -488,6 +488,159 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_grp(const TD* __restrict__ dy, 
   }
 }
 
+// ------------------------------------------------------------- channel-major rows, tiled
+// x channel-major (element (r, c) at x[c * x_cs + r], the triangle update's t[p][i][j]): a CTA stages
+// a [C][128-row] tile with 16-byte loads (every byte of the tile in flight at once, unlike a
+// thread-per-row kernel's 2-byte strided loads), one thread per row computes from shared memory,
+// and the row-major output tile leaves as contiguous 16-byte chunks.
+constexpr int CM_RT = 128;  // rows per CTA (one per thread)
+
+template <int C>
+__device__ __forceinline__ void cm_load_tile(bf16 (*xs)[CM_RT + 8], const bf16* __restrict__ x, int64_t x_cs,
+                                             int64_t r0, int nr) {
+  for (int i = threadIdx.x; i < C * CM_RT / 8; i += CM_RT) {
+    const int c = i / (CM_RT / 8), r8 = (i % (CM_RT / 8)) * 8;
+    const bf16* src = x + c * x_cs + r0 + r8;
+    if (r8 + 8 <= nr) {
+      *reinterpret_cast<uint4*>(&xs[c][r8]) = *reinterpret_cast<const uint4*>(src);
+    } else {
+      for (int e = 0; e < 8; ++e) xs[c][r8 + e] = r8 + e < nr ? src[e] : __float2bfloat16(0.f);
+    }
+  }
+}
+
+template <int C>
+__global__ void __launch_bounds__(CM_RT) ln_fwd_cm(const bf16* __restrict__ x, int64_t x_cs,
+                                                   const float* __restrict__ gamma, const float* __restrict__ beta,
+                                                   bf16* __restrict__ y, float* __restrict__ mean_out,
+                                                   float* __restrict__ rstd_out, int64_t rows, float eps) {
+  __shared__ __align__(16) bf16 xs[C][CM_RT + 8];
+  __shared__ __align__(16) bf16 ys[CM_RT][C + 8];
+  const int t = threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.x * CM_RT;
+  const int nr = rows - r0 < CM_RT ? (int)(rows - r0) : CM_RT;
+  cm_load_tile<C>(xs, x, x_cs, r0, nr);
+  __syncthreads();
+  if (t < nr) {
+    float v[C];
+    float s = 0.f;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      v[c] = __bfloat162float(xs[c][t]);
+      s += v[c];
+    }
+    const float mu = s * (1.0f / C);
+    float q = 0.f;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      v[c] -= mu;
+      q += v[c] * v[c];
+    }
+    const float rs = rsqrtf(q * (1.0f / C) + eps);
+#pragma unroll
+    for (int c = 0; c < C; c += 8) {
+      float o[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] = v[c + e] * rs * gamma[c + e] + beta[c + e];
+      uint4 u;
+      u.x = pack_bf16x2(o[0], o[1]); u.y = pack_bf16x2(o[2], o[3]);
+      u.z = pack_bf16x2(o[4], o[5]); u.w = pack_bf16x2(o[6], o[7]);
+      *reinterpret_cast<uint4*>(&ys[t][c]) = u;
+    }
+    if (mean_out) mean_out[r0 + t] = mu;
+    if (rstd_out) rstd_out[r0 + t] = rs;
+  }
+  __syncthreads();
+  for (int i = t; i < nr * (C / 8); i += CM_RT) {
+    const int r = i / (C / 8), c8 = (i % (C / 8)) * 8;
+    *reinterpret_cast<uint4*>(y + (r0 + r) * C + c8) = *reinterpret_cast<const uint4*>(&ys[r][c8]);
+  }
+}
+
+// backward: dy row-major [rows][C], x / dx / res channel-major; dgamma / dbeta per CTA + atomics
+template <int C>
+__global__ void __launch_bounds__(CM_RT) ln_bwd_cm(const bf16* __restrict__ dy, const bf16* __restrict__ x,
+                                                   int64_t x_cs, const float* __restrict__ gamma,
+                                                   const float* __restrict__ mean, const float* __restrict__ rstd,
+                                                   bf16* dx, const bf16* res, float* __restrict__ dgamma,
+                                                   float* __restrict__ dbeta, int64_t rows) {
+  __shared__ __align__(16) bf16 xs[C][CM_RT + 8];   // x, then dx (channel-major)
+  __shared__ __align__(16) bf16 ds[CM_RT][C + 8];   // dy (row-major)
+  __shared__ float red[C][CM_RT + 1];                // per-row dgamma / dbeta terms, summed per channel
+  const int t = threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.x * CM_RT;
+  const int nr = rows - r0 < CM_RT ? (int)(rows - r0) : CM_RT;
+  cm_load_tile<C>(xs, x, x_cs, r0, nr);
+  for (int i = t; i < nr * (C / 8); i += CM_RT) {
+    const int r = i / (C / 8), c8 = (i % (C / 8)) * 8;
+    *reinterpret_cast<uint4*>(&ds[r][c8]) = *reinterpret_cast<const uint4*>(dy + (r0 + r) * C + c8);
+  }
+  __syncthreads();
+  float dg[C], db[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) dg[c] = db[c] = 0.f;
+  if (t < nr) {
+    const float mu = mean[r0 + t], rs = rstd[r0 + t];
+    float xh[C], d[C], s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int c = 0; c < C; c += 8) {
+      const uint4 u = *reinterpret_cast<const uint4*>(&ds[t][c]);
+      unpack_bf16x2(u.x, d[c], d[c + 1]); unpack_bf16x2(u.y, d[c + 2], d[c + 3]);
+      unpack_bf16x2(u.z, d[c + 4], d[c + 5]); unpack_bf16x2(u.w, d[c + 6], d[c + 7]);
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      xh[c] = (__bfloat162float(xs[c][t]) - mu) * rs;
+      const float gd = gamma[c] * d[c];
+      s1 += gd;
+      s2 += gd * xh[c];
+      dg[c] = d[c] * xh[c];
+      db[c] = d[c];
+    }
+    s1 *= 1.0f / C;
+    s2 *= 1.0f / C;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      float o = rs * (gamma[c] * d[c] - s1 - xh[c] * s2);
+      if (res) o += __bfloat162float(res[c * x_cs + r0 + t]);
+      xs[c][t] = __float2bfloat16(o);  // own column of the tile: no barrier needed before the write
+    }
+  }
+  // (dgamma / dbeta: one smem transpose per term instead of 2 C warp reductions per warp)
+  if (dgamma) {
+#pragma unroll
+    for (int c = 0; c < C; ++c) red[c][t] = dg[c];
+  }
+  __syncthreads();
+  float sum_g = 0.f;
+  if (dgamma && t < C) {
+    for (int k = 0; k < nr; ++k) sum_g += red[t][k];
+  }
+  __syncthreads();
+  if (dbeta) {
+#pragma unroll
+    for (int c = 0; c < C; ++c) red[c][t] = db[c];
+  }
+  __syncthreads();
+  for (int i = t; i < C * CM_RT / 8; i += CM_RT) {
+    const int c = i / (CM_RT / 8), r8 = (i % (CM_RT / 8)) * 8;
+    bf16* dst = dx + c * x_cs + r0 + r8;
+    if (r8 + 8 <= nr) {
+      *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(&xs[c][r8]);
+    } else {
+      for (int e = 0; r8 + e < nr; ++e) dst[e] = xs[c][r8 + e];
+    }
+  }
+  if (t < C) {
+    if (dgamma) atomicAdd(dgamma + t, sum_g);
+    if (dbeta) {
+      float b = 0.f;
+      for (int k = 0; k < nr; ++k) b += red[t][k];
+      atomicAdd(dbeta + t, b);
+    }
+  }
+}
+
 // ------------------------------------------------------------- strided rows, thread per row
 template <typename TX, typename TY, int MAXC>
 __global__ void __launch_bounds__(256) ln_fwd_thread(const TX* __restrict__ x, int64_t x_rs, int64_t x_cs,
@@ -737,6 +890,15 @@ static int ln_fwd_impl(const void* x, int64_t x_rs, int64_t x_cs, const float* g
     return ln_fwd_dispatch_warp<TX, TY, 0>(x, x_rs, g, b, y, mean, rstd, rows, cols, eps, nullptr, nullptr, 0, st);
   }
   EVO_CHECK_ARG(cols <= 64, EVO_ERR_SHAPE, "layernorm: strided rows support cols <= 64 (got %lld)", (long long)cols);
+  if (sizeof(TX) == 2 && sizeof(TY) == 2 && x_rs == 1 && x_cs % 8 == 0 && ((uintptr_t)x & 15) == 0 &&
+      ((uintptr_t)y & 15) == 0 && (cols == 16 || cols == 32 || cols == 64)) {
+    dim3 gc((unsigned)((rows + CM_RT - 1) / CM_RT));
+    if (cols == 16) ln_fwd_cm<16><<<gc, CM_RT, 0, st>>>((const bf16*)x, x_cs, g, b, (bf16*)y, mean, rstd, rows, eps);
+    else if (cols == 32) ln_fwd_cm<32><<<gc, CM_RT, 0, st>>>((const bf16*)x, x_cs, g, b, (bf16*)y, mean, rstd, rows, eps);
+    else ln_fwd_cm<64><<<gc, CM_RT, 0, st>>>((const bf16*)x, x_cs, g, b, (bf16*)y, mean, rstd, rows, eps);
+    EVO_LAUNCH_CHECK("layernorm fwd channel-major");
+    return EVO_OK;
+  }
   dim3 grid((unsigned)((rows + 255) / 256));
   // exact widths get the 16-byte row stores (cols == MAXC)
 #define LFT(MC) ln_fwd_thread<TX, TY, MC><<<grid, 256, 0, st>>>((const TX*)x, x_rs, x_cs, g, b, (TY*)y, mean, rstd, \
@@ -853,6 +1015,18 @@ static int ln_bwd_impl(const void* dy, const void* x, int64_t x_rs, int64_t x_cs
     }
 #undef LNB
     EVO_LAUNCH_CHECK("layernorm bwd");
+    return EVO_OK;
+  }
+  if (sizeof(TD) == 2 && sizeof(TX) == 2 && sizeof(TO) == 2 && x_rs == 1 && x_cs % 8 == 0 &&
+      (((uintptr_t)x | (uintptr_t)dx | (uintptr_t)dy) & 15) == 0 && (cols == 16 || cols == 32)) {
+    dim3 gc((unsigned)((rows + CM_RT - 1) / CM_RT));
+#define LBC(CC)                                                                                                   \
+  ln_bwd_cm<CC><<<gc, CM_RT, 0, st>>>((const bf16*)dy, (const bf16*)x, x_cs, g, mean, rstd, (bf16*)dx, (const bf16*)res, \
+                                      dg, db, rows)
+    if (cols == 16) LBC(16);
+    else LBC(32);
+#undef LBC
+    EVO_LAUNCH_CHECK("layernorm bwd channel-major");
     return EVO_OK;
   }
   int64_t need = (rows + 255) / 256, cap = (int64_t)sm_count() * 4;

@@ -52,9 +52,13 @@ def test_layernorm_fwd_bwd(cols, dtype):
     assert rel(acc, base.float() + xr.grad) < tol
 
 
-def test_layernorm_strided_channel_major():
+@pytest.mark.parametrize("P,R,with_res", [(32, 777, False), (32, 776, False), (32, 4096, True), (16, 1000, True),
+                                          (64, 264, False)])
+def test_layernorm_strided_channel_major(P, R, with_res):
+    """channel-major LN (the triangle update's t[p][rows]): thread-per-row kernel for odd strides,
+    the tiled kernel (16-byte tile loads through shared memory) when the channel stride is a
+    multiple of 8"""
     g = torch.Generator(device=DEV).manual_seed(3)
-    P, R = 32, 777
     t_cm = torch.randn(P, R, device=DEV, generator=g).bfloat16()  # [channel][row]
     gamma = torch.randn(P, device=DEV, generator=g)
     beta = torch.randn(P, device=DEV, generator=g)
@@ -67,9 +71,13 @@ def test_layernorm_strided_channel_major():
     dx = torch.empty_like(t_cm)
     dg = torch.zeros(P, device=DEV)
     db = torch.zeros(P, device=DEV)
-    ops.layernorm_bwd(dy, t_cm, gamma, mean, rstd, R, P, x_rs=1, x_cs=R, dx=dx, dgamma=dg, dbeta=db)
-    assert rel(dx.float().t(), xr.grad) < 1e-2
+    res = torch.randn(P, R, device=DEV, generator=g).bfloat16() if with_res else None
+    ops.layernorm_bwd(dy, t_cm, gamma, mean, rstd, R, P, x_rs=1, x_cs=R, dx=dx, dgamma=dg, dbeta=db, res=res)
+    ref = xr.grad + (res.float().t() if with_res else 0)
+    assert rel(dx.float().t(), ref) < 1e-2
     assert rel(db, dy.float().sum(0)) < 1e-5
+    xh = (xr.detach() - xr.detach().mean(-1, keepdim=True)) * torch.rsqrt(xr.detach().var(-1, unbiased=False, keepdim=True) + 1e-5)
+    assert rel(dg, (dy.float() * xh).sum(0)) < 1e-3
 
 
 def test_layernorm_rowdot():
