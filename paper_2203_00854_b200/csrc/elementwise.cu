@@ -321,17 +321,40 @@ __global__ void __launch_bounds__(256) tri_gate_bwd_k(const bf16* __restrict__ y
     const int r = i / (W / 8), c = (i % (W / 8)) * 8;  // c in [0, 4P)
     if (r0 + r >= rows) continue;
     float o[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int which = (c + e) / (2 * P);              // 0: a block, 1: b block
-      const int cc = (c + e) % (2 * P);                 // [0, P) = sig part, [P, 2P) = lin part
+    if constexpr (P % 8 == 0) {
+      // the chunk's 8 columns share the block (a / b) and the part (sig / lin): its sig (and
+      // lin) inputs are 8 consecutive channels of the row -> 16-byte loads, not 16 scalar ones
+      const int which = c / (2 * P), cc0 = c % (2 * P), h0 = cc0 % P;
       const bf16* yrow = y + (r0 + r) * ld + hz + which * 2 * P;
-      const int h = cc % P;
-      const float s = bf2f(yrow[h]), l = bf2f(yrow[P + h]);
-      const float sg = sigmoidf_(s);
-      const float g = gs[r][which * P + h];
-      o[e] = cc < P ? g * l * sg * (1.f - sg) : g * sg;
-      acc[e] += o[e];
+      float sv[8], lv[8];
+      const uint4 us = *reinterpret_cast<const uint4*>(yrow + h0);
+      unpack_bf16x2(us.x, sv[0], sv[1]); unpack_bf16x2(us.y, sv[2], sv[3]);
+      unpack_bf16x2(us.z, sv[4], sv[5]); unpack_bf16x2(us.w, sv[6], sv[7]);
+      if (cc0 < P) {
+        const uint4 ul = *reinterpret_cast<const uint4*>(yrow + P + h0);
+        unpack_bf16x2(ul.x, lv[0], lv[1]); unpack_bf16x2(ul.y, lv[2], lv[3]);
+        unpack_bf16x2(ul.z, lv[4], lv[5]); unpack_bf16x2(ul.w, lv[6], lv[7]);
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float sg = sigmoidf_(sv[e]);
+        const float g = gs[r][which * P + h0 + e];
+        o[e] = cc0 < P ? g * lv[e] * sg * (1.f - sg) : g * sg;
+        acc[e] += o[e];
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int which = (c + e) / (2 * P);              // 0: a block, 1: b block
+        const int cc = (c + e) % (2 * P);                 // [0, P) = sig part, [P, 2P) = lin part
+        const bf16* yrow = y + (r0 + r) * ld + hz + which * 2 * P;
+        const int h = cc % P;
+        const float s = bf2f(yrow[h]), l = bf2f(yrow[P + h]);
+        const float sg = sigmoidf_(s);
+        const float g = gs[r][which * P + h];
+        o[e] = cc < P ? g * l * sg * (1.f - sg) : g * sg;
+        acc[e] += o[e];
+      }
     }
     st8<bf16>(dy + (r0 + r) * ld + hz + c, o);
   }
