@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
   constexpr bool BIASS = MODE == 2 && CP <= 32;
   using SM = BwdSmem<CP, BIASS>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bar1, bar2, tbar[2];
+  __shared__ uint64_t bar1, bar2, tbar[2], bbar;
   __shared__ uint32_t tmem_sh;
   const uint32_t sb = smem_u32(smem);
   constexpr bool PTM = SM::PTM;
@@ -360,10 +360,20 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
     mbar_init(&bar2, 1);
     mbar_init(&tbar[0], 1);
     mbar_init(&tbar[1], 1);
+    mbar_init(&bbar, 1);
     fence_mbar_init();
   }
   __syncthreads();  // the TMA path issues into tbar right below
   uint32_t t_par = 0;  // TMA path: completion parity of tbar[0] / tbar[1] in bits 0 / 1 (uniform over threads)
+  uint32_t b_par = 0;  // TMA path, BIASS: completion parity of bbar (the bias tile's own barrier)
+  // BIASS + TMA: the (key x query) bias tile has its own barrier and is issued as soon as the
+  // previous tile's softmax-backward phase has read it (under that tile's dV/dK/dQ MMAs and TMEM
+  // drain), not with the Q/dO tile after the MMAs: a phase trace showed the loop top waiting
+  // 1-5.6 us per tile on it (profiles/r02_attn_bwd_msa_row_trace.txt)
+  auto issue_bias = [&](int h, int k0, int q0) {
+    mbar_expect_tx(&bbar, (uint32_t)(BW_BK * SM::BROW * 2));
+    tma_ld3(sb + SM::BT, reinterpret_cast<uint64_t>(&maps.bt), q0, k0, h, smem_u32(&bbar));
+  };
   const int64_t HC = (int64_t)H * c;
   // every per-tile operand is a cp.async copy (dO, D and lse*log2e come from the prep kernel)
   const bool vec_stats = (L & 3) == 0;
@@ -377,15 +387,12 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
       if (threadIdx.x == 0) {
         const uint32_t tile = 128 * 32 * 2, vec = BW_BQ * 4;
         const int nq = L - q0 < BW_BQ ? L - q0 : BW_BQ;
-        mbar_expect_tx(&tbar[buf], (with_kv ? 4 : 2) * tile + 2 * (uint32_t)nq * 4 +
-                                       (BIASS ? (uint32_t)(BW_BK * SM::BROW * 2) : 0u));
+        mbar_expect_tx(&tbar[buf], (with_kv ? 4 : 2) * tile + 2 * (uint32_t)nq * 4);
         const uint32_t br = smem_u32(&tbar[buf]);
         if (with_kv) {
           tma_ld4(sb + SM::K, reinterpret_cast<uint64_t>(&maps.k), 0, h, k0, (int)b, br);
           tma_ld4(sb + SM::V, reinterpret_cast<uint64_t>(&maps.v), 0, h, k0, (int)b, br);
         }
-        if constexpr (BIASS)  // the padded 136-query rows of the smem tile ARE the box rows
-          tma_ld3(sb + SM::BT, reinterpret_cast<uint64_t>(&maps.bt), q0, k0, h, br);
         tma_ld4(sb + SM::Q + buf * SM::QD_BYTES, reinterpret_cast<uint64_t>(&maps.q), 0, h, q0, (int)b, br);
         tma_ld4(sb + SM::DO + buf * SM::QD_BYTES, reinterpret_cast<uint64_t>(&maps.dO), 0, h, q0, (int)b, br);
         bulk_ld(sb + lse_b, P.lse2 + st0, (uint32_t)nq * 4, &tbar[buf]);
@@ -436,7 +443,10 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
     int64_t b0;
     int h0, kt0;
     decode(blockIdx.x, b0, h0, kt0);
-    if ((int64_t)blockIdx.x < units) issue_loads(b0, h0, kt0 * BW_BK, 0, true, 0);
+    if ((int64_t)blockIdx.x < units) {
+      issue_loads(b0, h0, kt0 * BW_BK, 0, true, 0);
+      if constexpr (BIASS) if (tmaq && threadIdx.x == 0) issue_bias(h0, kt0 * BW_BK, 0);
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -495,7 +505,10 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
       if (tmaq) {
         mbar_wait(&tbar[buf], (t_par >> buf) & 1u);
         t_par ^= 1u << buf;
-        if (db_store && threadIdx.x == 0) bulk_wait_read<0>();  // the dS^T store has read the tile
+        if constexpr (BIASS) {
+          mbar_wait(&bbar, b_par);
+          b_par ^= 1u;
+        }
       }
       fence_async_smem();
       __syncthreads();
@@ -505,6 +518,9 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
       if (DB && qt + 1 < nqt) issue_loads(b, h, k0, qt + 1, false, buf ^ 1);
       if (threadIdx.x == 0) {
         tc_fence_after();
+        // the previous tile's dS^T store must have read DST before this tile's softmax-backward
+        // phase rewrites it; every thread passes bar1 (committed below) before writing DST
+        if (db_store && tmaq) bulk_wait_read<0>();
 #pragma unroll
         for (int kk = 0; kk < CP / 16; ++kk) {
           const uint32_t koff = kk * 2 * LBO_ROWS;
@@ -642,6 +658,16 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
       tc_fence_before();
       __syncthreads();
       if (db_per_key && wg == 0 && dbias_col) atomicAdd(dbias_col, P.scale * (s_kb[kr] + s_kb[BW_BK + kr]));
+      if constexpr (BIASS) if (tmaq && threadIdx.x == 0) {  // every thread has read the bias tile
+        if (qt + 1 < nqt) {
+          issue_bias(h, k0, q0 + BW_BQ);
+        } else if (u + gridDim.x < units) {
+          int64_t nb;
+          int nh, nkt_;
+          decode(u + gridDim.x, nb, nh, nkt_);
+          issue_bias(nh, nkt_ * BW_BK, 0);
+        }
+      }
       if (threadIdx.x == 0) {
         tc_fence_after();
 #if EVO_EXP != 2
@@ -667,12 +693,7 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
         mma_commit(&bar2);
       }
       if (db_store && tmaq) {
-        // dS^T tile -> workspace by one TMA tensor store (the map walks the canonical tile order);
-        // the tile is re-read only after bulk_wait_read at the next loop top
-        if (threadIdx.x == 0) {
-          tma_st5(reinterpret_cast<uint64_t>(&maps.ws), sb + SM::DST, 0, 0, k0 / 8, q0 / 8, (int)(b * H + h));
-          bulk_commit();
-        }
+        // (TMA store of the dS^T tile: issued after the next tile's loads, below)
       } else if constexpr (db_store) {
         // dS^T tile (unscaled bf16, canonical K-major [key][query]) -> workspace [b][h][key][query],
         // under the dV/dK/dQ MMAs (which only read the tile): all 8 smem reads of a thread first,
@@ -716,6 +737,14 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
           const int nkj = nkt_ * BW_BK + kr;
           kb_next = nkj < L ? F.bias[nb * F.bs0 + (int64_t)nh * F.bs1 + (int64_t)nkj * F.bs3] : f2bf(0.f);
         }
+      }
+      if (db_store && tmaq && threadIdx.x == 0) {
+        // dS^T tile -> workspace by one TMA tensor store (the map walks the canonical tile order),
+        // issued AFTER the next tile's loads: a store queued ahead of them held them back by 1-3 us
+        // per tile (phase trace); the tile is rewritten only after bulk_wait_read before the next
+        // S/dP MMAs
+        tma_st5(reinterpret_cast<uint64_t>(&maps.ws), sb + SM::DST, 0, 0, k0 / 8, q0 / 8, (int)(b * H + h));
+        bulk_commit();
       }
       BTRACE(it * 8 + 7);
 #if EVO_EXP != 3
