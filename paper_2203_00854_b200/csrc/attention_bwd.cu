@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
   // BIASS + TMA: the (key x query) bias tile has its own barrier and is issued as soon as the
   // previous tile's softmax-backward phase has read it (under that tile's dV/dK/dQ MMAs and TMEM
   // drain), not with the Q/dO tile after the MMAs: a phase trace showed the loop top waiting
-  // 1-5.6 us per tile on it (profiles/r02_attn_bwd_msa_row_trace.txt)
+  // 1-5.6 us per tile on it (profiles/r02_attn_bwd_msa_row_trace_before.txt)
   auto issue_bias = [&](int h, int k0, int q0) {
     mbar_expect_tx(&bbar, (uint32_t)(BW_BK * SM::BROW * 2));
     tma_ld3(sb + SM::BT, reinterpret_cast<uint64_t>(&maps.bt), q0, k0, h, smem_u32(&bbar));
@@ -455,8 +455,11 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
   const uint32_t t_lane = tmem + ((uint32_t)(wq * 32) << 16);
   // S^T [0,128) (PTM: P^T packed bf16 over it at wg*64 + part*8), dP^T [128,256); the
   // dV/dK/dQ products go where no operand of their own MMAs lives
+  // PTM: dS^T packed bf16 over the dP^T columns already read (128 + wg*64 + part*8) is the A
+  // operand of the dK MMA (TS: 32 KB less shared-memory operand traffic per tile); the dV / dK / dQ
+  // products go to the columns neither packed operand occupies
   constexpr uint32_t T_S = 0, T_DP = 128;
-  constexpr uint32_t T_DV = PTM ? 128 : 0, T_DK = T_DV + CP, T_DQ = T_DV + 2 * CP;
+  constexpr uint32_t T_DV = PTM ? 32 : 0, T_DK = PTM ? 96 : T_DV + CP, T_DQ = PTM ? 160 : T_DV + 2 * CP;
 
   constexpr uint32_t ID_SS = make_idesc_bf16(128, 128, 0, 0);  // S^T = K Q^T, dP^T = V dO^T
   constexpr uint32_t ID_KV = make_idesc_bf16(128, CP, 0, 1);   // dV = P^T dO, dK = dS^T Q  (B: MN-major view)
@@ -633,11 +636,15 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
               if (q0 + qc + e < L) atomicAdd(dbias_col + (int64_t)(q0 + qc + e) * P.db2, P.scale * dsv[e]);
           }
         }
-        if constexpr (PTM) {  // P^T over the S^T columns this warp has already read
+        uint32_t dk[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) dk[e] = pack_bf16x2(dsv[2 * e], dsv[2 * e + 1]);
+        if constexpr (PTM) {  // P^T over the S^T columns, dS^T over the dP^T columns this warp has read
           uint32_t pk[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) pk[e] = pack_bf16x2(pv[2 * e], pv[2 * e + 1]);
           bw_tmem_st8(t_lane + T_S + wg * 64 + part * 8, pk);
+          bw_tmem_st8(t_lane + T_DP + wg * 64 + part * 8, dk);
         }
 #pragma unroll
         for (int e = 0; e < 16; e += 8) {
@@ -645,9 +652,8 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
             st_shared_v4(sb + SM::PT + kmajor_off(kr, qc + e, 128), pack_bf16x2(pv[e], pv[e + 1]),
                          pack_bf16x2(pv[e + 2], pv[e + 3]), pack_bf16x2(pv[e + 4], pv[e + 5]),
                          pack_bf16x2(pv[e + 6], pv[e + 7]));
-          st_shared_v4(sb + SM::DST + kmajor_off(kr, qc + e, 128), pack_bf16x2(dsv[e], dsv[e + 1]),
-                       pack_bf16x2(dsv[e + 2], dsv[e + 3]), pack_bf16x2(dsv[e + 4], dsv[e + 5]),
-                       pack_bf16x2(dsv[e + 6], dsv[e + 7]));
+          st_shared_v4(sb + SM::DST + kmajor_off(kr, qc + e, 128), dk[e / 2], dk[e / 2 + 1], dk[e / 2 + 2],
+                       dk[e / 2 + 3]);
         }
       }
       if (db_per_key) s_kb[wg * BW_BK + kr] = kb_acc;
@@ -677,11 +683,14 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
           const uint32_t boff = kk * 2 * 128;
           const uint64_t d_do = tmaq ? bw_sw64_mn(sDO + kk * 1024) : make_sdesc(sDO + boff, 128, LBO_ROWS);
           const uint64_t d_q = tmaq ? bw_sw64_mn(sQ + kk * 1024) : make_sdesc(sQ + boff, 128, LBO_ROWS);
-          if constexpr (PTM)  // queries [0,64) at columns [0,32), [64,128) at [64,96)
-            bw_mma_ts(tmem + T_DV, tmem + T_S + (kk < 4 ? kk * 8 : 64 + (kk - 4) * 8), d_do, ID_KV, kk != 0);
-          else
+          if constexpr (PTM) {  // queries [0,64) at columns [0,32), [64,128) at [64,96) of each operand
+            const uint32_t ac = kk < 4 ? kk * 8 : 64 + (kk - 4) * 8;
+            bw_mma_ts(tmem + T_DV, tmem + T_S + ac, d_do, ID_KV, kk != 0);
+            bw_mma_ts(tmem + T_DK, tmem + T_DP + ac, d_q, ID_KV, kk != 0);
+          } else {
             mma_bf16(tmem + T_DV, make_sdesc(sb + SM::PT + aoff, LBO_ROWS, 128), d_do, ID_KV, kk != 0);
-          mma_bf16(tmem + T_DK, make_sdesc(sb + SM::DST + aoff, LBO_ROWS, 128), d_q, ID_KV, kk != 0);
+            mma_bf16(tmem + T_DK, make_sdesc(sb + SM::DST + aoff, LBO_ROWS, 128), d_q, ID_KV, kk != 0);
+          }
         }
 #pragma unroll
         for (int kk = 0; kk < BW_BK / 16; ++kk) {
