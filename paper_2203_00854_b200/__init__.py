@@ -50,8 +50,8 @@ def __getattr__(name):
         from . import autochunk
         return getattr(autochunk, name)
     if name == "precise":  # reference-precision parity mode (fp32 storage, three-term bf16 tensor-core products)
-        from . import precise
-        return precise
+        import importlib
+        return importlib.import_module(".precise", __name__)
     if name in ("TimelineEvent", "simulate_schedule", "events_from_json", "events_to_json", "measure_dap_forward",
                 "overlap_report"):
         from . import timeline

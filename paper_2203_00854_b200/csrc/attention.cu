@@ -165,7 +165,13 @@ __device__ __forceinline__ uint32_t vt_off(int key, int d) {
 template <int CP, int VAR>
 __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1) ? 3 : 4)) attn_fwd_kernel(
     AttnParams P, int nunits, const __grid_constant__ AttnFwdMaps maps, int tmaq) {
-  constexpr bool FB = VAR == 2, GS = VAR == 0;
+  // The epilogue's gate rows are fetched early, with the unit's last tile, so the epilogue does not
+  // wait on a DRAM load (a tile trace showed a 4.5-5.2K clk epilogue per unit, ~30 % of it, with the
+  // gate loaded there; profiles/r02_attn_fwd_tile_trace.txt): GS (no bias) into smem; GR (the smem-staged
+  // full-bias variant, 3 CTAs/SM: registers to spare) into registers (msa_row fwd 58.3 -> 54.6 us).  The
+  // per-key-bias variant (4 CTAs/SM at its register limit) keeps the epilogue load: the smem gate
+  // tile, registers and an L1 prefetch all measured 3-7 % slower there (spills)
+  constexpr bool FB = VAR == 2, GS = VAR == 0, GR = VAR == 2;
   using SM = AttnSmem<CP>;
   constexpr int CQ = SM::CQ, CV = SM::CV;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -298,6 +304,7 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1
     const unsigned short* kbias = kbias_of(cur);
     const bf16* bfull = bfull_of(cur);
     float m_run = -INFINITY;  // running max, scaled log2 units
+    uint4 greg[GR ? CP / 8 : 1];  // GR: the gate rows of this thread's query (loaded with the last tile)
     const bf16* brow = nullptr;
     if (VAR == 3 && qi < L) brow = P.bias + b * P.bs0 + (int64_t)h * P.bs1 + (int64_t)qi * P.bs2;
     uint32_t nb = 0;  // next tile's per-key bias (threads 0..63), stored with its K tile
@@ -352,6 +359,12 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1
         }
       }
       if (GS) cp_async_commit();
+      if (GR && j + 1 == nkt && qi < L) {  // gate rows into registers, consumed by the epilogue
+        const bf16* gsrc = P.g + b * P.g_sb + (int64_t)qi * P.g_sl + (int64_t)h * c;
+#pragma unroll
+        for (int d = 0; d < CP; d += 8)
+          if (d < c) greg[d / 8] = *reinterpret_cast<const uint4*>(gsrc + d);
+      }
 
       if (threadIdx.x == 0) {
         // S overwrites the columns the previous tile's P was read from: its PV must be complete
@@ -521,7 +534,9 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1
         if (d < c) {
           float o[8], gv[8];
           uint4 w0;
-          if (!GS) {
+          if constexpr (GR) {
+            w0 = greg[d / 8];
+          } else if constexpr (!GS) {
             w0 = *reinterpret_cast<const uint4*>(gp + d);
           } else {
             asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];\n" : "=r"(w0.x), "=r"(w0.y), "=r"(w0.z), "=r"(w0.w)
