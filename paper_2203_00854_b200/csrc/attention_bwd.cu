@@ -171,14 +171,25 @@ constexpr int PREP_PASSES = 2;  // measured: 2 beats 4 (more resident CTAs, load
 // STAGED (when H*c/8 divides the CTA's 8*32*PREP_PASSES chunks: the CTA covers whole rows): the
 // per-(b, h, l) statistics D and lse*log2e go through smem and are written (and lse read) as
 // runs of consecutive l per head instead of one scattered 4-byte access per head and row.
-template <bool STAGED>
-__global__ void __launch_bounds__(256) attn_bwd_prep(AttnBwdParams P, int64_t B) {
+// Index math: the (row, chunk), (b, l) and (chunk -> head) splits are shifts when H*c/8, L and c are
+// powers of two (every Evoformer shape; POW2), else 32-bit divisions.  The division form dominated
+// the instruction count (ncu: issue-active 68 %, ~12 emulated divisions per thread), so the splits are
+// also computed once per pass and reused by the math loop.
+struct PrepIdx {
+  uint32_t nch, L, c;
+  int sh_nch, sh_L, sh_c;
+};
+template <bool POW2>
+__device__ __forceinline__ uint32_t pdiv(uint32_t x, uint32_t d, int sh) { return POW2 ? x >> sh : x / d; }
+
+template <bool STAGED, bool POW2>
+__global__ void __launch_bounds__(256) attn_bwd_prep(AttnBwdParams P, int64_t B, PrepIdx ix) {
   constexpr int PER_CTA = 8 * PREP_PASSES * 32;
   __shared__ float s_D[STAGED ? PER_CTA : 1];
   const int lane = threadIdx.x & 31;
   const int L = P.f.L, H = P.f.H, c = P.f.c;
-  const uint32_t nch = H * c / 8;
-  // 32-bit (row, chunk) / (b, l) divisions: the host guarantees B*L*nch < 2^31
+  const uint32_t nch = ix.nch;
+  // 32-bit (row, chunk) / (b, l) splits: the host guarantees B*L*nch < 2^31
   const uint32_t total = (uint32_t)(B * L * nch);
   const uint32_t f0 = ((uint32_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * (PREP_PASSES * 32);
   if (!STAGED && f0 >= total) return;
@@ -186,28 +197,34 @@ __global__ void __launch_bounds__(256) attn_bwd_prep(AttnBwdParams P, int64_t B)
   const uint32_t row0 = (uint32_t)blockIdx.x * (PER_CTA / nch);  // STAGED: first row of this CTA
   uint4 ud[PREP_PASSES], ug[PREP_PASSES], uo[PREP_PASSES];
   float lse[PREP_PASSES];
+  uint32_t rw[PREP_PASSES], bb[PREP_PASSES], ll[PREP_PASSES];
+  int cl[PREP_PASSES];
 #pragma unroll
   for (int t = 0; t < PREP_PASSES; ++t) {
     const uint32_t f = f0 + t * 32 + lane;
+    const uint32_t row = pdiv<POW2>(f, nch, ix.sh_nch);
+    const uint32_t bu = pdiv<POW2>(row, (uint32_t)L, ix.sh_L);
+    rw[t] = row;
+    bb[t] = bu;
+    ll[t] = row - bu * (uint32_t)L;
+    cl[t] = (int)(f - row * nch) * 8;
     if (f < total) {
-      const uint32_t row = f / nch;
-      const int col = (int)(f - row * nch) * 8;
-      const uint32_t bu = row / (uint32_t)L;
-      const int64_t b = bu, l = row - bu * (uint32_t)L;
+      const int64_t b = bu, l = ll[t];
+      const int col = cl[t];
       ud[t] = *reinterpret_cast<const uint4*>(P.dout + b * P.do_sb + l * P.do_sl + col);
       ug[t] = *reinterpret_cast<const uint4*>(P.f.g + b * P.f.g_sb + l * P.f.g_sl + col);
       uo[t] = *reinterpret_cast<const uint4*>(P.f.orw + b * P.f.r_sb + l * P.f.r_sl + col);
-      if (!STAGED) lse[t] = (lane % lanes_per_head) == 0 ? P.f.lse[(b * H + col / c) * (int64_t)L + l] : 0.f;
+      if (!STAGED)
+        lse[t] = (lane % lanes_per_head) == 0 ? P.f.lse[(b * H + pdiv<POW2>(col, c, ix.sh_c)) * (int64_t)L + l] : 0.f;
     }
   }
 #pragma unroll
   for (int t = 0; t < PREP_PASSES; ++t) {
     const uint32_t f = f0 + t * 32 + lane;
     const bool ok = f < total;
-    const uint32_t row = ok ? f / nch : 0;
-    const int col = (int)(f - row * nch) * 8;
-    const uint32_t bu = row / (uint32_t)L;
-    const int64_t b = bu, l = row - bu * (uint32_t)L;
+    const uint32_t row = rw[t];
+    const int col = cl[t];
+    const int64_t b = bb[t], l = ll[t];
     float dsum = 0.f;
     if (ok) {
       float dout[8], g[8], o[8], dO[8], dg[8];
@@ -222,11 +239,16 @@ __global__ void __launch_bounds__(256) attn_bwd_prep(AttnBwdParams P, int64_t B)
         const float sg = sigmoidf_(g[e]);
         dO[e] = dout[e] * sg;
         dg[e] = dout[e] * o[e] * sg * (1.f - sg);
-        dsum += bf2f(f2bf(dO[e])) * o[e];  // D of the bf16 dO the MMAs see
       }
       uint4 w;
       w.x = pack_bf16x2(dO[0], dO[1]); w.y = pack_bf16x2(dO[2], dO[3]);
       w.z = pack_bf16x2(dO[4], dO[5]); w.w = pack_bf16x2(dO[6], dO[7]);
+      // D of the bf16 dO the MMAs see (the packed values, unpacked: no second rounding pass)
+      float r[8];
+      unpack_bf16x2(w.x, r[0], r[1]); unpack_bf16x2(w.y, r[2], r[3]);
+      unpack_bf16x2(w.z, r[4], r[5]); unpack_bf16x2(w.w, r[6], r[7]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) dsum = fmaf(r[e], o[e], dsum);
       *reinterpret_cast<uint4*>(P.dO + (int64_t)row * (H * c) + col) = w;
       w.x = pack_bf16x2(dg[0], dg[1]); w.y = pack_bf16x2(dg[2], dg[3]);
       w.z = pack_bf16x2(dg[4], dg[5]); w.w = pack_bf16x2(dg[6], dg[7]);
@@ -235,27 +257,28 @@ __global__ void __launch_bounds__(256) attn_bwd_prep(AttnBwdParams P, int64_t B)
     // segmented reduction over the lanes of one head (lanes_per_head is a power of 2)
     for (int o = 1; o < lanes_per_head; o <<= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
     if (ok && (lane % lanes_per_head) == 0) {
+      const int hh = (int)pdiv<POW2>(col, c, ix.sh_c);
       if (STAGED) {
-        s_D[(row - row0) * H + col / c] = dsum;
+        s_D[(row - row0) * H + hh] = dsum;
       } else {
-        const int64_t ix = (b * H + col / c) * (int64_t)L + l;
-        P.Dsum[ix] = dsum;
-        P.lse2[ix] = lse[t] * 1.4426950408889634f;
+        const int64_t ixo = (b * H + hh) * (int64_t)L + l;
+        P.Dsum[ixo] = dsum;
+        P.lse2[ixo] = lse[t] * 1.4426950408889634f;
       }
     }
   }
   if (STAGED) {
     __syncthreads();
-    const int R = PER_CTA / (int)nch;
+    const int R = PER_CTA / (int)nch;  // rows per CTA (a power of two when POW2)
     const uint32_t rows = (uint32_t)(B * L);
     for (int i = threadIdx.x; i < R * H; i += 256) {
-      const int h = i / R, rl = i - h * R;
+      const int h = POW2 ? i >> (31 - __clz(R)) : i / R, rl = i - h * R;
       const uint32_t row = row0 + rl;
       if (row < rows) {
-        const uint32_t bu = row / (uint32_t)L;
-        const int64_t ix = ((int64_t)bu * H + h) * L + (row - bu * (uint32_t)L);
-        P.Dsum[ix] = s_D[rl * H + h];
-        P.lse2[ix] = P.f.lse[ix] * 1.4426950408889634f;
+        const uint32_t bu = pdiv<POW2>(row, (uint32_t)L, ix.sh_L);
+        const int64_t ixo = ((int64_t)bu * H + h) * L + (row - bu * (uint32_t)L);
+        P.Dsum[ixo] = s_D[rl * H + h];
+        P.lse2[ixo] = P.f.lse[ixo] * 1.4426950408889634f;
       }
     }
   }
@@ -1047,8 +1070,15 @@ extern "C" int evo_gated_attention_bwd(const EvoAttnBwdDesc* d, void* stream) {
     const int64_t rows = B * L;
     const int64_t pairs = rows * (H * c / 8), per_cta = 8 * PREP_PASSES * 32;
     const unsigned g = (unsigned)((pairs + per_cta - 1) / per_cta);
-    if (per_cta % (H * c / 8) == 0) attn_bwd_prep<true><<<g, 256, 0, st>>>(p, B);
-    else attn_bwd_prep<false><<<g, 256, 0, st>>>(p, B);
+    auto lg = [](int64_t v) { int k = 0; while ((int64_t(1) << k) < v) ++k; return k; };
+    const PrepIdx ix{(uint32_t)(H * c / 8), (uint32_t)L, (uint32_t)c, lg(H * c / 8), lg(L), lg(c)};
+    const bool pow2 = (int64_t(1) << ix.sh_nch) == H * c / 8 && (int64_t(1) << ix.sh_L) == L &&
+                      (int64_t(1) << ix.sh_c) == c;
+    const bool staged = per_cta % (H * c / 8) == 0;
+    if (staged && pow2) attn_bwd_prep<true, true><<<g, 256, 0, st>>>(p, B, ix);
+    else if (staged) attn_bwd_prep<true, false><<<g, 256, 0, st>>>(p, B, ix);
+    else if (pow2) attn_bwd_prep<false, true><<<g, 256, 0, st>>>(p, B, ix);
+    else attn_bwd_prep<false, false><<<g, 256, 0, st>>>(p, B, ix);
     EVO_LAUNCH_CHECK("attention bwd prep");
   }
   if (p.dS) {
