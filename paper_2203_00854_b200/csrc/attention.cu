@@ -165,6 +165,7 @@ __device__ __forceinline__ uint32_t vt_off(int key, int d) {
 template <int CP, int VAR>
 __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1) ? 3 : 4)) attn_fwd_kernel(
     AttnParams P, int nunits, const __grid_constant__ AttnFwdMaps maps, int tmaq) {
+  pdl_wait();
   // The epilogue's gate rows are fetched early, with the unit's last tile, so the epilogue does not
   // wait on a DRAM load (a tile trace showed a 4.5-5.2K clk epilogue per unit, ~30 % of it, with the
   // gate loaded there; profiles/r02_attn_fwd_tile_trace.txt): GS (no bias) into smem; GR (the smem-staged
@@ -668,7 +669,7 @@ static int launch_attn_fwd_v(const AttnParams& p, int64_t B, cudaStream_t st) {
                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     }
   }
-  attn_fwd_kernel<CP, VAR><<<(unsigned)(nunits < cap ? nunits : cap), 128, bytes, st>>>(p, (int)nunits, maps, tmaq);
+  ::evo::pdl_launch(attn_fwd_kernel<CP, VAR>, (unsigned)(nunits < cap ? nunits : cap), 128, bytes, st, p, (int)nunits, maps, tmaq);
   EVO_LAUNCH_CHECK("attention fwd");
   return EVO_OK;
 }

@@ -70,6 +70,7 @@ struct AttnBwdParams {
 __global__ void __launch_bounds__(256) attn_dbias_reduce(const bf16* __restrict__ dS, float* __restrict__ dbias,
                                                          int64_t B, int H, int L, int64_t d1, int64_t d2, int64_t d3,
                                                          float scale) {
+  pdl_wait();
   constexpr int U = 8;
   __shared__ float part[2][32][33];
   const int h = blockIdx.z, k0 = blockIdx.y * 32, q0 = blockIdx.x * 32;
@@ -119,6 +120,7 @@ __global__ void __launch_bounds__(256) attn_dbias_reduce(const bf16* __restrict_
 // loads per thread and query group into two 16-byte loads.  32x32 tiles through smem.
 __global__ void __launch_bounds__(256) attn_bias_transpose(const bf16* __restrict__ bias, int64_t s1, int64_t s2,
                                                            bf16* __restrict__ bias_t, int L) {
+  pdl_wait();
   __shared__ bf16 tile[32][33];
   const int h = blockIdx.z;
   const int q0 = blockIdx.y * 32, k0 = blockIdx.x * 32;
@@ -184,6 +186,7 @@ __device__ __forceinline__ uint32_t pdiv(uint32_t x, uint32_t d, int sh) { retur
 
 template <bool STAGED, bool POW2>
 __global__ void __launch_bounds__(256) attn_bwd_prep(AttnBwdParams P, int64_t B, PrepIdx ix) {
+  pdl_wait();
   constexpr int PER_CTA = 8 * PREP_PASSES * 32;
   __shared__ float s_D[STAGED ? PER_CTA : 1];
   const int lane = threadIdx.x & 31;
@@ -353,6 +356,7 @@ __device__ __forceinline__ void bw_load(uint32_t sdst, const bf16* base, int64_t
 template <int CP, int MODE>
 __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int nkt, int dq_partial,
                                                           const __grid_constant__ BwdMaps maps, int tmaq) {
+  pdl_wait();
   constexpr bool BIASS = MODE == 2 && CP <= 32;
   using SM = BwdSmem<CP, BIASS>;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -876,6 +880,7 @@ namespace evo {
 #endif
 template <int NP>
 __global__ void __launch_bounds__(256) attn_bwd_dq_finish(AttnBwdParams P, int64_t B) {
+  pdl_wait();
   const int L = P.f.L, H = P.f.H, c = P.f.c;
   const int64_t n = B * L * (int64_t)H * c;
   const int64_t n8 = n / 8;
@@ -994,7 +999,7 @@ static int launch_bwd_m(AttnBwdParams& p, int64_t B, int dq_partial, cudaStream_
   // persistent: 2 CTAs per SM, units handed out round-robin
   const int64_t slots = (int64_t)sm_count() * 2;
   dim3 grid((unsigned)(units < slots ? units : slots));
-  attn_bwd_kernel<CP, MODE><<<grid, 256, SM::TOTAL, st>>>(p, (int)nkt, dq_partial, maps, tmaq);
+  ::evo::pdl_launch(attn_bwd_kernel<CP, MODE>, grid, 256, SM::TOTAL, st, p, (int)nkt, dq_partial, maps, tmaq);
   EVO_LAUNCH_CHECK("attention bwd main");
   return EVO_OK;
 }
@@ -1075,16 +1080,16 @@ extern "C" int evo_gated_attention_bwd(const EvoAttnBwdDesc* d, void* stream) {
     const bool pow2 = (int64_t(1) << ix.sh_nch) == H * c / 8 && (int64_t(1) << ix.sh_L) == L &&
                       (int64_t(1) << ix.sh_c) == c;
     const bool staged = per_cta % (H * c / 8) == 0;
-    if (staged && pow2) attn_bwd_prep<true, true><<<g, 256, 0, st>>>(p, B, ix);
-    else if (staged) attn_bwd_prep<true, false><<<g, 256, 0, st>>>(p, B, ix);
-    else if (pow2) attn_bwd_prep<false, true><<<g, 256, 0, st>>>(p, B, ix);
-    else attn_bwd_prep<false, false><<<g, 256, 0, st>>>(p, B, ix);
+    if (staged && pow2) ::evo::pdl_launch(attn_bwd_prep<true, true>, g, 256, 0, st, p, B, ix);
+    else if (staged) ::evo::pdl_launch(attn_bwd_prep<true, false>, g, 256, 0, st, p, B, ix);
+    else if (pow2) ::evo::pdl_launch(attn_bwd_prep<false, true>, g, 256, 0, st, p, B, ix);
+    else ::evo::pdl_launch(attn_bwd_prep<false, false>, g, 256, 0, st, p, B, ix);
     EVO_LAUNCH_CHECK("attention bwd prep");
   }
   if (p.dS) {
     bf16* bias_t = (bf16*)(ws + off_dS + ((B * H * L * L * 2 + 255) / 256) * 256);
     dim3 tg((unsigned)((L + 31) / 32), (unsigned)((L + 31) / 32), (unsigned)H);
-    attn_bias_transpose<<<tg, 256, 0, st>>>(p.f.bias, p.f.bs1, p.f.bs2, bias_t, (int)L);
+    ::evo::pdl_launch(attn_bias_transpose, tg, 256, 0, st, p.f.bias, p.f.bs1, p.f.bs2, bias_t, (int)L);
     EVO_LAUNCH_CHECK("attention bwd bias transpose");
     p.f.bias = bias_t;
     p.f.bs0 = 0; p.f.bs1 = L * L; p.f.bs2 = 1; p.f.bs3 = L;
@@ -1095,7 +1100,7 @@ extern "C" int evo_gated_attention_bwd(const EvoAttnBwdDesc* d, void* stream) {
   if (rc) return rc;
   if (p.dS) {
     const dim3 g2((unsigned)((L + 31) / 32), (unsigned)((L + 31) / 32), (unsigned)H);
-    attn_dbias_reduce<<<g2, 256, 0, st>>>(p.dS, p.dbias, B, H, L, p.db1, p.db2, p.db3, p.scale);
+    ::evo::pdl_launch(attn_dbias_reduce, g2, 256, 0, st, p.dS, p.dbias, B, H, L, p.db1, p.db2, p.db3, p.scale);
     EVO_LAUNCH_CHECK("attention bwd dbias reduce");
   }
   if (dq_partial == 2) return EVO_OK;
@@ -1103,10 +1108,10 @@ extern "C" int evo_gated_attention_bwd(const EvoAttnBwdDesc* d, void* stream) {
   int64_t g = (n8 + 255) / 256, cap = (int64_t)sm_count() * 16;
   const unsigned gf = (unsigned)(g < cap ? g : cap);
   switch (dq_partial ? (int)nkt : 0) {  // 0: fp32 atomic accumulator; 2..4: bf16 per-tile partials
-    case 0: attn_bwd_dq_finish<0><<<gf, 256, 0, st>>>(p, B); break;
-    case 2: attn_bwd_dq_finish<2><<<gf, 256, 0, st>>>(p, B); break;
-    case 3: attn_bwd_dq_finish<3><<<gf, 256, 0, st>>>(p, B); break;
-    default: attn_bwd_dq_finish<4><<<gf, 256, 0, st>>>(p, B); break;
+    case 0: ::evo::pdl_launch(attn_bwd_dq_finish<0>, gf, 256, 0, st, p, B); break;
+    case 2: ::evo::pdl_launch(attn_bwd_dq_finish<2>, gf, 256, 0, st, p, B); break;
+    case 3: ::evo::pdl_launch(attn_bwd_dq_finish<3>, gf, 256, 0, st, p, B); break;
+    default: ::evo::pdl_launch(attn_bwd_dq_finish<4>, gf, 256, 0, st, p, B); break;
   }
   EVO_LAUNCH_CHECK("attention bwd finish");
   return EVO_OK;

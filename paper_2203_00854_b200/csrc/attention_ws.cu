@@ -129,6 +129,7 @@ __device__ __forceinline__ void ws_scale_o(uint32_t taddr, float f) {
 
 template <int CP>
 __global__ void __launch_bounds__(WS_THREADS, 1) attn_fwd_ws_kernel(AttnParams P) {
+  pdl_wait();
   using SM = WsSmem<CP>;
   constexpr int CQ = SM::CQ, CV = SM::CV, WS_NS = SM::NS;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -447,7 +448,7 @@ int launch_attn_fwd_ws(const AttnParams& p, int64_t B, cudaStream_t st) {
     attr_bytes = smem;
   }
   dim3 grid((unsigned)((p.L + 2 * WS_BQ - 1) / (2 * WS_BQ)), (unsigned)p.H, (unsigned)B);
-  attn_fwd_ws_kernel<CP><<<grid, WS_THREADS, smem, st>>>(p);
+  ::evo::pdl_launch(attn_fwd_ws_kernel<CP>, grid, WS_THREADS, smem, st, p);
   EVO_LAUNCH_CHECK("attention fwd (warp-specialised)");
   return EVO_OK;
 }

@@ -1,3 +1,4 @@
+#include <cstdlib>
 // Library-level C-ABI entry points and the error-string plumbing shared by all
 // kernels (include/evo.h).  Errors are per host thread.
 #include <cstdarg>
@@ -24,6 +25,13 @@ int cuda_status(cudaError_t e, const char* where) {
 }  // namespace evo
 
 extern "C" const char* evo_version(void) { return "evo-b200 0.1.0 (sm_100a)"; }
+
+namespace evo {
+bool pdl_enabled() {
+  static const bool on = [] { const char* e = getenv("EVO_NO_PDL"); return !(e && e[0] == '1'); }();
+  return on;
+}
+}  // namespace evo
 
 extern "C" const char* evo_last_error_string(void) { return evo::g_err; }
 

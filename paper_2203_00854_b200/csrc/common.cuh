@@ -37,6 +37,31 @@ int cuda_status(cudaError_t e, const char* where);
 
 typedef __nv_bfloat16 bf16;
 
+// Programmatic dependent launch: every kernel of this library is launched with programmatic stream
+// serialization allowed and starts with griddepcontrol.wait, so its CTAs are scheduled (launch
+// latency, prologue) while the previous kernel of the stream drains, and touch global memory only
+// once that kernel has completed and flushed.  EVO_NO_PDL=1 launches them plainly (A/B switch).
+__device__ __forceinline__ void pdl_wait() {
+#if defined(__CUDA_ARCH__)
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+#endif
+}
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline void pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<Args&&>(args)...);
+}
+
 __device__ __forceinline__ float bf2f(bf16 v) { return __bfloat162float(v); }
 __device__ __forceinline__ bf16 f2bf(float v) { return __float2bfloat16_rn(v); }
 

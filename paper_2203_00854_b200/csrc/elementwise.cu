@@ -45,6 +45,7 @@ __global__ void __launch_bounds__(256) gated_residual_fwd_k(const T* __restrict_
                                                             int64_t y_rs, const float* __restrict__ bias,
                                                             const T* __restrict__ gp, int64_t gp_rs,
                                                             T* __restrict__ out, int64_t rows, int64_t cols) {
+  pdl_wait();
   const IDX cpr = (IDX)(cols / 8);
   const IDX n = (IDX)(rows * (cols / 8));
   for (IDX i = (IDX)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (IDX)gridDim.x * blockDim.x) {
@@ -111,6 +112,7 @@ __global__ void __launch_bounds__(256) gated_residual_bwd_k(const T* __restrict_
                                                             T* __restrict__ dgp, int64_t dgp_rs,
                                                             float* __restrict__ dbias, float* __restrict__ dgp_sum,
                                                             int64_t rows, int64_t cols) {
+  pdl_wait();
   extern __shared__ float red[];
   const ColTile t(rows, cols);
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -168,6 +170,7 @@ __global__ void __launch_bounds__(256) gated_residual_bwd_k(const T* __restrict_
 template <typename T>
 __global__ void __launch_bounds__(256) colsum_k(const T* __restrict__ x, int64_t ld, int64_t rows, int64_t cols,
                                                 float* __restrict__ out) {
+  pdl_wait();
   extern __shared__ float red[];
   const ColTile t(rows, cols);
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -195,6 +198,7 @@ __global__ void __launch_bounds__(256) colsum_k(const T* __restrict__ x, int64_t
 template <typename T, typename IDX>
 __global__ void __launch_bounds__(256) bias_act_fwd_k(T* __restrict__ y, const float* __restrict__ bias, int64_t rows,
                                                       int64_t cols, int act) {
+  pdl_wait();
   const IDX cpr = (IDX)(cols / 8), n = (IDX)(rows * (cols / 8));
   for (IDX i = (IDX)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (IDX)gridDim.x * blockDim.x) {
     const IDX rr = i / cpr;
@@ -214,6 +218,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) bias_act_bwd_k(const T* __restrict__ dh, const T* __restrict__ h,
                                                       T* __restrict__ dy, float* __restrict__ dbias, int64_t rows,
                                                       int64_t cols, int act) {
+  pdl_wait();
   extern __shared__ float red[];
   const ColTile t(rows, cols);
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -263,6 +268,7 @@ template <int P>
 __global__ void __launch_bounds__(256) tri_gate_fwd_k(const bf16* __restrict__ y, int64_t rows, int hz,
                                                       bf16* __restrict__ a_cm, bf16* __restrict__ b_cm,
                                                       bool pairs) {
+  pdl_wait();
   constexpr int W = 4 * P;
   constexpr int RB = P <= 32 ? 64 : 32;
   __shared__ float ys[RB][W + 1];
@@ -300,6 +306,7 @@ template <int P, typename TD>
 __global__ void __launch_bounds__(256) tri_gate_bwd_k(const bf16* __restrict__ y, const TD* __restrict__ da,
                                                       const TD* __restrict__ db, int64_t rows, int hz,
                                                       bf16* __restrict__ dy, float* __restrict__ dsum) {
+  pdl_wait();
   constexpr int W = 4 * P;
   __shared__ float gs[64][2 * P + 1];
   __shared__ float cs[256 / (W / 8 < 256 ? W / 8 : 256)][W + 1];  // per row-group column partials
@@ -374,6 +381,7 @@ __global__ void __launch_bounds__(256) tri_gate_bwd_k(const bf16* __restrict__ y
 
 template <typename T>
 __global__ void count_nonfinite_k(const T* __restrict__ x, int64_t n, unsigned int* counter) {
+  pdl_wait();
   unsigned int local = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     local += isfinite(ldf<T>(x + i)) ? 0u : 1u;
@@ -398,6 +406,7 @@ __global__ void __launch_bounds__(256, RLN_MINB) residual_ln_k(const bf16* __res
                                                         const float* __restrict__ beta, bf16* __restrict__ ln,
                                                         float* __restrict__ mean, float* __restrict__ rstd,
                                                         int64_t rows, float eps) {
+  pdl_wait();
   // loads stay raw (one uint4 per 8 bf16) until used and the per-column vectors are re-read
   // through smem at use: RLN_MINB CTAs per SM, RLN_U row-groups of 3 loads in flight per lane
   constexpr int LPR = COLS / 8, RPW = 32 / LPR;
@@ -509,7 +518,7 @@ extern "C" int evo_gated_residual_fwd(const void* res, const void* y, int64_t y_
   cudaStream_t st = (cudaStream_t)stream;
   unsigned g = grid_for(rows * cols / 8, 256);
   const bool i32 = rows * (cols / 8) < (1LL << 31);
-#define GRF(T, I) gated_residual_fwd_k<T, I><<<g, 256, 0, st>>>((const T*)res, (const T*)y, y_rs, bias, (const T*)gp, \
+#define GRF(T, I) ::evo::pdl_launch(gated_residual_fwd_k<T, I>, g, 256, 0, st, (const T*)res, (const T*)y, y_rs, bias, (const T*)gp, \
                                                                 gp_rs, (T*)out, rows, cols)
   if (dtype == EVO_BF16) {
     if (i32) GRF(bf16, uint32_t); else GRF(bf16, int64_t);
@@ -547,11 +556,11 @@ extern "C" int evo_gated_residual_bwd(const void* dout, const void* y, int64_t y
   int rc = col_grid(rows, cols, grid, smem);
   if (rc) return rc;
   if (dtype == EVO_BF16)
-    gated_residual_bwd_k<bf16><<<grid, 256, smem, st>>>((const bf16*)dout, (const bf16*)y, y_rs, bias,
+    ::evo::pdl_launch(gated_residual_bwd_k<bf16>, grid, 256, smem, st, (const bf16*)dout, (const bf16*)y, y_rs, bias,
                                                         (const bf16*)gp, gp_rs, (bf16*)dy, (bf16*)dgp, dgp_rs, dbias,
                                                         dgp_sum, rows, cols);
   else
-    gated_residual_bwd_k<float><<<grid, 256, smem, st>>>((const float*)dout, (const float*)y, y_rs, bias,
+    ::evo::pdl_launch(gated_residual_bwd_k<float>, grid, 256, smem, st, (const float*)dout, (const float*)y, y_rs, bias,
                                                          (const float*)gp, gp_rs, (float*)dy, (float*)dgp, dgp_rs,
                                                          dbias, dgp_sum, rows, cols);
   EVO_LAUNCH_CHECK("gated_residual bwd");
@@ -567,8 +576,8 @@ extern "C" int evo_colsum(const void* x, int dtype, int64_t ld, int64_t rows, in
   size_t smem;
   int rc = col_grid(rows, cols, grid, smem);
   if (rc) return rc;
-  if (dtype == EVO_BF16) colsum_k<bf16><<<grid, 256, smem, st>>>((const bf16*)x, ld, rows, cols, out);
-  else colsum_k<float><<<grid, 256, smem, st>>>((const float*)x, ld, rows, cols, out);
+  if (dtype == EVO_BF16) ::evo::pdl_launch(colsum_k<bf16>, grid, 256, smem, st, (const bf16*)x, ld, rows, cols, out);
+  else ::evo::pdl_launch(colsum_k<float>, grid, 256, smem, st, (const float*)x, ld, rows, cols, out);
   EVO_LAUNCH_CHECK("colsum");
   return EVO_OK;
 }
@@ -582,11 +591,11 @@ extern "C" int evo_bias_act_fwd(void* y, const float* bias, int64_t rows, int64_
   unsigned g = grid_for(rows * cols / 8, 256);
   const bool i32 = rows * (cols / 8) < (1LL << 31);
   if (dtype == EVO_BF16) {
-    if (i32) bias_act_fwd_k<bf16, uint32_t><<<g, 256, 0, st>>>((bf16*)y, bias, rows, cols, act);
-    else bias_act_fwd_k<bf16, int64_t><<<g, 256, 0, st>>>((bf16*)y, bias, rows, cols, act);
+    if (i32) ::evo::pdl_launch(bias_act_fwd_k<bf16, uint32_t>, g, 256, 0, st, (bf16*)y, bias, rows, cols, act);
+    else ::evo::pdl_launch(bias_act_fwd_k<bf16, int64_t>, g, 256, 0, st, (bf16*)y, bias, rows, cols, act);
   } else {
-    if (i32) bias_act_fwd_k<float, uint32_t><<<g, 256, 0, st>>>((float*)y, bias, rows, cols, act);
-    else bias_act_fwd_k<float, int64_t><<<g, 256, 0, st>>>((float*)y, bias, rows, cols, act);
+    if (i32) ::evo::pdl_launch(bias_act_fwd_k<float, uint32_t>, g, 256, 0, st, (float*)y, bias, rows, cols, act);
+    else ::evo::pdl_launch(bias_act_fwd_k<float, int64_t>, g, 256, 0, st, (float*)y, bias, rows, cols, act);
   }
   EVO_LAUNCH_CHECK("bias_act fwd");
   return EVO_OK;
@@ -602,9 +611,9 @@ extern "C" int evo_bias_act_bwd(const void* dh, const void* h, void* dy, float* 
   int rc = col_grid(rows, cols, grid, smem);
   if (rc) return rc;
   if (dtype == EVO_BF16)
-    bias_act_bwd_k<bf16><<<grid, 256, smem, st>>>((const bf16*)dh, (const bf16*)h, (bf16*)dy, dbias, rows, cols, act);
+    ::evo::pdl_launch(bias_act_bwd_k<bf16>, grid, 256, smem, st, (const bf16*)dh, (const bf16*)h, (bf16*)dy, dbias, rows, cols, act);
   else
-    bias_act_bwd_k<float><<<grid, 256, smem, st>>>((const float*)dh, (const float*)h, (float*)dy, dbias, rows, cols,
+    ::evo::pdl_launch(bias_act_bwd_k<float>, grid, 256, smem, st, (const float*)dh, (const float*)h, (float*)dy, dbias, rows, cols,
                                                    act);
   EVO_LAUNCH_CHECK("bias_act bwd");
   return EVO_OK;
@@ -618,7 +627,7 @@ extern "C" int evo_tri_gate_fwd(const void* y, int64_t rows, int hz, int p, void
   unsigned g = (unsigned)((rows + (p <= 32 ? 63 : 31)) / (p <= 32 ? 64 : 32));
   // paired 4-byte stores need an even row count and 4-byte aligned channel-major outputs
   const bool pairs = (rows & 1) == 0 && ((uintptr_t)a_cm & 3) == 0 && ((uintptr_t)b_cm & 3) == 0;
-#define TG(PP) tri_gate_fwd_k<PP><<<g, 256, 0, st>>>((const bf16*)y, rows, hz, (bf16*)a_cm, (bf16*)b_cm, pairs)
+#define TG(PP) ::evo::pdl_launch(tri_gate_fwd_k<PP>, g, 256, 0, st, (const bf16*)y, rows, hz, (bf16*)a_cm, (bf16*)b_cm, pairs)
   switch (p) {
     case 2: TG(2); break;
     case 4: TG(4); break;
@@ -642,9 +651,9 @@ extern "C" int evo_tri_gate_bwd(const void* y, const void* da_cm, const void* db
   unsigned g = (unsigned)((rows + 63) / 64);
 #define TGB(PP)                                                                                                  \
   (d_dtype == EVO_BF16                                                                                           \
-       ? tri_gate_bwd_k<PP, bf16><<<g, 256, 0, st>>>((const bf16*)y, (const bf16*)da_cm, (const bf16*)db_cm, rows, \
+       ? ::evo::pdl_launch(tri_gate_bwd_k<PP, bf16>, g, 256, 0, st, (const bf16*)y, (const bf16*)da_cm, (const bf16*)db_cm, rows, \
                                                      hz, (bf16*)dy, dsum)                                        \
-       : tri_gate_bwd_k<PP, float><<<g, 256, 0, st>>>((const bf16*)y, (const float*)da_cm, (const float*)db_cm,    \
+       : ::evo::pdl_launch(tri_gate_bwd_k<PP, float>, g, 256, 0, st, (const bf16*)y, (const float*)da_cm, (const float*)db_cm,    \
                                                       rows, hz, (bf16*)dy, dsum))
   switch (p) {
     case 2: TGB(2); break;
@@ -665,8 +674,8 @@ extern "C" int evo_count_nonfinite(const void* x, int dtype, int64_t n, unsigned
   if (n == 0) return EVO_OK;
   cudaStream_t st = (cudaStream_t)stream;
   unsigned g = grid_for(n, 256);
-  if (dtype == EVO_BF16) count_nonfinite_k<bf16><<<g, 256, 0, st>>>((const bf16*)x, n, counter);
-  else count_nonfinite_k<float><<<g, 256, 0, st>>>((const float*)x, n, counter);
+  if (dtype == EVO_BF16) ::evo::pdl_launch(count_nonfinite_k<bf16>, g, 256, 0, st, (const bf16*)x, n, counter);
+  else ::evo::pdl_launch(count_nonfinite_k<float>, g, 256, 0, st, (const float*)x, n, counter);
   EVO_LAUNCH_CHECK("count_nonfinite");
   return EVO_OK;
 }
@@ -686,7 +695,7 @@ extern "C" int evo_residual_layernorm_fwd(const void* res, const void* y, int64_
   const int64_t rpw = 32 / (cols / 8);
   int64_t need = (rows + 8 * rpw * RLN_U - 1) / (8 * rpw * RLN_U), cap = (int64_t)sm_count() * RLN_MINB;
   dim3 g((unsigned)(need < cap ? need : cap));
-#define RLN(CC) residual_ln_k<CC, RLN_U><<<g, 256, 0, st>>>((const bf16*)res, (const bf16*)y, y_rs, bias, (const bf16*)gp, \
+#define RLN(CC) ::evo::pdl_launch(residual_ln_k<CC, RLN_U>, g, 256, 0, st, (const bf16*)res, (const bf16*)y, y_rs, bias, (const bf16*)gp, \
                                                         gp_rs, (bf16*)out, gamma, beta, (bf16*)ln, mean, rstd, rows, eps)
   switch (cols) {
     case 32: RLN(32); break;
@@ -710,6 +719,7 @@ __global__ void __launch_bounds__(256) gate_mul_k(const T* __restrict__ gate, in
                                                   const T* __restrict__ y, int64_t y_rs,
                                                   const float* __restrict__ bias, T* __restrict__ out,
                                                   int64_t out_rs, int64_t rows, int64_t cols) {
+  pdl_wait();
   const int64_t n = rows * cols;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / cols, c = i - r * cols;
@@ -734,10 +744,10 @@ extern "C" int evo_gate_mul_fwd(const void* gate, int64_t gate_rs, int gate_act,
   cudaStream_t st = (cudaStream_t)stream;
   unsigned g = grid_for(rows * cols, 256);
   if (dtype == EVO_BF16)
-    gate_mul_k<bf16><<<g, 256, 0, st>>>((const bf16*)gate, gate_rs, gate_act, (const bf16*)y, y_rs, bias, (bf16*)out,
+    ::evo::pdl_launch(gate_mul_k<bf16>, g, 256, 0, st, (const bf16*)gate, gate_rs, gate_act, (const bf16*)y, y_rs, bias, (bf16*)out,
                                         out_rs, rows, cols);
   else
-    gate_mul_k<float><<<g, 256, 0, st>>>((const float*)gate, gate_rs, gate_act, (const float*)y, y_rs, bias,
+    ::evo::pdl_launch(gate_mul_k<float>, g, 256, 0, st, (const float*)gate, gate_rs, gate_act, (const float*)y, y_rs, bias,
                                          (float*)out, out_rs, rows, cols);
   EVO_LAUNCH_CHECK("gate_mul fwd");
   return EVO_OK;
@@ -749,6 +759,7 @@ extern "C" int evo_gate_mul_fwd(const void* gate, int64_t gate_rs, int gate_act,
 // across the warp, one 16-byte store for the usual 8 columns.
 __global__ void __launch_bounds__(256) key_bias_cols_k(const float* __restrict__ dbias, int64_t B, int nh, int64_t L,
                                                        bf16* __restrict__ dst, int64_t sb, int64_t sl, int cols) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= B * L) return;
   const int64_t b = i / L, l = i - b * L;
@@ -771,7 +782,7 @@ extern "C" int evo_key_bias_grad_cols(const float* dbias, int64_t B, int nh, int
   EVO_CHECK_ARG(dbias && dst, EVO_ERR_ARG, "key_bias_grad_cols: null pointer");
   EVO_CHECK_ARG(B >= 0 && L >= 0 && nh >= 1 && cols >= nh, EVO_ERR_SHAPE, "key_bias_grad_cols: bad extents");
   if (B * L == 0) return EVO_OK;
-  key_bias_cols_k<<<grid_for(B * L, 256), 256, 0, (cudaStream_t)stream>>>(dbias, B, nh, L, (bf16*)dst, dst_sb, dst_sl,
+  ::evo::pdl_launch(key_bias_cols_k, grid_for(B * L, 256), 256, 0, (cudaStream_t)stream, dbias, B, nh, L, (bf16*)dst, dst_sb, dst_sl,
                                                                           cols);
   EVO_LAUNCH_CHECK("key_bias_grad_cols");
   return EVO_OK;

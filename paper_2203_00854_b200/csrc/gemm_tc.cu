@@ -82,6 +82,7 @@ template <int BN, bool A_MN, bool B_MN, int STAGES, typename TC>
 __global__ void __launch_bounds__(128) bgemm_kernel(MatArg A, MatArg B, MatArg C, uint32_t M, uint32_t N,
                                                     uint32_t K, float alpha, float beta, int c_mode, int splits,
                                                     float* __restrict__ ws) {
+  pdl_wait();
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t mbar[STAGES];
   __shared__ uint32_t tmem_base_sh;
@@ -252,6 +253,7 @@ template <typename TC>
 __global__ void __launch_bounds__(256) bgemm_splitk_reduce(const float* __restrict__ ws, MatArg C, uint32_t M,
                                                            uint32_t N, int64_t batch, int splits, float alpha,
                                                            float beta, int rows_contig) {
+  pdl_wait();
   const int64_t MN = (int64_t)M * N;
   const int64_t n8 = batch * MN / 8;
   char* Cbase = const_cast<char*>(C.ptr);
@@ -461,6 +463,7 @@ __global__ void __launch_bounds__(WS_GEMM_THREADS, 1) bgemm_ws_kernel(MatArg A, 
                                                           const __grid_constant__ CUtensorMap tmA,
                                                           const __grid_constant__ CUtensorMap tmB, TmaOp opA,
                                                           TmaOp opB) {
+  pdl_wait();
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
   __shared__ uint32_t tmem_sh;
@@ -776,7 +779,7 @@ static int launch_bgemm_s(MatArg A, MatArg B, MatArg C, int64_t batch, int64_t M
     attr_set = true;
   }
   dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + GEMM_BM - 1) / GEMM_BM), (unsigned)(batch * splits));
-  kern<<<grid, 128, smem, st>>>(A, B, C, (uint32_t)M, (uint32_t)N, (uint32_t)K, alpha, beta, c_mode, splits,
+  ::evo::pdl_launch(kern, grid, 128, smem, st, A, B, C, (uint32_t)M, (uint32_t)N, (uint32_t)K, alpha, beta, c_mode, splits,
                                 splits > 1 ? ws : nullptr);
   EVO_LAUNCH_CHECK("bgemm launch");
   if (splits > 1) {
@@ -784,7 +787,7 @@ static int launch_bgemm_s(MatArg A, MatArg B, MatArg C, int64_t batch, int64_t M
     EVO_CHECK_ARG(rows_contig || N % 8 == 0, EVO_ERR_ALIGN, "bgemm split-K: M or N must be a multiple of 8");
     int64_t n8 = batch * M * N / 8;
     int64_t g = (n8 + 255) / 256, cap = (int64_t)sm_count() * 16;
-    bgemm_splitk_reduce<TC><<<(unsigned)(g < cap ? g : cap), 256, 0, st>>>(ws, C, (uint32_t)M, (uint32_t)N, batch,
+    ::evo::pdl_launch(bgemm_splitk_reduce<TC>, (unsigned)(g < cap ? g : cap), 256, 0, st, ws, C, (uint32_t)M, (uint32_t)N, batch,
                                                                            splits, alpha, beta, rows_contig ? 1 : 0);
     EVO_LAUNCH_CHECK("bgemm split-K reduce");
   }
@@ -899,7 +902,7 @@ static int launch_bgemm_ws(MatArg A, MatArg B, MatArg C, int64_t batch, int64_t 
       if (e != cudaSuccess) return cuda_status(e, "bgemm_ws attr");
       attr_set = smem;
     }
-    kern<<<(unsigned)grid, WS_GEMM_THREADS, smem, st>>>(A, B, C, (uint32_t)M, (uint32_t)N, (uint32_t)K, alpha, beta,
+    ::evo::pdl_launch(kern, (unsigned)grid, WS_GEMM_THREADS, smem, st, A, B, C, (uint32_t)M, (uint32_t)N, (uint32_t)K, alpha, beta,
                                                         c_mode, splits, splits > 1 ? ws : nullptr, (int)batch, ta, tb,
                                                         oa, ob);
     return EVO_OK;
@@ -915,7 +918,7 @@ static int launch_bgemm_ws(MatArg A, MatArg B, MatArg C, int64_t batch, int64_t 
     EVO_CHECK_ARG(rows_contig || N % 8 == 0, EVO_ERR_ALIGN, "bgemm split-K: M or N must be a multiple of 8");
     int64_t n8 = batch * M * N / 8;
     int64_t g = (n8 + 255) / 256, cap = (int64_t)sm_count() * 16;
-    bgemm_splitk_reduce<TC><<<(unsigned)(g < cap ? g : cap), 256, 0, st>>>(ws, C, (uint32_t)M, (uint32_t)N, batch,
+    ::evo::pdl_launch(bgemm_splitk_reduce<TC>, (unsigned)(g < cap ? g : cap), 256, 0, st, ws, C, (uint32_t)M, (uint32_t)N, batch,
                                                                            splits, alpha, beta, rows_contig ? 1 : 0);
     EVO_LAUNCH_CHECK("bgemm split-K reduce");
   }
@@ -1053,6 +1056,7 @@ static int wgrad_bn(int64_t N) { return N >= 192 ? 256 : (N > 64 ? 128 : 64); }
 // per-warp sums meet in shared memory and are added in warp order (deterministic).
 __global__ void __launch_bounds__(256) wgrad_reduce(const float* __restrict__ ws, float* __restrict__ dw, int64_t ldw,
                                                     int M, int N, int splits) {
+  pdl_wait();
   __shared__ float4 part[8][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t MN = (int64_t)M * N;
@@ -1124,7 +1128,7 @@ extern "C" int evo_wgrad(const void* x, int64_t ldx, const void* dy, int64_t ldy
   if (rc || splits == 1) return rc;
   EVO_CHECK_ARG(ldw % 4 == 0, EVO_ERR_ALIGN, "wgrad: ldw must be a multiple of 4");
   const int64_t groups = (M * N / 4 + 31) / 32;
-  wgrad_reduce<<<(unsigned)groups, 256, 0, st>>>(ws, dw, ldw, (int)M, (int)N, splits);
+  ::evo::pdl_launch(wgrad_reduce, (unsigned)groups, 256, 0, st, ws, dw, ldw, (int)M, (int)N, splits);
   EVO_LAUNCH_CHECK("wgrad reduce");
   return EVO_OK;
 }

@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(256) ln_fwd_warp(const TX* __restrict__ x, int
                                                    float* __restrict__ rstd_out, int64_t rows, float eps,
                                                    const float* __restrict__ w, TY* __restrict__ dot_out,
                                                    int64_t dot_hs) {
+  pdl_wait();
   static_assert(K == 0, "fused row dots live in ln_rowdot_fwd");
   constexpr int COLS = VPT * 32;
   constexpr int U = VPT <= 8 ? 2 : 1;  // rows in flight per warp
@@ -158,6 +159,7 @@ __global__ void __launch_bounds__(256) ln_rowdot_fwd(const TX* __restrict__ x, c
                                                      TX* __restrict__ out, int64_t out_hs, TX* __restrict__ ln_out,
                                                      float* __restrict__ mean_out, float* __restrict__ rstd_out,
                                                      int64_t rows, float eps) {
+  pdl_wait();
   constexpr int COLS = VPT * 32, K = 8;
   const int lane = threadIdx.x & 31;
   float g[VPT], bt[VPT], wr[VPT][K];
@@ -215,6 +217,7 @@ __global__ void __launch_bounds__(256) ln_rowdot_bwd(const TX* __restrict__ x, c
                                                      const TX* res, TX* dx, float* __restrict__ dgamma,
                                                      float* __restrict__ dbeta, float* __restrict__ dw,
                                                      int64_t rows) {
+  pdl_wait();
   constexpr int COLS = VPT * 32, K = 8;
   __shared__ float red[8][COLS * (2 + K) / 8 + 1];  // per-warp partials, flushed in column slices
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -317,6 +320,7 @@ __global__ void __launch_bounds__(256) ln_fwd_grp(const TX* __restrict__ x, int6
                                                   const float* __restrict__ gamma, const float* __restrict__ beta,
                                                   TY* __restrict__ y, float* __restrict__ mean_out,
                                                   float* __restrict__ rstd_out, int64_t rows, float eps) {
+  pdl_wait();
   constexpr int LPR = COLS / 8, RPW = 32 / LPR;  // lanes per row, rows per warp step
   const int lane = threadIdx.x & 31, sub = lane / LPR, cl = (lane % LPR) * 8;
   float g[8], b[8];
@@ -393,6 +397,7 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_grp(const TD* __restrict__ dy, 
                                                      const float* __restrict__ rstd, TO* dx, const TO* res,
                                                      float* __restrict__ dgamma, float* __restrict__ dbeta,
                                                      float* __restrict__ dsum, int64_t rows) {
+  pdl_wait();
   constexpr int LPR = COLS / 8, RPW = 32 / LPR;
   __shared__ float red[8][3][COLS];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, sub = lane / LPR, cl = (lane % LPR) * 8;
@@ -514,6 +519,7 @@ __global__ void __launch_bounds__(CM_RT) ln_fwd_cm(const bf16* __restrict__ x, i
                                                    const float* __restrict__ gamma, const float* __restrict__ beta,
                                                    bf16* __restrict__ y, float* __restrict__ mean_out,
                                                    float* __restrict__ rstd_out, int64_t rows, float eps) {
+  pdl_wait();
   __shared__ __align__(16) bf16 xs[C][CM_RT + 8];
   __shared__ __align__(16) bf16 ys[CM_RT][C + 8];
   const int t = threadIdx.x;
@@ -564,6 +570,7 @@ __global__ void __launch_bounds__(CM_RT) ln_bwd_cm(const bf16* __restrict__ dy, 
                                                    const float* __restrict__ mean, const float* __restrict__ rstd,
                                                    bf16* dx, const bf16* res, float* __restrict__ dgamma,
                                                    float* __restrict__ dbeta, int64_t rows) {
+  pdl_wait();
   __shared__ __align__(16) bf16 xs[C][CM_RT + 8];   // x, then dx (channel-major)
   __shared__ __align__(16) bf16 ds[CM_RT][C + 8];   // dy (row-major)
   __shared__ float red[C][CM_RT + 1];                // per-row dgamma / dbeta terms, summed per channel
@@ -648,6 +655,7 @@ __global__ void __launch_bounds__(256) ln_fwd_thread(const TX* __restrict__ x, i
                                                      TY* __restrict__ y, float* __restrict__ mean_out,
                                                      float* __restrict__ rstd_out, int64_t rows, int cols,
                                                      float eps) {
+  pdl_wait();
   const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= rows) return;
   float v[MAXC];
@@ -693,6 +701,7 @@ __global__ void __launch_bounds__(256) ln_bwd_warp(const TD* __restrict__ dy, co
                                                    const float* __restrict__ rstd, TO* dx, const TO* res,
                                                    float* __restrict__ dgamma, float* __restrict__ dbeta,
                                                    int64_t rows) {
+  pdl_wait();
   constexpr int COLS = VPT * 32;
   extern __shared__ float red[];  // [8 warps][2][COLS]
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -764,6 +773,7 @@ __global__ void __launch_bounds__(256) ln_bwd_thread(const TD* __restrict__ dy, 
                                                      const float* __restrict__ mean, const float* __restrict__ rstd,
                                                      TO* dx, const TO* res, float* __restrict__ dgamma,
                                                      float* __restrict__ dbeta, int64_t rows) {
+  pdl_wait();
   __shared__ float red[2][8][C];
   float dg[C], db[C];
 #pragma unroll
@@ -841,7 +851,7 @@ static int ln_fwd_dispatch_warp(const void* x, int64_t x_rs, const float* g, con
     const int64_t rpw = 32 / (cols / 8);
     int64_t need = (rows + 8 * rpw * 2 - 1) / (8 * rpw * 2), cap = (int64_t)sm_count() * 8;
     dim3 g2((unsigned)(need < cap ? need : cap));
-#define LNG(CC) ln_fwd_grp<TX, TY, CC, 2><<<g2, 256, 0, st>>>((const TX*)x, x_rs, g, b, (TY*)y, mean, rstd, rows, eps)
+#define LNG(CC) ::evo::pdl_launch(ln_fwd_grp<TX, TY, CC, 2>, g2, 256, 0, st, (const TX*)x, x_rs, g, b, (TY*)y, mean, rstd, rows, eps)
     switch (cols) {
       case 32: LNG(32); break;
       case 64: LNG(64); break;
@@ -856,7 +866,7 @@ static int ln_fwd_dispatch_warp(const void* x, int64_t x_rs, const float* g, con
   int64_t need = (rows + 2 * wpb - 1) / (2 * wpb), cap = (int64_t)sm_count() * 8;
   dim3 grid((unsigned)(need < cap ? need : cap));
 #define LNF(VPT)                                                                                             \
-  ln_fwd_warp<TX, TY, VPT, K><<<grid, wpb * 32, 0, st>>>((const TX*)x, x_rs, g, b, (TY*)y, mean, rstd, rows, \
+  ::evo::pdl_launch(ln_fwd_warp<TX, TY, VPT, K>, grid, wpb * 32, 0, st, (const TX*)x, x_rs, g, b, (TY*)y, mean, rstd, rows, \
                                                          eps, w, (TY*)dot, dot_hs)
   switch (cols) {
     case 32: LNF(1); break;
@@ -893,15 +903,15 @@ static int ln_fwd_impl(const void* x, int64_t x_rs, int64_t x_cs, const float* g
   if (sizeof(TX) == 2 && sizeof(TY) == 2 && x_rs == 1 && x_cs % 8 == 0 && ((uintptr_t)x & 15) == 0 &&
       ((uintptr_t)y & 15) == 0 && (cols == 16 || cols == 32 || cols == 64)) {
     dim3 gc((unsigned)((rows + CM_RT - 1) / CM_RT));
-    if (cols == 16) ln_fwd_cm<16><<<gc, CM_RT, 0, st>>>((const bf16*)x, x_cs, g, b, (bf16*)y, mean, rstd, rows, eps);
-    else if (cols == 32) ln_fwd_cm<32><<<gc, CM_RT, 0, st>>>((const bf16*)x, x_cs, g, b, (bf16*)y, mean, rstd, rows, eps);
-    else ln_fwd_cm<64><<<gc, CM_RT, 0, st>>>((const bf16*)x, x_cs, g, b, (bf16*)y, mean, rstd, rows, eps);
+    if (cols == 16) ::evo::pdl_launch(ln_fwd_cm<16>, gc, CM_RT, 0, st, (const bf16*)x, x_cs, g, b, (bf16*)y, mean, rstd, rows, eps);
+    else if (cols == 32) ::evo::pdl_launch(ln_fwd_cm<32>, gc, CM_RT, 0, st, (const bf16*)x, x_cs, g, b, (bf16*)y, mean, rstd, rows, eps);
+    else ::evo::pdl_launch(ln_fwd_cm<64>, gc, CM_RT, 0, st, (const bf16*)x, x_cs, g, b, (bf16*)y, mean, rstd, rows, eps);
     EVO_LAUNCH_CHECK("layernorm fwd channel-major");
     return EVO_OK;
   }
   dim3 grid((unsigned)((rows + 255) / 256));
   // exact widths get the 16-byte row stores (cols == MAXC)
-#define LFT(MC) ln_fwd_thread<TX, TY, MC><<<grid, 256, 0, st>>>((const TX*)x, x_rs, x_cs, g, b, (TY*)y, mean, rstd, \
+#define LFT(MC) ::evo::pdl_launch(ln_fwd_thread<TX, TY, MC>, grid, 256, 0, st, (const TX*)x, x_rs, x_cs, g, b, (TY*)y, mean, rstd, \
                                                                 rows, (int)cols, eps)
   if (cols == 32) LFT(32);
   else if (cols == 16) LFT(16);
@@ -935,7 +945,7 @@ extern "C" int evo_layernorm_rowdot_fwd(const void* x, int x_dtype, const float*
   int64_t need = (rows + 7) / 8, cap = (int64_t)sm_count() * 8;
   dim3 grid((unsigned)(need < cap ? need : cap));
 #define RDF(VPT)                                                                                               \
-  ln_rowdot_fwd<bf16, VPT><<<grid, 256, 0, st>>>((const bf16*)x, gamma, beta, w, (bf16*)out, out_hs, (bf16*)ln_out, \
+  ::evo::pdl_launch(ln_rowdot_fwd<bf16, VPT>, grid, 256, 0, st, (const bf16*)x, gamma, beta, w, (bf16*)out, out_hs, (bf16*)ln_out, \
                                                  mean, rstd, rows, eps)
   switch (cols) {
     case 32: RDF(1); break;
@@ -961,7 +971,7 @@ extern "C" int evo_layernorm_rowdot_bwd(const void* x, int x_dtype, const float*
   int64_t need = (rows + 63) / 64, cap = (int64_t)sm_count() * 2;
   dim3 grid((unsigned)(need < cap ? need : cap));
 #define RDB(VPT)                                                                                                 \
-  ln_rowdot_bwd<bf16, VPT><<<grid, 256, 0, st>>>((const bf16*)x, gamma, beta, w, dout, out_hs, mean, rstd,        \
+  ::evo::pdl_launch(ln_rowdot_bwd<bf16, VPT>, grid, 256, 0, st, (const bf16*)x, gamma, beta, w, dout, out_hs, mean, rstd,        \
                                                  (const bf16*)res, (bf16*)dx, dgamma, dbeta, dw, rows)
   switch (cols) {
     case 32: RDB(1); break;
@@ -983,7 +993,7 @@ static int ln_bwd_impl(const void* dy, const void* x, int64_t x_rs, int64_t x_cs
     int64_t need = (rows + 8 * rpw * 3 - 1) / (8 * rpw * 3), cap = (int64_t)sm_count() * 2;  // resident
     dim3 grid((unsigned)(need < cap ? need : cap));
 #define LBG(CC)                                                                                               \
-  ln_bwd_grp<TD, TX, TO, CC, 3><<<grid, 256, 0, st>>>((const TD*)dy, (const TX*)x, x_rs, g, mean, \
+  ::evo::pdl_launch(ln_bwd_grp<TD, TX, TO, CC, 3>, grid, 256, 0, st, (const TD*)dy, (const TX*)x, x_rs, g, mean, \
                                                                         rstd, (TO*)dx, (const TO*)res, dg, db, dsum, rows)
     switch (cols) {
       case 32: LBG(32); break;
@@ -1002,7 +1012,7 @@ static int ln_bwd_impl(const void* dy, const void* x, int64_t x_rs, int64_t x_cs
     dim3 grid((unsigned)(need < cap ? need : cap));
     size_t sm = 16 * cols * sizeof(float);
 #define LNB(VPT)                                                                                            \
-  ln_bwd_warp<TD, TX, TO, VPT><<<grid, 256, sm, st>>>((const TD*)dy, (const TX*)x, x_rs, g, mean, rstd,     \
+  ::evo::pdl_launch(ln_bwd_warp<TD, TX, TO, VPT>, grid, 256, sm, st, (const TD*)dy, (const TX*)x, x_rs, g, mean, rstd,     \
                                                       (TO*)dx, (const TO*)res, dg, db, rows)
     switch (cols) {
       case 32: LNB(1); break;
@@ -1021,7 +1031,7 @@ static int ln_bwd_impl(const void* dy, const void* x, int64_t x_rs, int64_t x_cs
       (((uintptr_t)x | (uintptr_t)dx | (uintptr_t)dy) & 15) == 0 && (cols == 16 || cols == 32)) {
     dim3 gc((unsigned)((rows + CM_RT - 1) / CM_RT));
 #define LBC(CC)                                                                                                   \
-  ln_bwd_cm<CC><<<gc, CM_RT, 0, st>>>((const bf16*)dy, (const bf16*)x, x_cs, g, mean, rstd, (bf16*)dx, (const bf16*)res, \
+  ::evo::pdl_launch(ln_bwd_cm<CC>, gc, CM_RT, 0, st, (const bf16*)dy, (const bf16*)x, x_cs, g, mean, rstd, (bf16*)dx, (const bf16*)res, \
                                       dg, db, rows)
     if (cols == 16) LBC(16);
     else LBC(32);
@@ -1032,7 +1042,7 @@ static int ln_bwd_impl(const void* dy, const void* x, int64_t x_rs, int64_t x_cs
   int64_t need = (rows + 255) / 256, cap = (int64_t)sm_count() * 4;
   dim3 grid((unsigned)(need < cap ? need : cap));
 #define LNT(CC)                                                                                              \
-  ln_bwd_thread<TD, TX, TO, CC><<<grid, 256, 0, st>>>((const TD*)dy, (const TX*)x, x_rs, x_cs, g, mean, rstd, \
+  ::evo::pdl_launch(ln_bwd_thread<TD, TX, TO, CC>, grid, 256, 0, st, (const TD*)dy, (const TX*)x, x_rs, x_cs, g, mean, rstd, \
                                                       (TO*)dx, (const TO*)res, dg, db, rows)
   switch (cols) {
     case 2: LNT(2); break;

@@ -109,6 +109,7 @@ template <int HZ>
 __global__ void __launch_bounds__(OPM_THREADS, 1)
     opm_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmO, OpmArgs g) {
+  pdl_wait();
   constexpr uint32_t WG_BYTES = HZ * 64 * 2;  // W_o granule: 64 k rows x HZ c
   constexpr uint32_t W_ATOM = HZ >= 64 ? 8192 : 4096;  // one 64-c (32-c) swizzle column of a granule
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -359,6 +360,7 @@ __global__ void __launch_bounds__(OPM_THREADS, 1)
 __global__ void __launch_bounds__(256) opm_transpose_kernel(const bf16* __restrict__ x, int64_t ld, int64_t col0, int S,
                                                             int R, int P, bf16* __restrict__ out_a,
                                                             bf16* __restrict__ out_b) {
+  pdl_wait();
   extern __shared__ __align__(16) uint8_t tsm[];
   bf16* t = reinterpret_cast<bf16*>(tsm);  // [S][CW + 8] (CW = P or 2P channels)
   const int r = blockIdx.x;
@@ -414,6 +416,7 @@ struct OpmBwdArgs {
 __global__ void __launch_bounds__(OB_THREADS, 1)
     opm_bwd_contract_kernel(const __grid_constant__ CUtensorMap tmDY, const __grid_constant__ CUtensorMap tmW,
                             const __grid_constant__ CUtensorMap tmO, OpmBwdArgs g) {
+  pdl_wait();
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t w_full, w_empty, dy_full[2], dy_empty[2], ot_full[2], ot_empty[2], da_full[2], da_empty[2],
       ab_full[2], ab_empty[2], acc_full, acc_empty;
@@ -625,6 +628,7 @@ template <typename TO>
 __global__ void __launch_bounds__(256) opm_bwd_finish(const float* __restrict__ part, int nsplit, int X, int S,
                                                       float alpha, TO* __restrict__ out, int64_t o_ss, int64_t o_sr,
                                                       int64_t o_sx, int x_split) {
+  pdl_wait();
   __shared__ float t[32][129];
   const int x = blockIdx.x;
   // the [32 p][128 s] slab: 4 float4 per thread and split, every load of a thread in flight
@@ -681,7 +685,7 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tw, 
     attr = true;
   }
   const int grid = a.tiles < sm_count() ? a.tiles : sm_count();
-  opm_fused_kernel<HZ><<<grid, OPM_THREADS, smem, st>>>(ta, tb, tw, to, a);
+  ::evo::pdl_launch(opm_fused_kernel<HZ>, grid, OPM_THREADS, smem, st, ta, tb, tw, to, a);
   EVO_LAUNCH_CHECK("opm_fused launch");
   return EVO_OK;
 }
@@ -779,7 +783,7 @@ extern "C" int evo_opm_transpose(const void* x, int64_t ld, int64_t col0, int64_
     if (e != cudaSuccess) return cuda_status(e, "opm_transpose attr");
     attr = true;
   }
-  opm_transpose_kernel<<<(unsigned)R, 256, smem, (cudaStream_t)stream>>>(
+  ::evo::pdl_launch(opm_transpose_kernel, (unsigned)R, 256, smem, (cudaStream_t)stream, 
       static_cast<const bf16*>(x), ld, col0, (int)S, (int)R, (int)P, static_cast<bf16*>(out_a), static_cast<bf16*>(out_b));
   EVO_LAUNCH_CHECK("opm_transpose launch");
   return EVO_OK;
@@ -837,13 +841,13 @@ static int opm_bwd_one(int role, const void* dy, int64_t ldy, const void* w_o, c
     attr = true;
   }
   const int grid = a.units < sm_count() ? a.units : sm_count();
-  opm_bwd_contract_kernel<<<grid, OB_THREADS, smem, st>>>(tdy, tw, to, a);
+  ::evo::pdl_launch(opm_bwd_contract_kernel, grid, OB_THREADS, smem, st, tdy, tw, to, a);
   EVO_LAUNCH_CHECK("opm_bwd contract launch");
   if (out_f32)
-    opm_bwd_finish<float><<<(unsigned)X, 256, 0, st>>>(part, nsplit, (int)X, (int)S, alpha, static_cast<float*>(out),
+    ::evo::pdl_launch(opm_bwd_finish<float>, (unsigned)X, 256, 0, st, part, nsplit, (int)X, (int)S, alpha, static_cast<float*>(out),
                                                        o_ss, o_sr, o_sx, (int)x_split);
   else
-    opm_bwd_finish<bf16><<<(unsigned)X, 256, 0, st>>>(part, nsplit, (int)X, (int)S, alpha, static_cast<bf16*>(out),
+    ::evo::pdl_launch(opm_bwd_finish<bf16>, (unsigned)X, 256, 0, st, part, nsplit, (int)X, (int)S, alpha, static_cast<bf16*>(out),
                                                       o_ss, o_sr, o_sx, (int)x_split);
   EVO_LAUNCH_CHECK("opm_bwd finish launch");
   return EVO_OK;

@@ -79,6 +79,7 @@ template <int VEC, int NCH>
 __global__ void __launch_bounds__(256) softmax_fwd_kernel(const void* __restrict__ x, int xd, Bcast bias, Bcast mask,
                                                           void* __restrict__ y, int yd, int64_t H, int64_t Q,
                                                           int64_t rows, int K, float scale_log2) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -143,6 +144,7 @@ template <int VEC, int NCH>
 __global__ void __launch_bounds__(256) softmax_bwd_kernel(const void* __restrict__ y, int yd, const void* __restrict__ dy,
                                                           int dyd, void* __restrict__ dx, int dxd, int64_t rows, int K,
                                                           float scale) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -181,29 +183,29 @@ using namespace evo;
     int nch = (int)((K + 32 * vec - 1) / (32 * vec));                                \
     if (vec == 8) {                                                                  \
       switch (nch) {                                                                 \
-        case 1: KERN<8, 1><<<grid, 256, 0, st>>>(__VA_ARGS__); break;                \
-        case 2: KERN<8, 2><<<grid, 256, 0, st>>>(__VA_ARGS__); break;                \
-        case 3: KERN<8, 3><<<grid, 256, 0, st>>>(__VA_ARGS__); break;                \
-        case 4: KERN<8, 4><<<grid, 256, 0, st>>>(__VA_ARGS__); break;                \
-        case 5: case 6: KERN<8, 6><<<grid, 256, 0, st>>>(__VA_ARGS__); break;        \
-        case 7: case 8: KERN<8, 8><<<grid, 256, 0, st>>>(__VA_ARGS__); break;        \
+        case 1: ::evo::pdl_launch(KERN<8, 1>, grid, 256, 0, st, __VA_ARGS__); break;                \
+        case 2: ::evo::pdl_launch(KERN<8, 2>, grid, 256, 0, st, __VA_ARGS__); break;                \
+        case 3: ::evo::pdl_launch(KERN<8, 3>, grid, 256, 0, st, __VA_ARGS__); break;                \
+        case 4: ::evo::pdl_launch(KERN<8, 4>, grid, 256, 0, st, __VA_ARGS__); break;                \
+        case 5: case 6: ::evo::pdl_launch(KERN<8, 6>, grid, 256, 0, st, __VA_ARGS__); break;        \
+        case 7: case 8: ::evo::pdl_launch(KERN<8, 8>, grid, 256, 0, st, __VA_ARGS__); break;        \
         default: set_error("softmax: K=%lld too large (max 2048)", (long long)K);   \
                  return EVO_ERR_SHAPE;                                               \
       }                                                                              \
     } else if (vec == 4) {                                                           \
       switch (nch) {                                                                 \
-        case 1: KERN<4, 1><<<grid, 256, 0, st>>>(__VA_ARGS__); break;                \
-        case 2: KERN<4, 2><<<grid, 256, 0, st>>>(__VA_ARGS__); break;                \
-        case 3: case 4: KERN<4, 4><<<grid, 256, 0, st>>>(__VA_ARGS__); break;        \
+        case 1: ::evo::pdl_launch(KERN<4, 1>, grid, 256, 0, st, __VA_ARGS__); break;                \
+        case 2: ::evo::pdl_launch(KERN<4, 2>, grid, 256, 0, st, __VA_ARGS__); break;                \
+        case 3: case 4: ::evo::pdl_launch(KERN<4, 4>, grid, 256, 0, st, __VA_ARGS__); break;        \
         default: set_error("softmax: K=%lld unsupported", (long long)K);             \
                  return EVO_ERR_SHAPE;                                               \
       }                                                                              \
     } else {                                                                         \
       switch (nch) {                                                                 \
-        case 1: KERN<1, 1><<<grid, 256, 0, st>>>(__VA_ARGS__); break;                \
-        case 2: KERN<1, 2><<<grid, 256, 0, st>>>(__VA_ARGS__); break;                \
-        case 3: case 4: KERN<1, 4><<<grid, 256, 0, st>>>(__VA_ARGS__); break;        \
-        case 5: case 6: case 7: case 8: KERN<1, 8><<<grid, 256, 0, st>>>(__VA_ARGS__); break; \
+        case 1: ::evo::pdl_launch(KERN<1, 1>, grid, 256, 0, st, __VA_ARGS__); break;                \
+        case 2: ::evo::pdl_launch(KERN<1, 2>, grid, 256, 0, st, __VA_ARGS__); break;                \
+        case 3: case 4: ::evo::pdl_launch(KERN<1, 4>, grid, 256, 0, st, __VA_ARGS__); break;        \
+        case 5: case 6: case 7: case 8: ::evo::pdl_launch(KERN<1, 8>, grid, 256, 0, st, __VA_ARGS__); break; \
         default: set_error("softmax: K=%lld unsupported", (long long)K);             \
                  return EVO_ERR_SHAPE;                                               \
       }                                                                              \
