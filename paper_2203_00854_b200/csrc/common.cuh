@@ -37,6 +37,13 @@ int cuda_status(cudaError_t e, const char* where);
 
 typedef __nv_bfloat16 bf16;
 
+// EVO_PDL_TRIGGER=1 (experiment builds): also trigger the dependent launch at kernel entry instead of
+// implicitly at exit - measured slower (105.5 -> 107.9-109.2 ms/step, profiles/r02_pdl_ab.txt): the
+// waiting dependent CTAs take issue slots and SM residency from the draining kernel
+#ifndef EVO_PDL_TRIGGER
+#define EVO_PDL_TRIGGER 0
+#endif
+
 // Programmatic dependent launch: every kernel of this library is launched with programmatic stream
 // serialization allowed and starts with griddepcontrol.wait, so its CTAs are scheduled (launch
 // latency, prologue) while the previous kernel of the stream drains, and touch global memory only
@@ -44,6 +51,9 @@ typedef __nv_bfloat16 bf16;
 __device__ __forceinline__ void pdl_wait() {
 #if defined(__CUDA_ARCH__)
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
+#if EVO_PDL_TRIGGER
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+#endif
 #endif
 }
 bool pdl_enabled();

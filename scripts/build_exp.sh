@@ -9,7 +9,7 @@ for n in "$@"; do
   for f in $P/csrc/*.cu; do
     o=/tmp/exp${n}_$(basename $f .cu).o
     nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr \
-      -I $ROOT/include -DEVO_EXP=$n -c $f -o $o &
+      -I $ROOT/include -DEVO_EXP=$n ${EXTRA_FLAGS} -c $f -o $o &
     objs="$objs $o"
   done
   wait
