@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
   constexpr bool BIASS = MODE == 2 && CP <= 32;
   using SM = BwdSmem<CP, BIASS>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bar1, bar2, tbar[2], bbar;
+  __shared__ uint64_t bar1, bar2, bar3, tbar[2], bbar;
   __shared__ uint32_t tmem_sh;
   const uint32_t sb = smem_u32(smem);
   constexpr bool PTM = SM::PTM;
@@ -388,6 +388,7 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
     mbar_init(&tbar[0], 1);
     mbar_init(&tbar[1], 1);
     mbar_init(&bbar, 1);
+    mbar_init(&bar3, 1);
     fence_mbar_init();
   }
   __syncthreads();  // the TMA path issues into tbar right below
@@ -501,6 +502,7 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
   }
 #endif
   int it = 0;
+  uint32_t n_early = 0;  // bar3 phases (one per early_next tile; uniform over threads)
   bf16 kb_next = f2bf(0.f);  // per-key bias of the next unit (MODE 1)
   bool first_unit = true;
   for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
@@ -527,6 +529,10 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
     for (int qt = 0; qt < nqt; ++qt, ++it) {
       const int q0 = qt * BW_BQ;
       const int buf = DB ? (it & 1) : 0;
+      // single-buffered tiles (msa_row's bias tile takes the second buffer's room): the next query
+      // tile of the unit is loaded as soon as the dV / dK MMAs (its last readers) are done, under the
+      // dQ MMAs, instead of after all of them
+      const bool early_next = !DB && tmaq && qt + 1 < nqt;
       const uint32_t sQ = sb + SM::Q + buf * SM::QD_BYTES, sDO = sb + SM::DO + buf * SM::QD_BYTES;
       const float* s_lse = reinterpret_cast<const float*>(smem + SM::LSE + buf * BW_BQ * 4);
       const float* s_D = reinterpret_cast<const float*>(smem + SM::DD + buf * BW_BQ * 4);
@@ -719,6 +725,7 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
             mma_bf16(tmem + T_DK, make_sdesc(sb + SM::DST + aoff, LBO_ROWS, 128), d_q, ID_KV, kk != 0);
           }
         }
+        if (early_next) mma_commit(&bar3);  // dV / dK done: Q and dO are free
 #pragma unroll
         for (int kk = 0; kk < BW_BK / 16; ++kk) {
           const uint32_t off = kk * 2 * 128;
@@ -727,7 +734,12 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
         }
 #endif
         mma_commit(&bar2);
+        if (early_next) {  // the next query tile's Q / dO / lse / D load under the dQ MMAs
+          mbar_wait(&bar3, n_early & 1);
+          issue_loads(b, h, k0, qt + 1, false, 0);
+        }
       }
+      if (early_next) ++n_early;
       if (db_store && tmaq) {
         // (TMA store of the dS^T tile: issued after the next tile's loads, below)
       } else if constexpr (db_store) {
@@ -761,7 +773,7 @@ __global__ void __launch_bounds__(256, 2) attn_bwd_kernel(AttnBwdParams P, int n
       // the tiles are free: prefetch the next (batch, query tile) while draining TMEM
       const bool last_q = qt + 1 == nqt;
       if (!last_q) {
-        if (!DB) issue_loads(b, h, k0, qt + 1, false, 0);
+        if (!DB && !early_next) issue_loads(b, h, k0, qt + 1, false, 0);
       } else if (u + gridDim.x < units) {
         int64_t nb;
         int nh, nkt_;
