@@ -942,7 +942,7 @@ extern "C" int evo_bwd_trace(void* dst) { return (int)cudaMemcpyFromSymbol(dst, 
 namespace evo {
 #endif
 template <int NP>
-__global__ void __launch_bounds__(256) attn_bwd_dq_finish(AttnBwdParams P, int64_t B) {
+__global__ void __launch_bounds__(256) attn_bwd_dq_finish(AttnBwdParams P, int64_t B, int sh_hc, int sh_l) {
   pdl_wait();
   const int L = P.f.L, H = P.f.H, c = P.f.c;
   const int64_t n = B * L * (int64_t)H * c;
@@ -950,7 +950,10 @@ __global__ void __launch_bounds__(256) attn_bwd_dq_finish(AttnBwdParams P, int64
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = i * 8;
     const uint32_t eu = (uint32_t)e, hc = (uint32_t)(H * c);  // n < 2^31 (host-checked)
-    const uint32_t rowu = eu / hc, bu = rowu / (uint32_t)L;
+    // shifts when H*c and L are powers of two (sh >= 0): the emulated divisions cost more issue
+    // slots than the element work
+    const uint32_t rowu = sh_hc >= 0 ? eu >> sh_hc : eu / hc;
+    const uint32_t bu = sh_l >= 0 ? rowu >> sh_l : rowu / (uint32_t)L;
     const int64_t col = eu - rowu * hc, b = bu, l = rowu - bu * (uint32_t)L;
     float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if constexpr (NP == 0) {  // one fp32 accumulator (atomics, > DQ_MAX_PARTS key tiles)
@@ -1176,11 +1179,13 @@ extern "C" int evo_gated_attention_bwd(const EvoAttnBwdDesc* d, void* stream) {
   int64_t n8 = B * L * H * c / 8;
   int64_t g = (n8 + 255) / 256, cap = (int64_t)sm_count() * 16;
   const unsigned gf = (unsigned)(g < cap ? g : cap);
+  auto lg2 = [](int64_t v) { int k = 0; while ((int64_t(1) << k) < v) ++k; return (int64_t(1) << k) == v ? k : -1; };
+  const int sh_hc = lg2((int64_t)H * c), sh_l = lg2(L);
   switch (dq_partial ? (int)nkt : 0) {  // 0: fp32 atomic accumulator; 2..4: bf16 per-tile partials
-    case 0: ::evo::pdl_launch(attn_bwd_dq_finish<0>, gf, 256, 0, st, p, B); break;
-    case 2: ::evo::pdl_launch(attn_bwd_dq_finish<2>, gf, 256, 0, st, p, B); break;
-    case 3: ::evo::pdl_launch(attn_bwd_dq_finish<3>, gf, 256, 0, st, p, B); break;
-    default: ::evo::pdl_launch(attn_bwd_dq_finish<4>, gf, 256, 0, st, p, B); break;
+    case 0: ::evo::pdl_launch(attn_bwd_dq_finish<0>, gf, 256, 0, st, p, B, sh_hc, sh_l); break;
+    case 2: ::evo::pdl_launch(attn_bwd_dq_finish<2>, gf, 256, 0, st, p, B, sh_hc, sh_l); break;
+    case 3: ::evo::pdl_launch(attn_bwd_dq_finish<3>, gf, 256, 0, st, p, B, sh_hc, sh_l); break;
+    default: ::evo::pdl_launch(attn_bwd_dq_finish<4>, gf, 256, 0, st, p, B, sh_hc, sh_l); break;
   }
   EVO_LAUNCH_CHECK("attention bwd finish");
   return EVO_OK;
