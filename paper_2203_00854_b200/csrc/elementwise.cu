@@ -397,7 +397,20 @@ __global__ void count_nonfinite_k(const T* __restrict__ x, int64_t n, unsigned i
 // U rows per lane group per step with every load issued first.
 // measured (scripts/rln_micro.py): 2 row groups per lane at 3 CTAs/SM beat 4 at 2 CTAs/SM
 // (e.g. [65536,128] 13.9 -> 13.1 us, gated 16.6 -> 15.2 us)
+// RLN_PIPE (default): one row group per lane, software-pipelined (the next group's loads issued
+// before this group's math), 3 CTAs/SM - scripts/rln_micro.py: [65536,128] 12.9 -> 12.1 us, gated
+// 14.9 -> 13.5 us, [32768,256] 13.1 -> 12.4 us against the unpipelined two-group form (RLN_PIPE=0)
+#ifndef RLN_PIPE
+#define RLN_PIPE 1
+#endif
+#if RLN_PIPE
+#ifndef RLN_MINB_PIPE
+#define RLN_MINB_PIPE 3
+#endif
+constexpr int RLN_U = 1, RLN_MINB = RLN_MINB_PIPE;
+#else
 constexpr int RLN_U = 2, RLN_MINB = 3;
+#endif
 template <int COLS, int U>
 __global__ void __launch_bounds__(256, RLN_MINB) residual_ln_k(const bf16* __restrict__ res, const bf16* __restrict__ y,
                                                         int64_t y_rs, const float* __restrict__ bias,
@@ -421,6 +434,92 @@ __global__ void __launch_bounds__(256, RLN_MINB) residual_ln_k(const bf16* __res
   const volatile float4* vg = cv[1];
   const volatile float4* vt = cv[2];
   const int lane = threadIdx.x & 31, sub = lane / LPR, cl = (lane % LPR) * 8;
+#if RLN_PIPE
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t step = nw * RPW * U;
+  uint4 rr[U], yr[U], gr[U];
+  auto load = [&](int64_t rb_) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t row = rb_ + u * RPW + sub;
+      if (row < rows) {
+        rr[u] = __ldcs(reinterpret_cast<const uint4*>(res + row * COLS + cl));
+        yr[u] = __ldcs(reinterpret_cast<const uint4*>(y + row * y_rs + cl));
+        if (gp) gr[u] = __ldcs(reinterpret_cast<const uint4*>(gp + row * gp_rs + cl));
+      }
+    }
+  };
+  int64_t rb = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * RPW * U;
+  if (rb < rows) load(rb);
+  for (; rb < rows; rb += step) {
+    // software pipeline (RLN_PIPE): the raw loads of this lane's next row group are issued before this
+    // group's math and stores, so the memory pipe never drains between groups
+    uint4 rc[U], yc[U], gc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) { rc[u] = rr[u]; yc[u] = yr[u]; gc[u] = gr[u]; }
+    if (rb + step < rows) load(rb + step);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t row = rb + u * RPW + sub;
+      float o[8], t[8], s = 0.f;
+      unpack_bf16x2(rc[u].x, o[0], o[1]); unpack_bf16x2(rc[u].y, o[2], o[3]);
+      unpack_bf16x2(rc[u].z, o[4], o[5]); unpack_bf16x2(rc[u].w, o[6], o[7]);
+      unpack_bf16x2(yc[u].x, t[0], t[1]); unpack_bf16x2(yc[u].y, t[2], t[3]);
+      unpack_bf16x2(yc[u].z, t[4], t[5]); unpack_bf16x2(yc[u].w, t[6], t[7]);
+      {
+        const float4 b0 = const_cast<const float4&>(vb[cl / 4]);
+        const float4 b1 = const_cast<const float4&>(vb[cl / 4 + 1]);
+        t[0] += b0.x; t[1] += b0.y; t[2] += b0.z; t[3] += b0.w;
+        t[4] += b1.x; t[5] += b1.y; t[6] += b1.z; t[7] += b1.w;
+      }
+      if (gp) {
+        float gv[8];
+        unpack_bf16x2(gc[u].x, gv[0], gv[1]); unpack_bf16x2(gc[u].y, gv[2], gv[3]);
+        unpack_bf16x2(gc[u].z, gv[4], gv[5]); unpack_bf16x2(gc[u].w, gv[6], gv[7]);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) t[e] = __fmul_rn(t[e], sigmoidf_(gv[e]));
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] += t[e];
+      // LayerNorm statistics of the bf16-rounded residual stream (what the next module reads)
+      uint4 w;
+      w.x = pack_bf16x2(o[0], o[1]); w.y = pack_bf16x2(o[2], o[3]);
+      w.z = pack_bf16x2(o[4], o[5]); w.w = pack_bf16x2(o[6], o[7]);
+      unpack_bf16x2(w.x, o[0], o[1]); unpack_bf16x2(w.y, o[2], o[3]);
+      unpack_bf16x2(w.z, o[4], o[5]); unpack_bf16x2(w.w, o[6], o[7]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s += o[e];
+#pragma unroll
+      for (int off = LPR / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      const float mu = s * (1.0f / COLS);
+      float q = 0.f;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) q += (o[e] - mu) * (o[e] - mu);
+#pragma unroll
+      for (int off = LPR / 2; off > 0; off >>= 1) q += __shfl_xor_sync(0xffffffffu, q, off);
+      const float rs = rsqrtf(q * (1.0f / COLS) + eps);
+      if (row < rows) {
+        *reinterpret_cast<uint4*>(out + row * COLS + cl) = w;
+        const float4 g0 = const_cast<const float4&>(vg[cl / 4]);
+        const float4 g1 = const_cast<const float4&>(vg[cl / 4 + 1]);
+        const float4 c0 = const_cast<const float4&>(vt[cl / 4]);
+        const float4 c1 = const_cast<const float4&>(vt[cl / 4 + 1]);
+        const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+        const float bb[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+        float lv[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) lv[e] = (o[e] - mu) * rs * gg[e] + bb[e];
+        st8<bf16>(ln + row * COLS + cl, lv);
+        if (cl == 0 && mean) {
+          mean[row] = mu;
+          rstd[row] = rs;
+        }
+      }
+    }
+  }
+}
+
+#else
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t rb = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * RPW * U; rb < rows;
        rb += nw * RPW * U) {
@@ -495,6 +594,7 @@ __global__ void __launch_bounds__(256, RLN_MINB) residual_ln_k(const bf16* __res
   }
 }
 
+#endif
 static unsigned grid_for(int64_t work, int threads) {
   int64_t need = (work + threads - 1) / threads;
   int64_t cap = (int64_t)sm_count() * 16;
