@@ -386,6 +386,66 @@ template <> struct Raw8<float> {
   }
 };
 
+#ifndef LNF_PIPE
+#define LNF_PIPE 1
+#endif
+// ln_fwd_grp with a software pipeline: the raw 16-byte loads of the lane's next U row groups are issued
+// before this step's statistics and stores, so the loads of consecutive steps overlap
+template <typename TX, typename TY, int COLS, int U>
+__global__ void __launch_bounds__(256) ln_fwd_grp_pipe(const TX* __restrict__ x, int64_t x_rs,
+                                                       const float* __restrict__ gamma, const float* __restrict__ beta,
+                                                       TY* __restrict__ y, float* __restrict__ mean_out,
+                                                       float* __restrict__ rstd_out, int64_t rows, float eps) {
+  pdl_wait();
+  constexpr int LPR = COLS / 8, RPW = 32 / LPR;
+  const int lane = threadIdx.x & 31, sub = lane / LPR, cl = (lane % LPR) * 8;
+  float g[8], b[8];
+  load_row<float, 8>(gamma + cl, g);
+  load_row<float, 8>(beta + cl, b);
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5), step = nw * RPW * U;
+  Raw8<TX> nx[U];
+  auto load = [&](int64_t rb_) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t row = rb_ + u * RPW + sub;
+      if (row < rows) nx[u].load(x + row * x_rs + cl); else nx[u].zero();
+    }
+  };
+  int64_t rb = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * RPW * U;
+  if (rb < rows) load(rb);
+  for (; rb < rows; rb += step) {
+    float v[U][8];
+#pragma unroll
+    for (int u = 0; u < U; ++u) nx[u].get(v[u]);
+    if (rb + step < rows) load(rb + step);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t row = rb + u * RPW + sub;
+      float s = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s += v[u][i];
+      const float mu = group_sum<LPR>(s) * (1.0f / COLS);
+      float q = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        v[u][i] -= mu;
+        q += v[u][i] * v[u][i];
+      }
+      const float rs = rsqrtf(group_sum<LPR>(q) * (1.0f / COLS) + eps);
+      if (row < rows) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[u][i] = v[u][i] * rs * g[i] + b[i];
+        if (y) store_row<TY, 8>(y + row * COLS + cl, v[u]);
+        if (cl == 0 && mean_out) {
+          mean_out[row] = mu;
+          rstd_out[row] = rs;
+        }
+      }
+    }
+  }
+}
+
+
 // LPR = COLS/8 lanes per row, each owning 8 channels; a CTA walks one contiguous slab of
 // rows, U row-groups per warp step with every load of the step issued before any math.
 // <= 128 registers (2 CTAs = 16 warps per SM) keep ~100 KB of loads in flight per SM.
@@ -851,7 +911,16 @@ static int ln_fwd_dispatch_warp(const void* x, int64_t x_rs, const float* g, con
     const int64_t rpw = 32 / (cols / 8);
     int64_t need = (rows + 8 * rpw * 2 - 1) / (8 * rpw * 2), cap = (int64_t)sm_count() * 8;
     dim3 g2((unsigned)(need < cap ? need : cap));
+#if LNF_PIPE  // pipelined for >= 64 columns (kernel_microbench: [65536,128] 8.4 -> 7.8 us, [32768,256] 8.8 -> 7.9,
+               // [1M,128] 97 -> 86 us = 96 % of HBM); 32 columns measured slower pipelined (2.45 -> 2.8 us)
+#define LNG(CC)                                                                                                    \
+  ((CC) >= 64 ? ::evo::pdl_launch(ln_fwd_grp_pipe<TX, TY, CC, 2>, g2, 256, 0, st, (const TX*)x, x_rs, g, b, (TY*)y, \
+                                  mean, rstd, rows, eps)                                                           \
+              : ::evo::pdl_launch(ln_fwd_grp<TX, TY, CC, 2>, g2, 256, 0, st, (const TX*)x, x_rs, g, b, (TY*)y, mean,  \
+                                  rstd, rows, eps))
+#else
 #define LNG(CC) ::evo::pdl_launch(ln_fwd_grp<TX, TY, CC, 2>, g2, 256, 0, st, (const TX*)x, x_rs, g, b, (TY*)y, mean, rstd, rows, eps)
+#endif
     switch (cols) {
       case 32: LNG(32); break;
       case 64: LNG(64); break;
