@@ -5,9 +5,13 @@
 // max/sum via warp shuffles, exp2 with log2(e) folded into the scale.  bias and
 // mask are broadcast through 4-D strides (stride 0 = broadcast) and read in the
 // same vectorised chunks when their key stride is 1.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace evo {
+
+int sm_count();
 
 struct Bcast {
   const void* p;
@@ -140,6 +144,80 @@ __global__ void __launch_bounds__(256) softmax_fwd_kernel(const void* __restrict
   }
 }
 
+// Persistent, software-pipelined forward for the common case (bf16 x / y, K a multiple of 256 up to
+// 512, bias / mask absent or bf16 with unit key stride): each warp walks rows with the raw 16-byte loads
+// of its next row (x, bias, mask) issued before this row's reductions and stores, so every warp keeps a
+// row in flight instead of one DRAM round trip per launched row; (b, h, q) splits are shifts when H and
+// Q are powers of two.
+template <int NCH>
+__global__ void __launch_bounds__(256) softmax_fwd_pipe(const bf16* __restrict__ x, const bf16* __restrict__ bias,
+                                                        int64_t bs0, int64_t bs1, int64_t bs2,
+                                                        const bf16* __restrict__ mask, int64_t ms0, int64_t ms1,
+                                                        int64_t ms2, bf16* __restrict__ y, uint32_t H, uint32_t Q,
+                                                        int sh_h, int sh_q, int64_t rows, int K, float sl2) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  uint4 nx[NCH], nb[NCH], nm[NCH];
+  auto load = [&](int64_t r) {
+    const uint32_t r32 = (uint32_t)r;
+    const uint32_t bh = sh_q >= 0 ? r32 >> sh_q : r32 / Q, q = r32 - bh * Q;
+    const uint32_t b = sh_h >= 0 ? bh >> sh_h : bh / H, h = bh - b * H;
+    const bf16* xb = x + r * K;
+    const bf16* bb = bias ? bias + b * bs0 + h * bs1 + q * bs2 : nullptr;
+    const bf16* mb = mask ? mask + b * ms0 + h * ms1 + q * ms2 : nullptr;
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {
+      const int k0 = (j * 32 + lane) * 8;
+      nx[j] = __ldcs(reinterpret_cast<const uint4*>(xb + k0));
+      nb[j] = bb ? *reinterpret_cast<const uint4*>(bb + k0) : make_uint4(0, 0, 0, 0);
+      nm[j] = mb ? *reinterpret_cast<const uint4*>(mb + k0) : make_uint4(0, 0, 0, 0);
+    }
+  };
+  if (row < rows) load(row);
+  for (; row < rows; row += nw) {
+    uint4 cx[NCH], cb[NCH], cm[NCH];
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) { cx[j] = nx[j]; cb[j] = nb[j]; cm[j] = nm[j]; }
+    if (row + nw < rows) load(row + nw);
+    float v[NCH][8];
+    float mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {
+      float xv[8], bv[8], mv[8];
+      unpack_bf16x2(cx[j].x, xv[0], xv[1]); unpack_bf16x2(cx[j].y, xv[2], xv[3]);
+      unpack_bf16x2(cx[j].z, xv[4], xv[5]); unpack_bf16x2(cx[j].w, xv[6], xv[7]);
+      unpack_bf16x2(cb[j].x, bv[0], bv[1]); unpack_bf16x2(cb[j].y, bv[2], bv[3]);
+      unpack_bf16x2(cb[j].z, bv[4], bv[5]); unpack_bf16x2(cb[j].w, bv[6], bv[7]);
+      unpack_bf16x2(cm[j].x, mv[0], mv[1]); unpack_bf16x2(cm[j].y, mv[2], mv[3]);
+      unpack_bf16x2(cm[j].z, mv[4], mv[5]); unpack_bf16x2(cm[j].w, mv[6], mv[7]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        v[j][i] = (xv[i] + bv[i]) * sl2 + mv[i] * 1.4426950408889634f;
+        mx = fmaxf(mx, v[j][i]);
+      }
+    }
+    mx = warp_max(mx);
+    float sum = 0.f;
+#pragma unroll
+    for (int j = 0; j < NCH; ++j)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        v[j][i] = ex2f(v[j][i] - mx);
+        sum += v[j][i];
+      }
+    const float inv = rcpf(warp_sum(sum));
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {
+      uint4 w;
+      w.x = pack_bf16x2(v[j][0] * inv, v[j][1] * inv); w.y = pack_bf16x2(v[j][2] * inv, v[j][3] * inv);
+      w.z = pack_bf16x2(v[j][4] * inv, v[j][5] * inv); w.w = pack_bf16x2(v[j][6] * inv, v[j][7] * inv);
+      *reinterpret_cast<uint4*>(y + row * K + (j * 32 + lane) * 8) = w;
+    }
+  }
+}
+
 template <int VEC, int NCH>
 __global__ void __launch_bounds__(256) softmax_bwd_kernel(const void* __restrict__ y, int yd, const void* __restrict__ dy,
                                                           int dyd, void* __restrict__ dx, int dxd, int64_t rows, int K,
@@ -237,8 +315,26 @@ extern "C" int evo_softmax_fwd(const void* x, int x_dtype, const void* bias, int
   EVO_CHECK_ARG(vec_ok(bb) && vec_ok(mm), EVO_ERR_ALIGN, "softmax: bias/mask rows must be vector aligned");
   cudaStream_t st = (cudaStream_t)stream;
   EVO_CHECK_ARG(rows < (1LL << 31), EVO_ERR_SHAPE, "softmax: more than 2^31 rows");
-  dim3 grid((unsigned)((rows + 7) / 8));
   const float sl2 = scale * 1.4426950408889634f;
+  const bool pipe_ok = x_dtype == EVO_BF16 && y_dtype == EVO_BF16 && (K == 256 || K == 512) &&
+                       (!bias || (bias_dtype == EVO_BF16 && bb.s3 == 1)) && (!mask || (mask_dtype == EVO_BF16 && mm.s3 == 1));
+  static const bool no_pipe = getenv("EVO_SOFTMAX_NO_PIPE") != nullptr;  // A/B switch
+  if (pipe_ok && !no_pipe) {
+    auto lg2 = [](int64_t v) { int k = 0; while ((int64_t(1) << k) < v) ++k; return (int64_t(1) << k) == v ? k : -1; };
+    const int64_t need = (rows + 7) / 8, cap = (int64_t)sm_count() * 8;
+    dim3 gp((unsigned)(need < cap ? need : cap));
+    if (K == 256)
+      ::evo::pdl_launch(softmax_fwd_pipe<1>, gp, 256, 0, st, (const bf16*)x, (const bf16*)bias, bb.s0, bb.s1, bb.s2,
+                        (const bf16*)mask, mm.s0, mm.s1, mm.s2, (bf16*)y, (uint32_t)H, (uint32_t)Q, lg2(H), lg2(Q), rows,
+                        (int)K, sl2);
+    else
+      ::evo::pdl_launch(softmax_fwd_pipe<2>, gp, 256, 0, st, (const bf16*)x, (const bf16*)bias, bb.s0, bb.s1, bb.s2,
+                        (const bf16*)mask, mm.s0, mm.s1, mm.s2, (bf16*)y, (uint32_t)H, (uint32_t)Q, lg2(H), lg2(Q), rows,
+                        (int)K, sl2);
+    EVO_LAUNCH_CHECK("softmax fwd");
+    return EVO_OK;
+  }
+  dim3 grid((unsigned)((rows + 7) / 8));
   SM_DISPATCH(softmax_fwd_kernel, x, x_dtype, bb, mm, y, y_dtype, H, Q, rows, (int)K, sl2);
   EVO_LAUNCH_CHECK("softmax fwd");
   return EVO_OK;
