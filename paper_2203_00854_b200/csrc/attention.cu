@@ -21,6 +21,7 @@
 #include <cstdlib>
 #include <cstring>
 
+
 namespace evo {
 
 constexpr int ATT_BQ = 128;
@@ -160,10 +161,11 @@ __device__ __forceinline__ uint32_t vt_off(int key, int d) {
 // unit already prefetches the next unit's first K/V tile, and the next unit's Q follows as
 // soon as this unit's last S MMA has read Q: the next unit's load latency hides under this
 // unit's last softmax and epilogue.
-// VAR: 0 = no bias (gate rows prefetched into smem for the epilogue), 1 = per-key bias,
+// VAR: 0 = no bias (gate rows prefetched into smem for the epilogue), 1 = per-key bias (4 = the same at
+// 3 CTAs/SM with register-prefetched gate rows, for rows of <= 512 keys),
 // 2 = full bias staged through smem (FB), 3 = generic full bias (strided global loads)
 template <int CP, int VAR>
-__global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1) ? 3 : 4)) attn_fwd_kernel(
+__global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || VAR == 4 || EVO_EXP == 1) ? 3 : 4)) attn_fwd_kernel(
     AttnParams P, int nunits, const __grid_constant__ AttnFwdMaps maps, int tmaq) {
   pdl_wait();
   // The epilogue's gate rows are fetched early, with the unit's last tile, so the epilogue does not
@@ -172,7 +174,7 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1
   // full-bias variant, 3 CTAs/SM: registers to spare) into registers (msa_row fwd 58.3 -> 54.6 us).  The
   // per-key-bias variant (4 CTAs/SM at its register limit) keeps the epilogue load: the smem gate
   // tile, registers and an L1 prefetch all measured 3-7 % slower there (spills)
-  constexpr bool FB = VAR == 2, GS = VAR == 0, GR = VAR == 2;
+  constexpr bool FB = VAR == 2, GS = VAR == 0, GR = VAR == 2 || VAR == 4;
   using SM = AttnSmem<CP>;
   constexpr int CQ = SM::CQ, CV = SM::CV;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -184,7 +186,7 @@ __global__ void __launch_bounds__(128, CP == 64 ? 2 : ((VAR == 2 || EVO_EXP == 1
   const int L = P.L, c = P.c, H = P.H;
   const int nqt = (L + ATT_BQ - 1) / ATT_BQ;
   const int r = warp * 32 + lane;  // query row inside the tile
-  const bool per_key_bias = VAR == 1;
+  const bool per_key_bias = VAR == 1 || VAR == 4;
   constexpr uint32_t ONE_BF16 = 0x3F80u;
   const int nkt = (L + ATT_BK - 1) / ATT_BK;
 
@@ -611,7 +613,7 @@ static int launch_attn_fwd_v(const AttnParams& p, int64_t B, cudaStream_t st) {
   // resident CTAs per SM: the launch bound (registers; TMEM 4 x 128 columns) or what fits in
   // 228 KB of shared memory (1 KB reserved per CTA), whichever is smaller.  The persistent grid
   // is exactly one wave: measured, a grid above the resident count is slower (uneven tails).
-  constexpr int occ_lb = CP == 64 ? 2 : ((FB || EVO_EXP == 1) ? 3 : 4);
+  constexpr int occ_lb = CP == 64 ? 2 : ((FB || VAR == 4 || EVO_EXP == 1) ? 3 : 4);
   constexpr int occ_sm = (int)((228u * 1024u) / (bytes + 1024u + 64u));
   static int occ = occ_lb < occ_sm ? occ_lb : occ_sm;
   if (EVO_EXP == 2) {
@@ -677,7 +679,10 @@ static int launch_attn_fwd_v(const AttnParams& p, int64_t B, cudaStream_t st) {
 template <int CP>
 static int launch_attn_fwd(const AttnParams& p, int64_t B, int flags, cudaStream_t st) {
   if (!p.bias) return launch_attn_fwd_v<CP, 0>(p, B, st);
-  if (p.bs2 == 0) return launch_attn_fwd_v<CP, 1>(p, B, st);
+  // per-key bias: up to 512 keys the 3-CTA/SM form with register-prefetched gate rows (VAR 4: pair_row /
+  // pair_col forward 50.3 / 51.2 -> 48.4 / 48.8 us at the training shape); longer rows keep 4 CTAs/SM
+  // (VAR 1: at N_r = 1024 / 2048 the 3-CTA form measured 9-10 % slower)
+  if (p.bs2 == 0) return p.L <= 512 ? launch_attn_fwd_v<CP, 4>(p, B, st) : launch_attn_fwd_v<CP, 1>(p, B, st);
   // a full bias is staged through smem with the K/V tiles unless EVO_ATTN_NO_BIAS_SMEM
   if (!(flags & EVO_ATTN_NO_BIAS_SMEM) && p.bias_vec) return launch_attn_fwd_v<CP, 2>(p, B, st);
   return launch_attn_fwd_v<CP, 3>(p, B, st);
